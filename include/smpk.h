@@ -1,0 +1,94 @@
+/*
+ * smpk.h — C ABI of libsmpk.so, the B200 (sm_100a) kernel library behind the
+ * tensor-parallel hot path of the SageMaker model-parallelism design
+ * (arXiv 2111.05972).
+ *
+ * The reference (/root/reference) has no FFI for this path: its tensor-parallel
+ * operators exist only as the SPEC's free functions over a TpGroup
+ * and as the paper's smp.nn API.  Every
+ * entry point below names the SPEC/PAPER operation whose per-rank local compute
+ * it performs; the collectives between them are issued by the host layer
+ * (paper_2111_05972_b200/collectives.py) or by the peer-memory entry points at
+ * the end of this header.
+ *
+ * Conventions
+ *   - All pointers are raw device pointers (host pointers only where stated).
+ *   - Tensors are bf16 unless the name says f32 / i64.  Leading dimensions and
+ *     strides are in ELEMENTS.
+ *   - `stream` is a cudaStream_t passed as void*; every call is asynchronous on
+ *     it and never allocates device memory.
+ *   - Every function returns 0 (SMPK_OK) or an SMPK_ERR_* code; the message is
+ *     available from smpk_last_error() (thread-local).
+ */
+#ifndef SMPK_H_
+#define SMPK_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SMPK_API __attribute__((visibility("default")))
+#else
+#define SMPK_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes (SPEC.md:417,426,435,444 name the error classes) ---- */
+#define SMPK_OK 0
+#define SMPK_ERR_BAD_SHAPE 1     /* SPEC "shape mismatch" */
+#define SMPK_ERR_NOT_DIVISIBLE 2 /* SPEC "non-divisible dimension" */
+#define SMPK_ERR_OOB_INDEX 3     /* SPEC "out-of-range index -- reported with position" */
+#define SMPK_ERR_PEER_TIMEOUT 4
+#define SMPK_ERR_CUDA 5
+#define SMPK_ERR_BAD_ARG 6
+#define SMPK_ERR_UNSUPPORTED 7
+
+/* ---- activations ("activation (gelu|relu)") ---- */
+#define SMPK_ACT_NONE 0
+#define SMPK_ACT_GELU_ERF 1  /* BERT gelu */
+#define SMPK_ACT_GELU_TANH 2 /* GPT-2/3 gelu_new */
+#define SMPK_ACT_RELU 3
+
+/* ---- GEMM epilogues ---- */
+#define SMPK_EPI_NONE 0     /* C = alpha*acc + beta*C                          */
+#define SMPK_EPI_BIAS 1     /* C = alpha*acc + bias[n] (+ beta*C)               */
+#define SMPK_EPI_BIAS_ACT 2 /* aux = acc + bias[n] (pre-activation); C = act(aux) */
+#define SMPK_EPI_DACT 3     /* C = acc * act'(aux[m,n])  (activation backward)  */
+#define SMPK_EPI_ADD 4      /* C = acc + aux[m,n]        (residual add)         */
+
+SMPK_API const char* smpk_last_error(void);
+SMPK_API int smpk_version(void);
+/* number of SMs of the current device and whether it is an sm_100 part */
+SMPK_API int smpk_device_info(int* num_sms, int* cc_major, int* cc_minor);
+
+/*
+ * smpk_gemm — batched C[m,n] = epi(alpha * sum_k A[m,k] * B[n,k]), tcgen05/TMEM/TMA.
+ *
+ * Replaces the local affine map inside dist_linear_forward/backward
+ * (Fig 5) and the column/row-parallel linears and
+ * attention contractions of dist_attention_forward / dist_mlp_forward
+ * (PAPER.md:699-717).
+ *
+ *   A: a_mn_major == 0 -> A[m,k] = a[m*lda + k]   (row-major M x K)
+ *      a_mn_major == 1 -> A[m,k] = a[k*lda + m]   (row-major K x M)
+ *   B: b_mn_major == 0 -> B[n,k] = b[n*ldb + k]   (row-major N x K, i.e. nn.Linear weight)
+ *      b_mn_major == 1 -> B[n,k] = b[k*ldb + n]   (row-major K x N)
+ *   C: row-major M x N with ldc; bf16, or fp32 when c_f32 != 0.
+ *   Batch: nb1 x nb2 problems; problem (i1,i2) offsets every operand by
+ *   i1*x_bs1 + i2*x_bs2 elements.  aux (for BIAS_ACT / DACT / ADD) is bf16,
+ *   row-major with ldaux and the same batch strides as C.
+ */
+SMPK_API int smpk_gemm(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, int64_t a_bs2,
+              const void* b, int b_mn_major, int64_t ldb, int64_t b_bs1, int64_t b_bs2,
+              void* c, int c_f32, int64_t ldc, int64_t c_bs1, int64_t c_bs2,
+              int M, int N, int K, int nb1, int nb2,
+              float alpha, float beta, int epilogue, int act,
+              const void* bias, void* aux, int64_t ldaux, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SMPK_H_ */

@@ -1,0 +1,28 @@
+"""CPU oracle for the tensor-parallel hot path — TEST INFRASTRUCTURE ONLY.
+
+This package restates, on the CPU, the algorithms the GPU path must reproduce:
+
+* ``tp``      — SPEC.md:390-516 (tensor_parallel module): the five collectives,
+                DistributedLinear forward/backward, dim-sharded DistributedEmbedding,
+                distributed LayerNorm, attention / MLP / transformer layer in speed
+                and memory modes, plan_replacement; plus the builder-defined
+                vocab-parallel embedding and cross-entropy.
+                fp64 torch CPU tensors, simulated ranks in ascending order
+                (SPEC.md:509).
+* ``philox``  — numpy Philox4x32-10 and the logical-coordinate dropout masks the
+                kernels draw (bit-exact).
+* ``mpsim_restated`` — plain-Python restatement of the reference's topology,
+                partition and scheduler rules used to pin the product's copies
+                (the reference itself is importable here and is used to generate
+                tests/golden/*.json by tests/golden/make_golden.py).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` leg may import this package.  The product path
+(``paper_2111_05972_b200``) never does: it fails loudly if libsmpk.so is absent.
+
+Parity pinning: the reference ships no tests (pkg/pyproject.toml:24-25 points at
+a missing tests/ dir), so the TP rows are pinned by the SPEC's worked examples
+and tolerances, which tests/test_oracle.py checks,
+and the partition/topology/schedule rows by golden vectors generated from the
+reference code itself (tests/golden/).
+"""

@@ -1,0 +1,90 @@
+"""Philox4x32-10 and logical-coordinate dropout masks (numpy, bit-exact).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+The GPU kernels (csrc/smpk_common.cuh: philox4x32_10 / dropout_keep) draw every
+dropout decision from Philox4x32-10 keyed by the 64-bit seed and countered by
+*logical* coordinates, never by buffer offsets (SURVEY.md Appendix C.2 "Dropout
+RNG rule"), so masks are invariant to the TP degree and the oracle reproduces
+them exactly:
+
+    counter = (col >> 2, row, layer, site);  word = output[col & 3]
+    keep    = float(word >> 8) * 2**-24 >= p
+
+Sites: 0 = attention probabilities (row = (global_sample*nh + global_head)*s_q + q,
+col = key position), 1 = attention-output hidden dropout, 2 = MLP-output hidden
+dropout (row = global token index = global_sample*s + t, col = channel).
+The SPEC disables dropout in equivalence tests; masks are
+exercised separately for bit-exactness.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+M0 = np.uint64(0xD2511F53)
+M1 = np.uint64(0xCD9E8D57)
+W0 = np.uint32(0x9E3779B9)
+W1 = np.uint32(0xBB67AE85)
+MASK32 = np.uint64(0xFFFFFFFF)
+
+SITE_ATTN_PROB = 0
+SITE_ATTN_OUT = 1
+SITE_MLP_OUT = 2
+
+
+def philox4x32_10(c0, c1, c2, c3, seed: int):
+    """Vectorised Philox4x32-10. c* are uint32 arrays (broadcastable); returns 4 uint32 arrays."""
+    c0, c1, c2, c3 = (np.asarray(c, dtype=np.uint32) for c in (c0, c1, c2, c3))
+    c0, c1, c2, c3 = np.broadcast_arrays(c0, c1, c2, c3)
+    x, y, z, w = (a.astype(np.uint32).copy() for a in (c0, c1, c2, c3))
+    k0 = np.uint32(seed & 0xFFFFFFFF)
+    k1 = np.uint32((seed >> 32) & 0xFFFFFFFF)
+    with np.errstate(over="ignore"):
+        for _ in range(10):
+            p0 = M0 * x.astype(np.uint64)
+            p1 = M1 * z.astype(np.uint64)
+            hi0 = (p0 >> np.uint64(32)).astype(np.uint32)
+            lo0 = (p0 & MASK32).astype(np.uint32)
+            hi1 = (p1 >> np.uint64(32)).astype(np.uint32)
+            lo1 = (p1 & MASK32).astype(np.uint32)
+            x, y, z, w = hi1 ^ y ^ k0, lo1, hi0 ^ w ^ k1, lo0
+            k0 = np.uint32((int(k0) + int(W0)) & 0xFFFFFFFF)
+            k1 = np.uint32((int(k1) + int(W1)) & 0xFFFFFFFF)
+    return x, y, z, w
+
+
+def uniform_words(rows: np.ndarray, cols: np.ndarray, layer: int, site: int, seed: int) -> np.ndarray:
+    """The 32-bit Philox word used for element (row, col); rows/cols broadcast."""
+    rows = np.asarray(rows, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    rows, cols = np.broadcast_arrays(rows, cols)
+    x, y, z, w = philox4x32_10((cols >> 2).astype(np.uint32), rows.astype(np.uint32),
+                               np.uint32(layer), np.uint32(site), seed)
+    lane = (cols & 3)
+    out = np.where(lane == 0, x, np.where(lane == 1, y, np.where(lane == 2, z, w)))
+    return out.astype(np.uint32)
+
+
+def keep_mask(rows, cols, layer: int, site: int, seed: int, p: float) -> np.ndarray:
+    """Boolean keep mask: keep iff (word >> 8) * 2^-24 >= p, compared in fp32."""
+    words = uniform_words(rows, cols, layer, site, seed)
+    u = (words >> np.uint32(8)).astype(np.float32) * np.float32(1.0 / 16777216.0)
+    return u >= np.float32(p)
+
+
+def hidden_mask(global_rows: np.ndarray, n_cols: int, layer: int, site: int, seed: int, p: float) -> np.ndarray:
+    """[len(rows), n_cols] keep mask for a hidden-dropout site."""
+    r = np.asarray(global_rows, dtype=np.int64)[:, None]
+    c = np.arange(n_cols, dtype=np.int64)[None, :]
+    return keep_mask(r, c, layer, site, seed, p)
+
+
+def attn_prob_mask(global_samples, global_heads, s_q: int, s_k: int, nh_global: int, layer: int, seed: int,
+                   p: float) -> np.ndarray:
+    """[len(samples), len(heads), s_q, s_k] keep mask for attention-probability dropout."""
+    gs = np.asarray(global_samples, dtype=np.int64)[:, None, None, None]
+    gh = np.asarray(global_heads, dtype=np.int64)[None, :, None, None]
+    q = np.arange(s_q, dtype=np.int64)[None, None, :, None]
+    k = np.arange(s_k, dtype=np.int64)[None, None, None, :]
+    rows = (gs * nh_global + gh) * s_q + q
+    return keep_mask(rows, k, layer, SITE_ATTN_PROB, seed, p)

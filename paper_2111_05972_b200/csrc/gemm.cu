@@ -1,0 +1,466 @@
+// gemm.cu — warp-specialised persistent tcgen05 GEMM for sm_100a.
+//
+// One CTA per SM.  Warp 0 lane 0 drives TMA (4-D tensor maps, SWIZZLE_128B) into
+// a STAGES-deep smem ring; warp 1 lane 0 issues tcgen05.mma (M=128, N=BN, K=16)
+// into a double-buffered TMEM accumulator; warps 4..7 drain TMEM with
+// tcgen05.ld, apply the fused epilogue (bias / activation / activation-backward
+// / residual / beta-accumulate) and store to HBM, overlapping the next tile's
+// main loop.  Both operand majors are supported through the UMMA descriptor, so
+// forward, dgrad and wgrad of every linear map onto the same kernel without
+// transposes.
+//
+// Hot-path role: the local GEMM of DistributedLinear / column- and row-parallel
+// transformer linears and the per-head
+// attention contractions.
+#include <cstdarg>
+#include <cstdio>
+#include <mutex>
+
+#include "smpk_common.cuh"
+
+namespace smpk {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B row
+constexpr int GEMM_THREADS = 256;
+
+struct GemmArgs {
+  int M, N, K;
+  int nb1, nb2;
+  int tiles_m, tiles_n, num_tiles, num_kb;
+  int a_mn, b_mn;
+  void* c;
+  int c_f32;
+  int64_t ldc, c_bs1, c_bs2;
+  float alpha, beta;
+  int epi, act;
+  const bf16* bias;
+  bf16* aux;
+  int64_t ldaux;
+  int vec_ok;  // 16B-aligned rows of C / aux
+};
+
+template <int BN, int STAGES>
+struct GemmCfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ void decode_tile(const GemmArgs& g, int tile, int& b1, int& b2, int& tm, int& tn) {
+  int per = g.tiles_m * g.tiles_n;
+  int b = tile / per;
+  int r = tile - b * per;
+  tn = r / g.tiles_m;
+  tm = r - tn * g.tiles_m;
+  b1 = b % g.nb1;
+  b2 = b / g.nb1;
+}
+
+// Epilogue for 32 consecutive accumulator columns of one row.
+__device__ __forceinline__ void epilogue_store32(const GemmArgs& g, int row, int col0, int b1, int b2,
+                                                 const uint32_t (&r)[32]) {
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * g.alpha;
+
+  const int64_t c_off = (int64_t)b1 * g.c_bs1 + (int64_t)b2 * g.c_bs2;
+  const bool full = (col0 + 32 <= g.N) && g.vec_ok;
+
+  if (g.epi == SMPK_EPI_BIAS || g.epi == SMPK_EPI_BIAS_ACT) {
+    if (full) {
+      const uint4* bp = reinterpret_cast<const uint4*>(g.bias + col0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 u = __ldg(bp + q);
+        uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float2 f = unpack_bf16x2(w[j]);
+          v[q * 8 + 2 * j] += f.x;
+          v[q * 8 + 2 * j + 1] += f.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < g.N) v[i] += bf2f(g.bias[col0 + i]);
+    }
+  }
+
+  if (g.epi == SMPK_EPI_BIAS_ACT || g.epi == SMPK_EPI_DACT || g.epi == SMPK_EPI_ADD) {
+    bf16* ap = g.aux + c_off + (int64_t)row * g.ldaux + col0;
+    if (g.epi == SMPK_EPI_BIAS_ACT) {
+      // store the pre-activation, then activate
+      if (full) {
+        uint4* d = reinterpret_cast<uint4*>(ap);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u;
+          u.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
+          u.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
+          u.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
+          u.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
+          d[q] = u;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (col0 + i < g.N) ap[i] = f2bf(v[i]);
+      }
+      // activation is applied to the bf16-rounded pre-activation so that the
+      // saved aux reproduces the forward exactly in the backward pass
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = act_fwd(g.act, bf2f(f2bf(v[i])));
+    } else {
+      float a[32];
+      if (full) {
+        const uint4* s = reinterpret_cast<const uint4*>(ap);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u = s[q];
+          uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float2 f = unpack_bf16x2(w[j]);
+            a[q * 8 + 2 * j] = f.x;
+            a[q * 8 + 2 * j + 1] = f.y;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) a[i] = (col0 + i < g.N) ? bf2f(ap[i]) : 0.f;
+      }
+      if (g.epi == SMPK_EPI_DACT) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] *= act_bwd(g.act, a[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] += a[i];
+      }
+    }
+  }
+
+  if (g.c_f32) {
+    float* cp = reinterpret_cast<float*>(g.c) + c_off + (int64_t)row * g.ldc + col0;
+    if (full) {
+      float4* d = reinterpret_cast<float4*>(cp);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        if (g.beta != 0.f) {
+          float4 old = d[q];
+          o.x += g.beta * old.x;
+          o.y += g.beta * old.y;
+          o.z += g.beta * old.z;
+          o.w += g.beta * old.w;
+        }
+        d[q] = o;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < g.N) cp[i] = v[i] + (g.beta != 0.f ? g.beta * cp[i] : 0.f);
+    }
+  } else {
+    bf16* cp = reinterpret_cast<bf16*>(g.c) + c_off + (int64_t)row * g.ldc + col0;
+    if (full) {
+      uint4* d = reinterpret_cast<uint4*>(cp);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (g.beta != 0.f) {
+          uint4 old = d[q];
+          uint32_t w[4] = {old.x, old.y, old.z, old.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float2 f = unpack_bf16x2(w[j]);
+            v[q * 8 + 2 * j] += g.beta * f.x;
+            v[q * 8 + 2 * j + 1] += g.beta * f.y;
+          }
+        }
+        uint4 u;
+        u.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
+        u.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
+        u.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
+        u.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
+        d[q] = u;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < g.N) cp[i] = f2bf(v[i] + (g.beta != 0.f ? g.beta * bf2f(cp[i]) : 0.f));
+    }
+  }
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const GemmArgs g) {
+  using Cfg = GemmCfg<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull_bar[i], 1);
+      mbar_init(&tempty_bar[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < g.num_tiles; tile += gridDim.x) {
+        int b1, b2, tm, tn;
+        decode_tile(g, tile, b1, b2, tm, tn);
+        for (int kb = 0; kb < g.num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+          uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
+          uint8_t* b_dst = sB + stage * Cfg::B_BYTES;
+          if (!g.a_mn) {
+            tma_load_4d(a_dst, &tmA, &full_bar[stage], kb * BK, tm * BM, b1, b2);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BM / 64; ++i)
+              tma_load_4d(a_dst + i * (BK * 128), &tmA, &full_bar[stage], tm * BM + i * 64, kb * BK, b1, b2);
+          }
+          if (!g.b_mn) {
+            tma_load_4d(b_dst, &tmB, &full_bar[stage], kb * BK, tn * BN, b1, b2);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BN / 64; ++i)
+              tma_load_4d(b_dst + i * (BK * 128), &tmB, &full_bar[stage], tn * BN + i * 64, kb * BK, b1, b2);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      const uint32_t idesc = make_idesc_bf16(BM, BN, g.a_mn, g.b_mn);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < g.num_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < g.num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + stage * Cfg::A_BYTES);
+          const uint32_t b_base = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t adesc = g.a_mn ? make_sw128_desc(a_base + k * 2048, BK * 128, 1024)
+                                          : make_sw128_desc(a_base + k * 32, 16, 1024);
+            const uint64_t bdesc = g.b_mn ? make_sw128_desc(b_base + k * 2048, BK * 128, 1024)
+                                          : make_sw128_desc(b_base + k * 32, 16, 1024);
+            umma_bf16(d_tmem, adesc, bdesc, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty_bar[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull_bar[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue ----------------
+    const int ew = warp - 4;  // TMEM lane quarter
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < g.num_tiles; tile += gridDim.x) {
+      int b1, b2, tm, tn;
+      decode_tile(g, tile, b1, b2, tm, tn);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int row = tm * BM + ew * 32 + lane;
+      const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        const int col0 = tn * BN + c * 32;
+        if (col0 >= g.N) break;  // warp-uniform
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_row + c * 32, r);
+        tmem_ld_wait();
+        if (row < g.M) epilogue_store32(g, row, col0, b1, b2, r);
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                      CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                      CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled_t get_encode_fn() {
+  static PFN_encodeTiled_t fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+  });
+  return fn;
+}
+
+// Operand view: rows x K logical, either K-major (K contiguous) or MN-major.
+static int make_operand_map(CUtensorMap* map, const void* ptr, bool mn_major, int rows, int K, int64_t ld,
+                            int nb1, int64_t s1, int nb2, int64_t s2, int box_rows, const char* name) {
+  PFN_encodeTiled_t enc = get_encode_fn();
+  SMPK_REQUIRE(enc != nullptr, SMPK_ERR_CUDA, "smpk_gemm: cuTensorMapEncodeTiled unavailable");
+  SMPK_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0, SMPK_ERR_BAD_ARG,
+               "smpk_gemm: operand %s must be 16-byte aligned", name);
+  SMPK_REQUIRE(ld % 8 == 0, SMPK_ERR_BAD_ARG, "smpk_gemm: leading dim of %s (%lld) must be a multiple of 8",
+               name, (long long)ld);
+  SMPK_REQUIRE((nb1 == 1 || s1 % 8 == 0) && (nb2 == 1 || s2 % 8 == 0), SMPK_ERR_BAD_ARG,
+               "smpk_gemm: batch strides of %s must be multiples of 8", name);
+  const int64_t inner = mn_major ? rows : K;
+  const int64_t outer = mn_major ? K : rows;
+  cuuint64_t dims[4] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)nb1, (cuuint64_t)nb2};
+  const int64_t fallback = ld * outer * 2;
+  cuuint64_t strides[3] = {(cuuint64_t)(ld * 2), (cuuint64_t)(nb1 > 1 ? s1 * 2 : fallback),
+                           (cuuint64_t)(nb2 > 1 ? s2 * 2 : fallback)};
+  cuuint32_t box[4] = {64u, (cuuint32_t)(mn_major ? BK : box_rows), 1u, 1u};
+  cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SMPK_REQUIRE(r == CUDA_SUCCESS, SMPK_ERR_CUDA, "smpk_gemm: tensor map for %s failed (CUresult %d)", name,
+               (int)r);
+  return SMPK_OK;
+}
+
+template <int BN, int STAGES>
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs& g, cudaStream_t st) {
+  using Cfg = GemmCfg<BN, STAGES>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::SMEM_BYTES);
+    SMPK_REQUIRE(e == cudaSuccess, SMPK_ERR_CUDA, "smpk_gemm: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    attr_set = true;
+  }
+  g.tiles_n = (g.N + BN - 1) / BN;
+  g.num_tiles = g.tiles_m * g.tiles_n * g.nb1 * g.nb2;
+  int grid = g.num_tiles < num_sms() ? g.num_tiles : num_sms();
+  gemm_bf16_tcgen05<BN, STAGES><<<grid, GEMM_THREADS, Cfg::SMEM_BYTES, st>>>(ta, tb, g);
+  return check_launch("smpk_gemm");
+}
+
+}  // namespace smpk
+
+using namespace smpk;
+
+extern "C" int smpk_gemm(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, int64_t a_bs2, const void* b,
+                         int b_mn_major, int64_t ldb, int64_t b_bs1, int64_t b_bs2, void* c, int c_f32,
+                         int64_t ldc, int64_t c_bs1, int64_t c_bs2, int M, int N, int K, int nb1, int nb2,
+                         float alpha, float beta, int epilogue, int act, const void* bias, void* aux,
+                         int64_t ldaux, void* stream) {
+  SMPK_REQUIRE(M > 0 && N > 0 && K > 0 && nb1 > 0 && nb2 > 0, SMPK_ERR_BAD_SHAPE,
+               "smpk_gemm: bad shape M=%d N=%d K=%d nb=%dx%d", M, N, K, nb1, nb2);
+  SMPK_REQUIRE(a && b && c, SMPK_ERR_BAD_ARG, "smpk_gemm: null operand");
+  SMPK_REQUIRE(epilogue >= SMPK_EPI_NONE && epilogue <= SMPK_EPI_ADD, SMPK_ERR_BAD_ARG,
+               "smpk_gemm: unknown epilogue %d", epilogue);
+  const bool need_bias = epilogue == SMPK_EPI_BIAS || epilogue == SMPK_EPI_BIAS_ACT;
+  const bool need_aux = epilogue == SMPK_EPI_BIAS_ACT || epilogue == SMPK_EPI_DACT || epilogue == SMPK_EPI_ADD;
+  SMPK_REQUIRE(!need_bias || bias, SMPK_ERR_BAD_ARG, "smpk_gemm: epilogue %d needs bias", epilogue);
+  SMPK_REQUIRE(!need_aux || aux, SMPK_ERR_BAD_ARG, "smpk_gemm: epilogue %d needs aux", epilogue);
+  SMPK_REQUIRE(!(need_aux && c_f32), SMPK_ERR_UNSUPPORTED, "smpk_gemm: aux epilogues need bf16 C");
+
+  int BN = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
+
+  CUtensorMap ta, tb;
+  int rc = make_operand_map(&ta, a, a_mn_major, M, K, lda, nb1, a_bs1, nb2, a_bs2, BM, "A");
+  if (rc) return rc;
+  rc = make_operand_map(&tb, b, b_mn_major, N, K, ldb, nb1, b_bs1, nb2, b_bs2, BN, "B");
+  if (rc) return rc;
+
+  GemmArgs g;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.nb1 = nb1;
+  g.nb2 = nb2;
+  g.tiles_m = (M + BM - 1) / BM;
+  g.num_kb = (K + BK - 1) / BK;
+  g.a_mn = a_mn_major ? 1 : 0;
+  g.b_mn = b_mn_major ? 1 : 0;
+  g.c = c;
+  g.c_f32 = c_f32 ? 1 : 0;
+  g.ldc = ldc;
+  g.c_bs1 = c_bs1;
+  g.c_bs2 = c_bs2;
+  g.alpha = alpha;
+  g.beta = beta;
+  g.epi = epilogue;
+  g.act = act;
+  g.bias = reinterpret_cast<const bf16*>(bias);
+  g.aux = reinterpret_cast<bf16*>(aux);
+  g.ldaux = ldaux;
+  const int esz = c_f32 ? 4 : 2;
+  bool vec = (reinterpret_cast<uintptr_t>(c) % 16 == 0) && ((ldc * esz) % 16 == 0) && ((c_bs1 * esz) % 16 == 0) &&
+             ((c_bs2 * esz) % 16 == 0);
+  if (need_bias) vec = vec && (reinterpret_cast<uintptr_t>(bias) % 16 == 0);
+  if (need_aux) vec = vec && (reinterpret_cast<uintptr_t>(aux) % 16 == 0) && (ldaux % 8 == 0);
+  g.vec_ok = vec ? 1 : 0;
+
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (BN == 64) return launch_gemm<64, 8>(ta, tb, g, st);
+  if (BN == 128) return launch_gemm<128, 6>(ta, tb, g, st);
+  return launch_gemm<256, 4>(ta, tb, g, st);
+}

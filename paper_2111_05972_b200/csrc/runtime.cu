@@ -1,0 +1,58 @@
+// runtime.cu — error reporting, device queries and version of libsmpk.
+#include <cstdarg>
+#include <cstdio>
+#include <mutex>
+
+#include "smpk_common.cuh"
+
+namespace smpk {
+
+static thread_local char g_last_error[1024] = "";
+
+void set_last_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_last_error("%s: launch failed: %s", what, cudaGetErrorString(e));
+    return SMPK_ERR_CUDA;
+  }
+  return SMPK_OK;
+}
+
+int num_sms() {
+  static int n[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (n[dev] == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n[dev] = v > 0 ? v : 148;
+  }
+  return n[dev];
+}
+
+}  // namespace smpk
+
+extern "C" const char* smpk_last_error(void) { return smpk::g_last_error; }
+
+extern "C" int smpk_version(void) { return 1; }
+
+extern "C" int smpk_device_info(int* nsm, int* cc_major, int* cc_minor) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) {
+    smpk::set_last_error("smpk_device_info: %s", cudaGetErrorString(e));
+    return SMPK_ERR_CUDA;
+  }
+  if (nsm) *nsm = smpk::num_sms();
+  if (cc_major) cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (cc_minor) cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return SMPK_OK;
+}

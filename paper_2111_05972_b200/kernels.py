@@ -1,0 +1,121 @@
+"""Thin torch-tensor front end over the C ABI (include/smpk.h).
+
+Each function validates dtypes/devices/contiguity, allocates outputs with the
+torch caching allocator and launches the sm_100a kernel on the current stream.
+No function here has a CPU path: a CPU tensor is an error.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .errors import ShapeMismatchError
+
+EPI_NONE, EPI_BIAS, EPI_BIAS_ACT, EPI_DACT, EPI_ADD = range(5)
+ACT = {"none": 0, "gelu": 1, "gelu_erf": 1, "gelu_tanh": 2, "relu": 3}
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _check_cuda(*ts: torch.Tensor | None) -> None:
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise RuntimeError("smpk kernels run on CUDA tensors only (no CPU fallback)")
+
+
+def gemm_raw(a, a_mn, lda, a_bs, b, b_mn, ldb, b_bs, c, ldc, c_bs, M, N, K, nb=(1, 1),
+             alpha=1.0, beta=0.0, epi=EPI_NONE, act=0, bias=None, aux=None, ldaux=0) -> None:
+    """Direct binding of smpk_gemm; strides in elements, batch strides as 2-tuples."""
+    _check_cuda(a, b, c, bias, aux)
+    _lib.call("smpk_gemm",
+              _ptr(a), int(a_mn), int(lda), int(a_bs[0]), int(a_bs[1]),
+              _ptr(b), int(b_mn), int(ldb), int(b_bs[0]), int(b_bs[1]),
+              _ptr(c), int(c.dtype == torch.float32), int(ldc), int(c_bs[0]), int(c_bs[1]),
+              int(M), int(N), int(K), int(nb[0]), int(nb[1]),
+              float(alpha), float(beta), int(epi), int(act),
+              _ptr(bias), _ptr(aux), int(ldaux), _stream())
+
+
+def _rowmajor(t: torch.Tensor, name: str) -> int:
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise ShapeMismatchError(f"{name} must be a 2-D row-major view, got shape {tuple(t.shape)} "
+                                 f"strides {t.stride()}")
+    return t.stride(0)
+
+
+def linear(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None, *, act: str = "none",
+           out: torch.Tensor | None = None, aux_out: torch.Tensor | None = None,
+           residual: torch.Tensor | None = None):
+    """y = x @ w.T (+ bias) (act) (+ residual). x [M,K], w [N,K] (nn.Linear layout).
+
+    With act != none returns (y, pre_activation)."""
+    M, K = x.shape
+    N, K2 = w.shape
+    if K != K2:
+        raise ShapeMismatchError(f"linear: x has {K} features, weight expects {K2}")
+    lda, ldb = _rowmajor(x, "x"), _rowmajor(w, "weight")
+    y = out if out is not None else torch.empty(M, N, dtype=x.dtype, device=x.device)
+    ldc = _rowmajor(y, "out")
+    epi, aux, a_code = EPI_NONE, None, ACT[act]
+    if act != "none":
+        if bias is None:
+            raise ShapeMismatchError("linear with activation needs a bias")
+        epi = EPI_BIAS_ACT
+        aux = aux_out if aux_out is not None else torch.empty(M, N, dtype=x.dtype, device=x.device)
+    elif residual is not None:
+        if bias is not None:
+            raise ShapeMismatchError("linear: bias + residual epilogue not fused; add bias separately")
+        epi, aux = EPI_ADD, residual
+    elif bias is not None:
+        epi = EPI_BIAS
+    gemm_raw(x, 0, lda, (0, 0), w, 0, ldb, (0, 0), y, ldc, (0, 0), M, N, K,
+             epi=epi, act=a_code, bias=bias, aux=aux, ldaux=(aux.stride(0) if aux is not None else 0))
+    if act != "none":
+        return y, aux
+    return y
+
+
+def matmul_nn(a: torch.Tensor, b: torch.Tensor, *, out=None, epi=EPI_NONE, act="none", aux=None,
+              alpha=1.0, beta=0.0) -> torch.Tensor:
+    """C = a @ b, a [M,K] row-major, b [K,N] row-major (B operand MN-major). dgrad: dX = dY @ W."""
+    M, K = a.shape
+    K2, N = b.shape
+    if K != K2:
+        raise ShapeMismatchError(f"matmul_nn: inner dims {K} vs {K2}")
+    c = out if out is not None else torch.empty(M, N, dtype=a.dtype, device=a.device)
+    gemm_raw(a, 0, _rowmajor(a, "a"), (0, 0), b, 1, _rowmajor(b, "b"), (0, 0), c, _rowmajor(c, "out"), (0, 0),
+             M, N, K, alpha=alpha, beta=beta, epi=epi, act=ACT[act], aux=aux,
+             ldaux=(aux.stride(0) if aux is not None else 0))
+    return c
+
+
+def matmul_tn(a: torch.Tensor, b: torch.Tensor, *, out=None, alpha=1.0, beta=0.0,
+              out_dtype=None) -> torch.Tensor:
+    """C = a.T @ b, a [K,M] row-major, b [K,N] row-major (both MN-major). wgrad: dW = dY.T @ X."""
+    K, M = a.shape
+    K2, N = b.shape
+    if K != K2:
+        raise ShapeMismatchError(f"matmul_tn: inner dims {K} vs {K2}")
+    c = out if out is not None else torch.empty(M, N, dtype=out_dtype or a.dtype, device=a.device)
+    gemm_raw(a, 1, _rowmajor(a, "a"), (0, 0), b, 1, _rowmajor(b, "b"), (0, 0), c, _rowmajor(c, "out"), (0, 0),
+             M, N, K, alpha=alpha, beta=beta)
+    return c
+
+
+def matmul_nt(a: torch.Tensor, b: torch.Tensor, *, out=None, alpha=1.0, beta=0.0,
+              out_dtype=None) -> torch.Tensor:
+    """C = a @ b.T, a [M,K], b [N,K] (both K-major)."""
+    M, K = a.shape
+    N, K2 = b.shape
+    if K != K2:
+        raise ShapeMismatchError(f"matmul_nt: inner dims {K} vs {K2}")
+    c = out if out is not None else torch.empty(M, N, dtype=out_dtype or a.dtype, device=a.device)
+    gemm_raw(a, 0, _rowmajor(a, "a"), (0, 0), b, 0, _rowmajor(b, "b"), (0, 0), c, _rowmajor(c, "out"), (0, 0),
+             M, N, K, alpha=alpha, beta=beta)
+    return c
