@@ -87,6 +87,61 @@ SMPK_API int smpk_gemm(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1
               float alpha, float beta, int epilogue, int act,
               const void* bias, void* aux, int64_t ldaux, void* stream);
 
+/*
+ * smpk_bdr_ln_fwd — r = residual + dropout(x + bias); y = LayerNorm(r; gamma, beta, eps).
+ *
+ * The epilogue of every sub-layer of dist_transformer_layer_forward
+ * ("attention -> residual -> norm"), i.e. the bias, hidden
+ * dropout (PAPER.md:818 hidden_dropout_prob), residual add and replicated
+ * LayerNorm of speed mode.  bias/residual may be NULL; with
+ * gamma == NULL no LayerNorm is applied (only r is produced); with r_out == NULL
+ * r is not stored.  x, r_out, y_out: [M, H]; mean/rstd: fp32 [M].  Dropout keeps
+ * element (row, col) per Philox4x32-10 with counter (col>>2, row_offset+row,
+ * layer, site) and key `seed` (oracle/philox.py).  H must be a multiple of 256.
+ */
+SMPK_API int smpk_bdr_ln_fwd(const void* x, const void* bias, const void* residual, void* r_out,
+                             const void* gamma, const void* beta, void* y_out, float* mean, float* rstd,
+                             int M, int H, float eps, float p_drop, uint64_t seed, int layer, int site,
+                             int64_t row_offset, void* stream);
+
+/*
+ * smpk_ln_bwd — backward of smpk_bdr_ln_fwd.
+ *   dr   = LN'(dy; r, mean, rstd, gamma) + dres          (dres may be NULL)
+ *   dsub = dropout'(dr)  (written only when p_drop > 0; otherwise dsub == dr)
+ *   dgamma = colsum(dy * xhat), dbeta = colsum(dy), dbias = colsum(dsub)
+ * Column sums are deterministic (fixed-order two-stage reduction) and written as
+ * fp32 (grads_f32) or bf16, overwriting or accumulating.  Any of dgamma / dbeta /
+ * dbias may be NULL.  workspace >= smpk_ln_bwd_workspace(M, H) bytes.
+ */
+SMPK_API int64_t smpk_ln_bwd_workspace(int M, int H);
+SMPK_API int smpk_ln_bwd(const void* dy, const void* r, const float* mean, const float* rstd, const void* gamma,
+                         const void* dres, void* dr_out, void* dsub_out, void* dgamma, void* dbeta, void* dbias,
+                         int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed, int layer,
+                         int site, int64_t row_offset, void* workspace, int64_t workspace_bytes, void* stream);
+
+/*
+ * smpk_softmax_fwd / smpk_softmax_bwd — masked, scaled softmax over attention
+ * scores with attention-probability dropout (the "scaled dot-product attention
+ * with softmax over masked scores" of dist_attention_forward).
+ *   scores, probs, probs_drop: [B, nh, sq, sk] bf16 contiguous.
+ *   P  = softmax(scale * S + mask_add[b, k]  (+ -inf where k > q + sk - sq if causal))
+ *   Pd = P * keep / (1 - p)   (written when p_drop > 0)
+ *   backward: dS = scale * (Pd * dPd - P * sum_k(Pd * dPd))  (dscores may alias dprobs_drop)
+ * Fully masked rows give P = 0.  Dropout row coordinate is
+ * ((sample_offset + b) * nh_global + head_offset + h) * sq + q, site 0.
+ */
+SMPK_API int smpk_softmax_fwd(const void* scores, void* probs, void* probs_drop, const float* mask_add, int B,
+                              int nh, int sq, int sk, float scale, int causal, float p_drop, uint64_t seed,
+                              int layer, int64_t sample_offset, int head_offset, int nh_global, void* stream);
+SMPK_API int smpk_softmax_bwd(const void* probs, const void* dprobs_drop, void* dscores, int B, int nh, int sq,
+                              int sk, float scale, float p_drop, uint64_t seed, int layer, int64_t sample_offset,
+                              int head_offset, int nh_global, void* stream);
+
+/* smpk_colsum — out[n] (+)= sum_m x[m, n] (bias gradients), deterministic. */
+SMPK_API int64_t smpk_colsum_workspace(int M, int N);
+SMPK_API int smpk_colsum(const void* x, int M, int N, int64_t ldx, void* out, int out_f32, int accumulate,
+                         void* workspace, int64_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,6 +27,17 @@ SIGNATURES: dict[str, list] = {
     "smpk_version": [],
     "smpk_device_info": [C.POINTER(I), C.POINTER(I), C.POINTER(I)],
     "smpk_gemm": [P, I, L, L, L, P, I, L, L, L, P, I, L, L, L, I, I, I, I, I, F, F, I, I, P, P, L, P],
+    "smpk_bdr_ln_fwd": [P, P, P, P, P, P, P, P, P, I, I, F, F, C.c_uint64, I, I, L, P],
+    "smpk_ln_bwd": [P, P, P, P, P, P, P, P, P, P, P, I, I, I, I, F, C.c_uint64, I, I, L, P, L, P],
+    "smpk_softmax_fwd": [P, P, P, P, I, I, I, I, F, I, F, C.c_uint64, I, L, I, I, P],
+    "smpk_softmax_bwd": [P, P, P, I, I, I, I, F, F, C.c_uint64, I, L, I, I, P],
+    "smpk_colsum": [P, I, I, L, P, I, I, P, L, P],
+}
+
+# functions returning int64 (sizes) rather than a status code
+SIZE_FUNCS: dict[str, list] = {
+    "smpk_ln_bwd_workspace": [I, I],
+    "smpk_colsum_workspace": [I, I],
 }
 
 
@@ -44,6 +55,10 @@ def _declare(lib: C.CDLL) -> None:
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = C.c_int
+    for name, args in SIZE_FUNCS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = C.c_int64
 
 
 def lib() -> C.CDLL:
@@ -62,6 +77,15 @@ def call(name: str, *args) -> None:
     rc = getattr(lib(), name)(*args)
     if rc != 0:
         raise_for(rc, lib().smpk_last_error().decode(errors="replace"))
+
+
+def size(name: str, *args) -> int:
+    return int(getattr(lib(), name)(*args))
+
+
+def exported_symbols() -> list[str]:
+    """Every entry point this binding declares (checked against include/smpk.h by the tests)."""
+    return ["smpk_last_error", *SIGNATURES, *SIZE_FUNCS]
 
 
 def last_error() -> str:

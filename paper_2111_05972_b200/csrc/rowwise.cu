@@ -1,0 +1,701 @@
+// rowwise.cu — HBM-bound row kernels of the transformer layer (sm_100a).
+//
+//   smpk_bdr_ln_fwd  : r = residual + dropout(x + bias);  y = LayerNorm(r)   (K7+K8+K9 fused)
+//   smpk_ln_bwd      : dr = LN'(dy) + dres;  dsub = dropout'(dr);  dgamma/dbeta/dbias column sums
+//   smpk_softmax_fwd : P = softmax(scale*S + mask [+causal]);  Pd = dropout(P)              (K6+K9)
+//   smpk_softmax_bwd : dS = scale * (Pd*dPd - P*sum(Pd*dPd))
+//   smpk_colsum      : deterministic column sums (bias gradients)
+//
+// 128-bit vectorised loads/stores, warp-shuffle reductions, row groups of W warps
+// (W*256*VPT = H) so each lane keeps its slice of the row in registers.  Every
+// reduction runs in a fixed order, so results are bit-stable run to run.
+// Dropout masks come from Philox4x32-10 keyed by logical coordinates
+// (oracle/philox.py reproduces them bit-exactly).
+#include "smpk_common.cuh"
+
+namespace smpk {
+
+constexpr int ROW_THREADS = 256;
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Sum over the W warps of one row group, fixed order (deterministic).
+template <int W>
+__device__ __forceinline__ float group_sum(float v, float* sm, int slot, int wi) {
+  v = warp_sum(v);
+  if constexpr (W == 1) {
+    return v;
+  } else {
+    if ((threadIdx.x & 31) == 0) sm[slot * W + wi] = v;
+    named_bar(1 + slot, W * 32);
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < W; ++i) s += sm[slot * W + i];
+    named_bar(1 + slot, W * 32);
+    return s;
+  }
+}
+
+__device__ __forceinline__ void load8(const bf16* p, float (&v)[8]) {
+  uint4 u = *reinterpret_cast<const uint4*>(p);
+  uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float2 f = unpack_bf16x2(w[j]);
+    v[2 * j] = f.x;
+    v[2 * j + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void store8(bf16* p, const float (&v)[8]) {
+  uint4 u;
+  u.x = pack_bf16x2(v[0], v[1]);
+  u.y = pack_bf16x2(v[2], v[3]);
+  u.z = pack_bf16x2(v[4], v[5]);
+  u.w = pack_bf16x2(v[6], v[7]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+__device__ __forceinline__ void round8(float (&v)[8]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = bf2f(f2bf(v[j]));
+}
+
+// keep flags for 8 consecutive columns col0..col0+7 (col0 % 8 == 0) of logical row g
+__device__ __forceinline__ void dropout_keep8(uint64_t seed, uint32_t layer, uint32_t site, uint64_t g, int col0,
+                                              float p, bool (&keep)[8]) {
+  const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    u32x4 c = {static_cast<uint32_t>((col0 >> 2) + h), static_cast<uint32_t>(g), layer, site};
+    u32x4 r = philox4x32_10(c, k0, k1);
+    keep[4 * h + 0] = dropout_keep(r.x, p);
+    keep[4 * h + 1] = dropout_keep(r.y, p);
+    keep[4 * h + 2] = dropout_keep(r.z, p);
+    keep[4 * h + 3] = dropout_keep(r.w, p);
+  }
+}
+
+struct RowGeom {
+  int W, VPT;
+};
+
+static bool row_geom(int H, RowGeom& g) {
+  if (H <= 0 || H % 256) return false;
+  const int n = H / 256;
+  for (int W = 1; W <= 8; W *= 2) {
+    if (n % W) continue;
+    const int v = n / W;
+    if (v <= 5 || (W == 8 && v <= 8)) {
+      g.W = W;
+      g.VPT = v;
+      return true;
+    }
+  }
+  return false;
+}
+
+static int row_grid(int M, int W) {
+  const int rows_per_cta = (ROW_THREADS / 32) / W;
+  int need = (M + rows_per_cta - 1) / rows_per_cta;
+  int cap = num_sms() * 4;
+  return need < cap ? need : cap;
+}
+
+// ===========================================================================
+// bias + dropout + residual + LayerNorm forward
+// ===========================================================================
+struct BdrLnArgs {
+  const bf16* x;
+  const bf16* bias;
+  const bf16* residual;
+  bf16* r_out;
+  const bf16* gamma;
+  const bf16* beta;
+  bf16* y_out;
+  float* mean;
+  float* rstd;
+  int M, H;
+  float eps, p;
+  uint64_t seed;
+  uint32_t layer, site;
+  int64_t row_offset;
+};
+
+template <int W, int VPT>
+__global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs a) {
+  __shared__ float sm[2 * 8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = warp / W, wi = warp % W;
+  const int rows_per_cta = (ROW_THREADS / 32) / W;
+  const float inv_keep = a.p > 0.f ? 1.f / (1.f - a.p) : 1.f;
+  for (int row0 = blockIdx.x * rows_per_cta; row0 < a.M; row0 += gridDim.x * rows_per_cta) {
+    const int row = row0 + slot;
+    const bool valid = row < a.M;
+    float v[VPT][8];
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int col = ((i * W + wi) * 32 + lane) * 8;
+      if (valid) {
+        load8(a.x + (int64_t)row * a.H + col, v[i]);
+        if (a.bias) {
+          float b[8];
+          load8(a.bias + col, b);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[i][j] += b[j];
+        }
+        if (a.p > 0.f) {
+          bool keep[8];
+          dropout_keep8(a.seed, a.layer, a.site, (uint64_t)(a.row_offset + row), col, a.p, keep);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[i][j] = keep[j] ? v[i][j] * inv_keep : 0.f;
+        }
+        if (a.residual) {
+          float rr[8];
+          load8(a.residual + (int64_t)row * a.H + col, rr);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[i][j] += rr[j];
+        }
+        round8(v[i]);
+        if (a.r_out) store8(a.r_out + (int64_t)row * a.H + col, v[i]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[i][j] = 0.f;
+      }
+    }
+    if (a.gamma == nullptr) continue;  // uniform across the CTA
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += v[i][j];
+    const float mu = group_sum<W>(s, sm, slot, wi) / a.H;
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float d = v[i][j] - mu;
+        q += d * d;
+      }
+    const float var = group_sum<W>(q, sm + 8, slot, wi) / a.H;
+    const float rs = rsqrtf(var + a.eps);
+    if (valid) {
+      if (wi == 0 && lane == 0) {
+        a.mean[row] = mu;
+        a.rstd[row] = rs;
+      }
+#pragma unroll
+      for (int i = 0; i < VPT; ++i) {
+        const int col = ((i * W + wi) * 32 + lane) * 8;
+        float gm[8], bt[8], o[8];
+        load8(a.gamma + col, gm);
+        load8(a.beta + col, bt);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = (v[i][j] - mu) * rs * gm[j] + bt[j];
+        store8(a.y_out + (int64_t)row * a.H + col, o);
+      }
+    }
+  }
+}
+
+// ===========================================================================
+// LayerNorm backward (+ residual grad, + dropout backward, + column partials)
+// ===========================================================================
+struct LnBwdArgs {
+  const bf16* dy;
+  const bf16* r;
+  const float* mean;
+  const float* rstd;
+  const bf16* gamma;
+  const bf16* dres;
+  bf16* dr_out;
+  bf16* dsub_out;
+  float* partials;  // [gridDim.x][3][H]: dgamma, dbeta, dbias
+  int M, H;
+  float p;
+  uint64_t seed;
+  uint32_t layer, site;
+  int64_t row_offset;
+};
+
+template <int W, int VPT>
+__device__ __forceinline__ void flush_partial(const float (&acc)[VPT][8], float* out, float* red, int nslots, int slot,
+                                              int wi, int lane) {
+  if (nslots == 1) {
+#pragma unroll
+    for (int i = 0; i < VPT; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) out[((i * W + wi) * 32 + lane) * 8 + j] = acc[i][j];
+    return;
+  }
+  float* buf = red + wi * (VPT * 8 * 32);
+  for (int sl = 0; sl < nslots; ++sl) {
+    if (slot == sl) {
+#pragma unroll
+      for (int i = 0; i < VPT; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float* d = buf + (i * 8 + j) * 32 + lane;
+          *d = (sl == 0) ? acc[i][j] : *d + acc[i][j];
+        }
+    }
+    __syncthreads();
+  }
+  if (slot == nslots - 1) {
+#pragma unroll
+    for (int i = 0; i < VPT; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) out[((i * W + wi) * 32 + lane) * 8 + j] = buf[(i * 8 + j) * 32 + lane];
+  }
+  __syncthreads();
+}
+
+template <int W, int VPT>
+__global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const LnBwdArgs a) {
+  __shared__ float sm[2 * 8];
+  extern __shared__ float red[];  // [W][VPT*8][32] slot reduction buffer
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = warp / W, wi = warp % W;
+  const int rows_per_cta = (ROW_THREADS / 32) / W;
+  const float inv_keep = a.p > 0.f ? 1.f / (1.f - a.p) : 1.f;
+  const bool has_ln = a.gamma != nullptr;  // no-LN mode: d = dy (+ dres)
+  float acc_g[VPT][8], acc_b[VPT][8], acc_d[VPT][8];
+#pragma unroll
+  for (int i = 0; i < VPT; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc_g[i][j] = acc_b[i][j] = acc_d[i][j] = 0.f;
+
+  for (int row0 = blockIdx.x * rows_per_cta; row0 < a.M; row0 += gridDim.x * rows_per_cta) {
+    const int row = row0 + slot;
+    const bool valid = row < a.M;
+    float xh[VPT][8], g[VPT][8];
+    float mu = 0.f, rs = 0.f;
+    if (valid && has_ln) {
+      mu = a.mean[row];
+      rs = a.rstd[row];
+    }
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int col = ((i * W + wi) * 32 + lane) * 8;
+      if (valid && !has_ln) {
+        load8(a.dy + (int64_t)row * a.H + col, g[i]);
+      } else if (valid) {
+        float dy[8], gm[8];
+        load8(a.r + (int64_t)row * a.H + col, xh[i]);
+        load8(a.dy + (int64_t)row * a.H + col, dy);
+        load8(a.gamma + col, gm);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          xh[i][j] = (xh[i][j] - mu) * rs;
+          g[i][j] = dy[j] * gm[j];
+          s1 += g[i][j];
+          s2 += g[i][j] * xh[i][j];
+          acc_g[i][j] += dy[j] * xh[i][j];
+          acc_b[i][j] += dy[j];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) xh[i][j] = g[i][j] = 0.f;
+      }
+    }
+    const float m1 = group_sum<W>(s1, sm, slot, wi) / a.H;
+    const float m2 = group_sum<W>(s2, sm + 8, slot, wi) / a.H;
+    if (!valid) continue;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int col = ((i * W + wi) * 32 + lane) * 8;
+      float d[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) d[j] = has_ln ? rs * (g[i][j] - m1 - xh[i][j] * m2) : g[i][j];
+      if (a.dres) {
+        float e[8];
+        load8(a.dres + (int64_t)row * a.H + col, e);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) d[j] += e[j];
+      }
+      round8(d);
+      if (a.dr_out) store8(a.dr_out + (int64_t)row * a.H + col, d);
+      if (a.p > 0.f) {
+        bool keep[8];
+        dropout_keep8(a.seed, a.layer, a.site, (uint64_t)(a.row_offset + row), col, a.p, keep);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) d[j] = keep[j] ? d[j] * inv_keep : 0.f;
+        round8(d);
+        store8(a.dsub_out + (int64_t)row * a.H + col, d);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc_d[i][j] += d[j];
+    }
+  }
+  // CTA partials: warps with the same wi own the same columns; slots are summed
+  // in ascending order through shared memory (deterministic).
+  float* out = a.partials + (int64_t)blockIdx.x * 3 * a.H;
+  flush_partial<W, VPT>(acc_g, out, red, rows_per_cta, slot, wi, lane);
+  flush_partial<W, VPT>(acc_b, out + a.H, red, rows_per_cta, slot, wi, lane);
+  flush_partial<W, VPT>(acc_d, out + 2 * a.H, red, rows_per_cta, slot, wi, lane);
+}
+
+// Reduce P partial rows of [P][K][H] to K outputs of H columns (fixed order).
+__global__ void colsum_reduce_kernel(const float* partials, int P, int K, int H, void* o0, void* o1, void* o2,
+                                     int out_f32, int accumulate) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = blockIdx.y;
+  if (col >= H) return;
+  void* o = k == 0 ? o0 : (k == 1 ? o1 : o2);
+  if (o == nullptr) return;
+  float s = 0.f;
+  for (int p = 0; p < P; ++p) s += partials[((int64_t)p * K + k) * H + col];
+  if (out_f32) {
+    float* f = reinterpret_cast<float*>(o);
+    f[col] = accumulate ? f[col] + s : s;
+  } else {
+    bf16* b = reinterpret_cast<bf16*>(o);
+    b[col] = f2bf(accumulate ? bf2f(b[col]) + s : s);
+  }
+}
+
+// generic column partial sums of a [M, N] bf16 matrix: grid.x = column blocks of 256, grid.y = row chunks
+__global__ void colsum_partial_kernel(const bf16* x, int M, int N, int64_t ldx, int rows_per_chunk, float* partials) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= N) return;
+  const int r0 = blockIdx.y * rows_per_chunk;
+  const int r1 = min(M, r0 + rows_per_chunk);
+  float s = 0.f;
+  for (int r = r0; r < r1; ++r) s += bf2f(x[(int64_t)r * ldx + col]);
+  partials[(int64_t)blockIdx.y * N + col] = s;
+}
+
+// ===========================================================================
+// softmax forward / backward over attention scores
+// ===========================================================================
+struct SoftmaxArgs {
+  const bf16* s;    // fwd: scores        bwd: probs P
+  const bf16* d;    // bwd: dPd (grad of dropped probs)
+  bf16* p_out;      // fwd: P             bwd: dS
+  bf16* pd_out;     // fwd: dropped probs (p > 0)
+  const float* mask;  // [B, s_k] additive, may be null
+  int B, nh, sq, sk;
+  float scale, p;
+  int causal;
+  uint64_t seed;
+  uint32_t layer;
+  int64_t sample_offset;
+  int head_offset, nh_global;
+};
+
+__device__ __forceinline__ uint64_t attn_logical_row(const SoftmaxArgs& a, int64_t row) {
+  const int64_t q = row % a.sq;
+  const int64_t bh = row / a.sq;
+  const int64_t h = bh % a.nh;
+  const int64_t b = bh / a.nh;
+  return (uint64_t)(((a.sample_offset + b) * a.nh_global + a.head_offset + h) * a.sq + q);
+}
+
+template <int NV>
+__global__ void __launch_bounds__(ROW_THREADS) softmax_fwd_kernel(const SoftmaxArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t rows = (int64_t)a.B * a.nh * a.sq;
+  const float inv_keep = a.p > 0.f ? 1.f / (1.f - a.p) : 1.f;
+  for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < rows; row += (int64_t)gridDim.x * 8) {
+    const int64_t q = row % a.sq;
+    const int64_t b = row / ((int64_t)a.nh * a.sq);
+    const int64_t lim = a.causal ? q + (a.sk - a.sq) : (int64_t)a.sk - 1;  // last visible key
+    const bf16* src = a.s + row * a.sk;
+    float v[NV][8];
+    float m = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int col = (i * 32 + lane) * 8;
+      if (col < a.sk) {
+        load8(src + col, v[i]);
+        float mk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (a.mask) {
+          const float4* mp = reinterpret_cast<const float4*>(a.mask + b * a.sk + col);
+          float4 m0 = mp[0], m1 = mp[1];
+          mk[0] = m0.x; mk[1] = m0.y; mk[2] = m0.z; mk[3] = m0.w;
+          mk[4] = m1.x; mk[5] = m1.y; mk[6] = m1.z; mk[7] = m1.w;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float t = v[i][j] * a.scale + mk[j];
+          v[i][j] = (col + j > lim) ? -INFINITY : t;
+          m = fmaxf(m, v[i][j]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[i][j] = -INFINITY;
+      }
+    }
+    m = warp_max(m);
+    const float msafe = (m == -INFINITY) ? 0.f : m;
+    float sum = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        v[i][j] = __expf(v[i][j] - msafe);
+        sum += v[i][j];
+      }
+    sum = warp_sum(sum);
+    const float inv = sum > 0.f ? 1.f / sum : 0.f;
+    const uint64_t g = a.p > 0.f ? attn_logical_row(a, row) : 0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int col = (i * 32 + lane) * 8;
+      if (col < a.sk) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[i][j] *= inv;
+        store8(a.p_out + row * a.sk + col, v[i]);
+        if (a.p > 0.f) {
+          bool keep[8];
+          dropout_keep8(a.seed, a.layer, 0u, g, col, a.p, keep);
+          float o[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) o[j] = keep[j] ? bf2f(f2bf(v[i][j])) * inv_keep : 0.f;
+          store8(a.pd_out + row * a.sk + col, o);
+        }
+      }
+    }
+  }
+}
+
+template <int NV>
+__global__ void __launch_bounds__(ROW_THREADS) softmax_bwd_kernel(const SoftmaxArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t rows = (int64_t)a.B * a.nh * a.sq;
+  const float inv_keep = a.p > 0.f ? 1.f / (1.f - a.p) : 1.f;
+  for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < rows; row += (int64_t)gridDim.x * 8) {
+    const uint64_t g = a.p > 0.f ? attn_logical_row(a, row) : 0;
+    float pv[NV][8], dv[NV][8], pdv[NV][8];
+    float c = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int col = (i * 32 + lane) * 8;
+      if (col < a.sk) {
+        load8(a.s + row * a.sk + col, pv[i]);
+        load8(a.d + row * a.sk + col, dv[i]);
+        bool keep[8];
+        if (a.p > 0.f) {
+          dropout_keep8(a.seed, a.layer, 0u, g, col, a.p, keep);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) keep[j] = true;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          pdv[i][j] = keep[j] ? pv[i][j] * inv_keep : 0.f;
+          c += pdv[i][j] * dv[i][j];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) pv[i][j] = dv[i][j] = pdv[i][j] = 0.f;
+      }
+    }
+    c = warp_sum(c);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int col = (i * 32 + lane) * 8;
+      if (col < a.sk) {
+        float o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = a.scale * (pdv[i][j] * dv[i][j] - pv[i][j] * c);
+        store8(a.p_out + row * a.sk + col, o);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// dispatch helpers
+// ---------------------------------------------------------------------------
+#define SMPK_UNPACK(...) __VA_ARGS__
+#define SMPK_ROW_CASE(W_, V_, KERNEL, CFG, ARGS) \
+  case W_ * 16 + V_:                             \
+    KERNEL<W_, V_><<<SMPK_UNPACK CFG>>> ARGS;    \
+    break;
+#define SMPK_DISPATCH_ROW(W_, VPT_, KERNEL, CFG, ARGS)                                                  \
+  switch ((W_) * 16 + (VPT_)) {                                                                       \
+    SMPK_ROW_CASE(1, 1, KERNEL, CFG, ARGS) SMPK_ROW_CASE(1, 2, KERNEL, CFG, ARGS)                      \
+    SMPK_ROW_CASE(1, 3, KERNEL, CFG, ARGS) SMPK_ROW_CASE(1, 4, KERNEL, CFG, ARGS)                      \
+    SMPK_ROW_CASE(1, 5, KERNEL, CFG, ARGS) SMPK_ROW_CASE(2, 3, KERNEL, CFG, ARGS)                      \
+    SMPK_ROW_CASE(2, 4, KERNEL, CFG, ARGS) SMPK_ROW_CASE(2, 5, KERNEL, CFG, ARGS)                      \
+    SMPK_ROW_CASE(4, 3, KERNEL, CFG, ARGS) SMPK_ROW_CASE(4, 4, KERNEL, CFG, ARGS)                      \
+    SMPK_ROW_CASE(4, 5, KERNEL, CFG, ARGS) SMPK_ROW_CASE(8, 3, KERNEL, CFG, ARGS)                      \
+    SMPK_ROW_CASE(8, 4, KERNEL, CFG, ARGS) SMPK_ROW_CASE(8, 5, KERNEL, CFG, ARGS)                      \
+    SMPK_ROW_CASE(8, 6, KERNEL, CFG, ARGS) SMPK_ROW_CASE(8, 7, KERNEL, CFG, ARGS)                      \
+    SMPK_ROW_CASE(8, 8, KERNEL, CFG, ARGS)                                                             \
+    default:                                                                                          \
+      set_last_error("unsupported row geometry W=%d VPT=%d", W_, VPT_);                               \
+      return SMPK_ERR_UNSUPPORTED;                                                                    \
+  }
+
+static bool geom_supported(const RowGeom& g) {
+  switch (g.W * 16 + g.VPT) {
+    case 17: case 18: case 19: case 20: case 21: case 35: case 36: case 37: case 67: case 68: case 69:
+    case 131: case 132: case 133: case 134: case 135: case 136:
+      return true;
+    default:
+      return false;
+  }
+}
+
+static int softmax_nv(int sk) {
+  int need = (sk + 255) / 256;
+  if (need <= 1) return 1;
+  if (need <= 2) return 2;
+  if (need <= 4) return 4;
+  if (need <= 8) return 8;
+  if (need <= 16) return 16;
+  return -1;
+}
+
+}  // namespace smpk
+
+using namespace smpk;
+
+extern "C" int smpk_bdr_ln_fwd(const void* x, const void* bias, const void* residual, void* r_out, const void* gamma,
+                               const void* beta, void* y_out, float* mean, float* rstd, int M, int H, float eps,
+                               float p_drop, uint64_t seed, int layer, int site, int64_t row_offset, void* stream) {
+  RowGeom geo;
+  SMPK_REQUIRE(M >= 0 && row_geom(H, geo) && geom_supported(geo), SMPK_ERR_UNSUPPORTED,
+               "smpk_bdr_ln_fwd: hidden size %d unsupported (need a multiple of 256)", H);
+  SMPK_REQUIRE(x != nullptr, SMPK_ERR_BAD_ARG, "smpk_bdr_ln_fwd: null x");
+  SMPK_REQUIRE(gamma == nullptr || (beta && y_out && mean && rstd), SMPK_ERR_BAD_ARG,
+               "smpk_bdr_ln_fwd: LayerNorm needs beta, y_out, mean and rstd");
+  SMPK_REQUIRE(gamma != nullptr || r_out != nullptr, SMPK_ERR_BAD_ARG, "smpk_bdr_ln_fwd: nothing to compute");
+  SMPK_REQUIRE(p_drop >= 0.f && p_drop < 1.f, SMPK_ERR_BAD_ARG, "smpk_bdr_ln_fwd: dropout p must be in [0,1)");
+  if (M == 0) return SMPK_OK;
+  BdrLnArgs a{reinterpret_cast<const bf16*>(x), reinterpret_cast<const bf16*>(bias),
+              reinterpret_cast<const bf16*>(residual), reinterpret_cast<bf16*>(r_out),
+              reinterpret_cast<const bf16*>(gamma), reinterpret_cast<const bf16*>(beta),
+              reinterpret_cast<bf16*>(y_out), mean, rstd, M, H, eps, p_drop, seed, (uint32_t)layer, (uint32_t)site,
+              row_offset};
+  const int grid = row_grid(M, geo.W);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  SMPK_DISPATCH_ROW(geo.W, geo.VPT, bdr_ln_fwd_kernel, (grid, ROW_THREADS, 0, st), (a));
+  return check_launch("smpk_bdr_ln_fwd");
+}
+
+static int64_t ln_bwd_grid(int M, int H) {
+  RowGeom geo;
+  if (!row_geom(H, geo)) return 0;
+  return row_grid(M, geo.W);
+}
+
+extern "C" int64_t smpk_ln_bwd_workspace(int M, int H) { return ln_bwd_grid(M, H) * 3 * (int64_t)H * 4; }
+
+extern "C" int smpk_ln_bwd(const void* dy, const void* r, const float* mean, const float* rstd, const void* gamma,
+                           const void* dres, void* dr_out, void* dsub_out, void* dgamma, void* dbeta, void* dbias,
+                           int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed, int layer,
+                           int site, int64_t row_offset, void* workspace, int64_t workspace_bytes, void* stream) {
+  RowGeom geo;
+  SMPK_REQUIRE(M > 0 && row_geom(H, geo) && geom_supported(geo), SMPK_ERR_UNSUPPORTED,
+               "smpk_ln_bwd: hidden size %d unsupported", H);
+  SMPK_REQUIRE(dy && (gamma == nullptr || (r && mean && rstd && dr_out)), SMPK_ERR_BAD_ARG,
+               "smpk_ln_bwd: null argument");
+  SMPK_REQUIRE(p_drop == 0.f || dsub_out, SMPK_ERR_BAD_ARG, "smpk_ln_bwd: dropout backward needs dsub_out");
+  const int grid = row_grid(M, geo.W);
+  SMPK_REQUIRE(workspace && workspace_bytes >= (int64_t)grid * 3 * H * 4, SMPK_ERR_BAD_ARG,
+               "smpk_ln_bwd: workspace too small (%lld < %lld)", (long long)workspace_bytes,
+               (long long)grid * 3 * H * 4);
+  LnBwdArgs a{reinterpret_cast<const bf16*>(dy), reinterpret_cast<const bf16*>(r), mean, rstd,
+              reinterpret_cast<const bf16*>(gamma), reinterpret_cast<const bf16*>(dres),
+              reinterpret_cast<bf16*>(dr_out), reinterpret_cast<bf16*>(dsub_out),
+              reinterpret_cast<float*>(workspace), M, H, p_drop, seed, (uint32_t)layer, (uint32_t)site, row_offset};
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int red_bytes = geo.W == 8 ? 0 : geo.W * geo.VPT * 8 * 32 * 4;
+  SMPK_DISPATCH_ROW(geo.W, geo.VPT, ln_bwd_kernel, (grid, ROW_THREADS, red_bytes, st), (a));
+  int rc = check_launch("smpk_ln_bwd");
+  if (rc) return rc;
+  dim3 rg((H + 255) / 256, 3);
+  colsum_reduce_kernel<<<rg, 256, 0, st>>>(reinterpret_cast<float*>(workspace), grid, 3, H, dgamma, dbeta, dbias,
+                                           grads_f32, accumulate);
+  return check_launch("smpk_ln_bwd(reduce)");
+}
+
+extern "C" int64_t smpk_colsum_workspace(int M, int N) {
+  int chunks = (M + 127) / 128;
+  return (int64_t)chunks * N * 4;
+}
+
+extern "C" int smpk_colsum(const void* x, int M, int N, int64_t ldx, void* out, int out_f32, int accumulate,
+                           void* workspace, int64_t workspace_bytes, void* stream) {
+  SMPK_REQUIRE(M > 0 && N > 0 && x && out, SMPK_ERR_BAD_ARG, "smpk_colsum: bad arguments");
+  const int rows = 128;
+  const int chunks = (M + rows - 1) / rows;
+  SMPK_REQUIRE(workspace && workspace_bytes >= (int64_t)chunks * N * 4, SMPK_ERR_BAD_ARG,
+               "smpk_colsum: workspace too small");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  dim3 g1((N + 255) / 256, chunks);
+  colsum_partial_kernel<<<g1, 256, 0, st>>>(reinterpret_cast<const bf16*>(x), M, N, ldx, rows,
+                                            reinterpret_cast<float*>(workspace));
+  int rc = check_launch("smpk_colsum");
+  if (rc) return rc;
+  dim3 g2((N + 255) / 256, 1);
+  colsum_reduce_kernel<<<g2, 256, 0, st>>>(reinterpret_cast<float*>(workspace), chunks, 1, N, out, nullptr, nullptr,
+                                           out_f32, accumulate);
+  return check_launch("smpk_colsum(reduce)");
+}
+
+#define SMPK_NV_CASE(NV_, KERNEL, CFG, ARGS) \
+  case NV_:                                  \
+    KERNEL<NV_><<<SMPK_UNPACK CFG>>> ARGS;   \
+    break;
+#define SMPK_DISPATCH_NV(NV_, KERNEL, CFG, ARGS)                                                 \
+  switch (NV_) {                                                                                 \
+    SMPK_NV_CASE(1, KERNEL, CFG, ARGS) SMPK_NV_CASE(2, KERNEL, CFG, ARGS)                        \
+    SMPK_NV_CASE(4, KERNEL, CFG, ARGS) SMPK_NV_CASE(8, KERNEL, CFG, ARGS)                        \
+    SMPK_NV_CASE(16, KERNEL, CFG, ARGS)                                                          \
+    default:                                                                                     \
+      set_last_error("unsupported key length");                                                 \
+      return SMPK_ERR_UNSUPPORTED;                                                               \
+  }
+
+extern "C" int smpk_softmax_fwd(const void* scores, void* probs, void* probs_drop, const float* mask_add, int B,
+                                int nh, int sq, int sk, float scale, int causal, float p_drop, uint64_t seed, int layer,
+                                int64_t sample_offset, int head_offset, int nh_global, void* stream) {
+  const int nv = softmax_nv(sk);
+  SMPK_REQUIRE(nv > 0 && sk % 8 == 0 && B > 0 && nh > 0 && sq > 0, SMPK_ERR_UNSUPPORTED,
+               "smpk_softmax_fwd: key length %d unsupported (multiple of 8, <= 4096)", sk);
+  SMPK_REQUIRE(scores && probs && (p_drop == 0.f || probs_drop), SMPK_ERR_BAD_ARG, "smpk_softmax_fwd: null argument");
+  SMPK_REQUIRE(!causal || sq <= sk, SMPK_ERR_BAD_SHAPE, "smpk_softmax_fwd: causal needs sq <= sk");
+  SoftmaxArgs a{reinterpret_cast<const bf16*>(scores), nullptr, reinterpret_cast<bf16*>(probs),
+                reinterpret_cast<bf16*>(probs_drop), mask_add, B, nh, sq, sk, scale, p_drop, causal, seed,
+                (uint32_t)layer, sample_offset, head_offset, nh_global};
+  const int64_t rows = (int64_t)B * nh * sq;
+  int64_t grid = (rows + 7) / 8;
+  if (grid > num_sms() * 8) grid = num_sms() * 8;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  SMPK_DISPATCH_NV(nv, softmax_fwd_kernel, ((int)grid, ROW_THREADS, 0, st), (a));
+  return check_launch("smpk_softmax_fwd");
+}
+
+extern "C" int smpk_softmax_bwd(const void* probs, const void* dprobs_drop, void* dscores, int B, int nh, int sq,
+                                int sk, float scale, float p_drop, uint64_t seed, int layer, int64_t sample_offset,
+                                int head_offset, int nh_global, void* stream) {
+  const int nv = softmax_nv(sk);
+  SMPK_REQUIRE(nv > 0 && sk % 8 == 0, SMPK_ERR_UNSUPPORTED, "smpk_softmax_bwd: key length %d unsupported", sk);
+  SMPK_REQUIRE(probs && dprobs_drop && dscores, SMPK_ERR_BAD_ARG, "smpk_softmax_bwd: null argument");
+  SoftmaxArgs a{reinterpret_cast<const bf16*>(probs), reinterpret_cast<const bf16*>(dprobs_drop),
+                reinterpret_cast<bf16*>(dscores), nullptr, nullptr, B, nh, sq, sk, scale, p_drop, 0, seed,
+                (uint32_t)layer, sample_offset, head_offset, nh_global};
+  const int64_t rows = (int64_t)B * nh * sq;
+  int64_t grid = (rows + 7) / 8;
+  if (grid > num_sms() * 8) grid = num_sms() * 8;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  SMPK_DISPATCH_NV(nv, softmax_bwd_kernel, ((int)grid, ROW_THREADS, 0, st), (a));
+  return check_launch("smpk_softmax_bwd");
+}

@@ -1,0 +1,207 @@
+"""Fused forward/backward of the transformer sub-layers on one TP rank (speed mode).
+
+``AttentionFn`` and ``MlpFn`` are torch.autograd.Functions whose forward and
+backward issue the sm_100a kernels of libsmpk directly (tcgen05 GEMMs with fused
+epilogues, fused softmax/dropout, fused bias-dropout-residual-LayerNorm), with
+the row-parallel partial-sum allreduce of the forward and the column-parallel
+input-gradient allreduce of the backward ("two allreduces during
+forward, and two allreduces during backward") issued over the TP group.
+
+Per-rank dataflow:
+  attention: [pre-LN] -> QKV_j (+b) -> per local head softmax(QK^T/sqrt(dh) + mask)
+             -> dropout -> .V -> ctx_j @ Wo_j^T -> AR -> +bo -> dropout -> +x -> [post-LN]
+  mlp:       [pre-LN] -> FC1_j (+b, act) -> FC2_j -> AR -> +b2 -> dropout -> +x -> [post-LN]
+The input x is the TP-group-replicated activation [B, s, H]; weights are the
+rank's shards in the Megatron layout (oracle/tp.py shard_layer_params_speed).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import collectives as C
+from . import kernels as K
+from . import ops
+from .ops import SITE_ATTN_OUT, SITE_MLP_OUT
+
+
+@dataclass
+class LayerMeta:
+    hidden: int
+    heads_local: int
+    heads_global: int
+    head_dim: int
+    eps: float
+    p_attn: float
+    p_hidden: float
+    causal: bool
+    pre_ln: bool
+    post_ln: bool
+    activation: str
+    layer_id: int
+    seed: int
+    head_offset: int
+    sample_offset: int  # global id of the first sample of x (dropout coordinates)
+    tp_size: int
+
+
+# ---------------------------------------------------------------------------
+# attention core: qkv [B*s, 3*hl*dh] -> ctx [B*s, hl*dh]
+# ---------------------------------------------------------------------------
+
+def attn_core_fwd(qkv: torch.Tensor, B: int, s: int, m: LayerMeta, mask_add):
+    hl, dh = m.heads_local, m.head_dim
+    hd = hl * dh
+    ld = 3 * hd
+    S = torch.empty(B, hl, s, s, dtype=qkv.dtype, device=qkv.device)
+    K.gemm_raw(qkv, 0, ld, (dh, s * ld), qkv[:, hd:], 0, ld, (dh, s * ld), S, s, (s * s, hl * s * s),
+               s, s, dh, nb=(hl, B))
+    P, Pd = ops.softmax_fwd(S, scale=1.0 / math.sqrt(dh), mask_add=mask_add, causal=m.causal, p=m.p_attn,
+                            seed=m.seed, layer=m.layer_id, sample_offset=m.sample_offset, head_offset=m.head_offset,
+                            nh_global=m.heads_global)
+    del S
+    ctx = torch.empty(B * s, hd, dtype=qkv.dtype, device=qkv.device)
+    K.gemm_raw(Pd, 0, s, (s * s, hl * s * s), qkv[:, 2 * hd:], 1, ld, (dh, s * ld), ctx, hd, (dh, s * hd),
+               s, dh, s, nb=(hl, B))
+    return ctx, P, Pd
+
+
+def attn_core_bwd(dctx: torch.Tensor, qkv: torch.Tensor, P, Pd, B: int, s: int, m: LayerMeta):
+    hl, dh = m.heads_local, m.head_dim
+    hd = hl * dh
+    ld = 3 * hd
+    dqkv = torch.empty_like(qkv)
+    # dPd = dctx V^T
+    dP = torch.empty(B, hl, s, s, dtype=qkv.dtype, device=qkv.device)
+    K.gemm_raw(dctx, 0, hd, (dh, s * hd), qkv[:, 2 * hd:], 0, ld, (dh, s * ld), dP, s, (s * s, hl * s * s),
+               s, s, dh, nb=(hl, B))
+    # dV = Pd^T dctx
+    K.gemm_raw(Pd, 1, s, (s * s, hl * s * s), dctx, 1, hd, (dh, s * hd), dqkv[:, 2 * hd:], ld, (dh, s * ld),
+               s, dh, s, nb=(hl, B))
+    dS = ops.softmax_bwd(P, dP, scale=1.0 / math.sqrt(dh), p=m.p_attn, seed=m.seed, layer=m.layer_id,
+                         sample_offset=m.sample_offset, head_offset=m.head_offset, nh_global=m.heads_global, out=dP)
+    # dQ = dS K ; dK = dS^T Q
+    K.gemm_raw(dS, 0, s, (s * s, hl * s * s), qkv[:, hd:], 1, ld, (dh, s * ld), dqkv, ld, (dh, s * ld),
+               s, dh, s, nb=(hl, B))
+    K.gemm_raw(dS, 1, s, (s * s, hl * s * s), qkv, 1, ld, (dh, s * ld), dqkv[:, hd:], ld, (dh, s * ld),
+               s, dh, s, nb=(hl, B))
+    return dqkv
+
+
+def _ln_in(x2, w, b, m: LayerMeta):
+    y, mean, rstd = ops.layer_norm(x2, w, b, m.eps)
+    return y, mean, rstd
+
+
+def _residual_bwd_out(dh: torch.Tensor, dr: torch.Tensor | None, x2, ln_w, mean, rstd, m: LayerMeta):
+    """Gradient wrt the sub-layer input x given dh (through the branch) and dr (through the residual)."""
+    if m.pre_ln:
+        dx, _, dgw, dgb, _ = ops.ln_bwd(dh, x2, mean, rstd, ln_w, dres=dr, want_dbias=False)
+        return dx, dgw, dgb
+    return ops.add(dh, dr), None, None
+
+
+# ---------------------------------------------------------------------------
+# attention sub-layer
+# ---------------------------------------------------------------------------
+
+class AttentionFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, wqkv, bqkv, wo, bo, pre_w, pre_b, post_w, post_b, mask_add, m: LayerMeta):
+        B, s, H = x.shape
+        x2 = x.reshape(B * s, H)
+        if m.pre_ln:
+            h, mu1, rs1 = _ln_in(x2, pre_w, pre_b, m)
+        else:
+            h, mu1, rs1 = x2, None, None
+        qkv = K.linear(h, wqkv, bqkv)
+        ctxv, P, Pd = attn_core_fwd(qkv, B, s, m, mask_add)
+        o = K.linear(ctxv, wo)
+        C.all_reduce(o)
+        r, y, mu2, rs2 = ops.bdr_ln(o, bias=bo, residual=x2, gamma=post_w if m.post_ln else None,
+                                    beta=post_b if m.post_ln else None, eps=m.eps, p=m.p_hidden, seed=m.seed,
+                                    layer=m.layer_id, site=SITE_ATTN_OUT, row_offset=m.sample_offset * s)
+        ctx.m, ctx.shape = m, (B, s, H)
+        ctx.save_for_backward(x2, h, mu1, rs1, qkv, P, Pd if Pd is not P else None, ctxv, r, mu2, rs2, wqkv, wo,
+                              pre_w, post_w)
+        out = y if m.post_ln else r
+        return out.view(B, s, H)
+
+    @staticmethod
+    def backward(ctx, dy):
+        m: LayerMeta = ctx.m
+        B, s, H = ctx.shape
+        x2, h, mu1, rs1, qkv, P, Pd, ctxv, r, mu2, rs2, wqkv, wo, pre_w, post_w = ctx.saved_tensors
+        if Pd is None:
+            Pd = P
+        dy2 = dy.reshape(B * s, H).contiguous()
+        # residual / post-LN / hidden dropout backward; dbo = colsum(do)
+        dr, do, dpost_w, dpost_b, dbo = ops.ln_bwd(dy2, r, mu2, rs2, post_w if m.post_ln else None, p=m.p_hidden,
+                                                   seed=m.seed, layer=m.layer_id, site=SITE_ATTN_OUT,
+                                                   row_offset=m.sample_offset * s, want_dr=m.post_ln)
+        if not m.post_ln:
+            dr = dy2
+        dwo = K.matmul_tn(do, ctxv)
+        dctx = K.matmul_nn(do, wo)
+        dqkv = attn_core_bwd(dctx, qkv, P, Pd, B, s, m)
+        dwqkv = K.matmul_tn(dqkv, h)
+        dbqkv = ops.colsum(dqkv)
+        if m.tp_size == 1 and not m.pre_ln:
+            dx = K.matmul_nn(dqkv, wqkv, epi=K.EPI_ADD, aux=dr)
+            dpre_w = dpre_b = None
+        else:
+            dh = K.matmul_nn(dqkv, wqkv)
+            C.all_reduce(dh)
+            dx, dpre_w, dpre_b = _residual_bwd_out(dh, dr, x2, pre_w, mu1, rs1, m)
+        return (dx.view(B, s, H), dwqkv, dbqkv, dwo, dbo, dpre_w, dpre_b, dpost_w, dpost_b, None, None)
+
+
+# ---------------------------------------------------------------------------
+# MLP sub-layer
+# ---------------------------------------------------------------------------
+
+class MlpFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, w1, b1, w2, b2, pre_w, pre_b, post_w, post_b, m: LayerMeta):
+        B, s, H = x.shape
+        x2 = x.reshape(B * s, H)
+        if m.pre_ln:
+            h, mu1, rs1 = _ln_in(x2, pre_w, pre_b, m)
+        else:
+            h, mu1, rs1 = x2, None, None
+        f, z = K.linear(h, w1, b1, act=m.activation)
+        g = K.linear(f, w2)
+        C.all_reduce(g)
+        r, y, mu2, rs2 = ops.bdr_ln(g, bias=b2, residual=x2, gamma=post_w if m.post_ln else None,
+                                    beta=post_b if m.post_ln else None, eps=m.eps, p=m.p_hidden, seed=m.seed,
+                                    layer=m.layer_id, site=SITE_MLP_OUT, row_offset=m.sample_offset * s)
+        ctx.m, ctx.shape = m, (B, s, H)
+        ctx.save_for_backward(x2, h, mu1, rs1, f, z, r, mu2, rs2, w1, w2, pre_w, post_w)
+        out = y if m.post_ln else r
+        return out.view(B, s, H)
+
+    @staticmethod
+    def backward(ctx, dy):
+        m: LayerMeta = ctx.m
+        B, s, H = ctx.shape
+        x2, h, mu1, rs1, f, z, r, mu2, rs2, w1, w2, pre_w, post_w = ctx.saved_tensors
+        dy2 = dy.reshape(B * s, H).contiguous()
+        dr, dg, dpost_w, dpost_b, db2 = ops.ln_bwd(dy2, r, mu2, rs2, post_w if m.post_ln else None, p=m.p_hidden,
+                                                   seed=m.seed, layer=m.layer_id, site=SITE_MLP_OUT,
+                                                   row_offset=m.sample_offset * s, want_dr=m.post_ln)
+        if not m.post_ln:
+            dr = dy2
+        dw2 = K.matmul_tn(dg, f)
+        dz = K.matmul_nn(dg, w2, epi=K.EPI_DACT, act=m.activation, aux=z)
+        db1 = ops.colsum(dz)
+        dw1 = K.matmul_tn(dz, h)
+        if m.tp_size == 1 and not m.pre_ln:
+            dx = K.matmul_nn(dz, w1, epi=K.EPI_ADD, aux=dr)
+            dpre_w = dpre_b = None
+        else:
+            dh = K.matmul_nn(dz, w1)
+            C.all_reduce(dh)
+            dx, dpre_w, dpre_b = _residual_bwd_out(dh, dr, x2, pre_w, mu1, rs1, m)
+        return (dx.view(B, s, H), dw1, db1, dw2, db2, dpre_w, dpre_b, dpost_w, dpost_b, None)

@@ -1,0 +1,301 @@
+"""smp.nn — distributed modules of the tensor-parallel hot path.
+
+Signatures follow the paper's API: DistributedLinear,
+DistributedEmbedding, DistributedTransformerLayer, DistributedTransformer,
+DistributedTransformerLMHead, plus the DistributedAttentionLayer /
+DistributedTransformerOutputLayer children and
+DistributedLayerNorm.  Parameters live on the current CUDA device
+in bf16, sharded by tp_rank; forward/backward run in libsmpk (no CPU path).
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+from torch import nn
+
+from . import collectives as C
+from . import layers as L
+from .errors import NotDivisibleError, ShapeMismatchError
+from .state import STATE, next_layer_id
+
+DTYPE = torch.bfloat16
+
+
+class DistributedModule(nn.Module):
+    """Base class of every smp.nn module."""
+
+    @property
+    def tp_size(self) -> int:
+        return STATE.tp_size
+
+    @property
+    def tp_rank(self) -> int:
+        return STATE.tp_rank
+
+
+def _device():
+    if not torch.cuda.is_available():
+        raise RuntimeError("smp.nn modules need a CUDA device (libsmpk has no CPU path)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _param(shape, std, gen, zero=False, one=False):
+    dev = _device()
+    if zero:
+        t = torch.zeros(shape, dtype=DTYPE, device=dev)
+    elif one:
+        t = torch.ones(shape, dtype=DTYPE, device=dev)
+    else:
+        t = (torch.randn(shape, generator=gen, dtype=torch.float32, device=dev) * std).to(DTYPE)
+    return nn.Parameter(t)
+
+
+def _gen(layer_id: int, salt: int):
+    g = torch.Generator(device=_device())
+    g.manual_seed((STATE.seed * 1000003 + layer_id * 7919 + salt * 104729 + STATE.tp_rank) % (2 ** 63))
+    return g
+
+
+def _mask_2d(attention_mask, B, s):
+    """Accept an additive mask [B, s] or HF-extended [B, 1, 1, s]; returns fp32 [B, s] or None."""
+    if attention_mask is None:
+        return None
+    m = attention_mask.reshape(B, -1)
+    if m.shape[1] != s:
+        raise ShapeMismatchError(f"attention_mask must have {s} key positions, got {tuple(attention_mask.shape)}")
+    return m.to(torch.float32).contiguous()
+
+
+# ---------------------------------------------------------------------------
+# transformer (speed mode)
+# ---------------------------------------------------------------------------
+
+class _LayerBase(DistributedModule):
+    def __init__(self, num_attention_heads, attention_head_size, hidden_size, intermediate_size,
+                 attention_dropout_prob, hidden_dropout_prob, activation, layernorm_epsilon, initializer_range,
+                 use_normal_initialization, causal_mask_size, add_cross_attention, pre_layernorm, post_layernorm,
+                 layer_id=None):
+        super().__init__()
+        if hidden_size != num_attention_heads * attention_head_size:
+            raise ShapeMismatchError("hidden_size must equal num_attention_heads * attention_head_size")
+        T = STATE.tp_size
+        if num_attention_heads % T:
+            raise NotDivisibleError(f"num_attention_heads {num_attention_heads} not divisible by "
+                                    f"tensor_parallel_degree {T}")
+        if intermediate_size % T:
+            raise NotDivisibleError(f"intermediate_size {intermediate_size} not divisible by {T}")
+        if add_cross_attention:
+            raise NotImplementedError("add_cross_attention: only self-attention is on the hot path "
+                                      "(SPEC.md:513 non-goal)")
+        if activation not in ("gelu", "gelu_erf", "gelu_tanh", "relu"):
+            raise ValueError(f"activation must be gelu | gelu_tanh | relu, got {activation!r}")
+        self.num_attention_heads = num_attention_heads
+        self.attention_head_size = attention_head_size
+        self.hidden_size = hidden_size
+        self.intermediate_size = intermediate_size
+        self.attention_dropout_prob = attention_dropout_prob
+        self.hidden_dropout_prob = hidden_dropout_prob
+        self.activation = activation
+        self.layernorm_epsilon = layernorm_epsilon
+        self.initializer_range = initializer_range
+        self.causal_mask_size = causal_mask_size
+        self.pre_layernorm = pre_layernorm
+        self.post_layernorm = post_layernorm
+        self.layer_id = next_layer_id() if layer_id is None else layer_id
+
+    def _meta(self, sample_offset: int) -> L.LayerMeta:
+        T = STATE.tp_size
+        hl = self.num_attention_heads // T
+        return L.LayerMeta(hidden=self.hidden_size, heads_local=hl, heads_global=self.num_attention_heads,
+                           head_dim=self.attention_head_size, eps=self.layernorm_epsilon,
+                           p_attn=self.attention_dropout_prob if self.training else 0.0,
+                           p_hidden=self.hidden_dropout_prob if self.training else 0.0,
+                           causal=self.causal_mask_size is not None, pre_ln=self.pre_layernorm,
+                           post_ln=self.post_layernorm, activation=self.activation, layer_id=self.layer_id,
+                           seed=STATE.seed + 0x9E3779B97F4A7C15 * STATE.step, head_offset=STATE.tp_rank * hl,
+                           sample_offset=sample_offset, tp_size=T)
+
+    def _ln_params(self, prefix):
+        H = self.hidden_size
+        for where, flag in (("pre", self.pre_layernorm), ("post", self.post_layernorm)):
+            if flag:
+                setattr(self, f"{prefix}{where}_ln_weight", _param((H,), 0, None, one=True))
+                setattr(self, f"{prefix}{where}_ln_bias", _param((H,), 0, None, zero=True))
+            else:
+                setattr(self, f"{prefix}{where}_ln_weight", None)
+                setattr(self, f"{prefix}{where}_ln_bias", None)
+
+
+class DistributedAttentionLayer(_LayerBase):
+    """Self-attention sub-layer (speed mode): QKV column-parallel by heads, out-proj row-parallel."""
+
+    def __init__(self, num_attention_heads=32, attention_head_size=32, hidden_size=1024, attention_dropout_prob=0.1,
+                 hidden_dropout_prob=0.1, layernorm_epsilon=1e-5, initializer_range=0.02,
+                 use_normal_initialization=False, causal_mask_size=None, add_cross_attention=False,
+                 pre_layernorm=False, post_layernorm=True, layer_id=None, _standalone=True):
+        super().__init__(num_attention_heads, attention_head_size, hidden_size, 4 * hidden_size,
+                         attention_dropout_prob, hidden_dropout_prob, "gelu", layernorm_epsilon, initializer_range,
+                         use_normal_initialization, causal_mask_size, add_cross_attention, pre_layernorm,
+                         post_layernorm, layer_id)
+        self._standalone = _standalone
+        T, H = STATE.tp_size, hidden_size
+        g = _gen(self.layer_id, 1)
+        std = initializer_range
+        self.qkv_weight = _param((3 * H // T, H), std, g)
+        self.qkv_bias = _param((3 * H // T,), 0, None, zero=True)
+        self.dense_weight = _param((H, H // T), std, g)
+        self.dense_bias = _param((H,), 0, None, zero=True)
+        self._ln_params("")
+
+    def sublayer(self, X, mask, sample_offset):
+        m = self._meta(sample_offset)
+        return L.AttentionFn.apply(X, self.qkv_weight, self.qkv_bias, self.dense_weight, self.dense_bias,
+                                   self.pre_ln_weight, self.pre_ln_bias, self.post_ln_weight, self.post_ln_bias,
+                                   mask, m)
+
+    def forward(self, hidden_states, attention_mask=None):
+        return _run_standalone(self, hidden_states, attention_mask)
+
+    @torch.no_grad()
+    def load_full(self, p: dict):
+        """Load unsharded parameters (oracle layout: wqkv=[q;k;v] [3H,H], wo [H,H], ...)."""
+        T, j, H = STATE.tp_size, STATE.tp_rank, self.hidden_size
+        hs = H // T
+        sl = slice(j * hs, (j + 1) * hs)
+        wq, wk, wv = p["wqkv"].split(H, 0)
+        bq, bk, bv = p["bqkv"].split(H, 0)
+        self.qkv_weight.copy_(torch.cat([wq[sl], wk[sl], wv[sl]], 0))
+        self.qkv_bias.copy_(torch.cat([bq[sl], bk[sl], bv[sl]], 0))
+        self.dense_weight.copy_(p["wo"][:, sl])
+        self.dense_bias.copy_(p["bo"])
+        for where in ("pre", "post"):
+            if getattr(self, f"{where}_ln_weight") is not None:
+                getattr(self, f"{where}_ln_weight").copy_(p[f"attn_{where}_ln_w"])
+                getattr(self, f"{where}_ln_bias").copy_(p[f"attn_{where}_ln_b"])
+
+
+class DistributedTransformerOutputLayer(_LayerBase):
+    """MLP sub-layer (speed mode): FC1 column-parallel, FC2 row-parallel."""
+
+    def __init__(self, hidden_size=1024, intermediate_size=4096, hidden_dropout_prob=0.1, activation="gelu",
+                 layernorm_epsilon=1e-5, initializer_range=0.02, use_normal_initialization=False,
+                 pre_layernorm=False, post_layernorm=True, layer_id=None, num_attention_heads=1, _standalone=True):
+        super().__init__(num_attention_heads, hidden_size // num_attention_heads, hidden_size, intermediate_size,
+                         0.0, hidden_dropout_prob, activation, layernorm_epsilon, initializer_range,
+                         use_normal_initialization, None, False, pre_layernorm, post_layernorm, layer_id)
+        self._standalone = _standalone
+        T, H, I = STATE.tp_size, hidden_size, intermediate_size
+        g = _gen(self.layer_id, 2)
+        std = initializer_range
+        self.fc1_weight = _param((I // T, H), std, g)
+        self.fc1_bias = _param((I // T,), 0, None, zero=True)
+        self.fc2_weight = _param((H, I // T), std, g)
+        self.fc2_bias = _param((H,), 0, None, zero=True)
+        self._ln_params("")
+
+    def sublayer(self, X, mask, sample_offset):
+        m = self._meta(sample_offset)
+        return L.MlpFn.apply(X, self.fc1_weight, self.fc1_bias, self.fc2_weight, self.fc2_bias, self.pre_ln_weight,
+                             self.pre_ln_bias, self.post_ln_weight, self.post_ln_bias, m)
+
+    def forward(self, hidden_states, attention_mask=None):
+        return _run_standalone(self, hidden_states, None)
+
+    @torch.no_grad()
+    def load_full(self, p: dict):
+        T, j, I = STATE.tp_size, STATE.tp_rank, self.intermediate_size
+        ins = I // T
+        sl = slice(j * ins, (j + 1) * ins)
+        self.fc1_weight.copy_(p["w1"][sl])
+        self.fc1_bias.copy_(p["b1"][sl])
+        self.fc2_weight.copy_(p["w2"][:, sl])
+        self.fc2_bias.copy_(p["b2"])
+        for where in ("pre", "post"):
+            if getattr(self, f"{where}_ln_weight") is not None:
+                getattr(self, f"{where}_ln_weight").copy_(p[f"mlp_{where}_ln_w"])
+                getattr(self, f"{where}_ln_bias").copy_(p[f"mlp_{where}_ln_b"])
+
+
+def _entry(x, attention_mask):
+    """TP-across-DP entry: gather the TP group's samples; prescaled: nothing."""
+    B, s = x.shape[0], x.shape[1]
+    mask = _mask_2d(attention_mask, B, s)
+    if STATE.prescaled or STATE.tp_size == 1:
+        return x, mask, STATE.rdp_rank * B if STATE.prescaled else STATE.dp_rank * B
+    X = C.tp_dp_entry(x)
+    if mask is not None:
+        mask = C.all_gather(mask, 0)
+    return X, mask, STATE.rdp_rank * STATE.tp_size * B
+
+
+def _exit(Y):
+    if STATE.prescaled or STATE.tp_size == 1:
+        return Y
+    return C.tp_dp_exit(Y)
+
+
+def _run_standalone(mod, hidden_states, attention_mask):
+    x = hidden_states.to(DTYPE).contiguous()
+    X, mask, off = _entry(x, attention_mask)
+    return _exit(mod.sublayer(X, mask, off))
+
+
+class DistributedTransformerLayer(DistributedModule):
+    """smp.nn.DistributedTransformerLayer: attention -> residual -> norm -> MLP ->
+    residual -> norm, honouring pre_layernorm / post_layernorm (each sub-layer owns its LNs)."""
+
+    def __init__(self, num_attention_heads=32, attention_head_size=32, hidden_size=1024, intermediate_size=4096,
+                 attention_dropout_prob=0.1, hidden_dropout_prob=0.1, activation="gelu", layernorm_epsilon=1e-5,
+                 initializer_range=0.02, use_normal_initialization=False, causal_mask_size=None,
+                 add_cross_attention=False, pre_layernorm=False, post_layernorm=True, layer_id=None):
+        super().__init__()
+        if STATE.optimize == "memory" and STATE.tp_size > 1:
+            raise NotImplementedError("optimize='memory' runs in the CPU oracle only in this build; "
+                                      "use optimize='speed' on the GPU path")
+        lid = next_layer_id() if layer_id is None else layer_id
+        self.layer_id = lid
+        self.attention = DistributedAttentionLayer(
+            num_attention_heads, attention_head_size, hidden_size, attention_dropout_prob, hidden_dropout_prob,
+            layernorm_epsilon, initializer_range, use_normal_initialization, causal_mask_size, add_cross_attention,
+            pre_layernorm, post_layernorm, layer_id=lid, _standalone=False)
+        self.output = DistributedTransformerOutputLayer(
+            hidden_size, intermediate_size, hidden_dropout_prob, activation, layernorm_epsilon, initializer_range,
+            use_normal_initialization, pre_layernorm, post_layernorm, layer_id=lid,
+            num_attention_heads=num_attention_heads, _standalone=False)
+
+    def sublayer(self, X, mask, sample_offset):
+        return self.output.sublayer(self.attention.sublayer(X, mask, sample_offset), mask, sample_offset)
+
+    def forward(self, hidden_states, attention_mask=None):
+        return _run_standalone(self, hidden_states, attention_mask)
+
+    def load_full(self, p: dict):
+        self.attention.load_full(p)
+        self.output.load_full(p)
+
+
+class DistributedTransformer(DistributedModule):
+    """smp.nn.DistributedTransformer: num_layers DistributedTransformerLayers; the
+    TP-across-DP gather/return happens once at the stack boundary."""
+
+    def __init__(self, num_layers=12, num_attention_heads=32, attention_head_size=32, hidden_size=1024,
+                 intermediate_size=4096, attention_dropout_prob=0.1, hidden_dropout_prob=0.1, activation="gelu",
+                 layernorm_epsilon=1e-5, initializer_range=0.02, use_normal_initialization=False,
+                 causal_mask_size=None, add_cross_attention=False, pre_layernorm=False, post_layernorm=True):
+        super().__init__()
+        self.num_layers = num_layers
+        self.seq_layers = nn.ModuleList([
+            DistributedTransformerLayer(num_attention_heads, attention_head_size, hidden_size, intermediate_size,
+                                        attention_dropout_prob, hidden_dropout_prob, activation, layernorm_epsilon,
+                                        initializer_range, use_normal_initialization, causal_mask_size,
+                                        add_cross_attention, pre_layernorm, post_layernorm)
+            for _ in range(num_layers)])
+
+    def sublayer(self, X, mask, sample_offset):
+        for layer in self.seq_layers:
+            X = layer.sublayer(X, mask, sample_offset)
+        return X
+
+    def forward(self, hidden_states, attention_mask=None):
+        return _run_standalone(self, hidden_states, attention_mask)

@@ -1,0 +1,106 @@
+"""Torch-tensor wrappers of the row kernels (LayerNorm, softmax, dropout, colsum).
+
+Same contract as kernels.py: CUDA tensors only, outputs from the torch caching
+allocator, launches on the current stream, no CPU path.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .kernels import _check_cuda, _ptr, _stream
+
+SITE_ATTN_PROB, SITE_ATTN_OUT, SITE_MLP_OUT = 0, 1, 2
+
+
+def _f32(t):
+    return None if t is None else t
+
+
+def bdr_ln(x: torch.Tensor, *, bias=None, residual=None, gamma=None, beta=None, eps=1e-5, p=0.0, seed=0,
+           layer=0, site=SITE_ATTN_OUT, row_offset=0, want_r=True):
+    """r = residual + dropout(x + bias); y = LN(r). Returns (r, y, mean, rstd) (None where not computed)."""
+    _check_cuda(x, bias, residual, gamma, beta)
+    M, H = x.shape
+    r = torch.empty_like(x) if want_r else None
+    y = mean = rstd = None
+    if gamma is not None:
+        y = torch.empty_like(x)
+        mean = torch.empty(M, dtype=torch.float32, device=x.device)
+        rstd = torch.empty(M, dtype=torch.float32, device=x.device)
+    _lib.call("smpk_bdr_ln_fwd", _ptr(x), _ptr(bias), _ptr(residual), _ptr(r), _ptr(gamma), _ptr(beta), _ptr(y),
+              _ptr(mean), _ptr(rstd), M, H, float(eps), float(p), int(seed) & (2 ** 64 - 1), int(layer), int(site),
+              int(row_offset), _stream())
+    return r, y, mean, rstd
+
+
+def layer_norm(x: torch.Tensor, gamma, beta, eps=1e-5):
+    _, y, mean, rstd = bdr_ln(x, gamma=gamma, beta=beta, eps=eps, want_r=False)
+    return y, mean, rstd
+
+
+def add(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """a + b through the row kernel (bf16 round once)."""
+    r, _, _, _ = bdr_ln(a, residual=b)
+    return r
+
+
+def ln_bwd(dy, r, mean, rstd, gamma, *, dres=None, p=0.0, seed=0, layer=0, site=SITE_ATTN_OUT, row_offset=0,
+           want_dgamma=True, want_dbias=True, grads_f32=False, want_dr=True):
+    """Backward of bdr_ln. Returns (dr, dsub, dgamma, dbeta, dbias); dsub is dr when p == 0.
+
+    gamma None = no-LayerNorm mode (d = dy + dres)."""
+    _check_cuda(dy, r, gamma, dres)
+    M, H = dy.shape
+    dr = torch.empty_like(dy) if want_dr else None
+    dsub = torch.empty_like(dy) if p > 0 else None
+    gdt = torch.float32 if grads_f32 else dy.dtype
+    dgamma = torch.empty(H, dtype=gdt, device=dy.device) if (want_dgamma and gamma is not None) else None
+    dbeta = torch.empty(H, dtype=gdt, device=dy.device) if (want_dgamma and gamma is not None) else None
+    dbias = torch.empty(H, dtype=gdt, device=dy.device) if want_dbias else None
+    ws_bytes = _lib.size("smpk_ln_bwd_workspace", M, H)
+    ws = torch.empty(max(ws_bytes, 4) // 4, dtype=torch.float32, device=dy.device)
+    _lib.call("smpk_ln_bwd", _ptr(dy), _ptr(r), _ptr(mean), _ptr(rstd), _ptr(gamma), _ptr(dres), _ptr(dr),
+              _ptr(dsub), _ptr(dgamma), _ptr(dbeta), _ptr(dbias), int(grads_f32), 0, M, H, float(p),
+              int(seed) & (2 ** 64 - 1), int(layer), int(site), int(row_offset), _ptr(ws), int(ws_bytes), _stream())
+    if dsub is None:
+        dsub = dr if dr is not None else dy
+    return dr, dsub, dgamma, dbeta, dbias
+
+
+def softmax_fwd(scores: torch.Tensor, *, scale: float, mask_add=None, causal=False, p=0.0, seed=0, layer=0,
+                sample_offset=0, head_offset=0, nh_global=None):
+    """scores [B, nh, sq, sk] -> (P, Pd) with Pd = P when p == 0."""
+    _check_cuda(scores, mask_add)
+    B, nh, sq, sk = scores.shape
+    P = torch.empty_like(scores)
+    Pd = torch.empty_like(scores) if p > 0 else None
+    if mask_add is not None:
+        mask_add = mask_add.reshape(B, sk).to(torch.float32).contiguous()
+    _lib.call("smpk_softmax_fwd", _ptr(scores), _ptr(P), _ptr(Pd), _ptr(mask_add), B, nh, sq, sk, float(scale),
+              int(bool(causal)), float(p), int(seed) & (2 ** 64 - 1), int(layer), int(sample_offset), int(head_offset),
+              int(nh_global if nh_global is not None else nh), _stream())
+    return P, (Pd if Pd is not None else P)
+
+
+def softmax_bwd(P: torch.Tensor, dPd: torch.Tensor, *, scale: float, p=0.0, seed=0, layer=0, sample_offset=0,
+                head_offset=0, nh_global=None, out=None):
+    _check_cuda(P, dPd)
+    B, nh, sq, sk = P.shape
+    dS = out if out is not None else torch.empty_like(P)
+    _lib.call("smpk_softmax_bwd", _ptr(P), _ptr(dPd), _ptr(dS), B, nh, sq, sk, float(scale), float(p),
+              int(seed) & (2 ** 64 - 1), int(layer), int(sample_offset), int(head_offset),
+              int(nh_global if nh_global is not None else nh), _stream())
+    return dS
+
+
+def colsum(x: torch.Tensor, *, out_dtype=None) -> torch.Tensor:
+    """Column sums of a row-major [M, N] bf16 matrix (bias gradient)."""
+    _check_cuda(x)
+    M, N = x.shape
+    out = torch.empty(N, dtype=out_dtype or x.dtype, device=x.device)
+    ws_bytes = _lib.size("smpk_colsum_workspace", M, N)
+    ws = torch.empty(max(ws_bytes, 4) // 4, dtype=torch.float32, device=x.device)
+    _lib.call("smpk_colsum", _ptr(x), M, N, x.stride(0), _ptr(out), int(out.dtype == torch.float32), 0, _ptr(ws),
+              int(ws_bytes), _stream())
+    return out
