@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""Benchmark: TP transformer fwd+bwd tokens/s on 1/2/4/8 B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1]): BERT-large DistributedTransformer — 24 layers,
+hidden 1024, 16 heads x 64, FFN 4096, seq 512, post-LN, GeLU(erf), dropout 0.1,
+bf16 storage / fp32 accumulate — forward + backward, speed mode, TP degree =
+number of GPUs, TP across data-parallel ranks with 8 sequences per GPU (weak
+scaling: the gathered GEMM M is 4096*T, per-GPU work fixed).  Synthetic
+hidden states and random-init weights (no dataset / checkpoint).
+
+One JSON line on rank 0:
+  value      whole-job tokens/s, inputs resident in HBM, device-timed (CUDA events, max over ranks)
+  e2e        same metric through the public API with pinned-host inputs copied in and the
+             loss read back every step
+  roofline   the dominant kernel (smpk tcgen05 GEMM): algorithmic FLOPs / event-timed launch time
+  cpu_baseline  the CPU oracle (oracle/tp.py, torch fp32 on the host cores) on a bounded sample
+``--impl reference`` times only the CPU reference path (the reference has no TP
+code; its algorithm is restated in oracle/).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+METRIC = "TP transformer fwd+bwd tokens/sec at 1/2/4/8 B200; % of bf16 tensor-core peak"
+UNIT = "tokens/s"
+CFG = dict(num_layers=24, num_attention_heads=16, attention_head_size=64, hidden_size=1024, intermediate_size=4096,
+           attention_dropout_prob=0.1, hidden_dropout_prob=0.1, activation="gelu", layernorm_epsilon=1e-5,
+           pre_layernorm=False, post_layernorm=True)
+SEQ = 512
+BATCH_PER_GPU = 8
+
+
+def flops_per_token_layer(H=1024, s=SEQ, causal=False):
+    """fwd+bwd algorithmic FLOPs per token per layer: 72 H^2 + 12 s H (non-causal)."""
+    return 72 * H * H + (6 if causal else 12) * s * H
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.proc, self.lines = index, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        loaded = [v for v in sm if mx and v > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (the oracle restatement; the reference has no TP code)
+# ---------------------------------------------------------------------------
+
+def cpu_reference_sample(max_seconds=15.0, min_iters=2):
+    """One BERT-large layer fwd+bwd, 1 sequence of 512 tokens, torch fp32 on all host cores.
+    Returns (tokens/s of the 24-layer stack, threads, seconds, iterations)."""
+    from oracle import tp
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    cfg = tp.LayerConfig(num_attention_heads=16, attention_head_size=64, hidden_size=1024, intermediate_size=4096,
+                         attention_dropout_prob=0.1, hidden_dropout_prob=0.1)
+    p = {k: v.requires_grad_(True) for k, v in tp.init_layer_params(cfg, 1, dtype=torch.float32).items()}
+    x = torch.randn(1, SEQ, 1024, requires_grad=True)
+    dy = torch.randn(1, SEQ, 1024)
+    dctx = tp.DropoutCtx(seed=0, layer=0, torch_rng=True)
+    tp.transformer_layer_ref(x, p, cfg, None, dctx).backward(dy)  # untimed warm-up
+    t0 = time.perf_counter()
+    it = 0
+    while it < min_iters or (time.perf_counter() - t0 < max_seconds and it < 50):
+        y = tp.transformer_layer_ref(x, p, cfg, None, dctx)
+        y.backward(dy)
+        it += 1
+    dt = time.perf_counter() - t0
+    per_layer_tok_s = SEQ * it / dt
+    return per_layer_tok_s / CFG["num_layers"], threads, dt, it
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    steps = []
+    for i in range(args.warmup + args.steps):
+        v, threads, dt, it = cpu_reference_sample(max_seconds=args.ref_seconds, min_iters=1)
+        if i >= args.warmup:
+            steps.append(v)
+    value = statistics.median(steps)
+    sample = (f"1 BERT-large layer fwd+bwd on 1x{SEQ} tokens, torch fp32 CPU oracle (oracle/tp.py), "
+              f"scaled to the 24-layer stack; {cpu_model()}")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "config": {"workload": "bert-large-24L-tp-layer-stack", "global_batch": BATCH_PER_GPU * args.gpus,
+                       "seq_len": SEQ, "parallelism": f"tp{args.gpus}"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU path
+# ---------------------------------------------------------------------------
+
+def barrier():
+    if dist.is_initialized():
+        dist.barrier()
+
+
+def max_over_ranks(v: float) -> float:
+    if not dist.is_initialized():
+        return v
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_gpu(args, rank, world, local):
+    import paper_2111_05972_b200 as smp
+    from paper_2111_05972_b200 import _lib, kernels
+
+    torch.cuda.set_device(local)
+    smp.init({"tensor_parallel_degree": world, "optimize": "speed", "seed": 1234})
+    torch.manual_seed(1000 + rank)
+    model = smp.nn.DistributedTransformer(**CFG)
+    model.train()
+    B, s, H = BATCH_PER_GPU, SEQ, CFG["hidden_size"]
+    x = torch.randn(B, s, H, device="cuda", dtype=torch.bfloat16, requires_grad=True)
+    dy = torch.randn(B, s, H, device="cuda", dtype=torch.bfloat16)
+
+    def step(inp, grad):
+        for prm in model.parameters():
+            prm.grad = None
+        y = model(inp)
+        y.backward(grad)
+        return y
+
+    run = lambda: step(x, dy)  # noqa: E731
+    if args.graph:
+        # capture the whole fwd+bwd step (every smpk launch + NCCL) in one CUDA graph:
+        # removes the host launch path from the step
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(max(args.warmup, 2)):
+                step(x, dy)
+        torch.cuda.current_stream().wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        launches_g0 = _lib.launch_count
+        with torch.cuda.graph(graph):
+            static_y = step(x, dy)
+        graph_launches = _lib.launch_count - launches_g0
+        run = graph.replay
+    for _ in range(args.warmup):
+        run()
+    torch.cuda.synchronize()
+    barrier()
+
+    # -------- timed region: inputs resident in HBM (activations >> 126 MB L2)
+    sampler = ClockSampler(local)
+    sampler.start()
+    kernels.PROFILER = None if args.graph else kernels.GemmProfiler()
+    launches0 = _lib.launch_count
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    launches = (_lib.launch_count - launches0) // args.steps
+    prof, kernels.PROFILER = kernels.PROFILER, None
+    gemm_flops, gemm_ms, gemm_launches = prof.flops_and_ms() if prof else (0.0, 0.0, 0)
+    if args.graph:
+        launches = graph_launches
+        # events cannot bracket launches inside a replayed graph: time the GEMMs on one
+        # eager step right after the timed region instead
+        kernels.PROFILER = kernels.GemmProfiler()
+        step(x, dy)
+        prof, kernels.PROFILER = kernels.PROFILER, None
+        gemm_flops, gemm_ms, gemm_launches = prof.flops_and_ms()
+        gemm_flops, gemm_ms, gemm_launches = gemm_flops * args.steps, gemm_ms * args.steps, gemm_launches * args.steps
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    tokens_step = B * s * world
+    value = tokens_step / (ms / 1e3)
+
+    # -------- e2e through the public API: pinned host input + upstream grad in, loss out
+    xh = torch.randn(B, s, H, dtype=torch.bfloat16).pin_memory()
+    dyh = torch.randn(B, s, H, dtype=torch.bfloat16).pin_memory()
+    lossh = torch.empty(1, dtype=torch.float32).pin_memory()
+    xd = torch.empty(B, s, H, device="cuda", dtype=torch.bfloat16)
+    dyd = torch.empty_like(xd)
+
+    def e2e_step():
+        if args.graph:
+            with torch.no_grad():  # the graph's static input buffers
+                x.copy_(xh, non_blocking=True)
+                dy.copy_(dyh, non_blocking=True)
+            run()
+            y, g = static_y, dy
+        else:
+            xd.copy_(xh, non_blocking=True)
+            dyd.copy_(dyh, non_blocking=True)
+            y = step(xd.detach().requires_grad_(True), dyd)
+            g = dyd
+        lossh.copy_((y.detach().float() * g.float()).sum().reshape(1), non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        e2e_step()
+    t1.record()
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(t0.elapsed_time(t1) / args.steps)
+    barrier()
+
+    if rank != 0:
+        return
+    peaks, peak_kind = load_peaks()
+    peak_sus = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
+    flops_tok = flops_per_token_layer() * CFG["num_layers"]
+    model_tflops = value / world * flops_tok / 1e12  # per GPU
+    cpu = None
+    if not args.skip_cpu_baseline:
+        v, threads, dt, it = cpu_reference_sample(max_seconds=args.ref_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"1 BERT-large layer fwd+bwd x {it} iters on 1x{SEQ} tokens ({dt:.1f} s), torch fp32 "
+                         f"CPU oracle, scaled to 24 layers; {cpu_model()}"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic tokens' hidden states, random-init weights",
+        "config": {"workload": "bert-large-24L-tp-layer-stack (BASELINE.json configs[1])",
+                   "model": "BERT-large DistributedTransformer 24L H1024 16x64 FFN4096 post-LN gelu dropout0.1",
+                   "global_batch": B * world, "per_gpu_batch": B, "seq_len": s,
+                   "parallelism": f"tp{world} (speed mode, TP across DP ranks)",
+                   "l2": "inputs larger than L2 (saved activations ~6 GB per step)"},
+        "mfu": {"model_tflops_per_gpu": model_tflops, "flops_per_token": flops_tok,
+                "frac_of_sustained": model_tflops / peak_sus, "frac_of_burst": model_tflops / peaks["bf16_tflops"],
+                "peak_kind": peak_kind},
+        "roofline": {"bound": "tensor", "kernel": "smpk gemm_bf16_tcgen05 (all GEMM launches of the step)",
+                     "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s", "frac": achieved / peak_sus,
+                     "peak_kind": f"{peak_kind} bf16_tflops_sustained (kernel timed inside a long step)",
+                     "launches_per_step": gemm_launches // args.steps,
+                     "gemm_ms_per_step": gemm_ms / args.steps, "traffic": None},
+        "cpu_baseline": cpu,
+        "e2e": {"value": tokens_step / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": 2 * xh.numel() * xh.element_size(), "d2h_bytes_per_step": 4},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="smpk", choices=["smpk", "reference"])
+    ap.add_argument("--ref-seconds", type=float, default=12.0)
+    ap.add_argument("--skip-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", type=int, default=1, help="capture the step in a CUDA graph (1) or run eagerly (0)")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1 and not dist.is_initialized():
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    run_gpu(args, rank, world, local)
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

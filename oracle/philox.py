@@ -8,8 +8,9 @@ dropout decision from Philox4x32-10 keyed by the 64-bit seed and countered by
 RNG rule"), so masks are invariant to the TP degree and the oracle reproduces
 them exactly:
 
-    counter = (col >> 2, row, layer, site);  word = output[col & 3]
-    keep    = float(word >> 8) * 2**-24 >= p
+    counter = (col >> 3, row, layer, site);  word = output[(col >> 1) & 3]
+    u16     = (word >> (16 * (col & 1))) & 0xffff
+    keep    = u16 >= rint(p * 65536)            (16 random bits per element)
 
 Sites: 0 = attention probabilities (row = (global_sample*nh + global_head)*s_q + q,
 col = key position), 1 = attention-output hidden dropout, 2 = MLP-output hidden
@@ -53,23 +54,27 @@ def philox4x32_10(c0, c1, c2, c3, seed: int):
     return x, y, z, w
 
 
-def uniform_words(rows: np.ndarray, cols: np.ndarray, layer: int, site: int, seed: int) -> np.ndarray:
-    """The 32-bit Philox word used for element (row, col); rows/cols broadcast."""
+def uniform16(rows: np.ndarray, cols: np.ndarray, layer: int, site: int, seed: int) -> np.ndarray:
+    """The 16-bit draw of element (row, col): one Philox call per 8 columns,
+    word = out[(col >> 1) & 3], low half for even col, high half for odd."""
     rows = np.asarray(rows, dtype=np.int64)
     cols = np.asarray(cols, dtype=np.int64)
     rows, cols = np.broadcast_arrays(rows, cols)
-    x, y, z, w = philox4x32_10((cols >> 2).astype(np.uint32), rows.astype(np.uint32),
+    x, y, z, w = philox4x32_10((cols >> 3).astype(np.uint32), rows.astype(np.uint32),
                                np.uint32(layer), np.uint32(site), seed)
-    lane = (cols & 3)
-    out = np.where(lane == 0, x, np.where(lane == 1, y, np.where(lane == 2, z, w)))
-    return out.astype(np.uint32)
+    lane = (cols >> 1) & 3
+    word = np.where(lane == 0, x, np.where(lane == 1, y, np.where(lane == 2, z, w))).astype(np.uint32)
+    return np.where((cols & 1) == 0, word & np.uint32(0xFFFF), word >> np.uint32(16)).astype(np.uint32)
+
+
+def threshold(p: float) -> int:
+    """rint(p * 65536) in fp32 (csrc/smpk_common.cuh dropout_threshold)."""
+    return int(np.rint(np.float32(p) * np.float32(65536.0)))
 
 
 def keep_mask(rows, cols, layer: int, site: int, seed: int, p: float) -> np.ndarray:
-    """Boolean keep mask: keep iff (word >> 8) * 2^-24 >= p, compared in fp32."""
-    words = uniform_words(rows, cols, layer, site, seed)
-    u = (words >> np.uint32(8)).astype(np.float32) * np.float32(1.0 / 16777216.0)
-    return u >= np.float32(p)
+    """Boolean keep mask: keep iff u16 >= rint(p * 65536)."""
+    return uniform16(rows, cols, layer, site, seed) >= np.uint32(threshold(p))
 
 
 def hidden_mask(global_rows: np.ndarray, n_cols: int, layer: int, site: int, seed: int, p: float) -> np.ndarray:

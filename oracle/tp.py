@@ -70,6 +70,9 @@ class DropoutCtx:
     seed: int = 0
     layer: int = 0
     sample_offset: int = 0  # global id of sample 0 of the tensor the op sees
+    # timing-only mode (bench.py CPU baseline): draw masks with torch's CPU RNG instead
+    # of the bit-exact numpy Philox, which would dominate a CPU timing
+    torch_rng: bool = False
 
 
 # ---------------------------------------------------------------------------
@@ -438,7 +441,9 @@ def attention_core(q, k, v, mask_add, causal, dctx: DropoutCtx | None, p_attn: f
     scores = (qh @ kh.transpose(-1, -2)) * (1.0 / math.sqrt(dh))
     scores = attention_scores_mask(scores, mask_add, causal)
     probs = safe_softmax(scores)
-    if dctx is not None and p_attn > 0:
+    if dctx is not None and p_attn > 0 and dctx.torch_rng:
+        probs = probs * (torch.rand(probs.shape, dtype=probs.dtype) >= p_attn) / (1.0 - p_attn)
+    elif dctx is not None and p_attn > 0:
         keep = philox.attn_prob_mask(np.arange(B) + dctx.sample_offset, np.arange(nh) + head_offset,
                                      s, s, nh_global, dctx.layer, dctx.seed, p_attn)
         probs = _dropout(probs, keep, p_attn)
@@ -449,6 +454,8 @@ def attention_core(q, k, v, mask_add, causal, dctx: DropoutCtx | None, p_attn: f
 def _hidden_keep(dctx, B, s, H, site, p, col_offset=0, n_cols=None):
     if dctx is None or p == 0:
         return None
+    if dctx.torch_rng:
+        return (torch.rand(B, s, n_cols if n_cols is not None else H) >= p).numpy()
     rows = np.arange(B * s) + dctx.sample_offset * s
     cols = np.arange(n_cols if n_cols is not None else H) + col_offset
     keep = philox.keep_mask(rows[:, None], cols[None, :], dctx.layer, site, dctx.seed, p)

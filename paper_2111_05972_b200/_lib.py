@@ -73,7 +73,14 @@ def lib() -> C.CDLL:
     return _lib
 
 
+# kernels launched by each entry point (for bench.py's gpu_launches count)
+LAUNCHES_PER_CALL = {"smpk_ln_bwd": 2, "smpk_colsum": 2}
+launch_count = 0
+
+
 def call(name: str, *args) -> None:
+    global launch_count
+    launch_count += LAUNCHES_PER_CALL.get(name, 1)
     rc = getattr(lib(), name)(*args)
     if rc != 0:
         raise_for(rc, lib().smpk_last_error().decode(errors="replace"))

@@ -22,7 +22,7 @@ namespace smpk {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B row
-constexpr int GEMM_THREADS = 256;
+constexpr int GEMM_THREADS = 384;  // warps 0-3: TMA, MMA, TMEM alloc, spare; 4-11: epilogue
 
 struct GemmArgs {
   int M, N, K;
@@ -59,17 +59,17 @@ __device__ __forceinline__ void decode_tile(const GemmArgs& g, int tile, int& b1
   b2 = b / g.nb1;
 }
 
-// Epilogue for 32 consecutive accumulator columns of one row.
-__device__ __forceinline__ void epilogue_store32(const GemmArgs& g, int row, int col0, int b1, int b2,
+// Epilogue for 32 consecutive accumulator columns of one row.  EPI / ACT / F32OUT /
+// BETA are compile-time so every instantiation is a straight-line, branch-free body.
+template <int EPI, int ACT, bool F32OUT, bool BETA>
+__device__ __forceinline__ void epilogue_store32(const GemmArgs& g, int row, int col0, int64_t c_off,
                                                  const uint32_t (&r)[32]) {
   float v[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * g.alpha;
-
-  const int64_t c_off = (int64_t)b1 * g.c_bs1 + (int64_t)b2 * g.c_bs2;
   const bool full = (col0 + 32 <= g.N) && g.vec_ok;
 
-  if (g.epi == SMPK_EPI_BIAS || g.epi == SMPK_EPI_BIAS_ACT) {
+  if constexpr (EPI == SMPK_EPI_BIAS || EPI == SMPK_EPI_BIAS_ACT) {
     if (full) {
       const uint4* bp = reinterpret_cast<const uint4*>(g.bias + col0);
 #pragma unroll
@@ -90,10 +90,12 @@ __device__ __forceinline__ void epilogue_store32(const GemmArgs& g, int row, int
     }
   }
 
-  if (g.epi == SMPK_EPI_BIAS_ACT || g.epi == SMPK_EPI_DACT || g.epi == SMPK_EPI_ADD) {
+  if constexpr (EPI == SMPK_EPI_BIAS_ACT || EPI == SMPK_EPI_DACT || EPI == SMPK_EPI_ADD) {
     bf16* ap = g.aux + c_off + (int64_t)row * g.ldaux + col0;
-    if (g.epi == SMPK_EPI_BIAS_ACT) {
-      // store the pre-activation, then activate
+    if constexpr (EPI == SMPK_EPI_BIAS_ACT) {
+      // store the pre-activation, then activate its bf16 rounding (what backward re-reads)
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = round_bf16(v[i]);
       if (full) {
         uint4* d = reinterpret_cast<uint4*>(ap);
 #pragma unroll
@@ -110,17 +112,15 @@ __device__ __forceinline__ void epilogue_store32(const GemmArgs& g, int row, int
         for (int i = 0; i < 32; ++i)
           if (col0 + i < g.N) ap[i] = f2bf(v[i]);
       }
-      // activation is applied to the bf16-rounded pre-activation so that the
-      // saved aux reproduces the forward exactly in the backward pass
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = act_fwd(g.act, bf2f(f2bf(v[i])));
+      for (int i = 0; i < 32; ++i) v[i] = act_fwd(ACT, v[i]);
     } else {
       float a[32];
       if (full) {
-        const uint4* s = reinterpret_cast<const uint4*>(ap);
+        const uint4* src = reinterpret_cast<const uint4*>(ap);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          uint4 u = s[q];
+          uint4 u = src[q];
           uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -133,9 +133,9 @@ __device__ __forceinline__ void epilogue_store32(const GemmArgs& g, int row, int
 #pragma unroll
         for (int i = 0; i < 32; ++i) a[i] = (col0 + i < g.N) ? bf2f(ap[i]) : 0.f;
       }
-      if (g.epi == SMPK_EPI_DACT) {
+      if constexpr (EPI == SMPK_EPI_DACT) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] *= act_bwd(g.act, a[i]);
+        for (int i = 0; i < 32; ++i) v[i] *= act_bwd(ACT, a[i]);
       } else {
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] += a[i];
@@ -143,14 +143,14 @@ __device__ __forceinline__ void epilogue_store32(const GemmArgs& g, int row, int
     }
   }
 
-  if (g.c_f32) {
+  if constexpr (F32OUT) {
     float* cp = reinterpret_cast<float*>(g.c) + c_off + (int64_t)row * g.ldc + col0;
     if (full) {
       float4* d = reinterpret_cast<float4*>(cp);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        if (g.beta != 0.f) {
+        if constexpr (BETA) {
           float4 old = d[q];
           o.x += g.beta * old.x;
           o.y += g.beta * old.y;
@@ -162,7 +162,7 @@ __device__ __forceinline__ void epilogue_store32(const GemmArgs& g, int row, int
     } else {
 #pragma unroll
       for (int i = 0; i < 32; ++i)
-        if (col0 + i < g.N) cp[i] = v[i] + (g.beta != 0.f ? g.beta * cp[i] : 0.f);
+        if (col0 + i < g.N) cp[i] = v[i] + (BETA ? g.beta * cp[i] : 0.f);
     }
   } else {
     bf16* cp = reinterpret_cast<bf16*>(g.c) + c_off + (int64_t)row * g.ldc + col0;
@@ -170,7 +170,7 @@ __device__ __forceinline__ void epilogue_store32(const GemmArgs& g, int row, int
       uint4* d = reinterpret_cast<uint4*>(cp);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        if (g.beta != 0.f) {
+        if constexpr (BETA) {
           uint4 old = d[q];
           uint32_t w[4] = {old.x, old.y, old.z, old.w};
 #pragma unroll
@@ -190,12 +190,12 @@ __device__ __forceinline__ void epilogue_store32(const GemmArgs& g, int row, int
     } else {
 #pragma unroll
       for (int i = 0; i < 32; ++i)
-        if (col0 + i < g.N) cp[i] = f2bf(v[i] + (g.beta != 0.f ? g.beta * bf2f(cp[i]) : 0.f));
+        if (col0 + i < g.N) cp[i] = f2bf(v[i] + (BETA ? g.beta * bf2f(cp[i]) : 0.f));
     }
   }
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int EPI, int ACT, bool F32OUT, bool BETA>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const GemmArgs g) {
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
-      mbar_init(&tempty_bar[i], 128);
+      mbar_init(&tempty_bar[i], 256);
     }
     fence_barrier_init();
   }
@@ -304,7 +304,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp >= 4) {
     // ---------------- epilogue ----------------
-    const int ew = warp - 4;  // TMEM lane quarter
+    // 8 warps: warp%4 selects the TMEM lane quarter (hardware rule), (warp-4)/4 the column half
+    const int quarter = warp & 3;
+    const int half = (warp - 4) >> 2;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < g.num_tiles; tile += gridDim.x) {
@@ -312,16 +314,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       decode_tile(g, tile, b1, b2, tm, tn);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      const int row = tm * BM + ew * 32 + lane;
-      const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        const int col0 = tn * BN + c * 32;
-        if (col0 >= g.N) break;  // warp-uniform
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(t_row + c * 32, r);
-        tmem_ld_wait();
-        if (row < g.M) epilogue_store32(g, row, col0, b1, b2, r);
+      const int row = tm * BM + quarter * 32 + lane;
+      const int64_t c_off = (int64_t)b1 * g.c_bs1 + (int64_t)b2 * g.c_bs2;
+      const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16);
+      // software-pipelined TMEM drain: the load of chunk i+1 is in flight while chunk i
+      // is processed and stored (tcgen05.wait::ld waits for all earlier loads).
+      constexpr int CH = BN / 64;  // 32-column chunks per warp
+      const int c_first = half * CH;
+      uint32_t r[2][32];
+      tmem_ld_32x32b_x32(t_row + c_first * 32, r[0]);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < CH; ++i) {
+        if (i + 1 < CH) tmem_ld_32x32b_x32(t_row + (c_first + i + 1) * 32, r[(i + 1) & 1]);
+        const int col0 = tn * BN + (c_first + i) * 32;
+        if (row < g.M && col0 < g.N) epilogue_store32<EPI, ACT, F32OUT, BETA>(g, row, col0, c_off, r[i & 1]);
+        if (i + 1 < CH) tmem_ld_wait();
       }
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
@@ -385,21 +393,54 @@ static int make_operand_map(CUtensorMap* map, const void* ptr, bool mn_major, in
   return SMPK_OK;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int EPI, int ACT, bool F32OUT, bool BETA>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs& g, cudaStream_t st) {
   using Cfg = GemmCfg<BN, STAGES>;
+  auto kern = gemm_bf16_tcgen05<BN, STAGES, EPI, ACT, F32OUT, BETA>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg::SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
     SMPK_REQUIRE(e == cudaSuccess, SMPK_ERR_CUDA, "smpk_gemm: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     attr_set = true;
   }
   g.tiles_n = (g.N + BN - 1) / BN;
   g.num_tiles = g.tiles_m * g.tiles_n * g.nb1 * g.nb2;
   int grid = g.num_tiles < num_sms() ? g.num_tiles : num_sms();
-  gemm_bf16_tcgen05<BN, STAGES><<<grid, GEMM_THREADS, Cfg::SMEM_BYTES, st>>>(ta, tb, g);
+  kern<<<grid, GEMM_THREADS, Cfg::SMEM_BYTES, st>>>(ta, tb, g);
   return check_launch("smpk_gemm");
+}
+
+template <int BN, int STAGES>
+static int dispatch_epilogue(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs& g, cudaStream_t st) {
+  const bool beta = g.beta != 0.f;
+  switch (g.epi) {
+    case SMPK_EPI_NONE:
+      if (g.c_f32) return beta ? launch_gemm<BN, STAGES, SMPK_EPI_NONE, 0, true, true>(ta, tb, g, st)
+                               : launch_gemm<BN, STAGES, SMPK_EPI_NONE, 0, true, false>(ta, tb, g, st);
+      return beta ? launch_gemm<BN, STAGES, SMPK_EPI_NONE, 0, false, true>(ta, tb, g, st)
+                  : launch_gemm<BN, STAGES, SMPK_EPI_NONE, 0, false, false>(ta, tb, g, st);
+    case SMPK_EPI_BIAS:
+      if (g.c_f32 || beta) break;
+      return launch_gemm<BN, STAGES, SMPK_EPI_BIAS, 0, false, false>(ta, tb, g, st);
+    case SMPK_EPI_BIAS_ACT:
+      if (g.c_f32 || beta) break;
+      if (g.act == SMPK_ACT_GELU_ERF) return launch_gemm<BN, STAGES, SMPK_EPI_BIAS_ACT, SMPK_ACT_GELU_ERF, false, false>(ta, tb, g, st);
+      if (g.act == SMPK_ACT_GELU_TANH) return launch_gemm<BN, STAGES, SMPK_EPI_BIAS_ACT, SMPK_ACT_GELU_TANH, false, false>(ta, tb, g, st);
+      if (g.act == SMPK_ACT_RELU) return launch_gemm<BN, STAGES, SMPK_EPI_BIAS_ACT, SMPK_ACT_RELU, false, false>(ta, tb, g, st);
+      break;
+    case SMPK_EPI_DACT:
+      if (g.c_f32 || beta) break;
+      if (g.act == SMPK_ACT_GELU_ERF) return launch_gemm<BN, STAGES, SMPK_EPI_DACT, SMPK_ACT_GELU_ERF, false, false>(ta, tb, g, st);
+      if (g.act == SMPK_ACT_GELU_TANH) return launch_gemm<BN, STAGES, SMPK_EPI_DACT, SMPK_ACT_GELU_TANH, false, false>(ta, tb, g, st);
+      if (g.act == SMPK_ACT_RELU) return launch_gemm<BN, STAGES, SMPK_EPI_DACT, SMPK_ACT_RELU, false, false>(ta, tb, g, st);
+      break;
+    case SMPK_EPI_ADD:
+      if (g.c_f32 || beta) break;
+      return launch_gemm<BN, STAGES, SMPK_EPI_ADD, 0, false, false>(ta, tb, g, st);
+  }
+  set_last_error("smpk_gemm: unsupported epilogue combination epi=%d act=%d c_f32=%d beta=%g", g.epi, g.act, g.c_f32,
+                 g.beta);
+  return SMPK_ERR_UNSUPPORTED;
 }
 
 }  // namespace smpk
@@ -460,7 +501,7 @@ extern "C" int smpk_gemm(const void* a, int a_mn_major, int64_t lda, int64_t a_b
   g.vec_ok = vec ? 1 : 0;
 
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (BN == 64) return launch_gemm<64, 8>(ta, tb, g, st);
-  if (BN == 128) return launch_gemm<128, 6>(ta, tb, g, st);
-  return launch_gemm<256, 4>(ta, tb, g, st);
+  if (BN == 64) return dispatch_epilogue<64, 8>(ta, tb, g, st);
+  if (BN == 128) return dispatch_epilogue<128, 6>(ta, tb, g, st);
+  return dispatch_epilogue<256, 4>(ta, tb, g, st);
 }

@@ -69,31 +69,27 @@ __device__ __forceinline__ void store8(bf16* p, const float (&v)[8]) {
 }
 __device__ __forceinline__ void round8(float (&v)[8]) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j) v[j] = bf2f(f2bf(v[j]));
-}
-
-// keep flags for 8 consecutive columns col0..col0+7 (col0 % 8 == 0) of logical row g
-__device__ __forceinline__ void dropout_keep8(uint64_t seed, uint32_t layer, uint32_t site, uint64_t g, int col0,
-                                              float p, bool (&keep)[8]) {
-  const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    u32x4 c = {static_cast<uint32_t>((col0 >> 2) + h), static_cast<uint32_t>(g), layer, site};
-    u32x4 r = philox4x32_10(c, k0, k1);
-    keep[4 * h + 0] = dropout_keep(r.x, p);
-    keep[4 * h + 1] = dropout_keep(r.y, p);
-    keep[4 * h + 2] = dropout_keep(r.z, p);
-    keep[4 * h + 3] = dropout_keep(r.w, p);
-  }
+  for (int j = 0; j < 8; ++j) v[j] = round_bf16(v[j]);
 }
 
 struct RowGeom {
   int W, VPT;
 };
 
+// Prefer <= 2 uint4 chunks per lane (register pressure / occupancy of the
+// memory-bound row kernels), spreading a row over up to 8 warps.
 static bool row_geom(int H, RowGeom& g) {
   if (H <= 0 || H % 256) return false;
   const int n = H / 256;
+  for (int W = 1; W <= 8; W *= 2) {
+    if (n % W) continue;
+    const int v = n / W;
+    if (v <= 2) {
+      g.W = W;
+      g.VPT = v;
+      return true;
+    }
+  }
   for (int W = 1; W <= 8; W *= 2) {
     if (n % W) continue;
     const int v = n / W;
@@ -157,7 +153,7 @@ __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs
         }
         if (a.p > 0.f) {
           bool keep[8];
-          dropout_keep8(a.seed, a.layer, a.site, (uint64_t)(a.row_offset + row), col, a.p, keep);
+          dropout_keep8(a.seed, a.layer, a.site, (uint64_t)(a.row_offset + row), col, dropout_threshold(a.p), keep);
 #pragma unroll
           for (int j = 0; j < 8; ++j) v[i][j] = keep[j] ? v[i][j] * inv_keep : 0.f;
         }
@@ -330,7 +326,7 @@ __global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const LnBwdArgs a) 
       if (a.dr_out) store8(a.dr_out + (int64_t)row * a.H + col, d);
       if (a.p > 0.f) {
         bool keep[8];
-        dropout_keep8(a.seed, a.layer, a.site, (uint64_t)(a.row_offset + row), col, a.p, keep);
+        dropout_keep8(a.seed, a.layer, a.site, (uint64_t)(a.row_offset + row), col, dropout_threshold(a.p), keep);
 #pragma unroll
         for (int j = 0; j < 8; ++j) d[j] = keep[j] ? d[j] * inv_keep : 0.f;
         round8(d);
@@ -349,15 +345,34 @@ __global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const LnBwdArgs a) 
 }
 
 // Reduce P partial rows of [P][K][H] to K outputs of H columns (fixed order).
-__global__ void colsum_reduce_kernel(const float* partials, int P, int K, int H, void* o0, void* o1, void* o2,
-                                     int out_f32, int accumulate) {
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+// block = 32 columns x 8 row groups; each thread sums every 8th partial row, then the
+// 8 group sums are added in ascending order (deterministic).
+__global__ void __launch_bounds__(256) colsum_reduce_kernel(const float* partials, int P, int K, int H, void* o0,
+                                                            void* o1, void* o2, int out_f32, int accumulate) {
+  __shared__ float sm[8][33];
+  const int c = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int col = blockIdx.x * 32 + c;
   const int k = blockIdx.y;
-  if (col >= H) return;
   void* o = k == 0 ? o0 : (k == 1 ? o1 : o2);
-  if (o == nullptr) return;
+  if (o == nullptr) return;  // uniform per block
+  float part = 0.f;
+  if (col < H) {
+    // 4 independent accumulators keep 4 loads in flight per thread; combined in fixed order
+    float q[4] = {0.f, 0.f, 0.f, 0.f};
+    int p = grp;
+    for (; p + 24 < P; p += 32) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) q[u] += partials[((int64_t)(p + 8 * u) * K + k) * H + col];
+    }
+    for (; p < P; p += 8) q[0] += partials[((int64_t)p * K + k) * H + col];
+    part = (q[0] + q[1]) + (q[2] + q[3]);
+  }
+  sm[grp][c] = part;
+  __syncthreads();
+  if (grp != 0 || col >= H) return;
   float s = 0.f;
-  for (int p = 0; p < P; ++p) s += partials[((int64_t)p * K + k) * H + col];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += sm[i][c];
   if (out_f32) {
     float* f = reinterpret_cast<float*>(o);
     f[col] = accumulate ? f[col] + s : s;
@@ -461,10 +476,10 @@ __global__ void __launch_bounds__(ROW_THREADS) softmax_fwd_kernel(const SoftmaxA
         store8(a.p_out + row * a.sk + col, v[i]);
         if (a.p > 0.f) {
           bool keep[8];
-          dropout_keep8(a.seed, a.layer, 0u, g, col, a.p, keep);
+          dropout_keep8(a.seed, a.layer, 0u, g, col, dropout_threshold(a.p), keep);
           float o[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) o[j] = keep[j] ? bf2f(f2bf(v[i][j])) * inv_keep : 0.f;
+          for (int j = 0; j < 8; ++j) o[j] = keep[j] ? round_bf16(v[i][j]) * inv_keep : 0.f;
           store8(a.pd_out + row * a.sk + col, o);
         }
       }
@@ -489,7 +504,7 @@ __global__ void __launch_bounds__(ROW_THREADS) softmax_bwd_kernel(const SoftmaxA
         load8(a.d + row * a.sk + col, dv[i]);
         bool keep[8];
         if (a.p > 0.f) {
-          dropout_keep8(a.seed, a.layer, 0u, g, col, a.p, keep);
+          dropout_keep8(a.seed, a.layer, 0u, g, col, dropout_threshold(a.p), keep);
         } else {
 #pragma unroll
           for (int j = 0; j < 8; ++j) keep[j] = true;
@@ -536,7 +551,8 @@ __global__ void __launch_bounds__(ROW_THREADS) softmax_bwd_kernel(const SoftmaxA
     SMPK_ROW_CASE(4, 5, KERNEL, CFG, ARGS) SMPK_ROW_CASE(8, 3, KERNEL, CFG, ARGS)                      \
     SMPK_ROW_CASE(8, 4, KERNEL, CFG, ARGS) SMPK_ROW_CASE(8, 5, KERNEL, CFG, ARGS)                      \
     SMPK_ROW_CASE(8, 6, KERNEL, CFG, ARGS) SMPK_ROW_CASE(8, 7, KERNEL, CFG, ARGS)                      \
-    SMPK_ROW_CASE(8, 8, KERNEL, CFG, ARGS)                                                             \
+    SMPK_ROW_CASE(8, 8, KERNEL, CFG, ARGS) SMPK_ROW_CASE(2, 2, KERNEL, CFG, ARGS)                      \
+    SMPK_ROW_CASE(4, 2, KERNEL, CFG, ARGS) SMPK_ROW_CASE(8, 2, KERNEL, CFG, ARGS)                      \
     default:                                                                                          \
       set_last_error("unsupported row geometry W=%d VPT=%d", W_, VPT_);                               \
       return SMPK_ERR_UNSUPPORTED;                                                                    \
@@ -545,7 +561,7 @@ __global__ void __launch_bounds__(ROW_THREADS) softmax_bwd_kernel(const SoftmaxA
 static bool geom_supported(const RowGeom& g) {
   switch (g.W * 16 + g.VPT) {
     case 17: case 18: case 19: case 20: case 21: case 35: case 36: case 37: case 67: case 68: case 69:
-    case 131: case 132: case 133: case 134: case 135: case 136:
+    case 131: case 132: case 133: case 134: case 135: case 136: case 34: case 66: case 130:
       return true;
     default:
       return false;
@@ -620,31 +636,69 @@ extern "C" int smpk_ln_bwd(const void* dy, const void* r, const float* mean, con
   SMPK_DISPATCH_ROW(geo.W, geo.VPT, ln_bwd_kernel, (grid, ROW_THREADS, red_bytes, st), (a));
   int rc = check_launch("smpk_ln_bwd");
   if (rc) return rc;
-  dim3 rg((H + 255) / 256, 3);
+  dim3 rg((H + 31) / 32, 3);
   colsum_reduce_kernel<<<rg, 256, 0, st>>>(reinterpret_cast<float*>(workspace), grid, 3, H, dgamma, dbeta, dbias,
                                            grads_f32, accumulate);
   return check_launch("smpk_ln_bwd(reduce)");
 }
 
+// Vectorised column partials: thread = 8 consecutive columns (one 16-B load per row),
+// 8 row groups per block interleaved over a 256-row chunk, summed in order in smem.
+__global__ void __launch_bounds__(256) colsum_partial_vec_kernel(const bf16* x, int M, int N, int64_t ldx,
+                                                                 float* partials) {
+  __shared__ float sm[8][32 * 8 + 1];
+  const int t = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int col0 = (blockIdx.x * 32 + t) * 8;
+  const int r0 = blockIdx.y * 256;
+  const int r1 = min(M, r0 + 256);
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (col0 < N) {
+#pragma unroll 4
+    for (int r = r0 + grp; r < r1; r += 8) {
+      float v[8];
+      load8(x + (int64_t)r * ldx + col0, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += v[j];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) sm[grp][t * 8 + j] = acc[j];
+  __syncthreads();
+  const int c = threadIdx.x;  // 256 columns of this block
+  const int col = blockIdx.x * 256 + c;
+  if (col < N) {
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += sm[i][c];
+    partials[(int64_t)blockIdx.y * N + col] = s;
+  }
+}
+
 extern "C" int64_t smpk_colsum_workspace(int M, int N) {
-  int chunks = (M + 127) / 128;
+  int chunks = (M + 255) / 256;
   return (int64_t)chunks * N * 4;
 }
 
 extern "C" int smpk_colsum(const void* x, int M, int N, int64_t ldx, void* out, int out_f32, int accumulate,
                            void* workspace, int64_t workspace_bytes, void* stream) {
   SMPK_REQUIRE(M > 0 && N > 0 && x && out, SMPK_ERR_BAD_ARG, "smpk_colsum: bad arguments");
-  const int rows = 128;
-  const int chunks = (M + rows - 1) / rows;
+  const int chunks = (M + 255) / 256;
   SMPK_REQUIRE(workspace && workspace_bytes >= (int64_t)chunks * N * 4, SMPK_ERR_BAD_ARG,
                "smpk_colsum: workspace too small");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  dim3 g1((N + 255) / 256, chunks);
-  colsum_partial_kernel<<<g1, 256, 0, st>>>(reinterpret_cast<const bf16*>(x), M, N, ldx, rows,
-                                            reinterpret_cast<float*>(workspace));
+  const bool vec = (N % 8 == 0) && (ldx % 8 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
+  if (vec) {
+    dim3 g1((N + 255) / 256, chunks);
+    colsum_partial_vec_kernel<<<g1, 256, 0, st>>>(reinterpret_cast<const bf16*>(x), M, N, ldx,
+                                                  reinterpret_cast<float*>(workspace));
+  } else {
+    dim3 g1((N + 255) / 256, chunks);
+    colsum_partial_kernel<<<g1, 256, 0, st>>>(reinterpret_cast<const bf16*>(x), M, N, ldx, 256,
+                                              reinterpret_cast<float*>(workspace));
+  }
   int rc = check_launch("smpk_colsum");
   if (rc) return rc;
-  dim3 g2((N + 255) / 256, 1);
+  dim3 g2((N + 31) / 32, 1);
   colsum_reduce_kernel<<<g2, 256, 0, st>>>(reinterpret_cast<float*>(workspace), chunks, 1, N, out, nullptr, nullptr,
                                            out_f32, accumulate);
   return check_launch("smpk_colsum(reduce)");

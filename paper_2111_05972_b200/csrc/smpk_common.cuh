@@ -178,28 +178,55 @@ __device__ __forceinline__ float2 unpack_bf16x2(uint32_t u) {
   return __bfloat1622float2(v);
 }
 
+// bf16 round-to-nearest-even kept in fp32, with integer ops (keeps the XU pipe free).
+__device__ __forceinline__ float round_bf16(float v) {
+  uint32_t u = __float_as_uint(v);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return __uint_as_float(u & 0xFFFF0000u);
+}
+
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Standard normal CDF Phi(z) = 0.5 (1 + erf(z/sqrt2)) with erf from Abramowitz & Stegun
+// 7.1.26 (|err| <= 1.5e-7): two MUFU ops (rcp, ex2) instead of libdevice erff + expf.
+// Also returns e = exp(-z^2/2), which the GeLU derivative reuses for the density.
+__device__ __forceinline__ float normal_cdf(float z, float& e) {
+  const float x = fabsf(z) * 0.7071067811865476f;
+  const float t = __fdividef(1.f, fmaf(0.3275911f, x, 1.f));
+  e = __expf(-x * x);
+  const float poly =
+      t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f), -0.284496736f), 0.254829592f);
+  const float erf_abs = 1.f - poly * e;
+  return 0.5f + 0.5f * copysignf(erf_abs, z);
+}
+
 // Activation functions. act: SMPK_ACT_GELU_ERF / SMPK_ACT_GELU_TANH / SMPK_ACT_RELU.
 __device__ __forceinline__ float act_fwd(int act, float z) {
   if (act == SMPK_ACT_RELU) return z > 0.f ? z : 0.f;
   if (act == SMPK_ACT_GELU_TANH) {
     const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-    float u = k0 * (z + k1 * z * z * z);
-    return 0.5f * z * (1.f + tanhf(u));
+    const float u = k0 * fmaf(k1 * z, z * z, z);
+    return 0.5f * z * (1.f + tanh_approx(u));
   }
-  return 0.5f * z * (1.f + erff(z * 0.7071067811865476f));
+  float e;
+  return z * normal_cdf(z, e);
 }
 
 __device__ __forceinline__ float act_bwd(int act, float z) {  // d act / dz
   if (act == SMPK_ACT_RELU) return z > 0.f ? 1.f : 0.f;
   if (act == SMPK_ACT_GELU_TANH) {
     const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-    float u = k0 * (z + k1 * z * z * z);
-    float t = tanhf(u);
-    return 0.5f * (1.f + t) + 0.5f * z * (1.f - t * t) * k0 * (1.f + 3.f * k1 * z * z);
+    const float u = k0 * fmaf(k1 * z, z * z, z);
+    const float t = tanh_approx(u);
+    return 0.5f * (1.f + t) + 0.5f * z * (1.f - t * t) * k0 * fmaf(3.f * k1, z * z, 1.f);
   }
-  float cdf = 0.5f * (1.f + erff(z * 0.7071067811865476f));
-  float pdf = 0.3989422804014327f * __expf(-0.5f * z * z);
-  return cdf + z * pdf;
+  float e;
+  const float cdf = normal_cdf(z, e);
+  return fmaf(z * 0.3989422804014327f, e, cdf);
 }
 
 // ---------------------------------------------------------------------------
@@ -229,9 +256,24 @@ __host__ __device__ __forceinline__ u32x4 philox4x32_10(u32x4 c, uint32_t k0, ui
   return c;
 }
 
-// keep iff uniform24(r) >= p, uniform24(r) = (r >> 8) * 2^-24 (exact in fp32)
-__host__ __device__ __forceinline__ bool dropout_keep(uint32_t r, float p) {
-  return static_cast<float>(r >> 8) * (1.0f / 16777216.0f) >= p;
+// Dropout draws 16 bits per element: one Philox call covers 8 consecutive columns.
+//   counter = (col >> 3, row, layer, site); word = out[(col >> 1) & 3];
+//   u16 = (word >> (16 * (col & 1))) & 0xffff;  keep iff u16 >= rint(p * 65536)
+__host__ __device__ __forceinline__ uint32_t dropout_threshold(float p) {
+  return static_cast<uint32_t>(rintf(p * 65536.f));
+}
+
+// keep flags for 8 consecutive columns col0..col0+7 (col0 % 8 == 0) of logical row g
+__device__ __forceinline__ void dropout_keep8(uint64_t seed, uint32_t layer, uint32_t site, uint64_t g, int col0,
+                                              uint32_t thresh, bool (&keep)[8]) {
+  u32x4 c = {static_cast<uint32_t>(col0 >> 3), static_cast<uint32_t>(g), layer, site};
+  u32x4 r = philox4x32_10(c, static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
+  const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    keep[2 * j] = (w[j] & 0xffffu) >= thresh;
+    keep[2 * j + 1] = (w[j] >> 16) >= thresh;
+  }
 }
 
 }  // namespace smpk

@@ -29,10 +29,30 @@ def _check_cuda(*ts: torch.Tensor | None) -> None:
             raise RuntimeError("smpk kernels run on CUDA tensors only (no CPU fallback)")
 
 
+class GemmProfiler:
+    """Brackets every smpk_gemm launch with CUDA events on its stream (bench.py roofline)."""
+
+    def __init__(self):
+        self.records = []  # (start_event, end_event, flops)
+
+    def flops_and_ms(self):
+        torch.cuda.synchronize()
+        fl = sum(r[2] for r in self.records)
+        ms = sum(r[0].elapsed_time(r[1]) for r in self.records)
+        return fl, ms, len(self.records)
+
+
+PROFILER: GemmProfiler | None = None
+
+
 def gemm_raw(a, a_mn, lda, a_bs, b, b_mn, ldb, b_bs, c, ldc, c_bs, M, N, K, nb=(1, 1),
              alpha=1.0, beta=0.0, epi=EPI_NONE, act=0, bias=None, aux=None, ldaux=0) -> None:
     """Direct binding of smpk_gemm; strides in elements, batch strides as 2-tuples."""
     _check_cuda(a, b, c, bias, aux)
+    prof = PROFILER
+    if prof is not None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
     _lib.call("smpk_gemm",
               _ptr(a), int(a_mn), int(lda), int(a_bs[0]), int(a_bs[1]),
               _ptr(b), int(b_mn), int(ldb), int(b_bs[0]), int(b_bs[1]),
@@ -40,6 +60,9 @@ def gemm_raw(a, a_mn, lda, a_bs, b, b_mn, ldb, b_bs, c, ldc, c_bs, M, N, K, nb=(
               int(M), int(N), int(K), int(nb[0]), int(nb[1]),
               float(alpha), float(beta), int(epi), int(act),
               _ptr(bias), _ptr(aux), int(ldaux), _stream())
+    if prof is not None:
+        e1.record()
+        prof.records.append((e0, e1, 2.0 * M * N * K * nb[0] * nb[1]))
 
 
 def _rowmajor(t: torch.Tensor, name: str) -> int:
