@@ -142,6 +142,47 @@ SMPK_API int64_t smpk_colsum_workspace(int M, int N);
 SMPK_API int smpk_colsum(const void* x, int M, int N, int64_t ldx, void* out, int out_f32, int accumulate,
                          void* workspace, int64_t workspace_bytes, void* stream);
 
+/*
+ * smpk_embed_fwd — embedding lookup of the rank's table slice.
+ *   Vocab-parallel (builder-defined extension): the rank owns global
+ *   rows [row_offset, row_offset + rows_local); non-owned ids give 0 (the TP combine
+ *   is an allreduce / reduce-scatter).  Embedding-dim sharded DistributedEmbedding
+ *   (SPEC.md:440-448): row_offset = 0, rows_local = vocab, table holds
+ *   the rank's D/T columns.  out[t, :dim] = lookup (+ pos_table[t % seq] if non-NULL).
+ *   Ids outside [0, vocab) set *err_pos = min(position) ("reported with
+ *   position"); err_pos must be initialised to UINT64_MAX by the caller.
+ */
+SMPK_API int smpk_embed_fwd(const int64_t* ids, int64_t n, const void* table, int64_t ld_table,
+                            int64_t row_offset, int64_t rows_local, int64_t vocab, int dim, void* out,
+                            int64_t ld_out, const void* pos_table, int64_t ld_pos, int seq,
+                            unsigned long long* err_pos, void* stream);
+/*
+ * smpk_embed_bwd — dtable[r] (+)= sum of dy[t] over tokens t with ids[t] == row_offset + r,
+ * accumulated in token order (bit-deterministic, no float atomics); rows equal to
+ * padding_row get no gradient (torch padding_idx semantics; pass -1 for none).
+ */
+SMPK_API int smpk_embed_bwd(const int64_t* ids, int64_t n, const void* dy, int64_t ld_dy, int64_t row_offset,
+                            int64_t rows_local, int dim, void* dtable, int64_t ld_dt, int out_f32,
+                            int accumulate, int64_t padding_row, void* stream);
+/*
+ * Vocab-parallel softmax cross-entropy (builder-defined).
+ *   fwd_local: stats[N][4] = {m_j, S_j = sum_{real cols} exp(l - m_j), l[target] if owned, owned}
+ *              for the shard covering global columns [col_offset, col_offset + v_local); columns
+ *              >= vocab are padding (-inf).
+ *   combine:   stats_all [T][N][4] (allgathered, rank order) -> loss[N] = log S + m - l_tgt with
+ *              m = max m_j, S = sum_j S_j e^{m_j - m}; ms[N][2] = (m, S).  Ignored rows -> 0.
+ *   bwd:       dlogits = (exp(l - m) / S - onehot(target)) * grad_loss[row] * grad_scale.
+ */
+SMPK_API int smpk_vocab_ce_fwd_local(const void* logits, int64_t ld, int64_t N, int v_local, int64_t col_offset,
+                                     int64_t vocab, const int64_t* targets, int64_t ignore_index, float* stats,
+                                     void* stream);
+SMPK_API int smpk_vocab_ce_combine(const float* stats_all, int T, int64_t N, const int64_t* targets,
+                                   int64_t ignore_index, float* loss, float* ms, void* stream);
+SMPK_API int smpk_vocab_ce_bwd(const void* logits, int64_t ld, int64_t N, int v_local, int64_t col_offset,
+                               int64_t vocab, const int64_t* targets, int64_t ignore_index, const float* ms,
+                               const float* grad_loss, float grad_scale, void* dlogits, int64_t ld_out,
+                               void* stream);
+
 #ifdef __cplusplus
 }
 #endif

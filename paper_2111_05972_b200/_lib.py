@@ -32,6 +32,11 @@ SIGNATURES: dict[str, list] = {
     "smpk_softmax_fwd": [P, P, P, P, I, I, I, I, F, I, F, C.c_uint64, I, L, I, I, P],
     "smpk_softmax_bwd": [P, P, P, I, I, I, I, F, F, C.c_uint64, I, L, I, I, P],
     "smpk_colsum": [P, I, I, L, P, I, I, P, L, P],
+    "smpk_embed_fwd": [P, L, P, L, L, L, L, I, P, L, P, L, I, P, P],
+    "smpk_embed_bwd": [P, L, P, L, L, L, I, P, L, I, I, L, P],
+    "smpk_vocab_ce_fwd_local": [P, L, L, I, L, L, P, L, P, P],
+    "smpk_vocab_ce_combine": [P, I, L, P, L, P, P, P],
+    "smpk_vocab_ce_bwd": [P, L, L, I, L, L, P, L, P, P, F, P, L, P],
 }
 
 # functions returning int64 (sizes) rather than a status code

@@ -165,6 +165,25 @@ class _TpDpExit(torch.autograd.Function):
         return all_gather(g.contiguous(), 0)
 
 
+class _AllGatherReplicated(torch.autograd.Function):
+    """Allgather of per-rank slices of a TP-replicated result (prescaled batch):
+    every rank computes the same loss, so the backward keeps the local slice (no comm)."""
+
+    @staticmethod
+    def forward(ctx, t, dim):
+        ctx.dim, ctx.n = dim, t.shape[dim]
+        return all_gather(t.contiguous(), dim)
+
+    @staticmethod
+    def backward(ctx, g):
+        i = STATE.tp_rank
+        return g.narrow(ctx.dim, i * ctx.n, ctx.n).contiguous(), None
+
+
+def allgather_replicated(t: torch.Tensor, dim: int) -> torch.Tensor:
+    return t if STATE.tp_size == 1 else _AllGatherReplicated.apply(t, dim)
+
+
 def tp_dp_entry(t: torch.Tensor) -> torch.Tensor:
     return t if STATE.tp_size == 1 else _TpDpEntry.apply(t)
 

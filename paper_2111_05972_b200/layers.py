@@ -47,6 +47,44 @@ class LayerMeta:
     tp_size: int
 
 
+class LinearFn(torch.autograd.Function):
+    """y = x @ W^T (+ b) on the tcgen05 GEMM; backward dX = dY W, dW = dY^T X, db = colsum(dY)."""
+
+    @staticmethod
+    def forward(ctx, x, W, b):
+        ctx.save_for_backward(x, W)
+        ctx.has_b = b is not None
+        return K.linear(x, W, b)
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, W = ctx.saved_tensors
+        dy = dy.contiguous()
+        dx = K.matmul_nn(dy, W) if ctx.needs_input_grad[0] else None
+        dW = K.matmul_tn(dy, x)
+        db = ops.colsum(dy) if ctx.has_b else None
+        return dx, dW, db
+
+
+class LayerNormFn(torch.autograd.Function):
+    """Replicated LayerNorm over the last dim (speed mode) on the row kernels."""
+
+    @staticmethod
+    def forward(ctx, x, w, b, eps):
+        shape = x.shape
+        x2 = x.reshape(-1, shape[-1]).contiguous()
+        y, mean, rstd = ops.layer_norm(x2, w, b, eps)
+        ctx.save_for_backward(x2, mean, rstd, w)
+        ctx.shape = shape
+        return y.view(shape)
+
+    @staticmethod
+    def backward(ctx, dy):
+        x2, mean, rstd, w = ctx.saved_tensors
+        dx, _, dw, db, _ = ops.ln_bwd(dy.reshape(x2.shape).contiguous(), x2, mean, rstd, w, want_dbias=False)
+        return dx.view(ctx.shape), dw, db, None
+
+
 # ---------------------------------------------------------------------------
 # attention core: qkv [B*s, 3*hl*dh] -> ctx [B*s, hl*dh]
 # ---------------------------------------------------------------------------

@@ -68,6 +68,63 @@ def _mask_2d(attention_mask, B, s):
 
 
 # ---------------------------------------------------------------------------
+# DistributedLinear (Fig 5, 802)
+# ---------------------------------------------------------------------------
+
+class _SliceFeatures(torch.autograd.Function):
+    """Prescaled input split: keep feature slice j; backward = allgather along features."""
+
+    @staticmethod
+    def forward(ctx, x, j, T):
+        n = x.shape[-1] // T
+        return x[..., j * n:(j + 1) * n]
+
+    @staticmethod
+    def backward(ctx, g):
+        return C.all_gather(g.contiguous(), -1), None, None
+
+
+class DistributedLinear(DistributedModule):
+    """smp.nn.DistributedLinear(in_features, out_features): W = [W_1 ... W_T] split column-wise
+    (over input features), bias only on tp_rank 0.  Each rank slices its input rows by
+    feature, all-to-all delivers slice j of every peer's samples to rank j, rank j applies
+    W_j to the gathered [T*b, in/T] block (+ b iff j == 0), and a reduce-scatter over the
+    batch returns y^(i) = sum_j W_j x_j^(i) (+ b) to rank i.  Prescaled batch: feature slice
+    -> partial product -> allreduce."""
+
+    def __init__(self, in_features, out_features, bias=True, initializer_range=0.02):
+        super().__init__()
+        T = STATE.tp_size
+        if in_features % T:
+            raise NotDivisibleError(f"in_features {in_features} not divisible by tensor_parallel_degree {T}")
+        self.in_features, self.out_features = in_features, out_features
+        g = _gen(next_layer_id(), 3)
+        self.weight = _param((out_features, in_features // T), initializer_range, g)
+        self.bias = _param((out_features,), 0, None, zero=True) if (bias and STATE.tp_rank == 0) else None
+
+    @torch.no_grad()
+    def load_full(self, W: torch.Tensor, b: torch.Tensor | None = None):
+        n = self.in_features // STATE.tp_size
+        j = STATE.tp_rank
+        self.weight.copy_(W[:, j * n:(j + 1) * n])
+        if self.bias is not None and b is not None:
+            self.bias.copy_(b)
+
+    def forward(self, x):
+        T, j = STATE.tp_size, STATE.tp_rank
+        lead = x.shape[:-1]
+        x2 = x.reshape(-1, self.in_features).to(DTYPE)
+        if T == 1:
+            y = L.LinearFn.apply(x2.contiguous(), self.weight, self.bias)
+        elif STATE.prescaled:
+            y = C.fwd_allreduce_for_tp(L.LinearFn.apply(_SliceFeatures.apply(x2, j, T), self.weight, self.bias))
+        else:
+            Xj = C.scatter_and_merge_for_tp(x2.contiguous(), -1, 0)  # [T*b, in/T]
+            y = C.reduce_scatter_for_tp(L.LinearFn.apply(Xj, self.weight, self.bias), 0)
+        return y.reshape(*lead, self.out_features)
+
+
+# ---------------------------------------------------------------------------
 # transformer (speed mode)
 # ---------------------------------------------------------------------------
 
@@ -299,3 +356,87 @@ class DistributedTransformer(DistributedModule):
 
     def forward(self, hidden_states, attention_mask=None):
         return _run_standalone(self, hidden_states, attention_mask)
+
+
+# ---------------------------------------------------------------------------
+# LayerNorm, embeddings, LM head
+# ---------------------------------------------------------------------------
+
+class DistributedLayerNorm(DistributedModule):
+    """smp.nn.DistributedLayerNorm.  In speed mode the LayerNorm is replicated
+    across the TP group and runs on the fused row kernel."""
+
+    def __init__(self, normalized_shape, eps=1e-5, elementwise_affine=True):
+        super().__init__()
+        n = normalized_shape if isinstance(normalized_shape, int) else normalized_shape[-1]
+        self.normalized_shape, self.eps = n, eps
+        self.weight = _param((n,), 0, None, one=True)
+        self.bias = _param((n,), 0, None, zero=True)
+
+    def forward(self, x):
+        return L.LayerNormFn.apply(x.to(DTYPE), self.weight, self.bias, self.eps)
+
+
+from .embedding import (DistributedEmbedding, VocabParallelEmbedding, lm_head_logits,  # noqa: E402
+                        vocab_parallel_cross_entropy)
+
+
+class DistributedTransformerLMHead(DistributedModule):
+    """smp.nn.DistributedTransformerLMHead: GPT-style LM with a vocab-parallel
+    word embedding tied to the LM head, learned position embeddings, a DistributedTransformer
+    stack, a final LayerNorm (pre-LN models) and the vocab-parallel cross-entropy.
+
+    forward(input_ids, attention_mask=None, labels=None): with labels returns the per-token
+    loss [b, s] (fp32, 0 where labels == -100); otherwise the vocab-sharded logits
+    [b, s, Vp/T].  The TP-across-DP gather happens once at the embedding (an allreduce of
+    the gathered partial lookups replaces reduce-scatter + the stack's allgather)."""
+
+    def __init__(self, num_layers=12, num_attention_heads=32, attention_head_size=32, hidden_size=1024,
+                 intermediate_size=4096, vocab_size=30522, num_positions=1024, attention_dropout_prob=0.1,
+                 hidden_dropout_prob=0.1, activation="gelu", layernorm_epsilon=1e-5, num_token_types=0,
+                 causal_mask_size=None, add_cross_attention=False, add_lm_head=True, initializer_range=0.02,
+                 use_normal_initialization=False, pre_layernorm=False, post_layernorm=True):
+        super().__init__()
+        if num_token_types:
+            raise NotImplementedError("token type embeddings are not on the TP hot path")
+        self.vocab_size, self.hidden_size, self.add_lm_head = vocab_size, hidden_size, add_lm_head
+        self.word_embedding = VocabParallelEmbedding(vocab_size, hidden_size, initializer_range=initializer_range)
+        g = _gen(next_layer_id(), 4)
+        self.position_embedding = nn.Parameter(
+            (torch.randn(num_positions, hidden_size, generator=g, device=_device()) * initializer_range).to(DTYPE))
+        self.transformer = DistributedTransformer(num_layers, num_attention_heads, attention_head_size, hidden_size,
+                                                  intermediate_size, attention_dropout_prob, hidden_dropout_prob,
+                                                  activation, layernorm_epsilon, initializer_range,
+                                                  use_normal_initialization, causal_mask_size, add_cross_attention,
+                                                  pre_layernorm, post_layernorm)
+        self.final_ln = DistributedLayerNorm(hidden_size, layernorm_epsilon) if pre_layernorm else None
+
+    def forward(self, input_ids, attention_mask=None, labels=None):
+        b, s = input_ids.shape
+        T = STATE.tp_size
+        gathered = not (STATE.prescaled or T == 1)
+        ids = C.all_gather(input_ids.contiguous(), 0) if gathered else input_ids
+        mask = _mask_2d(attention_mask, b, s)
+        if gathered and mask is not None:
+            mask = C.all_gather(mask, 0)
+        off = (STATE.rdp_rank * T * b) if gathered else (STATE.rdp_rank * b if STATE.prescaled else STATE.dp_rank * b)
+        we = self.word_embedding
+        from .embedding import _LookupFn
+        h = _LookupFn.apply(ids, we.weight, we.row_offset, we.num_embeddings, we.padding_idx,
+                            self.position_embedding if STATE.tp_rank == 0 else None, s, False)
+        h = h.reshape(ids.shape[0], s, self.hidden_size)
+        if T > 1:
+            h = C.fwd_allreduce_for_tp(h)
+        h = self.transformer.sublayer(h, mask, off)
+        if self.final_ln is not None:
+            h = self.final_ln(h)
+        if not self.add_lm_head:
+            return _exit(h) if gathered else h
+        logits = lm_head_logits(h, we.weight)  # [B*s, Vp/T]
+        if labels is None:
+            out = logits.reshape(ids.shape[0], s, -1)
+            return _exit(out) if gathered else out
+        lab = C.all_gather(labels.contiguous(), 0) if gathered else labels
+        loss = vocab_parallel_cross_entropy(logits, lab.reshape(-1), self.vocab_size)
+        loss = loss.reshape(ids.shape[0], s)
+        return _exit(loss) if gathered else loss

@@ -125,12 +125,113 @@ def run_case(smp, name, *, prescaled, causal, pre, post, p, layers=1, act="gelu"
     return bool(flag.item())
 
 
+def run_modules(smp, name, *, prescaled):
+    """DistributedLinear (Fig 5), DistributedEmbedding (dim-sharded) and the GPT LM head with
+    vocab-parallel embedding + cross-entropy at TP = world size."""
+    T, rank = dist.get_world_size(), dist.get_rank()
+    smp.init({"tensor_parallel_degree": T, "optimize": "speed", "_prescaled_batch": prescaled, "seed": 4})
+    g = torch.Generator().manual_seed(9)
+    B = 3
+    n = B if prescaled else B * T
+    errs = {}
+    # ---- DistributedLinear
+    W = (torch.randn(96, 64 * T, generator=g) * 0.1).to(torch.bfloat16)
+    bias = torch.randn(96, generator=g).to(torch.bfloat16)
+    X = torch.randn(n, 5, 64 * T, generator=g).to(torch.bfloat16)
+    DY = torch.randn(n, 5, 96, generator=g).to(torch.bfloat16)
+    sl = slice(0, n) if prescaled else slice(rank * B, (rank + 1) * B)
+    lin = smp.nn.DistributedLinear(64 * T, 96)
+    lin.load_full(W.cuda(), bias.cuda())
+    xg = X[sl].cuda().requires_grad_(True)
+    y = lin(xg)
+    y.backward(DY[sl].cuda())
+    ys, dxs, dws = gather_cpu(y.detach()), gather_cpu(xg.grad), gather_cpu(lin.weight.grad)
+    xr = X.double().requires_grad_(True)
+    Wr = W.double().requires_grad_(True)
+    br = bias.double().requires_grad_(True)
+    yr = xr @ Wr.t() + br
+    yr.backward(DY.double())
+    # ---- DistributedEmbedding (embedding-dim sharded)
+    V, D = 77, 16 * T
+    Et = torch.randn(V, D, generator=g).to(torch.bfloat16)
+    ids = torch.randint(0, V, (n, 6), generator=g)
+    emb = smp.nn.DistributedEmbedding(V, D)
+    emb.load_full(Et.cuda())
+    eo = emb(ids[sl].cuda())
+    eo.backward(torch.ones_like(eo))
+    eos, egs = gather_cpu(eo.detach()), gather_cpu(emb.weight.grad)
+    # ---- LM head: vocab-parallel embedding + tied head + vocab-parallel CE
+    L_, nh, dh, H, I, Vv, s = 1, 2 * T, 64, 128 * T, 256 * T, 1000 + 7, 64
+    model = smp.nn.DistributedTransformerLMHead(num_layers=L_, num_attention_heads=nh, attention_head_size=dh,
+                                                hidden_size=H, intermediate_size=I, vocab_size=Vv, num_positions=s,
+                                                attention_dropout_prob=0.0, hidden_dropout_prob=0.0,
+                                                activation="gelu_tanh", causal_mask_size=s, pre_layernorm=True,
+                                                post_layernorm=False)
+    cfg = tp.LayerConfig(num_attention_heads=nh, attention_head_size=dh, hidden_size=H, intermediate_size=I,
+                         activation="gelu_tanh", causal_mask_size=s, pre_layernorm=True, post_layernorm=False)
+    lp = {k: v.to(torch.bfloat16).double() for k, v in tp.init_layer_params(cfg, seed=21).items()}
+    Ew = (torch.randn(Vv, H, generator=g) * 0.02).to(torch.bfloat16).double()
+    wpe = (torch.randn(s, H, generator=g) * 0.02).to(torch.bfloat16).double()
+    model.transformer.seq_layers[0].load_full({k: v.to(torch.bfloat16) for k, v in lp.items()})
+    model.word_embedding.load_full(Ew.to(torch.bfloat16).cuda())
+    with torch.no_grad():
+        model.position_embedding.copy_(wpe.to(torch.bfloat16))
+    tok = torch.randint(0, Vv, (n, s), generator=g)
+    lab = torch.roll(tok, -1, 1)
+    lab[:, -1] = -100
+    loss = model(tok[sl].cuda(), labels=lab[sl].cuda())
+    loss.sum().backward()
+    losses = gather_cpu(loss.detach())
+    egrads = gather_cpu(model.word_embedding.weight.grad)
+    ok = True
+    if rank == 0:
+        if prescaled:
+            errs["lin_y"] = max(rel(v, yr.detach()) for v in ys)
+            errs["lin_dx"] = max(rel(v, xr.grad) for v in dxs)
+            errs["emb"] = max(rel(v, Et[ids].double()) for v in eos)
+        else:
+            errs["lin_y"] = rel(torch.cat(ys, 0), yr.detach())
+            errs["lin_dx"] = rel(torch.cat(dxs, 0), xr.grad)
+            errs["emb"] = rel(torch.cat(eos, 0), Et[ids].double())
+        n_in = 64
+        errs["lin_dw"] = max(rel(dws[j], Wr.grad[:, j * n_in:(j + 1) * n_in]) for j in range(T))
+        eg_ref = torch.zeros(V, D, dtype=torch.float64).index_add_(0, ids.reshape(-1),
+                                                                  torch.ones(ids.numel(), D, dtype=torch.float64))
+        if prescaled:  # every rank saw the same batch: each shard's grad = its column slice
+            errs["emb_dw"] = max(rel(egs[j], eg_ref[:, j * 16:(j + 1) * 16]) for j in range(T))
+        else:
+            errs["emb_dw"] = max(rel(egs[j], eg_ref[:, j * 16:(j + 1) * 16]) for j in range(T))
+        pr = {k: v.clone().requires_grad_(True) for k, v in lp.items()}
+        Er, wr = Ew.clone().requires_grad_(True), wpe.clone().requires_grad_(True)
+        h = Er[tok] + wr[None]
+        h = tp.transformer_layer_ref(h, pr, cfg, None, None)
+        h = tp.layer_norm(h, torch.ones(H, dtype=torch.float64), torch.zeros(H, dtype=torch.float64), 1e-5)
+        ref = tp.cross_entropy_ref((h @ Er.t()).reshape(-1, Vv), lab.reshape(-1), Vv).reshape(n, s)
+        ref.sum().backward()
+        errs["lm_loss"] = max(rel(v, ref.detach()) for v in losses) if prescaled else rel(torch.cat(losses, 0),
+                                                                                           ref.detach())
+        Vp = smp.embedding.vocab_padded(Vv, T)
+        full_g = torch.cat(egrads, 0)[:Vv]
+        errs["lm_dE"] = rel(full_g, Er.grad)
+        assert full_g.shape[0] == Vv and torch.cat(egrads, 0).shape[0] == Vp
+        bad = {k: v for k, v in errs.items() if not v < TOL}
+        ok = not bad
+        print(f"[{name}] T={T} {'OK' if ok else 'FAIL'} " + " ".join(f"{k}={v:.2e}" for k, v in errs.items()),
+              flush=True)
+    flag = torch.tensor([1 if ok else 0], device="cuda")
+    dist.broadcast(flag, 0)
+    smp.reset()
+    return bool(flag.item())
+
+
 def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2111_05972_b200 as smp
     results = [
+        run_modules(smp, "modules_tp_across_dp", prescaled=False),
+        run_modules(smp, "modules_prescaled", prescaled=True),
         run_case(smp, "tp_across_dp_post_ln", prescaled=False, causal=False, pre=False, post=True, p=0.0),
         run_case(smp, "prescaled_pre_ln_causal", prescaled=True, causal=True, pre=True, post=False, p=0.0),
         run_case(smp, "tp_across_dp_dropout", prescaled=False, causal=True, pre=True, post=False, p=0.1),
