@@ -183,6 +183,28 @@ SMPK_API int smpk_vocab_ce_bwd(const void* logits, int64_t ld, int64_t N, int v_
                                const float* grad_loss, float grad_scale, void* dlogits, int64_t ld_out,
                                void* stream);
 
+/*
+ * Pipeline stage send/recv over NVLink peer memory — the D2D communicator of the
+ * module server; replaces the simulated hop
+ * mpsim pipeline.py:653-712 (_transfer / _send_request / _send_response) whose routing
+ * and persistent-buffer accounting are comm.py:157-225.
+ *   smpk_p2p_alloc/free       persistent receive ring (slots + sequence words), zeroed
+ *   smpk_p2p_export/import    CUDA IPC handle (64 bytes) exchanged once per peer pair
+ *   smpk_p2p_send             [wait local_free >= wait_free] -> copy to peer slot ->
+ *                             peer_ready = seq + 1            (all stream-ordered)
+ *   smpk_p2p_recv             wait local_ready >= seq + 1 -> copy slot -> dst ->
+ *                             peer_free = seq + 1
+ */
+SMPK_API int smpk_p2p_alloc(int64_t bytes, void** ptr);
+SMPK_API int smpk_p2p_free(void* ptr);
+SMPK_API int smpk_p2p_export(void* ptr, void* handle_out);
+SMPK_API int smpk_p2p_import(const void* handle, void** ptr);
+SMPK_API int smpk_p2p_close(void* ptr);
+SMPK_API int smpk_p2p_send(void* peer_slot, const void* src, int64_t bytes, void* peer_ready, const void* local_free,
+                           uint32_t wait_free, uint32_t seq, void* stream);
+SMPK_API int smpk_p2p_recv(void* dst, const void* local_slot, int64_t bytes, const void* local_ready,
+                           void* peer_free, uint32_t seq, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

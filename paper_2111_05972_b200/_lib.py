@@ -37,6 +37,13 @@ SIGNATURES: dict[str, list] = {
     "smpk_vocab_ce_fwd_local": [P, L, L, I, L, L, P, L, P, P],
     "smpk_vocab_ce_combine": [P, I, L, P, L, P, P, P],
     "smpk_vocab_ce_bwd": [P, L, L, I, L, L, P, L, P, P, F, P, L, P],
+    "smpk_p2p_alloc": [L, C.POINTER(P)],
+    "smpk_p2p_free": [P],
+    "smpk_p2p_export": [P, P],
+    "smpk_p2p_import": [P, C.POINTER(P)],
+    "smpk_p2p_close": [P],
+    "smpk_p2p_send": [P, P, L, P, P, C.c_uint32, C.c_uint32, P],
+    "smpk_p2p_recv": [P, P, L, P, P, C.c_uint32, P],
 }
 
 # functions returning int64 (sizes) rather than a status code

@@ -1,0 +1,353 @@
+"""Pipeline parallelism: microbatch scheduler (Python) + D2D stage send/recv (libsmpk).
+
+* ``next_action`` / ``SchedulerState`` / ``SchedulePolicy`` restate the module-server
+  scheduler consulted at pp_rank 0 (mpsim pipeline.py:95-165): simple = forwards
+  0..M-1 then backwards in order, each gated on its forward; interleaved = a ready
+  backward (lowest microbatch) always wins over the next forward.
+* ``route`` / ``D2DBuffers`` restate the communication-backend routing rule
+  (comm.py:157-225): D2D unless the tensor is on CPU, the pair has
+  no NVLink (same node) / RDMA (cross node), or the persistent buffers are full,
+  in which case the transfer falls back (here: NCCL send/recv over the PP group).
+* ``StageChannel`` is the real D2D transport for one directed peer pair: persistent
+  IPC-mapped receive ring on the consumer, copy-engine peer copies on the producer's
+  stream, stream-ordered ready/free sequence words (csrc/p2p.cu) — no host sync.
+* ``static_schedule`` turns the scheduler decisions into per-stage op lists for a
+  chain of P stages (record-and-replay "static mode"), which
+  ``PipelineEngine`` executes SPMD (one process per GPU).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import heapq
+from dataclasses import dataclass, field
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+
+FWD = "forward"
+BWD = "backward"
+MPI = "MPI"
+D2D = "D2D"
+
+
+# ---------------------------------------------------------------------------
+# scheduler (pipeline.py:95-165)
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class SchedulePolicy:
+    kind: str = "interleaved"
+    microbatches: int = 1
+    forward_only: bool = False
+
+    def __post_init__(self):
+        if self.kind not in ("simple", "interleaved"):
+            raise ValueError(f"unknown pipeline policy {self.kind!r}")
+        if self.microbatches < 1:
+            raise ValueError("microbatch count must be >= 1")
+
+
+@dataclass
+class SchedulerState:
+    microbatches: int
+    issued_fwd: int = 0
+    completed_fwd: set = field(default_factory=set)
+    issued_bwd: set = field(default_factory=set)
+    completed_bwd: int = 0
+
+
+def ready_backwards(state: SchedulerState) -> list:
+    return sorted(m for m in state.completed_fwd if m not in state.issued_bwd)
+
+
+def next_action(policy: SchedulePolicy, state: SchedulerState):
+    """Next (microbatch, direction) to issue at pp_rank 0, or None to wait."""
+    M = policy.microbatches
+    ready = ready_backwards(state)
+    if policy.kind == "interleaved":
+        if not policy.forward_only and ready:
+            return (ready[0], BWD)
+        if state.issued_fwd < M:
+            return (state.issued_fwd, FWD)
+        return None
+    if state.issued_fwd < M:
+        return (state.issued_fwd, FWD)
+    if policy.forward_only:
+        return None
+    nb = len(state.issued_bwd)
+    if nb < M and nb in state.completed_fwd:
+        return (nb, BWD)
+    return None
+
+
+def static_schedule(policy: SchedulePolicy, stages: int, fwd_cost: float = 1.0, bwd_cost: float = 2.0):
+    """Record the scheduler's decisions on a P-stage chain and return per-stage op lists.
+
+    Event model: a forward of microbatch m visits stages 0..P-1 (each busy fwd_cost),
+    a backward visits P-1..0 (bwd_cost); stages execute their queue FIFO, one op at a
+    time.  pp_rank 0 consults next_action whenever it is idle, exactly like the module
+    server (pipeline.py:486-530).  Returns (decision_log, ops) with ops[stage] the ordered
+    list of (microbatch, direction) that stage executes."""
+    P, M = stages, policy.microbatches
+    st = SchedulerState(M)
+    busy_until = [0.0] * P
+    queues = [[] for _ in range(P)]  # (ready_time, seq, mb, dir)
+    ops = [[] for _ in range(P)]
+    log = []
+    events = []  # (time, seq, stage, mb, dir) completions
+    seq = 0
+    t = 0.0
+    done_bwd = 0
+    while done_bwd < M or (policy.forward_only and len(st.completed_fwd) < M):
+        # rank 0 consults the scheduler when idle and nothing is queued for it
+        if busy_until[0] <= t and not queues[0]:
+            act = next_action(policy, st)
+            if act is not None:
+                log.append({"t": t, "ready_backwards": ready_backwards(st), "action": list(act)})
+                mb, d = act
+                if d == FWD:
+                    st.issued_fwd += 1
+                    queues[0].append((t, seq, mb, d))
+                else:
+                    st.issued_bwd.add(mb)
+                    queues[P - 1].append((t, seq, mb, d))
+                seq += 1
+        # start queued work on idle stages
+        for s in range(P):
+            if busy_until[s] <= t and queues[s]:
+                queues[s].sort()
+                rt, _, mb, d = queues[s].pop(0)
+                cost = fwd_cost if d == FWD else bwd_cost
+                busy_until[s] = max(t, rt) + cost
+                ops[s].append((mb, d))
+                heapq.heappush(events, (busy_until[s], seq, s, mb, d))
+                seq += 1
+        if not events:
+            if policy.forward_only and len(st.completed_fwd) == M:
+                break
+            t += 1e-9
+            continue
+        t, _, s, mb, d = heapq.heappop(events)
+        if d == FWD:
+            if s + 1 < P:
+                queues[s + 1].append((t, seq, mb, d))
+                seq += 1
+            else:
+                st.completed_fwd.add(mb)
+        else:
+            if s > 0:
+                queues[s - 1].append((t, seq, mb, d))
+                seq += 1
+            else:
+                done_bwd += 1
+                st.completed_bwd += 1
+    return log, ops
+
+
+# ---------------------------------------------------------------------------
+# routing + persistent buffer accounting (comm.py:157-225)
+# ---------------------------------------------------------------------------
+
+class D2DBuffers:
+    def __init__(self, world_size: int, capacity_bytes: float):
+        self.capacity = capacity_bytes
+        self.send_used = [0.0] * world_size
+        self.recv_used = [0.0] * world_size
+
+    def reserve(self, rank: int, nbytes: float, kind: str) -> bool:
+        if nbytes < 0:
+            raise ValueError("cannot reserve negative bytes")
+        used = self.send_used if kind == "send" else self.recv_used
+        if used[rank] + nbytes > self.capacity:
+            return False
+        used[rank] += nbytes
+        return True
+
+    def release(self, rank: int, nbytes: float, kind: str) -> None:
+        used = self.send_used if kind == "send" else self.recv_used
+        if nbytes < 0 or used[rank] - nbytes < -1e-9:
+            raise ValueError(f"release of {nbytes} bytes exceeds reservations on rank {rank}")
+        used[rank] = max(used[rank] - nbytes, 0.0)
+
+    def try_reserve_pair(self, src: int, dst: int, nbytes: float) -> bool:
+        if not self.reserve(src, nbytes, "send"):
+            return False
+        if not self.reserve(dst, nbytes, "recv"):
+            self.release(src, nbytes, "send")
+            return False
+        return True
+
+    def release_pair(self, src: int, dst: int, nbytes: float) -> None:
+        self.release(src, nbytes, "send")
+        self.release(dst, nbytes, "recv")
+
+
+def route(device: str, nbytes: float, src: int, dst: int, *, same_node: bool, nvlink: bool, rdma: bool,
+          buffers: D2DBuffers) -> str:
+    """MPI (host-staged fallback) vs D2D for one tensor transfer, reserving D2D space."""
+    if src == dst:
+        raise ValueError("route requires distinct src and dst ranks")
+    if device == "cpu":
+        return MPI
+    if same_node:
+        if not nvlink:
+            return MPI
+    elif not rdma:
+        return MPI
+    if not buffers.try_reserve_pair(src, dst, nbytes):
+        return MPI
+    return D2D
+
+
+# ---------------------------------------------------------------------------
+# D2D transport
+# ---------------------------------------------------------------------------
+
+FLAG_BYTES = 256  # ready word at +0 of the flag block; free word at +128
+
+
+class _Ring:
+    """Device allocation: [slots * slot_bytes payload][flag block]."""
+
+    def __init__(self, slots: int, slot_bytes: int):
+        self.slots, self.slot_bytes = slots, slot_bytes
+        p = C.c_void_p()
+        _lib.call("smpk_p2p_alloc", slots * slot_bytes + FLAG_BYTES, C.byref(p))
+        self.base = p.value
+        self.flags = self.base + slots * slot_bytes
+
+    def handle(self) -> bytes:
+        buf = C.create_string_buffer(64)
+        _lib.call("smpk_p2p_export", self.base, buf)
+        return buf.raw
+
+    def free(self):
+        if self.base:
+            _lib.call("smpk_p2p_free", self.base)
+            self.base = None
+
+
+class StageChannel:
+    """Directed D2D channel src_rank -> dst_rank with a ring of `slots` persistent buffers.
+
+    Both ranks construct it (collectively over the PP group); the producer calls
+    ``send(t)``, the consumer ``recv(out)``, each on its current stream, in the same
+    order.  Flow control and completion are stream-ordered sequence words."""
+
+    def __init__(self, src: int, dst: int, slot_bytes: int, slots: int = 4, group=None):
+        self.src, self.dst, self.slots, self.slot_bytes = src, dst, slots, slot_bytes
+        self.rank = dist.get_rank() if dist.is_initialized() else 0
+        self.seq = 0
+        if self.rank not in (src, dst):
+            raise ValueError("StageChannel must be built by its two endpoint ranks")
+        is_dst = self.rank == dst
+        # dst owns the receive ring (+ ready word); src owns only a flag block (free word)
+        self.local = _Ring(slots if is_dst else 0, slot_bytes)
+        gathered = [None] * dist.get_world_size(group)
+        dist.all_gather_object(gathered, (self.rank, self.local.handle()), group=group)
+        peer = [h for r, h in gathered if r == (src if is_dst else dst)]
+        if not peer:
+            raise RuntimeError("StageChannel: peer handle missing (both ranks must construct the channel)")
+        p = C.c_void_p()
+        _lib.call("smpk_p2p_import", C.create_string_buffer(peer[0], 64), C.byref(p))
+        self.peer_base = p.value
+        self.peer_flags = self.peer_base + (0 if is_dst else slots * slot_bytes)
+
+    @staticmethod
+    def _stream():
+        return torch.cuda.current_stream().cuda_stream
+
+    def send(self, t: torch.Tensor) -> None:
+        assert self.rank == self.src
+        t = t.contiguous()
+        nbytes = t.numel() * t.element_size()
+        if nbytes > self.slot_bytes:
+            raise ValueError(f"StageChannel payload {nbytes} B exceeds slot size {self.slot_bytes} B")
+        k = self.seq % self.slots
+        wait_free = self.seq - self.slots + 1 if self.seq >= self.slots else 0
+        _lib.call("smpk_p2p_send", self.peer_base + k * self.slot_bytes, t.data_ptr(), nbytes,
+                  self.peer_flags, self.local.flags + 128, wait_free, self.seq, self._stream())
+        self.seq += 1
+
+    def recv(self, out: torch.Tensor) -> torch.Tensor:
+        assert self.rank == self.dst
+        nbytes = out.numel() * out.element_size()
+        k = self.seq % self.slots
+        _lib.call("smpk_p2p_recv", out.data_ptr(), self.local.base + k * self.slot_bytes, nbytes,
+                  self.local.flags, self.peer_flags + 128, self.seq, self._stream())
+        self.seq += 1
+        return out
+
+    def close(self):
+        if getattr(self, "peer_base", None):
+            _lib.call("smpk_p2p_close", self.peer_base)
+            self.peer_base = None
+        self.local.free()
+
+
+# ---------------------------------------------------------------------------
+# SPMD pipeline engine over a chain of stages
+# ---------------------------------------------------------------------------
+
+class PipelineEngine:
+    """Runs one training step of a P-stage chain with M microbatches (one process per stage).
+
+    stage_module: this rank's module (a callable on [mb, s, H] activations); the first
+    stage receives its microbatch inputs, the last stage applies ``loss_fn``.  Activations
+    go forward and gradients backward over D2D StageChannels; the per-stage op order is
+    the recorded schedule of ``next_action`` (static_schedule)."""
+
+    def __init__(self, stage_module, *, pp_rank: int, pp_size: int, ranks: list, act_shape, dtype=torch.bfloat16,
+                 policy: SchedulePolicy, slots: int = 4, group=None):
+        self.mod, self.s, self.P, self.ranks = stage_module, pp_rank, pp_size, ranks
+        self.shape, self.dtype, self.policy = tuple(act_shape), dtype, policy
+        nbytes = int(torch.Size(act_shape).numel()) * torch.tensor([], dtype=dtype).element_size()
+        self.log, ops = static_schedule(policy, pp_size)
+        self.ops = ops[pp_rank]
+        self.fwd_in = self.fwd_out = self.bwd_in = self.bwd_out = None
+        # build channels pairwise in a fixed global order so every rank participates consistently
+        for s in range(pp_size - 1):
+            a, b = ranks[s], ranks[s + 1]
+            if self.s in (s, s + 1):
+                pg = group if group is not None else dist.new_group([a, b])
+            else:
+                dist.new_group([a, b])
+                continue
+            fwd = StageChannel(a, b, nbytes, slots, group=pg)
+            bwd = StageChannel(b, a, nbytes, slots, group=pg)
+            if self.s == s:
+                self.fwd_out, self.bwd_in = fwd, bwd
+            else:
+                self.fwd_in, self.bwd_out = fwd, bwd
+
+    def step(self, inputs=None, loss_fn=None):
+        """inputs: list of M microbatch tensors (stage 0); loss_fn(mb, y) -> scalar (last stage).
+        Returns the list of per-microbatch losses on the last stage (None elsewhere)."""
+        saved, losses = {}, {}
+        dev = torch.device("cuda", torch.cuda.current_device())
+        for mb, d in self.ops:
+            if d == FWD:
+                if self.s == 0:
+                    x = inputs[mb]
+                else:
+                    x = self.fwd_in.recv(torch.empty(self.shape, dtype=self.dtype, device=dev)).requires_grad_(True)
+                y = self.mod(x)
+                saved[mb] = (x, y)
+                if self.s == self.P - 1:
+                    losses[mb] = loss_fn(mb, y)
+                else:
+                    self.fwd_out.send(y.detach())
+            else:
+                x, y = saved.pop(mb)
+                if self.s == self.P - 1:
+                    losses[mb].backward()
+                else:
+                    g = self.bwd_in.recv(torch.empty(self.shape, dtype=self.dtype, device=dev))
+                    torch.autograd.backward(y, g)
+                if self.s > 0:
+                    self.bwd_out.send(x.grad)
+        if self.s == self.P - 1:
+            return [losses[m] for m in range(self.policy.microbatches)]
+        return None
