@@ -7,7 +7,7 @@ without the reference on the box:
   * optimal consecutive segmentation, earliest-split tie-break (partition.py:34-75),
   * global-divisor D'Hondt apportionment (partition.py:78-99),
   * recursive device-set splitting and BFS tree partition (partition.py:102-178).
-tests/test_pipeline_planning.py checks every function bit-exactly against golden
+tests/test_planning_golden.py checks every function bit-exactly against golden
 vectors produced by the reference itself (tests/golden/make_golden.py).
 """
 from __future__ import annotations
@@ -261,3 +261,14 @@ def partition_tree(spec: ModelTree, degree: int, alpha: float = 0.5):
                 dsets[k] = (devs[0],)
     module_rank = {m: part[nid] for nid, n in nodes.items() for m in n.module_ids}
     return part, dsets, module_rank
+
+
+def partition_loads(spec: ModelTree, degree: int, alpha: float = 0.5) -> list:
+    """Per-partition total local cost (c(n) minus the children's share); sums to 1."""
+    nodes, root = build_nodes(spec)
+    c = node_costs(spec, nodes, root, alpha)
+    part, _, _ = partition_tree(spec, degree, alpha)
+    loads = [0.0] * degree
+    for nid, n in nodes.items():
+        loads[part[nid]] += c[nid] - sum(c[k] for k in n.children)
+    return loads
