@@ -22,3 +22,6 @@ from .errors import (IndexOutOfRangeError, NotDivisibleError, ShapeMismatchError
 from .state import (STATE, dp_rank, init, pp_rank, pp_size, rank, rdp_rank, reset, size, tp_rank,  # noqa: E402
                     tp_size)
 from .topology import Topology, build_topology  # noqa: E402
+from .replace import (DistributedModel, plan_replacement, set_tensor_parallelism, tensor_parallelism,  # noqa: E402
+                      tp_register, tp_register_with_module)
+from . import pipeline  # noqa: E402,F401
