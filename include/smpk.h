@@ -184,6 +184,20 @@ SMPK_API int smpk_vocab_ce_bwd(const void* logits, int64_t ld, int64_t N, int v_
                                void* stream);
 
 /*
+ * smpk_flash_attn_fwd — fused attention of one TP rank's local heads ("per-rank
+ * scaled dot-product attention with softmax over masked scores"), on the
+ * packed QKV buffer produced by the column-parallel QKV GEMM:
+ *   qkv [B*s, ld] with q | k | v blocks of nh*dh columns, head h at column h*dh of each block;
+ *   out [B*s, ld_out] (head h at column h*dh) = dropout(softmax(scale*QK^T + mask [+causal])) V;
+ *   lse [B, nh, s] = log2-sum-exp2 of the scaled masked scores (for the backward).
+ * dh in {64, 128}; s a multiple of 128; dropout bits identical to smpk_softmax_fwd.
+ */
+SMPK_API int smpk_flash_attn_fwd(const void* qkv, int64_t ld, int B, int nh, int s, int dh, void* out,
+                                 int64_t ld_out, float* lse, const float* mask_add, float scale, int causal,
+                                 float p_drop, uint64_t seed, int layer, int64_t sample_offset, int head_offset,
+                                 int nh_global, void* stream);
+
+/*
  * Pipeline stage send/recv over NVLink peer memory — the D2D communicator of the
  * module server; replaces the simulated hop
  * mpsim pipeline.py:653-712 (_transfer / _send_request / _send_response) whose routing

@@ -366,31 +366,35 @@ static PFN_encodeTiled_t get_encode_fn() {
   return fn;
 }
 
-// Operand view: rows x K logical, either K-major (K contiguous) or MN-major.
-static int make_operand_map(CUtensorMap* map, const void* ptr, bool mn_major, int rows, int K, int64_t ld,
-                            int nb1, int64_t s1, int nb2, int64_t s2, int box_rows, const char* name) {
+// 4-D bf16 tensor map {inner, outer, nb1, nb2} with SWIZZLE_128B boxes {box_inner, box_outer, 1, 1}.
+int make_tma_4d(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t ld, int nb1, int64_t s1,
+                int nb2, int64_t s2, int box_inner, int box_outer, const char* name) {
   PFN_encodeTiled_t enc = get_encode_fn();
-  SMPK_REQUIRE(enc != nullptr, SMPK_ERR_CUDA, "smpk_gemm: cuTensorMapEncodeTiled unavailable");
+  SMPK_REQUIRE(enc != nullptr, SMPK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   SMPK_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0, SMPK_ERR_BAD_ARG,
-               "smpk_gemm: operand %s must be 16-byte aligned", name);
-  SMPK_REQUIRE(ld % 8 == 0, SMPK_ERR_BAD_ARG, "smpk_gemm: leading dim of %s (%lld) must be a multiple of 8",
-               name, (long long)ld);
+               "operand %s must be 16-byte aligned", name);
+  SMPK_REQUIRE(ld % 8 == 0, SMPK_ERR_BAD_ARG, "leading dim of %s (%lld) must be a multiple of 8", name,
+               (long long)ld);
   SMPK_REQUIRE((nb1 == 1 || s1 % 8 == 0) && (nb2 == 1 || s2 % 8 == 0), SMPK_ERR_BAD_ARG,
-               "smpk_gemm: batch strides of %s must be multiples of 8", name);
-  const int64_t inner = mn_major ? rows : K;
-  const int64_t outer = mn_major ? K : rows;
+               "batch strides of %s must be multiples of 8", name);
   cuuint64_t dims[4] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)nb1, (cuuint64_t)nb2};
   const int64_t fallback = ld * outer * 2;
   cuuint64_t strides[3] = {(cuuint64_t)(ld * 2), (cuuint64_t)(nb1 > 1 ? s1 * 2 : fallback),
                            (cuuint64_t)(nb2 > 1 ? s2 * 2 : fallback)};
-  cuuint32_t box[4] = {64u, (cuuint32_t)(mn_major ? BK : box_rows), 1u, 1u};
+  cuuint32_t box[4] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer, 1u, 1u};
   cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  SMPK_REQUIRE(r == CUDA_SUCCESS, SMPK_ERR_CUDA, "smpk_gemm: tensor map for %s failed (CUresult %d)", name,
-               (int)r);
+  SMPK_REQUIRE(r == CUDA_SUCCESS, SMPK_ERR_CUDA, "tensor map for %s failed (CUresult %d)", name, (int)r);
   return SMPK_OK;
+}
+
+// Operand view: rows x K logical, either K-major (K contiguous) or MN-major.
+static int make_operand_map(CUtensorMap* map, const void* ptr, bool mn_major, int rows, int K, int64_t ld,
+                            int nb1, int64_t s1, int nb2, int64_t s2, int box_rows, const char* name) {
+  return make_tma_4d(map, ptr, mn_major ? rows : K, mn_major ? K : rows, ld, nb1, s1, nb2, s2, 64,
+                     mn_major ? BK : box_rows, name);
 }
 
 template <int BN, int STAGES, int EPI, int ACT, bool F32OUT, bool BETA>

@@ -104,3 +104,19 @@ def colsum(x: torch.Tensor, *, out_dtype=None) -> torch.Tensor:
     _lib.call("smpk_colsum", _ptr(x), M, N, x.stride(0), _ptr(out), int(out.dtype == torch.float32), 0, _ptr(ws),
               int(ws_bytes), _stream())
     return out
+
+
+def flash_attn_fwd(qkv: torch.Tensor, B: int, s: int, nh: int, dh: int, *, mask_add=None, causal=False, p=0.0,
+                   seed=0, layer=0, sample_offset=0, head_offset=0, nh_global=None, out=None):
+    """Fused attention on the packed QKV buffer [B*s, 3*nh*dh] (q | k | v blocks, heads inside each).
+    Returns (ctx [B*s, nh*dh] bf16, lse [B, nh, s] fp32 log2-domain)."""
+    _check_cuda(qkv, mask_add)
+    ctx = out if out is not None else torch.empty(B * s, nh * dh, dtype=qkv.dtype, device=qkv.device)
+    lse = torch.empty(B, nh, s, dtype=torch.float32, device=qkv.device)
+    if mask_add is not None:
+        mask_add = mask_add.reshape(B, s).to(torch.float32).contiguous()
+    _lib.call("smpk_flash_attn_fwd", _ptr(qkv), qkv.stride(0), B, nh, s, dh, _ptr(ctx), ctx.stride(0), _ptr(lse),
+              _ptr(mask_add), float(1.0 / dh ** 0.5), int(bool(causal)), float(p), int(seed) & (2 ** 64 - 1),
+              int(layer), int(sample_offset), int(head_offset), int(nh_global if nh_global is not None else nh),
+              _stream())
+    return ctx, lse

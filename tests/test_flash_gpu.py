@@ -1,0 +1,71 @@
+"""Fused (flash) attention on tcgen05 vs the fp64 oracle attention core, same bf16 inputs,
+same Philox dropout masks (oracle/philox.py)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import philox, tp
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a, b = a.double().cpu(), b.double().cpu()
+    return ((a - b).norm() / max(b.norm().item(), 1e-30)).item()
+
+
+CASES = [
+    # B, nh, s, dh, causal, masked, p
+    (2, 4, 256, 64, False, False, 0.0),
+    (2, 4, 512, 64, False, True, 0.0),
+    (2, 2, 384, 64, True, False, 0.0),
+    (1, 2, 256, 128, True, False, 0.0),
+    (2, 3, 256, 128, False, True, 0.0),
+    (2, 4, 256, 64, False, True, 0.1),
+    (1, 2, 512, 128, True, False, 0.1),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[str(c) for c in CASES])
+def test_flash_fwd_vs_oracle(case):
+    from paper_2111_05972_b200 import ops
+    B, nh, s, dh, causal, masked, p = case
+    g = torch.Generator().manual_seed(s + dh)
+    H = nh * dh
+    qkv = (torch.randn(B * s, 3 * H, generator=g)).to(torch.bfloat16)
+    mask = None
+    if masked:
+        mask = torch.zeros(B, s)
+        mask[0, -37:] = -10000.0
+        mask[-1, :5] = -10000.0
+    seed, layer, soff, hoff, nhg = 77, 3, 5, 2, nh + 4
+    ctx, lse = ops.flash_attn_fwd(qkv.cuda(), B, s, nh, dh, mask_add=None if mask is None else mask.cuda(),
+                                  causal=causal, p=p, seed=seed, layer=layer, sample_offset=soff, head_offset=hoff,
+                                  nh_global=nhg)
+    q, k, v = qkv.double().split(H, -1)
+    ref = tp.attention_core(q.reshape(B, s, nh, dh), k.reshape(B, s, nh, dh), v.reshape(B, s, nh, dh),
+                            None if mask is None else mask.double(), causal,
+                            tp.DropoutCtx(seed=seed, layer=layer, sample_offset=soff) if p > 0 else None, p, hoff, nhg)
+    assert rel(ctx.reshape(B, s, H), ref) < 1e-2
+    # log-sum-exp (log2 domain) of the scaled masked scores
+    sc = tp.attention_scores_mask((q.reshape(B, s, nh, dh).permute(0, 2, 1, 3) @
+                                   k.reshape(B, s, nh, dh).permute(0, 2, 3, 1)) / math.sqrt(dh),
+                                  None if mask is None else mask.double(), causal)
+    lse_ref = torch.logsumexp(sc, -1) / math.log(2.0)
+    assert (lse.cpu().double() - lse_ref).abs().max().item() < 2e-2
+
+
+def test_flash_matches_materialized_path():
+    """The fused kernel and the GEMM + softmax + GEMM path give the same context."""
+    from paper_2111_05972_b200 import layers as Lm
+    from paper_2111_05972_b200 import ops
+    B, nh, s, dh = 2, 4, 512, 64
+    qkv = torch.randn(B * s, 3 * nh * dh, device="cuda").bfloat16()
+    m = Lm.LayerMeta(hidden=nh * dh, heads_local=nh, heads_global=nh, head_dim=dh, eps=1e-5, p_attn=0.1,
+                     p_hidden=0.0, causal=False, pre_ln=False, post_ln=True, activation="gelu", layer_id=4, seed=9,
+                     head_offset=0, sample_offset=0, tp_size=1)
+    ctx_ref, _, _ = Lm.attn_core_fwd(qkv, B, s, m, None)
+    ctx, _ = ops.flash_attn_fwd(qkv, B, s, nh, dh, p=0.1, seed=9, layer=4)
+    assert rel(ctx, ctx_ref) < 1e-2
