@@ -198,6 +198,19 @@ SMPK_API int smpk_flash_attn_fwd(const void* qkv, int64_t ld, int B, int nh, int
                                  int nh_global, void* stream);
 
 /*
+ * smpk_flash_attn_bwd — backward of smpk_flash_attn_fwd: from dout (grad of out, same layout),
+ * the forward's out and lse, writes dQ | dK | dV into dqkv (same layout as qkv).  P is
+ * recomputed from lse (never stored); dQ partials of the key tiles are reduced in order
+ * (deterministic).  workspace >= smpk_flash_attn_bwd_workspace(B, nh, s, dh) bytes.
+ */
+SMPK_API int64_t smpk_flash_attn_bwd_workspace(int B, int nh, int s, int dh);
+SMPK_API int smpk_flash_attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const void* dout,
+                                 int64_t ld_dout, const float* lse, int B, int nh, int s, int dh, void* dqkv,
+                                 const float* mask_add, float scale, int causal, float p_drop, uint64_t seed,
+                                 int layer, int64_t sample_offset, int head_offset, int nh_global, void* workspace,
+                                 int64_t workspace_bytes, void* stream);
+
+/*
  * Pipeline stage send/recv over NVLink peer memory — the D2D communicator of the
  * module server; replaces the simulated hop
  * mpsim pipeline.py:653-712 (_transfer / _send_request / _send_response) whose routing

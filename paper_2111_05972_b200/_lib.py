@@ -38,6 +38,7 @@ SIGNATURES: dict[str, list] = {
     "smpk_vocab_ce_combine": [P, I, L, P, L, P, P, P],
     "smpk_vocab_ce_bwd": [P, L, L, I, L, L, P, L, P, P, F, P, L, P],
     "smpk_flash_attn_fwd": [P, L, I, I, I, I, P, L, P, P, F, I, F, C.c_uint64, I, L, I, I, P],
+    "smpk_flash_attn_bwd": [P, L, P, L, P, L, P, I, I, I, I, P, P, F, I, F, C.c_uint64, I, L, I, I, P, L, P],
     "smpk_p2p_alloc": [L, C.POINTER(P)],
     "smpk_p2p_free": [P],
     "smpk_p2p_export": [P, P],
@@ -51,6 +52,7 @@ SIGNATURES: dict[str, list] = {
 SIZE_FUNCS: dict[str, list] = {
     "smpk_ln_bwd_workspace": [I, I],
     "smpk_colsum_workspace": [I, I],
+    "smpk_flash_attn_bwd_workspace": [I, I, I, I],
 }
 
 

@@ -106,6 +106,24 @@ def colsum(x: torch.Tensor, *, out_dtype=None) -> torch.Tensor:
     return out
 
 
+def flash_attn_bwd(dctx: torch.Tensor, qkv: torch.Tensor, ctx: torch.Tensor, lse: torch.Tensor, B: int, s: int,
+                   nh: int, dh: int, *, mask_add=None, causal=False, p=0.0, seed=0, layer=0, sample_offset=0,
+                   head_offset=0, nh_global=None, dqkv=None):
+    """Backward of flash_attn_fwd: returns dqkv [B*s, 3*nh*dh] (dQ | dK | dV blocks)."""
+    _check_cuda(dctx, qkv, ctx, lse, mask_add)
+    dctx = dctx.contiguous()
+    dqkv = dqkv if dqkv is not None else torch.empty_like(qkv)
+    if mask_add is not None:
+        mask_add = mask_add.reshape(B, s).to(torch.float32).contiguous()
+    ws_bytes = _lib.size("smpk_flash_attn_bwd_workspace", B, nh, s, dh)
+    ws = torch.empty(ws_bytes // 4, dtype=torch.float32, device=qkv.device)
+    _lib.call("smpk_flash_attn_bwd", _ptr(qkv), qkv.stride(0), _ptr(ctx), ctx.stride(0), _ptr(dctx), dctx.stride(0),
+              _ptr(lse), B, nh, s, dh, _ptr(dqkv), _ptr(mask_add), float(1.0 / dh ** 0.5), int(bool(causal)),
+              float(p), int(seed) & (2 ** 64 - 1), int(layer), int(sample_offset), int(head_offset),
+              int(nh_global if nh_global is not None else nh), _ptr(ws), int(ws_bytes), _stream())
+    return dqkv
+
+
 def flash_attn_fwd(qkv: torch.Tensor, B: int, s: int, nh: int, dh: int, *, mask_add=None, causal=False, p=0.0,
                    seed=0, layer=0, sample_offset=0, head_offset=0, nh_global=None, out=None):
     """Fused attention on the packed QKV buffer [B*s, 3*nh*dh] (q | k | v blocks, heads inside each).

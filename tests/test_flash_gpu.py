@@ -57,6 +57,35 @@ def test_flash_fwd_vs_oracle(case):
     assert (lse.cpu().double() - lse_ref).abs().max().item() < 2e-2
 
 
+@pytest.mark.parametrize("case", CASES, ids=[str(c) for c in CASES])
+def test_flash_bwd_vs_oracle(case):
+    from paper_2111_05972_b200 import ops
+    B, nh, s, dh, causal, masked, p = case
+    g = torch.Generator().manual_seed(2 * s + dh)
+    H = nh * dh
+    qkv = torch.randn(B * s, 3 * H, generator=g).to(torch.bfloat16)
+    dctx = torch.randn(B * s, H, generator=g).to(torch.bfloat16)
+    mask = None
+    if masked:
+        mask = torch.zeros(B, s)
+        mask[0, -37:] = -10000.0
+    seed, layer, soff, hoff, nhg = 31, 1, 2, 1, nh + 2
+    kw = dict(mask_add=None if mask is None else mask.cuda(), causal=causal, p=p, seed=seed, layer=layer,
+              sample_offset=soff, head_offset=hoff, nh_global=nhg)
+    ctx, lse = ops.flash_attn_fwd(qkv.cuda(), B, s, nh, dh, **kw)
+    dqkv = ops.flash_attn_bwd(dctx.cuda(), qkv.cuda(), ctx, lse, B, s, nh, dh, **kw)
+    x = qkv.double().requires_grad_(True)
+    q, k, v = x.split(H, -1)
+    ref = tp.attention_core(q.reshape(B, s, nh, dh), k.reshape(B, s, nh, dh), v.reshape(B, s, nh, dh),
+                            None if mask is None else mask.double(), causal,
+                            tp.DropoutCtx(seed=seed, layer=layer, sample_offset=soff) if p > 0 else None, p, hoff, nhg)
+    ref.backward(dctx.double().reshape(B, s, H))
+    gq, gk, gv = x.grad.split(H, -1)
+    dq, dk, dv = dqkv.cpu().split(H, -1)
+    errs = {"dq": rel(dq, gq), "dk": rel(dk, gk), "dv": rel(dv, gv)}
+    assert all(e < 2e-2 for e in errs.values()), errs
+
+
 def test_flash_matches_materialized_path():
     """The fused kernel and the GEMM + softmax + GEMM path give the same context."""
     from paper_2111_05972_b200 import layers as Lm
