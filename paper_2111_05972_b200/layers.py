@@ -128,6 +128,16 @@ def attn_core_bwd(dctx: torch.Tensor, qkv: torch.Tensor, P, Pd, B: int, s: int, 
     return dqkv
 
 
+FLASH = {"enabled": True, "min_seq": 1024}
+
+
+def use_flash(s: int, head_dim: int) -> bool:
+    """Fused tcgen05 attention (csrc/flash_attn*.cu) for long sequences; the materialised path
+    (tcgen05 batched GEMMs + fused softmax kernels) is as fast at s <= 512 in this build
+    (scripts/attn_bench.py) and keeps the [s, s] tiles L2-resident there."""
+    return FLASH["enabled"] and s % 128 == 0 and head_dim in (64, 128) and s >= FLASH["min_seq"]
+
+
 def _ln_in(x2, w, b, m: LayerMeta):
     y, mean, rstd = ops.layer_norm(x2, w, b, m.eps)
     return y, mean, rstd
@@ -155,15 +165,22 @@ class AttentionFn(torch.autograd.Function):
         else:
             h, mu1, rs1 = x2, None, None
         qkv = K.linear(h, wqkv, bqkv)
-        ctxv, P, Pd = attn_core_fwd(qkv, B, s, m, mask_add)
+        fused = use_flash(s, m.head_dim)
+        if fused:
+            ctxv, lse = ops.flash_attn_fwd(qkv, B, s, m.heads_local, m.head_dim, mask_add=mask_add, causal=m.causal,
+                                           p=m.p_attn, seed=m.seed, layer=m.layer_id, sample_offset=m.sample_offset,
+                                           head_offset=m.head_offset, nh_global=m.heads_global)
+            P, Pd = lse, None
+        else:
+            ctxv, P, Pd = attn_core_fwd(qkv, B, s, m, mask_add)
         o = K.linear(ctxv, wo)
         C.all_reduce(o)
         r, y, mu2, rs2 = ops.bdr_ln(o, bias=bo, residual=x2, gamma=post_w if m.post_ln else None,
                                     beta=post_b if m.post_ln else None, eps=m.eps, p=m.p_hidden, seed=m.seed,
                                     layer=m.layer_id, site=SITE_ATTN_OUT, row_offset=m.sample_offset * s)
-        ctx.m, ctx.shape = m, (B, s, H)
+        ctx.m, ctx.shape, ctx.fused = m, (B, s, H), fused
         ctx.save_for_backward(x2, h, mu1, rs1, qkv, P, Pd if Pd is not P else None, ctxv, r, mu2, rs2, wqkv, wo,
-                              pre_w, post_w)
+                              pre_w, post_w, mask_add)
         out = y if m.post_ln else r
         return out.view(B, s, H)
 
@@ -171,7 +188,7 @@ class AttentionFn(torch.autograd.Function):
     def backward(ctx, dy):
         m: LayerMeta = ctx.m
         B, s, H = ctx.shape
-        x2, h, mu1, rs1, qkv, P, Pd, ctxv, r, mu2, rs2, wqkv, wo, pre_w, post_w = ctx.saved_tensors
+        x2, h, mu1, rs1, qkv, P, Pd, ctxv, r, mu2, rs2, wqkv, wo, pre_w, post_w, mask_add = ctx.saved_tensors
         if Pd is None:
             Pd = P
         dy2 = dy.reshape(B * s, H).contiguous()
@@ -183,7 +200,13 @@ class AttentionFn(torch.autograd.Function):
             dr = dy2
         dwo = K.matmul_tn(do, ctxv)
         dctx = K.matmul_nn(do, wo)
-        dqkv = attn_core_bwd(dctx, qkv, P, Pd, B, s, m)
+        if ctx.fused:
+            dqkv = ops.flash_attn_bwd(dctx, qkv, ctxv, P, B, s, m.heads_local, m.head_dim, mask_add=mask_add,
+                                      causal=m.causal, p=m.p_attn, seed=m.seed, layer=m.layer_id,
+                                      sample_offset=m.sample_offset, head_offset=m.head_offset,
+                                      nh_global=m.heads_global)
+        else:
+            dqkv = attn_core_bwd(dctx, qkv, P, Pd, B, s, m)
         dwqkv = K.matmul_tn(dqkv, h)
         dbqkv = ops.colsum(dqkv)
         if m.tp_size == 1 and not m.pre_ln:

@@ -37,9 +37,20 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("flash", [True, False], ids=["flash", "materialized"])
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
-def test_layer_fwd_bwd_vs_oracle(smp_single, case):
+def test_layer_fwd_bwd_vs_oracle(smp_single, case, flash):
     smp = smp_single
+    from paper_2111_05972_b200 import layers
+    saved = dict(layers.FLASH)
+    layers.FLASH.update(enabled=flash, min_seq=0)
+    try:
+        _run_case(smp, case)
+    finally:
+        layers.FLASH.update(saved)
+
+
+def _run_case(smp, case):
     name, nh, dh, H, I, s, B, causal, pre, post, act, p = case
     cfg = tp.LayerConfig(num_attention_heads=nh, attention_head_size=dh, hidden_size=H, intermediate_size=I,
                          attention_dropout_prob=p, hidden_dropout_prob=p, activation=act,
