@@ -238,11 +238,14 @@ class DistributedEmbedding(nn.Module):
 
 
 class _LMHeadFn(torch.autograd.Function):
-    """logits_j = h @ E_j^T on the replicated hidden state; backward: dh AR (bwd_allreduce), dE_j."""
+    """logits_j = h @ E_j^T on the TP-replicated hidden state; backward: dE_j, and dh summed
+    over the vocab shards (allreduce = bwd_allreduce_for_tp), unless the caller's allgather
+    already reduces it (its backward is a reduce-scatter)."""
 
     @staticmethod
-    def forward(ctx, h, E):
+    def forward(ctx, h, E, reduce_grad):
         ctx.save_for_backward(h, E)
+        ctx.reduce_grad = reduce_grad
         return K.matmul_nt(h, E)
 
     @staticmethod
@@ -250,11 +253,12 @@ class _LMHeadFn(torch.autograd.Function):
         h, E = ctx.saved_tensors
         dl = dl.contiguous()
         dh = K.matmul_nn(dl, E)
-        C.all_reduce(dh)
+        if ctx.reduce_grad:
+            C.all_reduce(dh)
         dE = K.matmul_tn(dl, h)
-        return dh, dE
+        return dh, dE, None
 
 
-def lm_head_logits(h: torch.Tensor, E_local: torch.Tensor) -> torch.Tensor:
+def lm_head_logits(h: torch.Tensor, E_local: torch.Tensor, reduce_grad: bool = True) -> torch.Tensor:
     """Vocab-sharded logits of the tied LM head: [N, H] x [Vp/T, H]^T -> [N, Vp/T]."""
-    return _LMHeadFn.apply(h.reshape(-1, h.shape[-1]).contiguous(), E_local)
+    return _LMHeadFn.apply(h.reshape(-1, h.shape[-1]).contiguous(), E_local, reduce_grad)

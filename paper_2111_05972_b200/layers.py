@@ -11,8 +11,9 @@ Per-rank dataflow:
   attention: [pre-LN] -> QKV_j (+b) -> per local head softmax(QK^T/sqrt(dh) + mask)
              -> dropout -> .V -> ctx_j @ Wo_j^T -> AR -> +bo -> dropout -> +x -> [post-LN]
   mlp:       [pre-LN] -> FC1_j (+b, act) -> FC2_j -> AR -> +b2 -> dropout -> +x -> [post-LN]
-The input x is the TP-group-replicated activation [B, s, H]; weights are the
-rank's shards in the Megatron layout (oracle/tp.py shard_layer_params_speed).
+Between sub-layers the activation is either TP-replicated (prescaled batch, AR) or
+row-sharded by owning rank (TP across DP: AG in, RS out); weights are the rank's
+shards in the Megatron layout (oracle/tp.py shard_layer_params_speed).
 """
 from __future__ import annotations
 
@@ -43,8 +44,10 @@ class LayerMeta:
     layer_id: int
     seed: int
     head_offset: int
-    sample_offset: int  # global id of the first sample of x (dropout coordinates)
+    sample_offset: int  # global id of the first sample the attention sees (gathered batch)
     tp_size: int
+    row_offset: int = 0  # global token row of this rank's first activation row (hidden dropout)
+    shard_rows: bool = False  # activations row-sharded between sub-layers (AG in / RS out)
 
 
 class LinearFn(torch.autograd.Function):
@@ -151,6 +154,46 @@ def _residual_bwd_out(dh: torch.Tensor, dr: torch.Tensor | None, x2, ln_w, mean,
     return ops.add(dh, dr), None, None
 
 
+# Row-sharded activations (TP across DP ranks, the default for tp_size > 1): every rank keeps
+# the rows of ITS OWN samples between sub-layers ([b*s, H]); the column-parallel GEMM input is
+# allgathered over the TP group and the row-parallel partial sums are reduce-scattered back
+# to the owning rank (AG + RS = the paper's allreduce, same bytes).  Bias / dropout / residual /
+# LayerNorm then run once per row instead of T times, and the stack needs no entry gather or exit
+# slice ("returns the combined data samples to their respective GPUs").
+# Replicated parameters (LayerNorms, row-parallel biases) see only their rank's rows, so their
+# gradients are allreduced once per sub-layer (one flat bucket).
+
+def _gather_rows(t, m: LayerMeta):
+    return C.all_gather(t.contiguous(), 0) if m.shard_rows else t
+
+
+def _combine_rows(partial, m: LayerMeta):
+    """Row-parallel partial sums -> own rows (RS) or replicated rows (AR)."""
+    if m.shard_rows:
+        return C.reduce_scatter(partial, 0)
+    return C.all_reduce(partial)
+
+
+def _sync_replicated(grads, m: LayerMeta):
+    """Allreduce the partial gradients of TP-replicated parameters in one bucket (row-sharded mode)."""
+    if not m.shard_rows:
+        return grads
+    live = [g for g in grads if g is not None]
+    if not live:
+        return grads
+    flat = torch.cat([g.float().reshape(-1) for g in live])
+    C.all_reduce(flat)
+    out, off = [], 0
+    for g in grads:
+        if g is None:
+            out.append(None)
+            continue
+        n = g.numel()
+        out.append(flat[off:off + n].view_as(g).to(g.dtype))
+        off += n
+    return out
+
+
 # ---------------------------------------------------------------------------
 # attention sub-layer
 # ---------------------------------------------------------------------------
@@ -158,13 +201,15 @@ def _residual_bwd_out(dh: torch.Tensor, dr: torch.Tensor | None, x2, ln_w, mean,
 class AttentionFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, wqkv, bqkv, wo, bo, pre_w, pre_b, post_w, post_b, mask_add, m: LayerMeta):
-        B, s, H = x.shape
-        x2 = x.reshape(B * s, H)
+        b, s, H = x.shape
+        x2 = x.reshape(b * s, H)
         if m.pre_ln:
             h, mu1, rs1 = _ln_in(x2, pre_w, pre_b, m)
         else:
             h, mu1, rs1 = x2, None, None
-        qkv = K.linear(h, wqkv, bqkv)
+        hf = _gather_rows(h, m)  # [B*s, H], B = T*b when row-sharded
+        B = hf.shape[0] // s
+        qkv = K.linear(hf, wqkv, bqkv)
         fused = use_flash(s, m.head_dim)
         if fused:
             ctxv, lse = ops.flash_attn_fwd(qkv, B, s, m.heads_local, m.head_dim, mask_add=mask_add, causal=m.causal,
@@ -173,33 +218,35 @@ class AttentionFn(torch.autograd.Function):
             P, Pd = lse, None
         else:
             ctxv, P, Pd = attn_core_fwd(qkv, B, s, m, mask_add)
-        o = K.linear(ctxv, wo)
-        C.all_reduce(o)
+        o = _combine_rows(K.linear(ctxv, wo), m)  # own rows (RS) or replicated (AR)
         r, y, mu2, rs2 = ops.bdr_ln(o, bias=bo, residual=x2, gamma=post_w if m.post_ln else None,
                                     beta=post_b if m.post_ln else None, eps=m.eps, p=m.p_hidden, seed=m.seed,
-                                    layer=m.layer_id, site=SITE_ATTN_OUT, row_offset=m.sample_offset * s)
-        ctx.m, ctx.shape, ctx.fused = m, (B, s, H), fused
-        ctx.save_for_backward(x2, h, mu1, rs1, qkv, P, Pd if Pd is not P else None, ctxv, r, mu2, rs2, wqkv, wo,
+                                    layer=m.layer_id, site=SITE_ATTN_OUT, row_offset=m.row_offset)
+        ctx.m, ctx.shape, ctx.fused, ctx.B = m, (b, s, H), fused, B
+        ctx.save_for_backward(x2, hf, mu1, rs1, qkv, P, Pd if Pd is not P else None, ctxv, r, mu2, rs2, wqkv, wo,
                               pre_w, post_w, mask_add)
         out = y if m.post_ln else r
-        return out.view(B, s, H)
+        return out.view(b, s, H)
 
     @staticmethod
     def backward(ctx, dy):
         m: LayerMeta = ctx.m
-        B, s, H = ctx.shape
-        x2, h, mu1, rs1, qkv, P, Pd, ctxv, r, mu2, rs2, wqkv, wo, pre_w, post_w, mask_add = ctx.saved_tensors
+        b, s, H = ctx.shape
+        B = ctx.B
+        x2, hf, mu1, rs1, qkv, P, Pd, ctxv, r, mu2, rs2, wqkv, wo, pre_w, post_w, mask_add = ctx.saved_tensors
         if Pd is None:
             Pd = P
-        dy2 = dy.reshape(B * s, H).contiguous()
-        # residual / post-LN / hidden dropout backward; dbo = colsum(do)
-        dr, do, dpost_w, dpost_b, dbo = ops.ln_bwd(dy2, r, mu2, rs2, post_w if m.post_ln else None, p=m.p_hidden,
-                                                   seed=m.seed, layer=m.layer_id, site=SITE_ATTN_OUT,
-                                                   row_offset=m.sample_offset * s, want_dr=m.post_ln)
+        dy2 = dy.reshape(b * s, H).contiguous()
+        # residual / post-LN / hidden dropout backward (own rows)
+        dr, do, dpost_w, dpost_b, _ = ops.ln_bwd(dy2, r, mu2, rs2, post_w if m.post_ln else None, p=m.p_hidden,
+                                                 seed=m.seed, layer=m.layer_id, site=SITE_ATTN_OUT,
+                                                 row_offset=m.row_offset, want_dr=m.post_ln, want_dbias=False)
         if not m.post_ln:
             dr = dy2
-        dwo = K.matmul_tn(do, ctxv)
-        dctx = K.matmul_nn(do, wo)
+        dof = _gather_rows(do, m)
+        dbo = ops.colsum(dof)  # over all rows of the group: complete on every rank
+        dwo = K.matmul_tn(dof, ctxv)
+        dctx = K.matmul_nn(dof, wo)
         if ctx.fused:
             dqkv = ops.flash_attn_bwd(dctx, qkv, ctxv, P, B, s, m.heads_local, m.head_dim, mask_add=mask_add,
                                       causal=m.causal, p=m.p_attn, seed=m.seed, layer=m.layer_id,
@@ -207,16 +254,16 @@ class AttentionFn(torch.autograd.Function):
                                       nh_global=m.heads_global)
         else:
             dqkv = attn_core_bwd(dctx, qkv, P, Pd, B, s, m)
-        dwqkv = K.matmul_tn(dqkv, h)
+        dwqkv = K.matmul_tn(dqkv, hf)
         dbqkv = ops.colsum(dqkv)
         if m.tp_size == 1 and not m.pre_ln:
             dx = K.matmul_nn(dqkv, wqkv, epi=K.EPI_ADD, aux=dr)
             dpre_w = dpre_b = None
         else:
-            dh = K.matmul_nn(dqkv, wqkv)
-            C.all_reduce(dh)
+            dh = _combine_rows(K.matmul_nn(dqkv, wqkv), m)
             dx, dpre_w, dpre_b = _residual_bwd_out(dh, dr, x2, pre_w, mu1, rs1, m)
-        return (dx.view(B, s, H), dwqkv, dbqkv, dwo, dbo, dpre_w, dpre_b, dpost_w, dpost_b, None, None)
+        dpost_w, dpost_b, dpre_w, dpre_b = _sync_replicated([dpost_w, dpost_b, dpre_w, dpre_b], m)
+        return (dx.view(b, s, H), dwqkv, dbqkv, dwo, dbo, dpre_w, dpre_b, dpost_w, dpost_b, None, None)
 
 
 # ---------------------------------------------------------------------------
@@ -226,43 +273,45 @@ class AttentionFn(torch.autograd.Function):
 class MlpFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w1, b1, w2, b2, pre_w, pre_b, post_w, post_b, m: LayerMeta):
-        B, s, H = x.shape
-        x2 = x.reshape(B * s, H)
+        b, s, H = x.shape
+        x2 = x.reshape(b * s, H)
         if m.pre_ln:
             h, mu1, rs1 = _ln_in(x2, pre_w, pre_b, m)
         else:
             h, mu1, rs1 = x2, None, None
-        f, z = K.linear(h, w1, b1, act=m.activation)
-        g = K.linear(f, w2)
-        C.all_reduce(g)
+        hf = _gather_rows(h, m)
+        f, z = K.linear(hf, w1, b1, act=m.activation)
+        g = _combine_rows(K.linear(f, w2), m)
         r, y, mu2, rs2 = ops.bdr_ln(g, bias=b2, residual=x2, gamma=post_w if m.post_ln else None,
                                     beta=post_b if m.post_ln else None, eps=m.eps, p=m.p_hidden, seed=m.seed,
-                                    layer=m.layer_id, site=SITE_MLP_OUT, row_offset=m.sample_offset * s)
-        ctx.m, ctx.shape = m, (B, s, H)
-        ctx.save_for_backward(x2, h, mu1, rs1, f, z, r, mu2, rs2, w1, w2, pre_w, post_w)
+                                    layer=m.layer_id, site=SITE_MLP_OUT, row_offset=m.row_offset)
+        ctx.m, ctx.shape = m, (b, s, H)
+        ctx.save_for_backward(x2, hf, mu1, rs1, f, z, r, mu2, rs2, w1, w2, pre_w, post_w)
         out = y if m.post_ln else r
-        return out.view(B, s, H)
+        return out.view(b, s, H)
 
     @staticmethod
     def backward(ctx, dy):
         m: LayerMeta = ctx.m
-        B, s, H = ctx.shape
-        x2, h, mu1, rs1, f, z, r, mu2, rs2, w1, w2, pre_w, post_w = ctx.saved_tensors
-        dy2 = dy.reshape(B * s, H).contiguous()
-        dr, dg, dpost_w, dpost_b, db2 = ops.ln_bwd(dy2, r, mu2, rs2, post_w if m.post_ln else None, p=m.p_hidden,
-                                                   seed=m.seed, layer=m.layer_id, site=SITE_MLP_OUT,
-                                                   row_offset=m.sample_offset * s, want_dr=m.post_ln)
+        b, s, H = ctx.shape
+        x2, hf, mu1, rs1, f, z, r, mu2, rs2, w1, w2, pre_w, post_w = ctx.saved_tensors
+        dy2 = dy.reshape(b * s, H).contiguous()
+        dr, dg, dpost_w, dpost_b, _ = ops.ln_bwd(dy2, r, mu2, rs2, post_w if m.post_ln else None, p=m.p_hidden,
+                                                 seed=m.seed, layer=m.layer_id, site=SITE_MLP_OUT,
+                                                 row_offset=m.row_offset, want_dr=m.post_ln, want_dbias=False)
         if not m.post_ln:
             dr = dy2
-        dw2 = K.matmul_tn(dg, f)
-        dz = K.matmul_nn(dg, w2, epi=K.EPI_DACT, act=m.activation, aux=z)
+        dgf = _gather_rows(dg, m)
+        db2 = ops.colsum(dgf)
+        dw2 = K.matmul_tn(dgf, f)
+        dz = K.matmul_nn(dgf, w2, epi=K.EPI_DACT, act=m.activation, aux=z)
         db1 = ops.colsum(dz)
-        dw1 = K.matmul_tn(dz, h)
+        dw1 = K.matmul_tn(dz, hf)
         if m.tp_size == 1 and not m.pre_ln:
             dx = K.matmul_nn(dz, w1, epi=K.EPI_ADD, aux=dr)
             dpre_w = dpre_b = None
         else:
-            dh = K.matmul_nn(dz, w1)
-            C.all_reduce(dh)
+            dh = _combine_rows(K.matmul_nn(dz, w1), m)
             dx, dpre_w, dpre_b = _residual_bwd_out(dh, dr, x2, pre_w, mu1, rs1, m)
-        return (dx.view(B, s, H), dw1, db1, dw2, db2, dpre_w, dpre_b, dpost_w, dpost_b, None)
+        dpost_w, dpost_b, dpre_w, dpre_b = _sync_replicated([dpost_w, dpost_b, dpre_w, dpre_b], m)
+        return (dx.view(b, s, H), dw1, db1, dw2, db2, dpre_w, dpre_b, dpost_w, dpost_b, None)

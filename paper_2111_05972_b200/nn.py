@@ -161,7 +161,9 @@ class _LayerBase(DistributedModule):
         self.post_layernorm = post_layernorm
         self.layer_id = next_layer_id() if layer_id is None else layer_id
 
-    def _meta(self, sample_offset: int) -> L.LayerMeta:
+    def _meta(self, rc) -> L.LayerMeta:
+        """rc = (attention sample offset, own first global token row, row-sharded?)."""
+        sample_offset, row_offset, shard = rc
         T = STATE.tp_size
         hl = self.num_attention_heads // T
         return L.LayerMeta(hidden=self.hidden_size, heads_local=hl, heads_global=self.num_attention_heads,
@@ -171,7 +173,7 @@ class _LayerBase(DistributedModule):
                            causal=self.causal_mask_size is not None, pre_ln=self.pre_layernorm,
                            post_ln=self.post_layernorm, activation=self.activation, layer_id=self.layer_id,
                            seed=STATE.seed + 0x9E3779B97F4A7C15 * STATE.step, head_offset=STATE.tp_rank * hl,
-                           sample_offset=sample_offset, tp_size=T)
+                           sample_offset=sample_offset, tp_size=T, row_offset=row_offset, shard_rows=shard)
 
     def _ln_params(self, prefix):
         H = self.hidden_size
@@ -205,8 +207,8 @@ class DistributedAttentionLayer(_LayerBase):
         self.dense_bias = _param((H,), 0, None, zero=True)
         self._ln_params("")
 
-    def sublayer(self, X, mask, sample_offset):
-        m = self._meta(sample_offset)
+    def sublayer(self, X, mask, rc):
+        m = self._meta(rc)
         return L.AttentionFn.apply(X, self.qkv_weight, self.qkv_bias, self.dense_weight, self.dense_bias,
                                    self.pre_ln_weight, self.pre_ln_bias, self.post_ln_weight, self.post_ln_bias,
                                    mask, m)
@@ -251,8 +253,8 @@ class DistributedTransformerOutputLayer(_LayerBase):
         self.fc2_bias = _param((H,), 0, None, zero=True)
         self._ln_params("")
 
-    def sublayer(self, X, mask, sample_offset):
-        m = self._meta(sample_offset)
+    def sublayer(self, X, mask, rc):
+        m = self._meta(rc)
         return L.MlpFn.apply(X, self.fc1_weight, self.fc1_bias, self.fc2_weight, self.fc2_bias, self.pre_ln_weight,
                              self.pre_ln_bias, self.post_ln_weight, self.post_ln_bias, m)
 
@@ -274,19 +276,33 @@ class DistributedTransformerOutputLayer(_LayerBase):
                 getattr(self, f"{where}_ln_bias").copy_(p[f"mlp_{where}_ln_b"])
 
 
+def _row_ctx(B: int, s: int):
+    """(attention sample offset, own first global token row, row-sharded) for a batch of B own samples.
+
+    TP across DP ranks: activations stay on the owning rank (row-sharded); the
+    attention of the local heads sees the whole TP group's samples, starting at global sample
+    rdp_rank*T*B.  Prescaled batch / T == 1: activations replicated, samples rdp_rank*B (dp_rank*B)."""
+    if STATE.tp_size == 1:
+        off = STATE.dp_rank * B
+        return (off, off * s, False)
+    if STATE.prescaled:
+        off = STATE.rdp_rank * B
+        return (off, off * s, False)
+    return (STATE.rdp_rank * STATE.tp_size * B, STATE.dp_rank * B * s, True)
+
+
 def _entry(x, attention_mask):
-    """TP-across-DP entry: gather the TP group's samples; prescaled: nothing."""
+    """Module entry: in row-sharded mode only the attention mask is gathered over the TP group."""
     B, s = x.shape[0], x.shape[1]
     mask = _mask_2d(attention_mask, B, s)
-    if STATE.prescaled or STATE.tp_size == 1:
-        return x, mask, STATE.rdp_rank * B if STATE.prescaled else STATE.dp_rank * B
-    X = C.tp_dp_entry(x)
-    if mask is not None:
+    rc = _row_ctx(B, s)
+    if rc[2] and mask is not None:
         mask = C.all_gather(mask, 0)
-    return X, mask, STATE.rdp_rank * STATE.tp_size * B
+    return x, mask, rc
 
 
 def _exit(Y):
+    """Return the rows of this rank's samples from a TP-replicated tensor (backward: allgather)."""
     if STATE.prescaled or STATE.tp_size == 1:
         return Y
     return C.tp_dp_exit(Y)
@@ -294,8 +310,8 @@ def _exit(Y):
 
 def _run_standalone(mod, hidden_states, attention_mask):
     x = hidden_states.to(DTYPE).contiguous()
-    X, mask, off = _entry(x, attention_mask)
-    return _exit(mod.sublayer(X, mask, off))
+    X, mask, rc = _entry(x, attention_mask)
+    return mod.sublayer(X, mask, rc)
 
 
 class DistributedTransformerLayer(DistributedModule):
@@ -321,8 +337,8 @@ class DistributedTransformerLayer(DistributedModule):
             use_normal_initialization, pre_layernorm, post_layernorm, layer_id=lid,
             num_attention_heads=num_attention_heads, _standalone=False)
 
-    def sublayer(self, X, mask, sample_offset):
-        return self.output.sublayer(self.attention.sublayer(X, mask, sample_offset), mask, sample_offset)
+    def sublayer(self, X, mask, rc):
+        return self.output.sublayer(self.attention.sublayer(X, mask, rc), mask, rc)
 
     def forward(self, hidden_states, attention_mask=None):
         return _run_standalone(self, hidden_states, attention_mask)
@@ -349,9 +365,9 @@ class DistributedTransformer(DistributedModule):
                                         add_cross_attention, pre_layernorm, post_layernorm)
             for _ in range(num_layers)])
 
-    def sublayer(self, X, mask, sample_offset):
+    def sublayer(self, X, mask, rc):
         for layer in self.seq_layers:
-            X = layer.sublayer(X, mask, sample_offset)
+            X = layer.sublayer(X, mask, rc)
         return X
 
     def forward(self, hidden_states, attention_mask=None):
@@ -419,20 +435,24 @@ class DistributedTransformerLMHead(DistributedModule):
         mask = _mask_2d(attention_mask, b, s)
         if gathered and mask is not None:
             mask = C.all_gather(mask, 0)
-        off = (STATE.rdp_rank * T * b) if gathered else (STATE.rdp_rank * b if STATE.prescaled else STATE.dp_rank * b)
+        rc = _row_ctx(b, s)
         we = self.word_embedding
         from .embedding import _LookupFn
         h = _LookupFn.apply(ids, we.weight, we.row_offset, we.num_embeddings, we.padding_idx,
                             self.position_embedding if STATE.tp_rank == 0 else None, s, False)
         h = h.reshape(ids.shape[0], s, self.hidden_size)
-        if T > 1:
+        if gathered:
+            h = C.reduce_scatter_for_tp(h, 0)  # partial lookups -> this rank's own rows
+        elif T > 1:
             h = C.fwd_allreduce_for_tp(h)
-        h = self.transformer.sublayer(h, mask, off)
+        h = self.transformer.sublayer(h, mask, rc)
         if self.final_ln is not None:
             h = self.final_ln(h)
         if not self.add_lm_head:
-            return _exit(h) if gathered else h
-        logits = lm_head_logits(h, we.weight)  # [B*s, Vp/T]
+            return h
+        if gathered:
+            h = C.fused_allgather_for_tp(h, 0)  # every rank scores all rows on its vocab shard
+        logits = lm_head_logits(h, we.weight, reduce_grad=not gathered)  # [B*s, Vp/T]
         if labels is None:
             out = logits.reshape(ids.shape[0], s, -1)
             return _exit(out) if gathered else out
