@@ -211,6 +211,40 @@ SMPK_API int smpk_flash_attn_bwd(const void* qkv, int64_t ld, const void* out, i
                                  int64_t workspace_bytes, void* stream);
 
 /*
+ * Fused tensor-parallel collectives over peer-mapped (symmetric) memory — the row-parallel
+ * "partial-sum allreduce fused into the GEMM epilogue through NVLink peer stores" of the
+ * north_star, in the reduce-scatter + allgather form used with row-sharded activations
+ * (fwd_allreduce_for_tp / reduce_scatter_for_tp / fused_allgather_for_tp).
+ *   smpk_gemm_rs        C = A B^T with row r stored to c_peers[r / rows_per_owner] + peer_slot_off
+ *                       + (r % rows_per_owner) * ldc (the owner's partial slot for this rank)
+ *   smpk_bdr_ln_fwd_ex  smpk_bdr_ln_fwd reading x as the ascending-rank sum of nslots partial slots
+ *                       (slot_stride elements apart) and storing its output to every out_peers[j]
+ *                       + peer_off (allgather producer)
+ *   smpk_ln_bwd_ex      smpk_ln_bwd with the same slot-sum input / peer-store output for dy / dsub
+ *   smpk_symm_export    IPC handle + offset of a pointer inside its allocation
+ *   smpk_symm_barrier   epoch barrier over the group (system-scope release/acquire flag words),
+ *                       times out after timeout_s; smpk_symm_timeout_peer reports 1 + the stuck peer
+ */
+SMPK_API int smpk_gemm_rs(const void* a, int a_mn_major, int64_t lda, const void* b, int b_mn_major, int64_t ldb,
+                          void* const* c_peers, int64_t ldc, int64_t rows_per_owner, int64_t peer_slot_off, int M,
+                          int N, int K, void* stream);
+SMPK_API int smpk_bdr_ln_fwd_ex(const void* x, int nslots, int64_t slot_stride, const void* bias, const void* residual,
+                                void* r_out, const void* gamma, const void* beta, void* y_out, float* mean,
+                                float* rstd, void* const* out_peers, int npeers, int64_t peer_off, int M, int H,
+                                float eps, float p_drop, uint64_t seed, int layer, int site, int64_t row_offset,
+                                void* stream);
+SMPK_API int smpk_ln_bwd_ex(const void* dy, int nslots, int64_t slot_stride, const void* r, const float* mean,
+                            const float* rstd, const void* gamma, const void* dres, void* dr_out, void* dsub_out,
+                            void* const* out_peers, int npeers, int64_t peer_off, void* dgamma, void* dbeta,
+                            void* dbias, int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed,
+                            int layer, int site, int64_t row_offset, void* workspace, int64_t workspace_bytes,
+                            void* stream);
+SMPK_API int smpk_symm_export(void* ptr, void* handle_out, int64_t* offset);
+SMPK_API int smpk_symm_barrier(void* const* peer_flags, const void* local_flags, int T, int rank, uint32_t epoch,
+                               double timeout_s, void* stream);
+SMPK_API int smpk_symm_timeout_peer(void);
+
+/*
  * Pipeline stage send/recv over NVLink peer memory — the D2D communicator of the
  * module server; replaces the simulated hop
  * mpsim pipeline.py:653-712 (_transfer / _send_request / _send_response) whose routing

@@ -39,6 +39,12 @@ SIGNATURES: dict[str, list] = {
     "smpk_vocab_ce_bwd": [P, L, L, I, L, L, P, L, P, P, F, P, L, P],
     "smpk_flash_attn_fwd": [P, L, I, I, I, I, P, L, P, P, F, I, F, C.c_uint64, I, L, I, I, P],
     "smpk_flash_attn_bwd": [P, L, P, L, P, L, P, I, I, I, I, P, P, F, I, F, C.c_uint64, I, L, I, I, P, L, P],
+    "smpk_gemm_rs": [P, I, L, P, I, L, P, L, L, L, I, I, I, P],
+    "smpk_bdr_ln_fwd_ex": [P, I, L, P, P, P, P, P, P, P, P, P, I, L, I, I, F, F, C.c_uint64, I, I, L, P],
+    "smpk_ln_bwd_ex": [P, I, L, P, P, P, P, P, P, P, P, I, L, P, P, P, I, I, I, I, F, C.c_uint64, I, I, L, P, L, P],
+    "smpk_symm_export": [P, P, C.POINTER(L)],
+    "smpk_symm_barrier": [P, P, I, I, C.c_uint32, C.c_double, P],
+    "smpk_symm_timeout_peer": [],
     "smpk_p2p_alloc": [L, C.POINTER(P)],
     "smpk_p2p_free": [P],
     "smpk_p2p_export": [P, P],
@@ -89,7 +95,7 @@ def lib() -> C.CDLL:
 
 
 # kernels launched by each entry point (for bench.py's gpu_launches count)
-LAUNCHES_PER_CALL = {"smpk_ln_bwd": 2, "smpk_colsum": 2}
+LAUNCHES_PER_CALL = {"smpk_ln_bwd": 2, "smpk_ln_bwd_ex": 2, "smpk_colsum": 2, "smpk_flash_attn_bwd": 3}
 launch_count = 0
 
 

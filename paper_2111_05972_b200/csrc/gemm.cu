@@ -38,6 +38,10 @@ struct GemmArgs {
   bf16* aux;
   int64_t ldaux;
   int vec_ok;  // 16B-aligned rows of C / aux
+  // reduce-scatter epilogue: row r of C goes to rank (r / rows_per_owner)'s peer-mapped
+  // buffer c_peers[owner] at element offset peer_slot_off + (r % rows_per_owner) * ldc
+  void* const* c_peers;
+  int64_t rows_per_owner, peer_slot_off;
 };
 
 template <int BN, int STAGES>
@@ -165,7 +169,14 @@ __device__ __forceinline__ void epilogue_store32(const GemmArgs& g, int row, int
         if (col0 + i < g.N) cp[i] = v[i] + (BETA ? g.beta * cp[i] : 0.f);
     }
   } else {
-    bf16* cp = reinterpret_cast<bf16*>(g.c) + c_off + (int64_t)row * g.ldc + col0;
+    bf16* cp;
+    if (g.c_peers != nullptr) {  // NVLink peer store into the owning rank's partial slot
+      const int64_t owner = row / g.rows_per_owner;
+      cp = reinterpret_cast<bf16*>(g.c_peers[owner]) + g.peer_slot_off + (row - owner * g.rows_per_owner) * g.ldc +
+           col0;
+    } else {
+      cp = reinterpret_cast<bf16*>(g.c) + c_off + (int64_t)row * g.ldc + col0;
+    }
     if (full) {
       uint4* d = reinterpret_cast<uint4*>(cp);
 #pragma unroll
@@ -451,14 +462,14 @@ static int dispatch_epilogue(const CUtensorMap& ta, const CUtensorMap& tb, GemmA
 
 using namespace smpk;
 
-extern "C" int smpk_gemm(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, int64_t a_bs2, const void* b,
-                         int b_mn_major, int64_t ldb, int64_t b_bs1, int64_t b_bs2, void* c, int c_f32,
-                         int64_t ldc, int64_t c_bs1, int64_t c_bs2, int M, int N, int K, int nb1, int nb2,
-                         float alpha, float beta, int epilogue, int act, const void* bias, void* aux,
-                         int64_t ldaux, void* stream) {
+static int gemm_impl(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, int64_t a_bs2, const void* b,
+                     int b_mn_major, int64_t ldb, int64_t b_bs1, int64_t b_bs2, void* c, int c_f32, int64_t ldc,
+                     int64_t c_bs1, int64_t c_bs2, int M, int N, int K, int nb1, int nb2, float alpha, float beta,
+                     int epilogue, int act, const void* bias, void* aux, int64_t ldaux, void* const* c_peers,
+                     int64_t rows_per_owner, int64_t peer_slot_off, void* stream) {
   SMPK_REQUIRE(M > 0 && N > 0 && K > 0 && nb1 > 0 && nb2 > 0, SMPK_ERR_BAD_SHAPE,
                "smpk_gemm: bad shape M=%d N=%d K=%d nb=%dx%d", M, N, K, nb1, nb2);
-  SMPK_REQUIRE(a && b && c, SMPK_ERR_BAD_ARG, "smpk_gemm: null operand");
+  SMPK_REQUIRE(a && b && (c || c_peers), SMPK_ERR_BAD_ARG, "smpk_gemm: null operand");
   SMPK_REQUIRE(epilogue >= SMPK_EPI_NONE && epilogue <= SMPK_EPI_ADD, SMPK_ERR_BAD_ARG,
                "smpk_gemm: unknown epilogue %d", epilogue);
   const bool need_bias = epilogue == SMPK_EPI_BIAS || epilogue == SMPK_EPI_BIAS_ACT;
@@ -497,9 +508,13 @@ extern "C" int smpk_gemm(const void* a, int a_mn_major, int64_t lda, int64_t a_b
   g.bias = reinterpret_cast<const bf16*>(bias);
   g.aux = reinterpret_cast<bf16*>(aux);
   g.ldaux = ldaux;
+  g.c_peers = c_peers;
+  g.rows_per_owner = rows_per_owner > 0 ? rows_per_owner : 1;
+  g.peer_slot_off = peer_slot_off;
   const int esz = c_f32 ? 4 : 2;
   bool vec = (reinterpret_cast<uintptr_t>(c) % 16 == 0) && ((ldc * esz) % 16 == 0) && ((c_bs1 * esz) % 16 == 0) &&
              ((c_bs2 * esz) % 16 == 0);
+  if (c_peers) vec = ((ldc * esz) % 16 == 0) && ((peer_slot_off * esz) % 16 == 0);
   if (need_bias) vec = vec && (reinterpret_cast<uintptr_t>(bias) % 16 == 0);
   if (need_aux) vec = vec && (reinterpret_cast<uintptr_t>(aux) % 16 == 0) && (ldaux % 8 == 0);
   g.vec_ok = vec ? 1 : 0;
@@ -508,4 +523,24 @@ extern "C" int smpk_gemm(const void* a, int a_mn_major, int64_t lda, int64_t a_b
   if (BN == 64) return dispatch_epilogue<64, 8>(ta, tb, g, st);
   if (BN == 128) return dispatch_epilogue<128, 6>(ta, tb, g, st);
   return dispatch_epilogue<256, 4>(ta, tb, g, st);
+}
+
+extern "C" int smpk_gemm(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, int64_t a_bs2, const void* b,
+                         int b_mn_major, int64_t ldb, int64_t b_bs1, int64_t b_bs2, void* c, int c_f32,
+                         int64_t ldc, int64_t c_bs1, int64_t c_bs2, int M, int N, int K, int nb1, int nb2,
+                         float alpha, float beta, int epilogue, int act, const void* bias, void* aux,
+                         int64_t ldaux, void* stream) {
+  return gemm_impl(a, a_mn_major, lda, a_bs1, a_bs2, b, b_mn_major, ldb, b_bs1, b_bs2, c, c_f32, ldc, c_bs1, c_bs2,
+                   M, N, K, nb1, nb2, alpha, beta, epilogue, act, bias, aux, ldaux, nullptr, 0, 0, stream);
+}
+
+extern "C" int smpk_gemm_rs(const void* a, int a_mn_major, int64_t lda, const void* b, int b_mn_major, int64_t ldb,
+                            void* const* c_peers, int64_t ldc, int64_t rows_per_owner, int64_t peer_slot_off, int M,
+                            int N, int K, void* stream) {
+  SMPK_REQUIRE(c_peers != nullptr, SMPK_ERR_BAD_ARG, "smpk_gemm_rs: null peer table");
+  SMPK_REQUIRE(rows_per_owner > 0 && rows_per_owner % 128 == 0 && M % rows_per_owner == 0, SMPK_ERR_NOT_DIVISIBLE,
+               "smpk_gemm_rs: rows per owner %lld must divide M=%d and be a multiple of 128",
+               (long long)rows_per_owner, M);
+  return gemm_impl(a, a_mn_major, lda, 0, 0, b, b_mn_major, ldb, 0, 0, nullptr, 0, ldc, 0, 0, M, N, K, 1, 1, 1.f,
+                   0.f, SMPK_EPI_NONE, 0, nullptr, nullptr, 0, c_peers, rows_per_owner, peer_slot_off, stream);
 }

@@ -127,7 +127,34 @@ struct BdrLnArgs {
   uint64_t seed;
   uint32_t layer, site;
   int64_t row_offset;
+  // reduce-scatter consumer: x = sum_{j < nslots} x[j * slot_stride + ...] (ascending rank)
+  int nslots;
+  int64_t slot_stride;
+  // allgather producer: the final output (y, or r without LN) is also stored to every
+  // peer-mapped buffer out_peers[j] + peer_off (NVLink peer stores)
+  bf16* const* out_peers;
+  int npeers;
+  int64_t peer_off;
 };
+
+__device__ __forceinline__ void load8_slots(const bf16* p, int nslots, int64_t stride, float (&v)[8]) {
+  load8(p, v);
+  for (int j = 1; j < nslots; ++j) {
+    float t[8];
+    load8(p + j * stride, t);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] += t[e];
+  }
+}
+
+__device__ __forceinline__ void store8_peers(bf16* const* peers, int npeers, int64_t off, const float (&v)[8]) {
+  uint4 u;
+  u.x = pack_bf16x2(v[0], v[1]);
+  u.y = pack_bf16x2(v[2], v[3]);
+  u.z = pack_bf16x2(v[4], v[5]);
+  u.w = pack_bf16x2(v[6], v[7]);
+  for (int j = 0; j < npeers; ++j) *reinterpret_cast<uint4*>(peers[j] + off) = u;
+}
 
 template <int W, int VPT>
 __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs a) {
@@ -144,7 +171,7 @@ __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs
     for (int i = 0; i < VPT; ++i) {
       const int col = ((i * W + wi) * 32 + lane) * 8;
       if (valid) {
-        load8(a.x + (int64_t)row * a.H + col, v[i]);
+        load8_slots(a.x + (int64_t)row * a.H + col, a.nslots, a.slot_stride, v[i]);
         if (a.bias) {
           float b[8];
           load8(a.bias + col, b);
@@ -165,6 +192,7 @@ __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs
         }
         round8(v[i]);
         if (a.r_out) store8(a.r_out + (int64_t)row * a.H + col, v[i]);
+        if (a.npeers && a.gamma == nullptr) store8_peers(a.out_peers, a.npeers, a.peer_off + (int64_t)row * a.H + col, v[i]);
       } else {
 #pragma unroll
         for (int j = 0; j < 8; ++j) v[i][j] = 0.f;
@@ -200,7 +228,8 @@ __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs
         load8(a.beta + col, bt);
 #pragma unroll
         for (int j = 0; j < 8; ++j) o[j] = (v[i][j] - mu) * rs * gm[j] + bt[j];
-        store8(a.y_out + (int64_t)row * a.H + col, o);
+        if (a.y_out) store8(a.y_out + (int64_t)row * a.H + col, o);
+        if (a.npeers) store8_peers(a.out_peers, a.npeers, a.peer_off + (int64_t)row * a.H + col, o);
       }
     }
   }
@@ -224,6 +253,11 @@ struct LnBwdArgs {
   uint64_t seed;
   uint32_t layer, site;
   int64_t row_offset;
+  int nslots;          // dy = sum of nslots partial slots (reduce-scatter consumer)
+  int64_t slot_stride;
+  bf16* const* out_peers;  // dsub also stored to every peer buffer (allgather producer)
+  int npeers;
+  int64_t peer_off;
 };
 
 template <int W, int VPT>
@@ -287,11 +321,11 @@ __global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const LnBwdArgs a) 
     for (int i = 0; i < VPT; ++i) {
       const int col = ((i * W + wi) * 32 + lane) * 8;
       if (valid && !has_ln) {
-        load8(a.dy + (int64_t)row * a.H + col, g[i]);
+        load8_slots(a.dy + (int64_t)row * a.H + col, a.nslots, a.slot_stride, g[i]);
       } else if (valid) {
         float dy[8], gm[8];
         load8(a.r + (int64_t)row * a.H + col, xh[i]);
-        load8(a.dy + (int64_t)row * a.H + col, dy);
+        load8_slots(a.dy + (int64_t)row * a.H + col, a.nslots, a.slot_stride, dy);
         load8(a.gamma + col, gm);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -332,6 +366,7 @@ __global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const LnBwdArgs a) 
         round8(d);
         store8(a.dsub_out + (int64_t)row * a.H + col, d);
       }
+      if (a.npeers) store8_peers(a.out_peers, a.npeers, a.peer_off + (int64_t)row * a.H + col, d);
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc_d[i][j] += d[j];
     }
@@ -582,27 +617,38 @@ static int softmax_nv(int sk) {
 
 using namespace smpk;
 
-extern "C" int smpk_bdr_ln_fwd(const void* x, const void* bias, const void* residual, void* r_out, const void* gamma,
-                               const void* beta, void* y_out, float* mean, float* rstd, int M, int H, float eps,
-                               float p_drop, uint64_t seed, int layer, int site, int64_t row_offset, void* stream) {
+extern "C" int smpk_bdr_ln_fwd_ex(const void* x, int nslots, int64_t slot_stride, const void* bias,
+                                  const void* residual, void* r_out, const void* gamma, const void* beta, void* y_out,
+                                  float* mean, float* rstd, void* const* out_peers, int npeers, int64_t peer_off, int M,
+                                  int H, float eps, float p_drop, uint64_t seed, int layer, int site,
+                                  int64_t row_offset, void* stream) {
   RowGeom geo;
   SMPK_REQUIRE(M >= 0 && row_geom(H, geo) && geom_supported(geo), SMPK_ERR_UNSUPPORTED,
                "smpk_bdr_ln_fwd: hidden size %d unsupported (need a multiple of 256)", H);
-  SMPK_REQUIRE(x != nullptr, SMPK_ERR_BAD_ARG, "smpk_bdr_ln_fwd: null x");
-  SMPK_REQUIRE(gamma == nullptr || (beta && y_out && mean && rstd), SMPK_ERR_BAD_ARG,
-               "smpk_bdr_ln_fwd: LayerNorm needs beta, y_out, mean and rstd");
-  SMPK_REQUIRE(gamma != nullptr || r_out != nullptr, SMPK_ERR_BAD_ARG, "smpk_bdr_ln_fwd: nothing to compute");
+  SMPK_REQUIRE(x != nullptr && nslots >= 1, SMPK_ERR_BAD_ARG, "smpk_bdr_ln_fwd: null x");
+  SMPK_REQUIRE(gamma == nullptr || (beta && mean && rstd && (y_out || npeers)), SMPK_ERR_BAD_ARG,
+               "smpk_bdr_ln_fwd: LayerNorm needs beta, mean, rstd and an output");
+  SMPK_REQUIRE(gamma != nullptr || r_out != nullptr || npeers > 0, SMPK_ERR_BAD_ARG,
+               "smpk_bdr_ln_fwd: nothing to compute");
+  SMPK_REQUIRE(npeers == 0 || out_peers != nullptr, SMPK_ERR_BAD_ARG, "smpk_bdr_ln_fwd: null peer table");
   SMPK_REQUIRE(p_drop >= 0.f && p_drop < 1.f, SMPK_ERR_BAD_ARG, "smpk_bdr_ln_fwd: dropout p must be in [0,1)");
   if (M == 0) return SMPK_OK;
   BdrLnArgs a{reinterpret_cast<const bf16*>(x), reinterpret_cast<const bf16*>(bias),
               reinterpret_cast<const bf16*>(residual), reinterpret_cast<bf16*>(r_out),
               reinterpret_cast<const bf16*>(gamma), reinterpret_cast<const bf16*>(beta),
               reinterpret_cast<bf16*>(y_out), mean, rstd, M, H, eps, p_drop, seed, (uint32_t)layer, (uint32_t)site,
-              row_offset};
+              row_offset, nslots, slot_stride, reinterpret_cast<bf16* const*>(out_peers), npeers, peer_off};
   const int grid = row_grid(M, geo.W);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   SMPK_DISPATCH_ROW(geo.W, geo.VPT, bdr_ln_fwd_kernel, (grid, ROW_THREADS, 0, st), (a));
   return check_launch("smpk_bdr_ln_fwd");
+}
+
+extern "C" int smpk_bdr_ln_fwd(const void* x, const void* bias, const void* residual, void* r_out, const void* gamma,
+                               const void* beta, void* y_out, float* mean, float* rstd, int M, int H, float eps,
+                               float p_drop, uint64_t seed, int layer, int site, int64_t row_offset, void* stream) {
+  return smpk_bdr_ln_fwd_ex(x, 1, 0, bias, residual, r_out, gamma, beta, y_out, mean, rstd, nullptr, 0, 0, M, H, eps,
+                            p_drop, seed, layer, site, row_offset, stream);
 }
 
 static int64_t ln_bwd_grid(int M, int H) {
@@ -613,16 +659,19 @@ static int64_t ln_bwd_grid(int M, int H) {
 
 extern "C" int64_t smpk_ln_bwd_workspace(int M, int H) { return ln_bwd_grid(M, H) * 3 * (int64_t)H * 4; }
 
-extern "C" int smpk_ln_bwd(const void* dy, const void* r, const float* mean, const float* rstd, const void* gamma,
-                           const void* dres, void* dr_out, void* dsub_out, void* dgamma, void* dbeta, void* dbias,
-                           int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed, int layer,
-                           int site, int64_t row_offset, void* workspace, int64_t workspace_bytes, void* stream) {
+extern "C" int smpk_ln_bwd_ex(const void* dy, int nslots, int64_t slot_stride, const void* r, const float* mean,
+                              const float* rstd, const void* gamma, const void* dres, void* dr_out, void* dsub_out,
+                              void* const* out_peers, int npeers, int64_t peer_off, void* dgamma, void* dbeta,
+                              void* dbias, int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed,
+                              int layer, int site, int64_t row_offset, void* workspace, int64_t workspace_bytes,
+                              void* stream) {
   RowGeom geo;
   SMPK_REQUIRE(M > 0 && row_geom(H, geo) && geom_supported(geo), SMPK_ERR_UNSUPPORTED,
                "smpk_ln_bwd: hidden size %d unsupported", H);
-  SMPK_REQUIRE(dy && (gamma == nullptr || (r && mean && rstd && dr_out)), SMPK_ERR_BAD_ARG,
+  SMPK_REQUIRE(dy && nslots >= 1 && (gamma == nullptr || (r && mean && rstd && dr_out)), SMPK_ERR_BAD_ARG,
                "smpk_ln_bwd: null argument");
   SMPK_REQUIRE(p_drop == 0.f || dsub_out, SMPK_ERR_BAD_ARG, "smpk_ln_bwd: dropout backward needs dsub_out");
+  SMPK_REQUIRE(npeers == 0 || out_peers, SMPK_ERR_BAD_ARG, "smpk_ln_bwd: null peer table");
   const int grid = row_grid(M, geo.W);
   SMPK_REQUIRE(workspace && workspace_bytes >= (int64_t)grid * 3 * H * 4, SMPK_ERR_BAD_ARG,
                "smpk_ln_bwd: workspace too small (%lld < %lld)", (long long)workspace_bytes,
@@ -630,16 +679,27 @@ extern "C" int smpk_ln_bwd(const void* dy, const void* r, const float* mean, con
   LnBwdArgs a{reinterpret_cast<const bf16*>(dy), reinterpret_cast<const bf16*>(r), mean, rstd,
               reinterpret_cast<const bf16*>(gamma), reinterpret_cast<const bf16*>(dres),
               reinterpret_cast<bf16*>(dr_out), reinterpret_cast<bf16*>(dsub_out),
-              reinterpret_cast<float*>(workspace), M, H, p_drop, seed, (uint32_t)layer, (uint32_t)site, row_offset};
+              reinterpret_cast<float*>(workspace), M, H, p_drop, seed, (uint32_t)layer, (uint32_t)site, row_offset,
+              nslots, slot_stride, reinterpret_cast<bf16* const*>(out_peers), npeers, peer_off};
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int red_bytes = geo.W == 8 ? 0 : geo.W * geo.VPT * 8 * 32 * 4;
   SMPK_DISPATCH_ROW(geo.W, geo.VPT, ln_bwd_kernel, (grid, ROW_THREADS, red_bytes, st), (a));
   int rc = check_launch("smpk_ln_bwd");
   if (rc) return rc;
+  if (!dgamma && !dbeta && !dbias) return SMPK_OK;
   dim3 rg((H + 31) / 32, 3);
   colsum_reduce_kernel<<<rg, 256, 0, st>>>(reinterpret_cast<float*>(workspace), grid, 3, H, dgamma, dbeta, dbias,
                                            grads_f32, accumulate);
   return check_launch("smpk_ln_bwd(reduce)");
+}
+
+extern "C" int smpk_ln_bwd(const void* dy, const void* r, const float* mean, const float* rstd, const void* gamma,
+                           const void* dres, void* dr_out, void* dsub_out, void* dgamma, void* dbeta, void* dbias,
+                           int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed, int layer,
+                           int site, int64_t row_offset, void* workspace, int64_t workspace_bytes, void* stream) {
+  return smpk_ln_bwd_ex(dy, 1, 0, r, mean, rstd, gamma, dres, dr_out, dsub_out, nullptr, 0, 0, dgamma, dbeta, dbias,
+                        grads_f32, accumulate, M, H, p_drop, seed, layer, site, row_offset, workspace,
+                        workspace_bytes, stream);
 }
 
 // Vectorised column partials: thread = 8 consecutive columns (one 16-B load per row),

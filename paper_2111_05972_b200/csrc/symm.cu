@@ -1,0 +1,93 @@
+// symm.cu — symmetric (peer-mapped) memory for the fused tensor-parallel collectives.
+//
+// Every rank of a TP group allocates the same pool, exports a CUDA IPC handle once and
+// maps all peers' pools (persistent pre-registered buffers).  The row-parallel
+// GEMM epilogue stores its partial tiles straight into the owning rank's pool
+// (smpk_gemm_rs), the row kernels read the T partial slots in ascending rank order and
+// store allgathered rows into every peer's pool (smpk_bdr_ln_fwd_ex / smpk_ln_bwd_ex), and
+// smpk_symm_barrier orders those NVLink stores between ranks: each rank writes its epoch
+// into every peer's flag word (st.release.sys after a system fence) and waits until all
+// peers' epochs have arrived (ld.acquire.sys), with a wall-clock timeout that reports the
+// stuck peer instead of hanging.
+#include <mutex>
+
+#include "smpk_common.cuh"
+
+namespace smpk {
+
+__device__ unsigned long long g_symm_timeout_peer = 0;  // 1 + peer index that never arrived
+
+__global__ void symm_barrier_kernel(uint32_t* const* peer_flags, const uint32_t* local_flags, int T, int rank,
+                                    uint32_t epoch, unsigned long long timeout_ns) {
+  const int t = threadIdx.x;
+  if (t >= T) return;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(peer_flags[t] + rank), "r"(epoch) : "memory");
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (true) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(local_flags + t) : "memory");
+    if ((int32_t)(v - epoch) >= 0) break;
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (now - t0 > timeout_ns) {
+      atomicExch(&g_symm_timeout_peer, (unsigned long long)(t + 1));
+      break;
+    }
+    __nanosleep(64);
+  }
+}
+
+typedef CUresult (*PFN_getAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+static PFN_getAddressRange get_range_fn() {
+  static PFN_getAddressRange fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_getAddressRange>(p);
+  });
+  return fn;
+}
+
+}  // namespace smpk
+
+using namespace smpk;
+
+// IPC handle of the allocation containing ptr, and ptr's byte offset inside it.
+extern "C" int smpk_symm_export(void* ptr, void* handle_out, int64_t* offset) {
+  SMPK_REQUIRE(ptr && handle_out && offset, SMPK_ERR_BAD_ARG, "smpk_symm_export: bad arguments");
+  PFN_getAddressRange fn = get_range_fn();
+  SMPK_REQUIRE(fn != nullptr, SMPK_ERR_CUDA, "smpk_symm_export: cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  CUresult r = fn(&base, &size, (CUdeviceptr)ptr);
+  SMPK_REQUIRE(r == CUDA_SUCCESS, SMPK_ERR_CUDA, "smpk_symm_export: address range (%d)", (int)r);
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  SMPK_REQUIRE(e == cudaSuccess, SMPK_ERR_CUDA, "smpk_symm_export: %s", cudaGetErrorString(e));
+  memcpy(handle_out, &h, sizeof(h));
+  *offset = (int64_t)((CUdeviceptr)ptr - base);
+  return SMPK_OK;
+}
+
+extern "C" int smpk_symm_barrier(void* const* peer_flags, const void* local_flags, int T, int rank, uint32_t epoch,
+                                 double timeout_s, void* stream) {
+  SMPK_REQUIRE(peer_flags && local_flags && T > 0 && T <= 32 && rank >= 0 && rank < T, SMPK_ERR_BAD_ARG,
+               "smpk_symm_barrier: bad arguments");
+  symm_barrier_kernel<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<uint32_t* const*>(peer_flags), reinterpret_cast<const uint32_t*>(local_flags), T, rank, epoch,
+      (unsigned long long)(timeout_s * 1e9));
+  return check_launch("smpk_symm_barrier");
+}
+
+// 0 = no timeout so far; otherwise 1 + index of the peer whose signal never arrived (host sync).
+extern "C" int smpk_symm_timeout_peer(void) {
+  unsigned long long v = 0;
+  cudaMemcpyFromSymbol(&v, g_symm_timeout_peer, sizeof(v));
+  return (int)v;
+}

@@ -65,6 +65,24 @@ def gemm_raw(a, a_mn, lda, a_bs, b, b_mn, ldb, b_bs, c, ldc, c_bs, M, N, K, nb=(
         prof.records.append((e0, e1, 2.0 * M * N * K * nb[0] * nb[1]))
 
 
+def gemm_rs(a: torch.Tensor, b: torch.Tensor, b_mn: bool, c_table: torch.Tensor, *, ldc: int, rows_per_owner: int,
+            slot_off: int) -> None:
+    """Row-parallel product a @ B^T (B [N,K]; b_mn: B given as [K,N]) whose rows are stored straight
+    into the owning ranks' peer-mapped partial slots (c_table: device table of T addresses)."""
+    _check_cuda(a, b, c_table)
+    M, Kd = a.shape
+    N = b.shape[1] if b_mn else b.shape[0]
+    prof = PROFILER
+    if prof is not None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+    _lib.call("smpk_gemm_rs", a.data_ptr(), 0, _rowmajor(a, "a"), b.data_ptr(), int(bool(b_mn)), _rowmajor(b, "b"),
+              c_table.data_ptr(), int(ldc), int(rows_per_owner), int(slot_off), M, N, Kd, _stream())
+    if prof is not None:
+        e1.record()
+        prof.records.append((e0, e1, 2.0 * M * N * Kd))
+
+
 def _rowmajor(t: torch.Tensor, name: str) -> int:
     if t.dim() != 2 or t.stride(1) != 1:
         raise ShapeMismatchError(f"{name} must be a 2-D row-major view, got shape {tuple(t.shape)} "

@@ -26,6 +26,7 @@ from . import collectives as C
 from . import kernels as K
 from . import ops
 from .ops import SITE_ATTN_OUT, SITE_MLP_OUT
+from .state import get_pool
 
 
 @dataclass
@@ -48,6 +49,7 @@ class LayerMeta:
     tp_size: int
     row_offset: int = 0  # global token row of this rank's first activation row (hidden dropout)
     shard_rows: bool = False  # activations row-sharded between sub-layers (AG in / RS out)
+    comm: str = "peer"  # "peer": fused NVLink peer-store collectives; "nccl": torch.distributed
 
 
 class LinearFn(torch.autograd.Function):
@@ -194,6 +196,89 @@ def _sync_replicated(grads, m: LayerMeta):
     return out
 
 
+# With tp_comm == "peer" the AG / RS above are fused into the producing kernels over the TP
+# group's symmetric peer-mapped pool (symm.py, csrc/symm.cu): the row kernel that produces a
+# sub-layer input stores it into every peer's gather region, the row-parallel GEMM epilogue
+# stores its partial tiles into the owning rank's slot region (NVLink peer stores overlapped
+# with the MMA main loop), and the consuming row kernel sums the T slots in ascending rank
+# order.  One epoch barrier orders each exchange.
+
+def _peer(m: LayerMeta) -> bool:
+    return m.shard_rows and m.comm == "peer"
+
+
+def _gather_in(x2, m: LayerMeta, ln=None):
+    """Column-parallel GEMM input: [pre-LN](own rows) gathered over the group.
+    Returns (hf, mean, rstd, pool region or None)."""
+    if _peer(m):
+        pool = get_pool()
+        R, H = x2.shape
+        G = pool.alloc(m.tp_size * R * H * 2)
+        tbl, off = pool.table(G), pool.me * R * H
+        mean = rstd = None
+        if ln is not None:
+            _, _, mean, rstd = ops.bdr_ln(x2, gamma=ln[0], beta=ln[1], eps=m.eps, want_r=False, want_y=False,
+                                          out_peers=tbl, peer_off=off)
+        else:
+            ops.bdr_ln(x2, want_r=False, out_peers=tbl, peer_off=off)
+        pool.barrier()
+        return pool.view(G, (m.tp_size * R, H)), mean, rstd, G
+    if ln is not None:
+        h, mean, rstd = ops.layer_norm(x2, ln[0], ln[1], m.eps)
+    else:
+        h, mean, rstd = x2, None, None
+    return _gather_rows(h, m), mean, rstd, None
+
+
+def _rs_out(a, w, w_mn: bool, m: LayerMeta, R: int, N: int):
+    """Row-parallel product combined over the group -> (x, nslots, slot_stride, region).
+    x is dense (nslots == 1) or the pool's T partial slots of this rank's rows."""
+    if _peer(m):
+        pool = get_pool()
+        P = pool.alloc(m.tp_size * R * N * 2)
+        K.gemm_rs(a, w, w_mn, pool.table(P), ldc=N, rows_per_owner=R, slot_off=pool.me * R * N)
+        pool.barrier()
+        return pool.view(P, (m.tp_size * R, N)), m.tp_size, R * N, P
+    y = K.matmul_nn(a, w) if w_mn else K.linear(a, w)
+    return _combine_rows(y, m), 1, 0, None
+
+
+def _gather_grad(dy2, r, mean, rstd, m: LayerMeta, site: int):
+    """Backward of the sub-layer epilogue on own rows; the branch gradient is gathered for the
+    column/row-parallel GEMMs.  Returns (dr, dbranch_full, dgamma, dbeta, region)."""
+    gamma = m_gamma = None
+    R, H = dy2.shape
+    kw = dict(p=m.p_hidden, seed=m.seed, layer=m.layer_id, site=site, row_offset=m.row_offset,
+              want_dr=m.post_ln, want_dbias=False)
+    if _peer(m):
+        pool = get_pool()
+        G = pool.alloc(m.tp_size * R * H * 2)
+        dr, _, dgw, dgb, _ = ops.ln_bwd(dy2, r, mean, rstd, m._post_w, out_peers=pool.table(G),
+                                        peer_off=pool.me * R * H, **kw)
+        pool.barrier()
+        return dr, pool.view(G, (m.tp_size * R, H)), dgw, dgb, G
+    dr, d, dgw, dgb, _ = ops.ln_bwd(dy2, r, mean, rstd, m._post_w, **kw)
+    return dr, _gather_rows(d, m), dgw, dgb, None
+
+
+def _input_grad(dhx, ns, st, dr, x2, pre_w, mu1, rs1, m: LayerMeta, R: int, H: int):
+    """dx = [pre-LN backward](sum of dh slots) + residual gradient dr."""
+    if m.pre_ln:
+        dx, _, dgw, dgb, _ = ops.ln_bwd(dhx, x2, mu1, rs1, pre_w, dres=dr, want_dbias=False, nslots=ns,
+                                        slot_stride=st, rows=R, cols=H)
+        return dx, dgw, dgb
+    dx, _, _, _ = ops.bdr_ln(dhx, residual=dr, nslots=ns, slot_stride=st, rows=R, cols=H)
+    return dx, None, None
+
+
+def _free(*regions):
+    if any(r is not None for r in regions):
+        pool = get_pool()
+        for r in regions:
+            if r is not None:
+                pool.free(r)
+
+
 # ---------------------------------------------------------------------------
 # attention sub-layer
 # ---------------------------------------------------------------------------
@@ -202,13 +287,10 @@ class AttentionFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, wqkv, bqkv, wo, bo, pre_w, pre_b, post_w, post_b, mask_add, m: LayerMeta):
         b, s, H = x.shape
-        x2 = x.reshape(b * s, H)
-        if m.pre_ln:
-            h, mu1, rs1 = _ln_in(x2, pre_w, pre_b, m)
-        else:
-            h, mu1, rs1 = x2, None, None
-        hf = _gather_rows(h, m)  # [B*s, H], B = T*b when row-sharded
-        B = hf.shape[0] // s
+        R = b * s
+        x2 = x.reshape(R, H)
+        hf, mu1, rs1, G = _gather_in(x2, m, (pre_w, pre_b) if m.pre_ln else None)
+        B = hf.shape[0] // s  # T*b samples when row-sharded
         qkv = K.linear(hf, wqkv, bqkv)
         fused = use_flash(s, m.head_dim)
         if fused:
@@ -218,11 +300,16 @@ class AttentionFn(torch.autograd.Function):
             P, Pd = lse, None
         else:
             ctxv, P, Pd = attn_core_fwd(qkv, B, s, m, mask_add)
-        o = _combine_rows(K.linear(ctxv, wo), m)  # own rows (RS) or replicated (AR)
-        r, y, mu2, rs2 = ops.bdr_ln(o, bias=bo, residual=x2, gamma=post_w if m.post_ln else None,
+        ox, ns, st, PR = _rs_out(ctxv, wo, False, m, R, H)
+        r, y, mu2, rs2 = ops.bdr_ln(ox, bias=bo, residual=x2, gamma=post_w if m.post_ln else None,
                                     beta=post_b if m.post_ln else None, eps=m.eps, p=m.p_hidden, seed=m.seed,
-                                    layer=m.layer_id, site=SITE_ATTN_OUT, row_offset=m.row_offset)
-        ctx.m, ctx.shape, ctx.fused, ctx.B = m, (b, s, H), fused, B
+                                    layer=m.layer_id, site=SITE_ATTN_OUT, row_offset=m.row_offset, nslots=ns,
+                                    slot_stride=st, rows=R, cols=H)
+        _free(PR)
+        if not any(ctx.needs_input_grad):
+            _free(G)
+            G = None
+        ctx.m, ctx.shape, ctx.fused, ctx.B, ctx.G = m, (b, s, H), fused, B, G
         ctx.save_for_backward(x2, hf, mu1, rs1, qkv, P, Pd if Pd is not P else None, ctxv, r, mu2, rs2, wqkv, wo,
                               pre_w, post_w, mask_add)
         out = y if m.post_ln else r
@@ -232,18 +319,15 @@ class AttentionFn(torch.autograd.Function):
     def backward(ctx, dy):
         m: LayerMeta = ctx.m
         b, s, H = ctx.shape
-        B = ctx.B
+        R, B = b * s, ctx.B
         x2, hf, mu1, rs1, qkv, P, Pd, ctxv, r, mu2, rs2, wqkv, wo, pre_w, post_w, mask_add = ctx.saved_tensors
         if Pd is None:
             Pd = P
-        dy2 = dy.reshape(b * s, H).contiguous()
-        # residual / post-LN / hidden dropout backward (own rows)
-        dr, do, dpost_w, dpost_b, _ = ops.ln_bwd(dy2, r, mu2, rs2, post_w if m.post_ln else None, p=m.p_hidden,
-                                                 seed=m.seed, layer=m.layer_id, site=SITE_ATTN_OUT,
-                                                 row_offset=m.row_offset, want_dr=m.post_ln, want_dbias=False)
+        dy2 = dy.reshape(R, H).contiguous()
+        m._post_w = post_w if m.post_ln else None
+        dr, dof, dpost_w, dpost_b, G2 = _gather_grad(dy2, r, mu2, rs2, m, SITE_ATTN_OUT)
         if not m.post_ln:
             dr = dy2
-        dof = _gather_rows(do, m)
         dbo = ops.colsum(dof)  # over all rows of the group: complete on every rank
         dwo = K.matmul_tn(dof, ctxv)
         dctx = K.matmul_nn(dof, wo)
@@ -260,8 +344,10 @@ class AttentionFn(torch.autograd.Function):
             dx = K.matmul_nn(dqkv, wqkv, epi=K.EPI_ADD, aux=dr)
             dpre_w = dpre_b = None
         else:
-            dh = _combine_rows(K.matmul_nn(dqkv, wqkv), m)
-            dx, dpre_w, dpre_b = _residual_bwd_out(dh, dr, x2, pre_w, mu1, rs1, m)
+            dhx, ns, st, PR = _rs_out(dqkv, wqkv, True, m, R, H)
+            dx, dpre_w, dpre_b = _input_grad(dhx, ns, st, dr, x2, pre_w, mu1, rs1, m, R, H)
+            _free(PR)
+        _free(G2, ctx.G)
         dpost_w, dpost_b, dpre_w, dpre_b = _sync_replicated([dpost_w, dpost_b, dpre_w, dpre_b], m)
         return (dx.view(b, s, H), dwqkv, dbqkv, dwo, dbo, dpre_w, dpre_b, dpost_w, dpost_b, None, None)
 
@@ -274,18 +360,20 @@ class MlpFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w1, b1, w2, b2, pre_w, pre_b, post_w, post_b, m: LayerMeta):
         b, s, H = x.shape
-        x2 = x.reshape(b * s, H)
-        if m.pre_ln:
-            h, mu1, rs1 = _ln_in(x2, pre_w, pre_b, m)
-        else:
-            h, mu1, rs1 = x2, None, None
-        hf = _gather_rows(h, m)
+        R = b * s
+        x2 = x.reshape(R, H)
+        hf, mu1, rs1, G = _gather_in(x2, m, (pre_w, pre_b) if m.pre_ln else None)
         f, z = K.linear(hf, w1, b1, act=m.activation)
-        g = _combine_rows(K.linear(f, w2), m)
-        r, y, mu2, rs2 = ops.bdr_ln(g, bias=b2, residual=x2, gamma=post_w if m.post_ln else None,
+        gx, ns, st, PR = _rs_out(f, w2, False, m, R, H)
+        r, y, mu2, rs2 = ops.bdr_ln(gx, bias=b2, residual=x2, gamma=post_w if m.post_ln else None,
                                     beta=post_b if m.post_ln else None, eps=m.eps, p=m.p_hidden, seed=m.seed,
-                                    layer=m.layer_id, site=SITE_MLP_OUT, row_offset=m.row_offset)
-        ctx.m, ctx.shape = m, (b, s, H)
+                                    layer=m.layer_id, site=SITE_MLP_OUT, row_offset=m.row_offset, nslots=ns,
+                                    slot_stride=st, rows=R, cols=H)
+        _free(PR)
+        if not any(ctx.needs_input_grad):
+            _free(G)
+            G = None
+        ctx.m, ctx.shape, ctx.G = m, (b, s, H), G
         ctx.save_for_backward(x2, hf, mu1, rs1, f, z, r, mu2, rs2, w1, w2, pre_w, post_w)
         out = y if m.post_ln else r
         return out.view(b, s, H)
@@ -294,14 +382,13 @@ class MlpFn(torch.autograd.Function):
     def backward(ctx, dy):
         m: LayerMeta = ctx.m
         b, s, H = ctx.shape
+        R = b * s
         x2, hf, mu1, rs1, f, z, r, mu2, rs2, w1, w2, pre_w, post_w = ctx.saved_tensors
-        dy2 = dy.reshape(b * s, H).contiguous()
-        dr, dg, dpost_w, dpost_b, _ = ops.ln_bwd(dy2, r, mu2, rs2, post_w if m.post_ln else None, p=m.p_hidden,
-                                                 seed=m.seed, layer=m.layer_id, site=SITE_MLP_OUT,
-                                                 row_offset=m.row_offset, want_dr=m.post_ln, want_dbias=False)
+        dy2 = dy.reshape(R, H).contiguous()
+        m._post_w = post_w if m.post_ln else None
+        dr, dgf, dpost_w, dpost_b, G2 = _gather_grad(dy2, r, mu2, rs2, m, SITE_MLP_OUT)
         if not m.post_ln:
             dr = dy2
-        dgf = _gather_rows(dg, m)
         db2 = ops.colsum(dgf)
         dw2 = K.matmul_tn(dgf, f)
         dz = K.matmul_nn(dgf, w2, epi=K.EPI_DACT, act=m.activation, aux=z)
@@ -311,7 +398,9 @@ class MlpFn(torch.autograd.Function):
             dx = K.matmul_nn(dz, w1, epi=K.EPI_ADD, aux=dr)
             dpre_w = dpre_b = None
         else:
-            dh = _combine_rows(K.matmul_nn(dz, w1), m)
-            dx, dpre_w, dpre_b = _residual_bwd_out(dh, dr, x2, pre_w, mu1, rs1, m)
+            dhx, ns, st, PR = _rs_out(dz, w1, True, m, R, H)
+            dx, dpre_w, dpre_b = _input_grad(dhx, ns, st, dr, x2, pre_w, mu1, rs1, m, R, H)
+            _free(PR)
+        _free(G2, ctx.G)
         dpost_w, dpost_b, dpre_w, dpre_b = _sync_replicated([dpost_w, dpost_b, dpre_w, dpre_b], m)
         return (dx.view(b, s, H), dw1, db1, dw2, db2, dpre_w, dpre_b, dpost_w, dpost_b, None)

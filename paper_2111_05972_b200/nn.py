@@ -173,7 +173,8 @@ class _LayerBase(DistributedModule):
                            causal=self.causal_mask_size is not None, pre_ln=self.pre_layernorm,
                            post_ln=self.post_layernorm, activation=self.activation, layer_id=self.layer_id,
                            seed=STATE.seed + 0x9E3779B97F4A7C15 * STATE.step, head_offset=STATE.tp_rank * hl,
-                           sample_offset=sample_offset, tp_size=T, row_offset=row_offset, shard_rows=shard)
+                           sample_offset=sample_offset, tp_size=T, row_offset=row_offset, shard_rows=shard,
+                           comm=STATE.config.get("tp_comm", "peer"))
 
     def _ln_params(self, prefix):
         H = self.hidden_size

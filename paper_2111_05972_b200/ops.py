@@ -18,19 +18,25 @@ def _f32(t):
 
 
 def bdr_ln(x: torch.Tensor, *, bias=None, residual=None, gamma=None, beta=None, eps=1e-5, p=0.0, seed=0,
-           layer=0, site=SITE_ATTN_OUT, row_offset=0, want_r=True):
-    """r = residual + dropout(x + bias); y = LN(r). Returns (r, y, mean, rstd) (None where not computed)."""
+           layer=0, site=SITE_ATTN_OUT, row_offset=0, want_r=True, want_y=True, nslots=1, slot_stride=0,
+           out_peers=None, peer_off=0, rows=None, cols=None):
+    """r = residual + dropout(x + bias); y = LN(r). Returns (r, y, mean, rstd) (None where not computed).
+
+    nslots > 1: x is the ascending-rank sum of nslots partial slots slot_stride elements apart
+    (reduce-scatter consumer); out_peers (device table of peer addresses): the output is also
+    stored to every peer at element offset peer_off (allgather producer)."""
     _check_cuda(x, bias, residual, gamma, beta)
-    M, H = x.shape
-    r = torch.empty_like(x) if want_r else None
+    M, H = (rows, cols) if rows is not None else x.shape
+    r = torch.empty(M, H, dtype=torch.bfloat16, device=x.device) if want_r else None
     y = mean = rstd = None
     if gamma is not None:
-        y = torch.empty_like(x)
+        y = torch.empty(M, H, dtype=torch.bfloat16, device=x.device) if want_y else None
         mean = torch.empty(M, dtype=torch.float32, device=x.device)
         rstd = torch.empty(M, dtype=torch.float32, device=x.device)
-    _lib.call("smpk_bdr_ln_fwd", _ptr(x), _ptr(bias), _ptr(residual), _ptr(r), _ptr(gamma), _ptr(beta), _ptr(y),
-              _ptr(mean), _ptr(rstd), M, H, float(eps), float(p), int(seed) & (2 ** 64 - 1), int(layer), int(site),
-              int(row_offset), _stream())
+    npeers = 0 if out_peers is None else out_peers.numel()
+    _lib.call("smpk_bdr_ln_fwd_ex", _ptr(x), int(nslots), int(slot_stride), _ptr(bias), _ptr(residual), _ptr(r),
+              _ptr(gamma), _ptr(beta), _ptr(y), _ptr(mean), _ptr(rstd), _ptr(out_peers), npeers, int(peer_off), M, H,
+              float(eps), float(p), int(seed) & (2 ** 64 - 1), int(layer), int(site), int(row_offset), _stream())
     return r, y, mean, rstd
 
 
@@ -46,25 +52,30 @@ def add(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
 
 
 def ln_bwd(dy, r, mean, rstd, gamma, *, dres=None, p=0.0, seed=0, layer=0, site=SITE_ATTN_OUT, row_offset=0,
-           want_dgamma=True, want_dbias=True, grads_f32=False, want_dr=True):
+           want_dgamma=True, want_dbias=True, grads_f32=False, want_dr=True, nslots=1, slot_stride=0,
+           out_peers=None, peer_off=0, rows=None, cols=None):
     """Backward of bdr_ln. Returns (dr, dsub, dgamma, dbeta, dbias); dsub is dr when p == 0.
 
-    gamma None = no-LayerNorm mode (d = dy + dres)."""
+    gamma None = no-LayerNorm mode (d = dy + dres).  nslots / out_peers as in bdr_ln (dy read as a
+    slot sum; dsub also stored to every peer)."""
     _check_cuda(dy, r, gamma, dres)
-    M, H = dy.shape
-    dr = torch.empty_like(dy) if want_dr else None
-    dsub = torch.empty_like(dy) if p > 0 else None
-    gdt = torch.float32 if grads_f32 else dy.dtype
-    dgamma = torch.empty(H, dtype=gdt, device=dy.device) if (want_dgamma and gamma is not None) else None
-    dbeta = torch.empty(H, dtype=gdt, device=dy.device) if (want_dgamma and gamma is not None) else None
-    dbias = torch.empty(H, dtype=gdt, device=dy.device) if want_dbias else None
+    M, H = (rows, cols) if rows is not None else dy.shape
+    dev = dy.device
+    dr = torch.empty(M, H, dtype=torch.bfloat16, device=dev) if want_dr else None
+    dsub = torch.empty(M, H, dtype=torch.bfloat16, device=dev) if p > 0 else None
+    gdt = torch.float32 if grads_f32 else torch.bfloat16
+    dgamma = torch.empty(H, dtype=gdt, device=dev) if (want_dgamma and gamma is not None) else None
+    dbeta = torch.empty(H, dtype=gdt, device=dev) if (want_dgamma and gamma is not None) else None
+    dbias = torch.empty(H, dtype=gdt, device=dev) if want_dbias else None
     ws_bytes = _lib.size("smpk_ln_bwd_workspace", M, H)
-    ws = torch.empty(max(ws_bytes, 4) // 4, dtype=torch.float32, device=dy.device)
-    _lib.call("smpk_ln_bwd", _ptr(dy), _ptr(r), _ptr(mean), _ptr(rstd), _ptr(gamma), _ptr(dres), _ptr(dr),
-              _ptr(dsub), _ptr(dgamma), _ptr(dbeta), _ptr(dbias), int(grads_f32), 0, M, H, float(p),
-              int(seed) & (2 ** 64 - 1), int(layer), int(site), int(row_offset), _ptr(ws), int(ws_bytes), _stream())
+    ws = torch.empty(max(ws_bytes, 4) // 4, dtype=torch.float32, device=dev)
+    npeers = 0 if out_peers is None else out_peers.numel()
+    _lib.call("smpk_ln_bwd_ex", _ptr(dy), int(nslots), int(slot_stride), _ptr(r), _ptr(mean), _ptr(rstd),
+              _ptr(gamma), _ptr(dres), _ptr(dr), _ptr(dsub), _ptr(out_peers), npeers, int(peer_off), _ptr(dgamma),
+              _ptr(dbeta), _ptr(dbias), int(grads_f32), 0, M, H, float(p), int(seed) & (2 ** 64 - 1), int(layer),
+              int(site), int(row_offset), _ptr(ws), int(ws_bytes), _stream())
     if dsub is None:
-        dsub = dr if dr is not None else dy
+        dsub = dr if dr is not None else (dy if nslots == 1 else None)
     return dr, dsub, dgamma, dbeta, dbias
 
 

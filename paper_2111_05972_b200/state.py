@@ -31,6 +31,8 @@ DEFAULTS = {
     "activation_loading_horizon": 4,
     "seed": 0,
     "ddp": True,
+    "tp_comm": "peer",  # fused NVLink peer-store collectives ("nccl": torch.distributed calls)
+    "symm_pool_bytes": 4 << 30,
 }
 
 
@@ -113,6 +115,10 @@ def init(config: dict | None = None, *, backend: str | None = None) -> State:
     tp, pp = int(cfg["tensor_parallel_degree"]), int(cfg["pipeline_parallel_degree"])
     topo = build_topology(world, pp, tp, cfg["placement_strategy"], bool(cfg["_prescaled_batch"]))
     st = STATE
+    old_pool = getattr(st, "_pool", None)
+    if old_pool is not None:
+        old_pool.close()
+    st._pool = None
     st.config, st.rank, st.world_size, st.local_rank, st.topology = cfg, rank, world, local, topo
     st.tp_group = st.pp_group = st.rdp_group = None
     st.tp_group_ranks, st.pp_group_ranks = topo.tp_group(rank), topo.pp_group(rank)
@@ -130,7 +136,28 @@ def init(config: dict | None = None, *, backend: str | None = None) -> State:
 
 def reset() -> None:
     global STATE
+    pool = getattr(STATE, "_pool", None)
+    if pool is not None:
+        pool.close()
     STATE.__init__()
+    STATE._pool = None
+
+
+def tp_comm() -> str:
+    """'peer' (fused NVLink peer-store collectives over the symmetric pool) or 'nccl'."""
+    return STATE.config.get("tp_comm", "peer")
+
+
+def get_pool():
+    """The TP group's symmetric peer-mapped pool (created collectively on first use)."""
+    pool = getattr(STATE, "_pool", None)
+    if pool is None:
+        from .symm import SymmPool
+        cap = int(STATE.config.get("symm_pool_bytes", 4 << 30))
+        ranks = STATE.tp_group_ranks
+        pool = SymmPool(cap, STATE.tp_group, ranks, ranks.index(STATE.rank))
+        STATE._pool = pool
+    return pool
 
 
 def next_layer_id() -> int:

@@ -1,0 +1,116 @@
+"""Symmetric peer-mapped memory pool of a TP group (csrc/symm.cu).
+
+Each rank allocates one pool (torch allocation) and one flag block, exports CUDA IPC handles
+once, and maps every peer's pool — the persistent pre-registered buffers of the paper's D2D
+backend, reused here for the tensor-parallel collectives.  Regions are handed
+out by a LIFO bump allocator: every rank executes the same sequence of allocations (SPMD),
+so the same offset is valid in every peer's pool.  Forward regions that back saved tensors
+are released by the backward (reverse order), transient ones right after use.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+
+ALIGN = 1024
+
+
+class SymmPool:
+    def __init__(self, capacity_bytes: int, group, ranks: list, my_index: int, timeout_s: float = 30.0):
+        self.T, self.me, self.timeout_s = len(ranks), my_index, timeout_s
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.buf = torch.empty(capacity_bytes, dtype=torch.uint8, device=dev)
+        self.flags = torch.zeros(64, dtype=torch.int32, device=dev)
+        self.capacity = capacity_bytes
+        mine = (self._export(self.buf), self._export(self.flags))
+        gathered = [None] * self.T
+        dist.all_gather_object(gathered, mine, group=group)
+        self._mapped = []
+        bases, flag_bases = [], []
+        for j, ((hb, ob), (hf, of)) in enumerate(gathered):
+            if j == self.me:
+                bases.append(self.buf.data_ptr())
+                flag_bases.append(self.flags.data_ptr())
+                continue
+            pb, pf = self._import(hb), self._import(hf)
+            self._mapped += [pb, pf]
+            bases.append(pb + ob)
+            flag_bases.append(pf + of)
+        self.bases = bases
+        self.flag_table = torch.tensor(flag_bases, dtype=torch.int64, device=dev)
+        self._tables: dict = {}
+        self.epoch = 0
+        self.top = 0
+        self.regions: list = []  # [offset, size, live, epoch at release]
+
+    @staticmethod
+    def _export(t: torch.Tensor):
+        h = C.create_string_buffer(64)
+        off = C.c_int64()
+        _lib.call("smpk_symm_export", t.data_ptr(), h, C.byref(off))
+        return h.raw, off.value
+
+    @staticmethod
+    def _import(handle: bytes) -> int:
+        p = C.c_void_p()
+        _lib.call("smpk_p2p_import", C.create_string_buffer(handle, 64), C.byref(p))
+        return p.value
+
+    # -- allocation (identical sequence on every rank) -------------------------------
+    def alloc(self, nbytes: int) -> int:
+        # A freed region becomes reusable only once a barrier has been issued after its release:
+        # peers write into a region only after a barrier, and every rank passes a barrier only
+        # after the previous readers of that region (on every rank) have finished.
+        while self.regions and not self.regions[-1][2] and self.regions[-1][3] != self.epoch:
+            self.regions.pop()
+        self.top = (self.regions[-1][0] + self.regions[-1][1]) if self.regions else 0
+        off = (self.top + ALIGN - 1) // ALIGN * ALIGN
+        if off + nbytes > self.capacity:
+            raise RuntimeError(f"symmetric pool exhausted: need {off + nbytes} B of {self.capacity} B "
+                               f"(raise smp config 'symm_pool_bytes')")
+        self.top = off + nbytes
+        self.regions.append([off, nbytes, True, -1])
+        return off
+
+    def free(self, off: int) -> None:
+        for r in reversed(self.regions):
+            if r[0] == off and r[2]:
+                r[2] = False
+                r[3] = self.epoch  # released under this epoch; reusable after the next barrier
+                return
+        raise RuntimeError(f"symmetric pool: free of unknown region {off}")
+
+    def table(self, off: int) -> torch.Tensor:
+        """Device array of the T peer addresses of region offset `off` (cached; built outside capture)."""
+        t = self._tables.get(off)
+        if t is None:
+            t = torch.tensor([b + off for b in self.bases], dtype=torch.int64,
+                             device=self.buf.device)
+            self._tables[off] = t
+        return t
+
+    def view(self, off: int, shape, dtype=torch.bfloat16) -> torch.Tensor:
+        n = 1
+        for s in shape:
+            n *= s
+        nbytes = n * torch.tensor([], dtype=dtype).element_size()
+        return self.buf[off:off + nbytes].view(dtype).view(*shape)
+
+    def barrier(self) -> None:
+        self.epoch = (self.epoch + 1) & 0x7FFFFFFF
+        _lib.call("smpk_symm_barrier", self.flag_table.data_ptr(), self.flags.data_ptr(), self.T, self.me,
+                  self.epoch, float(self.timeout_s), torch.cuda.current_stream().cuda_stream)
+
+    def check(self) -> None:
+        peer = _lib.lib().smpk_symm_timeout_peer()
+        if peer:
+            raise RuntimeError(f"symmetric-memory barrier timed out waiting for TP peer {peer - 1}")
+
+    def close(self) -> None:
+        for p in self._mapped:
+            _lib.call("smpk_p2p_close", p)
+        self._mapped = []

@@ -33,9 +33,10 @@ def gather_cpu(t):
     return [o.cpu() for o in out]
 
 
-def run_case(smp, name, *, prescaled, causal, pre, post, p, layers=1, act="gelu"):
+def run_case(smp, name, *, prescaled, causal, pre, post, p, layers=1, act="gelu", comm="peer"):
     T, rank = dist.get_world_size(), dist.get_rank()
-    smp.init({"tensor_parallel_degree": T, "optimize": "speed", "_prescaled_batch": prescaled, "seed": 11})
+    smp.init({"tensor_parallel_degree": T, "optimize": "speed", "_prescaled_batch": prescaled, "seed": 11,
+              "tp_comm": comm, "symm_pool_bytes": 256 << 20})
     nh, dh, I, s, B = 2 * T, 64, 512 * T, 128, 2
     H = nh * dh
     cfg = tp.LayerConfig(num_attention_heads=nh, attention_head_size=dh, hidden_size=H, intermediate_size=I,
@@ -236,6 +237,9 @@ def main():
         run_case(smp, "prescaled_pre_ln_causal", prescaled=True, causal=True, pre=True, post=False, p=0.0),
         run_case(smp, "tp_across_dp_dropout", prescaled=False, causal=True, pre=True, post=False, p=0.1),
         run_case(smp, "stack2_both_ln", prescaled=False, causal=False, pre=True, post=True, p=0.1, layers=2),
+        run_case(smp, "stack2_nccl_comm", prescaled=False, causal=True, pre=True, post=False, p=0.1, layers=2,
+                 comm="nccl"),
+        run_case(smp, "stack3_peer_post_ln", prescaled=False, causal=False, pre=False, post=True, p=0.1, layers=3),
     ]
     dist.barrier()
     dist.destroy_process_group()
