@@ -203,16 +203,17 @@ def _sync_replicated(grads, m: LayerMeta):
 # with the MMA main loop), and the consuming row kernel sums the T slots in ascending rank
 # order.  One epoch barrier orders each exchange.
 
-def _peer(m: LayerMeta) -> bool:
-    return m.shard_rows and m.comm == "peer"
+def _peer(m: LayerMeta, R: int) -> bool:
+    """Peer-store collectives need whole 128-row GEMM tiles per owner; otherwise NCCL."""
+    return m.shard_rows and m.comm == "peer" and R % 128 == 0
 
 
 def _gather_in(x2, m: LayerMeta, ln=None):
     """Column-parallel GEMM input: [pre-LN](own rows) gathered over the group.
     Returns (hf, mean, rstd, pool region or None)."""
-    if _peer(m):
+    R, H = x2.shape
+    if _peer(m, R):
         pool = get_pool()
-        R, H = x2.shape
         G = pool.alloc(m.tp_size * R * H * 2)
         tbl, off = pool.table(G), pool.me * R * H
         mean = rstd = None
@@ -233,7 +234,7 @@ def _gather_in(x2, m: LayerMeta, ln=None):
 def _rs_out(a, w, w_mn: bool, m: LayerMeta, R: int, N: int):
     """Row-parallel product combined over the group -> (x, nslots, slot_stride, region).
     x is dense (nslots == 1) or the pool's T partial slots of this rank's rows."""
-    if _peer(m):
+    if _peer(m, R):
         pool = get_pool()
         P = pool.alloc(m.tp_size * R * N * 2)
         K.gemm_rs(a, w, w_mn, pool.table(P), ldc=N, rows_per_owner=R, slot_off=pool.me * R * N)
@@ -246,11 +247,10 @@ def _rs_out(a, w, w_mn: bool, m: LayerMeta, R: int, N: int):
 def _gather_grad(dy2, r, mean, rstd, m: LayerMeta, site: int):
     """Backward of the sub-layer epilogue on own rows; the branch gradient is gathered for the
     column/row-parallel GEMMs.  Returns (dr, dbranch_full, dgamma, dbeta, region)."""
-    gamma = m_gamma = None
     R, H = dy2.shape
     kw = dict(p=m.p_hidden, seed=m.seed, layer=m.layer_id, site=site, row_offset=m.row_offset,
               want_dr=m.post_ln, want_dbias=False)
-    if _peer(m):
+    if _peer(m, R):
         pool = get_pool()
         G = pool.alloc(m.tp_size * R * H * 2)
         dr, _, dgw, dgb, _ = ops.ln_bwd(dy2, r, mean, rstd, m._post_w, out_peers=pool.table(G),
