@@ -185,12 +185,35 @@ def max_over_ranks(v: float) -> float:
     return float(t.item())
 
 
+def trace_kernels(run, path_prefix: str, rank: int, steps: int = 2) -> None:
+    """Diagnostics only (never the bench value): CUPTI kernel trace of `steps` steps,
+    aggregated per kernel name, written to <prefix>_rank<r>.txt."""
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(steps):
+            run()
+        torch.cuda.synchronize()
+    agg = {}
+    for ev in prof.events():
+        if ev.device_type != torch.autograd.DeviceType.CUDA:
+            continue
+        a = agg.setdefault(ev.name, [0, 0.0])
+        a[0] += 1
+        a[1] += ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total
+    tot = sum(v[1] for v in agg.values())
+    with open(f"{path_prefix}_rank{rank}.txt", "w") as f:
+        f.write(f"# {steps} steps, total kernel time {tot / steps / 1e3:.3f} ms/step\n")
+        for name, (n, us) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+            f.write(f"{us / steps:10.1f} us/step {n // steps:5d} launches/step  {us / n:8.2f} us/launch  {name[:150]}\n")
+
+
 def run_gpu(args, rank, world, local):
     import paper_2111_05972_b200 as smp
     from paper_2111_05972_b200 import _lib, kernels
 
     torch.cuda.set_device(local)
-    smp.init({"tensor_parallel_degree": world, "optimize": "speed", "seed": 1234})
+    smp.init({"tensor_parallel_degree": world, "optimize": "speed", "seed": 1234, "tp_comm": args.tp_comm})
     torch.manual_seed(1000 + rank)
     model = smp.nn.DistributedTransformer(**CFG)
     model.train()
@@ -255,6 +278,8 @@ def run_gpu(args, rank, world, local):
         gemm_flops, gemm_ms, gemm_launches = gemm_flops * args.steps, gemm_ms * args.steps, gemm_launches * args.steps
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     tokens_step = B * s * world
+    if args.trace:
+        trace_kernels(run, args.trace, rank)
     value = tokens_step / (ms / 1e3)
 
     # -------- e2e through the public API: pinned host input + upstream grad in, loss out
@@ -339,6 +364,9 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--graph", type=int, default=1, help="capture the step in a CUDA graph (1) or run eagerly (0)")
+    ap.add_argument("--tp-comm", default="peer", choices=["peer", "nccl"],
+                    help="TP collectives: fused NVLink peer stores (default) or NCCL calls")
+    ap.add_argument("--trace", default="", help="diagnostics: write a per-kernel CUPTI trace summary to PREFIX_rankR.txt")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

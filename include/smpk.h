@@ -88,6 +88,23 @@ SMPK_API int smpk_gemm(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1
               const void* bias, void* aux, int64_t ldaux, void* stream);
 
 /*
+ * smpk_gemm_ex — smpk_gemm with a split-K workspace.  When the output has too few
+ * 128 x BN tiles to fill the SMs (the weight-gradient GEMMs dW = dY^T X, whose K is the
+ * token count), the K range is split across CTAs; every split stores an fp32 partial
+ * tile into `workspace` and the tile's splits then reduce it in split order
+ * (deterministic) and apply the epilogue.  smpk_gemm_workspace returns the bytes the
+ * chosen split needs (0: no split); a NULL / smaller workspace runs unsplit.
+ */
+SMPK_API int64_t smpk_gemm_workspace(int M, int N, int K, int nb1, int nb2);
+SMPK_API int smpk_gemm_ex(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, int64_t a_bs2,
+                          const void* b, int b_mn_major, int64_t ldb, int64_t b_bs1, int64_t b_bs2,
+                          void* c, int c_f32, int64_t ldc, int64_t c_bs1, int64_t c_bs2,
+                          int M, int N, int K, int nb1, int nb2,
+                          float alpha, float beta, int epilogue, int act,
+                          const void* bias, void* aux, int64_t ldaux, void* workspace, int64_t workspace_bytes,
+                          void* stream);
+
+/*
  * smpk_bdr_ln_fwd — r = residual + dropout(x + bias); y = LayerNorm(r; gamma, beta, eps).
  *
  * The epilogue of every sub-layer of dist_transformer_layer_forward
@@ -215,19 +232,23 @@ SMPK_API int smpk_flash_attn_bwd(const void* qkv, int64_t ld, const void* out, i
  * "partial-sum allreduce fused into the GEMM epilogue through NVLink peer stores" of the
  * north_star, in the reduce-scatter + allgather form used with row-sharded activations
  * (fwd_allreduce_for_tp / reduce_scatter_for_tp / fused_allgather_for_tp).
- *   smpk_gemm_rs        C = A B^T with row r stored to c_peers[r / rows_per_owner] + peer_slot_off
- *                       + (r % rows_per_owner) * ldc (the owner's partial slot for this rank)
+ *   smpk_gemm_rs        C = A B^T with row r stored (TMA bulk stores over NVLink) to
+ *                       peers[r / rows_per_owner] + peer_slot_off; peers is a HOST array of the
+ *                       npeers peer-mapped base addresses, M = npeers * rows_per_owner;
+ *                       row r lands at element (r % rows_per_owner) * ldc of the owner's slot
  *   smpk_bdr_ln_fwd_ex  smpk_bdr_ln_fwd reading x as the ascending-rank sum of nslots partial slots
  *                       (slot_stride elements apart) and storing its output to every out_peers[j]
  *                       + peer_off (allgather producer)
  *   smpk_ln_bwd_ex      smpk_ln_bwd with the same slot-sum input / peer-store output for dy / dsub
  *   smpk_symm_export    IPC handle + offset of a pointer inside its allocation
- *   smpk_symm_barrier   epoch barrier over the group (system-scope release/acquire flag words),
- *                       times out after timeout_s; smpk_symm_timeout_peer reports 1 + the stuck peer
+ *   smpk_symm_barrier   epoch barrier over the group (system-scope release/acquire flag words);
+ *                       the epoch counter is device-resident (local_flags[32]) so a barrier
+ *                       captured in a CUDA graph advances on every replay; times out after
+ *                       timeout_s; smpk_symm_timeout_peer reports 1 + the stuck peer
  */
 SMPK_API int smpk_gemm_rs(const void* a, int a_mn_major, int64_t lda, const void* b, int b_mn_major, int64_t ldb,
-                          void* const* c_peers, int64_t ldc, int64_t rows_per_owner, int64_t peer_slot_off, int M,
-                          int N, int K, void* stream);
+                          void* const* peers, int npeers, int64_t ldc, int64_t rows_per_owner,
+                          int64_t peer_slot_off, int M, int N, int K, void* stream);
 SMPK_API int smpk_bdr_ln_fwd_ex(const void* x, int nslots, int64_t slot_stride, const void* bias, const void* residual,
                                 void* r_out, const void* gamma, const void* beta, void* y_out, float* mean,
                                 float* rstd, void* const* out_peers, int npeers, int64_t peer_off, int M, int H,
@@ -240,8 +261,8 @@ SMPK_API int smpk_ln_bwd_ex(const void* dy, int nslots, int64_t slot_stride, con
                             int layer, int site, int64_t row_offset, void* workspace, int64_t workspace_bytes,
                             void* stream);
 SMPK_API int smpk_symm_export(void* ptr, void* handle_out, int64_t* offset);
-SMPK_API int smpk_symm_barrier(void* const* peer_flags, const void* local_flags, int T, int rank, uint32_t epoch,
-                               double timeout_s, void* stream);
+SMPK_API int smpk_symm_barrier(void* const* peer_flags, void* local_flags, int T, int rank, double timeout_s,
+                               void* stream);
 SMPK_API int smpk_symm_timeout_peer(void);
 
 /*

@@ -27,6 +27,7 @@ SIGNATURES: dict[str, list] = {
     "smpk_version": [],
     "smpk_device_info": [C.POINTER(I), C.POINTER(I), C.POINTER(I)],
     "smpk_gemm": [P, I, L, L, L, P, I, L, L, L, P, I, L, L, L, I, I, I, I, I, F, F, I, I, P, P, L, P],
+    "smpk_gemm_ex": [P, I, L, L, L, P, I, L, L, L, P, I, L, L, L, I, I, I, I, I, F, F, I, I, P, P, L, P, L, P],
     "smpk_bdr_ln_fwd": [P, P, P, P, P, P, P, P, P, I, I, F, F, C.c_uint64, I, I, L, P],
     "smpk_ln_bwd": [P, P, P, P, P, P, P, P, P, P, P, I, I, I, I, F, C.c_uint64, I, I, L, P, L, P],
     "smpk_softmax_fwd": [P, P, P, P, I, I, I, I, F, I, F, C.c_uint64, I, L, I, I, P],
@@ -39,11 +40,11 @@ SIGNATURES: dict[str, list] = {
     "smpk_vocab_ce_bwd": [P, L, L, I, L, L, P, L, P, P, F, P, L, P],
     "smpk_flash_attn_fwd": [P, L, I, I, I, I, P, L, P, P, F, I, F, C.c_uint64, I, L, I, I, P],
     "smpk_flash_attn_bwd": [P, L, P, L, P, L, P, I, I, I, I, P, P, F, I, F, C.c_uint64, I, L, I, I, P, L, P],
-    "smpk_gemm_rs": [P, I, L, P, I, L, P, L, L, L, I, I, I, P],
+    "smpk_gemm_rs": [P, I, L, P, I, L, P, I, L, L, L, I, I, I, P],
     "smpk_bdr_ln_fwd_ex": [P, I, L, P, P, P, P, P, P, P, P, P, I, L, I, I, F, F, C.c_uint64, I, I, L, P],
     "smpk_ln_bwd_ex": [P, I, L, P, P, P, P, P, P, P, P, I, L, P, P, P, I, I, I, I, F, C.c_uint64, I, I, L, P, L, P],
     "smpk_symm_export": [P, P, C.POINTER(L)],
-    "smpk_symm_barrier": [P, P, I, I, C.c_uint32, C.c_double, P],
+    "smpk_symm_barrier": [P, P, I, I, C.c_double, P],
     "smpk_symm_timeout_peer": [],
     "smpk_p2p_alloc": [L, C.POINTER(P)],
     "smpk_p2p_free": [P],
@@ -58,6 +59,7 @@ SIGNATURES: dict[str, list] = {
 SIZE_FUNCS: dict[str, list] = {
     "smpk_ln_bwd_workspace": [I, I],
     "smpk_colsum_workspace": [I, I],
+    "smpk_gemm_workspace": [I, I, I, I, I],
     "smpk_flash_attn_bwd_workspace": [I, I, I, I],
 }
 

@@ -132,6 +132,66 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// ---- CTA pair (cta_group::2): two CTAs of a cluster on one TPC share one M=256 MMA ----
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// TMA load issued by either CTA of the pair; the transaction bytes complete on the LEADER's
+// (rank 0) barrier at the same shared offset (clearing the peer bit of the cluster address).
+__device__ __forceinline__ void tma_load_4d_pair(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                 int c2, int c3) {
+  const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(mbar)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* slot, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// completion of the pair's prior MMAs arrives on the barrier at this offset in every CTA of mask
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+// arrive (release, cluster scope) on the barrier at this offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
 // 32 lanes x 32 consecutive fp32 columns: thread t receives lane (base_lane + t).
 __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -165,6 +225,23 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 // make generic-proxy shared-memory writes visible to the async proxy (tcgen05.mma / TMA)
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// true in exactly one lane of the (converged) warp
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .b32 rx;\n\t.reg .pred px;\n\t"
+      "elect.sync rx|px, 0xffffffff;\n\t"
+      "@px mov.s32 %0, 1;\n\t}"
+      : "+r"(pred));
+  return pred != 0;
+}
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
 __device__ __forceinline__ void named_barrier_sync(int id, int nthreads) {
@@ -235,26 +312,35 @@ __device__ __forceinline__ float tanh_approx(float x) {
   return y;
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // Standard normal CDF Phi(z) = 0.5 (1 + erf(z/sqrt2)) with erf from Abramowitz & Stegun
-// 7.1.26 (|err| <= 1.5e-7): two MUFU ops (rcp, ex2) instead of libdevice erff + expf.
-// Also returns e = exp(-z^2/2), which the GeLU derivative reuses for the density.
+// 7.1.26 (|err| <= 1.5e-7) written for the epilogue issue budget: one rcp.approx and one
+// ex2.approx (no range fix-ups), the 1/sqrt2, log2(e) and the final 1/2 folded into the
+// constants.  With x = |z|/sqrt2:  t = 1/(1 + p x),  q = 0.5 poly(t) exp(-x^2),
+// Phi = 1 - q (z >= 0) or q (z < 0).  Also returns e = exp(-z^2/2) for the density.
 __device__ __forceinline__ float normal_cdf(float z, float& e) {
-  const float x = fabsf(z) * 0.7071067811865476f;
-  const float t = __fdividef(1.f, fmaf(0.3275911f, x, 1.f));
-  e = __expf(-x * x);
-  const float poly =
-      t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f), -0.284496736f), 0.254829592f);
-  const float erf_abs = 1.f - poly * e;
-  return 0.5f + 0.5f * copysignf(erf_abs, z);
+  const float t = rcp_approx(fmaf(fabsf(z), 0.23164188f /* p / sqrt2 */, 1.f));
+  e = ex2_approx((z * -0.72134752f /* -log2(e)/2 */) * z);
+  const float ph =
+      t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 0.5307027145f, -0.7265760135f), 0.7107068705f), -0.142248368f),
+               0.127414796f);  // 0.5 * A&S a1..a5
+  const float q = ph * e;
+  return z >= 0.f ? 1.f - q : q;
 }
 
 // Activation functions. act: SMPK_ACT_GELU_ERF / SMPK_ACT_GELU_TANH / SMPK_ACT_RELU.
 __device__ __forceinline__ float act_fwd(int act, float z) {
   if (act == SMPK_ACT_RELU) return z > 0.f ? z : 0.f;
   if (act == SMPK_ACT_GELU_TANH) {
-    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-    const float u = k0 * fmaf(k1 * z, z * z, z);
-    return 0.5f * z * (1.f + tanh_approx(u));
+    // 0.5 z (1 + tanh(k0 (z + k1 z^3))) with k0 folded: u = z (k0 + k0 k1 z^2)
+    const float u = z * fmaf(z * z, 0.0356774081f, 0.7978845608f);
+    const float hz = 0.5f * z;
+    return fmaf(hz, tanh_approx(u), hz);
   }
   float e;
   return z * normal_cdf(z, e);
@@ -263,10 +349,12 @@ __device__ __forceinline__ float act_fwd(int act, float z) {
 __device__ __forceinline__ float act_bwd(int act, float z) {  // d act / dz
   if (act == SMPK_ACT_RELU) return z > 0.f ? 1.f : 0.f;
   if (act == SMPK_ACT_GELU_TANH) {
-    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-    const float u = k0 * fmaf(k1 * z, z * z, z);
+    const float z2 = z * z;
+    const float u = z * fmaf(z2, 0.0356774081f, 0.7978845608f);
     const float t = tanh_approx(u);
-    return 0.5f * (1.f + t) + 0.5f * z * (1.f - t * t) * k0 * fmaf(3.f * k1, z * z, 1.f);
+    // 0.5 (1 + t) + 0.5 z (1 - t^2) k0 (1 + 3 k1 z^2)
+    const float du = fmaf(z2, 0.1070322243f, 0.7978845608f);  // k0 (1 + 3 k1 z^2)
+    return fmaf(0.5f * z * du, fmaf(-t, t, 1.f), fmaf(0.5f, t, 0.5f));
   }
   float e;
   const float cdf = normal_cdf(z, e);

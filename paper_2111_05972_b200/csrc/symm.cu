@@ -5,8 +5,8 @@
 // GEMM epilogue stores its partial tiles straight into the owning rank's pool
 // (smpk_gemm_rs), the row kernels read the T partial slots in ascending rank order and
 // store allgathered rows into every peer's pool (smpk_bdr_ln_fwd_ex / smpk_ln_bwd_ex), and
-// smpk_symm_barrier orders those NVLink stores between ranks: each rank writes its epoch
-// into every peer's flag word (st.release.sys after a system fence) and waits until all
+// smpk_symm_barrier orders those NVLink stores between ranks: each rank advances its device-resident epoch,
+// writes it into every peer's flag word (st.release.sys after a system fence) and waits until all
 // peers' epochs have arrived (ld.acquire.sys), with a wall-clock timeout that reports the
 // stuck peer instead of hanging.
 #include <mutex>
@@ -17,9 +17,15 @@ namespace smpk {
 
 __device__ unsigned long long g_symm_timeout_peer = 0;  // 1 + peer index that never arrived
 
-__global__ void symm_barrier_kernel(uint32_t* const* peer_flags, const uint32_t* local_flags, int T, int rank,
-                                    uint32_t epoch, unsigned long long timeout_ns) {
+// local_flags[0..31]: epoch last signalled by each peer; local_flags[32]: this rank's epoch
+// counter (device-resident so graph replays advance it; every rank runs the same barrier
+// sequence, so the counters stay in lockstep).
+__global__ void symm_barrier_kernel(uint32_t* const* peer_flags, uint32_t* local_flags, int T, int rank,
+                                    unsigned long long timeout_ns) {
   const int t = threadIdx.x;
+  const uint32_t epoch = *reinterpret_cast<volatile uint32_t*>(local_flags + 32) + 1;
+  __syncwarp();
+  if (t == 0) local_flags[32] = epoch;
   if (t >= T) return;
   __threadfence_system();
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(peer_flags[t] + rank), "r"(epoch) : "memory");
@@ -75,12 +81,12 @@ extern "C" int smpk_symm_export(void* ptr, void* handle_out, int64_t* offset) {
   return SMPK_OK;
 }
 
-extern "C" int smpk_symm_barrier(void* const* peer_flags, const void* local_flags, int T, int rank, uint32_t epoch,
-                                 double timeout_s, void* stream) {
+extern "C" int smpk_symm_barrier(void* const* peer_flags, void* local_flags, int T, int rank, double timeout_s,
+                                 void* stream) {
   SMPK_REQUIRE(peer_flags && local_flags && T > 0 && T <= 32 && rank >= 0 && rank < T, SMPK_ERR_BAD_ARG,
                "smpk_symm_barrier: bad arguments");
   symm_barrier_kernel<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<uint32_t* const*>(peer_flags), reinterpret_cast<const uint32_t*>(local_flags), T, rank, epoch,
+      reinterpret_cast<uint32_t* const*>(peer_flags), reinterpret_cast<uint32_t*>(local_flags), T, rank,
       (unsigned long long)(timeout_s * 1e9));
   return check_launch("smpk_symm_barrier");
 }

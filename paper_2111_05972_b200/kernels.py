@@ -53,23 +53,26 @@ def gemm_raw(a, a_mn, lda, a_bs, b, b_mn, ldb, b_bs, c, ldc, c_bs, M, N, K, nb=(
     if prof is not None:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-    _lib.call("smpk_gemm",
+    # split-K workspace (weight-gradient shapes with few output tiles); 0 bytes = unsplit
+    ws_bytes = _lib.size("smpk_gemm_workspace", int(M), int(N), int(K), int(nb[0]), int(nb[1]))
+    ws = torch.empty(ws_bytes // 4, dtype=torch.float32, device=c.device) if ws_bytes else None
+    _lib.call("smpk_gemm_ex",
               _ptr(a), int(a_mn), int(lda), int(a_bs[0]), int(a_bs[1]),
               _ptr(b), int(b_mn), int(ldb), int(b_bs[0]), int(b_bs[1]),
               _ptr(c), int(c.dtype == torch.float32), int(ldc), int(c_bs[0]), int(c_bs[1]),
               int(M), int(N), int(K), int(nb[0]), int(nb[1]),
               float(alpha), float(beta), int(epi), int(act),
-              _ptr(bias), _ptr(aux), int(ldaux), _stream())
+              _ptr(bias), _ptr(aux), int(ldaux), _ptr(ws), int(ws_bytes), _stream())
     if prof is not None:
         e1.record()
         prof.records.append((e0, e1, 2.0 * M * N * K * nb[0] * nb[1]))
 
 
-def gemm_rs(a: torch.Tensor, b: torch.Tensor, b_mn: bool, c_table: torch.Tensor, *, ldc: int, rows_per_owner: int,
+def gemm_rs(a: torch.Tensor, b: torch.Tensor, b_mn: bool, peers, *, ldc: int, rows_per_owner: int,
             slot_off: int) -> None:
     """Row-parallel product a @ B^T (B [N,K]; b_mn: B given as [K,N]) whose rows are stored straight
-    into the owning ranks' peer-mapped partial slots (c_table: device table of T addresses)."""
-    _check_cuda(a, b, c_table)
+    into the owning ranks' peer-mapped partial slots (peers: ctypes array of the T base addresses)."""
+    _check_cuda(a, b)
     M, Kd = a.shape
     N = b.shape[1] if b_mn else b.shape[0]
     prof = PROFILER
@@ -77,7 +80,7 @@ def gemm_rs(a: torch.Tensor, b: torch.Tensor, b_mn: bool, c_table: torch.Tensor,
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
     _lib.call("smpk_gemm_rs", a.data_ptr(), 0, _rowmajor(a, "a"), b.data_ptr(), int(bool(b_mn)), _rowmajor(b, "b"),
-              c_table.data_ptr(), int(ldc), int(rows_per_owner), int(slot_off), M, N, Kd, _stream())
+              peers, len(peers), int(ldc), int(rows_per_owner), int(slot_off), M, N, Kd, _stream())
     if prof is not None:
         e1.record()
         prof.records.append((e0, e1, 2.0 * M * N * Kd))

@@ -215,7 +215,7 @@ def _gather_in(x2, m: LayerMeta, ln=None):
     if _peer(m, R):
         pool = get_pool()
         G = pool.alloc(m.tp_size * R * H * 2)
-        tbl, off = pool.table(G), pool.me * R * H
+        tbl, off = pool.peers(G, pool.me * R * H)
         mean = rstd = None
         if ln is not None:
             _, _, mean, rstd = ops.bdr_ln(x2, gamma=ln[0], beta=ln[1], eps=m.eps, want_r=False, want_y=False,
@@ -236,10 +236,11 @@ def _rs_out(a, w, w_mn: bool, m: LayerMeta, R: int, N: int):
     x is dense (nslots == 1) or the pool's T partial slots of this rank's rows."""
     if _peer(m, R):
         pool = get_pool()
-        P = pool.alloc(m.tp_size * R * N * 2)
-        K.gemm_rs(a, w, w_mn, pool.table(P), ldc=N, rows_per_owner=R, slot_off=pool.me * R * N)
+        P = pool.scratch("partials", m.tp_size * R * N * 2)
+        peers, off = pool.host_peers(P, pool.me * R * N)
+        K.gemm_rs(a, w, w_mn, peers, ldc=N, rows_per_owner=R, slot_off=off)
         pool.barrier()
-        return pool.view(P, (m.tp_size * R, N)), m.tp_size, R * N, P
+        return pool.view(P, (m.tp_size * R, N)), m.tp_size, R * N, None
     y = K.matmul_nn(a, w) if w_mn else K.linear(a, w)
     return _combine_rows(y, m), 1, 0, None
 
@@ -252,11 +253,11 @@ def _gather_grad(dy2, r, mean, rstd, m: LayerMeta, site: int):
               want_dr=m.post_ln, want_dbias=False)
     if _peer(m, R):
         pool = get_pool()
-        G = pool.alloc(m.tp_size * R * H * 2)
-        dr, _, dgw, dgb, _ = ops.ln_bwd(dy2, r, mean, rstd, m._post_w, out_peers=pool.table(G),
-                                        peer_off=pool.me * R * H, **kw)
+        G = pool.scratch("grad_gather", m.tp_size * R * H * 2)
+        tbl, off = pool.peers(G, pool.me * R * H)
+        dr, _, dgw, dgb, _ = ops.ln_bwd(dy2, r, mean, rstd, m._post_w, out_peers=tbl, peer_off=off, **kw)
         pool.barrier()
-        return dr, pool.view(G, (m.tp_size * R, H)), dgw, dgb, G
+        return dr, pool.view(G, (m.tp_size * R, H)), dgw, dgb, None
     dr, d, dgw, dgb, _ = ops.ln_bwd(dy2, r, mean, rstd, m._post_w, **kw)
     return dr, _gather_rows(d, m), dgw, dgb, None
 

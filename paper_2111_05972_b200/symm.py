@@ -42,10 +42,13 @@ class SymmPool:
             flag_bases.append(pf + of)
         self.bases = bases
         self.flag_table = torch.tensor(flag_bases, dtype=torch.int64, device=dev)
-        self._tables: dict = {}
+        self.base_table = torch.tensor(bases, dtype=torch.int64, device=dev)
+        self.base_array = (C.c_void_p * self.T)(*bases)  # host copy (TMA-store descriptors)
         self.epoch = 0
         self.top = 0
         self.regions: list = []  # [offset, size, live, epoch at release]
+        self._scratch: dict = {}
+        self._scratch_bottom = capacity_bytes
 
     @staticmethod
     def _export(t: torch.Tensor):
@@ -69,8 +72,8 @@ class SymmPool:
             self.regions.pop()
         self.top = (self.regions[-1][0] + self.regions[-1][1]) if self.regions else 0
         off = (self.top + ALIGN - 1) // ALIGN * ALIGN
-        if off + nbytes > self.capacity:
-            raise RuntimeError(f"symmetric pool exhausted: need {off + nbytes} B of {self.capacity} B "
+        if off + nbytes > self._scratch_bottom:
+            raise RuntimeError(f"symmetric pool exhausted: need {off + nbytes} B of {self._scratch_bottom} B "
                                f"(raise smp config 'symm_pool_bytes')")
         self.top = off + nbytes
         self.regions.append([off, nbytes, True, -1])
@@ -84,14 +87,35 @@ class SymmPool:
                 return
         raise RuntimeError(f"symmetric pool: free of unknown region {off}")
 
-    def table(self, off: int) -> torch.Tensor:
-        """Device array of the T peer addresses of region offset `off` (cached; built outside capture)."""
-        t = self._tables.get(off)
-        if t is None:
-            t = torch.tensor([b + off for b in self.bases], dtype=torch.int64,
-                             device=self.buf.device)
-            self._tables[off] = t
-        return t
+    def scratch(self, kind: str, nbytes: int) -> int:
+        """Permanent transient region per (kind, size), carved from the END of the pool.
+
+        Transient exchanges (row-parallel partial slots, backward gathers) alternate with a
+        barrier in between (every reader of one use finishes before any rank passes the barrier
+        that precedes the next use's remote writers), so one region per kind suffices."""
+        key = (kind, nbytes)
+        off = self._scratch.get(key)
+        if off is None:
+            end = self._scratch_bottom - nbytes
+            off = end // ALIGN * ALIGN
+            if off < self.top:
+                raise RuntimeError("symmetric pool exhausted by scratch regions (raise 'symm_pool_bytes')")
+            self._scratch_bottom = off
+            self._scratch[key] = off
+        return off
+
+    def peers(self, off: int, elem_off: int = 0, elem_size: int = 2):
+        """(device table of the T pool bases, element offset of region `off` + elem_off).
+
+        The table is built once at construction, so kernels launched inside a CUDA-graph capture
+        never need a host->device copy; the region offset travels as the kernels' int64 offset."""
+        assert off % elem_size == 0
+        return self.base_table, off // elem_size + elem_off
+
+    def host_peers(self, off: int, elem_off: int = 0, elem_size: int = 2):
+        """(host array of the T pool bases, element offset of region `off` + elem_off)."""
+        assert off % elem_size == 0
+        return self.base_array, off // elem_size + elem_off
 
     def view(self, off: int, shape, dtype=torch.bfloat16) -> torch.Tensor:
         n = 1
@@ -103,7 +127,7 @@ class SymmPool:
     def barrier(self) -> None:
         self.epoch = (self.epoch + 1) & 0x7FFFFFFF
         _lib.call("smpk_symm_barrier", self.flag_table.data_ptr(), self.flags.data_ptr(), self.T, self.me,
-                  self.epoch, float(self.timeout_s), torch.cuda.current_stream().cuda_stream)
+                  float(self.timeout_s), torch.cuda.current_stream().cuda_stream)
 
     def check(self) -> None:
         peer = _lib.lib().smpk_symm_timeout_peer()
