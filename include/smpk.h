@@ -207,12 +207,23 @@ SMPK_API int smpk_vocab_ce_bwd(const void* logits, int64_t ld, int64_t N, int v_
  *   qkv [B*s, ld] with q | k | v blocks of nh*dh columns, head h at column h*dh of each block;
  *   out [B*s, ld_out] (head h at column h*dh) = dropout(softmax(scale*QK^T + mask [+causal])) V;
  *   lse [B, nh, s] = log2-sum-exp2 of the scaled masked scores (for the backward).
- * dh in {64, 128}; s a multiple of 128; dropout bits identical to smpk_softmax_fwd.
+ * dh in {64, 128}; s a multiple of 128.  Dropout (p_drop > 0) zeroes the probabilities whose
+ * keep bit is clear in keep_bits (from smpk_attn_dropout_bits; the same bits smpk_softmax_fwd
+ * draws) and scales the kept ones by 1/(1-p).
  */
 SMPK_API int smpk_flash_attn_fwd(const void* qkv, int64_t ld, int B, int nh, int s, int dh, void* out,
                                  int64_t ld_out, float* lse, const float* mask_add, float scale, int causal,
-                                 float p_drop, uint64_t seed, int layer, int64_t sample_offset, int head_offset,
-                                 int nh_global, void* stream);
+                                 float p_drop, const uint32_t* keep_bits, void* stream);
+
+/*
+ * smpk_attn_dropout_bits — attention-probability dropout keep bits of one TP rank's local
+ * heads: word ((b*nh + h)*sq + q)*(sk/32) + k/32, bit k%32 = keep(q, k) of the Philox4x32-10
+ * stream (site 0, row = ((sample_offset+b)*nh_global + head_offset+h)*sq + q, col = k) that
+ * oracle/philox.py restates.  Generated once per layer and read by the forward and backward.
+ */
+SMPK_API int smpk_attn_dropout_bits(int B, int nh, int sq, int sk, float p_drop, uint64_t seed, int layer,
+                                    int64_t sample_offset, int head_offset, int nh_global, uint32_t* bits,
+                                    void* stream);
 
 /*
  * smpk_flash_attn_bwd — backward of smpk_flash_attn_fwd: from dout (grad of out, same layout),
@@ -223,9 +234,8 @@ SMPK_API int smpk_flash_attn_fwd(const void* qkv, int64_t ld, int B, int nh, int
 SMPK_API int64_t smpk_flash_attn_bwd_workspace(int B, int nh, int s, int dh);
 SMPK_API int smpk_flash_attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const void* dout,
                                  int64_t ld_dout, const float* lse, int B, int nh, int s, int dh, void* dqkv,
-                                 const float* mask_add, float scale, int causal, float p_drop, uint64_t seed,
-                                 int layer, int64_t sample_offset, int head_offset, int nh_global, void* workspace,
-                                 int64_t workspace_bytes, void* stream);
+                                 const float* mask_add, float scale, int causal, float p_drop,
+                                 const uint32_t* keep_bits, void* workspace, int64_t workspace_bytes, void* stream);
 
 /*
  * Fused tensor-parallel collectives over peer-mapped (symmetric) memory — the row-parallel

@@ -1,24 +1,33 @@
-// flash_attn.cu — fused attention forward on tcgen05/TMEM/TMA (sm_100a).
+// flash_attn.cu — fused attention forward on tcgen05/TMEM/TMA (sm_100a), and the
+// attention-dropout keep-bit generator shared by the forward and the backward.
 //
 // The attention core of dist_attention_forward for one TP rank's
 // local heads: softmax(Q K^T / sqrt(dh) + mask [+ causal]) -> dropout -> . V, without
 // materialising the [s, s] score / probability matrices in HBM.
 //
-// CTA = (128-row query tile, local head, sample); 256 threads:
-//   warp 0   TMA producer: Q once, K/V tiles through a 2-stage ring
-//   warp 1   MMA issuer:   S = Q K^T (M=128,N=128) into TMEM; O += P V (M=128,N=dh)
-//   warp 2   TMEM allocator (256 columns: S 128 + O dh)
-//   warps 4-7 softmax: thread = query row (TMEM lane); online max / sum in the exp2
-//            domain, O rescaled in TMEM when the running max grows, dropout from the
-//            Philox stream of oracle/philox.py, P written to smem as the bf16 K-major
-//            A operand of the P.V MMA; final O / l and log-sum-exp stored.
-// Two CTAs share an SM (TMEM 2 x 256 columns), so one CTA's softmax overlaps the
-// other's tensor-core work.
+// CTA = two 128-row query tiles (Q0, Q1) of one (head, sample); 384 threads:
+//   warp 0      TMA producer: Q0/Q1 once, K/V tiles through an NS-stage ring (shared by
+//               both query tiles, so K/V are read once per 256 queries)
+//   warp 1      MMA issuer (whole warp, one elected lane issues):
+//                 S_t = Q_t K_j^T (M=128, N=128) into TMEM;  O_t += P_t V_j (M=128, N=dh)
+//               ping-pong order  PV0_j, S0_{j+1}, PV1_j, S1_{j+1}  so each softmax group
+//               gets its next scores while the other one computes
+//   warp 2      TMEM allocator (512 columns: S0 | S1 | O0 | O1)
+//   warps 4-7   softmax group 0 (query tile Q0), warps 8-11 softmax group 1 (Q1):
+//               thread = query row = TMEM lane; the 128 scores of the row are read once
+//               into registers; online max / sum in the exp2 domain; O rescaled in TMEM
+//               only when some row's running max grew; dropout from precomputed keep bits
+//               (smpk_attn_dropout_bits, the Philox stream of oracle/philox.py); P written to
+//               smem as the swizzled K-major A operand of P.V; 1/(1-p) and 1/l applied once
+//               in the epilogue.
 #include "smpk_common.cuh"
 
 namespace smpk {
 
-constexpr int FA_THREADS = 256;
+int make_tma_4d(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t ld, int nb1, int64_t s1,
+                int nb2, int64_t s2, int box_inner, int box_outer, const char* name);
+
+constexpr int FA_THREADS = 384;
 constexpr int FA_BQ = 128;
 constexpr int FA_BK = 128;
 
@@ -26,86 +35,72 @@ struct FaFwdArgs {
   int B, nh, s;
   bf16* out;
   int64_t ld_out;
-  float* lse;         // [B, nh, s] log2-domain log-sum-exp of the scaled+masked scores
-  const float* mask;  // [B, s] additive, may be null
-  float scale_log2;   // log2(e) / sqrt(dh)
+  float* lse;                // [B, nh, s] log2-domain log-sum-exp of the scaled+masked scores
+  const float* mask;         // [B, s] additive, may be null
+  const uint32_t* keep;      // [B, nh, s, s/32] dropout keep bits (null: no dropout)
+  float scale_log2;          // log2(e) / sqrt(dh)
   int causal;
-  float p, inv_keep;
-  uint32_t thresh;
-  uint64_t seed;
-  uint32_t layer;
-  int64_t sample_offset;
-  int head_offset, nh_global;
+  float inv_keep;
 };
 
 template <int DH>
 struct FaFwdCfg {
+  static constexpr int NS = DH == 64 ? 2 : 1;  // K/V ring depth
   static constexpr int Q_BYTES = FA_BQ * DH * 2;
   static constexpr int K_BYTES = FA_BK * DH * 2;
   static constexpr int V_BYTES = FA_BK * DH * 2;
   static constexpr int P_BYTES = FA_BQ * FA_BK * 2;
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + Q_BYTES;
-  static constexpr int OFF_V = OFF_K + 2 * K_BYTES;
-  static constexpr int OFF_P = OFF_V + 2 * V_BYTES;
-  static constexpr int OFF_BAR = OFF_P + P_BYTES;
+  static constexpr int OFF_Q = 0;                          // Q0, Q1
+  static constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
+  static constexpr int OFF_V = OFF_K + NS * K_BYTES;
+  static constexpr int OFF_P = OFF_V + NS * V_BYTES;       // P0, P1
+  static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
   static constexpr int SMEM = 1024 + OFF_BAR + 256;
-  static constexpr uint32_t TMEM_COLS = 256;  // S: [0,128), O: [128, 128+DH)
+  static constexpr uint32_t TMEM_COLS = 512;  // S0 [0,128) S1 [128,256) O0 [256,256+DH) O1 [256+DH, 256+2DH)
 };
 
-__device__ __forceinline__ void fa_keep128(uint64_t seed, uint32_t layer, uint64_t row, int key0, uint32_t thresh,
-                                           uint32_t (&bits)[4]) {
-  // 128 keep bits (keys key0 .. key0+127) of one probability row, 16 Philox calls
-#pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    uint32_t word = 0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      bool k8[8];
-      dropout_keep8(seed, layer, 0u, row, key0 + w * 32 + c * 8, thresh, k8);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) word |= (k8[e] ? 1u : 0u) << (c * 8 + e);
-    }
-    bits[w] = word;
-  }
-}
-
 template <int DH>
-__global__ void __launch_bounds__(FA_THREADS, (DH == 64 ? 2 : 1))
+__global__ void __launch_bounds__(FA_THREADS, 1)
     flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const FaFwdArgs a) {
   using Cfg = FaFwdCfg<DH>;
+  constexpr int NS = Cfg::NS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
   uint64_t* q_full = bar + 0;
-  uint64_t* kv_full = bar + 1;   // [2]
-  uint64_t* kv_empty = bar + 3;  // [2]
-  uint64_t* s_full = bar + 5;
-  uint64_t* s_free = bar + 6;
-  uint64_t* p_full = bar + 7;
-  uint64_t* o_done = bar + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
+  uint64_t* kv_full = bar + 1;        // [NS]
+  uint64_t* kv_empty = bar + 3;       // [NS]
+  uint64_t* s_full = bar + 5;         // [2]
+  uint64_t* p_full = bar + 7;         // [2]
+  uint64_t* o_done = bar + 9;         // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_qt = (a.s + FA_BQ - 1) / FA_BQ;
-  const int qt = n_qt - 1 - (int)blockIdx.x;  // heavy (causal) tiles first
+  const int n_qt = a.s / FA_BQ;
+  const int n_kv = a.s / FA_BK;
+  const int qt0 = 2 * (int)blockIdx.x;
+  const int nq = min(2, n_qt - qt0);  // query tiles of this CTA
   const int h = blockIdx.y, b = blockIdx.z;
-  const int n_kt = a.causal ? (qt + 1) : (a.s + FA_BK - 1) / FA_BK;
+  // key tiles each query tile needs, and the iteration count of the shared K/V stream
+  const int nkt0 = a.causal ? qt0 + 1 : n_kv;
+  const int nkt1 = nq > 1 ? (a.causal ? qt0 + 2 : n_kv) : 0;
+  const int n_iter = max(nkt0, nkt1);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NS; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(s_free, 128);
-    mbar_init(p_full, 128);
-    mbar_init(o_done, 1);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 4);  // one arrive per softmax warp
+      mbar_init(&o_done[t], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
@@ -113,18 +108,19 @@ __global__ void __launch_bounds__(FA_THREADS, (DH == 64 ? 2 : 1))
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem, tO = tmem + 128;
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
-      mbar_arrive_expect_tx(q_full, Cfg::Q_BYTES);
+      mbar_arrive_expect_tx(q_full, nq * Cfg::Q_BYTES);
+      for (int t = 0; t < nq; ++t)
 #pragma unroll
-      for (int kb = 0; kb < DH / 64; ++kb)
-        tma_load_4d(smem + Cfg::OFF_Q + kb * (FA_BQ * 128), &tmQ, q_full, kb * 64, qt * FA_BQ, h, b);
-      for (int j = 0; j < n_kt; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        for (int kb = 0; kb < DH / 64; ++kb)
+          tma_load_4d(smem + Cfg::OFF_Q + t * Cfg::Q_BYTES + kb * (FA_BQ * 128), &tmQ, q_full, kb * 64,
+                      (qt0 + t) * FA_BQ, h, b);
+      for (int j = 0; j < n_iter; ++j) {
+        const int st = j % NS;
+        mbar_wait(&kv_empty[st], ((j / NS) & 1) ^ 1);
         mbar_arrive_expect_tx(&kv_full[st], Cfg::K_BYTES + Cfg::V_BYTES);
         uint8_t* k_dst = smem + Cfg::OFF_K + st * Cfg::K_BYTES;
         uint8_t* v_dst = smem + Cfg::OFF_V + st * Cfg::V_BYTES;
@@ -140,163 +136,194 @@ __global__ void __launch_bounds__(FA_THREADS, (DH == 64 ? 2 : 1))
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
-      const uint32_t idS = make_idesc_bf16(128, FA_BK, false, false);
-      const uint32_t idO = make_idesc_bf16(128, DH, false, true);
-      const uint32_t q_base = smem_u32(smem + Cfg::OFF_Q);
-      const uint32_t p_base = smem_u32(smem + Cfg::OFF_P);
-      mbar_wait(q_full, 0);
-      for (int j = 0; j <= n_kt; ++j) {
-        if (j < n_kt) {
-          const int st = j & 1;
-          mbar_wait(&kv_full[st], (j >> 1) & 1);
-          if (j > 0) mbar_wait(s_free, (j - 1) & 1);  // softmax has read S_{j-1}
-          tc_fence_after();
-          const uint32_t k_base = smem_u32(smem + Cfg::OFF_K + st * Cfg::K_BYTES);
+    // ---------------- MMA issuer (whole warp; one elected lane issues) ----------------
+    const uint32_t idS = make_idesc_bf16(128, FA_BK, false, false);
+    const uint32_t idO = make_idesc_bf16(128, DH, false, true);
+    const uint32_t q_base = smem_u32(smem + Cfg::OFF_Q);
+    const uint32_t p_base = smem_u32(smem + Cfg::OFF_P);
+    auto issue_s = [&](int t, int j) {  // S_t = Q_t K_j^T
+      const int st = j % NS;
+      mbar_wait(&kv_full[st], (j / NS) & 1);
+      tc_fence_after();
+      const uint32_t qb = q_base + t * Cfg::Q_BYTES;
+      const uint32_t kbase = smem_u32(smem + Cfg::OFF_K + st * Cfg::K_BYTES);
+      if (elect_one()) {
 #pragma unroll
-          for (int kb = 0; kb < DH / 64; ++kb)
+        for (int kb = 0; kb < DH / 64; ++kb)
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              umma_bf16(tS, make_sw128_desc(q_base + kb * (FA_BQ * 128) + k * 32, 16, 1024),
-                        make_sw128_desc(k_base + kb * (FA_BK * 128) + k * 32, 16, 1024), idS, (kb | k) != 0);
-          umma_commit(s_full);
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(tmem + t * 128, make_sw128_desc(qb + kb * (FA_BQ * 128) + k * 32, 16, 1024),
+                      make_sw128_desc(kbase + kb * (FA_BK * 128) + k * 32, 16, 1024), idS, (kb | k) != 0);
+        umma_commit(&s_full[t]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int t, int j) {  // O_t += P_t V_j
+      const int st = j % NS;
+      mbar_wait(&p_full[t], j & 1);
+      tc_fence_after();
+      const uint32_t pb = p_base + t * Cfg::P_BYTES;
+      const uint32_t vbase = smem_u32(smem + Cfg::OFF_V + st * Cfg::V_BYTES);
+      if (elect_one()) {
+#pragma unroll
+        for (int kb = 0; kb < FA_BK / 64; ++kb)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(tmem + 256 + t * DH, make_sw128_desc(pb + kb * (FA_BQ * 128) + k * 32, 16, 1024),
+                      make_sw128_desc(vbase + kb * (DH / 64) * 8192 + k * 2048, 8192, 1024), idO,
+                      (j > 0) || ((kb | k) != 0));
+        umma_commit(&o_done[t]);
+      }
+      __syncwarp();
+    };
+    mbar_wait(q_full, 0);
+    if (nkt0 > 0) issue_s(0, 0);
+    if (nkt1 > 0) issue_s(1, 0);
+    for (int j = 0; j < n_iter; ++j) {
+      // S_t(j+1) overwrites S_t(j): p_full_t(j) implies the softmax group has read it
+      if constexpr (NS > 1) {
+        if (j < nkt0) {
+          issue_pv(0, j);
+          if (j + 1 < nkt0) issue_s(0, j + 1);
         }
-        if (j > 0) {
-          const int jp = j - 1, st = jp & 1;
-          mbar_wait(p_full, jp & 1);  // P_{j-1} in smem, O rescaled
-          tc_fence_after();
-          const uint32_t v_base = smem_u32(smem + Cfg::OFF_V + st * Cfg::V_BYTES);
-#pragma unroll
-          for (int kb = 0; kb < FA_BK / 64; ++kb)
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              umma_bf16(tO, make_sw128_desc(p_base + kb * (FA_BQ * 128) + k * 32, 16, 1024),
-                        make_sw128_desc(v_base + kb * (DH / 64) * 8192 + k * 2048, 8192, 1024), idO,
-                        (jp > 0) || ((kb | k) != 0));
-          umma_commit(o_done);
-          umma_commit(&kv_empty[st]);
+        if (j < nkt1) {
+          issue_pv(1, j);
+          if (j + 1 < nkt1) issue_s(1, j + 1);
         }
+        if (elect_one()) umma_commit(&kv_empty[j % NS]);  // K_j / V_j consumed by every MMA above
+        __syncwarp();
+      } else {
+        // single K/V stage: both P.V products must release it before K_{j+1} can land
+        if (j < nkt0) issue_pv(0, j);
+        if (j < nkt1) issue_pv(1, j);
+        if (elect_one()) umma_commit(&kv_empty[0]);
+        __syncwarp();
+        if (j + 1 < nkt0) issue_s(0, j + 1);
+        if (j + 1 < nkt1) issue_s(1, j + 1);
       }
     }
   } else if (warp >= 4) {
-    // ---------------- softmax / epilogue (thread = query row) ----------------
-    const int r = (warp - 4) * 32 + lane;  // row within tile == TMEM lane
+    // ---------------- softmax groups (thread = query row) ----------------
+    const int t = (warp - 4) >> 2;  // query tile of this group
+    const int nkt = t == 0 ? nkt0 : nkt1;
+    const int r = (warp & 3) * 32 + lane;  // row within tile == TMEM lane
+    const int qt = qt0 + t;
     const int q = qt * FA_BQ + r;
     const uint32_t t_lane = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + t * 128 + t_lane;
+    const uint32_t tO = tmem + 256 + t * DH + t_lane;
     const float* mrow = a.mask ? a.mask + (int64_t)b * a.s : nullptr;
-    const uint64_t prow = (uint64_t)(((a.sample_offset + b) * a.nh_global + a.head_offset + h) * (int64_t)a.s + q);
-    uint8_t* p_smem = smem + Cfg::OFF_P;
+    const uint32_t* krow = a.keep ? a.keep + (((int64_t)b * a.nh + h) * a.s + q) * (a.s / 32) : nullptr;
+    uint8_t* p_smem = smem + Cfg::OFF_P + t * Cfg::P_BYTES;
     float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_kt; ++j) {
+    for (int j = 0; j < nkt; ++j) {
       const int key0 = j * FA_BK;
       const bool diag = a.causal && (j == qt);
-      mbar_wait(s_full, j & 1);
+      uint4 kw = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+      if (krow) kw = __ldg(reinterpret_cast<const uint4*>(krow + key0 / 32));
+      mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
-      // pass 1: row max of the scaled, masked scores (read TMEM 32 columns at a time)
-      float mx = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tS + t_lane + c * 32, v);
-        tmem_ld_wait();
+      uint32_t sv[128];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int key = key0 + c * 32 + e;
-          float x = __uint_as_float(v[e]) * a.scale_log2;
-          if (mrow) x += __ldg(mrow + key) * 1.4426950408889634f;
-          if ((diag && key > q) || key >= a.s) x = -INFINITY;
-          mx = fmaxf(mx, x);
+      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(sv + c * 32));
+      tmem_ld_wait();
+      // scaled (+ masked) scores in the log2 domain
+      float x[128];
+      if (mrow) {
+        const float4* mp = reinterpret_cast<const float4*>(mrow + key0);
+#pragma unroll
+        for (int k4 = 0; k4 < 32; ++k4) {
+          const float4 mk = __ldg(mp + k4);
+          x[4 * k4 + 0] = fmaf(__uint_as_float(sv[4 * k4 + 0]), a.scale_log2, mk.x * 1.4426950408889634f);
+          x[4 * k4 + 1] = fmaf(__uint_as_float(sv[4 * k4 + 1]), a.scale_log2, mk.y * 1.4426950408889634f);
+          x[4 * k4 + 2] = fmaf(__uint_as_float(sv[4 * k4 + 2]), a.scale_log2, mk.z * 1.4426950408889634f);
+          x[4 * k4 + 3] = fmaf(__uint_as_float(sv[4 * k4 + 3]), a.scale_log2, mk.w * 1.4426950408889634f);
         }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 128; ++k) x[k] = __uint_as_float(sv[k]) * a.scale_log2;
       }
+      if (diag) {
+#pragma unroll
+        for (int k = 0; k < 128; ++k)
+          if (k > r) x[k] = -INFINITY;
+      }
+      float mx = x[0];
+#pragma unroll
+      for (int k = 1; k < 128; ++k) mx = fmaxf(mx, x[k]);
       const float m_new = fmaxf(m, mx);
       const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
       const float alpha = (m == -INFINITY) ? 0.f : ex2_approx(m - m_use);
-      uint32_t keep[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
-      if (a.p > 0.f) fa_keep128(a.seed, a.layer, prow, key0, a.thresh, keep);
+      // P = exp2(x - m); rowsum before dropout; dropped entries zero (1/(1-p) in the epilogue)
+      uint32_t pk[64];
+      float rowsum = 0.f;
+      const uint32_t kws[4] = {kw.x, kw.y, kw.z, kw.w};
+#pragma unroll
+      for (int k = 0; k < 128; k += 2) {
+        const float p0 = ex2_approx(x[k] - m_use);
+        const float p1 = ex2_approx(x[k + 1] - m_use);
+        rowsum += p0 + p1;
+        const uint32_t w = kws[k >> 5];
+        pk[k >> 1] = pack_bf16x2(((w >> (k & 31)) & 1u) ? p0 : 0.f, ((w >> ((k + 1) & 31)) & 1u) ? p1 : 0.f);
+      }
+      l = l * alpha + rowsum;
+      m = m_new;
       if (j > 0) {
-        // P.V of tile j-1 must have finished: it reads the P buffer we overwrite below
-        // and accumulates into the O we rescale
-        mbar_wait(o_done, (j - 1) & 1);
+        // P.V of tile j-1 must have finished: it reads the P buffer we overwrite below and
+        // accumulates into the O we rescale
+        mbar_wait(&o_done[t], (j - 1) & 1);
         tc_fence_after();
         if (!__all_sync(0xffffffffu, alpha == 1.f)) {
 #pragma unroll
           for (int c = 0; c < DH / 32; ++c) {
             uint32_t o[32];
-            tmem_ld_32x32b_x32(tO + t_lane + c * 32, o);
+            tmem_ld_32x32b_x32(tO + c * 32, o);
             tmem_ld_wait();
 #pragma unroll
             for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-            tmem_st_32x32b_x32(tO + t_lane + c * 32, o);
+            tmem_st_32x32b_x32(tO + c * 32, o);
           }
           tmem_st_wait();
         }
       }
-      // pass 2: p = exp2(x - m); row sum; dropout; bf16 P -> smem as the swizzled K-major
-      // A operand (keys [64kb, 64kb+64) in sub-tile kb; 16-B granule g = keys 8g..8g+7)
-      float rowsum = 0.f;
+      // P -> smem as the swizzled K-major A operand (keys [64kb, 64kb+64) in sub-tile kb;
+      // 16-B granule g = keys 8g..8g+7)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tS + t_lane + c * 32, v);
-        tmem_ld_wait();
-        if (c == 3) {
-          tc_fence_before();
-          mbar_arrive(s_free);  // S fully read: the MMA warp may overwrite it
-        }
-        uint32_t pk[16];
+      for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float pe[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int key = key0 + c * 32 + e + u;
-            float x = __uint_as_float(v[e + u]) * a.scale_log2;
-            if (mrow) x += __ldg(mrow + key) * 1.4426950408889634f;
-            if ((diag && key > q) || key >= a.s) x = -INFINITY;
-            const float pr = ex2_approx(x - m_use);
-            rowsum += pr;
-            pe[u] = ((keep[c] >> (e + u)) & 1u) ? pr * a.inv_keep : 0.f;
-          }
-          pk[e / 2] = pack_bf16x2(pe[0], pe[1]);
-        }
-        const int kb = c >> 1;
-#pragma unroll
-        for (int gg = 0; gg < 4; ++gg) {
-          const int g = (c & 1) * 4 + gg;
+        for (int g = 0; g < 8; ++g) {
+          const int w0 = kb * 32 + g * 4;
           *reinterpret_cast<uint4*>(p_smem + kb * (FA_BQ * 128) + sw128_offset(r, g)) =
-              make_uint4(pk[gg * 4], pk[gg * 4 + 1], pk[gg * 4 + 2], pk[gg * 4 + 3]);
+              make_uint4(pk[w0], pk[w0 + 1], pk[w0 + 2], pk[w0 + 3]);
         }
-      }
-      l = l * alpha + rowsum;
-      m = m_new;
       fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(p_full);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[t]);
     }
-    // epilogue: O / l -> bf16; lse
-    mbar_wait(o_done, (n_kt - 1) & 1);
-    tc_fence_after();
-    const float inv_l = l > 0.f ? 1.f / l : 0.f;
-    bf16* orow = a.out + ((int64_t)b * a.s + q) * a.ld_out + (int64_t)h * DH;
+    // epilogue: O * (1/(1-p)) / l -> bf16; lse
+    if (nkt > 0) {
+      mbar_wait(&o_done[t], (nkt - 1) & 1);
+      tc_fence_after();
+      const float sc = l > 0.f ? a.inv_keep / l : 0.f;
+      bf16* orow = a.out + ((int64_t)b * a.s + q) * a.ld_out + (int64_t)h * DH;
 #pragma unroll
-    for (int c = 0; c < DH / 32; ++c) {
-      uint32_t o[32];
-      tmem_ld_32x32b_x32(tO + t_lane + c * 32, o);
-      tmem_ld_wait();
-      if (q < a.s) {
+      for (int c = 0; c < DH / 32; ++c) {
+        uint32_t o[32];
+        tmem_ld_32x32b_x32(tO + c * 32, o);
+        tmem_ld_wait();
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           uint4 u;
-          u.x = pack_bf16x2(__uint_as_float(o[g * 8 + 0]) * inv_l, __uint_as_float(o[g * 8 + 1]) * inv_l);
-          u.y = pack_bf16x2(__uint_as_float(o[g * 8 + 2]) * inv_l, __uint_as_float(o[g * 8 + 3]) * inv_l);
-          u.z = pack_bf16x2(__uint_as_float(o[g * 8 + 4]) * inv_l, __uint_as_float(o[g * 8 + 5]) * inv_l);
-          u.w = pack_bf16x2(__uint_as_float(o[g * 8 + 6]) * inv_l, __uint_as_float(o[g * 8 + 7]) * inv_l);
+          u.x = pack_bf16x2(__uint_as_float(o[g * 8 + 0]) * sc, __uint_as_float(o[g * 8 + 1]) * sc);
+          u.y = pack_bf16x2(__uint_as_float(o[g * 8 + 2]) * sc, __uint_as_float(o[g * 8 + 3]) * sc);
+          u.z = pack_bf16x2(__uint_as_float(o[g * 8 + 4]) * sc, __uint_as_float(o[g * 8 + 5]) * sc);
+          u.w = pack_bf16x2(__uint_as_float(o[g * 8 + 6]) * sc, __uint_as_float(o[g * 8 + 7]) * sc);
           *reinterpret_cast<uint4*>(orow + c * 32 + g * 8) = u;
         }
       }
+      if (a.lse) a.lse[((int64_t)b * a.nh + h) * a.s + q] = (l > 0.f) ? m + __log2f(l) : -INFINITY;
     }
-    if (q < a.s && a.lse) a.lse[((int64_t)b * a.nh + h) * a.s + q] = (l > 0.f) ? m + __log2f(l) : -INFINITY;
   }
   tc_fence_before();
   __syncthreads();
@@ -306,25 +333,58 @@ __global__ void __launch_bounds__(FA_THREADS, (DH == 64 ? 2 : 1))
   }
 }
 
+// Attention-probability dropout keep bits (site 0 of the Philox scheme, oracle/philox.py):
+// word ((b*nh + h)*sq + q)*(sk/32) + k/32, bit k%32 = keep(row = (gs*nh_global + gh)*sq + q,
+// col = k) with gs = sample_offset + b, gh = head_offset + h.  One thread per word
+// (4 Philox4x32-10 calls = 32 keys).
+__global__ void __launch_bounds__(128) attn_dropout_bits_kernel(int nh, int sq, int wpr, uint32_t thresh,
+                                                                uint64_t seed, uint32_t layer,
+                                                                int64_t sample_offset, int head_offset, int nh_global,
+                                                                uint32_t* __restrict__ bits) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // (q, w) of this (b, h)
+  if (idx >= sq * wpr) return;
+  const int bh = blockIdx.y;
+  const int q = idx / wpr, w = idx - q * wpr;
+  const int h = bh % nh, b = bh / nh;
+  const uint64_t grow = (uint64_t)(((sample_offset + b) * nh_global + head_offset + h) * (int64_t)sq + q);
+  uint32_t word = 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    bool k8[8];
+    dropout_keep8(seed, layer, 0u, grow, w * 32 + c * 8, thresh, k8);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) word |= (k8[e] ? 1u : 0u) << (c * 8 + e);
+  }
+  bits[(int64_t)bh * sq * wpr + idx] = word;
+}
+
 }  // namespace smpk
 
 using namespace smpk;
 
-// defined in gemm.cu
-namespace smpk {
-int make_tma_4d(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t ld, int nb1, int64_t s1,
-                int nb2, int64_t s2, int box_inner, int box_outer, const char* name);
+extern "C" int smpk_attn_dropout_bits(int B, int nh, int sq, int sk, float p_drop, uint64_t seed, int layer,
+                                      int64_t sample_offset, int head_offset, int nh_global, uint32_t* bits,
+                                      void* stream) {
+  SMPK_REQUIRE(B > 0 && nh > 0 && sq > 0 && sk > 0 && sk % 32 == 0 && bits, SMPK_ERR_BAD_ARG,
+               "smpk_attn_dropout_bits: bad arguments (sk must be a multiple of 32)");
+  SMPK_REQUIRE(p_drop >= 0.f && p_drop < 1.f, SMPK_ERR_BAD_ARG, "smpk_attn_dropout_bits: p in [0,1)");
+  SMPK_REQUIRE((int64_t)B * nh < 65536, SMPK_ERR_UNSUPPORTED, "smpk_attn_dropout_bits: B*nh must be < 65536");
+  const int wpr = sk / 32;
+  dim3 grid((unsigned)((sq * wpr + 127) / 128), (unsigned)(B * nh));
+  attn_dropout_bits_kernel<<<grid, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      nh, sq, wpr, dropout_threshold(p_drop), seed, (uint32_t)layer, sample_offset, head_offset, nh_global, bits);
+  return check_launch("smpk_attn_dropout_bits");
 }
 
 extern "C" int smpk_flash_attn_fwd(const void* qkv, int64_t ld, int B, int nh, int s, int dh, void* out,
                                    int64_t ld_out, float* lse, const float* mask_add, float scale, int causal,
-                                   float p_drop, uint64_t seed, int layer, int64_t sample_offset, int head_offset,
-                                   int nh_global, void* stream) {
+                                   float p_drop, const uint32_t* keep_bits, void* stream) {
   SMPK_REQUIRE(dh == 64 || dh == 128, SMPK_ERR_UNSUPPORTED, "smpk_flash_attn_fwd: head dim %d (64 or 128)", dh);
   SMPK_REQUIRE(s % 128 == 0 && s > 0, SMPK_ERR_UNSUPPORTED, "smpk_flash_attn_fwd: seq %d must be a multiple of 128",
                s);
   SMPK_REQUIRE(qkv && out && B > 0 && nh > 0, SMPK_ERR_BAD_ARG, "smpk_flash_attn_fwd: bad arguments");
   SMPK_REQUIRE(p_drop >= 0.f && p_drop < 1.f, SMPK_ERR_BAD_ARG, "smpk_flash_attn_fwd: dropout p in [0,1)");
+  SMPK_REQUIRE(p_drop == 0.f || keep_bits, SMPK_ERR_BAD_ARG, "smpk_flash_attn_fwd: dropout needs keep bits");
   SMPK_REQUIRE(ld_out % 8 == 0, SMPK_ERR_BAD_ARG, "smpk_flash_attn_fwd: ld_out must be a multiple of 8");
   const int64_t hd = (int64_t)nh * dh;
   const bf16* base = reinterpret_cast<const bf16*>(qkv);
@@ -341,17 +401,11 @@ extern "C" int smpk_flash_attn_fwd(const void* qkv, int64_t ld, int B, int nh, i
   a.ld_out = ld_out;
   a.lse = lse;
   a.mask = mask_add;
+  a.keep = p_drop > 0.f ? keep_bits : nullptr;
   a.scale_log2 = scale * 1.4426950408889634f;
   a.causal = causal;
-  a.p = p_drop;
   a.inv_keep = p_drop > 0.f ? 1.f / (1.f - p_drop) : 1.f;
-  a.thresh = dropout_threshold(p_drop);
-  a.seed = seed;
-  a.layer = (uint32_t)layer;
-  a.sample_offset = sample_offset;
-  a.head_offset = head_offset;
-  a.nh_global = nh_global;
-  dim3 grid(s / 128, nh, B);
+  dim3 grid((s / 128 + 1) / 2, nh, B);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (dh == 64) {
     static bool once = false;

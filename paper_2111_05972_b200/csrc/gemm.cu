@@ -647,6 +647,13 @@ int make_tma_4d(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer,
                         box_outer, name);
 }
 
+// fp32 / 32-bit-word map without swizzle (keep-bit tiles of the attention backward).
+int make_tma_4d_b32(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t ld, int box_inner,
+                    int box_outer, const char* name) {
+  return make_tma_4d_ex(map, ptr, true, CU_TENSOR_MAP_SWIZZLE_NONE, inner, outer, ld, 1, 0, 1, 0, box_inner,
+                        box_outer, name);
+}
+
 // TMA-store map of an output [nb2][nb1][rows][cols] with 32 x 32 boxes (see stage_*_row).
 static int make_store_map(CUtensorMap* map, const void* ptr, bool f32, int rows, int cols, int64_t ld, int nb1,
                           int64_t s1, int nb2, int64_t s2, const char* name) {

@@ -133,14 +133,43 @@ def attn_core_bwd(dctx: torch.Tensor, qkv: torch.Tensor, P, Pd, B: int, s: int, 
     return dqkv
 
 
-FLASH = {"enabled": True, "min_seq": 1024}
+FLASH = {"enabled": True, "min_seq": 128}
 
 
 def use_flash(s: int, head_dim: int) -> bool:
-    """Fused tcgen05 attention (csrc/flash_attn*.cu) for long sequences; the materialised path
-    (tcgen05 batched GEMMs + fused softmax kernels) is as fast at s <= 512 in this build
-    (scripts/attn_bench.py) and keeps the [s, s] tiles L2-resident there."""
+    """Fused tcgen05 attention (csrc/flash_attn*.cu) whenever its shape constraints hold; the
+    materialised path (tcgen05 batched GEMMs + fused softmax kernels) covers the rest and is the
+    A/B reference (scripts/attn_bench.py: 36 + 122 us vs 115 + 155 us at BERT-large s=512)."""
     return FLASH["enabled"] and s % 128 == 0 and head_dim in (64, 128) and s >= FLASH["min_seq"]
+
+
+_SIDE: dict = {}
+
+
+def _side_stream() -> torch.cuda.Stream:
+    """Per-device side stream for data-independent work (attention dropout keep bits) that can
+    run concurrently with the GEMM in front of it."""
+    dev = torch.cuda.current_device()
+    st = _SIDE.get(dev)
+    if st is None:
+        st = _SIDE[dev] = torch.cuda.Stream(device=dev)
+    return st
+
+
+def _keep_bits_async(B: int, s: int, m: LayerMeta, device):
+    """Launch the attention keep-bit generator on the side stream; returns (bits, join) where
+    join() makes the current stream wait for it (fork/join is CUDA-graph capturable)."""
+    if m.p_attn <= 0:
+        return None, (lambda: None)
+    main = torch.cuda.current_stream()
+    bits = torch.empty(B, m.heads_local, s, s // 32, dtype=torch.int32, device=device)  # main-stream allocation
+    side = _side_stream()
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        ops.attn_dropout_bits(B, m.heads_local, s, s, p=m.p_attn, seed=m.seed, layer=m.layer_id,
+                              sample_offset=m.sample_offset, head_offset=m.head_offset, nh_global=m.heads_global,
+                              out=bits)
+    return bits, (lambda: main.wait_stream(side))
 
 
 def _ln_in(x2, w, b, m: LayerMeta):
@@ -290,15 +319,18 @@ class AttentionFn(torch.autograd.Function):
         b, s, H = x.shape
         R = b * s
         x2 = x.reshape(R, H)
-        hf, mu1, rs1, G = _gather_in(x2, m, (pre_w, pre_b) if m.pre_ln else None)
-        B = hf.shape[0] // s  # T*b samples when row-sharded
-        qkv = K.linear(hf, wqkv, bqkv)
         fused = use_flash(s, m.head_dim)
+        B = b * (m.tp_size if m.shard_rows else 1)  # T*b samples when row-sharded
+        if fused:  # keep bits depend only on (seed, layer, coordinates): overlap them with the QKV GEMM
+            bits, join = _keep_bits_async(B, s, m, x.device)
+        hf, mu1, rs1, G = _gather_in(x2, m, (pre_w, pre_b) if m.pre_ln else None)
+        assert hf.shape[0] == B * s
+        qkv = K.linear(hf, wqkv, bqkv)
         if fused:
+            join()
             ctxv, lse = ops.flash_attn_fwd(qkv, B, s, m.heads_local, m.head_dim, mask_add=mask_add, causal=m.causal,
-                                           p=m.p_attn, seed=m.seed, layer=m.layer_id, sample_offset=m.sample_offset,
-                                           head_offset=m.head_offset, nh_global=m.heads_global)
-            P, Pd = lse, None
+                                           p=m.p_attn, keep_bits=bits)
+            P, Pd = lse, bits  # the backward re-reads the same keep bits
         else:
             ctxv, P, Pd = attn_core_fwd(qkv, B, s, m, mask_add)
         ox, ns, st, PR = _rs_out(ctxv, wo, False, m, R, H)
@@ -334,9 +366,7 @@ class AttentionFn(torch.autograd.Function):
         dctx = K.matmul_nn(dof, wo)
         if ctx.fused:
             dqkv = ops.flash_attn_bwd(dctx, qkv, ctxv, P, B, s, m.heads_local, m.head_dim, mask_add=mask_add,
-                                      causal=m.causal, p=m.p_attn, seed=m.seed, layer=m.layer_id,
-                                      sample_offset=m.sample_offset, head_offset=m.head_offset,
-                                      nh_global=m.heads_global)
+                                      causal=m.causal, p=m.p_attn, keep_bits=Pd if m.p_attn > 0 else None)
         else:
             dqkv = attn_core_bwd(dctx, qkv, P, Pd, B, s, m)
         dwqkv = K.matmul_tn(dqkv, hf)

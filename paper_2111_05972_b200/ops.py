@@ -117,11 +117,27 @@ def colsum(x: torch.Tensor, *, out_dtype=None) -> torch.Tensor:
     return out
 
 
+def attn_dropout_bits(B: int, nh: int, sq: int, sk: int, *, p: float, seed=0, layer=0, sample_offset=0,
+                      head_offset=0, nh_global=None, device=None, out=None) -> torch.Tensor | None:
+    """Keep bits [B, nh, sq, sk/32] (uint32 words as int32) of the attention-probability dropout;
+    None when p == 0.  Generated once per layer and shared by the forward and the backward."""
+    if p <= 0.0:
+        return None
+    bits = out if out is not None else torch.empty(B, nh, sq, sk // 32, dtype=torch.int32,
+                                                   device=device or torch.cuda.current_device())
+    _check_cuda(bits)
+    _lib.call("smpk_attn_dropout_bits", B, nh, sq, sk, float(p), int(seed) & (2 ** 64 - 1), int(layer),
+              int(sample_offset), int(head_offset), int(nh_global if nh_global is not None else nh), _ptr(bits),
+              _stream())
+    return bits
+
+
 def flash_attn_bwd(dctx: torch.Tensor, qkv: torch.Tensor, ctx: torch.Tensor, lse: torch.Tensor, B: int, s: int,
-                   nh: int, dh: int, *, mask_add=None, causal=False, p=0.0, seed=0, layer=0, sample_offset=0,
-                   head_offset=0, nh_global=None, dqkv=None):
+                   nh: int, dh: int, *, mask_add=None, causal=False, p=0.0, keep_bits=None, dqkv=None):
     """Backward of flash_attn_fwd: returns dqkv [B*s, 3*nh*dh] (dQ | dK | dV blocks)."""
-    _check_cuda(dctx, qkv, ctx, lse, mask_add)
+    _check_cuda(dctx, qkv, ctx, lse, mask_add, keep_bits)
+    if p > 0 and keep_bits is None:
+        raise ValueError("flash_attn_bwd: dropout needs the forward's keep bits")
     dctx = dctx.contiguous()
     dqkv = dqkv if dqkv is not None else torch.empty_like(qkv)
     if mask_add is not None:
@@ -130,22 +146,23 @@ def flash_attn_bwd(dctx: torch.Tensor, qkv: torch.Tensor, ctx: torch.Tensor, lse
     ws = torch.empty(ws_bytes // 4, dtype=torch.float32, device=qkv.device)
     _lib.call("smpk_flash_attn_bwd", _ptr(qkv), qkv.stride(0), _ptr(ctx), ctx.stride(0), _ptr(dctx), dctx.stride(0),
               _ptr(lse), B, nh, s, dh, _ptr(dqkv), _ptr(mask_add), float(1.0 / dh ** 0.5), int(bool(causal)),
-              float(p), int(seed) & (2 ** 64 - 1), int(layer), int(sample_offset), int(head_offset),
-              int(nh_global if nh_global is not None else nh), _ptr(ws), int(ws_bytes), _stream())
+              float(p), _ptr(keep_bits if p > 0 else None), _ptr(ws), int(ws_bytes), _stream())
     return dqkv
 
 
 def flash_attn_fwd(qkv: torch.Tensor, B: int, s: int, nh: int, dh: int, *, mask_add=None, causal=False, p=0.0,
-                   seed=0, layer=0, sample_offset=0, head_offset=0, nh_global=None, out=None):
+                   keep_bits=None, out=None):
     """Fused attention on the packed QKV buffer [B*s, 3*nh*dh] (q | k | v blocks, heads inside each).
+    Dropout (p > 0) uses keep_bits from attn_dropout_bits.
     Returns (ctx [B*s, nh*dh] bf16, lse [B, nh, s] fp32 log2-domain)."""
-    _check_cuda(qkv, mask_add)
+    _check_cuda(qkv, mask_add, keep_bits)
+    if p > 0 and keep_bits is None:
+        raise ValueError("flash_attn_fwd: dropout needs keep bits (ops.attn_dropout_bits)")
     ctx = out if out is not None else torch.empty(B * s, nh * dh, dtype=qkv.dtype, device=qkv.device)
     lse = torch.empty(B, nh, s, dtype=torch.float32, device=qkv.device)
     if mask_add is not None:
         mask_add = mask_add.reshape(B, s).to(torch.float32).contiguous()
     _lib.call("smpk_flash_attn_fwd", _ptr(qkv), qkv.stride(0), B, nh, s, dh, _ptr(ctx), ctx.stride(0), _ptr(lse),
-              _ptr(mask_add), float(1.0 / dh ** 0.5), int(bool(causal)), float(p), int(seed) & (2 ** 64 - 1),
-              int(layer), int(sample_offset), int(head_offset), int(nh_global if nh_global is not None else nh),
-              _stream())
+              _ptr(mask_add), float(1.0 / dh ** 0.5), int(bool(causal)), float(p),
+              _ptr(keep_bits if p > 0 else None), _stream())
     return ctx, lse

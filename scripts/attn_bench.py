@@ -30,12 +30,14 @@ for (B, nh, s, dh, causal, p) in [(8, 16, 512, 64, False, 0.1), (8, 16, 512, 64,
                      causal=causal, pre_ln=False, post_ln=True, activation="gelu", layer_id=0, seed=1, head_offset=0,
                      sample_offset=0, tp_size=1)
     ctx_m, P, Pd = Lm.attn_core_fwd(qkv, B, s, m, None)
-    ctx_f, lse = ops.flash_attn_fwd(qkv, B, s, nh, dh, causal=causal, p=p, seed=1)
+    bits = ops.attn_dropout_bits(B, nh, s, s, p=p, seed=1)
+    ctx_f, lse = ops.flash_attn_fwd(qkv, B, s, nh, dh, causal=causal, p=p, keep_bits=bits)
     flops_f = 4 * B * nh * s * s * dh * (0.5 if causal else 1.0)
     t_mf = timeit(lambda: Lm.attn_core_fwd(qkv, B, s, m, None))
-    t_ff = timeit(lambda: ops.flash_attn_fwd(qkv, B, s, nh, dh, causal=causal, p=p, seed=1))
+    t_bits = timeit(lambda: ops.attn_dropout_bits(B, nh, s, s, p=p, seed=1)) if p > 0 else 0.0
+    t_ff = timeit(lambda: ops.flash_attn_fwd(qkv, B, s, nh, dh, causal=causal, p=p, keep_bits=bits))
     t_mb = timeit(lambda: Lm.attn_core_bwd(dctx, qkv, P, Pd, B, s, m))
-    t_fb = timeit(lambda: ops.flash_attn_bwd(dctx, qkv, ctx_f, lse, B, s, nh, dh, causal=causal, p=p, seed=1))
+    t_fb = timeit(lambda: ops.flash_attn_bwd(dctx, qkv, ctx_f, lse, B, s, nh, dh, causal=causal, p=p, keep_bits=bits))
     print(f"B={B} nh={nh} s={s} dh={dh} causal={causal} p={p}: fwd materialized {t_mf:.1f} us, flash {t_ff:.1f} us "
-          f"({flops_f / t_ff / 1e6:.0f} TF/s) | bwd materialized {t_mb:.1f} us, flash {t_fb:.1f} us "
+          f"({flops_f / t_ff / 1e6:.0f} TF/s) + bits {t_bits:.1f} us | bwd materialized {t_mb:.1f} us, flash {t_fb:.1f} us "
           f"({2.5 * flops_f / t_fb / 1e6:.0f} TF/s)", flush=True)

@@ -11,6 +11,11 @@ from oracle import philox, tp
 pytestmark = pytest.mark.gpu
 
 
+def keep_bits(ops, B, nh, s, p, seed, layer, soff, hoff, nhg):
+    return ops.attn_dropout_bits(B, nh, s, s, p=p, seed=seed, layer=layer, sample_offset=soff, head_offset=hoff,
+                                 nh_global=nhg, device="cuda")
+
+
 def rel(a, b):
     a, b = a.double().cpu(), b.double().cpu()
     return ((a - b).norm() / max(b.norm().item(), 1e-30)).item()
@@ -42,8 +47,8 @@ def test_flash_fwd_vs_oracle(case):
         mask[-1, :5] = -10000.0
     seed, layer, soff, hoff, nhg = 77, 3, 5, 2, nh + 4
     ctx, lse = ops.flash_attn_fwd(qkv.cuda(), B, s, nh, dh, mask_add=None if mask is None else mask.cuda(),
-                                  causal=causal, p=p, seed=seed, layer=layer, sample_offset=soff, head_offset=hoff,
-                                  nh_global=nhg)
+                                  causal=causal, p=p,
+                                  keep_bits=keep_bits(ops, B, nh, s, p, seed, layer, soff, hoff, nhg))
     q, k, v = qkv.double().split(H, -1)
     ref = tp.attention_core(q.reshape(B, s, nh, dh), k.reshape(B, s, nh, dh), v.reshape(B, s, nh, dh),
                             None if mask is None else mask.double(), causal,
@@ -70,8 +75,8 @@ def test_flash_bwd_vs_oracle(case):
         mask = torch.zeros(B, s)
         mask[0, -37:] = -10000.0
     seed, layer, soff, hoff, nhg = 31, 1, 2, 1, nh + 2
-    kw = dict(mask_add=None if mask is None else mask.cuda(), causal=causal, p=p, seed=seed, layer=layer,
-              sample_offset=soff, head_offset=hoff, nh_global=nhg)
+    kw = dict(mask_add=None if mask is None else mask.cuda(), causal=causal, p=p,
+              keep_bits=keep_bits(ops, B, nh, s, p, seed, layer, soff, hoff, nhg))
     ctx, lse = ops.flash_attn_fwd(qkv.cuda(), B, s, nh, dh, **kw)
     dqkv = ops.flash_attn_bwd(dctx.cuda(), qkv.cuda(), ctx, lse, B, s, nh, dh, **kw)
     x = qkv.double().requires_grad_(True)
@@ -96,5 +101,18 @@ def test_flash_matches_materialized_path():
                      p_hidden=0.0, causal=False, pre_ln=False, post_ln=True, activation="gelu", layer_id=4, seed=9,
                      head_offset=0, sample_offset=0, tp_size=1)
     ctx_ref, _, _ = Lm.attn_core_fwd(qkv, B, s, m, None)
-    ctx, _ = ops.flash_attn_fwd(qkv, B, s, nh, dh, p=0.1, seed=9, layer=4)
+    ctx, _ = ops.flash_attn_fwd(qkv, B, s, nh, dh, p=0.1, keep_bits=keep_bits(ops, B, nh, s, 0.1, 9, 4, 0, 0, nh))
     assert rel(ctx, ctx_ref) < 1e-2
+
+
+@pytest.mark.parametrize("shape", [(2, 3, 128, 256, 5, 1, 7), (1, 2, 512, 512, 0, 0, 2)])
+def test_dropout_bits_bit_exact(shape):
+    """smpk_attn_dropout_bits == oracle/philox.py attn_prob_mask, bit for bit."""
+    from paper_2111_05972_b200 import ops
+    B, nh, sq, sk, soff, hoff, nhg = shape
+    p, seed, layer = 0.15, 123456789012, 6
+    bits = ops.attn_dropout_bits(B, nh, sq, sk, p=p, seed=seed, layer=layer, sample_offset=soff, head_offset=hoff,
+                                 nh_global=nhg, device="cuda").cpu().numpy().view(np.uint32)
+    got = ((bits[..., None] >> np.arange(32, dtype=np.uint32)) & 1).reshape(B, nh, sq, sk).astype(bool)
+    ref = philox.attn_prob_mask(np.arange(B) + soff, np.arange(nh) + hoff, sq, sk, nhg, layer, seed, p)
+    assert np.array_equal(got, ref)
