@@ -166,12 +166,20 @@ __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs
   for (int row0 = blockIdx.x * rows_per_cta; row0 < a.M; row0 += gridDim.x * rows_per_cta) {
     const int row = row0 + slot;
     const bool valid = row < a.M;
-    float v[VPT][8];
+    float v[VPT][8], res[VPT][8];
+    // every load of the row first (memory-level parallelism), then the math
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       const int col = ((i * W + wi) * 32 + lane) * 8;
       if (valid) {
         load8_slots(a.x + (int64_t)row * a.H + col, a.nslots, a.slot_stride, v[i]);
+        if (a.residual) load8(a.residual + (int64_t)row * a.H + col, res[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int col = ((i * W + wi) * 32 + lane) * 8;
+      if (valid) {
         if (a.bias) {
           float b[8];
           load8(a.bias + col, b);
@@ -185,10 +193,8 @@ __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs
           for (int j = 0; j < 8; ++j) v[i][j] = keep[j] ? v[i][j] * inv_keep : 0.f;
         }
         if (a.residual) {
-          float rr[8];
-          load8(a.residual + (int64_t)row * a.H + col, rr);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) v[i][j] += rr[j];
+          for (int j = 0; j < 8; ++j) v[i][j] += res[i][j];
         }
         round8(v[i]);
         if (a.r_out) store8(a.r_out + (int64_t)row * a.H + col, v[i]);
@@ -317,6 +323,12 @@ __global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const LnBwdArgs a) 
       rs = a.rstd[row];
     }
     float s1 = 0.f, s2 = 0.f;
+    uint4 dres_raw[VPT];  // residual-gradient loads issued with the others (memory-level parallelism)
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int col = ((i * W + wi) * 32 + lane) * 8;
+      if (valid && a.dres) dres_raw[i] = *reinterpret_cast<const uint4*>(a.dres + (int64_t)row * a.H + col);
+    }
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       const int col = ((i * W + wi) * 32 + lane) * 8;
@@ -351,10 +363,13 @@ __global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const LnBwdArgs a) 
 #pragma unroll
       for (int j = 0; j < 8; ++j) d[j] = has_ln ? rs * (g[i][j] - m1 - xh[i][j] * m2) : g[i][j];
       if (a.dres) {
-        float e[8];
-        load8(a.dres + (int64_t)row * a.H + col, e);
+        const uint32_t w[4] = {dres_raw[i].x, dres_raw[i].y, dres_raw[i].z, dres_raw[i].w};
 #pragma unroll
-        for (int j = 0; j < 8; ++j) d[j] += e[j];
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = unpack_bf16x2(w[j]);
+          d[2 * j] += f.x;
+          d[2 * j + 1] += f.y;
+        }
       }
       round8(d);
       if (a.dr_out) store8(a.dr_out + (int64_t)row * a.H + col, d);
@@ -651,10 +666,19 @@ extern "C" int smpk_bdr_ln_fwd(const void* x, const void* bias, const void* resi
                             p_drop, seed, layer, site, row_offset, stream);
 }
 
+// The backward keeps per-column accumulators in registers (two CTAs per SM): one wave of
+// 2 x #SM persistent CTAs, each flushing its column partials once.
+static int ln_bwd_grid_geo(int M, int W) {
+  const int rows_per_cta = (ROW_THREADS / 32) / W;
+  const int need = (M + rows_per_cta - 1) / rows_per_cta;
+  const int cap = 2 * num_sms();
+  return need < cap ? need : cap;
+}
+
 static int64_t ln_bwd_grid(int M, int H) {
   RowGeom geo;
   if (!row_geom(H, geo)) return 0;
-  return row_grid(M, geo.W);
+  return ln_bwd_grid_geo(M, geo.W);
 }
 
 extern "C" int64_t smpk_ln_bwd_workspace(int M, int H) { return ln_bwd_grid(M, H) * 3 * (int64_t)H * 4; }
@@ -672,7 +696,7 @@ extern "C" int smpk_ln_bwd_ex(const void* dy, int nslots, int64_t slot_stride, c
                "smpk_ln_bwd: null argument");
   SMPK_REQUIRE(p_drop == 0.f || dsub_out, SMPK_ERR_BAD_ARG, "smpk_ln_bwd: dropout backward needs dsub_out");
   SMPK_REQUIRE(npeers == 0 || out_peers, SMPK_ERR_BAD_ARG, "smpk_ln_bwd: null peer table");
-  const int grid = row_grid(M, geo.W);
+  const int grid = ln_bwd_grid_geo(M, geo.W);
   SMPK_REQUIRE(workspace && workspace_bytes >= (int64_t)grid * 3 * H * 4, SMPK_ERR_BAD_ARG,
                "smpk_ln_bwd: workspace too small (%lld < %lld)", (long long)workspace_bytes,
                (long long)grid * 3 * H * 4);
@@ -703,22 +727,33 @@ extern "C" int smpk_ln_bwd(const void* dy, const void* r, const float* mean, con
 }
 
 // Vectorised column partials: thread = 8 consecutive columns (one 16-B load per row),
-// 8 row groups per block interleaved over a 256-row chunk, summed in order in smem.
+// 8 row groups per block interleaved over a RPC-row chunk, summed in order in smem.
+template <int RPC>
 __global__ void __launch_bounds__(256) colsum_partial_vec_kernel(const bf16* x, int M, int N, int64_t ldx,
                                                                  float* partials) {
   __shared__ float sm[8][32 * 8 + 1];
   const int t = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int col0 = (blockIdx.x * 32 + t) * 8;
-  const int r0 = blockIdx.y * 256;
-  const int r1 = min(M, r0 + 256);
+  const int r0 = blockIdx.y * RPC;
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (col0 < N) {
-#pragma unroll 4
-    for (int r = r0 + grp; r < r1; r += 8) {
-      float v[8];
-      load8(x + (int64_t)r * ldx + col0, v);
+    // all RPC/8 loads of this thread in flight at once
+    uint4 u[RPC / 8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j] += v[j];
+    for (int k = 0; k < RPC / 8; ++k) {
+      const int r = min(r0 + grp + 8 * k, M - 1);  // clamped (re-read) rows are masked below
+      u[k] = *reinterpret_cast<const uint4*>(x + (int64_t)r * ldx + col0);
+    }
+#pragma unroll
+    for (int k = 0; k < RPC / 8; ++k) {
+      if (r0 + grp + 8 * k >= M) continue;
+      const uint32_t w[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = unpack_bf16x2(w[j]);
+        acc[2 * j] += f.x;
+        acc[2 * j + 1] += f.y;
+      }
     }
   }
 #pragma unroll
@@ -734,33 +769,43 @@ __global__ void __launch_bounds__(256) colsum_partial_vec_kernel(const bf16* x, 
   }
 }
 
+// rows per partial chunk: enough blocks to cover every SM twice, at most 256 rows
+static int colsum_rpc(int M, int N) {
+  const int cblocks = (N + 255) / 256;
+  for (int rpc = 256; rpc > 64; rpc >>= 1)
+    if ((int64_t)cblocks * ((M + rpc - 1) / rpc) >= 2 * num_sms()) return rpc;
+  return 64;
+}
+
 extern "C" int64_t smpk_colsum_workspace(int M, int N) {
-  int chunks = (M + 255) / 256;
-  return (int64_t)chunks * N * 4;
+  if (M <= 0 || N <= 0) return 0;
+  const int rpc = colsum_rpc(M, N);
+  return (int64_t)((M + rpc - 1) / rpc) * N * 4;
 }
 
 extern "C" int smpk_colsum(const void* x, int M, int N, int64_t ldx, void* out, int out_f32, int accumulate,
                            void* workspace, int64_t workspace_bytes, void* stream) {
   SMPK_REQUIRE(M > 0 && N > 0 && x && out, SMPK_ERR_BAD_ARG, "smpk_colsum: bad arguments");
-  const int chunks = (M + 255) / 256;
+  const bool vec = (N % 8 == 0) && (ldx % 8 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
+  const int rpc = vec ? colsum_rpc(M, N) : 256;
+  const int chunks = (M + rpc - 1) / rpc;
   SMPK_REQUIRE(workspace && workspace_bytes >= (int64_t)chunks * N * 4, SMPK_ERR_BAD_ARG,
                "smpk_colsum: workspace too small");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const bool vec = (N % 8 == 0) && (ldx % 8 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
+  dim3 g1((N + 255) / 256, chunks);
+  float* ws = reinterpret_cast<float*>(workspace);
+  const bf16* xb = reinterpret_cast<const bf16*>(x);
   if (vec) {
-    dim3 g1((N + 255) / 256, chunks);
-    colsum_partial_vec_kernel<<<g1, 256, 0, st>>>(reinterpret_cast<const bf16*>(x), M, N, ldx,
-                                                  reinterpret_cast<float*>(workspace));
+    if (rpc == 256) colsum_partial_vec_kernel<256><<<g1, 256, 0, st>>>(xb, M, N, ldx, ws);
+    else if (rpc == 128) colsum_partial_vec_kernel<128><<<g1, 256, 0, st>>>(xb, M, N, ldx, ws);
+    else colsum_partial_vec_kernel<64><<<g1, 256, 0, st>>>(xb, M, N, ldx, ws);
   } else {
-    dim3 g1((N + 255) / 256, chunks);
-    colsum_partial_kernel<<<g1, 256, 0, st>>>(reinterpret_cast<const bf16*>(x), M, N, ldx, 256,
-                                              reinterpret_cast<float*>(workspace));
+    colsum_partial_kernel<<<g1, 256, 0, st>>>(xb, M, N, ldx, 256, ws);
   }
   int rc = check_launch("smpk_colsum");
   if (rc) return rc;
   dim3 g2((N + 31) / 32, 1);
-  colsum_reduce_kernel<<<g2, 256, 0, st>>>(reinterpret_cast<float*>(workspace), chunks, 1, N, out, nullptr, nullptr,
-                                           out_f32, accumulate);
+  colsum_reduce_kernel<<<g2, 256, 0, st>>>(ws, chunks, 1, N, out, nullptr, nullptr, out_f32, accumulate);
   return check_launch("smpk_colsum(reduce)");
 }
 
