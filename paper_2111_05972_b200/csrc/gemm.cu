@@ -439,7 +439,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensor
       const int row = row0 + lane;
       const int64_t c_off = (int64_t)b1 * g.c_bs1 + (int64_t)b2 * g.c_bs2;
       const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16);
-      if (PAIR || g.splits == 1) {
+      if (g.splits == 1) {
 #pragma unroll 1
         for (int i = 0; i < CPW; ++i) {
           const int ch = cgroup + 4 * i;
@@ -492,11 +492,14 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensor
             epilogue_direct32<EPI, F32OUT>(g, row, col0, c_off, v, pre);
           }
         }
-      } else if constexpr (!PAIR) {
-        // split-K: raw fp32 partial tile of this split -> ws, column-major inside the tile so
-        // that a warp's store of one accumulator column is one contiguous 128-byte line
+      } else {
+        // split-K: raw fp32 partial of this CTA's 128 x BN block -> ws, column-major inside the
+        // block so that a warp's store of one accumulator column is one contiguous 128-byte line
+        constexpr int HALVES = PAIR ? 2 : 1;
         const int split = u / g.num_tiles;
-        float* part = g.ws + ((int64_t)split * g.num_tiles + tile) * (BM * BN) + rl;
+        const int sidx = tile * HALVES + (int)rank;  // this CTA's block of the tile
+        const int64_t blk = (int64_t)BM * BN;
+        float* part = g.ws + ((int64_t)split * g.num_tiles * HALVES + sidx) * blk + rl;
 #pragma unroll 1
         for (int i = 0; i < CPW; ++i) {
           const int ch = cgroup + 4 * i;
@@ -511,19 +514,23 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensor
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty_bar[acc]);
-        // all splits of a tile are co-resident (host guarantees num_units <= grid == #CTAs):
-        // wait for every partial, then this split reduces its stripe of the tile's rows in
-        // split order (deterministic) and runs the epilogue on it.
+        if (lane == 0) {
+          if constexpr (PAIR) mbar_arrive_cluster(&tempty_bar[acc], 0);
+          else mbar_arrive(&tempty_bar[acc]);
+        }
+        // all splits of a tile are co-resident (host guarantees num_units <= grid slots): wait
+        // for every partial, then this split reduces its stripe of the block's rows in split
+        // order (deterministic) and runs the epilogue on it.
         __threadfence();
         named_barrier_sync(1, 32 * NUM_EPI_WARPS);
         if (etid == 0) {
-          atomicAdd(g.sem + tile, 1);
-          while (ld_acquire_gpu(g.sem + tile) < g.splits) __nanosleep(32);
+          const int nblk = g.num_tiles * HALVES;
+          atomicAdd(g.sem + sidx, 1);
+          while (ld_acquire_gpu(g.sem + sidx) < g.splits) __nanosleep(32);
           // last one out re-arms both counters for the next launch
-          if (atomicAdd(g.sem + g.num_tiles + tile, 1) == g.splits - 1) {
-            g.sem[tile] = 0;
-            g.sem[g.num_tiles + tile] = 0;
+          if (atomicAdd(g.sem + nblk + sidx, 1) == g.splits - 1) {
+            g.sem[sidx] = 0;
+            g.sem[nblk + sidx] = 0;
           }
         }
         named_barrier_sync(1, 32 * NUM_EPI_WARPS);
@@ -532,14 +539,14 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensor
         const int r0 = split * rows_per;
         const int nrows = min(rows_per, BM - r0);
         const int ngroups = (nrows + 31) >> 5;  // 32-row groups: lane = row
-        const int64_t sstride = (int64_t)g.num_tiles * (BM * BN);
-        const float* tbase = g.ws + (int64_t)tile * (BM * BN);
+        const int64_t sstride = (int64_t)g.num_tiles * HALVES * blk;
+        const float* tbase = g.ws + (int64_t)sidx * blk;
         const int ewarp = etid >> 5;
         for (int item = ewarp; item < ngroups * NCH; item += NUM_EPI_WARPS) {
           const int rg = item / NCH;
           const int ch = item - rg * NCH;
           const int rr = r0 + rg * 32 + lane;
-          const int grow = tm * BM + rr;
+          const int grow = tm * BMT + (int)rank * BM + rr;
           const int col0 = tn * BN + ch * 32;
           if (rr >= r0 + nrows || grow >= g.M || col0 >= g.N) continue;
           float v[32];
@@ -725,7 +732,7 @@ static int dispatch_epilogue(const CUtensorMap& ta, const CUtensorMap& tb, const
 // splitting adds a fixed sync/fix-up cost and the fp32 partial round trip through L2.
 // Splits are only used while every unit fits in one wave (the fix-up waits for all splits
 // of a tile, so all of them must be co-resident).
-static int choose_splits(int num_tiles, int num_kb, int BN, int nsm) {
+static int choose_splits(int num_tiles, int num_kb, int BN, int nsm, int halves) {
   const double t_kb = 2.0 * BM * BN * BK / 9.0e6;  // us per k-block (~1.33 PFLOP/s over 148 SMs)
   const double t_unit = 1.5, t_fix = 3.0, l2_bytes_per_us = 12.0e6;
   double best = ((num_tiles + nsm - 1) / nsm) * (num_kb * t_kb + t_unit);
@@ -734,7 +741,8 @@ static int choose_splits(int num_tiles, int num_kb, int BN, int nsm) {
     const int kb_per = (num_kb + s - 1) / s;
     if (kb_per < 4) break;
     const int se = (num_kb + kb_per - 1) / kb_per;
-    const double t = kb_per * t_kb + t_unit + t_fix + 2.0 * se * num_tiles * BM * BN * 4.0 / l2_bytes_per_us;
+    const double t =
+        kb_per * t_kb + t_unit + t_fix + 2.0 * se * num_tiles * halves * BM * BN * 4.0 / l2_bytes_per_us;
     if (t < best * 0.95) {
       best = t;
       best_s = se;
@@ -755,17 +763,28 @@ static bool pair_enabled() {
 
 static int pick_bn(int N) { return N <= 64 ? 64 : (N <= 128 ? 128 : 256); }
 
-static void plan_gemm(int M, int N, int K, int nb1, int nb2, int& BN, int& tiles, int& num_kb, int& splits,
-                      int& kb_per) {
+// Tile plan: CTA pairs (256-row tiles, cta_group::2) whenever N >= 128 and M >= 256, else
+// single CTAs; then the split-K count for that tile grid (pairs occupy two SMs per unit).
+static void plan_gemm(int M, int N, int K, int nb1, int nb2, int& BN, bool& pair, int& tiles, int& num_kb,
+                      int& splits, int& kb_per) {
   BN = pick_bn(N);
-  tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * nb1 * nb2;
+  pair = BN >= 128 && M >= 2 * BM && pair_enabled();
+  const int rows = pair ? 2 * BM : BM;
+  tiles = ((M + rows - 1) / rows) * ((N + BN - 1) / BN) * nb1 * nb2;
   num_kb = (K + BK - 1) / BK;
-  splits = choose_splits(tiles, num_kb, BN, num_sms());
+  splits = choose_splits(tiles, num_kb, BN, pair ? num_sms() / 2 : num_sms(), pair ? 2 : 1);
+  if (pair && splits > 1) {
+    // measured: split-K runs faster on single-CTA tiles (finer units, shorter fix-up)
+    pair = false;
+    tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * nb1 * nb2;
+    splits = choose_splits(tiles, num_kb, BN, num_sms(), 1);
+  }
   kb_per = (num_kb + splits - 1) / splits;
 }
 
-static int64_t splitk_ws_bytes(int BN, int tiles, int splits) {
-  return splits > 1 ? (int64_t)splits * tiles * BM * BN * 4 : 0;
+// fp32 partial tiles of every (split, tile, CTA of the pair)
+static int64_t splitk_ws_bytes(int BN, bool pair, int tiles, int splits) {
+  return splits > 1 ? (int64_t)splits * tiles * (pair ? 2 : 1) * BM * BN * 4 : 0;
 }
 
 // Per-device split-K arrival counters (zeroed once, re-armed by every launch that uses them);
@@ -802,8 +821,9 @@ using namespace smpk;
 extern "C" int64_t smpk_gemm_workspace(int M, int N, int K, int nb1, int nb2) {
   if (M <= 0 || N <= 0 || K <= 0 || nb1 <= 0 || nb2 <= 0) return 0;
   int BN, tiles, num_kb, splits, kb_per;
-  plan_gemm(M, N, K, nb1, nb2, BN, tiles, num_kb, splits, kb_per);
-  return splitk_ws_bytes(BN, tiles, splits);
+  bool pair;
+  plan_gemm(M, N, K, nb1, nb2, BN, pair, tiles, num_kb, splits, kb_per);
+  return splitk_ws_bytes(BN, pair, tiles, splits);
 }
 
 static int gemm_impl(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, int64_t a_bs2, const void* b,
@@ -824,14 +844,12 @@ static int gemm_impl(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, 
   SMPK_REQUIRE(!(need_aux && c_f32), SMPK_ERR_UNSUPPORTED, "smpk_gemm: aux epilogues need bf16 C");
 
   int BN, tiles, num_kb, splits, kb_per;
-  plan_gemm(M, N, K, nb1, nb2, BN, tiles, num_kb, splits, kb_per);
-  if (npeers || splits > 1 && (workspace == nullptr || workspace_bytes < splitk_ws_bytes(BN, tiles, splits))) {
+  bool pair;
+  plan_gemm(M, N, K, nb1, nb2, BN, pair, tiles, num_kb, splits, kb_per);
+  if (npeers || splits > 1 && (workspace == nullptr || workspace_bytes < splitk_ws_bytes(BN, pair, tiles, splits))) {
     splits = 1;  // no (or too small a) workspace: single pass over K
     kb_per = num_kb;
   }
-  // CTA-pair (cta_group::2, 256-row tiles) for every unsplit GEMM with N >= 128 and M >= 256
-  const bool pair = splits == 1 && BN >= 128 && M >= 2 * BM && pair_enabled();
-  if (pair) tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN) * nb1 * nb2;
 
   CUtensorMap ta, tb;
   int rc = make_operand_map(&ta, a, a_mn_major, M, K, lda, nb1, a_bs1, nb2, a_bs2, BM, "A");
@@ -858,7 +876,7 @@ static int gemm_impl(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, 
     SMPK_REQUIRE((reinterpret_cast<uintptr_t>(workspace) & 15) == 0, SMPK_ERR_BAD_ARG,
                  "smpk_gemm: workspace must be 16-byte aligned");
     int rc2;
-    g.sem = splitk_semaphores(tiles, rc2);
+    g.sem = splitk_semaphores(tiles * (pair ? 2 : 1), rc2);
     if (rc2) return rc2;
   }
   g.a_mn = a_mn_major ? 1 : 0;
