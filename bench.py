@@ -213,7 +213,7 @@ def run_gpu(args, rank, world, local):
     from paper_2111_05972_b200 import _lib, kernels
 
     torch.cuda.set_device(local)
-    smp.init({"tensor_parallel_degree": world, "optimize": "speed", "seed": 1234, "tp_comm": args.tp_comm})
+    smp.init({"tensor_parallel_degree": world, "optimize": args.optimize, "seed": 1234, "tp_comm": args.tp_comm})
     torch.manual_seed(1000 + rank)
     model = smp.nn.DistributedTransformer(**CFG)
     model.train()
@@ -336,7 +336,7 @@ def run_gpu(args, rank, world, local):
         "config": {"workload": "bert-large-24L-tp-layer-stack (BASELINE.json configs[1])",
                    "model": "BERT-large DistributedTransformer 24L H1024 16x64 FFN4096 post-LN gelu dropout0.1",
                    "global_batch": B * world, "per_gpu_batch": B, "seq_len": s,
-                   "parallelism": f"tp{world} (speed mode, TP across DP ranks)",
+                   "parallelism": f"tp{world} ({args.optimize} mode, TP across DP ranks)",
                    "l2": "inputs larger than L2 (saved activations ~6 GB per step)"},
         "mfu": {"model_tflops_per_gpu": model_tflops, "flops_per_token": flops_tok,
                 "frac_of_sustained": model_tflops / peak_sus, "frac_of_burst": model_tflops / peaks["bf16_tflops"],
@@ -364,6 +364,8 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--graph", type=int, default=1, help="capture the step in a CUDA graph (1) or run eagerly (0)")
+    ap.add_argument("--optimize", default="speed", choices=["speed", "memory"],
+                    help="smp optimize mode of the TP layers (PAPER.md:763); the headline is speed")
     ap.add_argument("--tp-comm", default="peer", choices=["peer", "nccl"],
                     help="TP collectives: fused NVLink peer stores (default) or NCCL calls")
     ap.add_argument("--trace", default="", help="diagnostics: write a per-kernel CUPTI trace summary to PREFIX_rankR.txt")

@@ -77,8 +77,9 @@ SMPK_API int smpk_device_info(int* num_sms, int* cc_major, int* cc_minor);
  *      b_mn_major == 1 -> B[n,k] = b[k*ldb + n]   (row-major K x N)
  *   C: row-major M x N with ldc; bf16, or fp32 when c_f32 != 0.
  *   Batch: nb1 x nb2 problems; problem (i1,i2) offsets every operand by
- *   i1*x_bs1 + i2*x_bs2 elements.  aux (for BIAS_ACT / DACT / ADD) is bf16,
- *   row-major with ldaux and the same batch strides as C.
+ *   i1*x_bs1 + i2*x_bs2 elements (a zero A / B batch stride broadcasts that operand).
+ *   aux (for BIAS_ACT / DACT / ADD) is bf16, row-major with ldaux and the same batch
+ *   strides as C.
  */
 SMPK_API int smpk_gemm(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, int64_t a_bs2,
               const void* b, int b_mn_major, int64_t ldb, int64_t b_bs1, int64_t b_bs2,
@@ -270,6 +271,36 @@ SMPK_API int smpk_ln_bwd_ex(const void* dy, int nslots, int64_t slot_stride, con
                             void* dbias, int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed,
                             int layer, int site, int64_t row_offset, void* workspace, int64_t workspace_bytes,
                             void* stream);
+/*
+ * Channel-sharded (memory-mode) LayerNorm, "local sum x, sum x^2 -> scalar
+ * allreduce -> ApplyLayerNorm": activations hold H/T of the H_total channels.
+ *   smpk_bdr_ln_fwd_dist  as smpk_bdr_ln_fwd on the local columns, with the hidden-dropout column
+ *                         index offset by col_offset; row_sums_out != NULL stores the partial
+ *                         [M][2] (sum r, sum r^2); ext_sums != NULL normalises with the group's
+ *                         sums (mean = S1/H_total, var = S2/H_total - mean^2).
+ *   smpk_ln_bwd_dist      as smpk_ln_bwd; row_sums_out != NULL is a sums-only pass storing the
+ *                         partial [M][2] (sum g, sum g*xhat; g = dy*gamma); ext_sums != NULL uses
+ *                         the group's sums for the row means of the LayerNorm backward.
+ * The [M][2] partials are summed across the TP group (NCCL allreduce) between the passes.
+ */
+SMPK_API int smpk_bdr_ln_fwd_dist(const void* x, const void* bias, const void* residual, void* r_out,
+                                  const void* gamma, const void* beta, void* y_out, float* mean, float* rstd, int M,
+                                  int H, float eps, float p_drop, uint64_t seed, int layer, int site,
+                                  int64_t row_offset, int64_t col_offset, float* row_sums_out, const float* ext_sums,
+                                  int H_total, void* stream);
+SMPK_API int smpk_ln_bwd_dist(const void* dy, const void* r, const float* mean, const float* rstd, const void* gamma,
+                              const void* dres, void* dr_out, void* dsub_out, void* dgamma, void* dbeta, void* dbias,
+                              int grads_f32, int M, int H, float p_drop, uint64_t seed, int layer, int site,
+                              int64_t row_offset, int64_t col_offset, float* row_sums_out, const float* ext_sums,
+                              int H_total, void* workspace, int64_t workspace_bytes, void* stream);
+/*
+ * smpk_bias_act_fwd — pre = bf16(x + bias) (bias per column), y = act(pre); [M, N] row-major.
+ * smpk_act_bwd      — dx = dy * act'(pre).  The MLP activation of memory mode, which follows a
+ * reduce-scatter and so cannot be fused into the GEMM epilogue.
+ */
+SMPK_API int smpk_bias_act_fwd(const void* x, const void* bias, int M, int N, int act, void* pre_out, void* y,
+                               void* stream);
+SMPK_API int smpk_act_bwd(const void* dy, const void* pre, int M, int N, int act, void* dx, void* stream);
 SMPK_API int smpk_symm_export(void* ptr, void* handle_out, int64_t* offset);
 SMPK_API int smpk_symm_barrier(void* const* peer_flags, void* local_flags, int T, int rank, double timeout_s,
                                void* stream);

@@ -43,6 +43,10 @@ SIGNATURES: dict[str, list] = {
     "smpk_flash_attn_bwd": [P, L, P, L, P, L, P, I, I, I, I, P, P, F, I, F, P, P, L, P],
     "smpk_gemm_rs": [P, I, L, P, I, L, P, I, L, L, L, I, I, I, P],
     "smpk_bdr_ln_fwd_ex": [P, I, L, P, P, P, P, P, P, P, P, P, I, L, I, I, F, F, C.c_uint64, I, I, L, P],
+    "smpk_bdr_ln_fwd_dist": [P, P, P, P, P, P, P, P, P, I, I, F, F, C.c_uint64, I, I, L, L, P, P, I, P],
+    "smpk_ln_bwd_dist": [P, P, P, P, P, P, P, P, P, P, P, I, I, I, F, C.c_uint64, I, I, L, L, P, P, I, P, L, P],
+    "smpk_bias_act_fwd": [P, P, I, I, I, P, P, P],
+    "smpk_act_bwd": [P, P, I, I, I, P, P],
     "smpk_ln_bwd_ex": [P, I, L, P, P, P, P, P, P, P, P, I, L, P, P, P, I, I, I, I, F, C.c_uint64, I, I, L, P, L, P],
     "smpk_symm_export": [P, P, C.POINTER(L)],
     "smpk_symm_barrier": [P, P, I, I, C.c_double, P],
@@ -98,13 +102,15 @@ def lib() -> C.CDLL:
 
 
 # kernels launched by each entry point (for bench.py's gpu_launches count)
-LAUNCHES_PER_CALL = {"smpk_ln_bwd": 2, "smpk_ln_bwd_ex": 2, "smpk_colsum": 2, "smpk_flash_attn_bwd": 3}
+LAUNCHES_PER_CALL = {"smpk_ln_bwd": 2, "smpk_ln_bwd_ex": 2, "smpk_ln_bwd_dist": 2, "smpk_colsum": 2, "smpk_flash_attn_bwd": 3}
 launch_count = 0
 
 
-def call(name: str, *args) -> None:
+def call(name: str, *args, launches: int | None = None) -> None:
+    """Invoke an ABI entry point; launches overrides the per-entry kernel count it adds to
+    launch_count (entries whose second reduction kernel is conditional)."""
     global launch_count
-    launch_count += LAUNCHES_PER_CALL.get(name, 1)
+    launch_count += LAUNCHES_PER_CALL.get(name, 1) if launches is None else launches
     rc = getattr(lib(), name)(*args)
     if rc != 0:
         raise_for(rc, lib().smpk_last_error().decode(errors="replace"))

@@ -35,6 +35,8 @@ struct GemmArgs {
   int nb1, nb2;
   int tiles_m, tiles_n, num_tiles, num_kb;
   int a_mn, b_mn;
+  // batch dims in which an operand is broadcast (batch stride 0): its TMA coordinate stays 0
+  int a_bc1, a_bc2, b_bc1, b_bc2;
   void* c;
   int c_f32;
   int64_t ldc, c_bs1, c_bs2;
@@ -319,6 +321,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensor
         decode_tile(g, tile, b1, b2, tm, tn);
         const int arow = tm * BMT + (int)rank * BM;
         const int brow = tn * BN + (int)rank * BNL;
+        const int ab1 = g.a_bc1 ? 0 : b1, ab2 = g.a_bc2 ? 0 : b2;
+        const int bb1 = g.b_bc1 ? 0 : b1, bb2 = g.b_bc2 ? 0 : b2;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
@@ -326,34 +330,34 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensor
           if constexpr (PAIR) {
             if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::STAGE_BYTES);
             if (!g.a_mn) {
-              tma_load_4d_pair(a_dst, tmA, &full_bar[stage], kb * BK, arow, b1, b2);
+              tma_load_4d_pair(a_dst, tmA, &full_bar[stage], kb * BK, arow, ab1, ab2);
             } else {
 #pragma unroll
               for (int i = 0; i < BM / 64; ++i)
-                tma_load_4d_pair(a_dst + i * (BK * 128), tmA, &full_bar[stage], arow + i * 64, kb * BK, b1, b2);
+                tma_load_4d_pair(a_dst + i * (BK * 128), tmA, &full_bar[stage], arow + i * 64, kb * BK, ab1, ab2);
             }
             if (!g.b_mn) {
-              tma_load_4d_pair(b_dst, tmB, &full_bar[stage], kb * BK, brow, b1, b2);
+              tma_load_4d_pair(b_dst, tmB, &full_bar[stage], kb * BK, brow, bb1, bb2);
             } else {
 #pragma unroll
               for (int i = 0; i < BNL / 64; ++i)
-                tma_load_4d_pair(b_dst + i * (BK * 128), tmB, &full_bar[stage], brow + i * 64, kb * BK, b1, b2);
+                tma_load_4d_pair(b_dst + i * (BK * 128), tmB, &full_bar[stage], brow + i * 64, kb * BK, bb1, bb2);
             }
           } else {
             mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
             if (!g.a_mn) {
-              tma_load_4d(a_dst, tmA, &full_bar[stage], kb * BK, arow, b1, b2);
+              tma_load_4d(a_dst, tmA, &full_bar[stage], kb * BK, arow, ab1, ab2);
             } else {
 #pragma unroll
               for (int i = 0; i < BM / 64; ++i)
-                tma_load_4d(a_dst + i * (BK * 128), tmA, &full_bar[stage], arow + i * 64, kb * BK, b1, b2);
+                tma_load_4d(a_dst + i * (BK * 128), tmA, &full_bar[stage], arow + i * 64, kb * BK, ab1, ab2);
             }
             if (!g.b_mn) {
-              tma_load_4d(b_dst, tmB, &full_bar[stage], kb * BK, brow, b1, b2);
+              tma_load_4d(b_dst, tmB, &full_bar[stage], kb * BK, brow, bb1, bb2);
             } else {
 #pragma unroll
               for (int i = 0; i < BNL / 64; ++i)
-                tma_load_4d(b_dst + i * (BK * 128), tmB, &full_bar[stage], brow + i * 64, kb * BK, b1, b2);
+                tma_load_4d(b_dst + i * (BK * 128), tmB, &full_bar[stage], brow + i * 64, kb * BK, bb1, bb2);
             }
           }
           if (++stage == STAGES) {
@@ -852,9 +856,13 @@ static int gemm_impl(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, 
   }
 
   CUtensorMap ta, tb;
-  int rc = make_operand_map(&ta, a, a_mn_major, M, K, lda, nb1, a_bs1, nb2, a_bs2, BM, "A");
+  // an operand with batch stride 0 is broadcast over that batch dim (one map slice, coordinate 0)
+  const bool a_bc1 = nb1 > 1 && a_bs1 == 0, a_bc2 = nb2 > 1 && a_bs2 == 0;
+  const bool b_bc1 = nb1 > 1 && b_bs1 == 0, b_bc2 = nb2 > 1 && b_bs2 == 0;
+  int rc = make_operand_map(&ta, a, a_mn_major, M, K, lda, a_bc1 ? 1 : nb1, a_bs1, a_bc2 ? 1 : nb2, a_bs2, BM, "A");
   if (rc) return rc;
-  rc = make_operand_map(&tb, b, b_mn_major, N, K, ldb, nb1, b_bs1, nb2, b_bs2, pair ? BN / 2 : BN, "B");
+  rc = make_operand_map(&tb, b, b_mn_major, N, K, ldb, b_bc1 ? 1 : nb1, b_bs1, b_bc2 ? 1 : nb2, b_bs2,
+                        pair ? BN / 2 : BN, "B");
   if (rc) return rc;
 
   GemmArgs g;
@@ -880,6 +888,10 @@ static int gemm_impl(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, 
     if (rc2) return rc2;
   }
   g.a_mn = a_mn_major ? 1 : 0;
+  g.a_bc1 = a_bc1;
+  g.a_bc2 = a_bc2;
+  g.b_bc1 = b_bc1;
+  g.b_bc2 = b_bc2;
   g.b_mn = b_mn_major ? 1 : 0;
   g.c = c;
   g.c_f32 = c_f32 ? 1 : 0;

@@ -78,9 +78,11 @@ struct RowGeom {
 
 // Prefer <= 2 uint4 chunks per lane (register pressure / occupancy of the
 // memory-bound row kernels), spreading a row over up to 8 warps.
+// H need only be a multiple of 8: the last 256-column chunk may be partial (lanes past H idle),
+// which the channel-sharded (memory-mode) widths H/T and 3H/T need.
 static bool row_geom(int H, RowGeom& g) {
-  if (H <= 0 || H % 256) return false;
-  const int n = H / 256;
+  if (H <= 0 || H % 8) return false;
+  const int n = (H + 255) / 256;
   for (int W = 1; W <= 8; W *= 2) {
     if (n % W) continue;
     const int v = n / W;
@@ -135,6 +137,12 @@ struct BdrLnArgs {
   bf16* const* out_peers;
   int npeers;
   int64_t peer_off;
+  // channel-sharded LayerNorm (memory mode): dropout column offset of this shard; partial
+  // row sums (sum r, sum r^2 over the local columns) out; or the group's row sums in
+  int64_t col_offset;
+  float* row_sums_out;
+  const float* ext_sums;
+  int H_total;
 };
 
 __device__ __forceinline__ void load8_slots(const bf16* p, int nslots, int64_t stride, float (&v)[8]) {
@@ -171,7 +179,7 @@ __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       const int col = ((i * W + wi) * 32 + lane) * 8;
-      if (valid) {
+      if (valid && col < a.H) {
         load8_slots(a.x + (int64_t)row * a.H + col, a.nslots, a.slot_stride, v[i]);
         if (a.residual) load8(a.residual + (int64_t)row * a.H + col, res[i]);
       }
@@ -179,7 +187,7 @@ __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       const int col = ((i * W + wi) * 32 + lane) * 8;
-      if (valid) {
+      if (valid && col < a.H) {
         if (a.bias) {
           float b[8];
           load8(a.bias + col, b);
@@ -188,7 +196,8 @@ __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs
         }
         if (a.p > 0.f) {
           bool keep[8];
-          dropout_keep8(a.seed, a.layer, a.site, (uint64_t)(a.row_offset + row), col, dropout_threshold(a.p), keep);
+          dropout_keep8(a.seed, a.layer, a.site, (uint64_t)(a.row_offset + row), (int)(a.col_offset + col),
+                        dropout_threshold(a.p), keep);
 #pragma unroll
           for (int j = 0; j < 8; ++j) v[i][j] = keep[j] ? v[i][j] * inv_keep : 0.f;
         }
@@ -204,22 +213,46 @@ __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs
         for (int j = 0; j < 8; ++j) v[i][j] = 0.f;
       }
     }
-    if (a.gamma == nullptr) continue;  // uniform across the CTA
-    float s = 0.f;
+    if (a.row_sums_out) {  // partial row sums of r over this shard's columns (uniform branch)
+      float s = 0.f, q = 0.f;
 #pragma unroll
-    for (int i = 0; i < VPT; ++i)
+      for (int i = 0; i < VPT; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) s += v[i][j];
-    const float mu = group_sum<W>(s, sm, slot, wi) / a.H;
-    float q = 0.f;
-#pragma unroll
-    for (int i = 0; i < VPT; ++i)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        float d = v[i][j] - mu;
-        q += d * d;
+        for (int j = 0; j < 8; ++j) {
+          s += v[i][j];
+          q += v[i][j] * v[i][j];
+        }
+      s = group_sum<W>(s, sm, slot, wi);
+      q = group_sum<W>(q, sm + 8, slot, wi);
+      if (valid && wi == 0 && lane == 0) {
+        a.row_sums_out[2 * (int64_t)row] = s;
+        a.row_sums_out[2 * (int64_t)row + 1] = q;
       }
-    const float var = group_sum<W>(q, sm + 8, slot, wi) / a.H;
+    }
+    if (a.gamma == nullptr) continue;  // uniform across the CTA
+    float mu, var;
+    if (a.ext_sums) {  // the TP group's row sums: mean = S1/n, var = S2/n - mean^2
+      mu = valid ? a.ext_sums[2 * (int64_t)row] / a.H_total : 0.f;
+      var = valid ? fmaxf(a.ext_sums[2 * (int64_t)row + 1] / a.H_total - mu * mu, 0.f) : 0.f;
+    } else {
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < VPT; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s += v[i][j];
+      mu = group_sum<W>(s, sm, slot, wi) / a.H;
+      float q = 0.f;
+#pragma unroll
+      for (int i = 0; i < VPT; ++i) {
+        if (((i * W + wi) * 32 + lane) * 8 >= a.H) continue;  // idle lanes of a partial chunk
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float d = v[i][j] - mu;
+          q += d * d;
+        }
+      }
+      var = group_sum<W>(q, sm + 8, slot, wi) / a.H;
+    }
     const float rs = rsqrtf(var + a.eps);
     if (valid) {
       if (wi == 0 && lane == 0) {
@@ -229,6 +262,7 @@ __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs
 #pragma unroll
       for (int i = 0; i < VPT; ++i) {
         const int col = ((i * W + wi) * 32 + lane) * 8;
+        if (col >= a.H) continue;
         float gm[8], bt[8], o[8];
         load8(a.gamma + col, gm);
         load8(a.beta + col, bt);
@@ -264,16 +298,24 @@ struct LnBwdArgs {
   bf16* const* out_peers;  // dsub also stored to every peer buffer (allgather producer)
   int npeers;
   int64_t peer_off;
+  // channel-sharded LayerNorm (memory mode): dropout column offset; sums-only pass writing the
+  // partial row sums (sum g, sum g*xhat; g = dy*gamma) of the local columns; or the group's sums in
+  int64_t col_offset;
+  float* row_sums_out;
+  const float* ext_sums;
+  int H_total;
 };
 
 template <int W, int VPT>
 __device__ __forceinline__ void flush_partial(const float (&acc)[VPT][8], float* out, float* red, int nslots, int slot,
-                                              int wi, int lane) {
+                                              int wi, int lane, int H) {
   if (nslots == 1) {
 #pragma unroll
-    for (int i = 0; i < VPT; ++i)
+    for (int i = 0; i < VPT; ++i) {
+      if (((i * W + wi) * 32 + lane) * 8 >= H) continue;
 #pragma unroll
       for (int j = 0; j < 8; ++j) out[((i * W + wi) * 32 + lane) * 8 + j] = acc[i][j];
+    }
     return;
   }
   float* buf = red + wi * (VPT * 8 * 32);
@@ -291,9 +333,11 @@ __device__ __forceinline__ void flush_partial(const float (&acc)[VPT][8], float*
   }
   if (slot == nslots - 1) {
 #pragma unroll
-    for (int i = 0; i < VPT; ++i)
+    for (int i = 0; i < VPT; ++i) {
+      if (((i * W + wi) * 32 + lane) * 8 >= H) continue;
 #pragma unroll
       for (int j = 0; j < 8; ++j) out[((i * W + wi) * 32 + lane) * 8 + j] = buf[(i * 8 + j) * 32 + lane];
+    }
   }
   __syncthreads();
 }
@@ -327,14 +371,15 @@ __global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const LnBwdArgs a) 
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       const int col = ((i * W + wi) * 32 + lane) * 8;
-      if (valid && a.dres) dres_raw[i] = *reinterpret_cast<const uint4*>(a.dres + (int64_t)row * a.H + col);
+      if (valid && a.dres && col < a.H)
+        dres_raw[i] = *reinterpret_cast<const uint4*>(a.dres + (int64_t)row * a.H + col);
     }
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       const int col = ((i * W + wi) * 32 + lane) * 8;
-      if (valid && !has_ln) {
+      if (valid && col < a.H && !has_ln) {
         load8_slots(a.dy + (int64_t)row * a.H + col, a.nslots, a.slot_stride, g[i]);
-      } else if (valid) {
+      } else if (valid && col < a.H) {
         float dy[8], gm[8];
         load8(a.r + (int64_t)row * a.H + col, xh[i]);
         load8_slots(a.dy + (int64_t)row * a.H + col, a.nslots, a.slot_stride, dy);
@@ -353,12 +398,28 @@ __global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const LnBwdArgs a) 
         for (int j = 0; j < 8; ++j) xh[i][j] = g[i][j] = 0.f;
       }
     }
-    const float m1 = group_sum<W>(s1, sm, slot, wi) / a.H;
-    const float m2 = group_sum<W>(s2, sm + 8, slot, wi) / a.H;
+    float m1, m2;
+    if (a.ext_sums) {
+      m1 = valid ? a.ext_sums[2 * (int64_t)row] / a.H_total : 0.f;
+      m2 = valid ? a.ext_sums[2 * (int64_t)row + 1] / a.H_total : 0.f;
+    } else {
+      m1 = group_sum<W>(s1, sm, slot, wi);
+      m2 = group_sum<W>(s2, sm + 8, slot, wi);
+      if (a.row_sums_out) {  // sums-only pass (uniform branch)
+        if (valid && wi == 0 && lane == 0) {
+          a.row_sums_out[2 * (int64_t)row] = m1;
+          a.row_sums_out[2 * (int64_t)row + 1] = m2;
+        }
+        continue;
+      }
+      m1 /= a.H;
+      m2 /= a.H;
+    }
     if (!valid) continue;
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       const int col = ((i * W + wi) * 32 + lane) * 8;
+      if (col >= a.H) continue;  // idle lanes of a partial chunk
       float d[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) d[j] = has_ln ? rs * (g[i][j] - m1 - xh[i][j] * m2) : g[i][j];
@@ -375,7 +436,8 @@ __global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const LnBwdArgs a) 
       if (a.dr_out) store8(a.dr_out + (int64_t)row * a.H + col, d);
       if (a.p > 0.f) {
         bool keep[8];
-        dropout_keep8(a.seed, a.layer, a.site, (uint64_t)(a.row_offset + row), col, dropout_threshold(a.p), keep);
+        dropout_keep8(a.seed, a.layer, a.site, (uint64_t)(a.row_offset + row), (int)(a.col_offset + col),
+                      dropout_threshold(a.p), keep);
 #pragma unroll
         for (int j = 0; j < 8; ++j) d[j] = keep[j] ? d[j] * inv_keep : 0.f;
         round8(d);
@@ -388,10 +450,11 @@ __global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const LnBwdArgs a) 
   }
   // CTA partials: warps with the same wi own the same columns; slots are summed
   // in ascending order through shared memory (deterministic).
+  if (a.row_sums_out) return;  // sums-only pass: no column partials
   float* out = a.partials + (int64_t)blockIdx.x * 3 * a.H;
-  flush_partial<W, VPT>(acc_g, out, red, rows_per_cta, slot, wi, lane);
-  flush_partial<W, VPT>(acc_b, out + a.H, red, rows_per_cta, slot, wi, lane);
-  flush_partial<W, VPT>(acc_d, out + 2 * a.H, red, rows_per_cta, slot, wi, lane);
+  flush_partial<W, VPT>(acc_g, out, red, rows_per_cta, slot, wi, lane, a.H);
+  flush_partial<W, VPT>(acc_b, out + a.H, red, rows_per_cta, slot, wi, lane, a.H);
+  flush_partial<W, VPT>(acc_d, out + 2 * a.H, red, rows_per_cta, slot, wi, lane, a.H);
 }
 
 // Reduce P partial rows of [P][K][H] to K outputs of H columns (fixed order).
@@ -632,19 +695,20 @@ static int softmax_nv(int sk) {
 
 using namespace smpk;
 
-extern "C" int smpk_bdr_ln_fwd_ex(const void* x, int nslots, int64_t slot_stride, const void* bias,
-                                  const void* residual, void* r_out, const void* gamma, const void* beta, void* y_out,
-                                  float* mean, float* rstd, void* const* out_peers, int npeers, int64_t peer_off, int M,
-                                  int H, float eps, float p_drop, uint64_t seed, int layer, int site,
-                                  int64_t row_offset, void* stream) {
+static int bdr_ln_impl(const void* x, int nslots, int64_t slot_stride, const void* bias, const void* residual,
+                       void* r_out, const void* gamma, const void* beta, void* y_out, float* mean, float* rstd,
+                       void* const* out_peers, int npeers, int64_t peer_off, int M, int H, float eps, float p_drop,
+                       uint64_t seed, int layer, int site, int64_t row_offset, int64_t col_offset,
+                       float* row_sums_out, const float* ext_sums, int H_total, void* stream) {
   RowGeom geo;
   SMPK_REQUIRE(M >= 0 && row_geom(H, geo) && geom_supported(geo), SMPK_ERR_UNSUPPORTED,
-               "smpk_bdr_ln_fwd: hidden size %d unsupported (need a multiple of 256)", H);
+               "smpk_bdr_ln_fwd: hidden size %d unsupported (need a multiple of 8)", H);
   SMPK_REQUIRE(x != nullptr && nslots >= 1, SMPK_ERR_BAD_ARG, "smpk_bdr_ln_fwd: null x");
   SMPK_REQUIRE(gamma == nullptr || (beta && mean && rstd && (y_out || npeers)), SMPK_ERR_BAD_ARG,
                "smpk_bdr_ln_fwd: LayerNorm needs beta, mean, rstd and an output");
-  SMPK_REQUIRE(gamma != nullptr || r_out != nullptr || npeers > 0, SMPK_ERR_BAD_ARG,
+  SMPK_REQUIRE(gamma != nullptr || r_out != nullptr || npeers > 0 || row_sums_out, SMPK_ERR_BAD_ARG,
                "smpk_bdr_ln_fwd: nothing to compute");
+  SMPK_REQUIRE(!ext_sums || H_total > 0, SMPK_ERR_BAD_ARG, "smpk_bdr_ln_fwd_dist: H_total must be positive");
   SMPK_REQUIRE(npeers == 0 || out_peers != nullptr, SMPK_ERR_BAD_ARG, "smpk_bdr_ln_fwd: null peer table");
   SMPK_REQUIRE(p_drop >= 0.f && p_drop < 1.f, SMPK_ERR_BAD_ARG, "smpk_bdr_ln_fwd: dropout p must be in [0,1)");
   if (M == 0) return SMPK_OK;
@@ -652,11 +716,30 @@ extern "C" int smpk_bdr_ln_fwd_ex(const void* x, int nslots, int64_t slot_stride
               reinterpret_cast<const bf16*>(residual), reinterpret_cast<bf16*>(r_out),
               reinterpret_cast<const bf16*>(gamma), reinterpret_cast<const bf16*>(beta),
               reinterpret_cast<bf16*>(y_out), mean, rstd, M, H, eps, p_drop, seed, (uint32_t)layer, (uint32_t)site,
-              row_offset, nslots, slot_stride, reinterpret_cast<bf16* const*>(out_peers), npeers, peer_off};
+              row_offset, nslots, slot_stride, reinterpret_cast<bf16* const*>(out_peers), npeers, peer_off,
+              col_offset, row_sums_out, ext_sums, H_total};
   const int grid = row_grid(M, geo.W);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   SMPK_DISPATCH_ROW(geo.W, geo.VPT, bdr_ln_fwd_kernel, (grid, ROW_THREADS, 0, st), (a));
   return check_launch("smpk_bdr_ln_fwd");
+}
+
+extern "C" int smpk_bdr_ln_fwd_ex(const void* x, int nslots, int64_t slot_stride, const void* bias,
+                                  const void* residual, void* r_out, const void* gamma, const void* beta, void* y_out,
+                                  float* mean, float* rstd, void* const* out_peers, int npeers, int64_t peer_off, int M,
+                                  int H, float eps, float p_drop, uint64_t seed, int layer, int site,
+                                  int64_t row_offset, void* stream) {
+  return bdr_ln_impl(x, nslots, slot_stride, bias, residual, r_out, gamma, beta, y_out, mean, rstd, out_peers, npeers,
+                     peer_off, M, H, eps, p_drop, seed, layer, site, row_offset, 0, nullptr, nullptr, 0, stream);
+}
+
+extern "C" int smpk_bdr_ln_fwd_dist(const void* x, const void* bias, const void* residual, void* r_out,
+                                    const void* gamma, const void* beta, void* y_out, float* mean, float* rstd,
+                                    int M, int H, float eps, float p_drop, uint64_t seed, int layer, int site,
+                                    int64_t row_offset, int64_t col_offset, float* row_sums_out,
+                                    const float* ext_sums, int H_total, void* stream) {
+  return bdr_ln_impl(x, 1, 0, bias, residual, r_out, gamma, beta, y_out, mean, rstd, nullptr, 0, 0, M, H, eps, p_drop,
+                     seed, layer, site, row_offset, col_offset, row_sums_out, ext_sums, H_total, stream);
 }
 
 extern "C" int smpk_bdr_ln_fwd(const void* x, const void* bias, const void* residual, void* r_out, const void* gamma,
@@ -683,18 +766,22 @@ static int64_t ln_bwd_grid(int M, int H) {
 
 extern "C" int64_t smpk_ln_bwd_workspace(int M, int H) { return ln_bwd_grid(M, H) * 3 * (int64_t)H * 4; }
 
-extern "C" int smpk_ln_bwd_ex(const void* dy, int nslots, int64_t slot_stride, const void* r, const float* mean,
-                              const float* rstd, const void* gamma, const void* dres, void* dr_out, void* dsub_out,
-                              void* const* out_peers, int npeers, int64_t peer_off, void* dgamma, void* dbeta,
-                              void* dbias, int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed,
-                              int layer, int site, int64_t row_offset, void* workspace, int64_t workspace_bytes,
-                              void* stream) {
+static int ln_bwd_impl(const void* dy, int nslots, int64_t slot_stride, const void* r, const float* mean,
+                       const float* rstd, const void* gamma, const void* dres, void* dr_out, void* dsub_out,
+                       void* const* out_peers, int npeers, int64_t peer_off, void* dgamma, void* dbeta, void* dbias,
+                       int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed, int layer, int site,
+                       int64_t row_offset, int64_t col_offset, float* row_sums_out, const float* ext_sums,
+                       int H_total, void* workspace, int64_t workspace_bytes, void* stream) {
   RowGeom geo;
   SMPK_REQUIRE(M > 0 && row_geom(H, geo) && geom_supported(geo), SMPK_ERR_UNSUPPORTED,
                "smpk_ln_bwd: hidden size %d unsupported", H);
-  SMPK_REQUIRE(dy && nslots >= 1 && (gamma == nullptr || (r && mean && rstd && dr_out)), SMPK_ERR_BAD_ARG,
-               "smpk_ln_bwd: null argument");
-  SMPK_REQUIRE(p_drop == 0.f || dsub_out, SMPK_ERR_BAD_ARG, "smpk_ln_bwd: dropout backward needs dsub_out");
+  SMPK_REQUIRE(dy && nslots >= 1 && (gamma == nullptr || (r && mean && rstd && (dr_out || row_sums_out))),
+               SMPK_ERR_BAD_ARG, "smpk_ln_bwd: null argument");
+  SMPK_REQUIRE(!row_sums_out || (gamma && !ext_sums), SMPK_ERR_BAD_ARG,
+               "smpk_ln_bwd_dist: the sums pass needs gamma and no external sums");
+  SMPK_REQUIRE(!ext_sums || H_total > 0, SMPK_ERR_BAD_ARG, "smpk_ln_bwd_dist: H_total must be positive");
+  SMPK_REQUIRE(p_drop == 0.f || dsub_out || row_sums_out, SMPK_ERR_BAD_ARG,
+               "smpk_ln_bwd: dropout backward needs dsub_out");
   SMPK_REQUIRE(npeers == 0 || out_peers, SMPK_ERR_BAD_ARG, "smpk_ln_bwd: null peer table");
   const int grid = ln_bwd_grid_geo(M, geo.W);
   SMPK_REQUIRE(workspace && workspace_bytes >= (int64_t)grid * 3 * H * 4, SMPK_ERR_BAD_ARG,
@@ -704,17 +791,40 @@ extern "C" int smpk_ln_bwd_ex(const void* dy, int nslots, int64_t slot_stride, c
               reinterpret_cast<const bf16*>(gamma), reinterpret_cast<const bf16*>(dres),
               reinterpret_cast<bf16*>(dr_out), reinterpret_cast<bf16*>(dsub_out),
               reinterpret_cast<float*>(workspace), M, H, p_drop, seed, (uint32_t)layer, (uint32_t)site, row_offset,
-              nslots, slot_stride, reinterpret_cast<bf16* const*>(out_peers), npeers, peer_off};
+              nslots, slot_stride, reinterpret_cast<bf16* const*>(out_peers), npeers, peer_off, col_offset,
+              row_sums_out, ext_sums, H_total};
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int red_bytes = geo.W == 8 ? 0 : geo.W * geo.VPT * 8 * 32 * 4;
   SMPK_DISPATCH_ROW(geo.W, geo.VPT, ln_bwd_kernel, (grid, ROW_THREADS, red_bytes, st), (a));
   int rc = check_launch("smpk_ln_bwd");
   if (rc) return rc;
-  if (!dgamma && !dbeta && !dbias) return SMPK_OK;
+  if (row_sums_out || (!dgamma && !dbeta && !dbias)) return SMPK_OK;
   dim3 rg((H + 31) / 32, 3);
   colsum_reduce_kernel<<<rg, 256, 0, st>>>(reinterpret_cast<float*>(workspace), grid, 3, H, dgamma, dbeta, dbias,
                                            grads_f32, accumulate);
   return check_launch("smpk_ln_bwd(reduce)");
+}
+
+extern "C" int smpk_ln_bwd_ex(const void* dy, int nslots, int64_t slot_stride, const void* r, const float* mean,
+                              const float* rstd, const void* gamma, const void* dres, void* dr_out, void* dsub_out,
+                              void* const* out_peers, int npeers, int64_t peer_off, void* dgamma, void* dbeta,
+                              void* dbias, int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed,
+                              int layer, int site, int64_t row_offset, void* workspace, int64_t workspace_bytes,
+                              void* stream) {
+  return ln_bwd_impl(dy, nslots, slot_stride, r, mean, rstd, gamma, dres, dr_out, dsub_out, out_peers, npeers,
+                     peer_off, dgamma, dbeta, dbias, grads_f32, accumulate, M, H, p_drop, seed, layer, site,
+                     row_offset, 0, nullptr, nullptr, 0, workspace, workspace_bytes, stream);
+}
+
+extern "C" int smpk_ln_bwd_dist(const void* dy, const void* r, const float* mean, const float* rstd,
+                                const void* gamma, const void* dres, void* dr_out, void* dsub_out, void* dgamma,
+                                void* dbeta, void* dbias, int grads_f32, int M, int H, float p_drop, uint64_t seed,
+                                int layer, int site, int64_t row_offset, int64_t col_offset, float* row_sums_out,
+                                const float* ext_sums, int H_total, void* workspace, int64_t workspace_bytes,
+                                void* stream) {
+  return ln_bwd_impl(dy, 1, 0, r, mean, rstd, gamma, dres, dr_out, dsub_out, nullptr, 0, 0, dgamma, dbeta, dbias,
+                     grads_f32, 0, M, H, p_drop, seed, layer, site, row_offset, col_offset, row_sums_out, ext_sums,
+                     H_total, workspace, workspace_bytes, stream);
 }
 
 extern "C" int smpk_ln_bwd(const void* dy, const void* r, const float* mean, const float* rstd, const void* gamma,
@@ -724,6 +834,82 @@ extern "C" int smpk_ln_bwd(const void* dy, const void* r, const float* mean, con
   return smpk_ln_bwd_ex(dy, 1, 0, r, mean, rstd, gamma, dres, dr_out, dsub_out, nullptr, 0, 0, dgamma, dbeta, dbias,
                         grads_f32, accumulate, M, H, p_drop, seed, layer, site, row_offset, workspace,
                         workspace_bytes, stream);
+}
+
+// ===========================================================================
+// bias + activation (channel-sharded MLP of memory mode: the activation follows a
+// reduce-scatter, so it cannot live in the GEMM epilogue)
+// ===========================================================================
+template <int ACT>
+__global__ void __launch_bounds__(256) bias_act_fwd_kernel(const bf16* __restrict__ x, const bf16* __restrict__ bias,
+                                                           int64_t n8, int N, bf16* __restrict__ pre,
+                                                           bf16* __restrict__ y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const int col = (int)((i * 8) % N);
+    float v[8], b[8];
+    load8(x + i * 8, v);
+    load8(bias + col, b);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = round_bf16(v[j] + b[j]);
+    store8(pre + i * 8, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = act_fwd(ACT, v[j]);
+    store8(y + i * 8, v);
+  }
+}
+
+template <int ACT>
+__global__ void __launch_bounds__(256) act_bwd_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ pre,
+                                                      int64_t n8, bf16* __restrict__ dx) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    float g[8], z[8];
+    load8(dy + i * 8, g);
+    load8(pre + i * 8, z);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) g[j] *= act_bwd(ACT, z[j]);
+    store8(dx + i * 8, g);
+  }
+}
+
+static int elementwise_grid(int64_t n8) {
+  const int64_t want = (n8 + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  return (int)(want < cap ? want : cap);
+}
+
+extern "C" int smpk_bias_act_fwd(const void* x, const void* bias, int M, int N, int act, void* pre_out, void* y,
+                                 void* stream) {
+  SMPK_REQUIRE(x && bias && pre_out && y && M > 0 && N > 0 && N % 8 == 0, SMPK_ERR_BAD_ARG,
+               "smpk_bias_act_fwd: bad arguments (N must be a multiple of 8)");
+  const int64_t n8 = (int64_t)M * N / 8;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bf16 *xb = reinterpret_cast<const bf16*>(x), *bb = reinterpret_cast<const bf16*>(bias);
+  bf16 *pb = reinterpret_cast<bf16*>(pre_out), *yb = reinterpret_cast<bf16*>(y);
+  const int grid = elementwise_grid(n8);
+  switch (act) {
+    case SMPK_ACT_GELU_ERF: bias_act_fwd_kernel<SMPK_ACT_GELU_ERF><<<grid, 256, 0, st>>>(xb, bb, n8, N, pb, yb); break;
+    case SMPK_ACT_GELU_TANH: bias_act_fwd_kernel<SMPK_ACT_GELU_TANH><<<grid, 256, 0, st>>>(xb, bb, n8, N, pb, yb); break;
+    case SMPK_ACT_RELU: bias_act_fwd_kernel<SMPK_ACT_RELU><<<grid, 256, 0, st>>>(xb, bb, n8, N, pb, yb); break;
+    default: SMPK_REQUIRE(false, SMPK_ERR_BAD_ARG, "smpk_bias_act_fwd: unknown activation %d", act);
+  }
+  return check_launch("smpk_bias_act_fwd");
+}
+
+extern "C" int smpk_act_bwd(const void* dy, const void* pre, int M, int N, int act, void* dx, void* stream) {
+  SMPK_REQUIRE(dy && pre && dx && M > 0 && N > 0 && N % 8 == 0, SMPK_ERR_BAD_ARG,
+               "smpk_act_bwd: bad arguments (N must be a multiple of 8)");
+  const int64_t n8 = (int64_t)M * N / 8;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bf16 *gb = reinterpret_cast<const bf16*>(dy), *zb = reinterpret_cast<const bf16*>(pre);
+  bf16* db = reinterpret_cast<bf16*>(dx);
+  const int grid = elementwise_grid(n8);
+  switch (act) {
+    case SMPK_ACT_GELU_ERF: act_bwd_kernel<SMPK_ACT_GELU_ERF><<<grid, 256, 0, st>>>(gb, zb, n8, db); break;
+    case SMPK_ACT_GELU_TANH: act_bwd_kernel<SMPK_ACT_GELU_TANH><<<grid, 256, 0, st>>>(gb, zb, n8, db); break;
+    case SMPK_ACT_RELU: act_bwd_kernel<SMPK_ACT_RELU><<<grid, 256, 0, st>>>(gb, zb, n8, db); break;
+    default: SMPK_REQUIRE(false, SMPK_ERR_BAD_ARG, "smpk_act_bwd: unknown activation %d", act);
+  }
+  return check_launch("smpk_act_bwd");
 }
 
 // Vectorised column partials: thread = 8 consecutive columns (one 16-B load per row),

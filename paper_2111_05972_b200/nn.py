@@ -16,6 +16,7 @@ from torch import nn
 
 from . import collectives as C
 from . import layers as L
+from . import memory_mode as MM
 from .errors import NotDivisibleError, ShapeMismatchError
 from .state import STATE, next_layer_id
 
@@ -161,6 +162,11 @@ class _LayerBase(DistributedModule):
         self.post_layernorm = post_layernorm
         self.layer_id = next_layer_id() if layer_id is None else layer_id
 
+    @property
+    def _memory(self) -> bool:
+        """Memory mode: channel-sharded activations, input-split linears."""
+        return STATE.optimize == "memory" and STATE.tp_size > 1
+
     def _meta(self, rc) -> L.LayerMeta:
         """rc = (attention sample offset, own first global token row, row-sharded?)."""
         sample_offset, row_offset, shard = rc
@@ -177,7 +183,7 @@ class _LayerBase(DistributedModule):
                            comm=STATE.config.get("tp_comm", "peer"))
 
     def _ln_params(self, prefix):
-        H = self.hidden_size
+        H = self.hidden_size // STATE.tp_size if self._memory else self.hidden_size  # memory: channel chunk
         for where, flag in (("pre", self.pre_layernorm), ("post", self.post_layernorm)):
             if flag:
                 setattr(self, f"{prefix}{where}_ln_weight", _param((H,), 0, None, one=True))
@@ -202,14 +208,21 @@ class DistributedAttentionLayer(_LayerBase):
         T, H = STATE.tp_size, hidden_size
         g = _gen(self.layer_id, 1)
         std = initializer_range
-        self.qkv_weight = _param((3 * H // T, H), std, g)
+        if self._memory:
+            # input-split QKV (all 3H output rows, rank-major q_j|k_j|v_j, local input channels)
+            self.qkv_weight = _param((3 * H, H // T), std, g)
+            self.dense_bias = _param((H // T,), 0, None, zero=True)
+        else:
+            self.qkv_weight = _param((3 * H // T, H), std, g)
+            self.dense_bias = _param((H,), 0, None, zero=True)
         self.qkv_bias = _param((3 * H // T,), 0, None, zero=True)
         self.dense_weight = _param((H, H // T), std, g)
-        self.dense_bias = _param((H,), 0, None, zero=True)
         self._ln_params("")
 
     def sublayer(self, X, mask, rc):
         m = self._meta(rc)
+        if self._memory:
+            return MM.attention(X, self, mask, m, STATE.tp_rank)
         return L.AttentionFn.apply(X, self.qkv_weight, self.qkv_bias, self.dense_weight, self.dense_bias,
                                    self.pre_ln_weight, self.pre_ln_bias, self.post_ln_weight, self.post_ln_bias,
                                    mask, m)
@@ -225,14 +238,20 @@ class DistributedAttentionLayer(_LayerBase):
         sl = slice(j * hs, (j + 1) * hs)
         wq, wk, wv = p["wqkv"].split(H, 0)
         bq, bk, bv = p["bqkv"].split(H, 0)
-        self.qkv_weight.copy_(torch.cat([wq[sl], wk[sl], wv[sl]], 0))
         self.qkv_bias.copy_(torch.cat([bq[sl], bk[sl], bv[sl]], 0))
         self.dense_weight.copy_(p["wo"][:, sl])
-        self.dense_bias.copy_(p["bo"])
+        if self._memory:  # rows rank-major (q_r | k_r | v_r for r = 0..T-1), local input channels
+            perm = torch.cat([torch.cat([w[r * hs:(r + 1) * hs] for w in (wq, wk, wv)], 0) for r in range(T)], 0)
+            self.qkv_weight.copy_(perm[:, sl])
+            self.dense_bias.copy_(p["bo"][sl])
+        else:
+            self.qkv_weight.copy_(torch.cat([wq[sl], wk[sl], wv[sl]], 0))
+            self.dense_bias.copy_(p["bo"])
+        ln_sl = sl if self._memory else slice(None)
         for where in ("pre", "post"):
             if getattr(self, f"{where}_ln_weight") is not None:
-                getattr(self, f"{where}_ln_weight").copy_(p[f"attn_{where}_ln_w"])
-                getattr(self, f"{where}_ln_bias").copy_(p[f"attn_{where}_ln_b"])
+                getattr(self, f"{where}_ln_weight").copy_(p[f"attn_{where}_ln_w"][ln_sl])
+                getattr(self, f"{where}_ln_bias").copy_(p[f"attn_{where}_ln_b"][ln_sl])
 
 
 class DistributedTransformerOutputLayer(_LayerBase):
@@ -248,14 +267,20 @@ class DistributedTransformerOutputLayer(_LayerBase):
         T, H, I = STATE.tp_size, hidden_size, intermediate_size
         g = _gen(self.layer_id, 2)
         std = initializer_range
-        self.fc1_weight = _param((I // T, H), std, g)
+        if self._memory:  # input-split FC1 (all 4H rows, local input channels)
+            self.fc1_weight = _param((I, H // T), std, g)
+            self.fc2_bias = _param((H // T,), 0, None, zero=True)
+        else:
+            self.fc1_weight = _param((I // T, H), std, g)
+            self.fc2_bias = _param((H,), 0, None, zero=True)
         self.fc1_bias = _param((I // T,), 0, None, zero=True)
         self.fc2_weight = _param((H, I // T), std, g)
-        self.fc2_bias = _param((H,), 0, None, zero=True)
         self._ln_params("")
 
     def sublayer(self, X, mask, rc):
         m = self._meta(rc)
+        if self._memory:
+            return MM.mlp(X, self, m, STATE.tp_rank)
         return L.MlpFn.apply(X, self.fc1_weight, self.fc1_bias, self.fc2_weight, self.fc2_bias, self.pre_ln_weight,
                              self.pre_ln_bias, self.post_ln_weight, self.post_ln_bias, m)
 
@@ -267,14 +292,25 @@ class DistributedTransformerOutputLayer(_LayerBase):
         T, j, I = STATE.tp_size, STATE.tp_rank, self.intermediate_size
         ins = I // T
         sl = slice(j * ins, (j + 1) * ins)
-        self.fc1_weight.copy_(p["w1"][sl])
+        hs = self.hidden_size // T
+        hsl = slice(j * hs, (j + 1) * hs)
         self.fc1_bias.copy_(p["b1"][sl])
         self.fc2_weight.copy_(p["w2"][:, sl])
-        self.fc2_bias.copy_(p["b2"])
+        if self._memory:
+            self.fc1_weight.copy_(p["w1"][:, hsl])
+            self.fc2_bias.copy_(p["b2"][hsl])
+        else:
+            self.fc1_weight.copy_(p["w1"][sl])
+            self.fc2_bias.copy_(p["b2"])
+        ln_sl = hsl if self._memory else slice(None)
         for where in ("pre", "post"):
             if getattr(self, f"{where}_ln_weight") is not None:
-                getattr(self, f"{where}_ln_weight").copy_(p[f"mlp_{where}_ln_w"])
-                getattr(self, f"{where}_ln_bias").copy_(p[f"mlp_{where}_ln_b"])
+                getattr(self, f"{where}_ln_weight").copy_(p[f"mlp_{where}_ln_w"][ln_sl])
+                getattr(self, f"{where}_ln_bias").copy_(p[f"mlp_{where}_ln_b"][ln_sl])
+
+
+def _memory_mode() -> bool:
+    return STATE.optimize == "memory" and STATE.tp_size > 1
 
 
 def _row_ctx(B: int, s: int):
@@ -285,6 +321,9 @@ def _row_ctx(B: int, s: int):
     rdp_rank*T*B.  Prescaled batch / T == 1: activations replicated, samples rdp_rank*B (dp_rank*B)."""
     if STATE.tp_size == 1:
         off = STATE.dp_rank * B
+        return (off, off * s, False)
+    if _memory_mode():  # channel-sharded activations hold every sample of the group (prescaled: own)
+        off = STATE.rdp_rank * B * (1 if STATE.prescaled else STATE.tp_size)
         return (off, off * s, False)
     if STATE.prescaled:
         off = STATE.rdp_rank * B
@@ -297,6 +336,10 @@ def _entry(x, attention_mask):
     B, s = x.shape[0], x.shape[1]
     mask = _mask_2d(attention_mask, B, s)
     rc = _row_ctx(B, s)
+    if _memory_mode():  # scatter_and_merge(split channel, merge batch) -> [T*b, s, H/T]
+        if not STATE.prescaled and mask is not None:
+            mask = C.all_gather(mask, 0)
+        return MM.entry(x, STATE.tp_size, STATE.tp_rank, STATE.prescaled), mask, rc
     if rc[2] and mask is not None:
         mask = C.all_gather(mask, 0)
     return x, mask, rc
@@ -312,7 +355,8 @@ def _exit(Y):
 def _run_standalone(mod, hidden_states, attention_mask):
     x = hidden_states.to(DTYPE).contiguous()
     X, mask, rc = _entry(x, attention_mask)
-    return mod.sublayer(X, mask, rc)
+    Y = mod.sublayer(X, mask, rc)
+    return MM.exit(Y, STATE.prescaled) if _memory_mode() else Y
 
 
 class DistributedTransformerLayer(DistributedModule):
@@ -324,9 +368,6 @@ class DistributedTransformerLayer(DistributedModule):
                  initializer_range=0.02, use_normal_initialization=False, causal_mask_size=None,
                  add_cross_attention=False, pre_layernorm=False, post_layernorm=True, layer_id=None):
         super().__init__()
-        if STATE.optimize == "memory" and STATE.tp_size > 1:
-            raise NotImplementedError("optimize='memory' runs in the CPU oracle only in this build; "
-                                      "use optimize='speed' on the GPU path")
         lid = next_layer_id() if layer_id is None else layer_id
         self.layer_id = lid
         self.attention = DistributedAttentionLayer(
@@ -446,7 +487,11 @@ class DistributedTransformerLMHead(DistributedModule):
             h = C.reduce_scatter_for_tp(h, 0)  # partial lookups -> this rank's own rows
         elif T > 1:
             h = C.fwd_allreduce_for_tp(h)
-        h = self.transformer.sublayer(h, mask, rc)
+        if _memory_mode():  # channel-sharded stack between the embedding and the LM head
+            h = MM.exit(self.transformer.sublayer(MM.entry(h, T, STATE.tp_rank, STATE.prescaled), mask, rc),
+                        STATE.prescaled)
+        else:
+            h = self.transformer.sublayer(h, mask, rc)
         if self.final_ln is not None:
             h = self.final_ln(h)
         if not self.add_lm_head:

@@ -73,7 +73,8 @@ def ln_bwd(dy, r, mean, rstd, gamma, *, dres=None, p=0.0, seed=0, layer=0, site=
     _lib.call("smpk_ln_bwd_ex", _ptr(dy), int(nslots), int(slot_stride), _ptr(r), _ptr(mean), _ptr(rstd),
               _ptr(gamma), _ptr(dres), _ptr(dr), _ptr(dsub), _ptr(out_peers), npeers, int(peer_off), _ptr(dgamma),
               _ptr(dbeta), _ptr(dbias), int(grads_f32), 0, M, H, float(p), int(seed) & (2 ** 64 - 1), int(layer),
-              int(site), int(row_offset), _ptr(ws), int(ws_bytes), _stream())
+              int(site), int(row_offset), _ptr(ws), int(ws_bytes), _stream(),
+              launches=2 if (dgamma is not None or dbeta is not None or dbias is not None) else 1)
     if dsub is None:
         dsub = dr if dr is not None else (dy if nslots == 1 else None)
     return dr, dsub, dgamma, dbeta, dbias
@@ -166,3 +167,76 @@ def flash_attn_fwd(qkv: torch.Tensor, B: int, s: int, nh: int, dh: int, *, mask_
               _ptr(mask_add), float(1.0 / dh ** 0.5), int(bool(causal)), float(p),
               _ptr(keep_bits if p > 0 else None), _stream())
     return ctx, lse
+
+
+# ---------------------------------------------------------------------------
+# channel-sharded (memory-mode) LayerNorm and the standalone bias + activation
+# ---------------------------------------------------------------------------
+
+def bdr_ln_dist(x: torch.Tensor, *, bias=None, residual=None, gamma=None, beta=None, eps=1e-5, p=0.0, seed=0, layer=0,
+                site=SITE_ATTN_OUT, row_offset=0, col_offset=0, want_r=True, row_sums=False, ext_sums=None,
+                h_total=0):
+    """smpk_bdr_ln_fwd_dist on the local H/T columns.  row_sums=True also returns the partial
+    [M, 2] (sum r, sum r^2); ext_sums (the group's [M, 2] sums) normalises with the full-row
+    statistics.  Returns (r, y, mean, rstd, sums)."""
+    _check_cuda(x, bias, residual, gamma, beta, ext_sums)
+    M, H = x.shape
+    dev = x.device
+    r = torch.empty(M, H, dtype=torch.bfloat16, device=dev) if want_r else None
+    y = mean = rstd = None
+    if gamma is not None:
+        y = torch.empty(M, H, dtype=torch.bfloat16, device=dev)
+        mean = torch.empty(M, dtype=torch.float32, device=dev)
+        rstd = torch.empty(M, dtype=torch.float32, device=dev)
+    sums = torch.empty(M, 2, dtype=torch.float32, device=dev) if row_sums else None
+    _lib.call("smpk_bdr_ln_fwd_dist", _ptr(x), _ptr(bias), _ptr(residual), _ptr(r), _ptr(gamma), _ptr(beta), _ptr(y),
+              _ptr(mean), _ptr(rstd), M, H, float(eps), float(p), int(seed) & (2 ** 64 - 1), int(layer), int(site),
+              int(row_offset), int(col_offset), _ptr(sums), _ptr(ext_sums), int(h_total), _stream())
+    return r, y, mean, rstd, sums
+
+
+def ln_bwd_dist(dy, r, mean, rstd, gamma, *, dres=None, p=0.0, seed=0, layer=0, site=SITE_ATTN_OUT, row_offset=0,
+                col_offset=0, sums_only=False, ext_sums=None, h_total=0, want_dbias=False):
+    """smpk_ln_bwd_dist.  sums_only=True returns the partial [M, 2] (sum g, sum g*xhat); otherwise
+    (dr, dsub, dgamma, dbeta, dbias) with the row means taken from ext_sums (gamma None: no LN)."""
+    _check_cuda(dy, r, gamma, dres, ext_sums)
+    M, H = dy.shape
+    dev = dy.device
+    ws_bytes = _lib.size("smpk_ln_bwd_workspace", M, H)
+    ws = torch.empty(max(ws_bytes, 4) // 4, dtype=torch.float32, device=dev)
+    if sums_only:
+        sums = torch.empty(M, 2, dtype=torch.float32, device=dev)
+        _lib.call("smpk_ln_bwd_dist", _ptr(dy), _ptr(r), _ptr(mean), _ptr(rstd), _ptr(gamma), None, None, None, None,
+                  None, None, 0, M, H, float(p), int(seed) & (2 ** 64 - 1), int(layer), int(site), int(row_offset),
+                  int(col_offset), _ptr(sums), None, 0, _ptr(ws), int(ws_bytes), _stream(), launches=1)
+        return sums
+    dr = torch.empty(M, H, dtype=torch.bfloat16, device=dev)
+    dsub = torch.empty(M, H, dtype=torch.bfloat16, device=dev) if p > 0 else None
+    dgamma = torch.empty(H, dtype=torch.bfloat16, device=dev) if gamma is not None else None
+    dbeta = torch.empty(H, dtype=torch.bfloat16, device=dev) if gamma is not None else None
+    dbias = torch.empty(H, dtype=torch.bfloat16, device=dev) if want_dbias else None
+    _lib.call("smpk_ln_bwd_dist", _ptr(dy), _ptr(r), _ptr(mean), _ptr(rstd), _ptr(gamma), _ptr(dres), _ptr(dr),
+              _ptr(dsub), _ptr(dgamma), _ptr(dbeta), _ptr(dbias), 0, M, H, float(p), int(seed) & (2 ** 64 - 1),
+              int(layer), int(site), int(row_offset), int(col_offset), None, _ptr(ext_sums), int(h_total), _ptr(ws),
+              int(ws_bytes), _stream(), launches=2 if (dgamma is not None or dbias is not None) else 1)
+    return dr, (dsub if dsub is not None else dr), dgamma, dbeta, dbias
+
+
+def bias_act(x: torch.Tensor, bias: torch.Tensor, act: str):
+    """(y, pre): pre = bf16(x + bias), y = act(pre)."""
+    from .kernels import ACT
+    _check_cuda(x, bias)
+    M, N = x.shape
+    pre = torch.empty_like(x)
+    y = torch.empty_like(x)
+    _lib.call("smpk_bias_act_fwd", _ptr(x), _ptr(bias), M, N, ACT[act], _ptr(pre), _ptr(y), _stream())
+    return y, pre
+
+
+def act_bwd(dy: torch.Tensor, pre: torch.Tensor, act: str) -> torch.Tensor:
+    from .kernels import ACT
+    _check_cuda(dy, pre)
+    M, N = dy.shape
+    dx = torch.empty_like(dy)
+    _lib.call("smpk_act_bwd", _ptr(dy.contiguous()), _ptr(pre), M, N, ACT[act], _ptr(dx), _stream())
+    return dx

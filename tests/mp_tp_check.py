@@ -33,9 +33,9 @@ def gather_cpu(t):
     return [o.cpu() for o in out]
 
 
-def run_case(smp, name, *, prescaled, causal, pre, post, p, layers=1, act="gelu", comm="peer"):
+def run_case(smp, name, *, prescaled, causal, pre, post, p, layers=1, act="gelu", comm="peer", optimize="speed"):
     T, rank = dist.get_world_size(), dist.get_rank()
-    smp.init({"tensor_parallel_degree": T, "optimize": "speed", "_prescaled_batch": prescaled, "seed": 11,
+    smp.init({"tensor_parallel_degree": T, "optimize": optimize, "_prescaled_batch": prescaled, "seed": 11,
               "tp_comm": comm, "symm_pool_bytes": 256 << 20})
     nh, dh, I, s, B = 2 * T, 64, 512 * T, 128, 2
     H = nh * dh
@@ -101,22 +101,27 @@ def run_case(smp, name, *, prescaled, causal, pre, post, p, layers=1, act="gelu"
             wq, wk, wv = gr["wqkv"].grad.split(H, 0)
             bq, bk, bv = gr["bqkv"].grad.split(H, 0)
             sg = shard_grads[l]
+            mem = optimize == "memory"
+            perm = torch.cat([torch.cat([w[r * hs:(r + 1) * hs] for w in (wq, wk, wv)], 0) for r in range(T)], 0)
             for j in range(T):
                 sl = slice(j * hs, (j + 1) * hs)
                 isl = slice(j * ins, (j + 1) * ins)
-                e = {
-                    "qkv_w": rel(sg["qkv_w"][j], torch.cat([wq[sl], wk[sl], wv[sl]], 0)),
+                e = {  # shard layouts: speed = output-split QKV / FC1; memory = input-split (nn.py)
+                    "qkv_w": rel(sg["qkv_w"][j], perm[:, sl] if mem else torch.cat([wq[sl], wk[sl], wv[sl]], 0)),
                     "qkv_b": rel(sg["qkv_b"][j], torch.cat([bq[sl], bk[sl], bv[sl]], 0)),
                     "wo": rel(sg["wo"][j], gr["wo"].grad[:, sl]),
-                    "bo": rel(sg["bo"][j], gr["bo"].grad),
-                    "w1": rel(sg["w1"][j], gr["w1"].grad[isl]),
+                    "bo": rel(sg["bo"][j], gr["bo"].grad[sl] if mem else gr["bo"].grad),
+                    "w1": rel(sg["w1"][j], gr["w1"].grad[:, sl] if mem else gr["w1"].grad[isl]),
                     "b1": rel(sg["b1"][j], gr["b1"].grad[isl]),
                     "w2": rel(sg["w2"][j], gr["w2"].grad[:, isl]),
-                    "b2": rel(sg["b2"][j], gr["b2"].grad),
+                    "b2": rel(sg["b2"][j], gr["b2"].grad[sl] if mem else gr["b2"].grad),
                 }
                 for k, v in e.items():
                     errs[f"L{l}.r{j}.{k}"] = v
-        bad = {k: v for k, v in errs.items() if not v < TOL}
+        # ReLU-gated gradients (FC1): relu' flips where the bf16-rounded pre-activation crosses 0,
+        # the documented relaxed bound of tests/test_layer_gpu.py
+        relu_tol = lambda k: 6e-2 if act == "relu" and k.endswith((".w1", ".b1")) else TOL  # noqa: E731
+        bad = {k: v for k, v in errs.items() if not v < relu_tol(k)}
         ok = not bad
         print(f"[{name}] T={T} {'OK' if ok else 'FAIL'} max_err={max(errs.values()):.3e} "
               f"y={errs['y']:.2e} dx={errs['dx']:.2e} {bad if bad else ''}", flush=True)
@@ -240,6 +245,14 @@ def main():
         run_case(smp, "stack2_nccl_comm", prescaled=False, causal=True, pre=True, post=False, p=0.1, layers=2,
                  comm="nccl"),
         run_case(smp, "stack3_peer_post_ln", prescaled=False, causal=False, pre=False, post=True, p=0.1, layers=3),
+        run_case(smp, "memory_post_ln", prescaled=False, causal=False, pre=False, post=True, p=0.0,
+                 optimize="memory"),
+        run_case(smp, "memory_pre_ln_causal_dropout", prescaled=False, causal=True, pre=True, post=False, p=0.1,
+                 optimize="memory"),
+        run_case(smp, "memory_prescaled_stack2", prescaled=True, causal=False, pre=True, post=True, p=0.1,
+                 layers=2, optimize="memory"),
+        run_case(smp, "memory_relu", prescaled=False, causal=False, pre=False, post=True, p=0.0,
+                 optimize="memory", act="relu"),
     ]
     dist.barrier()
     dist.destroy_process_group()

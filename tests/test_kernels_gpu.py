@@ -31,7 +31,7 @@ def ops():
     return ops
 
 
-@pytest.mark.parametrize("H", [256, 1024, 2048, 5120])
+@pytest.mark.parametrize("H", [128, 256, 384, 1024, 2048, 5120])
 @pytest.mark.parametrize("p", [0.0, 0.1])
 def test_bdr_ln_fwd(ops, H, p):
     g = torch.Generator().manual_seed(H)
@@ -55,7 +55,7 @@ def test_bdr_ln_fwd(ops, H, p):
         assert torch.equal(r.cpu()[dropped], bf(res.double())[dropped])
 
 
-@pytest.mark.parametrize("H", [256, 1024, 2048])
+@pytest.mark.parametrize("H", [128, 256, 384, 1024, 2048])
 @pytest.mark.parametrize("p", [0.0, 0.2])
 @pytest.mark.parametrize("with_ln", [True, False])
 def test_ln_bwd(ops, H, p, with_ln):
