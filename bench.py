@@ -48,6 +48,15 @@ def flops_per_token_layer(H=1024, s=SEQ, causal=False):
     return 72 * H * H + (6 if causal else 12) * s * H
 
 
+def gemm_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per GEMM launch from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
+            return json.load(f)["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -185,6 +194,21 @@ def max_over_ranks(v: float) -> float:
     return float(t.item())
 
 
+def kernel_ms_per_step(run, name_part: str, steps: int = 3) -> float:
+    """Device time (CUPTI kernel records) per step of the kernels whose name contains name_part."""
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(steps):
+            run()
+        torch.cuda.synchronize()
+    us = 0.0
+    for ev in prof.events():
+        if ev.device_type == torch.autograd.DeviceType.CUDA and name_part in ev.name:
+            us += ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total
+    return us / steps / 1e3
+
+
 def trace_kernels(run, path_prefix: str, rank: int, steps: int = 2) -> None:
     """Diagnostics only (never the bench value): CUPTI kernel trace of `steps` steps,
     aggregated per kernel name, written to <prefix>_rank<r>.txt."""
@@ -240,8 +264,10 @@ def run_gpu(args, rank, world, local):
         torch.cuda.current_stream().wait_stream(side)
         graph = torch.cuda.CUDAGraph()
         launches_g0 = _lib.launch_count
+        kernels.PROFILER = graph_prof = kernels.GemmProfiler(count_only=True)  # GEMM FLOPs of one step
         with torch.cuda.graph(graph):
             static_y = step(x, dy)
+        kernels.PROFILER = None
         graph_launches = _lib.launch_count - launches_g0
         run = graph.replay
     for _ in range(args.warmup):
@@ -268,14 +294,14 @@ def run_gpu(args, rank, world, local):
     prof, kernels.PROFILER = kernels.PROFILER, None
     gemm_flops, gemm_ms, gemm_launches = prof.flops_and_ms() if prof else (0.0, 0.0, 0)
     if args.graph:
+        # Event brackets cannot sit inside the replayed graph without adding event-record nodes
+        # (measured: +~10 us per GEMM), so the GEMM durations come from the device-side kernel
+        # records (CUPTI) of replays of the same graph right after the timed region.
         launches = graph_launches
-        # events cannot bracket launches inside a replayed graph: time the GEMMs on one
-        # eager step right after the timed region instead
-        kernels.PROFILER = kernels.GemmProfiler()
-        step(x, dy)
-        prof, kernels.PROFILER = kernels.PROFILER, None
-        gemm_flops, gemm_ms, gemm_launches = prof.flops_and_ms()
-        gemm_flops, gemm_ms, gemm_launches = gemm_flops * args.steps, gemm_ms * args.steps, gemm_launches * args.steps
+        gemm_ms = kernel_ms_per_step(run, "gemm_bf16_tcgen05", steps=3)
+        gemm_launches = len(graph_prof.records)
+        gemm_flops, gemm_ms, gemm_launches = (graph_prof.flops() * args.steps, gemm_ms * args.steps,
+                                              gemm_launches * args.steps)
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     tokens_step = B * s * world
     if args.trace:
@@ -342,10 +368,13 @@ def run_gpu(args, rank, world, local):
                 "frac_of_sustained": model_tflops / peak_sus, "frac_of_burst": model_tflops / peaks["bf16_tflops"],
                 "peak_kind": peak_kind},
         "roofline": {"bound": "tensor", "kernel": "smpk gemm_bf16_tcgen05 (all GEMM launches of the step)",
+                     "timing": ("CUPTI kernel records of replays of the step graph" if args.graph
+                                else "CUDA events around each GEMM launch (eager)"),
                      "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s", "frac": achieved / peak_sus,
                      "peak_kind": f"{peak_kind} bf16_tflops_sustained (kernel timed inside a long step)",
                      "launches_per_step": gemm_launches // args.steps,
-                     "gemm_ms_per_step": gemm_ms / args.steps, "traffic": None},
+                     "gemm_ms_per_step": gemm_ms / args.steps, "traffic": gemm_traffic(),
+                     "traffic_unit": "DRAM bytes per GEMM launch (ncu, profiles/gemm_traffic.json)"},
         "cpu_baseline": cpu,
         "e2e": {"value": tokens_step / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": 2 * xh.numel() * xh.element_size(), "d2h_bytes_per_step": 4},

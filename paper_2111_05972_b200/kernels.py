@@ -30,10 +30,20 @@ def _check_cuda(*ts: torch.Tensor | None) -> None:
 
 
 class GemmProfiler:
-    """Brackets every smpk_gemm launch with CUDA events on its stream (bench.py roofline)."""
+    """Brackets every smpk_gemm launch with CUDA events on its stream (bench.py roofline).
 
-    def __init__(self):
+    count_only=True records only the algorithmic FLOPs of each launch (used while a CUDA graph
+    is captured; the durations then come from the device-side kernel records of the replay)."""
+
+    def __init__(self, count_only: bool = False):
         self.records = []  # (start_event, end_event, flops)
+        self.count_only = count_only
+
+    def event(self):
+        return None if self.count_only else torch.cuda.Event(enable_timing=True)
+
+    def flops(self) -> float:
+        return sum(r[2] for r in self.records)
 
     def flops_and_ms(self):
         torch.cuda.synchronize()
@@ -51,8 +61,9 @@ def gemm_raw(a, a_mn, lda, a_bs, b, b_mn, ldb, b_bs, c, ldc, c_bs, M, N, K, nb=(
     _check_cuda(a, b, c, bias, aux)
     prof = PROFILER
     if prof is not None:
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
+        e0, e1 = prof.event(), prof.event()
+        if e0 is not None:
+            e0.record()
     # split-K workspace (weight-gradient shapes with few output tiles); 0 bytes = unsplit
     ws_bytes = _lib.size("smpk_gemm_workspace", int(M), int(N), int(K), int(nb[0]), int(nb[1]))
     ws = torch.empty(ws_bytes // 4, dtype=torch.float32, device=c.device) if ws_bytes else None
@@ -64,7 +75,8 @@ def gemm_raw(a, a_mn, lda, a_bs, b, b_mn, ldb, b_bs, c, ldc, c_bs, M, N, K, nb=(
               float(alpha), float(beta), int(epi), int(act),
               _ptr(bias), _ptr(aux), int(ldaux), _ptr(ws), int(ws_bytes), _stream())
     if prof is not None:
-        e1.record()
+        if e1 is not None:
+            e1.record()
         prof.records.append((e0, e1, 2.0 * M * N * K * nb[0] * nb[1]))
 
 
@@ -77,12 +89,14 @@ def gemm_rs(a: torch.Tensor, b: torch.Tensor, b_mn: bool, peers, *, ldc: int, ro
     N = b.shape[1] if b_mn else b.shape[0]
     prof = PROFILER
     if prof is not None:
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
+        e0, e1 = prof.event(), prof.event()
+        if e0 is not None:
+            e0.record()
     _lib.call("smpk_gemm_rs", a.data_ptr(), 0, _rowmajor(a, "a"), b.data_ptr(), int(bool(b_mn)), _rowmajor(b, "b"),
               peers, len(peers), int(ldc), int(rows_per_owner), int(slot_off), M, N, Kd, _stream())
     if prof is not None:
-        e1.record()
+        if e1 is not None:
+            e1.record()
         prof.records.append((e0, e1, 2.0 * M * N * Kd))
 
 
