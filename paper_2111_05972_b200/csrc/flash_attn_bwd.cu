@@ -55,7 +55,8 @@ struct FaBwdCfg {
   static constexpr int OFF_LSE = OFF_PS + 32768;
   static constexpr int OFF_DELTA = OFF_LSE + 512;
   static constexpr int OFF_BITS = OFF_DELTA + 512;  // [128 queries][4 words]
-  static constexpr int OFF_BAR = OFF_BITS + 2048;
+  static constexpr int OFF_KBT = OFF_BITS + 2048;   // the same bits transposed [4 words][128 queries]
+  static constexpr int OFF_BAR = OFF_KBT + 2048;
   static constexpr int SMEM = 1024 + OFF_BAR + 256;
   // TMEM: A [0,128) (S^T -> dP^T -> dQ), dV [128, 128+DH), dK [128+DH, 128+2DH)
   static constexpr uint32_t TMEM_COLS = DH == 64 ? 256 : 512;
@@ -203,14 +204,31 @@ __global__ void __launch_bounds__(FB_THREADS, (DH == 64 ? 2 : 1))
     const uint32_t t_lane = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const float mk = a.mask ? a.mask[(int64_t)b * a.s + key] * 1.4426950408889634f : 0.f;
     uint8_t* ps_s = smem + Cfg::OFF_PS;
-    const float* lse_s = reinterpret_cast<const float*>(smem + Cfg::OFF_LSE);
+    float* nl_s = reinterpret_cast<float*>(smem + Cfg::OFF_LSE);   // -lse2 per query (in place)
     const float* del_s = reinterpret_cast<const float*>(smem + Cfg::OFF_DELTA);
-    const uint32_t* bits_s = reinterpret_cast<const uint32_t*>(smem + Cfg::OFF_BITS) + (r >> 5);
+    uint32_t* bits_s = reinterpret_cast<uint32_t*>(smem + Cfg::OFF_BITS);  // [q][4 words] as loaded
+    uint32_t* kbt_s = reinterpret_cast<uint32_t*>(smem + Cfg::OFF_KBT);    // [4 words][q] transposed
+    const uint32_t* kb_row = kbt_s + (r >> 5) * 128;  // this thread's key word, all 128 queries
     const int bit = r & 31;
+    const float scale_log2 = a.scale_log2, inv_keep = a.inv_keep;
     for (int t = 0; t < nt; ++t) {
       const int i = i0 + t;
       const bool diag = a.causal && (i == j);
       mbar_wait(qdo_full, t & 1);  // lse / delta / bits of this query tile in smem
+      {
+        // per-tile preamble (thread r = query r): -lse (fully masked rows -> -inf so P = 0) and the
+        // keep-bit words transposed so a thread reads 4 queries of its key word per 16-B load
+        const float l2 = nl_s[r];
+        nl_s[r] = (l2 == -INFINITY) ? -INFINITY : -l2;
+        if (a.dropout) {
+          const uint4 w = *reinterpret_cast<const uint4*>(bits_s + r * 4);
+          kbt_s[r] = w.x;
+          kbt_s[128 + r] = w.y;
+          kbt_s[256 + r] = w.z;
+          kbt_s[384 + r] = w.w;
+        }
+        named_barrier_sync(1, 128);
+      }
       mbar_wait(s_full, t & 1);
       tc_fence_after();
       // P (bf16, kept for dS) and Pd^T = keep ? P : 0 -> smem, 32 queries per TMEM load
@@ -223,23 +241,34 @@ __global__ void __launch_bounds__(FB_THREADS, (DH == 64 ? 2 : 1))
 #pragma unroll
         for (int c4 = 0; c4 < 4; ++c4) {  // 8 queries per 16-B granule
           const int c = cc * 4 + c4;
+          const float4 n0 = *reinterpret_cast<const float4*>(nl_s + c * 8);
+          const float4 n1 = *reinterpret_cast<const float4*>(nl_s + c * 8 + 4);
+          const float nl[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
+          uint32_t kw[8];
+          if (a.dropout) {
+            const uint4 k0 = *reinterpret_cast<const uint4*>(kb_row + c * 8);
+            const uint4 k1 = *reinterpret_cast<const uint4*>(kb_row + c * 8 + 4);
+            kw[0] = k0.x; kw[1] = k0.y; kw[2] = k0.z; kw[3] = k0.w;
+            kw[4] = k1.x; kw[5] = k1.y; kw[6] = k1.z; kw[7] = k1.w;
+          }
+          float pr[8], pk[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int qq = c * 8 + e;
+            pr[e] = ex2_approx(fmaf(__uint_as_float(sv[qq & 31]), scale_log2, mk + nl[e]));
+          }
+          if (diag) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (r > c * 8 + e) pr[e] = 0.f;
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) pk[e] = (!a.dropout || ((kw[e] >> bit) & 1u)) ? pr[e] : 0.f;
           uint32_t pd[4];
 #pragma unroll
           for (int e = 0; e < 8; e += 2) {
-            float pr[2], pk[2];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const int qq = c * 8 + e + u;
-              const float l2 = lse_s[qq];
-              const float x = fmaf(__uint_as_float(sv[qq & 31]), a.scale_log2, mk - l2);
-              float p = ex2_approx(x);
-              if (l2 == -INFINITY || (diag && r > qq)) p = 0.f;
-              pr[u] = p;
-              const bool kp = !a.dropout || ((bits_s[qq * 4] >> bit) & 1u);
-              pk[u] = kp ? p : 0.f;
-            }
-            pp[(c * 8 + e) >> 1] = pack_bf16x2(pr[0], pr[1]);
-            pd[e >> 1] = pack_bf16x2(pk[0], pk[1]);
+            pp[(c * 8 + e) >> 1] = pack_bf16x2(pr[e], pr[e + 1]);
+            pd[e >> 1] = pack_bf16x2(pk[e], pk[e + 1]);
           }
           *reinterpret_cast<uint4*>(ps_s + (c >> 3) * 16384 + sw128_offset(r, c & 7)) =
               make_uint4(pd[0], pd[1], pd[2], pd[3]);
@@ -260,6 +289,16 @@ __global__ void __launch_bounds__(FB_THREADS, (DH == 64 ? 2 : 1))
 #pragma unroll
         for (int c4 = 0; c4 < 4; ++c4) {
           const int c = cc * 4 + c4;
+          const float4 d0 = *reinterpret_cast<const float4*>(del_s + c * 8);
+          const float4 d1 = *reinterpret_cast<const float4*>(del_s + c * 8 + 4);
+          const float dl[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+          uint32_t kw[8];
+          if (a.dropout) {
+            const uint4 k0 = *reinterpret_cast<const uint4*>(kb_row + c * 8);
+            const uint4 k1 = *reinterpret_cast<const uint4*>(kb_row + c * 8 + 4);
+            kw[0] = k0.x; kw[1] = k0.y; kw[2] = k0.z; kw[3] = k0.w;
+            kw[4] = k1.x; kw[5] = k1.y; kw[6] = k1.z; kw[7] = k1.w;
+          }
           uint32_t dsw[4];
 #pragma unroll
           for (int e = 0; e < 8; e += 2) {
@@ -268,9 +307,9 @@ __global__ void __launch_bounds__(FB_THREADS, (DH == 64 ? 2 : 1))
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
               const int qq = c * 8 + e + u;
-              const bool kp = !a.dropout || ((bits_s[qq * 4] >> bit) & 1u);
-              const float dp = kp ? __uint_as_float(sv[qq & 31]) * a.inv_keep : 0.f;
-              ds[u] = (u ? pf.y : pf.x) * (dp - del_s[qq]);
+              const bool kp = !a.dropout || ((kw[e + u] >> bit) & 1u);
+              const float dp = kp ? __uint_as_float(sv[qq & 31]) * inv_keep : 0.f;
+              ds[u] = (u ? pf.y : pf.x) * (dp - dl[e + u]);
             }
             dsw[e >> 1] = pack_bf16x2(ds[0], ds[1]);
           }
