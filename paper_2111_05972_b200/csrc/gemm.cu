@@ -25,8 +25,12 @@ namespace smpk {
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B row
 
-constexpr int NUM_EPI_WARPS = 16;                          // warps 4..19
-constexpr int GEMM_THREADS = 128 + 32 * NUM_EPI_WARPS;      // warps 0-3: TMA, MMA, TMEM alloc, spare
+// Epilogue warps (warps 4..): 16 for the activation epilogues (issue-heavy: GeLU / dGeLU per
+// element), 8 otherwise — fewer staging boxes leave room for a deeper operand ring.
+__host__ __device__ constexpr int epi_warps(int epi) {
+  return (epi == SMPK_EPI_BIAS_ACT || epi == SMPK_EPI_DACT) ? 16 : 8;
+}
+__host__ __device__ constexpr int gemm_threads(int epi) { return 128 + 32 * epi_warps(epi); }
 constexpr int STG_BYTES = 4096;                             // TMA-store staging per epilogue warp
 constexpr int MAX_PEERS = 8;
 
@@ -67,14 +71,14 @@ struct EpiMaps {
   CUtensorMap peer[MAX_PEERS];
 };
 
-template <int BN, int STAGES, bool PAIR = false>
+template <int BN, int STAGES, bool PAIR = false, int EPW = 8>
 struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int SMEM_BYTES =
-      1024 /*align slack*/ + STAGES * STAGE_BYTES + NUM_EPI_WARPS * STG_BYTES + 256 /*barriers*/;
+      1024 /*align slack*/ + STAGES * STAGE_BYTES + EPW * STG_BYTES + 256 /*barriers*/;
 };
 
 __device__ __forceinline__ void decode_unit(const GemmArgs& g, int u, int& tile, int& kb0, int& kb1) {
@@ -267,7 +271,8 @@ __device__ __forceinline__ void stage_f32_row(uint8_t* box, int r, const float (
 template <int BN, int STAGES, int EPI, int ACT, bool F32OUT, bool BETA, bool PAIR>
 __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensorMap* tmB, const EpiMaps* maps,
                                           const GemmArgs& g) {
-  using Cfg = GemmCfg<BN, STAGES, PAIR>;
+  constexpr int NUM_EPI_WARPS = epi_warps(EPI);
+  using Cfg = GemmCfg<BN, STAGES, PAIR, NUM_EPI_WARPS>;
   constexpr int BMT = PAIR ? 2 * BM : BM;  // tile rows
   constexpr int BNL = PAIR ? BN / 2 : BN;  // B rows staged by this CTA
   extern __shared__ uint8_t smem_raw[];
@@ -425,9 +430,10 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensor
     // (warp - 4) / 4 the column group; a warp owns the 32-column chunks cg, cg+4, ...
     const int quarter = warp & 3;
     const int cgroup = (warp - 4) >> 2;
+    constexpr int NGR = NUM_EPI_WARPS / 4;                 // column groups
     constexpr int NCH = BN / 32;                           // 32-column chunks per tile
-    constexpr int CPW = NCH >= 4 ? NCH / 4 : 1;            // chunks per warp
-    const bool active = cgroup < NCH;                      // BN == 64: column groups 2, 3 idle
+    constexpr int CPW = NCH >= NGR ? NCH / NGR : 1;        // chunks per warp
+    const bool active = cgroup < NCH;                      // small BN: surplus column groups idle
     uint8_t* stg = sStg + (warp - 4) * STG_BYTES;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -446,7 +452,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensor
       if (g.splits == 1) {
 #pragma unroll 1
         for (int i = 0; i < CPW; ++i) {
-          const int ch = cgroup + 4 * i;
+          const int ch = cgroup + NGR * i;
           uint32_t r[32];
           if (active) {
             tmem_ld_32x32b_x32(t_row + ch * 32, r);
@@ -506,7 +512,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensor
         float* part = g.ws + ((int64_t)split * g.num_tiles * HALVES + sidx) * blk + rl;
 #pragma unroll 1
         for (int i = 0; i < CPW; ++i) {
-          const int ch = cgroup + 4 * i;
+          const int ch = cgroup + NGR * i;
           uint32_t r[32];
           if (active) {
             tmem_ld_32x32b_x32(t_row + ch * 32, r);
@@ -590,14 +596,14 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensor
 }
 
 template <int BN, int STAGES, int EPI, int ACT, bool F32OUT, bool BETA>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __launch_bounds__(gemm_threads(EPI), 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ EpiMaps maps, const GemmArgs g) {
   gemm_body<BN, STAGES, EPI, ACT, F32OUT, BETA, false>(&tmA, &tmB, &maps, g);
 }
 
 template <int BN, int STAGES, int EPI, int ACT, bool F32OUT, bool BETA>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm_threads(EPI), 1)
     gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                            const __grid_constant__ EpiMaps maps, const GemmArgs g) {
   gemm_body<BN, STAGES, EPI, ACT, F32OUT, BETA, true>(&tmA, &tmB, &maps, g);
@@ -679,10 +685,19 @@ static int make_operand_map(CUtensorMap* map, const void* ptr, bool mn_major, in
                      mn_major ? BK : box_rows, name);
 }
 
-template <int BN, int STAGES, bool PAIR, int EPI, int ACT, bool F32OUT, bool BETA>
+// Operand-ring depth: as many stages as fit next to the epilogue staging boxes (max 8).
+constexpr int stages_for(int BN, bool pair, int epw) {
+  const int stage = BM * BK * 2 + (pair ? BN / 2 : BN) * BK * 2;
+  const int budget = 232448 - 1024 - 256 - epw * STG_BYTES;
+  return budget / stage < 8 ? budget / stage : 8;
+}
+
+template <int BN, int STAGES_UNUSED, bool PAIR, int EPI, int ACT, bool F32OUT, bool BETA>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& maps, GemmArgs& g,
                        cudaStream_t st) {
-  using Cfg = GemmCfg<BN, STAGES, PAIR>;
+  constexpr int STAGES = stages_for(BN, PAIR, epi_warps(EPI));
+  using Cfg = GemmCfg<BN, STAGES, PAIR, epi_warps(EPI)>;
+  static_assert(Cfg::SMEM_BYTES <= 232448, "shared memory budget");
   auto kern = PAIR ? gemm_bf16_tcgen05_pair<BN, STAGES, EPI, ACT, F32OUT, BETA>
                    : gemm_bf16_tcgen05<BN, STAGES, EPI, ACT, F32OUT, BETA>;
   static bool attr_set = false;
@@ -694,7 +709,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMa
   const int slots = PAIR ? num_sms() / 2 : num_sms();  // CTA pairs (one per TPC) or CTAs
   int grid = g.num_units < slots ? g.num_units : slots;
   if (PAIR) grid *= 2;
-  kern<<<grid, GEMM_THREADS, Cfg::SMEM_BYTES, st>>>(ta, tb, maps, g);
+  kern<<<grid, gemm_threads(EPI), Cfg::SMEM_BYTES, st>>>(ta, tb, maps, g);
   return check_launch("smpk_gemm");
 }
 
@@ -934,11 +949,12 @@ static int gemm_impl(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, 
   g.tma_store = tma ? 1 : 0;
 
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (BN == 64) return dispatch_epilogue<64, 6, false>(ta, tb, maps, g, st);
-  if (BN == 128) return pair ? dispatch_epilogue<128, 5, true>(ta, tb, maps, g, st)
-                             : dispatch_epilogue<128, 4, false>(ta, tb, maps, g, st);
-  return pair ? dispatch_epilogue<256, 4, true>(ta, tb, maps, g, st)
-              : dispatch_epilogue<256, 3, false>(ta, tb, maps, g, st);
+  // stage counts: stages_for() (fills the 227 KB of shared memory next to the staging boxes)
+  if (BN == 64) return dispatch_epilogue<64, 0, false>(ta, tb, maps, g, st);
+  if (BN == 128) return pair ? dispatch_epilogue<128, 0, true>(ta, tb, maps, g, st)
+                             : dispatch_epilogue<128, 0, false>(ta, tb, maps, g, st);
+  return pair ? dispatch_epilogue<256, 0, true>(ta, tb, maps, g, st)
+              : dispatch_epilogue<256, 0, false>(ta, tb, maps, g, st);
 }
 
 extern "C" int smpk_gemm(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, int64_t a_bs2, const void* b,
