@@ -251,6 +251,9 @@ SMPK_API int smpk_flash_attn_bwd(const void* qkv, int64_t ld, const void* out, i
  *                       (slot_stride elements apart) and storing its output to every out_peers[j]
  *                       + peer_off (allgather producer)
  *   smpk_ln_bwd_ex      smpk_ln_bwd with the same slot-sum input / peer-store output for dy / dsub
+ *                       keep_out (forward, may be NULL) stores the hidden-dropout keep bits as
+ *                       [M][H/8] bytes (bit j = column 8c+j); keep_in (backward) reads them
+ *                       instead of re-drawing the Philox stream
  *   smpk_symm_export    IPC handle + offset of a pointer inside its allocation
  *   smpk_symm_barrier   epoch barrier over the group (system-scope release/acquire flag words);
  *                       the epoch counter is device-resident (local_flags[32]) so a barrier
@@ -264,13 +267,13 @@ SMPK_API int smpk_bdr_ln_fwd_ex(const void* x, int nslots, int64_t slot_stride, 
                                 void* r_out, const void* gamma, const void* beta, void* y_out, float* mean,
                                 float* rstd, void* const* out_peers, int npeers, int64_t peer_off, int M, int H,
                                 float eps, float p_drop, uint64_t seed, int layer, int site, int64_t row_offset,
-                                void* stream);
+                                void* keep_out, void* stream);
 SMPK_API int smpk_ln_bwd_ex(const void* dy, int nslots, int64_t slot_stride, const void* r, const float* mean,
                             const float* rstd, const void* gamma, const void* dres, void* dr_out, void* dsub_out,
                             void* const* out_peers, int npeers, int64_t peer_off, void* dgamma, void* dbeta,
                             void* dbias, int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed,
-                            int layer, int site, int64_t row_offset, void* workspace, int64_t workspace_bytes,
-                            void* stream);
+                            int layer, int site, int64_t row_offset, const void* keep_in, void* workspace,
+                            int64_t workspace_bytes, void* stream);
 /*
  * Channel-sharded (memory-mode) LayerNorm, "local sum x, sum x^2 -> scalar
  * allreduce -> ApplyLayerNorm": activations hold H/T of the H_total channels.

@@ -67,9 +67,33 @@ __device__ __forceinline__ void store8(bf16* p, const float (&v)[8]) {
   u.w = pack_bf16x2(v[6], v[7]);
   *reinterpret_cast<uint4*>(p) = u;
 }
-__device__ __forceinline__ void round8(float (&v)[8]) {
+__device__ __forceinline__ void round8_int(float (&v)[8]) {
 #pragma unroll
   for (int j = 0; j < 8; ++j) v[j] = round_bf16(v[j]);
+}
+
+// bf16 round-to-nearest-even kept in fp32: one cvt.rn.bf16x2 per pair + unpack (the row
+// kernels are not XU-bound, unlike the GEMM epilogue that keeps the integer form)
+__device__ __forceinline__ void round8(float (&v)[8]) {
+#pragma unroll
+  for (int j = 0; j < 8; j += 2) {
+    const float2 f = unpack_bf16x2(pack_bf16x2(v[j], v[j + 1]));
+    v[j] = f.x;
+    v[j + 1] = f.y;
+  }
+}
+
+// keep flags of 8 columns: from the stored keep byte (bit j = column j) when the forward
+// saved it, else from Philox
+__device__ __forceinline__ void keep8_from_byte(uint32_t byte, bool (&keep)[8]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) keep[j] = (byte >> j) & 1u;
+}
+__device__ __forceinline__ uint32_t keep8_to_byte(const bool (&keep)[8]) {
+  uint32_t b = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) b |= (keep[j] ? 1u : 0u) << j;
+  return b;
 }
 
 struct RowGeom {
@@ -143,6 +167,7 @@ struct BdrLnArgs {
   float* row_sums_out;
   const float* ext_sums;
   int H_total;
+  uint8_t* keep_out;  // [M][H/8] hidden-dropout keep bytes for the backward (may be null)
 };
 
 __device__ __forceinline__ void load8_slots(const bf16* p, int nslots, int64_t stride, float (&v)[8]) {
@@ -198,6 +223,7 @@ __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs
           bool keep[8];
           dropout_keep8(a.seed, a.layer, a.site, (uint64_t)(a.row_offset + row), (int)(a.col_offset + col),
                         dropout_threshold(a.p), keep);
+          if (a.keep_out) a.keep_out[(int64_t)row * (a.H / 8) + col / 8] = (uint8_t)keep8_to_byte(keep);
 #pragma unroll
           for (int j = 0; j < 8; ++j) v[i][j] = keep[j] ? v[i][j] * inv_keep : 0.f;
         }
@@ -304,6 +330,7 @@ struct LnBwdArgs {
   float* row_sums_out;
   const float* ext_sums;
   int H_total;
+  const uint8_t* keep_in;  // [M][H/8] keep bytes saved by the forward (null: recompute Philox)
 };
 
 template <int W, int VPT>
@@ -436,8 +463,11 @@ __global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const LnBwdArgs a) 
       if (a.dr_out) store8(a.dr_out + (int64_t)row * a.H + col, d);
       if (a.p > 0.f) {
         bool keep[8];
-        dropout_keep8(a.seed, a.layer, a.site, (uint64_t)(a.row_offset + row), (int)(a.col_offset + col),
-                      dropout_threshold(a.p), keep);
+        if (a.keep_in)
+          keep8_from_byte(a.keep_in[(int64_t)row * (a.H / 8) + col / 8], keep);
+        else
+          dropout_keep8(a.seed, a.layer, a.site, (uint64_t)(a.row_offset + row), (int)(a.col_offset + col),
+                        dropout_threshold(a.p), keep);
 #pragma unroll
         for (int j = 0; j < 8; ++j) d[j] = keep[j] ? d[j] * inv_keep : 0.f;
         round8(d);
@@ -699,7 +729,8 @@ static int bdr_ln_impl(const void* x, int nslots, int64_t slot_stride, const voi
                        void* r_out, const void* gamma, const void* beta, void* y_out, float* mean, float* rstd,
                        void* const* out_peers, int npeers, int64_t peer_off, int M, int H, float eps, float p_drop,
                        uint64_t seed, int layer, int site, int64_t row_offset, int64_t col_offset,
-                       float* row_sums_out, const float* ext_sums, int H_total, void* stream) {
+                       float* row_sums_out, const float* ext_sums, int H_total, uint8_t* keep_out,
+                       void* stream) {
   RowGeom geo;
   SMPK_REQUIRE(M >= 0 && row_geom(H, geo) && geom_supported(geo), SMPK_ERR_UNSUPPORTED,
                "smpk_bdr_ln_fwd: hidden size %d unsupported (need a multiple of 8)", H);
@@ -717,7 +748,7 @@ static int bdr_ln_impl(const void* x, int nslots, int64_t slot_stride, const voi
               reinterpret_cast<const bf16*>(gamma), reinterpret_cast<const bf16*>(beta),
               reinterpret_cast<bf16*>(y_out), mean, rstd, M, H, eps, p_drop, seed, (uint32_t)layer, (uint32_t)site,
               row_offset, nslots, slot_stride, reinterpret_cast<bf16* const*>(out_peers), npeers, peer_off,
-              col_offset, row_sums_out, ext_sums, H_total};
+              col_offset, row_sums_out, ext_sums, H_total, keep_out};
   const int grid = row_grid(M, geo.W);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   SMPK_DISPATCH_ROW(geo.W, geo.VPT, bdr_ln_fwd_kernel, (grid, ROW_THREADS, 0, st), (a));
@@ -728,9 +759,10 @@ extern "C" int smpk_bdr_ln_fwd_ex(const void* x, int nslots, int64_t slot_stride
                                   const void* residual, void* r_out, const void* gamma, const void* beta, void* y_out,
                                   float* mean, float* rstd, void* const* out_peers, int npeers, int64_t peer_off, int M,
                                   int H, float eps, float p_drop, uint64_t seed, int layer, int site,
-                                  int64_t row_offset, void* stream) {
+                                  int64_t row_offset, void* keep_out, void* stream) {
   return bdr_ln_impl(x, nslots, slot_stride, bias, residual, r_out, gamma, beta, y_out, mean, rstd, out_peers, npeers,
-                     peer_off, M, H, eps, p_drop, seed, layer, site, row_offset, 0, nullptr, nullptr, 0, stream);
+                     peer_off, M, H, eps, p_drop, seed, layer, site, row_offset, 0, nullptr, nullptr, 0,
+                     reinterpret_cast<uint8_t*>(keep_out), stream);
 }
 
 extern "C" int smpk_bdr_ln_fwd_dist(const void* x, const void* bias, const void* residual, void* r_out,
@@ -739,14 +771,14 @@ extern "C" int smpk_bdr_ln_fwd_dist(const void* x, const void* bias, const void*
                                     int64_t row_offset, int64_t col_offset, float* row_sums_out,
                                     const float* ext_sums, int H_total, void* stream) {
   return bdr_ln_impl(x, 1, 0, bias, residual, r_out, gamma, beta, y_out, mean, rstd, nullptr, 0, 0, M, H, eps, p_drop,
-                     seed, layer, site, row_offset, col_offset, row_sums_out, ext_sums, H_total, stream);
+                     seed, layer, site, row_offset, col_offset, row_sums_out, ext_sums, H_total, nullptr, stream);
 }
 
 extern "C" int smpk_bdr_ln_fwd(const void* x, const void* bias, const void* residual, void* r_out, const void* gamma,
                                const void* beta, void* y_out, float* mean, float* rstd, int M, int H, float eps,
                                float p_drop, uint64_t seed, int layer, int site, int64_t row_offset, void* stream) {
   return smpk_bdr_ln_fwd_ex(x, 1, 0, bias, residual, r_out, gamma, beta, y_out, mean, rstd, nullptr, 0, 0, M, H, eps,
-                            p_drop, seed, layer, site, row_offset, stream);
+                            p_drop, seed, layer, site, row_offset, nullptr, stream);
 }
 
 // The backward keeps per-column accumulators in registers (two CTAs per SM): one wave of
@@ -771,7 +803,8 @@ static int ln_bwd_impl(const void* dy, int nslots, int64_t slot_stride, const vo
                        void* const* out_peers, int npeers, int64_t peer_off, void* dgamma, void* dbeta, void* dbias,
                        int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed, int layer, int site,
                        int64_t row_offset, int64_t col_offset, float* row_sums_out, const float* ext_sums,
-                       int H_total, void* workspace, int64_t workspace_bytes, void* stream) {
+                       int H_total, const uint8_t* keep_in, void* workspace, int64_t workspace_bytes,
+                       void* stream) {
   RowGeom geo;
   SMPK_REQUIRE(M > 0 && row_geom(H, geo) && geom_supported(geo), SMPK_ERR_UNSUPPORTED,
                "smpk_ln_bwd: hidden size %d unsupported", H);
@@ -792,7 +825,7 @@ static int ln_bwd_impl(const void* dy, int nslots, int64_t slot_stride, const vo
               reinterpret_cast<bf16*>(dr_out), reinterpret_cast<bf16*>(dsub_out),
               reinterpret_cast<float*>(workspace), M, H, p_drop, seed, (uint32_t)layer, (uint32_t)site, row_offset,
               nslots, slot_stride, reinterpret_cast<bf16* const*>(out_peers), npeers, peer_off, col_offset,
-              row_sums_out, ext_sums, H_total};
+              row_sums_out, ext_sums, H_total, keep_in};
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int red_bytes = geo.W == 8 ? 0 : geo.W * geo.VPT * 8 * 32 * 4;
   SMPK_DISPATCH_ROW(geo.W, geo.VPT, ln_bwd_kernel, (grid, ROW_THREADS, red_bytes, st), (a));
@@ -809,11 +842,12 @@ extern "C" int smpk_ln_bwd_ex(const void* dy, int nslots, int64_t slot_stride, c
                               const float* rstd, const void* gamma, const void* dres, void* dr_out, void* dsub_out,
                               void* const* out_peers, int npeers, int64_t peer_off, void* dgamma, void* dbeta,
                               void* dbias, int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed,
-                              int layer, int site, int64_t row_offset, void* workspace, int64_t workspace_bytes,
-                              void* stream) {
+                              int layer, int site, int64_t row_offset, const void* keep_in, void* workspace,
+                              int64_t workspace_bytes, void* stream) {
   return ln_bwd_impl(dy, nslots, slot_stride, r, mean, rstd, gamma, dres, dr_out, dsub_out, out_peers, npeers,
                      peer_off, dgamma, dbeta, dbias, grads_f32, accumulate, M, H, p_drop, seed, layer, site,
-                     row_offset, 0, nullptr, nullptr, 0, workspace, workspace_bytes, stream);
+                     row_offset, 0, nullptr, nullptr, 0, reinterpret_cast<const uint8_t*>(keep_in), workspace,
+                     workspace_bytes, stream);
 }
 
 extern "C" int smpk_ln_bwd_dist(const void* dy, const void* r, const float* mean, const float* rstd,
@@ -824,7 +858,7 @@ extern "C" int smpk_ln_bwd_dist(const void* dy, const void* r, const float* mean
                                 void* stream) {
   return ln_bwd_impl(dy, 1, 0, r, mean, rstd, gamma, dres, dr_out, dsub_out, nullptr, 0, 0, dgamma, dbeta, dbias,
                      grads_f32, 0, M, H, p_drop, seed, layer, site, row_offset, col_offset, row_sums_out, ext_sums,
-                     H_total, workspace, workspace_bytes, stream);
+                     H_total, nullptr, workspace, workspace_bytes, stream);
 }
 
 extern "C" int smpk_ln_bwd(const void* dy, const void* r, const float* mean, const float* rstd, const void* gamma,
@@ -832,7 +866,7 @@ extern "C" int smpk_ln_bwd(const void* dy, const void* r, const float* mean, con
                            int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed, int layer,
                            int site, int64_t row_offset, void* workspace, int64_t workspace_bytes, void* stream) {
   return smpk_ln_bwd_ex(dy, 1, 0, r, mean, rstd, gamma, dres, dr_out, dsub_out, nullptr, 0, 0, dgamma, dbeta, dbias,
-                        grads_f32, accumulate, M, H, p_drop, seed, layer, site, row_offset, workspace,
+                        grads_f32, accumulate, M, H, p_drop, seed, layer, site, row_offset, nullptr, workspace,
                         workspace_bytes, stream);
 }
 

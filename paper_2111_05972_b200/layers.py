@@ -274,12 +274,13 @@ def _rs_out(a, w, w_mn: bool, m: LayerMeta, R: int, N: int):
     return _combine_rows(y, m), 1, 0, None
 
 
-def _gather_grad(dy2, r, mean, rstd, m: LayerMeta, site: int):
+def _gather_grad(dy2, r, mean, rstd, m: LayerMeta, site: int, keep=None):
     """Backward of the sub-layer epilogue on own rows; the branch gradient is gathered for the
-    column/row-parallel GEMMs.  Returns (dr, dbranch_full, dgamma, dbeta, region)."""
+    column/row-parallel GEMMs.  keep: the forward's hidden-dropout keep bytes.
+    Returns (dr, dbranch_full, dgamma, dbeta, region)."""
     R, H = dy2.shape
     kw = dict(p=m.p_hidden, seed=m.seed, layer=m.layer_id, site=site, row_offset=m.row_offset,
-              want_dr=m.post_ln, want_dbias=False)
+              want_dr=m.post_ln, want_dbias=False, keep_in=keep)
     if _peer(m, R):
         pool = get_pool()
         G = pool.scratch("grad_gather", m.tp_size * R * H * 2)
@@ -334,10 +335,12 @@ class AttentionFn(torch.autograd.Function):
         else:
             ctxv, P, Pd = attn_core_fwd(qkv, B, s, m, mask_add)
         ox, ns, st, PR = _rs_out(ctxv, wo, False, m, R, H)
+        kb = ops.keep_bytes(R, H, x.device) if m.p_hidden > 0 else None  # reused by the backward
         r, y, mu2, rs2 = ops.bdr_ln(ox, bias=bo, residual=x2, gamma=post_w if m.post_ln else None,
                                     beta=post_b if m.post_ln else None, eps=m.eps, p=m.p_hidden, seed=m.seed,
                                     layer=m.layer_id, site=SITE_ATTN_OUT, row_offset=m.row_offset, nslots=ns,
-                                    slot_stride=st, rows=R, cols=H)
+                                    slot_stride=st, rows=R, cols=H, keep_out=kb)
+        ctx.kb = kb
         _free(PR)
         if not any(ctx.needs_input_grad):
             _free(G)
@@ -358,7 +361,7 @@ class AttentionFn(torch.autograd.Function):
             Pd = P
         dy2 = dy.reshape(R, H).contiguous()
         m._post_w = post_w if m.post_ln else None
-        dr, dof, dpost_w, dpost_b, G2 = _gather_grad(dy2, r, mu2, rs2, m, SITE_ATTN_OUT)
+        dr, dof, dpost_w, dpost_b, G2 = _gather_grad(dy2, r, mu2, rs2, m, SITE_ATTN_OUT, ctx.kb)
         if not m.post_ln:
             dr = dy2
         dbo = ops.colsum(dof)  # over all rows of the group: complete on every rank
@@ -396,10 +399,12 @@ class MlpFn(torch.autograd.Function):
         hf, mu1, rs1, G = _gather_in(x2, m, (pre_w, pre_b) if m.pre_ln else None)
         f, z = K.linear(hf, w1, b1, act=m.activation)
         gx, ns, st, PR = _rs_out(f, w2, False, m, R, H)
+        kb = ops.keep_bytes(R, H, x.device) if m.p_hidden > 0 else None  # reused by the backward
         r, y, mu2, rs2 = ops.bdr_ln(gx, bias=b2, residual=x2, gamma=post_w if m.post_ln else None,
                                     beta=post_b if m.post_ln else None, eps=m.eps, p=m.p_hidden, seed=m.seed,
                                     layer=m.layer_id, site=SITE_MLP_OUT, row_offset=m.row_offset, nslots=ns,
-                                    slot_stride=st, rows=R, cols=H)
+                                    slot_stride=st, rows=R, cols=H, keep_out=kb)
+        ctx.kb = kb
         _free(PR)
         if not any(ctx.needs_input_grad):
             _free(G)
@@ -417,7 +422,7 @@ class MlpFn(torch.autograd.Function):
         x2, hf, mu1, rs1, f, z, r, mu2, rs2, w1, w2, pre_w, post_w = ctx.saved_tensors
         dy2 = dy.reshape(R, H).contiguous()
         m._post_w = post_w if m.post_ln else None
-        dr, dgf, dpost_w, dpost_b, G2 = _gather_grad(dy2, r, mu2, rs2, m, SITE_MLP_OUT)
+        dr, dgf, dpost_w, dpost_b, G2 = _gather_grad(dy2, r, mu2, rs2, m, SITE_MLP_OUT, ctx.kb)
         if not m.post_ln:
             dr = dy2
         db2 = ops.colsum(dgf)

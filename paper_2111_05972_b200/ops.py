@@ -19,12 +19,13 @@ def _f32(t):
 
 def bdr_ln(x: torch.Tensor, *, bias=None, residual=None, gamma=None, beta=None, eps=1e-5, p=0.0, seed=0,
            layer=0, site=SITE_ATTN_OUT, row_offset=0, want_r=True, want_y=True, nslots=1, slot_stride=0,
-           out_peers=None, peer_off=0, rows=None, cols=None):
+           out_peers=None, peer_off=0, rows=None, cols=None, keep_out=None):
     """r = residual + dropout(x + bias); y = LN(r). Returns (r, y, mean, rstd) (None where not computed).
 
     nslots > 1: x is the ascending-rank sum of nslots partial slots slot_stride elements apart
     (reduce-scatter consumer); out_peers (device table of peer addresses): the output is also
-    stored to every peer at element offset peer_off (allgather producer)."""
+    stored to every peer at element offset peer_off (allgather producer); keep_out ([M, H/8]
+    uint8) receives the hidden-dropout keep bits for the backward."""
     _check_cuda(x, bias, residual, gamma, beta)
     M, H = (rows, cols) if rows is not None else x.shape
     r = torch.empty(M, H, dtype=torch.bfloat16, device=x.device) if want_r else None
@@ -36,13 +37,19 @@ def bdr_ln(x: torch.Tensor, *, bias=None, residual=None, gamma=None, beta=None, 
     npeers = 0 if out_peers is None else out_peers.numel()
     _lib.call("smpk_bdr_ln_fwd_ex", _ptr(x), int(nslots), int(slot_stride), _ptr(bias), _ptr(residual), _ptr(r),
               _ptr(gamma), _ptr(beta), _ptr(y), _ptr(mean), _ptr(rstd), _ptr(out_peers), npeers, int(peer_off), M, H,
-              float(eps), float(p), int(seed) & (2 ** 64 - 1), int(layer), int(site), int(row_offset), _stream())
+              float(eps), float(p), int(seed) & (2 ** 64 - 1), int(layer), int(site), int(row_offset),
+              _ptr(keep_out if p > 0 else None), _stream())
     return r, y, mean, rstd
 
 
 def layer_norm(x: torch.Tensor, gamma, beta, eps=1e-5):
     _, y, mean, rstd = bdr_ln(x, gamma=gamma, beta=beta, eps=eps, want_r=False)
     return y, mean, rstd
+
+
+def keep_bytes(M: int, H: int, device) -> torch.Tensor:
+    """Buffer for the hidden-dropout keep bits of an [M, H] activation ([M, H/8] bytes)."""
+    return torch.empty(M, (H + 7) // 8, dtype=torch.uint8, device=device)
 
 
 def add(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
@@ -53,7 +60,7 @@ def add(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
 
 def ln_bwd(dy, r, mean, rstd, gamma, *, dres=None, p=0.0, seed=0, layer=0, site=SITE_ATTN_OUT, row_offset=0,
            want_dgamma=True, want_dbias=True, grads_f32=False, want_dr=True, nslots=1, slot_stride=0,
-           out_peers=None, peer_off=0, rows=None, cols=None):
+           out_peers=None, peer_off=0, rows=None, cols=None, keep_in=None):
     """Backward of bdr_ln. Returns (dr, dsub, dgamma, dbeta, dbias); dsub is dr when p == 0.
 
     gamma None = no-LayerNorm mode (d = dy + dres).  nslots / out_peers as in bdr_ln (dy read as a
@@ -73,7 +80,7 @@ def ln_bwd(dy, r, mean, rstd, gamma, *, dres=None, p=0.0, seed=0, layer=0, site=
     _lib.call("smpk_ln_bwd_ex", _ptr(dy), int(nslots), int(slot_stride), _ptr(r), _ptr(mean), _ptr(rstd),
               _ptr(gamma), _ptr(dres), _ptr(dr), _ptr(dsub), _ptr(out_peers), npeers, int(peer_off), _ptr(dgamma),
               _ptr(dbeta), _ptr(dbias), int(grads_f32), 0, M, H, float(p), int(seed) & (2 ** 64 - 1), int(layer),
-              int(site), int(row_offset), _ptr(ws), int(ws_bytes), _stream(),
+              int(site), int(row_offset), _ptr(keep_in if p > 0 else None), _ptr(ws), int(ws_bytes), _stream(),
               launches=2 if (dgamma is not None or dbeta is not None or dbias is not None) else 1)
     if dsub is None:
         dsub = dr if dr is not None else (dy if nslots == 1 else None)

@@ -140,3 +140,27 @@ def test_bdr_ln_deterministic(ops):
     b = ops.bdr_ln(x, gamma=gam, beta=bet, p=0.1, seed=3)
     for u, v in zip(a, b):
         assert torch.equal(u, v)
+
+
+def test_hidden_keep_bytes_roundtrip(ops):
+    """bdr_ln stores the hidden-dropout keep bits it draws; ln_bwd reading them is bit-identical
+    to re-drawing the Philox stream, and the bits equal oracle/philox.py's mask."""
+    M, H, p, seed, layer, site, row0 = 640, 1024, 0.2, 77, 5, ops.SITE_MLP_OUT, 4096
+    g = torch.Generator().manual_seed(3)
+    x = bf(torch.randn(M, H, generator=g)).cuda()
+    res = bf(torch.randn(M, H, generator=g)).cuda()
+    gam = bf(1 + 0.1 * torch.randn(H, generator=g)).cuda()
+    bet = bf(0.1 * torch.randn(H, generator=g)).cuda()
+    kb = ops.keep_bytes(M, H, "cuda")
+    r, y, mean, rstd = ops.bdr_ln(x, residual=res, gamma=gam, beta=bet, p=p, seed=seed, layer=layer, site=site,
+                                  row_offset=row0, keep_out=kb)
+    bits = np.unpackbits(kb.cpu().numpy(), axis=1, bitorder="little").astype(bool)
+    ref = philox.hidden_mask(np.arange(M) + row0, H, layer, site, seed, p)
+    assert np.array_equal(bits, ref.reshape(M, H))
+    dy = bf(torch.randn(M, H, generator=g)).cuda()
+    kw = dict(p=p, seed=seed, layer=layer, site=site, row_offset=row0)
+    a = ops.ln_bwd(dy, r, mean, rstd, gam, **kw)
+    b = ops.ln_bwd(dy, r, mean, rstd, gam, keep_in=kb, **kw)
+    for u, v in zip(a, b):
+        if u is not None:
+            assert torch.equal(u, v)
