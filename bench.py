@@ -226,6 +226,11 @@ def trace_kernels(run, path_prefix: str, rank: int, steps: int = 2) -> None:
         a[0] += 1
         a[1] += ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total
     tot = sum(v[1] for v in agg.values())
+    seq = [(ev.name, ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total)
+           for ev in prof.events() if ev.device_type == torch.autograd.DeviceType.CUDA]
+    with open(f"{path_prefix}_rank{rank}_seq.txt", "w") as f:  # launch order of the first step
+        for name, us in seq[:len(seq) // steps]:
+            f.write(f"{us:9.1f}  {name[:110]}\n")
     with open(f"{path_prefix}_rank{rank}.txt", "w") as f:
         f.write(f"# {steps} steps, total kernel time {tot / steps / 1e3:.3f} ms/step\n")
         for name, (n, us) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
@@ -237,7 +242,8 @@ def run_gpu(args, rank, world, local):
     from paper_2111_05972_b200 import _lib, kernels
 
     torch.cuda.set_device(local)
-    smp.init({"tensor_parallel_degree": world, "optimize": args.optimize, "seed": 1234, "tp_comm": args.tp_comm})
+    smp.init({"tensor_parallel_degree": world, "optimize": args.optimize, "seed": 1234, "tp_comm": args.tp_comm,
+              "tp_rs": args.tp_rs})
     torch.manual_seed(1000 + rank)
     model = smp.nn.DistributedTransformer(**CFG)
     model.train()
@@ -397,6 +403,8 @@ def main():
                     help="smp optimize mode of the TP layers (PAPER.md:763); the headline is speed")
     ap.add_argument("--tp-comm", default="peer", choices=["peer", "nccl"],
                     help="TP collectives: fused NVLink peer stores (default) or NCCL calls")
+    ap.add_argument("--tp-rs", default="pull", choices=["pull", "push"],
+                    help="peer reduce-scatter: consumer pulls partials over NVLink, or GEMM epilogue pushes")
     ap.add_argument("--trace", default="", help="diagnostics: write a per-kernel CUPTI trace summary to PREFIX_rankR.txt")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))

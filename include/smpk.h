@@ -253,7 +253,10 @@ SMPK_API int smpk_flash_attn_bwd(const void* qkv, int64_t ld, const void* out, i
  *   smpk_ln_bwd_ex      smpk_ln_bwd with the same slot-sum input / peer-store output for dy / dsub
  *                       keep_out (forward, may be NULL) stores the hidden-dropout keep bits as
  *                       [M][H/8] bytes (bit j = column 8c+j); keep_in (backward) reads them
- *                       instead of re-drawing the Philox stream
+ *                       instead of re-drawing the Philox stream; x_peers / dy_peers (device table
+ *                       of the T peer-mapped pool bases, may be NULL) make the input the
+ *                       ascending-rank sum of the nslots peers' rows at element offset
+ *                       x_peer_off (reduce-scatter consumer pulling the partials over NVLink)
  *   smpk_symm_export    IPC handle + offset of a pointer inside its allocation
  *   smpk_symm_barrier   epoch barrier over the group (system-scope release/acquire flag words);
  *                       the epoch counter is device-resident (local_flags[32]) so a barrier
@@ -267,13 +270,13 @@ SMPK_API int smpk_bdr_ln_fwd_ex(const void* x, int nslots, int64_t slot_stride, 
                                 void* r_out, const void* gamma, const void* beta, void* y_out, float* mean,
                                 float* rstd, void* const* out_peers, int npeers, int64_t peer_off, int M, int H,
                                 float eps, float p_drop, uint64_t seed, int layer, int site, int64_t row_offset,
-                                void* keep_out, void* stream);
+                                void* keep_out, void* const* x_peers, int64_t x_peer_off, void* stream);
 SMPK_API int smpk_ln_bwd_ex(const void* dy, int nslots, int64_t slot_stride, const void* r, const float* mean,
                             const float* rstd, const void* gamma, const void* dres, void* dr_out, void* dsub_out,
                             void* const* out_peers, int npeers, int64_t peer_off, void* dgamma, void* dbeta,
                             void* dbias, int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed,
-                            int layer, int site, int64_t row_offset, const void* keep_in, void* workspace,
-                            int64_t workspace_bytes, void* stream);
+                            int layer, int site, int64_t row_offset, const void* keep_in, void* const* dy_peers,
+                            int64_t dy_peer_off, void* workspace, int64_t workspace_bytes, void* stream);
 /*
  * Channel-sharded (memory-mode) LayerNorm, "local sum x, sum x^2 -> scalar
  * allreduce -> ApplyLayerNorm": activations hold H/T of the H_total channels.
@@ -304,6 +307,8 @@ SMPK_API int smpk_ln_bwd_dist(const void* dy, const void* r, const float* mean, 
 SMPK_API int smpk_bias_act_fwd(const void* x, const void* bias, int M, int N, int act, void* pre_out, void* y,
                                void* stream);
 SMPK_API int smpk_act_bwd(const void* dy, const void* pre, int M, int N, int act, void* dx, void* stream);
+/* smpk_copy_async — stream-ordered device-to-device copy (copy engine; dst may be peer-mapped). */
+SMPK_API int smpk_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
 SMPK_API int smpk_symm_export(void* ptr, void* handle_out, int64_t* offset);
 SMPK_API int smpk_symm_barrier(void* const* peer_flags, void* local_flags, int T, int rank, double timeout_s,
                                void* stream);

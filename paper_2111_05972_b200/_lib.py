@@ -42,12 +42,14 @@ SIGNATURES: dict[str, list] = {
     "smpk_attn_dropout_bits": [I, I, I, I, F, C.c_uint64, I, L, I, I, P, P],
     "smpk_flash_attn_bwd": [P, L, P, L, P, L, P, I, I, I, I, P, P, F, I, F, P, P, L, P],
     "smpk_gemm_rs": [P, I, L, P, I, L, P, I, L, L, L, I, I, I, P],
-    "smpk_bdr_ln_fwd_ex": [P, I, L, P, P, P, P, P, P, P, P, P, I, L, I, I, F, F, C.c_uint64, I, I, L, P, P],
+    "smpk_bdr_ln_fwd_ex": [P, I, L, P, P, P, P, P, P, P, P, P, I, L, I, I, F, F, C.c_uint64, I, I, L, P, P, L, P],
     "smpk_bdr_ln_fwd_dist": [P, P, P, P, P, P, P, P, P, I, I, F, F, C.c_uint64, I, I, L, L, P, P, I, P],
     "smpk_ln_bwd_dist": [P, P, P, P, P, P, P, P, P, P, P, I, I, I, F, C.c_uint64, I, I, L, L, P, P, I, P, L, P],
     "smpk_bias_act_fwd": [P, P, I, I, I, P, P, P],
     "smpk_act_bwd": [P, P, I, I, I, P, P],
-    "smpk_ln_bwd_ex": [P, I, L, P, P, P, P, P, P, P, P, I, L, P, P, P, I, I, I, I, F, C.c_uint64, I, I, L, P, P, L, P],
+    "smpk_copy_async": [P, P, L, P],
+    "smpk_ln_bwd_ex": [P, I, L, P, P, P, P, P, P, P, P, I, L, P, P, P, I, I, I, I, F, C.c_uint64, I, I, L, P, P, L, P,
+                       L, P],
     "smpk_symm_export": [P, P, C.POINTER(L)],
     "smpk_symm_barrier": [P, P, I, I, C.c_double, P],
     "smpk_symm_timeout_peer": [],
@@ -102,7 +104,7 @@ def lib() -> C.CDLL:
 
 
 # kernels launched by each entry point (for bench.py's gpu_launches count)
-LAUNCHES_PER_CALL = {"smpk_ln_bwd": 2, "smpk_ln_bwd_ex": 2, "smpk_ln_bwd_dist": 2, "smpk_colsum": 2, "smpk_flash_attn_bwd": 3}
+LAUNCHES_PER_CALL = {"smpk_copy_async": 0, "smpk_ln_bwd": 2, "smpk_ln_bwd_ex": 2, "smpk_ln_bwd_dist": 2, "smpk_colsum": 2, "smpk_flash_attn_bwd": 3}
 launch_count = 0
 
 

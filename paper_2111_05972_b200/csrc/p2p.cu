@@ -104,6 +104,16 @@ extern "C" int smpk_p2p_send(void* peer_slot, const void* src, int64_t bytes, vo
   return SMPK_OK;
 }
 
+// Plain stream-ordered device copy (copy engine), also to a peer-mapped address: the TP
+// exchanges issued on side streams so the SMs keep computing while the bytes move.
+extern "C" int smpk_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  SMPK_REQUIRE(dst && src && bytes >= 0, SMPK_ERR_BAD_ARG, "smpk_copy_async: bad arguments");
+  cudaError_t e = cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice,
+                                  reinterpret_cast<cudaStream_t>(stream));
+  SMPK_REQUIRE(e == cudaSuccess, SMPK_ERR_CUDA, "smpk_copy_async: %s", cudaGetErrorString(e));
+  return SMPK_OK;
+}
+
 // Receiver side: wait local_ready >= seq + 1, copy slot -> dst (if dst), then free the
 // slot by writing peer_free = seq + 1 (mapped address of the sender's free-counter).
 extern "C" int smpk_p2p_recv(void* dst, const void* local_slot, int64_t bytes, const void* local_ready,

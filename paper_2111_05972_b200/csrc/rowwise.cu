@@ -168,6 +168,9 @@ struct BdrLnArgs {
   const float* ext_sums;
   int H_total;
   uint8_t* keep_out;  // [M][H/8] hidden-dropout keep bytes for the backward (may be null)
+  // x read as the ascending-rank sum over the nslots peers' buffers x_peers[j] + x_peer_off
+  const bf16* const* x_peers;
+  int64_t x_peer_off;
 };
 
 __device__ __forceinline__ void load8_slots(const bf16* p, int nslots, int64_t stride, float (&v)[8]) {
@@ -177,6 +180,29 @@ __device__ __forceinline__ void load8_slots(const bf16* p, int nslots, int64_t s
     load8(p + j * stride, t);
 #pragma unroll
     for (int e = 0; e < 8; ++e) v[e] += t[e];
+  }
+}
+
+// reduce-scatter consumer over peer memory (pull): the ascending-rank sum of the T ranks'
+// partial rows, rank j's at peers[j] + off (its own GEMM output in its symmetric pool)
+__device__ __forceinline__ void load8_peer_slots(const bf16* const* peers, int n, int64_t off, float (&v)[8]) {
+  // all (<= 8) remote loads in flight before the first add: NVLink latency is ~us
+  uint4 raw[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (j < n) raw[j] = *reinterpret_cast<const uint4*>(peers[j] + off);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) v[e] = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (j >= n) break;
+    const uint32_t w[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 f = unpack_bf16x2(w[q]);
+      v[2 * q] += f.x;
+      v[2 * q + 1] += f.y;
+    }
   }
 }
 
@@ -205,7 +231,10 @@ __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs
     for (int i = 0; i < VPT; ++i) {
       const int col = ((i * W + wi) * 32 + lane) * 8;
       if (valid && col < a.H) {
-        load8_slots(a.x + (int64_t)row * a.H + col, a.nslots, a.slot_stride, v[i]);
+        if (a.x_peers)
+          load8_peer_slots(a.x_peers, a.nslots, a.x_peer_off + (int64_t)row * a.H + col, v[i]);
+        else
+          load8_slots(a.x + (int64_t)row * a.H + col, a.nslots, a.slot_stride, v[i]);
         if (a.residual) load8(a.residual + (int64_t)row * a.H + col, res[i]);
       }
     }
@@ -331,6 +360,8 @@ struct LnBwdArgs {
   const float* ext_sums;
   int H_total;
   const uint8_t* keep_in;  // [M][H/8] keep bytes saved by the forward (null: recompute Philox)
+  const bf16* const* dy_peers;  // dy = ascending-rank sum over dy_peers[j] + dy_peer_off (pull)
+  int64_t dy_peer_off;
 };
 
 template <int W, int VPT>
@@ -405,11 +436,17 @@ __global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const LnBwdArgs a) 
     for (int i = 0; i < VPT; ++i) {
       const int col = ((i * W + wi) * 32 + lane) * 8;
       if (valid && col < a.H && !has_ln) {
-        load8_slots(a.dy + (int64_t)row * a.H + col, a.nslots, a.slot_stride, g[i]);
+        if (a.dy_peers)
+          load8_peer_slots(a.dy_peers, a.nslots, a.dy_peer_off + (int64_t)row * a.H + col, g[i]);
+        else
+          load8_slots(a.dy + (int64_t)row * a.H + col, a.nslots, a.slot_stride, g[i]);
       } else if (valid && col < a.H) {
         float dy[8], gm[8];
         load8(a.r + (int64_t)row * a.H + col, xh[i]);
-        load8_slots(a.dy + (int64_t)row * a.H + col, a.nslots, a.slot_stride, dy);
+        if (a.dy_peers)
+          load8_peer_slots(a.dy_peers, a.nslots, a.dy_peer_off + (int64_t)row * a.H + col, dy);
+        else
+          load8_slots(a.dy + (int64_t)row * a.H + col, a.nslots, a.slot_stride, dy);
         load8(a.gamma + col, gm);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -730,11 +767,12 @@ static int bdr_ln_impl(const void* x, int nslots, int64_t slot_stride, const voi
                        void* const* out_peers, int npeers, int64_t peer_off, int M, int H, float eps, float p_drop,
                        uint64_t seed, int layer, int site, int64_t row_offset, int64_t col_offset,
                        float* row_sums_out, const float* ext_sums, int H_total, uint8_t* keep_out,
-                       void* stream) {
+                       void* const* x_peers, int64_t x_peer_off, void* stream) {
   RowGeom geo;
   SMPK_REQUIRE(M >= 0 && row_geom(H, geo) && geom_supported(geo), SMPK_ERR_UNSUPPORTED,
                "smpk_bdr_ln_fwd: hidden size %d unsupported (need a multiple of 8)", H);
-  SMPK_REQUIRE(x != nullptr && nslots >= 1, SMPK_ERR_BAD_ARG, "smpk_bdr_ln_fwd: null x");
+  SMPK_REQUIRE((x != nullptr || x_peers != nullptr) && nslots >= 1, SMPK_ERR_BAD_ARG, "smpk_bdr_ln_fwd: null x");
+  SMPK_REQUIRE(!x_peers || nslots <= 8, SMPK_ERR_UNSUPPORTED, "smpk_bdr_ln_fwd: at most 8 peer slots");
   SMPK_REQUIRE(gamma == nullptr || (beta && mean && rstd && (y_out || npeers)), SMPK_ERR_BAD_ARG,
                "smpk_bdr_ln_fwd: LayerNorm needs beta, mean, rstd and an output");
   SMPK_REQUIRE(gamma != nullptr || r_out != nullptr || npeers > 0 || row_sums_out, SMPK_ERR_BAD_ARG,
@@ -748,7 +786,8 @@ static int bdr_ln_impl(const void* x, int nslots, int64_t slot_stride, const voi
               reinterpret_cast<const bf16*>(gamma), reinterpret_cast<const bf16*>(beta),
               reinterpret_cast<bf16*>(y_out), mean, rstd, M, H, eps, p_drop, seed, (uint32_t)layer, (uint32_t)site,
               row_offset, nslots, slot_stride, reinterpret_cast<bf16* const*>(out_peers), npeers, peer_off,
-              col_offset, row_sums_out, ext_sums, H_total, keep_out};
+              col_offset, row_sums_out, ext_sums, H_total, keep_out, reinterpret_cast<const bf16* const*>(x_peers),
+              x_peer_off};
   const int grid = row_grid(M, geo.W);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   SMPK_DISPATCH_ROW(geo.W, geo.VPT, bdr_ln_fwd_kernel, (grid, ROW_THREADS, 0, st), (a));
@@ -759,10 +798,11 @@ extern "C" int smpk_bdr_ln_fwd_ex(const void* x, int nslots, int64_t slot_stride
                                   const void* residual, void* r_out, const void* gamma, const void* beta, void* y_out,
                                   float* mean, float* rstd, void* const* out_peers, int npeers, int64_t peer_off, int M,
                                   int H, float eps, float p_drop, uint64_t seed, int layer, int site,
-                                  int64_t row_offset, void* keep_out, void* stream) {
+                                  int64_t row_offset, void* keep_out, void* const* x_peers, int64_t x_peer_off,
+                                  void* stream) {
   return bdr_ln_impl(x, nslots, slot_stride, bias, residual, r_out, gamma, beta, y_out, mean, rstd, out_peers, npeers,
                      peer_off, M, H, eps, p_drop, seed, layer, site, row_offset, 0, nullptr, nullptr, 0,
-                     reinterpret_cast<uint8_t*>(keep_out), stream);
+                     reinterpret_cast<uint8_t*>(keep_out), x_peers, x_peer_off, stream);
 }
 
 extern "C" int smpk_bdr_ln_fwd_dist(const void* x, const void* bias, const void* residual, void* r_out,
@@ -771,14 +811,15 @@ extern "C" int smpk_bdr_ln_fwd_dist(const void* x, const void* bias, const void*
                                     int64_t row_offset, int64_t col_offset, float* row_sums_out,
                                     const float* ext_sums, int H_total, void* stream) {
   return bdr_ln_impl(x, 1, 0, bias, residual, r_out, gamma, beta, y_out, mean, rstd, nullptr, 0, 0, M, H, eps, p_drop,
-                     seed, layer, site, row_offset, col_offset, row_sums_out, ext_sums, H_total, nullptr, stream);
+                     seed, layer, site, row_offset, col_offset, row_sums_out, ext_sums, H_total, nullptr, nullptr, 0,
+                     stream);
 }
 
 extern "C" int smpk_bdr_ln_fwd(const void* x, const void* bias, const void* residual, void* r_out, const void* gamma,
                                const void* beta, void* y_out, float* mean, float* rstd, int M, int H, float eps,
                                float p_drop, uint64_t seed, int layer, int site, int64_t row_offset, void* stream) {
   return smpk_bdr_ln_fwd_ex(x, 1, 0, bias, residual, r_out, gamma, beta, y_out, mean, rstd, nullptr, 0, 0, M, H, eps,
-                            p_drop, seed, layer, site, row_offset, nullptr, stream);
+                            p_drop, seed, layer, site, row_offset, nullptr, nullptr, 0, stream);
 }
 
 // The backward keeps per-column accumulators in registers (two CTAs per SM): one wave of
@@ -803,12 +844,13 @@ static int ln_bwd_impl(const void* dy, int nslots, int64_t slot_stride, const vo
                        void* const* out_peers, int npeers, int64_t peer_off, void* dgamma, void* dbeta, void* dbias,
                        int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed, int layer, int site,
                        int64_t row_offset, int64_t col_offset, float* row_sums_out, const float* ext_sums,
-                       int H_total, const uint8_t* keep_in, void* workspace, int64_t workspace_bytes,
-                       void* stream) {
+                       int H_total, const uint8_t* keep_in, void* const* dy_peers, int64_t dy_peer_off,
+                       void* workspace, int64_t workspace_bytes, void* stream) {
   RowGeom geo;
   SMPK_REQUIRE(M > 0 && row_geom(H, geo) && geom_supported(geo), SMPK_ERR_UNSUPPORTED,
                "smpk_ln_bwd: hidden size %d unsupported", H);
-  SMPK_REQUIRE(dy && nslots >= 1 && (gamma == nullptr || (r && mean && rstd && (dr_out || row_sums_out))),
+  SMPK_REQUIRE(!dy_peers || nslots <= 8, SMPK_ERR_UNSUPPORTED, "smpk_ln_bwd: at most 8 peer slots");
+  SMPK_REQUIRE((dy || dy_peers) && nslots >= 1 && (gamma == nullptr || (r && mean && rstd && (dr_out || row_sums_out))),
                SMPK_ERR_BAD_ARG, "smpk_ln_bwd: null argument");
   SMPK_REQUIRE(!row_sums_out || (gamma && !ext_sums), SMPK_ERR_BAD_ARG,
                "smpk_ln_bwd_dist: the sums pass needs gamma and no external sums");
@@ -825,7 +867,7 @@ static int ln_bwd_impl(const void* dy, int nslots, int64_t slot_stride, const vo
               reinterpret_cast<bf16*>(dr_out), reinterpret_cast<bf16*>(dsub_out),
               reinterpret_cast<float*>(workspace), M, H, p_drop, seed, (uint32_t)layer, (uint32_t)site, row_offset,
               nslots, slot_stride, reinterpret_cast<bf16* const*>(out_peers), npeers, peer_off, col_offset,
-              row_sums_out, ext_sums, H_total, keep_in};
+              row_sums_out, ext_sums, H_total, keep_in, reinterpret_cast<const bf16* const*>(dy_peers), dy_peer_off};
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int red_bytes = geo.W == 8 ? 0 : geo.W * geo.VPT * 8 * 32 * 4;
   SMPK_DISPATCH_ROW(geo.W, geo.VPT, ln_bwd_kernel, (grid, ROW_THREADS, red_bytes, st), (a));
@@ -842,12 +884,12 @@ extern "C" int smpk_ln_bwd_ex(const void* dy, int nslots, int64_t slot_stride, c
                               const float* rstd, const void* gamma, const void* dres, void* dr_out, void* dsub_out,
                               void* const* out_peers, int npeers, int64_t peer_off, void* dgamma, void* dbeta,
                               void* dbias, int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed,
-                              int layer, int site, int64_t row_offset, const void* keep_in, void* workspace,
-                              int64_t workspace_bytes, void* stream) {
+                              int layer, int site, int64_t row_offset, const void* keep_in, void* const* dy_peers,
+                              int64_t dy_peer_off, void* workspace, int64_t workspace_bytes, void* stream) {
   return ln_bwd_impl(dy, nslots, slot_stride, r, mean, rstd, gamma, dres, dr_out, dsub_out, out_peers, npeers,
                      peer_off, dgamma, dbeta, dbias, grads_f32, accumulate, M, H, p_drop, seed, layer, site,
-                     row_offset, 0, nullptr, nullptr, 0, reinterpret_cast<const uint8_t*>(keep_in), workspace,
-                     workspace_bytes, stream);
+                     row_offset, 0, nullptr, nullptr, 0, reinterpret_cast<const uint8_t*>(keep_in), dy_peers,
+                     dy_peer_off, workspace, workspace_bytes, stream);
 }
 
 extern "C" int smpk_ln_bwd_dist(const void* dy, const void* r, const float* mean, const float* rstd,
@@ -858,7 +900,7 @@ extern "C" int smpk_ln_bwd_dist(const void* dy, const void* r, const float* mean
                                 void* stream) {
   return ln_bwd_impl(dy, 1, 0, r, mean, rstd, gamma, dres, dr_out, dsub_out, nullptr, 0, 0, dgamma, dbeta, dbias,
                      grads_f32, 0, M, H, p_drop, seed, layer, site, row_offset, col_offset, row_sums_out, ext_sums,
-                     H_total, nullptr, workspace, workspace_bytes, stream);
+                     H_total, nullptr, nullptr, 0, workspace, workspace_bytes, stream);
 }
 
 extern "C" int smpk_ln_bwd(const void* dy, const void* r, const float* mean, const float* rstd, const void* gamma,
@@ -866,8 +908,8 @@ extern "C" int smpk_ln_bwd(const void* dy, const void* r, const float* mean, con
                            int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed, int layer,
                            int site, int64_t row_offset, void* workspace, int64_t workspace_bytes, void* stream) {
   return smpk_ln_bwd_ex(dy, 1, 0, r, mean, rstd, gamma, dres, dr_out, dsub_out, nullptr, 0, 0, dgamma, dbeta, dbias,
-                        grads_f32, accumulate, M, H, p_drop, seed, layer, site, row_offset, nullptr, workspace,
-                        workspace_bytes, stream);
+                        grads_f32, accumulate, M, H, p_drop, seed, layer, site, row_offset, nullptr, nullptr, 0,
+                        workspace, workspace_bytes, stream);
 }
 
 // ===========================================================================

@@ -26,7 +26,7 @@ from . import collectives as C
 from . import kernels as K
 from . import ops
 from .ops import SITE_ATTN_OUT, SITE_MLP_OUT
-from .state import get_pool
+from .state import STATE, get_pool
 
 
 @dataclass
@@ -50,6 +50,7 @@ class LayerMeta:
     row_offset: int = 0  # global token row of this rank's first activation row (hidden dropout)
     shard_rows: bool = False  # activations row-sharded between sub-layers (AG in / RS out)
     comm: str = "peer"  # "peer": fused NVLink peer-store collectives; "nccl": torch.distributed
+    push_next: bool = False  # the next sub-layer gathers this output unnormalised: push it from the epilogue
 
 
 class LinearFn(torch.autograd.Function):
@@ -237,12 +238,31 @@ def _peer(m: LayerMeta, R: int) -> bool:
     return m.shard_rows and m.comm == "peer" and R % 128 == 0
 
 
+# (data_ptr, numel) of a sub-layer output -> the pool region its producer already stored it
+# into on every rank (the previous sub-layer's epilogue did the allgather's peer stores)
+_PUSHED: dict = {}
+
+
+def _push_target(m: LayerMeta, R: int, H: int):
+    """Gather region the sub-layer epilogue stores its output into (push_next), or None."""
+    if not (m.push_next and _peer(m, R)):
+        return None, {}
+    pool = get_pool()
+    G = pool.alloc(m.tp_size * R * H * 2)
+    tbl, off = pool.peers(G, pool.me * R * H)
+    return G, dict(out_peers=tbl, peer_off=off)
+
+
 def _gather_in(x2, m: LayerMeta, ln=None):
     """Column-parallel GEMM input: [pre-LN](own rows) gathered over the group.
     Returns (hf, mean, rstd, pool region or None)."""
     R, H = x2.shape
     if _peer(m, R):
         pool = get_pool()
+        G = _PUSHED.pop((x2.data_ptr(), x2.numel()), None) if ln is None else None
+        if G is not None:  # rows already stored into every rank's region by the producer
+            pool.barrier()
+            return pool.view(G, (m.tp_size * R, H)), None, None, G
         G = pool.alloc(m.tp_size * R * H * 2)
         tbl, off = pool.peers(G, pool.me * R * H)
         mean = rstd = None
@@ -261,17 +281,32 @@ def _gather_in(x2, m: LayerMeta, ln=None):
 
 
 def _rs_out(a, w, w_mn: bool, m: LayerMeta, R: int, N: int):
-    """Row-parallel product combined over the group -> (x, nslots, slot_stride, region).
-    x is dense (nslots == 1) or the pool's T partial slots of this rank's rows."""
+    """Row-parallel product combined over the group -> (x, slot kwargs, region).
+
+    Peer mode, "pull" (default): every rank writes its full partial product into its own
+    symmetric-pool region with a local TMA-store epilogue; after one epoch barrier the consumer
+    row kernel reads its rows from all T ranks' regions over NVLink and sums them in ascending
+    rank order (the slot kwargs carry the peer table and offset).  "push": the GEMM epilogue
+    stores each output box straight into the owner's slot (smpk_gemm_rs).  Otherwise NCCL."""
     if _peer(m, R):
         pool = get_pool()
-        P = pool.scratch("partials", m.tp_size * R * N * 2)
+        T = m.tp_size
+        if STATE.config.get("tp_rs", "pull") == "pull":
+            P = pool.scratch("rs_out", T * R * N * 2)
+            out = pool.view(P, (T * R, N))
+            if w_mn:
+                K.matmul_nn(a, w, out=out)
+            else:
+                K.linear(a, w, out=out)
+            pool.barrier()
+            return out, dict(nslots=T, x_peers=pool.base_table, x_peer_off=P // 2 + pool.me * R * N), None
+        P = pool.scratch("partials", T * R * N * 2)
         peers, off = pool.host_peers(P, pool.me * R * N)
         K.gemm_rs(a, w, w_mn, peers, ldc=N, rows_per_owner=R, slot_off=off)
         pool.barrier()
-        return pool.view(P, (m.tp_size * R, N)), m.tp_size, R * N, None
+        return pool.view(P, (T * R, N)), dict(nslots=T, slot_stride=R * N), None
     y = K.matmul_nn(a, w) if w_mn else K.linear(a, w)
-    return _combine_rows(y, m), 1, 0, None
+    return _combine_rows(y, m), {}, None
 
 
 def _gather_grad(dy2, r, mean, rstd, m: LayerMeta, site: int, keep=None):
@@ -292,13 +327,13 @@ def _gather_grad(dy2, r, mean, rstd, m: LayerMeta, site: int, keep=None):
     return dr, _gather_rows(d, m), dgw, dgb, None
 
 
-def _input_grad(dhx, ns, st, dr, x2, pre_w, mu1, rs1, m: LayerMeta, R: int, H: int):
+def _input_grad(dhx, skw, dr, x2, pre_w, mu1, rs1, m: LayerMeta, R: int, H: int):
     """dx = [pre-LN backward](sum of dh slots) + residual gradient dr."""
     if m.pre_ln:
-        dx, _, dgw, dgb, _ = ops.ln_bwd(dhx, x2, mu1, rs1, pre_w, dres=dr, want_dbias=False, nslots=ns,
-                                        slot_stride=st, rows=R, cols=H)
+        dx, _, dgw, dgb, _ = ops.ln_bwd(dhx, x2, mu1, rs1, pre_w, dres=dr, want_dbias=False, rows=R, cols=H,
+                                        **skw)
         return dx, dgw, dgb
-    dx, _, _, _ = ops.bdr_ln(dhx, residual=dr, nslots=ns, slot_stride=st, rows=R, cols=H)
+    dx, _, _, _ = ops.bdr_ln(dhx, residual=dr, rows=R, cols=H, **skw)
     return dx, None, None
 
 
@@ -334,12 +369,13 @@ class AttentionFn(torch.autograd.Function):
             P, Pd = lse, bits  # the backward re-reads the same keep bits
         else:
             ctxv, P, Pd = attn_core_fwd(qkv, B, s, m, mask_add)
-        ox, ns, st, PR = _rs_out(ctxv, wo, False, m, R, H)
+        ox, skw, PR = _rs_out(ctxv, wo, False, m, R, H)
         kb = ops.keep_bytes(R, H, x.device) if m.p_hidden > 0 else None  # reused by the backward
+        Gn, pkw = _push_target(m, R, H)
         r, y, mu2, rs2 = ops.bdr_ln(ox, bias=bo, residual=x2, gamma=post_w if m.post_ln else None,
                                     beta=post_b if m.post_ln else None, eps=m.eps, p=m.p_hidden, seed=m.seed,
-                                    layer=m.layer_id, site=SITE_ATTN_OUT, row_offset=m.row_offset, nslots=ns,
-                                    slot_stride=st, rows=R, cols=H, keep_out=kb)
+                                    layer=m.layer_id, site=SITE_ATTN_OUT, row_offset=m.row_offset, rows=R, cols=H,
+                                    keep_out=kb, **skw, **pkw)
         ctx.kb = kb
         _free(PR)
         if not any(ctx.needs_input_grad):
@@ -349,6 +385,8 @@ class AttentionFn(torch.autograd.Function):
         ctx.save_for_backward(x2, hf, mu1, rs1, qkv, P, Pd if Pd is not P else None, ctxv, r, mu2, rs2, wqkv, wo,
                               pre_w, post_w, mask_add)
         out = y if m.post_ln else r
+        if Gn is not None:
+            _PUSHED[(out.data_ptr(), out.numel())] = Gn
         return out.view(b, s, H)
 
     @staticmethod
@@ -378,8 +416,8 @@ class AttentionFn(torch.autograd.Function):
             dx = K.matmul_nn(dqkv, wqkv, epi=K.EPI_ADD, aux=dr)
             dpre_w = dpre_b = None
         else:
-            dhx, ns, st, PR = _rs_out(dqkv, wqkv, True, m, R, H)
-            dx, dpre_w, dpre_b = _input_grad(dhx, ns, st, dr, x2, pre_w, mu1, rs1, m, R, H)
+            dhx, skw, PR = _rs_out(dqkv, wqkv, True, m, R, H)
+            dx, dpre_w, dpre_b = _input_grad(dhx, skw, dr, x2, pre_w, mu1, rs1, m, R, H)
             _free(PR)
         _free(G2, ctx.G)
         dpost_w, dpost_b, dpre_w, dpre_b = _sync_replicated([dpost_w, dpost_b, dpre_w, dpre_b], m)
@@ -398,12 +436,13 @@ class MlpFn(torch.autograd.Function):
         x2 = x.reshape(R, H)
         hf, mu1, rs1, G = _gather_in(x2, m, (pre_w, pre_b) if m.pre_ln else None)
         f, z = K.linear(hf, w1, b1, act=m.activation)
-        gx, ns, st, PR = _rs_out(f, w2, False, m, R, H)
+        gx, skw, PR = _rs_out(f, w2, False, m, R, H)
         kb = ops.keep_bytes(R, H, x.device) if m.p_hidden > 0 else None  # reused by the backward
+        Gn, pkw = _push_target(m, R, H)
         r, y, mu2, rs2 = ops.bdr_ln(gx, bias=b2, residual=x2, gamma=post_w if m.post_ln else None,
                                     beta=post_b if m.post_ln else None, eps=m.eps, p=m.p_hidden, seed=m.seed,
-                                    layer=m.layer_id, site=SITE_MLP_OUT, row_offset=m.row_offset, nslots=ns,
-                                    slot_stride=st, rows=R, cols=H, keep_out=kb)
+                                    layer=m.layer_id, site=SITE_MLP_OUT, row_offset=m.row_offset, rows=R, cols=H,
+                                    keep_out=kb, **skw, **pkw)
         ctx.kb = kb
         _free(PR)
         if not any(ctx.needs_input_grad):
@@ -412,6 +451,8 @@ class MlpFn(torch.autograd.Function):
         ctx.m, ctx.shape, ctx.G = m, (b, s, H), G
         ctx.save_for_backward(x2, hf, mu1, rs1, f, z, r, mu2, rs2, w1, w2, pre_w, post_w)
         out = y if m.post_ln else r
+        if Gn is not None:
+            _PUSHED[(out.data_ptr(), out.numel())] = Gn
         return out.view(b, s, H)
 
     @staticmethod
@@ -434,8 +475,8 @@ class MlpFn(torch.autograd.Function):
             dx = K.matmul_nn(dz, w1, epi=K.EPI_ADD, aux=dr)
             dpre_w = dpre_b = None
         else:
-            dhx, ns, st, PR = _rs_out(dz, w1, True, m, R, H)
-            dx, dpre_w, dpre_b = _input_grad(dhx, ns, st, dr, x2, pre_w, mu1, rs1, m, R, H)
+            dhx, skw, PR = _rs_out(dz, w1, True, m, R, H)
+            dx, dpre_w, dpre_b = _input_grad(dhx, skw, dr, x2, pre_w, mu1, rs1, m, R, H)
             _free(PR)
         _free(G2, ctx.G)
         dpost_w, dpost_b, dpre_w, dpre_b = _sync_replicated([dpost_w, dpost_b, dpre_w, dpre_b], m)

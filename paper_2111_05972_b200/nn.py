@@ -219,8 +219,9 @@ class DistributedAttentionLayer(_LayerBase):
         self.dense_weight = _param((H, H // T), std, g)
         self._ln_params("")
 
-    def sublayer(self, X, mask, rc):
+    def sublayer(self, X, mask, rc, push_next=False):
         m = self._meta(rc)
+        m.push_next = push_next
         if self._memory:
             return MM.attention(X, self, mask, m, STATE.tp_rank)
         return L.AttentionFn.apply(X, self.qkv_weight, self.qkv_bias, self.dense_weight, self.dense_bias,
@@ -277,8 +278,9 @@ class DistributedTransformerOutputLayer(_LayerBase):
         self.fc2_weight = _param((H, I // T), std, g)
         self._ln_params("")
 
-    def sublayer(self, X, mask, rc):
+    def sublayer(self, X, mask, rc, push_next=False):
         m = self._meta(rc)
+        m.push_next = push_next
         if self._memory:
             return MM.mlp(X, self, m, STATE.tp_rank)
         return L.MlpFn.apply(X, self.fc1_weight, self.fc1_bias, self.fc2_weight, self.fc2_bias, self.pre_ln_weight,
@@ -379,8 +381,11 @@ class DistributedTransformerLayer(DistributedModule):
             use_normal_initialization, pre_layernorm, post_layernorm, layer_id=lid,
             num_attention_heads=num_attention_heads, _standalone=False)
 
-    def sublayer(self, X, mask, rc):
-        return self.output.sublayer(self.attention.sublayer(X, mask, rc), mask, rc)
+    def sublayer(self, X, mask, rc, push_last=False):
+        """push_last: a following sub-layer gathers this layer's output (stack-internal)."""
+        nopre = not self.output.pre_layernorm
+        Y = self.attention.sublayer(X, mask, rc, push_next=nopre)
+        return self.output.sublayer(Y, mask, rc, push_next=push_last and not self.attention.pre_layernorm)
 
     def forward(self, hidden_states, attention_mask=None):
         return _run_standalone(self, hidden_states, attention_mask)
@@ -408,8 +413,9 @@ class DistributedTransformer(DistributedModule):
             for _ in range(num_layers)])
 
     def sublayer(self, X, mask, rc):
-        for layer in self.seq_layers:
-            X = layer.sublayer(X, mask, rc)
+        n = len(self.seq_layers)
+        for i, layer in enumerate(self.seq_layers):
+            X = layer.sublayer(X, mask, rc, push_last=i + 1 < n)
         return X
 
     def forward(self, hidden_states, attention_mask=None):

@@ -19,7 +19,7 @@ def _f32(t):
 
 def bdr_ln(x: torch.Tensor, *, bias=None, residual=None, gamma=None, beta=None, eps=1e-5, p=0.0, seed=0,
            layer=0, site=SITE_ATTN_OUT, row_offset=0, want_r=True, want_y=True, nslots=1, slot_stride=0,
-           out_peers=None, peer_off=0, rows=None, cols=None, keep_out=None):
+           out_peers=None, peer_off=0, rows=None, cols=None, keep_out=None, x_peers=None, x_peer_off=0):
     """r = residual + dropout(x + bias); y = LN(r). Returns (r, y, mean, rstd) (None where not computed).
 
     nslots > 1: x is the ascending-rank sum of nslots partial slots slot_stride elements apart
@@ -38,7 +38,7 @@ def bdr_ln(x: torch.Tensor, *, bias=None, residual=None, gamma=None, beta=None, 
     _lib.call("smpk_bdr_ln_fwd_ex", _ptr(x), int(nslots), int(slot_stride), _ptr(bias), _ptr(residual), _ptr(r),
               _ptr(gamma), _ptr(beta), _ptr(y), _ptr(mean), _ptr(rstd), _ptr(out_peers), npeers, int(peer_off), M, H,
               float(eps), float(p), int(seed) & (2 ** 64 - 1), int(layer), int(site), int(row_offset),
-              _ptr(keep_out if p > 0 else None), _stream())
+              _ptr(keep_out if p > 0 else None), _ptr(x_peers), int(x_peer_off), _stream())
     return r, y, mean, rstd
 
 
@@ -60,7 +60,7 @@ def add(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
 
 def ln_bwd(dy, r, mean, rstd, gamma, *, dres=None, p=0.0, seed=0, layer=0, site=SITE_ATTN_OUT, row_offset=0,
            want_dgamma=True, want_dbias=True, grads_f32=False, want_dr=True, nslots=1, slot_stride=0,
-           out_peers=None, peer_off=0, rows=None, cols=None, keep_in=None):
+           out_peers=None, peer_off=0, rows=None, cols=None, keep_in=None, x_peers=None, x_peer_off=0):
     """Backward of bdr_ln. Returns (dr, dsub, dgamma, dbeta, dbias); dsub is dr when p == 0.
 
     gamma None = no-LayerNorm mode (d = dy + dres).  nslots / out_peers as in bdr_ln (dy read as a
@@ -80,7 +80,8 @@ def ln_bwd(dy, r, mean, rstd, gamma, *, dres=None, p=0.0, seed=0, layer=0, site=
     _lib.call("smpk_ln_bwd_ex", _ptr(dy), int(nslots), int(slot_stride), _ptr(r), _ptr(mean), _ptr(rstd),
               _ptr(gamma), _ptr(dres), _ptr(dr), _ptr(dsub), _ptr(out_peers), npeers, int(peer_off), _ptr(dgamma),
               _ptr(dbeta), _ptr(dbias), int(grads_f32), 0, M, H, float(p), int(seed) & (2 ** 64 - 1), int(layer),
-              int(site), int(row_offset), _ptr(keep_in if p > 0 else None), _ptr(ws), int(ws_bytes), _stream(),
+              int(site), int(row_offset), _ptr(keep_in if p > 0 else None), _ptr(x_peers), int(x_peer_off), _ptr(ws),
+              int(ws_bytes), _stream(),
               launches=2 if (dgamma is not None or dbeta is not None or dbias is not None) else 1)
     if dsub is None:
         dsub = dr if dr is not None else (dy if nslots == 1 else None)

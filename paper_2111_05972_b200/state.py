@@ -31,7 +31,8 @@ DEFAULTS = {
     "activation_loading_horizon": 4,
     "seed": 0,
     "ddp": True,
-    "tp_comm": "peer",  # fused NVLink peer-store collectives ("nccl": torch.distributed calls)
+    "tp_comm": "peer",  # fused NVLink peer-memory collectives ("nccl": torch.distributed calls)
+    "tp_rs": "pull",  # peer reduce-scatter: consumer pulls the partials ("push": GEMM epilogue stores)
     "symm_pool_bytes": 4 << 30,
 }
 
