@@ -11,6 +11,8 @@
 // reduction runs in a fixed order, so results are bit-stable run to run.
 // Dropout masks come from Philox4x32-10 keyed by logical coordinates
 // (oracle/philox.py reproduces them bit-exactly).
+#include <cstdlib>
+
 #include "smpk_common.cuh"
 
 namespace smpk {
@@ -186,23 +188,14 @@ __device__ __forceinline__ void load8_slots(const bf16* p, int nslots, int64_t s
 // reduce-scatter consumer over peer memory (pull): the ascending-rank sum of the T ranks'
 // partial rows, rank j's at peers[j] + off (its own GEMM output in its symmetric pool)
 __device__ __forceinline__ void load8_peer_slots(const bf16* const* peers, int n, int64_t off, float (&v)[8]) {
-  // all (<= 8) remote loads in flight before the first add: NVLink latency is ~us
-  uint4 raw[8];
+  // sequential (few registers: these kernels keep per-column accumulators in registers; the
+  // bandwidth-critical pull path is the pipelined bulk-copy kernel)
+  load8(peers[0] + off, v);
+  for (int j = 1; j < n; ++j) {
+    float t[8];
+    load8(peers[j] + off, t);
 #pragma unroll
-  for (int j = 0; j < 8; ++j)
-    if (j < n) raw[j] = *reinterpret_cast<const uint4*>(peers[j] + off);
-#pragma unroll
-  for (int e = 0; e < 8; ++e) v[e] = 0.f;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    if (j >= n) break;
-    const uint32_t w[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float2 f = unpack_bf16x2(w[q]);
-      v[2 * q] += f.x;
-      v[2 * q + 1] += f.y;
-    }
+    for (int e = 0; e < 8; ++e) v[e] += t[e];
   }
 }
 
@@ -758,9 +751,239 @@ static int softmax_nv(int sk) {
   return -1;
 }
 
+
+// ===========================================================================
+// Pipelined bias + dropout + residual + LayerNorm (the fast path of smpk_bdr_ln_fwd)
+// ===========================================================================
+// Persistent CTAs (one per SM).  Warp 0 streams whole input rows into a deep shared-memory
+// ring with cp.async.bulk (every partial slot -- local or a peer's over NVLink -- plus the
+// residual), so each SM keeps ~100+ KB of row data in flight; 8 consumer warps each own a row
+// (lane = 4 x 8-column chunks at H=1024), reduce with warp shuffles only, store r / y locally
+// and push y to the peers' gather buffers with bulk shared->global copies.
+constexpr int PIPE_CW = 8;  // consumer warps
+
+struct BdrPipeArgs {
+  const bf16* x;
+  int64_t slot_stride;
+  const bf16* const* x_peers;
+  int64_t x_peer_off;
+  int nslots;
+  const bf16* bias;
+  const bf16* residual;
+  bf16* r_out;
+  const bf16* gamma;
+  const bf16* beta;
+  bf16* y_out;
+  float* mean;
+  float* rstd;
+  int M, H;
+  float eps, p;
+  uint64_t seed;
+  uint32_t layer, site;
+  int64_t row_offset;
+  uint8_t* keep_out;
+  bf16* const* out_peers;  // host-built table copied to the kernel params (<= 8)
+  int npeers;
+  int64_t peer_off;
+  int nst;  // ring stages
+};
+
+__device__ __forceinline__ void bulk_store_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(reinterpret_cast<uint64_t>(gdst)),
+               "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
+
+template <int CH>
+__global__ void __launch_bounds__(32 * (PIPE_CW + 1), 1) bdr_ln_pipe_kernel(const BdrPipeArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  const int H = a.H;
+  const int nin = a.nslots + (a.residual ? 1 : 0);
+  const int stage_bytes = nin * H * 2;
+  // per-column parameters (bias | gamma | beta) staged once per CTA
+  bf16* par = reinterpret_cast<bf16*>(smem + a.nst * stage_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.nst * stage_bytes + 3 * H * 2);
+  uint64_t* empty = full + a.nst;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < a.nst; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    fence_barrier_init();
+  }
+  for (int i = threadIdx.x * 8; i < H; i += blockDim.x * 8) {
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    *reinterpret_cast<uint4*>(par + i) = a.bias ? *reinterpret_cast<const uint4*>(a.bias + i) : z;
+    *reinterpret_cast<uint4*>(par + H + i) = a.gamma ? *reinterpret_cast<const uint4*>(a.gamma + i) : z;
+    *reinterpret_cast<uint4*>(par + 2 * H + i) = a.gamma ? *reinterpret_cast<const uint4*>(a.beta + i) : z;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int row = blockIdx.x; row < a.M; row += gridDim.x, ++it) {
+        const int st = it % a.nst;
+        mbar_wait(&empty[st], ((it / a.nst) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[st], stage_bytes);
+        uint8_t* dst = smem + st * stage_bytes;
+        for (int j = 0; j < a.nslots; ++j) {
+          const bf16* src = a.x_peers ? a.x_peers[j] + a.x_peer_off + (int64_t)row * H
+                                      : a.x + j * a.slot_stride + (int64_t)row * H;
+          bulk_load(dst + j * H * 2, src, H * 2, &full[st]);
+        }
+        if (a.residual) bulk_load(dst + a.nslots * H * 2, a.residual + (int64_t)row * H, H * 2, &full[st]);
+      }
+    }
+    return;
+  }
+  // ---------------- consumers: warp c handles iterations it == c (mod PIPE_CW) ----------------
+  const int c = warp - 1;
+  const float inv_keep = a.p > 0.f ? 1.f / (1.f - a.p) : 1.f;
+  const uint32_t thresh = dropout_threshold(a.p);
+  int it = c;
+  for (int row = blockIdx.x + c * gridDim.x; row < a.M; row += PIPE_CW * gridDim.x, it += PIPE_CW) {
+    const int st = it % a.nst;
+    mbar_wait(&full[st], (it / a.nst) & 1);
+    const uint8_t* buf = smem + st * stage_bytes;
+    float v[CH][8];
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const int col = (k * 32 + lane) * 8;
+      load8(reinterpret_cast<const bf16*>(buf) + col, v[k]);
+      for (int j = 1; j < a.nslots; ++j) {  // ascending rank order
+        float t[8];
+        load8(reinterpret_cast<const bf16*>(buf + j * H * 2) + col, t);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[k][e] += t[e];
+      }
+      if (a.bias) {
+        float bv[8];
+        load8(par + col, bv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[k][e] += bv[e];
+      }
+      if (a.p > 0.f) {
+        bool keep[8];
+        dropout_keep8(a.seed, a.layer, a.site, (uint64_t)(a.row_offset + row), col, thresh, keep);
+        if (a.keep_out) a.keep_out[(int64_t)row * (H / 8) + col / 8] = (uint8_t)keep8_to_byte(keep);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[k][e] = keep[e] ? v[k][e] * inv_keep : 0.f;
+      }
+      if (a.residual) {
+        float rr[8];
+        load8(reinterpret_cast<const bf16*>(buf + a.nslots * H * 2) + col, rr);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[k][e] += rr[e];
+      }
+      round8(v[k]);
+    }
+    __syncwarp();
+    const bool push = a.npeers > 0;
+    if (!push) {
+      if (lane == 0) mbar_arrive(&empty[st]);  // inputs consumed: the producer may refill
+    }
+    if (a.r_out) {
+#pragma unroll
+      for (int k = 0; k < CH; ++k) store8(a.r_out + (int64_t)row * H + (k * 32 + lane) * 8, v[k]);
+    }
+    float o[CH][8];
+    if (a.gamma) {
+      float s = 0.f;
+#pragma unroll
+      for (int k = 0; k < CH; ++k)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s += v[k][e];
+      const float mu = warp_sum(s) / H;
+      float q = 0.f;
+#pragma unroll
+      for (int k = 0; k < CH; ++k)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float d = v[k][e] - mu;
+          q += d * d;
+        }
+      const float rs = rsqrtf(warp_sum(q) / H + a.eps);
+      if (lane == 0) {
+        a.mean[row] = mu;
+        a.rstd[row] = rs;
+      }
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+        float gv[8], bv[8];
+        load8(par + H + (k * 32 + lane) * 8, gv);
+        load8(par + 2 * H + (k * 32 + lane) * 8, bv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[k][e] = (v[k][e] - mu) * rs * gv[e] + bv[e];
+      }
+      if (a.y_out) {
+#pragma unroll
+        for (int k = 0; k < CH; ++k) store8(a.y_out + (int64_t)row * H + (k * 32 + lane) * 8, o[k]);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < CH; ++k)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[k][e] = v[k][e];
+    }
+    if (push) {
+      // the stage's first slot row becomes the bf16 output row, pushed to every peer in bulk
+      bf16* obuf = reinterpret_cast<bf16*>(smem + st * stage_bytes);
+#pragma unroll
+      for (int k = 0; k < CH; ++k) store8(obuf + (k * 32 + lane) * 8, o[k]);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        for (int j = 0; j < a.npeers; ++j)
+          bulk_store_s2g(a.out_peers[j] + a.peer_off + (int64_t)row * H, obuf, H * 2);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        mbar_arrive(&empty[st]);
+      }
+      __syncwarp();
+    }
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+static int bdr_ln_pipe_launch(const BdrPipeArgs& a, cudaStream_t st) {
+  const int nin = a.nslots + (a.residual ? 1 : 0);
+  const int stage_bytes = nin * a.H * 2;
+  const int smem = a.nst * stage_bytes + 3 * a.H * 2 + 2 * a.nst * 8 + 128;
+  const int grid = a.M < num_sms() ? a.M : num_sms();
+  switch (a.H / 256) {
+#define SMPK_PIPE_CASE(CH_)                                                                              \
+  case CH_: {                                                                                            \
+    static bool once = false;                                                                            \
+    if (!once) {                                                                                         \
+      cudaFuncSetAttribute(bdr_ln_pipe_kernel<CH_>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448); \
+      once = true;                                                                                       \
+    }                                                                                                    \
+    bdr_ln_pipe_kernel<CH_><<<grid, 32 * (PIPE_CW + 1), smem, st>>>(a);                                  \
+    break;                                                                                               \
+  }
+    SMPK_PIPE_CASE(1) SMPK_PIPE_CASE(2) SMPK_PIPE_CASE(4) SMPK_PIPE_CASE(8)
+#undef SMPK_PIPE_CASE
+    default:
+      return SMPK_ERR_UNSUPPORTED;
+  }
+  return check_launch("smpk_bdr_ln_fwd(pipe)");
+}
+
 }  // namespace smpk
 
 using namespace smpk;
+
+// SMPK_ROW_PIPE=0 selects the register-only row kernel (A/B measurements)
+static bool pipe_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SMPK_ROW_PIPE");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
 
 static int bdr_ln_impl(const void* x, int nslots, int64_t slot_stride, const void* bias, const void* residual,
                        void* r_out, const void* gamma, const void* beta, void* y_out, float* mean, float* rstd,
@@ -788,8 +1011,30 @@ static int bdr_ln_impl(const void* x, int nslots, int64_t slot_stride, const voi
               row_offset, nslots, slot_stride, reinterpret_cast<bf16* const*>(out_peers), npeers, peer_off,
               col_offset, row_sums_out, ext_sums, H_total, keep_out, reinterpret_cast<const bf16* const*>(x_peers),
               x_peer_off};
-  const int grid = row_grid(M, geo.W);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // pipelined path for the TP exchanges (partials pulled from peers and/or output pushed to peers:
+  // bulk copies keep enough NVLink traffic in flight); whole 16-B aligned rows, <= 2048 columns.
+  // Purely local rows stay on the register kernel below (measured faster for them).
+  const int ch = H / 256;
+  const bool al = (reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(residual) |
+                   reinterpret_cast<uintptr_t>(r_out) | reinterpret_cast<uintptr_t>(y_out)) % 16 == 0 &&
+                  (slot_stride * 2) % 16 == 0 && (x_peer_off * 2) % 16 == 0 && (peer_off * 2) % 16 == 0;
+  if (pipe_enabled() && (x_peers || npeers) && H % 256 == 0 && (ch == 1 || ch == 2 || ch == 4 || ch == 8) && al &&
+      !row_sums_out &&
+      !ext_sums && col_offset == 0 && nslots <= 8 && npeers <= 8) {
+    BdrPipeArgs pa{reinterpret_cast<const bf16*>(x), slot_stride, reinterpret_cast<const bf16* const*>(x_peers),
+                   x_peer_off, nslots, reinterpret_cast<const bf16*>(bias), reinterpret_cast<const bf16*>(residual),
+                   reinterpret_cast<bf16*>(r_out), reinterpret_cast<const bf16*>(gamma),
+                   reinterpret_cast<const bf16*>(beta), reinterpret_cast<bf16*>(y_out), mean, rstd, M, H, eps,
+                   p_drop, seed, (uint32_t)layer, (uint32_t)site, row_offset, keep_out,
+                   reinterpret_cast<bf16* const*>(out_peers), npeers, peer_off, 0};
+    const int nin = nslots + (residual ? 1 : 0);
+    const int budget = 200 * 1024 - 3 * H * 2;
+    const int nst = budget / (nin * H * 2);
+    pa.nst = nst > 16 ? 16 : nst;
+    if (pa.nst >= 2) return bdr_ln_pipe_launch(pa, st);
+  }
+  const int grid = row_grid(M, geo.W);
   SMPK_DISPATCH_ROW(geo.W, geo.VPT, bdr_ln_fwd_kernel, (grid, ROW_THREADS, 0, st), (a));
   return check_launch("smpk_bdr_ln_fwd");
 }
