@@ -206,8 +206,15 @@ def _combine_rows(partial, m: LayerMeta):
     return C.all_reduce(partial)
 
 
-def _sync_replicated(grads, m: LayerMeta):
-    """Allreduce the partial gradients of TP-replicated parameters in one bucket (row-sharded mode)."""
+def _sync_replicated(grads, m: LayerMeta, keep=None):
+    """Allreduce the partial gradients of TP-replicated parameters in one bucket (row-sharded mode).
+    keep: (post-LN weight, bias) gradients already summed over the peer pool (slots 0, 1)."""
+    if keep is not None:
+        grads = list(grads)
+        grads[0], grads[1] = keep
+        synced = grads[:2]
+        rest = _sync_replicated([None, None] + grads[2:], m)
+        return synced + rest[2:]
     if not m.shard_rows:
         return grads
     live = [g for g in grads if g is not None]
@@ -318,11 +325,24 @@ def _gather_grad(dy2, r, mean, rstd, m: LayerMeta, site: int, keep=None):
               want_dr=m.post_ln, want_dbias=False, keep_in=keep)
     if _peer(m, R):
         pool = get_pool()
-        G = pool.scratch("grad_gather", m.tp_size * R * H * 2)
+        T = m.tp_size
+        G = pool.scratch("grad_gather", T * R * H * 2)
         tbl, off = pool.peers(G, pool.me * R * H)
-        dr, _, dgw, dgb, _ = ops.ln_bwd(dy2, r, mean, rstd, m._post_w, out_peers=tbl, peer_off=off, **kw)
+        pg = torch.empty(2, H, dtype=torch.bfloat16, device=dy2.device) if m._post_w is not None else None
+        dr, _, dgw, dgb, _ = ops.ln_bwd(dy2, r, mean, rstd, m._post_w, out_peers=tbl, peer_off=off,
+                                        param_grads_out=pg, **kw)
+        if pg is not None:
+            # the LN parameter gradients ride the same barrier: push this rank's [2, H] partial into
+            # every peer's slot, then sum the T slots in ascending rank order
+            L = pool.scratch("ln_grads", T * 2 * H * 2)
+            ltbl, loff = pool.peers(L, pool.me * 2 * H)
+            ops.bdr_ln(pg, want_r=False, out_peers=ltbl, peer_off=loff)
         pool.barrier()
-        return dr, pool.view(G, (m.tp_size * R, H)), dgw, dgb, None
+        if pg is not None:
+            tot, _, _, _ = ops.bdr_ln(pool.view(L, (T * 2, H)), nslots=T, slot_stride=2 * H, rows=2, cols=H)
+            dgw, dgb = tot[0], tot[1]
+            m._post_synced = True
+        return dr, pool.view(G, (T * R, H)), dgw, dgb, None
     dr, d, dgw, dgb, _ = ops.ln_bwd(dy2, r, mean, rstd, m._post_w, **kw)
     return dr, _gather_rows(d, m), dgw, dgb, None
 
@@ -420,7 +440,9 @@ class AttentionFn(torch.autograd.Function):
             dx, dpre_w, dpre_b = _input_grad(dhx, skw, dr, x2, pre_w, mu1, rs1, m, R, H)
             _free(PR)
         _free(G2, ctx.G)
-        dpost_w, dpost_b, dpre_w, dpre_b = _sync_replicated([dpost_w, dpost_b, dpre_w, dpre_b], m)
+        dpost_w, dpost_b, dpre_w, dpre_b = _sync_replicated(
+            [None, None, dpre_w, dpre_b] if getattr(m, "_post_synced", False) else [dpost_w, dpost_b, dpre_w, dpre_b],
+            m, keep=(dpost_w, dpost_b) if getattr(m, "_post_synced", False) else None)
         return (dx.view(b, s, H), dwqkv, dbqkv, dwo, dbo, dpre_w, dpre_b, dpost_w, dpost_b, None, None)
 
 
@@ -479,5 +501,7 @@ class MlpFn(torch.autograd.Function):
             dx, dpre_w, dpre_b = _input_grad(dhx, skw, dr, x2, pre_w, mu1, rs1, m, R, H)
             _free(PR)
         _free(G2, ctx.G)
-        dpost_w, dpost_b, dpre_w, dpre_b = _sync_replicated([dpost_w, dpost_b, dpre_w, dpre_b], m)
+        dpost_w, dpost_b, dpre_w, dpre_b = _sync_replicated(
+            [None, None, dpre_w, dpre_b] if getattr(m, "_post_synced", False) else [dpost_w, dpost_b, dpre_w, dpre_b],
+            m, keep=(dpost_w, dpost_b) if getattr(m, "_post_synced", False) else None)
         return (dx.view(b, s, H), dw1, db1, dw2, db2, dpre_w, dpre_b, dpost_w, dpost_b, None)

@@ -77,9 +77,14 @@ def run_case(smp, name, *, prescaled, causal, pre, post, p, layers=1, act="gelu"
     shard_grads = []
     for lay in lays:
         a, o = lay.attention, lay.output
-        shard_grads.append({k: gather_cpu(t.grad) for k, t in {
-            "qkv_w": a.qkv_weight, "qkv_b": a.qkv_bias, "wo": a.dense_weight, "bo": a.dense_bias,
-            "w1": o.fc1_weight, "b1": o.fc1_bias, "w2": o.fc2_weight, "b2": o.fc2_bias}.items()})
+        tens = {"qkv_w": a.qkv_weight, "qkv_b": a.qkv_bias, "wo": a.dense_weight, "bo": a.dense_bias,
+                "w1": o.fc1_weight, "b1": o.fc1_bias, "w2": o.fc2_weight, "b2": o.fc2_bias}
+        for blk, mod_ in (("attn", a), ("mlp", o)):  # LayerNorm parameters (replicated / memory: chunks)
+            for where in ("pre", "post"):
+                if getattr(mod_, f"{where}_ln_weight") is not None:
+                    tens[f"{blk}_{where}_ln_w"] = getattr(mod_, f"{where}_ln_weight")
+                    tens[f"{blk}_{where}_ln_b"] = getattr(mod_, f"{where}_ln_bias")
+        shard_grads.append({k: gather_cpu(t.grad) for k, t in tens.items()})
     ok = True
     if rank == 0:
         xr = X.double().requires_grad_(True)
@@ -117,6 +122,10 @@ def run_case(smp, name, *, prescaled, causal, pre, post, p, layers=1, act="gelu"
                     "w2": rel(sg["w2"][j], gr["w2"].grad[:, isl]),
                     "b2": rel(sg["b2"][j], gr["b2"].grad[sl] if mem else gr["b2"].grad),
                 }
+                for k in sg:
+                    if k.endswith(("_ln_w", "_ln_b")):
+                        full = gr[k].grad
+                        e[k] = rel(sg[k][j], full[sl] if mem else full)
                 for k, v in e.items():
                     errs[f"L{l}.r{j}.{k}"] = v
         # ReLU-gated gradients (FC1): relu' flips where the bf16-rounded pre-activation crosses 0,
