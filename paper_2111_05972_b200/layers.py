@@ -319,32 +319,35 @@ def _rs_out(a, w, w_mn: bool, m: LayerMeta, R: int, N: int):
 def _gather_grad(dy2, r, mean, rstd, m: LayerMeta, site: int, keep=None):
     """Backward of the sub-layer epilogue on own rows; the branch gradient is gathered for the
     column/row-parallel GEMMs.  keep: the forward's hidden-dropout keep bytes.
-    Returns (dr, dbranch_full, dgamma, dbeta, region)."""
+    Returns (dr, dbranch_full, dgamma, dbeta, dbias, region); dbias (the sub-layer output bias
+    gradient, column sums of the branch gradient over all rows of the group) is None when the
+    caller has to reduce it itself."""
     R, H = dy2.shape
+    has_ln = m._post_w is not None
     kw = dict(p=m.p_hidden, seed=m.seed, layer=m.layer_id, site=site, row_offset=m.row_offset,
-              want_dr=m.post_ln, want_dbias=False, keep_in=keep)
+              want_dr=m.post_ln, keep_in=keep)
     if _peer(m, R):
         pool = get_pool()
         T = m.tp_size
         G = pool.scratch("grad_gather", T * R * H * 2)
         tbl, off = pool.peers(G, pool.me * R * H)
-        pg = torch.empty(2, H, dtype=torch.bfloat16, device=dy2.device) if m._post_w is not None else None
-        dr, _, dgw, dgb, _ = ops.ln_bwd(dy2, r, mean, rstd, m._post_w, out_peers=tbl, peer_off=off,
-                                        param_grads_out=pg, **kw)
-        if pg is not None:
-            # the LN parameter gradients ride the same barrier: push this rank's [2, H] partial into
-            # every peer's slot, then sum the T slots in ascending rank order
-            L = pool.scratch("ln_grads", T * 2 * H * 2)
-            ltbl, loff = pool.peers(L, pool.me * 2 * H)
-            ops.bdr_ln(pg, want_r=False, out_peers=ltbl, peer_off=loff)
+        nv = 3 if has_ln else 1  # [dgamma, dbeta,] dbias: this rank's partial sums over its own rows
+        pg = torch.empty(nv, H, dtype=torch.bfloat16, device=dy2.device)
+        dr, _, dgw, dgb, dbias = ops.ln_bwd(dy2, r, mean, rstd, m._post_w, out_peers=tbl, peer_off=off,
+                                            param_grads_out=pg, want_dbias=True, **kw)
+        # the replicated-parameter gradients ride the same barrier: push this rank's [nv, H] partial
+        # into every peer's slot, then sum the T slots in ascending rank order
+        L = pool.scratch(f"vec_grads{nv}", T * nv * H * 2)
+        ltbl, loff = pool.peers(L, pool.me * nv * H)
+        ops.bdr_ln(pg, want_r=False, out_peers=ltbl, peer_off=loff)
         pool.barrier()
-        if pg is not None:
-            tot, _, _, _ = ops.bdr_ln(pool.view(L, (T * 2, H)), nslots=T, slot_stride=2 * H, rows=2, cols=H)
+        tot, _, _, _ = ops.bdr_ln(pool.view(L, (T * nv, H)), nslots=T, slot_stride=nv * H, rows=nv, cols=H)
+        if has_ln:
             dgw, dgb = tot[0], tot[1]
             m._post_synced = True
-        return dr, pool.view(G, (T * R, H)), dgw, dgb, None
-    dr, d, dgw, dgb, _ = ops.ln_bwd(dy2, r, mean, rstd, m._post_w, **kw)
-    return dr, _gather_rows(d, m), dgw, dgb, None
+        return dr, pool.view(G, (T * R, H)), dgw, dgb, tot[nv - 1], None
+    dr, d, dgw, dgb, dbias = ops.ln_bwd(dy2, r, mean, rstd, m._post_w, want_dbias=not m.shard_rows, **kw)
+    return dr, _gather_rows(d, m), dgw, dgb, dbias, None
 
 
 def _input_grad(dhx, skw, dr, x2, pre_w, mu1, rs1, m: LayerMeta, R: int, H: int):
@@ -419,10 +422,11 @@ class AttentionFn(torch.autograd.Function):
             Pd = P
         dy2 = dy.reshape(R, H).contiguous()
         m._post_w = post_w if m.post_ln else None
-        dr, dof, dpost_w, dpost_b, G2 = _gather_grad(dy2, r, mu2, rs2, m, SITE_ATTN_OUT, ctx.kb)
+        dr, dof, dpost_w, dpost_b, dbo, G2 = _gather_grad(dy2, r, mu2, rs2, m, SITE_ATTN_OUT, ctx.kb)
         if not m.post_ln:
             dr = dy2
-        dbo = ops.colsum(dof)  # over all rows of the group: complete on every rank
+        if dbo is None:
+            dbo = ops.colsum(dof)  # over all rows of the group: complete on every rank
         dwo = K.matmul_tn(dof, ctxv)
         dctx = K.matmul_nn(dof, wo)
         if ctx.fused:
@@ -485,10 +489,11 @@ class MlpFn(torch.autograd.Function):
         x2, hf, mu1, rs1, f, z, r, mu2, rs2, w1, w2, pre_w, post_w = ctx.saved_tensors
         dy2 = dy.reshape(R, H).contiguous()
         m._post_w = post_w if m.post_ln else None
-        dr, dgf, dpost_w, dpost_b, G2 = _gather_grad(dy2, r, mu2, rs2, m, SITE_MLP_OUT, ctx.kb)
+        dr, dgf, dpost_w, dpost_b, db2, G2 = _gather_grad(dy2, r, mu2, rs2, m, SITE_MLP_OUT, ctx.kb)
         if not m.post_ln:
             dr = dy2
-        db2 = ops.colsum(dgf)
+        if db2 is None:
+            db2 = ops.colsum(dgf)
         dw2 = K.matmul_tn(dgf, f)
         dz = K.matmul_nn(dgf, w2, epi=K.EPI_DACT, act=m.activation, aux=z)
         db1 = ops.colsum(dz)

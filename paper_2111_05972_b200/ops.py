@@ -63,7 +63,7 @@ def ln_bwd(dy, r, mean, rstd, gamma, *, dres=None, p=0.0, seed=0, layer=0, site=
            out_peers=None, peer_off=0, rows=None, cols=None, keep_in=None, x_peers=None, x_peer_off=0,
            param_grads_out=None):
     """Backward of bdr_ln. Returns (dr, dsub, dgamma, dbeta, dbias); dsub is dr when p == 0.
-    param_grads_out: a [2, H] buffer receiving (dgamma, dbeta) as one contiguous block.
+    param_grads_out: one contiguous [n, H] buffer receiving the rows (dgamma, dbeta) [+ dbias].
 
     gamma None = no-LayerNorm mode (d = dy + dres).  nslots / out_peers as in bdr_ln (dy read as a
     slot sum; dsub also stored to every peer)."""
@@ -75,9 +75,13 @@ def ln_bwd(dy, r, mean, rstd, gamma, *, dres=None, p=0.0, seed=0, layer=0, site=
     gdt = torch.float32 if grads_f32 else torch.bfloat16
     dgamma = torch.empty(H, dtype=gdt, device=dev) if (want_dgamma and gamma is not None) else None
     dbeta = torch.empty(H, dtype=gdt, device=dev) if (want_dgamma and gamma is not None) else None
-    if param_grads_out is not None and dgamma is not None:
-        dgamma, dbeta = param_grads_out[0], param_grads_out[1]
     dbias = torch.empty(H, dtype=gdt, device=dev) if want_dbias else None
+    if param_grads_out is not None:  # rows: [dgamma, dbeta,] [dbias]
+        k = 0
+        if dgamma is not None:
+            dgamma, dbeta, k = param_grads_out[0], param_grads_out[1], 2
+        if dbias is not None:
+            dbias = param_grads_out[k]
     ws_bytes = _lib.size("smpk_ln_bwd_workspace", M, H)
     ws = torch.empty(max(ws_bytes, 4) // 4, dtype=torch.float32, device=dev)
     npeers = 0 if out_peers is None else out_peers.numel()
