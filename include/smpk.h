@@ -106,6 +106,22 @@ SMPK_API int smpk_gemm_ex(const void* a, int a_mn_major, int64_t lda, int64_t a_
                           void* stream);
 
 /*
+ * smpk_gemm_ex2 — smpk_gemm_ex that also emits the output's column sums (the bias gradient of the
+ * layer whose input gradient it produces): colsum_part [smpk_gemm_colsum_rows(M)][N] fp32 receives
+ * the sum of every 32-row output box (bf16 values as stored); smpk_colsum_partials reduces the
+ * partial rows in order.  bf16, unbatched, unsplit outputs on the TMA-store path only.
+ */
+SMPK_API int64_t smpk_gemm_colsum_rows(int M);
+SMPK_API int smpk_gemm_ex2(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, int64_t a_bs2,
+                           const void* b, int b_mn_major, int64_t ldb, int64_t b_bs1, int64_t b_bs2,
+                           void* c, int c_f32, int64_t ldc, int64_t c_bs1, int64_t c_bs2,
+                           int M, int N, int K, int nb1, int nb2,
+                           float alpha, float beta, int epilogue, int act,
+                           const void* bias, void* aux, int64_t ldaux, void* workspace, int64_t workspace_bytes,
+                           float* colsum_part, void* stream);
+SMPK_API int smpk_colsum_partials(const float* part, int P, int N, void* out, int out_f32, void* stream);
+
+/*
  * smpk_bdr_ln_fwd — r = residual + dropout(x + bias); y = LayerNorm(r; gamma, beta, eps).
  *
  * The epilogue of every sub-layer of dist_transformer_layer_forward

@@ -28,6 +28,8 @@ SIGNATURES: dict[str, list] = {
     "smpk_device_info": [C.POINTER(I), C.POINTER(I), C.POINTER(I)],
     "smpk_gemm": [P, I, L, L, L, P, I, L, L, L, P, I, L, L, L, I, I, I, I, I, F, F, I, I, P, P, L, P],
     "smpk_gemm_ex": [P, I, L, L, L, P, I, L, L, L, P, I, L, L, L, I, I, I, I, I, F, F, I, I, P, P, L, P, L, P],
+    "smpk_gemm_ex2": [P, I, L, L, L, P, I, L, L, L, P, I, L, L, L, I, I, I, I, I, F, F, I, I, P, P, L, P, L, P, P],
+    "smpk_colsum_partials": [P, I, I, P, I, P],
     "smpk_bdr_ln_fwd": [P, P, P, P, P, P, P, P, P, I, I, F, F, C.c_uint64, I, I, L, P],
     "smpk_ln_bwd": [P, P, P, P, P, P, P, P, P, P, P, I, I, I, I, F, C.c_uint64, I, I, L, P, L, P],
     "smpk_softmax_fwd": [P, P, P, P, I, I, I, I, F, I, F, C.c_uint64, I, L, I, I, P],
@@ -67,6 +69,7 @@ SIZE_FUNCS: dict[str, list] = {
     "smpk_ln_bwd_workspace": [I, I],
     "smpk_colsum_workspace": [I, I],
     "smpk_gemm_workspace": [I, I, I, I, I],
+    "smpk_gemm_colsum_rows": [I],
     "smpk_flash_attn_bwd_workspace": [I, I, I, I],
 }
 

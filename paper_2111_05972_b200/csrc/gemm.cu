@@ -61,6 +61,9 @@ struct GemmArgs {
   int splits, kb_per, num_units;
   float* ws;
   int* sem;
+  // fused bias-gradient column sums (TMA-store path): colsum_part[row / 32][col] = sum of the 32
+  // stored bf16 rows of each output box (ceil(M/32) partial rows, reduced afterwards in order)
+  float* colsum_part;
 };
 
 // TMA store descriptors: C, the pre-activation (BIAS_ACT) and, for the reduce-scatter
@@ -488,6 +491,19 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensor
             }
             fence_proxy_async_smem();
             __syncwarp();
+            if constexpr (!F32OUT) {
+              if (g.colsum_part != nullptr && row0 < g.M && col0 + lane < g.N) {  // rows >= M hold zeros
+                // lane = column: sum the box's 32 stored rows (SWIZZLE_64B granule order)
+                float cs = 0.f;
+#pragma unroll 8
+                for (int rr = 0; rr < 32; ++rr) {
+                  const bf16* e = reinterpret_cast<const bf16*>(
+                      stg + rr * 64 + ((((lane >> 3) ^ ((rr >> 1) & 3))) << 4) + (lane & 7) * 2);
+                  cs += bf2f(*e);
+                }
+                g.colsum_part[(int64_t)(row0 >> 5) * g.N + col0 + lane] = cs;
+              }
+            }
             if (lane == 0) {
               if (g.npeers) {  // reduce-scatter: rows of one CTA belong to one owner
                 const int owner = (int)(row0 / g.rows_per_owner);
@@ -850,7 +866,7 @@ static int gemm_impl(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, 
                      int64_t c_bs1, int64_t c_bs2, int M, int N, int K, int nb1, int nb2, float alpha, float beta,
                      int epilogue, int act, const void* bias, void* aux, int64_t ldaux, void* const* peers_host,
                      int npeers, int64_t rows_per_owner, int64_t peer_slot_off, void* workspace,
-                     int64_t workspace_bytes, void* stream) {
+                     int64_t workspace_bytes, float* colsum_part, void* stream) {
   SMPK_REQUIRE(M > 0 && N > 0 && K > 0 && nb1 > 0 && nb2 > 0, SMPK_ERR_BAD_SHAPE,
                "smpk_gemm: bad shape M=%d N=%d K=%d nb=%dx%d", M, N, K, nb1, nb2);
   SMPK_REQUIRE(a && b && (c || npeers), SMPK_ERR_BAD_ARG, "smpk_gemm: null operand");
@@ -947,6 +963,9 @@ static int gemm_impl(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, 
       tma = make_store_map(&maps.aux, aux, false, M, N, ldaux, nb1, c_bs1, nb2, c_bs2, "aux") == SMPK_OK;
   }
   g.tma_store = tma ? 1 : 0;
+  g.colsum_part = colsum_part;
+  SMPK_REQUIRE(!colsum_part || (tma && !c_f32 && nb1 == 1 && nb2 == 1 && splits == 1), SMPK_ERR_UNSUPPORTED,
+               "smpk_gemm: fused column sums need a bf16, unbatched, unsplit TMA-store output");
 
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   // stage counts: stages_for() (fills the 227 KB of shared memory next to the staging boxes)
@@ -964,7 +983,7 @@ extern "C" int smpk_gemm(const void* a, int a_mn_major, int64_t lda, int64_t a_b
                          int64_t ldaux, void* stream) {
   return gemm_impl(a, a_mn_major, lda, a_bs1, a_bs2, b, b_mn_major, ldb, b_bs1, b_bs2, c, c_f32, ldc, c_bs1, c_bs2,
                    M, N, K, nb1, nb2, alpha, beta, epilogue, act, bias, aux, ldaux, nullptr, 0, 0, 0, nullptr, 0,
-                   stream);
+                   nullptr, stream);
 }
 
 extern "C" int smpk_gemm_ex(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, int64_t a_bs2, const void* b,
@@ -974,7 +993,20 @@ extern "C" int smpk_gemm_ex(const void* a, int a_mn_major, int64_t lda, int64_t 
                             int64_t ldaux, void* workspace, int64_t workspace_bytes, void* stream) {
   return gemm_impl(a, a_mn_major, lda, a_bs1, a_bs2, b, b_mn_major, ldb, b_bs1, b_bs2, c, c_f32, ldc, c_bs1, c_bs2,
                    M, N, K, nb1, nb2, alpha, beta, epilogue, act, bias, aux, ldaux, nullptr, 0, 0, 0, workspace,
-                   workspace_bytes, stream);
+                   workspace_bytes, nullptr, stream);
+}
+
+extern "C" int64_t smpk_gemm_colsum_rows(int M) { return (M + 31) / 32; }
+
+extern "C" int smpk_gemm_ex2(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, int64_t a_bs2, const void* b,
+                             int b_mn_major, int64_t ldb, int64_t b_bs1, int64_t b_bs2, void* c, int c_f32,
+                             int64_t ldc, int64_t c_bs1, int64_t c_bs2, int M, int N, int K, int nb1, int nb2,
+                             float alpha, float beta, int epilogue, int act, const void* bias, void* aux,
+                             int64_t ldaux, void* workspace, int64_t workspace_bytes, float* colsum_part,
+                             void* stream) {
+  return gemm_impl(a, a_mn_major, lda, a_bs1, a_bs2, b, b_mn_major, ldb, b_bs1, b_bs2, c, c_f32, ldc, c_bs1, c_bs2,
+                   M, N, K, nb1, nb2, alpha, beta, epilogue, act, bias, aux, ldaux, nullptr, 0, 0, 0, workspace,
+                   workspace_bytes, colsum_part, stream);
 }
 
 extern "C" int smpk_gemm_rs(const void* a, int a_mn_major, int64_t lda, const void* b, int b_mn_major, int64_t ldb,
@@ -987,5 +1019,5 @@ extern "C" int smpk_gemm_rs(const void* a, int a_mn_major, int64_t lda, const vo
                (long long)rows_per_owner);
   return gemm_impl(a, a_mn_major, lda, 0, 0, b, b_mn_major, ldb, 0, 0, nullptr, 0, ldc, 0, 0, M, N, K, 1, 1, 1.f,
                    0.f, SMPK_EPI_NONE, 0, nullptr, nullptr, 0, peers, npeers, rows_per_owner, peer_slot_off, nullptr,
-                   0, stream);
+                   0, nullptr, stream);
 }

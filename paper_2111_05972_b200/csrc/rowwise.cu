@@ -1157,6 +1157,15 @@ extern "C" int smpk_ln_bwd(const void* dy, const void* r, const float* mean, con
                         workspace, workspace_bytes, stream);
 }
 
+// Column sums from fp32 partial rows [P][N] (e.g. the GEMM epilogue's per-box sums), in order.
+extern "C" int smpk_colsum_partials(const float* part, int P, int N, void* out, int out_f32, void* stream) {
+  SMPK_REQUIRE(part && out && P > 0 && N > 0, SMPK_ERR_BAD_ARG, "smpk_colsum_partials: bad arguments");
+  dim3 g2((N + 31) / 32, 1);
+  colsum_reduce_kernel<<<g2, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(part, P, 1, N, out, nullptr, nullptr,
+                                                                             out_f32, 0);
+  return check_launch("smpk_colsum_partials");
+}
+
 // ===========================================================================
 // bias + activation (channel-sharded MLP of memory mode: the activation follows a
 // reduce-scatter, so it cannot live in the GEMM epilogue)

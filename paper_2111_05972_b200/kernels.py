@@ -56,8 +56,9 @@ PROFILER: GemmProfiler | None = None
 
 
 def gemm_raw(a, a_mn, lda, a_bs, b, b_mn, ldb, b_bs, c, ldc, c_bs, M, N, K, nb=(1, 1),
-             alpha=1.0, beta=0.0, epi=EPI_NONE, act=0, bias=None, aux=None, ldaux=0) -> None:
-    """Direct binding of smpk_gemm; strides in elements, batch strides as 2-tuples."""
+             alpha=1.0, beta=0.0, epi=EPI_NONE, act=0, bias=None, aux=None, ldaux=0, colsum_part=None) -> None:
+    """Direct binding of smpk_gemm; strides in elements, batch strides as 2-tuples.
+    colsum_part: fp32 [ceil(M/32), N] receiving per-32-row column sums of the output."""
     _check_cuda(a, b, c, bias, aux)
     prof = PROFILER
     if prof is not None:
@@ -65,15 +66,16 @@ def gemm_raw(a, a_mn, lda, a_bs, b, b_mn, ldb, b_bs, c, ldc, c_bs, M, N, K, nb=(
         if e0 is not None:
             e0.record()
     # split-K workspace (weight-gradient shapes with few output tiles); 0 bytes = unsplit
-    ws_bytes = _lib.size("smpk_gemm_workspace", int(M), int(N), int(K), int(nb[0]), int(nb[1]))
+    ws_bytes = 0 if colsum_part is not None else _lib.size("smpk_gemm_workspace", int(M), int(N), int(K),
+                                                               int(nb[0]), int(nb[1]))
     ws = torch.empty(ws_bytes // 4, dtype=torch.float32, device=c.device) if ws_bytes else None
-    _lib.call("smpk_gemm_ex",
+    _lib.call("smpk_gemm_ex2",
               _ptr(a), int(a_mn), int(lda), int(a_bs[0]), int(a_bs[1]),
               _ptr(b), int(b_mn), int(ldb), int(b_bs[0]), int(b_bs[1]),
               _ptr(c), int(c.dtype == torch.float32), int(ldc), int(c_bs[0]), int(c_bs[1]),
               int(M), int(N), int(K), int(nb[0]), int(nb[1]),
               float(alpha), float(beta), int(epi), int(act),
-              _ptr(bias), _ptr(aux), int(ldaux), _ptr(ws), int(ws_bytes), _stream())
+              _ptr(bias), _ptr(aux), int(ldaux), _ptr(ws), int(ws_bytes), _ptr(colsum_part), _stream())
     if prof is not None:
         if e1 is not None:
             e1.record()
@@ -140,16 +142,24 @@ def linear(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None, *
 
 
 def matmul_nn(a: torch.Tensor, b: torch.Tensor, *, out=None, epi=EPI_NONE, act="none", aux=None,
-              alpha=1.0, beta=0.0) -> torch.Tensor:
-    """C = a @ b, a [M,K] row-major, b [K,N] row-major (B operand MN-major). dgrad: dX = dY @ W."""
+              alpha=1.0, beta=0.0, want_colsum=False):
+    """C = a @ b, a [M,K] row-major, b [K,N] row-major (B operand MN-major). dgrad: dX = dY @ W.
+    want_colsum: also return the column sums of C (bf16 [N]) fused into the epilogue."""
     M, K = a.shape
     K2, N = b.shape
     if K != K2:
         raise ShapeMismatchError(f"matmul_nn: inner dims {K} vs {K2}")
     c = out if out is not None else torch.empty(M, N, dtype=a.dtype, device=a.device)
+    part = None
+    if want_colsum:
+        part = torch.empty(_lib.size("smpk_gemm_colsum_rows", M), N, dtype=torch.float32, device=a.device)
     gemm_raw(a, 0, _rowmajor(a, "a"), (0, 0), b, 1, _rowmajor(b, "b"), (0, 0), c, _rowmajor(c, "out"), (0, 0),
              M, N, K, alpha=alpha, beta=beta, epi=epi, act=ACT[act], aux=aux,
-             ldaux=(aux.stride(0) if aux is not None else 0))
+             ldaux=(aux.stride(0) if aux is not None else 0), colsum_part=part)
+    if want_colsum:
+        cs = torch.empty(N, dtype=c.dtype, device=c.device)
+        _lib.call("smpk_colsum_partials", _ptr(part), part.shape[0], N, _ptr(cs), 0, _stream())
+        return c, cs
     return c
 
 

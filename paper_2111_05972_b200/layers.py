@@ -495,8 +495,7 @@ class MlpFn(torch.autograd.Function):
         if db2 is None:
             db2 = ops.colsum(dgf)
         dw2 = K.matmul_tn(dgf, f)
-        dz = K.matmul_nn(dgf, w2, epi=K.EPI_DACT, act=m.activation, aux=z)
-        db1 = ops.colsum(dz)
+        dz, db1 = K.matmul_nn(dgf, w2, epi=K.EPI_DACT, act=m.activation, aux=z, want_colsum=True)
         dw1 = K.matmul_tn(dz, hf)
         if m.tp_size == 1 and not m.pre_ln:
             dx = K.matmul_nn(dz, w1, epi=K.EPI_ADD, aux=dr)

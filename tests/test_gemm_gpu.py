@@ -89,6 +89,21 @@ def test_bias_act_and_dact(K, act):
     f(p).backward(dy.float() @ w2.float())
     tol = 6e-2 if act == "relu" else TOL  # relu' flips on bf16-rounded pre-activations near 0
     assert rel(d.float(), p.grad) < tol
+    # fused bias-gradient column sums of the stored output (per-32-row partials, reduced in order)
+    d2, cs = kernels.matmul_nn(dy, w2, epi=kernels.EPI_DACT, act=act, aux=pre, want_colsum=True)
+    assert torch.equal(d2, d)
+    assert rel(cs.float(), d.float().sum(0)) < TOL
+
+
+@pytest.mark.parametrize("M,N", [(1000, 776), (96, 4096), (4096, 40)])
+def test_dgrad_colsum_ragged(K, M, N):
+    kernels, _ = K
+    dy, w = rnd(M, 256), rnd(256, N)
+    d, cs = kernels.matmul_nn(dy, w, want_colsum=True)
+    assert torch.equal(d, kernels.matmul_nn(dy, w))
+    assert rel(cs.float(), d.float().sum(0)) < TOL
+    _, cs2 = kernels.matmul_nn(dy, w, want_colsum=True)
+    assert torch.equal(cs, cs2)
 
 
 def test_bias_and_residual_epilogues(K):
