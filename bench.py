@@ -237,13 +237,18 @@ def trace_kernels(run, path_prefix: str, rank: int, steps: int = 2) -> None:
             f.write(f"{us / steps:10.1f} us/step {n // steps:5d} launches/step  {us / n:8.2f} us/launch  {name[:150]}\n")
 
 
+STATE_OVERLAP: dict = {}
+
+
 def run_gpu(args, rank, world, local):
     import paper_2111_05972_b200 as smp
     from paper_2111_05972_b200 import _lib, kernels
 
     torch.cuda.set_device(local)
     smp.init({"tensor_parallel_degree": world, "optimize": args.optimize, "seed": 1234, "tp_comm": args.tp_comm,
-              "tp_rs": args.tp_rs})
+              "tp_rs": args.tp_rs,
+              "tp_overlap_sms": args.tp_overlap_sms if args.tp_overlap_sms >= 0 else (96 if world >= 4 else 0)})
+    STATE_OVERLAP["sms"] = smp.state.STATE.config.get("tp_overlap_sms", 0) if world > 1 else 0
     torch.manual_seed(1000 + rank)
     model = smp.nn.DistributedTransformer(**CFG)
     model.train()
@@ -369,6 +374,7 @@ def run_gpu(args, rank, world, local):
                    "model": "BERT-large DistributedTransformer 24L H1024 16x64 FFN4096 post-LN gelu dropout0.1",
                    "global_batch": B * world, "per_gpu_batch": B, "seq_len": s,
                    "parallelism": f"tp{world} ({args.optimize} mode, TP across DP ranks)",
+                   "tp_comm": args.tp_comm, "tp_overlap_sms": STATE_OVERLAP.get("sms", 0),
                    "l2": "inputs larger than L2 (saved activations ~6 GB per step)"},
         "mfu": {"model_tflops_per_gpu": model_tflops, "flops_per_token": flops_tok,
                 "frac_of_sustained": model_tflops / peak_sus, "frac_of_burst": model_tflops / peaks["bf16_tflops"],
@@ -405,6 +411,9 @@ def main():
                     help="TP collectives: fused NVLink peer stores (default) or NCCL calls")
     ap.add_argument("--tp-rs", default="pull", choices=["pull", "push"],
                     help="peer reduce-scatter: consumer pulls partials over NVLink, or GEMM epilogue pushes")
+    ap.add_argument("--tp-overlap-sms", type=int, default=int(os.environ.get("SMPK_TP_OVERLAP_SMS", "-1")),
+                    help="T>1: SMs for the backward weight-gradient GEMMs beside the exchange (0 = serial; "
+                         "-1 = 96 at T >= 4, where it measured faster, else 0)")
     ap.add_argument("--trace", default="", help="diagnostics: write a per-kernel CUPTI trace summary to PREFIX_rankR.txt")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))

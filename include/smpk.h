@@ -97,6 +97,9 @@ SMPK_API int smpk_gemm(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1
  * chosen split needs (0: no split); a NULL / smaller workspace runs unsplit.
  */
 SMPK_API int64_t smpk_gemm_workspace(int M, int N, int K, int nb1, int nb2);
+/* smpk_set_sm_limits — cap the persistent grids of the GEMM (gemm_sms) and row / exchange kernels
+ * (row_sms) launched after this call (0 = whole GPU), so kernels on two streams can share the SMs. */
+SMPK_API int smpk_set_sm_limits(int gemm_sms, int row_sms);
 SMPK_API int smpk_gemm_ex(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, int64_t a_bs2,
                           const void* b, int b_mn_major, int64_t ldb, int64_t b_bs1, int64_t b_bs2,
                           void* c, int c_f32, int64_t ldc, int64_t c_bs1, int64_t c_bs2,

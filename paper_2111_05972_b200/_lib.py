@@ -69,6 +69,7 @@ SIZE_FUNCS: dict[str, list] = {
     "smpk_ln_bwd_workspace": [I, I],
     "smpk_colsum_workspace": [I, I],
     "smpk_gemm_workspace": [I, I, I, I, I],
+    "smpk_set_sm_limits": [I, I],
     "smpk_gemm_colsum_rows": [I],
     "smpk_flash_attn_bwd_workspace": [I, I, I, I],
 }
@@ -107,7 +108,7 @@ def lib() -> C.CDLL:
 
 
 # kernels launched by each entry point (for bench.py's gpu_launches count)
-LAUNCHES_PER_CALL = {"smpk_copy_async": 0, "smpk_ln_bwd": 2, "smpk_ln_bwd_ex": 2, "smpk_ln_bwd_dist": 2, "smpk_colsum": 2, "smpk_flash_attn_bwd": 3}
+LAUNCHES_PER_CALL = {"smpk_copy_async": 0, "smpk_set_sm_limits": 0, "smpk_ln_bwd": 2, "smpk_ln_bwd_ex": 2, "smpk_ln_bwd_dist": 2, "smpk_colsum": 2, "smpk_flash_attn_bwd": 3}
 launch_count = 0
 
 
@@ -132,3 +133,17 @@ def exported_symbols() -> list[str]:
 
 def last_error() -> str:
     return lib().smpk_last_error().decode(errors="replace")
+
+
+_SMS: dict = {}
+
+
+def device_sms() -> int:
+    """SM count of the current CUDA device (smpk_device_info, cached)."""
+    import torch
+    dev = torch.cuda.current_device()
+    if dev not in _SMS:
+        n, a, b = C.c_int(0), C.c_int(0), C.c_int(0)
+        call("smpk_device_info", C.byref(n), C.byref(a), C.byref(b), launches=0)
+        _SMS[dev] = n.value
+    return _SMS[dev]

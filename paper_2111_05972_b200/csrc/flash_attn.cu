@@ -408,18 +408,12 @@ extern "C" int smpk_flash_attn_fwd(const void* qkv, int64_t ld, int B, int nh, i
   dim3 grid((s / 128 + 1) / 2, nh, B);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (dh == 64) {
-    static bool once = false;
-    if (!once) {
-      cudaFuncSetAttribute(flash_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, FaFwdCfg<64>::SMEM);
-      once = true;
-    }
+    static unsigned long long once = 0;
+    smem_attr_once(flash_fwd_kernel<64>, FaFwdCfg<64>::SMEM, once);
     flash_fwd_kernel<64><<<grid, FA_THREADS, FaFwdCfg<64>::SMEM, st>>>(tq, tk, tv, a);
   } else {
-    static bool once = false;
-    if (!once) {
-      cudaFuncSetAttribute(flash_fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, FaFwdCfg<128>::SMEM);
-      once = true;
-    }
+    static unsigned long long once = 0;
+    smem_attr_once(flash_fwd_kernel<128>, FaFwdCfg<128>::SMEM, once);
     flash_fwd_kernel<128><<<grid, FA_THREADS, FaFwdCfg<128>::SMEM, st>>>(tq, tk, tv, a);
   }
   return check_launch("smpk_flash_attn_fwd");

@@ -486,18 +486,12 @@ extern "C" int smpk_flash_attn_bwd(const void* qkv, int64_t ld, const void* out,
   a.dq_part = dq_part;
   dim3 grid(n_kt, nh, B);
   if (dh == 64) {
-    static bool once = false;
-    if (!once) {
-      cudaFuncSetAttribute(flash_bwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, FaBwdCfg<64>::SMEM);
-      once = true;
-    }
+    static unsigned long long once = 0;
+    smem_attr_once(flash_bwd_kernel<64>, FaBwdCfg<64>::SMEM, once);
     flash_bwd_kernel<64><<<grid, FB_THREADS, FaBwdCfg<64>::SMEM, st>>>(tq, tk, tv, tdo, tbits, a);
   } else {
-    static bool once = false;
-    if (!once) {
-      cudaFuncSetAttribute(flash_bwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, FaBwdCfg<128>::SMEM);
-      once = true;
-    }
+    static unsigned long long once = 0;
+    smem_attr_once(flash_bwd_kernel<128>, FaBwdCfg<128>::SMEM, once);
     flash_bwd_kernel<128><<<grid, FB_THREADS, FaBwdCfg<128>::SMEM, st>>>(tq, tk, tv, tdo, tbits, a);
   }
   rc = check_launch("smpk_flash_attn_bwd");

@@ -716,13 +716,10 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMa
   static_assert(Cfg::SMEM_BYTES <= 232448, "shared memory budget");
   auto kern = PAIR ? gemm_bf16_tcgen05_pair<BN, STAGES, EPI, ACT, F32OUT, BETA>
                    : gemm_bf16_tcgen05<BN, STAGES, EPI, ACT, F32OUT, BETA>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-    SMPK_REQUIRE(e == cudaSuccess, SMPK_ERR_CUDA, "smpk_gemm: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-    attr_set = true;
-  }
-  const int slots = PAIR ? num_sms() / 2 : num_sms();  // CTA pairs (one per TPC) or CTAs
+  static unsigned long long attr_set = 0;
+  cudaError_t e = smem_attr_once(kern, Cfg::SMEM_BYTES, attr_set);
+  SMPK_REQUIRE(e == cudaSuccess, SMPK_ERR_CUDA, "smpk_gemm: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+  const int slots = PAIR ? gemm_sms() / 2 : gemm_sms();  // CTA pairs (one per TPC) or CTAs
   int grid = g.num_units < slots ? g.num_units : slots;
   if (PAIR) grid *= 2;
   kern<<<grid, gemm_threads(EPI), Cfg::SMEM_BYTES, st>>>(ta, tb, maps, g);
@@ -807,12 +804,12 @@ static void plan_gemm(int M, int N, int K, int nb1, int nb2, int& BN, bool& pair
   const int rows = pair ? 2 * BM : BM;
   tiles = ((M + rows - 1) / rows) * ((N + BN - 1) / BN) * nb1 * nb2;
   num_kb = (K + BK - 1) / BK;
-  splits = choose_splits(tiles, num_kb, BN, pair ? num_sms() / 2 : num_sms(), pair ? 2 : 1);
+  splits = choose_splits(tiles, num_kb, BN, pair ? gemm_sms() / 2 : gemm_sms(), pair ? 2 : 1);
   if (pair && splits > 1) {
     // measured: split-K runs faster on single-CTA tiles (finer units, shorter fix-up)
     pair = false;
     tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * nb1 * nb2;
-    splits = choose_splits(tiles, num_kb, BN, num_sms(), 1);
+    splits = choose_splits(tiles, num_kb, BN, gemm_sms(), 1);
   }
   kb_per = (num_kb + splits - 1) / splits;
 }

@@ -133,7 +133,7 @@ static bool row_geom(int H, RowGeom& g) {
 static int row_grid(int M, int W) {
   const int rows_per_cta = (ROW_THREADS / 32) / W;
   int need = (M + rows_per_cta - 1) / rows_per_cta;
-  int cap = num_sms() * 4;
+  int cap = row_sms() * 4;
   return need < cap ? need : cap;
 }
 
@@ -951,15 +951,12 @@ static int bdr_ln_pipe_launch(const BdrPipeArgs& a, cudaStream_t st) {
   const int nin = a.nslots + (a.residual ? 1 : 0);
   const int stage_bytes = nin * a.H * 2;
   const int smem = a.nst * stage_bytes + 3 * a.H * 2 + 2 * a.nst * 8 + 128;
-  const int grid = a.M < num_sms() ? a.M : num_sms();
+  const int grid = a.M < row_sms() ? a.M : row_sms();
   switch (a.H / 256) {
 #define SMPK_PIPE_CASE(CH_)                                                                              \
   case CH_: {                                                                                            \
-    static bool once = false;                                                                            \
-    if (!once) {                                                                                         \
-      cudaFuncSetAttribute(bdr_ln_pipe_kernel<CH_>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448); \
-      once = true;                                                                                       \
-    }                                                                                                    \
+    static unsigned long long once = 0;                                                                  \
+    smem_attr_once(bdr_ln_pipe_kernel<CH_>, 232448, once);                                               \
     bdr_ln_pipe_kernel<CH_><<<grid, 32 * (PIPE_CW + 1), smem, st>>>(a);                                  \
     break;                                                                                               \
   }
@@ -1072,7 +1069,7 @@ extern "C" int smpk_bdr_ln_fwd(const void* x, const void* bias, const void* resi
 static int ln_bwd_grid_geo(int M, int W) {
   const int rows_per_cta = (ROW_THREADS / 32) / W;
   const int need = (M + rows_per_cta - 1) / rows_per_cta;
-  const int cap = 2 * num_sms();
+  const int cap = 2 * row_sms();
   return need < cap ? need : cap;
 }
 
@@ -1203,7 +1200,7 @@ __global__ void __launch_bounds__(256) act_bwd_kernel(const bf16* __restrict__ d
 
 static int elementwise_grid(int64_t n8) {
   const int64_t want = (n8 + 255) / 256;
-  const int64_t cap = (int64_t)num_sms() * 8;
+  const int64_t cap = (int64_t)row_sms() * 8;
   return (int)(want < cap ? want : cap);
 }
 
@@ -1289,7 +1286,7 @@ __global__ void __launch_bounds__(256) colsum_partial_vec_kernel(const bf16* x, 
 static int colsum_rpc(int M, int N) {
   const int cblocks = (N + 255) / 256;
   for (int rpc = 256; rpc > 64; rpc >>= 1)
-    if ((int64_t)cblocks * ((M + rpc - 1) / rpc) >= 2 * num_sms()) return rpc;
+    if ((int64_t)cblocks * ((M + rpc - 1) / rpc) >= 2 * row_sms()) return rpc;
   return 64;
 }
 
@@ -1352,7 +1349,7 @@ extern "C" int smpk_softmax_fwd(const void* scores, void* probs, void* probs_dro
                 (uint32_t)layer, sample_offset, head_offset, nh_global};
   const int64_t rows = (int64_t)B * nh * sq;
   int64_t grid = (rows + 7) / 8;
-  if (grid > num_sms() * 8) grid = num_sms() * 8;
+  if (grid > row_sms() * 8) grid = row_sms() * 8;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   SMPK_DISPATCH_NV(nv, softmax_fwd_kernel, ((int)grid, ROW_THREADS, 0, st), (a));
   return check_launch("smpk_softmax_fwd");
@@ -1369,7 +1366,7 @@ extern "C" int smpk_softmax_bwd(const void* probs, const void* dprobs_drop, void
                 (uint32_t)layer, sample_offset, head_offset, nh_global};
   const int64_t rows = (int64_t)B * nh * sq;
   int64_t grid = (rows + 7) / 8;
-  if (grid > num_sms() * 8) grid = num_sms() * 8;
+  if (grid > row_sms() * 8) grid = row_sms() * 8;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   SMPK_DISPATCH_NV(nv, softmax_bwd_kernel, ((int)grid, ROW_THREADS, 0, st), (a));
   return check_launch("smpk_softmax_bwd");

@@ -38,7 +38,24 @@ int num_sms() {
   return n[dev];
 }
 
+// SM budgets for concurrently running kernels (0 = the whole GPU): GEMMs launched on a side
+// stream next to the TP exchange kernels cap their persistent grid, and the exchange kernels cap
+// theirs to the SMs left over, so neither waits for the other's CTAs to retire.
+static int g_sm_limit_gemm = 0, g_sm_limit_rows = 0;
+static int capped(int lim) {
+  const int n = num_sms();
+  return (lim > 0 && lim < n) ? lim : n;
+}
+int gemm_sms() { return capped(g_sm_limit_gemm) & ~1; }
+int row_sms() { return capped(g_sm_limit_rows); }
+
 }  // namespace smpk
+
+extern "C" int smpk_set_sm_limits(int gemm_sms, int row_sms) {
+  smpk::g_sm_limit_gemm = gemm_sms > 0 ? gemm_sms : 0;
+  smpk::g_sm_limit_rows = row_sms > 0 ? row_sms : 0;
+  return SMPK_OK;
+}
 
 extern "C" const char* smpk_last_error(void) { return smpk::g_last_error; }
 

@@ -31,6 +31,8 @@ int check_launch(const char* what);
   } while (0)
 
 int num_sms();
+int gemm_sms();  // num_sms() under smpk_set_sm_limits (even)
+int row_sms();
 
 // ---------------------------------------------------------------------------
 // shared-memory / mbarrier
@@ -409,6 +411,18 @@ __device__ __forceinline__ void dropout_keep8(uint64_t seed, uint32_t layer, uin
     keep[2 * j] = (w[j] & 0xffffu) >= thresh;
     keep[2 * j + 1] = (w[j] >> 16) >= thresh;
   }
+}
+
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: set once per (kernel, device).
+template <typename Kern>
+inline cudaError_t smem_attr_once(Kern kern, int bytes, unsigned long long& done_mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if ((done_mask >> dev) & 1ull) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done_mask |= 1ull << dev;
+  return e;
 }
 
 }  // namespace smpk

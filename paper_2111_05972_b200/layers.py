@@ -173,6 +173,51 @@ def _keep_bits_async(B: int, s: int, m: LayerMeta, device):
     return bits, (lambda: main.wait_stream(side))
 
 
+class _SmLimits:
+    """smpk_set_sm_limits for the duration of a with-block (launch-time grid caps)."""
+
+    def __init__(self, gemm_sms: int, row_sms: int):
+        self.lim = (int(gemm_sms), int(row_sms))
+
+    def __enter__(self):
+        from . import _lib
+        _lib.call("smpk_set_sm_limits", *self.lim)
+
+    def __exit__(self, *exc):
+        from . import _lib
+        _lib.call("smpk_set_sm_limits", 0, 0)
+
+
+def _overlap_sms(m: LayerMeta) -> int:
+    """SMs given to the backward's weight-gradient GEMMs while the input-gradient exchange runs
+    next to them (tp_overlap_sms; 0 = serial).  Only with the peer-memory exchange at T > 1."""
+    if m.tp_size == 1 or STATE.config.get("tp_comm", "peer") != "peer":
+        return 0
+    return int(STATE.config.get("tp_overlap_sms", 0))
+
+
+def _wgrad_async(m: LayerMeta, jobs):
+    """Run the weight-gradient GEMMs `jobs` (no data dependence on the exchange that follows) on
+    the side stream with a capped grid; returns (join, row_sms) — the exchange kernels launched
+    before join() should cap their grids at row_sms so both streams fit on the GPU at once.
+    The fork / join is CUDA-graph capturable.  Output tensors must be allocated by the caller on
+    the main stream."""
+    gs = _overlap_sms(m)
+    if gs <= 0:
+        for f in jobs:
+            f()
+        return (lambda: None), 0
+    from . import _lib
+    nsm = _lib.device_sms()
+    main = torch.cuda.current_stream()
+    side = _side_stream()
+    side.wait_stream(main)
+    with torch.cuda.stream(side), _SmLimits(gs, 0):
+        for f in jobs:
+            f()
+    return (lambda: main.wait_stream(side)), max(nsm - gs, 8)
+
+
 def _ln_in(x2, w, b, m: LayerMeta):
     y, mean, rstd = ops.layer_norm(x2, w, b, m.eps)
     return y, mean, rstd
@@ -427,21 +472,28 @@ class AttentionFn(torch.autograd.Function):
             dr = dy2
         if dbo is None:
             dbo = ops.colsum(dof)  # over all rows of the group: complete on every rank
-        dwo = K.matmul_tn(dof, ctxv)
+        ov = _overlap_sms(m) > 0 and not (m.tp_size == 1 and not m.pre_ln)
+        dwo = torch.empty_like(wo) if ov else K.matmul_tn(dof, ctxv)
         dctx = K.matmul_nn(dof, wo)
         if ctx.fused:
             dqkv = ops.flash_attn_bwd(dctx, qkv, ctxv, P, B, s, m.heads_local, m.head_dim, mask_add=mask_add,
                                       causal=m.causal, p=m.p_attn, keep_bits=Pd if m.p_attn > 0 else None)
         else:
             dqkv = attn_core_bwd(dctx, qkv, P, Pd, B, s, m)
-        dwqkv = K.matmul_tn(dqkv, hf)
+        dwqkv = torch.empty_like(wqkv) if ov else K.matmul_tn(dqkv, hf)
         dbqkv = ops.colsum(dqkv)
         if m.tp_size == 1 and not m.pre_ln:
             dx = K.matmul_nn(dqkv, wqkv, epi=K.EPI_ADD, aux=dr)
             dpre_w = dpre_b = None
         else:
             dhx, skw, PR = _rs_out(dqkv, wqkv, True, m, R, H)
-            dx, dpre_w, dpre_b = _input_grad(dhx, skw, dr, x2, pre_w, mu1, rs1, m, R, H)
+            join, rsm = (lambda: None), 0
+            if ov:  # weight gradients on the side stream, next to the reduce-scatter consumer
+                join, rsm = _wgrad_async(m, [lambda: K.matmul_tn(dof, ctxv, out=dwo),
+                                             lambda: K.matmul_tn(dqkv, hf, out=dwqkv)])
+            with _SmLimits(0, rsm):
+                dx, dpre_w, dpre_b = _input_grad(dhx, skw, dr, x2, pre_w, mu1, rs1, m, R, H)
+            join()
             _free(PR)
         _free(G2, ctx.G)
         dpost_w, dpost_b, dpre_w, dpre_b = _sync_replicated(
@@ -494,15 +546,22 @@ class MlpFn(torch.autograd.Function):
             dr = dy2
         if db2 is None:
             db2 = ops.colsum(dgf)
-        dw2 = K.matmul_tn(dgf, f)
+        ov = _overlap_sms(m) > 0 and not (m.tp_size == 1 and not m.pre_ln)
+        dw2 = torch.empty_like(w2) if ov else K.matmul_tn(dgf, f)
         dz, db1 = K.matmul_nn(dgf, w2, epi=K.EPI_DACT, act=m.activation, aux=z, want_colsum=True)
-        dw1 = K.matmul_tn(dz, hf)
+        dw1 = torch.empty_like(w1) if ov else K.matmul_tn(dz, hf)
         if m.tp_size == 1 and not m.pre_ln:
             dx = K.matmul_nn(dz, w1, epi=K.EPI_ADD, aux=dr)
             dpre_w = dpre_b = None
         else:
             dhx, skw, PR = _rs_out(dz, w1, True, m, R, H)
-            dx, dpre_w, dpre_b = _input_grad(dhx, skw, dr, x2, pre_w, mu1, rs1, m, R, H)
+            join, rsm = (lambda: None), 0
+            if ov:  # weight gradients on the side stream, next to the reduce-scatter consumer
+                join, rsm = _wgrad_async(m, [lambda: K.matmul_tn(dgf, f, out=dw2),
+                                             lambda: K.matmul_tn(dz, hf, out=dw1)])
+            with _SmLimits(0, rsm):
+                dx, dpre_w, dpre_b = _input_grad(dhx, skw, dr, x2, pre_w, mu1, rs1, m, R, H)
+            join()
             _free(PR)
         _free(G2, ctx.G)
         dpost_w, dpost_b, dpre_w, dpre_b = _sync_replicated(

@@ -32,7 +32,8 @@ DEFAULTS = {
     "seed": 0,
     "ddp": True,
     "tp_comm": "peer",  # fused NVLink peer-memory collectives ("nccl": torch.distributed calls)
-    "tp_rs": "pull",  # peer reduce-scatter: consumer pulls the partials ("push": GEMM epilogue stores)
+    "tp_rs": "pull",
+    "tp_overlap_sms": 0,  # >0: backward weight-gradient GEMMs on this many SMs beside the exchange  # peer reduce-scatter: consumer pulls the partials ("push": GEMM epilogue stores)
     "symm_pool_bytes": 4 << 30,
 }
 
