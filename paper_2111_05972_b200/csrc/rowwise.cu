@@ -419,11 +419,13 @@ __global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const LnBwdArgs a) 
     }
     float s1 = 0.f, s2 = 0.f;
     uint4 dres_raw[VPT];  // residual-gradient loads issued with the others (memory-level parallelism)
+    uint32_t keep_raw[VPT];  // stored keep bytes, likewise loaded up front
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       const int col = ((i * W + wi) * 32 + lane) * 8;
       if (valid && a.dres && col < a.H)
         dres_raw[i] = *reinterpret_cast<const uint4*>(a.dres + (int64_t)row * a.H + col);
+      keep_raw[i] = (valid && a.keep_in && col < a.H) ? a.keep_in[(int64_t)row * (a.H / 8) + col / 8] : 0u;
     }
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
@@ -494,7 +496,7 @@ __global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const LnBwdArgs a) 
       if (a.p > 0.f) {
         bool keep[8];
         if (a.keep_in)
-          keep8_from_byte(a.keep_in[(int64_t)row * (a.H / 8) + col / 8], keep);
+          keep8_from_byte(keep_raw[i], keep);
         else
           dropout_keep8(a.seed, a.layer, a.site, (uint64_t)(a.row_offset + row), (int)(a.col_offset + col),
                         dropout_threshold(a.p), keep);
