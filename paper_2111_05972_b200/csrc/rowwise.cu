@@ -520,11 +520,13 @@ __global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const LnBwdArgs a) 
 }
 
 // Reduce P partial rows of [P][K][H] to K outputs of H columns (fixed order).
-// block = 32 columns x 8 row groups; each thread sums every 8th partial row, then the
-// 8 group sums are added in ascending order (deterministic).
-__global__ void __launch_bounds__(256) colsum_reduce_kernel(const float* partials, int P, int K, int H, void* o0,
-                                                            void* o1, void* o2, int out_f32, int accumulate) {
-  __shared__ float sm[8][33];
+// block = 32 columns x NG row groups; each thread sums every NG-th partial row (4 independent
+// accumulators), then the NG group sums are added in ascending order (deterministic).  NG = 32
+// for long partial lists: ~4x fewer dependent load round trips per thread than NG = 8.
+template <int NG>
+__global__ void __launch_bounds__(32 * NG) colsum_reduce_kernel(const float* partials, int P, int K, int H, void* o0,
+                                                                void* o1, void* o2, int out_f32, int accumulate) {
+  __shared__ float sm[NG][33];
   const int c = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int col = blockIdx.x * 32 + c;
   const int k = blockIdx.y;
@@ -532,14 +534,13 @@ __global__ void __launch_bounds__(256) colsum_reduce_kernel(const float* partial
   if (o == nullptr) return;  // uniform per block
   float part = 0.f;
   if (col < H) {
-    // 4 independent accumulators keep 4 loads in flight per thread; combined in fixed order
     float q[4] = {0.f, 0.f, 0.f, 0.f};
     int p = grp;
-    for (; p + 24 < P; p += 32) {
+    for (; p + 3 * NG < P; p += 4 * NG) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) q[u] += partials[((int64_t)(p + 8 * u) * K + k) * H + col];
+      for (int u = 0; u < 4; ++u) q[u] += partials[((int64_t)(p + NG * u) * K + k) * H + col];
     }
-    for (; p < P; p += 8) q[0] += partials[((int64_t)p * K + k) * H + col];
+    for (; p < P; p += NG) q[0] += partials[((int64_t)p * K + k) * H + col];
     part = (q[0] + q[1]) + (q[2] + q[3]);
   }
   sm[grp][c] = part;
@@ -547,7 +548,7 @@ __global__ void __launch_bounds__(256) colsum_reduce_kernel(const float* partial
   if (grp != 0 || col >= H) return;
   float s = 0.f;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) s += sm[i][c];
+  for (int i = 0; i < NG; ++i) s += sm[i][c];
   if (out_f32) {
     float* f = reinterpret_cast<float*>(o);
     f[col] = accumulate ? f[col] + s : s;
@@ -555,6 +556,14 @@ __global__ void __launch_bounds__(256) colsum_reduce_kernel(const float* partial
     bf16* b = reinterpret_cast<bf16*>(o);
     b[col] = f2bf(accumulate ? bf2f(b[col]) + s : s);
   }
+}
+
+static void colsum_reduce_launch(dim3 grid, const float* partials, int P, int K, int H, void* o0, void* o1, void* o2,
+                                 int out_f32, int accumulate, cudaStream_t st) {
+  if (P >= 64)
+    colsum_reduce_kernel<32><<<grid, 1024, 0, st>>>(partials, P, K, H, o0, o1, o2, out_f32, accumulate);
+  else
+    colsum_reduce_kernel<8><<<grid, 256, 0, st>>>(partials, P, K, H, o0, o1, o2, out_f32, accumulate);
 }
 
 // generic column partial sums of a [M, N] bf16 matrix: grid.x = column blocks of 256, grid.y = row chunks
@@ -1119,8 +1128,8 @@ static int ln_bwd_impl(const void* dy, int nslots, int64_t slot_stride, const vo
   if (rc) return rc;
   if (row_sums_out || (!dgamma && !dbeta && !dbias)) return SMPK_OK;
   dim3 rg((H + 31) / 32, 3);
-  colsum_reduce_kernel<<<rg, 256, 0, st>>>(reinterpret_cast<float*>(workspace), grid, 3, H, dgamma, dbeta, dbias,
-                                           grads_f32, accumulate);
+  colsum_reduce_launch(rg, reinterpret_cast<float*>(workspace), grid, 3, H, dgamma, dbeta, dbias, grads_f32,
+                       accumulate, st);
   return check_launch("smpk_ln_bwd(reduce)");
 }
 
@@ -1160,8 +1169,8 @@ extern "C" int smpk_ln_bwd(const void* dy, const void* r, const float* mean, con
 extern "C" int smpk_colsum_partials(const float* part, int P, int N, void* out, int out_f32, void* stream) {
   SMPK_REQUIRE(part && out && P > 0 && N > 0, SMPK_ERR_BAD_ARG, "smpk_colsum_partials: bad arguments");
   dim3 g2((N + 31) / 32, 1);
-  colsum_reduce_kernel<<<g2, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(part, P, 1, N, out, nullptr, nullptr,
-                                                                             out_f32, 0);
+  colsum_reduce_launch(g2, part, P, 1, N, out, nullptr, nullptr, out_f32, 0,
+                       reinterpret_cast<cudaStream_t>(stream));
   return check_launch("smpk_colsum_partials");
 }
 
@@ -1320,7 +1329,7 @@ extern "C" int smpk_colsum(const void* x, int M, int N, int64_t ldx, void* out, 
   int rc = check_launch("smpk_colsum");
   if (rc) return rc;
   dim3 g2((N + 31) / 32, 1);
-  colsum_reduce_kernel<<<g2, 256, 0, st>>>(ws, chunks, 1, N, out, nullptr, nullptr, out_f32, accumulate);
+  colsum_reduce_launch(g2, ws, chunks, 1, N, out, nullptr, nullptr, out_f32, accumulate, st);
   return check_launch("smpk_colsum(reduce)");
 }
 
