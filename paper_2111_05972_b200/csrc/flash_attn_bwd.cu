@@ -126,17 +126,22 @@ __global__ void __launch_bounds__(FB_THREADS, (DH == 64 ? 2 : 1))
       const int64_t bh_row = ((int64_t)b * a.nh + h) * a.s;
       for (int t = 0; t < nt; ++t) {
         const int i = i0 + t;
-        mbar_wait(qdo_empty, (t & 1) ^ 1);
+        // dO, lse, Delta and the keep bits of tile t are loaded as soon as tile t-1's dS pass has
+        // read them (ds_full: after the dV / dP^T MMAs and the softmax warps' last use), i.e. while
+        // tile t-1's dK / dQ MMAs and dQ drain still run; Q waits for those MMAs (qdo_empty).
+        if (t > 0) mbar_wait(ds_full, (t - 1) & 1);
         mbar_arrive_expect_tx(qdo_full, 2 * Cfg::TILE + 1024 + (a.dropout ? 2048 : 0));
 #pragma unroll
-        for (int c = 0; c < DH / 64; ++c) {
-          tma_load_4d(smem + Cfg::OFF_Q + c * 16384, &tmQ, qdo_full, c * 64, i * 128, h, b);
+        for (int c = 0; c < DH / 64; ++c)
           tma_load_4d(smem + Cfg::OFF_DO + c * 16384, &tmDO, qdo_full, c * 64, i * 128, h, b);
-        }
         const int64_t off = bh_row + (int64_t)i * 128;
         bulk_load(smem + Cfg::OFF_LSE, a.lse + off, 512, qdo_full);
         bulk_load(smem + Cfg::OFF_DELTA, a.delta + off, 512, qdo_full);
         if (a.dropout) tma_load_4d(smem + Cfg::OFF_BITS, &tmBits, qdo_full, j * 4, (int)off, 0, 0);
+        mbar_wait(qdo_empty, (t & 1) ^ 1);
+#pragma unroll
+        for (int c = 0; c < DH / 64; ++c)
+          tma_load_4d(smem + Cfg::OFF_Q + c * 16384, &tmQ, qdo_full, c * 64, i * 128, h, b);
       }
     }
   } else if (warp == 1) {
