@@ -51,6 +51,15 @@ __device__ __forceinline__ float group_sum(float v, float* sm, int slot, int wi)
   }
 }
 
+__device__ __forceinline__ void unpack8(const uint4 u, float (&v)[8]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 f = unpack_bf16x2(w[j]);
+    v[2 * j] = f.x;
+    v[2 * j + 1] = f.y;
+  }
+}
 __device__ __forceinline__ void load8(const bf16* p, float (&v)[8]) {
   uint4 u = *reinterpret_cast<const uint4*>(p);
   uint32_t w[4] = {u.x, u.y, u.z, u.w};
@@ -130,10 +139,10 @@ static bool row_geom(int H, RowGeom& g) {
   return false;
 }
 
-static int row_grid(int M, int W) {
+static int row_grid(int M, int W, int ctas_per_sm = 4) {
   const int rows_per_cta = (ROW_THREADS / 32) / W;
   int need = (M + rows_per_cta - 1) / rows_per_cta;
-  int cap = row_sms() * 4;
+  int cap = row_sms() * ctas_per_sm;
   return need < cap ? need : cap;
 }
 
@@ -215,7 +224,23 @@ __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs
   const int slot = warp / W, wi = warp % W;
   const int rows_per_cta = (ROW_THREADS / 32) / W;
   const float inv_keep = a.p > 0.f ? 1.f / (1.f - a.p) : 1.f;
-  for (int row0 = blockIdx.x * rows_per_cta; row0 < a.M; row0 += gridDim.x * rows_per_cta) {
+  // Single-slot local input: the next row's x / residual are loaded into registers before this
+  // row's dropout / statistics / stores, so a row's math overlaps the next row's HBM latency.
+  const bool prefetch = a.x_peers == nullptr && a.nslots == 1;
+  const int row_step = gridDim.x * rows_per_cta;
+  uint4 px[VPT], pr[VPT];
+  auto issue = [&](int row) {
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int col = ((i * W + wi) * 32 + lane) * 8;
+      if (row < a.M && col < a.H) {
+        px[i] = *reinterpret_cast<const uint4*>(a.x + (int64_t)row * a.H + col);
+        if (a.residual) pr[i] = *reinterpret_cast<const uint4*>(a.residual + (int64_t)row * a.H + col);
+      }
+    }
+  };
+  if (prefetch) issue(blockIdx.x * rows_per_cta + slot);
+  for (int row0 = blockIdx.x * rows_per_cta; row0 < a.M; row0 += row_step) {
     const int row = row0 + slot;
     const bool valid = row < a.M;
     float v[VPT][8], res[VPT][8];
@@ -223,7 +248,12 @@ __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       const int col = ((i * W + wi) * 32 + lane) * 8;
-      if (valid && col < a.H) {
+      if (prefetch) {
+        if (valid && col < a.H) {
+          unpack8(px[i], v[i]);
+          if (a.residual) unpack8(pr[i], res[i]);
+        }
+      } else if (valid && col < a.H) {
         if (a.x_peers)
           load8_peer_slots(a.x_peers, a.nslots, a.x_peer_off + (int64_t)row * a.H + col, v[i]);
         else
@@ -231,6 +261,7 @@ __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs
         if (a.residual) load8(a.residual + (int64_t)row * a.H + col, res[i]);
       }
     }
+    if (prefetch) issue(row + row_step);
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       const int col = ((i * W + wi) * 32 + lane) * 8;
@@ -1042,7 +1073,8 @@ static int bdr_ln_impl(const void* x, int nslots, int64_t slot_stride, const voi
     pa.nst = nst > 16 ? 16 : nst;
     if (pa.nst >= 2) return bdr_ln_pipe_launch(pa, st);
   }
-  const int grid = row_grid(M, geo.W);
+  // 80 registers with the next-row prefetch: 3 resident CTAs per SM, one wave
+  const int grid = row_grid(M, geo.W, 3);
   SMPK_DISPATCH_ROW(geo.W, geo.VPT, bdr_ln_fwd_kernel, (grid, ROW_THREADS, 0, st), (a));
   return check_launch("smpk_bdr_ln_fwd");
 }
