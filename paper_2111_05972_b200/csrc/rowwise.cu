@@ -51,6 +51,13 @@ __device__ __forceinline__ float group_sum(float v, float* sm, int slot, int wi)
   }
 }
 
+// Bulk L2 prefetch of a contiguous 16-byte-aligned span (no registers held; the row kernels use it
+// to pull the next row's inputs toward L2 while the current row computes).
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  if ((reinterpret_cast<uintptr_t>(p) | bytes) & 15u) return;  // the bulk form needs 16-byte granules
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void unpack8(const uint4 u, float (&v)[8]) {
   const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
@@ -442,6 +449,16 @@ __global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const LnBwdArgs a) 
   for (int row0 = blockIdx.x * rows_per_cta; row0 < a.M; row0 += gridDim.x * rows_per_cta) {
     const int row = row0 + slot;
     const bool valid = row < a.M;
+    {  // next row of this slot: dy / r / dres / keep bytes toward L2 (registers are the limiter here)
+      const int nrow = row + gridDim.x * rows_per_cta;
+      if (wi == 0 && lane == 0 && nrow < a.M) {
+        const uint32_t rb = (uint32_t)a.H * 2;
+        if (a.dy_peers == nullptr && a.nslots == 1) prefetch_l2(a.dy + (int64_t)nrow * a.H, rb);
+        if (has_ln) prefetch_l2(a.r + (int64_t)nrow * a.H, rb);
+        if (a.dres) prefetch_l2(a.dres + (int64_t)nrow * a.H, rb);
+        if (a.keep_in) prefetch_l2(a.keep_in + (int64_t)nrow * (a.H / 8), a.H / 8);
+      }
+    }
     float xh[VPT][8], g[VPT][8];
     float mu = 0.f, rs = 0.f;
     if (valid && has_ln) {
