@@ -380,29 +380,42 @@ __global__ void __launch_bounds__(FB_THREADS, (DH == 64 ? 2 : 1))
   }
 }
 
-// Delta[b, h, q] = sum_d dO[b*s+q, h*dh+d] * O[b*s+q, h*dh+d]   (one thread per (row, head))
-__global__ void flash_delta_kernel(const bf16* __restrict__ o, int64_t ld_o, const bf16* __restrict__ dout,
-                                   int64_t ld_do, int B, int nh, int s, int dh, float* __restrict__ delta) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// Delta[b, h, q] = sum_d dO[b*s+q, h*dh+d] * O[b*s+q, h*dh+d]
+// 8 lanes per (row, head): each lane loads 16 B of O and dO per 64 columns (coalesced 128-byte
+// segments, every load of the head issued up front), then a 3-step xor-shuffle sum.
+__global__ void __launch_bounds__(256) flash_delta_kernel(const bf16* __restrict__ o, int64_t ld_o,
+                                                          const bf16* __restrict__ dout, int64_t ld_do, int B,
+                                                          int nh, int s, int dh, float* __restrict__ delta) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t idx = t >> 3;
+  const int sub = (int)(t & 7);
   const int64_t total = (int64_t)B * s * nh;
-  if (idx >= total) return;
-  const int h = (int)(idx % nh);
-  const int64_t row = idx / nh;
-  const bf16* op = o + row * ld_o + (int64_t)h * dh;
-  const bf16* dp = dout + row * ld_do + (int64_t)h * dh;
+  const bool valid = idx < total;  // no early exit: the whole warp takes part in the shuffles
+  const int h = valid ? (int)(idx % nh) : 0;
+  const int64_t row = valid ? idx / nh : 0;
   float acc = 0.f;
-  for (int d = 0; d < dh; d += 8) {
-    uint4 a = *reinterpret_cast<const uint4*>(op + d);
-    uint4 c = *reinterpret_cast<const uint4*>(dp + d);
-    uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wc[4] = {c.x, c.y, c.z, c.w};
+  if (valid) {
+    const bf16* op = o + row * ld_o + (int64_t)h * dh;
+    const bf16* dp = dout + row * ld_do + (int64_t)h * dh;
+#pragma unroll 2
+    for (int d = sub * 8; d < dh; d += 64) {
+      const uint4 a = *reinterpret_cast<const uint4*>(op + d);
+      const uint4 c = *reinterpret_cast<const uint4*>(dp + d);
+      const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wc[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      float2 fa = unpack_bf16x2(wa[k]), fc = unpack_bf16x2(wc[k]);
-      acc += fa.x * fc.x + fa.y * fc.y;
+      for (int k = 0; k < 4; ++k) {
+        const float2 fa = unpack_bf16x2(wa[k]), fc = unpack_bf16x2(wc[k]);
+        acc += fa.x * fc.x + fa.y * fc.y;
+      }
     }
   }
-  const int64_t b = row / s, q = row % s;
-  delta[(b * nh + h) * s + q] = acc;
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+  if (valid && sub == 0) {
+    const int64_t b = row / s, q = row % s;
+    delta[(b * nh + h) * s + q] = acc;
+  }
 }
 
 // dQ[row, col] = sum over key tiles j (j <= row's query tile if causal) of dq_part[j][row][col]
@@ -456,7 +469,7 @@ extern "C" int smpk_flash_attn_bwd(const void* qkv, int64_t ld, const void* out,
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   {
     const int64_t total = (int64_t)B * s * nh;
-    flash_delta_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
+    flash_delta_kernel<<<(unsigned)((total * 8 + 255) / 256), 256, 0, st>>>(
         reinterpret_cast<const bf16*>(out), ld_out, reinterpret_cast<const bf16*>(dout), ld_dout, B, nh, s, dh,
         delta);
     int rc = check_launch("smpk_flash_attn_bwd(delta)");
