@@ -134,11 +134,12 @@ SMPK_API int smpk_colsum_partials(const float* part, int P, int N, void* out, in
  * gamma == NULL no LayerNorm is applied (only r is produced); with r_out == NULL
  * r is not stored.  x, r_out, y_out: [M, H]; mean/rstd: fp32 [M].  Dropout keeps
  * element (row, col) per Philox4x32-10 with counter (col>>2, row_offset+row,
- * layer, site) and key `seed` (oracle/philox.py).  H must be a multiple of 256.
+ * layer, site) and key `seed + *rng_step * 0x9E3779B97F4A7C15` (oracle/philox.py step_key;
+ * rng_step may be null = step 0; it is the per-forward snapshot written by smpk_rng_next).  H must be a multiple of 256.
  */
 SMPK_API int smpk_bdr_ln_fwd(const void* x, const void* bias, const void* residual, void* r_out,
                              const void* gamma, const void* beta, void* y_out, float* mean, float* rstd,
-                             int M, int H, float eps, float p_drop, uint64_t seed, int layer, int site,
+                             int M, int H, float eps, float p_drop, uint64_t seed, const uint64_t* rng_step, int layer, int site,
                              int64_t row_offset, void* stream);
 
 /*
@@ -153,7 +154,7 @@ SMPK_API int smpk_bdr_ln_fwd(const void* x, const void* bias, const void* residu
 SMPK_API int64_t smpk_ln_bwd_workspace(int M, int H);
 SMPK_API int smpk_ln_bwd(const void* dy, const void* r, const float* mean, const float* rstd, const void* gamma,
                          const void* dres, void* dr_out, void* dsub_out, void* dgamma, void* dbeta, void* dbias,
-                         int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed, int layer,
+                         int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed, const uint64_t* rng_step, int layer,
                          int site, int64_t row_offset, void* workspace, int64_t workspace_bytes, void* stream);
 
 /*
@@ -168,10 +169,10 @@ SMPK_API int smpk_ln_bwd(const void* dy, const void* r, const float* mean, const
  * ((sample_offset + b) * nh_global + head_offset + h) * sq + q, site 0.
  */
 SMPK_API int smpk_softmax_fwd(const void* scores, void* probs, void* probs_drop, const float* mask_add, int B,
-                              int nh, int sq, int sk, float scale, int causal, float p_drop, uint64_t seed,
+                              int nh, int sq, int sk, float scale, int causal, float p_drop, uint64_t seed, const uint64_t* rng_step,
                               int layer, int64_t sample_offset, int head_offset, int nh_global, void* stream);
 SMPK_API int smpk_softmax_bwd(const void* probs, const void* dprobs_drop, void* dscores, int B, int nh, int sq,
-                              int sk, float scale, float p_drop, uint64_t seed, int layer, int64_t sample_offset,
+                              int sk, float scale, float p_drop, uint64_t seed, const uint64_t* rng_step, int layer, int64_t sample_offset,
                               int head_offset, int nh_global, void* stream);
 
 /* smpk_colsum — out[n] (+)= sum_m x[m, n] (bias gradients), deterministic. */
@@ -241,7 +242,7 @@ SMPK_API int smpk_flash_attn_fwd(const void* qkv, int64_t ld, int B, int nh, int
  * stream (site 0, row = ((sample_offset+b)*nh_global + head_offset+h)*sq + q, col = k) that
  * oracle/philox.py restates.  Generated once per layer and read by the forward and backward.
  */
-SMPK_API int smpk_attn_dropout_bits(int B, int nh, int sq, int sk, float p_drop, uint64_t seed, int layer,
+SMPK_API int smpk_attn_dropout_bits(int B, int nh, int sq, int sk, float p_drop, uint64_t seed, const uint64_t* rng_step, int layer,
                                     int64_t sample_offset, int head_offset, int nh_global, uint32_t* bits,
                                     void* stream);
 
@@ -279,8 +280,11 @@ SMPK_API int smpk_flash_attn_bwd(const void* qkv, int64_t ld, const void* out, i
  *   smpk_symm_export    IPC handle + offset of a pointer inside its allocation
  *   smpk_symm_barrier   epoch barrier over the group (system-scope release/acquire flag words);
  *                       the epoch counter is device-resident (local_flags[32]) so a barrier
- *                       captured in a CUDA graph advances on every replay; times out after
- *                       timeout_s; smpk_symm_timeout_peer reports 1 + the stuck peer
+ *                       captured in a CUDA graph advances on every replay.  After timeout_s
+ *                       without a peer's signal the kernel records 1 + that peer in pinned
+ *                       mapped host memory and traps (a sticky CUDA error: no stale peer data is
+ *                       ever consumed); smpk_symm_timeout_peer reads the record without a CUDA
+ *                       call, so the host can raise PEER_TIMEOUT naming the stuck peer
  */
 SMPK_API int smpk_gemm_rs(const void* a, int a_mn_major, int64_t lda, const void* b, int b_mn_major, int64_t ldb,
                           void* const* peers, int npeers, int64_t ldc, int64_t rows_per_owner,
@@ -288,12 +292,12 @@ SMPK_API int smpk_gemm_rs(const void* a, int a_mn_major, int64_t lda, const void
 SMPK_API int smpk_bdr_ln_fwd_ex(const void* x, int nslots, int64_t slot_stride, const void* bias, const void* residual,
                                 void* r_out, const void* gamma, const void* beta, void* y_out, float* mean,
                                 float* rstd, void* const* out_peers, int npeers, int64_t peer_off, int M, int H,
-                                float eps, float p_drop, uint64_t seed, int layer, int site, int64_t row_offset,
+                                float eps, float p_drop, uint64_t seed, const uint64_t* rng_step, int layer, int site, int64_t row_offset,
                                 void* keep_out, void* const* x_peers, int64_t x_peer_off, void* stream);
 SMPK_API int smpk_ln_bwd_ex(const void* dy, int nslots, int64_t slot_stride, const void* r, const float* mean,
                             const float* rstd, const void* gamma, const void* dres, void* dr_out, void* dsub_out,
                             void* const* out_peers, int npeers, int64_t peer_off, void* dgamma, void* dbeta,
-                            void* dbias, int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed,
+                            void* dbias, int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed, const uint64_t* rng_step,
                             int layer, int site, int64_t row_offset, const void* keep_in, void* const* dy_peers,
                             int64_t dy_peer_off, void* workspace, int64_t workspace_bytes, void* stream);
 /*
@@ -310,12 +314,12 @@ SMPK_API int smpk_ln_bwd_ex(const void* dy, int nslots, int64_t slot_stride, con
  */
 SMPK_API int smpk_bdr_ln_fwd_dist(const void* x, const void* bias, const void* residual, void* r_out,
                                   const void* gamma, const void* beta, void* y_out, float* mean, float* rstd, int M,
-                                  int H, float eps, float p_drop, uint64_t seed, int layer, int site,
+                                  int H, float eps, float p_drop, uint64_t seed, const uint64_t* rng_step, int layer, int site,
                                   int64_t row_offset, int64_t col_offset, float* row_sums_out, const float* ext_sums,
                                   int H_total, void* stream);
 SMPK_API int smpk_ln_bwd_dist(const void* dy, const void* r, const float* mean, const float* rstd, const void* gamma,
                               const void* dres, void* dr_out, void* dsub_out, void* dgamma, void* dbeta, void* dbias,
-                              int grads_f32, int M, int H, float p_drop, uint64_t seed, int layer, int site,
+                              int grads_f32, int M, int H, float p_drop, uint64_t seed, const uint64_t* rng_step, int layer, int site,
                               int64_t row_offset, int64_t col_offset, float* row_sums_out, const float* ext_sums,
                               int H_total, void* workspace, int64_t workspace_bytes, void* stream);
 /*
@@ -354,6 +358,15 @@ SMPK_API int smpk_p2p_send(void* peer_slot, const void* src, int64_t bytes, void
                            uint32_t wait_free, uint32_t seq, void* stream);
 SMPK_API int smpk_p2p_recv(void* dst, const void* local_slot, int64_t bytes, const void* local_ready,
                            void* peer_free, uint32_t seq, void* stream);
+
+
+/* Per-step dropout RNG (PAPER.md:818 dropout 0.1).  Every dropout-drawing
+ * call takes `const uint64_t* rng_step`: the Philox key is seed + (*rng_step) * 0x9E3779B97F4A7C15.
+ * smpk_rng_next copies the device counter into *snapshot and increments the counter, on `stream`
+ * (one tiny kernel: CUDA-graph capturable, so every replay of a captured training step draws new
+ * masks).  A forward passes its snapshot to every kernel it launches and its backward re-reads
+ * the same snapshot, so interleaved microbatches (pipeline schedules) stay consistent. */
+SMPK_API int smpk_rng_next(uint64_t* counter, uint64_t* snapshot, void* stream);
 
 #ifdef __cplusplus
 }

@@ -11,10 +11,13 @@ This package restates, on the CPU, the algorithms the GPU path must reproduce:
                 (SPEC.md:509).
 * ``philox``  — numpy Philox4x32-10 and the logical-coordinate dropout masks the
                 kernels draw (bit-exact).
-* ``mpsim_restated`` — plain-Python restatement of the reference's topology,
-                partition and scheduler rules used to pin the product's copies
-                (the reference itself is importable here and is used to generate
-                tests/golden/*.json by tests/golden/make_golden.py).
+* ``philox_grid.c`` — C restatement of the same masks (oracle/Makefile ->
+                libphilox_grid.so), so 24-layer oracle stacks draw their masks fast;
+                tests/test_philox.py checks it against the numpy version.
+The partition / topology / schedule rows need no restatement here: the reference
+itself is importable in this container and tests/golden/make_golden.py generates
+tests/golden/reference_golden.json from it, against which the product's vendored
+copies are checked bit-exactly.
 
 Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
 ``--impl reference`` leg may import this package.  The product path

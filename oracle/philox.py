@@ -28,6 +28,15 @@ W0 = np.uint32(0x9E3779B9)
 W1 = np.uint32(0xBB67AE85)
 MASK32 = np.uint64(0xFFFFFFFF)
 
+GOLDEN64 = 0x9E3779B97F4A7C15
+
+
+def step_key(seed: int, step: int) -> int:
+    """Philox key of training step `step` (csrc/smpk_common.cuh philox_key): the device-resident
+    step word snapshotted per top-level forward is folded into the 64-bit key."""
+    return (int(seed) + int(step) * GOLDEN64) % (1 << 64)
+
+
 SITE_ATTN_PROB = 0
 SITE_ATTN_OUT = 1
 SITE_MLP_OUT = 2
@@ -77,8 +86,43 @@ def keep_mask(rows, cols, layer: int, site: int, seed: int, p: float) -> np.ndar
     return uniform16(rows, cols, layer, site, seed) >= np.uint32(threshold(p))
 
 
+_CLIB = None
+
+
+def _clib():
+    """oracle/libphilox_grid.so (oracle/philox_grid.c, built by oracle/Makefile), or None."""
+    global _CLIB
+    if _CLIB is None:
+        import ctypes
+        import os
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libphilox_grid.so")
+        _CLIB = False
+        if os.path.exists(path):
+            lib = ctypes.CDLL(path)
+            lib.philox_keep_grid.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_uint32,
+                                             ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p]
+            lib.philox_keep_grid.restype = None
+            _CLIB = lib
+    return _CLIB or None
+
+
+def keep_grid(rows, n_cols: int, layer: int, site: int, seed: int, p: float, use_c: bool = True) -> np.ndarray:
+    """[len(rows), n_cols] keep mask of logical rows `rows` x columns 0..n_cols-1 (the C
+    restatement when built, else numpy; tests/test_philox.py checks they agree)."""
+    r = np.ascontiguousarray(np.asarray(rows, dtype=np.int64).reshape(-1))
+    lib = _clib() if use_c else None
+    if lib is None:
+        return keep_mask(r[:, None], np.arange(n_cols, dtype=np.int64)[None, :], layer, site, seed, p)
+    out = np.empty((r.size, n_cols), dtype=np.uint8)
+    lib.philox_keep_grid(r.ctypes.data, r.size, int(n_cols), int(layer) & 0xFFFFFFFF, int(site) & 0xFFFFFFFF,
+                         int(seed) % (1 << 64), threshold(p), out.ctypes.data)
+    return out.astype(bool)
+
+
 def hidden_mask(global_rows: np.ndarray, n_cols: int, layer: int, site: int, seed: int, p: float) -> np.ndarray:
     """[len(rows), n_cols] keep mask for a hidden-dropout site."""
+    if _clib() is not None:
+        return keep_grid(global_rows, n_cols, layer, site, seed, p)
     r = np.asarray(global_rows, dtype=np.int64)[:, None]
     c = np.arange(n_cols, dtype=np.int64)[None, :]
     return keep_mask(r, c, layer, site, seed, p)
@@ -92,4 +136,6 @@ def attn_prob_mask(global_samples, global_heads, s_q: int, s_k: int, nh_global: 
     q = np.arange(s_q, dtype=np.int64)[None, None, :, None]
     k = np.arange(s_k, dtype=np.int64)[None, None, None, :]
     rows = (gs * nh_global + gh) * s_q + q
+    if _clib() is not None:
+        return keep_grid(rows, s_k, layer, SITE_ATTN_PROB, seed, p).reshape(rows.shape[:3] + (s_k,))
     return keep_mask(rows, k, layer, SITE_ATTN_PROB, seed, p)

@@ -70,6 +70,7 @@ class DropoutCtx:
     seed: int = 0
     layer: int = 0
     sample_offset: int = 0  # global id of sample 0 of the tensor the op sees
+    step: int = 0  # training step (device step word snapshot); key = philox.step_key(seed, step)
     # timing-only mode (bench.py CPU baseline): draw masks with torch's CPU RNG instead
     # of the bit-exact numpy Philox, which would dominate a CPU timing
     torch_rng: bool = False
@@ -445,7 +446,7 @@ def attention_core(q, k, v, mask_add, causal, dctx: DropoutCtx | None, p_attn: f
         probs = probs * (torch.rand(probs.shape, dtype=probs.dtype) >= p_attn) / (1.0 - p_attn)
     elif dctx is not None and p_attn > 0:
         keep = philox.attn_prob_mask(np.arange(B) + dctx.sample_offset, np.arange(nh) + head_offset,
-                                     s, s, nh_global, dctx.layer, dctx.seed, p_attn)
+                                     s, s, nh_global, dctx.layer, philox.step_key(dctx.seed, dctx.step), p_attn)
         probs = _dropout(probs, keep, p_attn)
     ctx = probs @ vh
     return ctx.permute(0, 2, 1, 3).reshape(B, s, nh * dh)
@@ -458,7 +459,7 @@ def _hidden_keep(dctx, B, s, H, site, p, col_offset=0, n_cols=None):
         return (torch.rand(B, s, n_cols if n_cols is not None else H) >= p).numpy()
     rows = np.arange(B * s) + dctx.sample_offset * s
     cols = np.arange(n_cols if n_cols is not None else H) + col_offset
-    keep = philox.keep_mask(rows[:, None], cols[None, :], dctx.layer, site, dctx.seed, p)
+    keep = philox.keep_mask(rows[:, None], cols[None, :], dctx.layer, site, philox.step_key(dctx.seed, dctx.step), p)
     return keep.reshape(B, s, -1)
 
 

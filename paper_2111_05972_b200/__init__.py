@@ -19,8 +19,8 @@ from .collectives import (bwd_allreduce_for_tp, fused_allgather_for_tp, fwd_allr
                           reduce_scatter_for_tp, scatter_and_merge_for_tp)
 from .errors import (IndexOutOfRangeError, NotDivisibleError, ShapeMismatchError,  # noqa: E402
                      TensorParallelError, TopologyError)
-from .state import (STATE, dp_rank, init, pp_rank, pp_size, rank, rdp_rank, reset, size, tp_rank,  # noqa: E402
-                    tp_size)
+from .state import (STATE, dp_rank, init, pp_rank, pp_size, rank, rdp_rank, reset, rng_step, set_rng_step, size,  # noqa: E402
+                    tp_rank, tp_size)
 from .topology import Topology, build_topology  # noqa: E402
 from .replace import (DistributedModel, plan_replacement, set_tensor_parallelism, tensor_parallelism,  # noqa: E402
                       tp_register, tp_register_with_module)

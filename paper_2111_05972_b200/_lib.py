@@ -30,10 +30,10 @@ SIGNATURES: dict[str, list] = {
     "smpk_gemm_ex": [P, I, L, L, L, P, I, L, L, L, P, I, L, L, L, I, I, I, I, I, F, F, I, I, P, P, L, P, L, P],
     "smpk_gemm_ex2": [P, I, L, L, L, P, I, L, L, L, P, I, L, L, L, I, I, I, I, I, F, F, I, I, P, P, L, P, L, P, P],
     "smpk_colsum_partials": [P, I, I, P, I, P],
-    "smpk_bdr_ln_fwd": [P, P, P, P, P, P, P, P, P, I, I, F, F, C.c_uint64, I, I, L, P],
-    "smpk_ln_bwd": [P, P, P, P, P, P, P, P, P, P, P, I, I, I, I, F, C.c_uint64, I, I, L, P, L, P],
-    "smpk_softmax_fwd": [P, P, P, P, I, I, I, I, F, I, F, C.c_uint64, I, L, I, I, P],
-    "smpk_softmax_bwd": [P, P, P, I, I, I, I, F, F, C.c_uint64, I, L, I, I, P],
+    "smpk_bdr_ln_fwd": [P, P, P, P, P, P, P, P, P, I, I, F, F, C.c_uint64, P, I, I, L, P],
+    "smpk_ln_bwd": [P, P, P, P, P, P, P, P, P, P, P, I, I, I, I, F, C.c_uint64, P, I, I, L, P, L, P],
+    "smpk_softmax_fwd": [P, P, P, P, I, I, I, I, F, I, F, C.c_uint64, P, I, L, I, I, P],
+    "smpk_softmax_bwd": [P, P, P, I, I, I, I, F, F, C.c_uint64, P, I, L, I, I, P],
     "smpk_colsum": [P, I, I, L, P, I, I, P, L, P],
     "smpk_embed_fwd": [P, L, P, L, L, L, L, I, P, L, P, L, I, P, P],
     "smpk_embed_bwd": [P, L, P, L, L, L, I, P, L, I, I, L, P],
@@ -41,16 +41,17 @@ SIGNATURES: dict[str, list] = {
     "smpk_vocab_ce_combine": [P, I, L, P, L, P, P, P],
     "smpk_vocab_ce_bwd": [P, L, L, I, L, L, P, L, P, P, F, P, L, P],
     "smpk_flash_attn_fwd": [P, L, I, I, I, I, P, L, P, P, F, I, F, P, P],
-    "smpk_attn_dropout_bits": [I, I, I, I, F, C.c_uint64, I, L, I, I, P, P],
+    "smpk_attn_dropout_bits": [I, I, I, I, F, C.c_uint64, P, I, L, I, I, P, P],
     "smpk_flash_attn_bwd": [P, L, P, L, P, L, P, I, I, I, I, P, P, F, I, F, P, P, L, P],
     "smpk_gemm_rs": [P, I, L, P, I, L, P, I, L, L, L, I, I, I, P],
-    "smpk_bdr_ln_fwd_ex": [P, I, L, P, P, P, P, P, P, P, P, P, I, L, I, I, F, F, C.c_uint64, I, I, L, P, P, L, P],
-    "smpk_bdr_ln_fwd_dist": [P, P, P, P, P, P, P, P, P, I, I, F, F, C.c_uint64, I, I, L, L, P, P, I, P],
-    "smpk_ln_bwd_dist": [P, P, P, P, P, P, P, P, P, P, P, I, I, I, F, C.c_uint64, I, I, L, L, P, P, I, P, L, P],
+    "smpk_bdr_ln_fwd_ex": [P, I, L, P, P, P, P, P, P, P, P, P, I, L, I, I, F, F, C.c_uint64, P, I, I, L, P, P, L, P],
+    "smpk_bdr_ln_fwd_dist": [P, P, P, P, P, P, P, P, P, I, I, F, F, C.c_uint64, P, I, I, L, L, P, P, I, P],
+    "smpk_ln_bwd_dist": [P, P, P, P, P, P, P, P, P, P, P, I, I, I, F, C.c_uint64, P, I, I, L, L, P, P, I, P, L, P],
     "smpk_bias_act_fwd": [P, P, I, I, I, P, P, P],
     "smpk_act_bwd": [P, P, I, I, I, P, P],
     "smpk_copy_async": [P, P, L, P],
-    "smpk_ln_bwd_ex": [P, I, L, P, P, P, P, P, P, P, P, I, L, P, P, P, I, I, I, I, F, C.c_uint64, I, I, L, P, P, L, P,
+    "smpk_rng_next": [P, P, P],
+    "smpk_ln_bwd_ex": [P, I, L, P, P, P, P, P, P, P, P, I, L, P, P, P, I, I, I, I, F, C.c_uint64, P, I, I, L, P, P, L, P,
                        L, P],
     "smpk_symm_export": [P, P, C.POINTER(L)],
     "smpk_symm_barrier": [P, P, I, I, C.c_double, P],

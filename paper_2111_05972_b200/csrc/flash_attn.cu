@@ -338,11 +338,13 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
 // col = k) with gs = sample_offset + b, gh = head_offset + h.  One thread per word
 // (4 Philox4x32-10 calls = 32 keys).
 __global__ void __launch_bounds__(128) attn_dropout_bits_kernel(int nh, int sq, int wpr, uint32_t thresh,
-                                                                uint64_t seed, uint32_t layer,
+                                                                uint64_t seed, const uint64_t* rng_step,
+                                                                uint32_t layer,
                                                                 int64_t sample_offset, int head_offset, int nh_global,
                                                                 uint32_t* __restrict__ bits) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // (q, w) of this (b, h)
   if (idx >= sq * wpr) return;
+  const uint64_t pkey = philox_key(seed, rng_step);
   const int bh = blockIdx.y;
   const int q = idx / wpr, w = idx - q * wpr;
   const int h = bh % nh, b = bh / nh;
@@ -351,7 +353,7 @@ __global__ void __launch_bounds__(128) attn_dropout_bits_kernel(int nh, int sq, 
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     bool k8[8];
-    dropout_keep8(seed, layer, 0u, grow, w * 32 + c * 8, thresh, k8);
+    dropout_keep8(pkey, layer, 0u, grow, w * 32 + c * 8, thresh, k8);
 #pragma unroll
     for (int e = 0; e < 8; ++e) word |= (k8[e] ? 1u : 0u) << (c * 8 + e);
   }
@@ -362,7 +364,8 @@ __global__ void __launch_bounds__(128) attn_dropout_bits_kernel(int nh, int sq, 
 
 using namespace smpk;
 
-extern "C" int smpk_attn_dropout_bits(int B, int nh, int sq, int sk, float p_drop, uint64_t seed, int layer,
+extern "C" int smpk_attn_dropout_bits(int B, int nh, int sq, int sk, float p_drop, uint64_t seed,
+                                      const uint64_t* rng_step, int layer,
                                       int64_t sample_offset, int head_offset, int nh_global, uint32_t* bits,
                                       void* stream) {
   SMPK_REQUIRE(B > 0 && nh > 0 && sq > 0 && sk > 0 && sk % 32 == 0 && bits, SMPK_ERR_BAD_ARG,
@@ -372,7 +375,7 @@ extern "C" int smpk_attn_dropout_bits(int B, int nh, int sq, int sk, float p_dro
   const int wpr = sk / 32;
   dim3 grid((unsigned)((sq * wpr + 127) / 128), (unsigned)(B * nh));
   attn_dropout_bits_kernel<<<grid, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      nh, sq, wpr, dropout_threshold(p_drop), seed, (uint32_t)layer, sample_offset, head_offset, nh_global, bits);
+      nh, sq, wpr, dropout_threshold(p_drop), seed, rng_step, (uint32_t)layer, sample_offset, head_offset, nh_global, bits);
   return check_launch("smpk_attn_dropout_bits");
 }
 

@@ -189,6 +189,7 @@ struct BdrLnArgs {
   // x read as the ascending-rank sum over the nslots peers' buffers x_peers[j] + x_peer_off
   const bf16* const* x_peers;
   int64_t x_peer_off;
+  const uint64_t* rng_step = nullptr;  // device step word: Philox key = seed + step * golden (may be null)
 };
 
 __device__ __forceinline__ void load8_slots(const bf16* p, int nslots, int64_t stride, float (&v)[8]) {
@@ -226,6 +227,7 @@ __device__ __forceinline__ void store8_peers(bf16* const* peers, int npeers, int
 
 template <int W, int VPT>
 __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs a) {
+  const uint64_t pkey = philox_key(a.seed, a.rng_step);
   __shared__ float sm[2 * 8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = warp / W, wi = warp % W;
@@ -281,7 +283,7 @@ __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs
         }
         if (a.p > 0.f) {
           bool keep[8];
-          dropout_keep8(a.seed, a.layer, a.site, (uint64_t)(a.row_offset + row), (int)(a.col_offset + col),
+          dropout_keep8(pkey, a.layer, a.site, (uint64_t)(a.row_offset + row), (int)(a.col_offset + col),
                         dropout_threshold(a.p), keep);
           if (a.keep_out) a.keep_out[(int64_t)row * (a.H / 8) + col / 8] = (uint8_t)keep8_to_byte(keep);
 #pragma unroll
@@ -393,6 +395,7 @@ struct LnBwdArgs {
   const uint8_t* keep_in;  // [M][H/8] keep bytes saved by the forward (null: recompute Philox)
   const bf16* const* dy_peers;  // dy = ascending-rank sum over dy_peers[j] + dy_peer_off (pull)
   int64_t dy_peer_off;
+  const uint64_t* rng_step = nullptr;
 };
 
 template <int W, int VPT>
@@ -433,6 +436,7 @@ __device__ __forceinline__ void flush_partial(const float (&acc)[VPT][8], float*
 
 template <int W, int VPT>
 __global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const LnBwdArgs a) {
+  const uint64_t pkey = philox_key(a.seed, a.rng_step);
   __shared__ float sm[2 * 8];
   extern __shared__ float red[];  // [W][VPT*8][32] slot reduction buffer
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -546,7 +550,7 @@ __global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const LnBwdArgs a) 
         if (a.keep_in)
           keep8_from_byte(keep_raw[i], keep);
         else
-          dropout_keep8(a.seed, a.layer, a.site, (uint64_t)(a.row_offset + row), (int)(a.col_offset + col),
+          dropout_keep8(pkey, a.layer, a.site, (uint64_t)(a.row_offset + row), (int)(a.col_offset + col),
                         dropout_threshold(a.p), keep);
 #pragma unroll
         for (int j = 0; j < 8; ++j) d[j] = keep[j] ? d[j] * inv_keep : 0.f;
@@ -641,6 +645,7 @@ struct SoftmaxArgs {
   uint32_t layer;
   int64_t sample_offset;
   int head_offset, nh_global;
+  const uint64_t* rng_step = nullptr;
 };
 
 __device__ __forceinline__ uint64_t attn_logical_row(const SoftmaxArgs& a, int64_t row) {
@@ -653,6 +658,7 @@ __device__ __forceinline__ uint64_t attn_logical_row(const SoftmaxArgs& a, int64
 
 template <int NV>
 __global__ void __launch_bounds__(ROW_THREADS) softmax_fwd_kernel(const SoftmaxArgs a) {
+  const uint64_t pkey = philox_key(a.seed, a.rng_step);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t rows = (int64_t)a.B * a.nh * a.sq;
   const float inv_keep = a.p > 0.f ? 1.f / (1.f - a.p) : 1.f;
@@ -708,7 +714,7 @@ __global__ void __launch_bounds__(ROW_THREADS) softmax_fwd_kernel(const SoftmaxA
         store8(a.p_out + row * a.sk + col, v[i]);
         if (a.p > 0.f) {
           bool keep[8];
-          dropout_keep8(a.seed, a.layer, 0u, g, col, dropout_threshold(a.p), keep);
+          dropout_keep8(pkey, a.layer, 0u, g, col, dropout_threshold(a.p), keep);
           float o[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) o[j] = keep[j] ? round_bf16(v[i][j]) * inv_keep : 0.f;
@@ -721,6 +727,7 @@ __global__ void __launch_bounds__(ROW_THREADS) softmax_fwd_kernel(const SoftmaxA
 
 template <int NV>
 __global__ void __launch_bounds__(ROW_THREADS) softmax_bwd_kernel(const SoftmaxArgs a) {
+  const uint64_t pkey = philox_key(a.seed, a.rng_step);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t rows = (int64_t)a.B * a.nh * a.sq;
   const float inv_keep = a.p > 0.f ? 1.f / (1.f - a.p) : 1.f;
@@ -736,7 +743,7 @@ __global__ void __launch_bounds__(ROW_THREADS) softmax_bwd_kernel(const SoftmaxA
         load8(a.d + row * a.sk + col, dv[i]);
         bool keep[8];
         if (a.p > 0.f) {
-          dropout_keep8(a.seed, a.layer, 0u, g, col, dropout_threshold(a.p), keep);
+          dropout_keep8(pkey, a.layer, 0u, g, col, dropout_threshold(a.p), keep);
         } else {
 #pragma unroll
           for (int j = 0; j < 8; ++j) keep[j] = true;
@@ -845,6 +852,7 @@ struct BdrPipeArgs {
   int npeers;
   int64_t peer_off;
   int nst;  // ring stages
+  const uint64_t* rng_step = nullptr;
 };
 
 __device__ __forceinline__ void bulk_store_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
@@ -855,6 +863,7 @@ __device__ __forceinline__ void bulk_store_s2g(void* gdst, const void* ssrc, uin
 
 template <int CH>
 __global__ void __launch_bounds__(32 * (PIPE_CW + 1), 1) bdr_ln_pipe_kernel(const BdrPipeArgs a) {
+  const uint64_t pkey = philox_key(a.seed, a.rng_step);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   const int H = a.H;
@@ -925,7 +934,7 @@ __global__ void __launch_bounds__(32 * (PIPE_CW + 1), 1) bdr_ln_pipe_kernel(cons
       }
       if (a.p > 0.f) {
         bool keep[8];
-        dropout_keep8(a.seed, a.layer, a.site, (uint64_t)(a.row_offset + row), col, thresh, keep);
+        dropout_keep8(pkey, a.layer, a.site, (uint64_t)(a.row_offset + row), col, thresh, keep);
         if (a.keep_out) a.keep_out[(int64_t)row * (H / 8) + col / 8] = (uint8_t)keep8_to_byte(keep);
 #pragma unroll
         for (int e = 0; e < 8; ++e) v[k][e] = keep[e] ? v[k][e] * inv_keep : 0.f;
@@ -1044,9 +1053,9 @@ static bool pipe_enabled() {
 static int bdr_ln_impl(const void* x, int nslots, int64_t slot_stride, const void* bias, const void* residual,
                        void* r_out, const void* gamma, const void* beta, void* y_out, float* mean, float* rstd,
                        void* const* out_peers, int npeers, int64_t peer_off, int M, int H, float eps, float p_drop,
-                       uint64_t seed, int layer, int site, int64_t row_offset, int64_t col_offset,
-                       float* row_sums_out, const float* ext_sums, int H_total, uint8_t* keep_out,
-                       void* const* x_peers, int64_t x_peer_off, void* stream) {
+                       uint64_t seed, const uint64_t* rng_step, int layer, int site, int64_t row_offset,
+                       int64_t col_offset, float* row_sums_out, const float* ext_sums, int H_total,
+                       uint8_t* keep_out, void* const* x_peers, int64_t x_peer_off, void* stream) {
   RowGeom geo;
   SMPK_REQUIRE(M >= 0 && row_geom(H, geo) && geom_supported(geo), SMPK_ERR_UNSUPPORTED,
                "smpk_bdr_ln_fwd: hidden size %d unsupported (need a multiple of 8)", H);
@@ -1067,6 +1076,7 @@ static int bdr_ln_impl(const void* x, int nslots, int64_t slot_stride, const voi
               row_offset, nslots, slot_stride, reinterpret_cast<bf16* const*>(out_peers), npeers, peer_off,
               col_offset, row_sums_out, ext_sums, H_total, keep_out, reinterpret_cast<const bf16* const*>(x_peers),
               x_peer_off};
+  a.rng_step = rng_step;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   // pipelined path for the TP exchanges (partials pulled from peers and/or output pushed to peers:
   // bulk copies keep enough NVLink traffic in flight); whole 16-B aligned rows, <= 2048 columns.
@@ -1084,11 +1094,16 @@ static int bdr_ln_impl(const void* x, int nslots, int64_t slot_stride, const voi
                    reinterpret_cast<const bf16*>(beta), reinterpret_cast<bf16*>(y_out), mean, rstd, M, H, eps,
                    p_drop, seed, (uint32_t)layer, (uint32_t)site, row_offset, keep_out,
                    reinterpret_cast<bf16* const*>(out_peers), npeers, peer_off, 0};
+  pa.rng_step = rng_step;
     const int nin = nslots + (residual ? 1 : 0);
     const int budget = 200 * 1024 - 3 * H * 2;
     const int nst = budget / (nin * H * 2);
-    pa.nst = nst > 16 ? 16 : nst;
-    if (pa.nst >= 2) return bdr_ln_pipe_launch(pa, st);
+    // consumer warp c owns the iterations it == c (mod PIPE_CW) and reads stage it % nst: with nst a
+    // multiple of PIPE_CW every stage has exactly one owning warp, so a warp can never wait on a
+    // stage phase that another warp's row is still filling or reading (nst = 5 / 9 / 10
+    // aliased stages across warps).  Fewer than PIPE_CW stages fit: use the register kernel.
+    pa.nst = ((nst > 16 ? 16 : nst) / PIPE_CW) * PIPE_CW;
+    if (pa.nst >= PIPE_CW) return bdr_ln_pipe_launch(pa, st);
   }
   // 80 registers with the next-row prefetch: 3 resident CTAs per SM, one wave
   const int grid = row_grid(M, geo.W, 3);
@@ -1099,29 +1114,29 @@ static int bdr_ln_impl(const void* x, int nslots, int64_t slot_stride, const voi
 extern "C" int smpk_bdr_ln_fwd_ex(const void* x, int nslots, int64_t slot_stride, const void* bias,
                                   const void* residual, void* r_out, const void* gamma, const void* beta, void* y_out,
                                   float* mean, float* rstd, void* const* out_peers, int npeers, int64_t peer_off, int M,
-                                  int H, float eps, float p_drop, uint64_t seed, int layer, int site,
+                                  int H, float eps, float p_drop, uint64_t seed, const uint64_t* rng_step, int layer, int site,
                                   int64_t row_offset, void* keep_out, void* const* x_peers, int64_t x_peer_off,
                                   void* stream) {
   return bdr_ln_impl(x, nslots, slot_stride, bias, residual, r_out, gamma, beta, y_out, mean, rstd, out_peers, npeers,
-                     peer_off, M, H, eps, p_drop, seed, layer, site, row_offset, 0, nullptr, nullptr, 0,
+                     peer_off, M, H, eps, p_drop, seed, rng_step, layer, site, row_offset, 0, nullptr, nullptr, 0,
                      reinterpret_cast<uint8_t*>(keep_out), x_peers, x_peer_off, stream);
 }
 
 extern "C" int smpk_bdr_ln_fwd_dist(const void* x, const void* bias, const void* residual, void* r_out,
                                     const void* gamma, const void* beta, void* y_out, float* mean, float* rstd,
-                                    int M, int H, float eps, float p_drop, uint64_t seed, int layer, int site,
+                                    int M, int H, float eps, float p_drop, uint64_t seed, const uint64_t* rng_step, int layer, int site,
                                     int64_t row_offset, int64_t col_offset, float* row_sums_out,
                                     const float* ext_sums, int H_total, void* stream) {
   return bdr_ln_impl(x, 1, 0, bias, residual, r_out, gamma, beta, y_out, mean, rstd, nullptr, 0, 0, M, H, eps, p_drop,
-                     seed, layer, site, row_offset, col_offset, row_sums_out, ext_sums, H_total, nullptr, nullptr, 0,
+                     seed, rng_step, layer, site, row_offset, col_offset, row_sums_out, ext_sums, H_total, nullptr, nullptr, 0,
                      stream);
 }
 
 extern "C" int smpk_bdr_ln_fwd(const void* x, const void* bias, const void* residual, void* r_out, const void* gamma,
                                const void* beta, void* y_out, float* mean, float* rstd, int M, int H, float eps,
-                               float p_drop, uint64_t seed, int layer, int site, int64_t row_offset, void* stream) {
+                               float p_drop, uint64_t seed, const uint64_t* rng_step, int layer, int site, int64_t row_offset, void* stream) {
   return smpk_bdr_ln_fwd_ex(x, 1, 0, bias, residual, r_out, gamma, beta, y_out, mean, rstd, nullptr, 0, 0, M, H, eps,
-                            p_drop, seed, layer, site, row_offset, nullptr, nullptr, 0, stream);
+                            p_drop, seed, rng_step, layer, site, row_offset, nullptr, nullptr, 0, stream);
 }
 
 // The backward keeps per-column accumulators in registers (two CTAs per SM): one wave of
@@ -1144,7 +1159,7 @@ extern "C" int64_t smpk_ln_bwd_workspace(int M, int H) { return ln_bwd_grid(M, H
 static int ln_bwd_impl(const void* dy, int nslots, int64_t slot_stride, const void* r, const float* mean,
                        const float* rstd, const void* gamma, const void* dres, void* dr_out, void* dsub_out,
                        void* const* out_peers, int npeers, int64_t peer_off, void* dgamma, void* dbeta, void* dbias,
-                       int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed, int layer, int site,
+                       int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed, const uint64_t* rng_step, int layer, int site,
                        int64_t row_offset, int64_t col_offset, float* row_sums_out, const float* ext_sums,
                        int H_total, const uint8_t* keep_in, void* const* dy_peers, int64_t dy_peer_off,
                        void* workspace, int64_t workspace_bytes, void* stream) {
@@ -1170,6 +1185,7 @@ static int ln_bwd_impl(const void* dy, int nslots, int64_t slot_stride, const vo
               reinterpret_cast<float*>(workspace), M, H, p_drop, seed, (uint32_t)layer, (uint32_t)site, row_offset,
               nslots, slot_stride, reinterpret_cast<bf16* const*>(out_peers), npeers, peer_off, col_offset,
               row_sums_out, ext_sums, H_total, keep_in, reinterpret_cast<const bf16* const*>(dy_peers), dy_peer_off};
+  a.rng_step = rng_step;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int red_bytes = geo.W == 8 ? 0 : geo.W * geo.VPT * 8 * 32 * 4;
   SMPK_DISPATCH_ROW(geo.W, geo.VPT, ln_bwd_kernel, (grid, ROW_THREADS, red_bytes, st), (a));
@@ -1185,32 +1201,32 @@ static int ln_bwd_impl(const void* dy, int nslots, int64_t slot_stride, const vo
 extern "C" int smpk_ln_bwd_ex(const void* dy, int nslots, int64_t slot_stride, const void* r, const float* mean,
                               const float* rstd, const void* gamma, const void* dres, void* dr_out, void* dsub_out,
                               void* const* out_peers, int npeers, int64_t peer_off, void* dgamma, void* dbeta,
-                              void* dbias, int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed,
+                              void* dbias, int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed, const uint64_t* rng_step,
                               int layer, int site, int64_t row_offset, const void* keep_in, void* const* dy_peers,
                               int64_t dy_peer_off, void* workspace, int64_t workspace_bytes, void* stream) {
   return ln_bwd_impl(dy, nslots, slot_stride, r, mean, rstd, gamma, dres, dr_out, dsub_out, out_peers, npeers,
-                     peer_off, dgamma, dbeta, dbias, grads_f32, accumulate, M, H, p_drop, seed, layer, site,
+                     peer_off, dgamma, dbeta, dbias, grads_f32, accumulate, M, H, p_drop, seed, rng_step, layer, site,
                      row_offset, 0, nullptr, nullptr, 0, reinterpret_cast<const uint8_t*>(keep_in), dy_peers,
                      dy_peer_off, workspace, workspace_bytes, stream);
 }
 
 extern "C" int smpk_ln_bwd_dist(const void* dy, const void* r, const float* mean, const float* rstd,
                                 const void* gamma, const void* dres, void* dr_out, void* dsub_out, void* dgamma,
-                                void* dbeta, void* dbias, int grads_f32, int M, int H, float p_drop, uint64_t seed,
+                                void* dbeta, void* dbias, int grads_f32, int M, int H, float p_drop, uint64_t seed, const uint64_t* rng_step,
                                 int layer, int site, int64_t row_offset, int64_t col_offset, float* row_sums_out,
                                 const float* ext_sums, int H_total, void* workspace, int64_t workspace_bytes,
                                 void* stream) {
   return ln_bwd_impl(dy, 1, 0, r, mean, rstd, gamma, dres, dr_out, dsub_out, nullptr, 0, 0, dgamma, dbeta, dbias,
-                     grads_f32, 0, M, H, p_drop, seed, layer, site, row_offset, col_offset, row_sums_out, ext_sums,
+                     grads_f32, 0, M, H, p_drop, seed, rng_step, layer, site, row_offset, col_offset, row_sums_out, ext_sums,
                      H_total, nullptr, nullptr, 0, workspace, workspace_bytes, stream);
 }
 
 extern "C" int smpk_ln_bwd(const void* dy, const void* r, const float* mean, const float* rstd, const void* gamma,
                            const void* dres, void* dr_out, void* dsub_out, void* dgamma, void* dbeta, void* dbias,
-                           int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed, int layer,
+                           int grads_f32, int accumulate, int M, int H, float p_drop, uint64_t seed, const uint64_t* rng_step, int layer,
                            int site, int64_t row_offset, void* workspace, int64_t workspace_bytes, void* stream) {
   return smpk_ln_bwd_ex(dy, 1, 0, r, mean, rstd, gamma, dres, dr_out, dsub_out, nullptr, 0, 0, dgamma, dbeta, dbias,
-                        grads_f32, accumulate, M, H, p_drop, seed, layer, site, row_offset, nullptr, nullptr, 0,
+                        grads_f32, accumulate, M, H, p_drop, seed, rng_step, layer, site, row_offset, nullptr, nullptr, 0,
                         workspace, workspace_bytes, stream);
 }
 
@@ -1397,7 +1413,7 @@ extern "C" int smpk_colsum(const void* x, int M, int N, int64_t ldx, void* out, 
   }
 
 extern "C" int smpk_softmax_fwd(const void* scores, void* probs, void* probs_drop, const float* mask_add, int B,
-                                int nh, int sq, int sk, float scale, int causal, float p_drop, uint64_t seed, int layer,
+                                int nh, int sq, int sk, float scale, int causal, float p_drop, uint64_t seed, const uint64_t* rng_step, int layer,
                                 int64_t sample_offset, int head_offset, int nh_global, void* stream) {
   const int nv = softmax_nv(sk);
   SMPK_REQUIRE(nv > 0 && sk % 8 == 0 && B > 0 && nh > 0 && sq > 0, SMPK_ERR_UNSUPPORTED,
@@ -1407,6 +1423,7 @@ extern "C" int smpk_softmax_fwd(const void* scores, void* probs, void* probs_dro
   SoftmaxArgs a{reinterpret_cast<const bf16*>(scores), nullptr, reinterpret_cast<bf16*>(probs),
                 reinterpret_cast<bf16*>(probs_drop), mask_add, B, nh, sq, sk, scale, p_drop, causal, seed,
                 (uint32_t)layer, sample_offset, head_offset, nh_global};
+  a.rng_step = rng_step;
   const int64_t rows = (int64_t)B * nh * sq;
   int64_t grid = (rows + 7) / 8;
   if (grid > row_sms() * 8) grid = row_sms() * 8;
@@ -1416,7 +1433,7 @@ extern "C" int smpk_softmax_fwd(const void* scores, void* probs, void* probs_dro
 }
 
 extern "C" int smpk_softmax_bwd(const void* probs, const void* dprobs_drop, void* dscores, int B, int nh, int sq,
-                                int sk, float scale, float p_drop, uint64_t seed, int layer, int64_t sample_offset,
+                                int sk, float scale, float p_drop, uint64_t seed, const uint64_t* rng_step, int layer, int64_t sample_offset,
                                 int head_offset, int nh_global, void* stream) {
   const int nv = softmax_nv(sk);
   SMPK_REQUIRE(nv > 0 && sk % 8 == 0, SMPK_ERR_UNSUPPORTED, "smpk_softmax_bwd: key length %d unsupported", sk);
@@ -1424,6 +1441,7 @@ extern "C" int smpk_softmax_bwd(const void* probs, const void* dprobs_drop, void
   SoftmaxArgs a{reinterpret_cast<const bf16*>(probs), reinterpret_cast<const bf16*>(dprobs_drop),
                 reinterpret_cast<bf16*>(dscores), nullptr, nullptr, B, nh, sq, sk, scale, p_drop, 0, seed,
                 (uint32_t)layer, sample_offset, head_offset, nh_global};
+  a.rng_step = rng_step;
   const int64_t rows = (int64_t)B * nh * sq;
   int64_t grid = (rows + 7) / 8;
   if (grid > row_sms() * 8) grid = row_sms() * 8;

@@ -73,3 +73,18 @@ extern "C" int smpk_device_info(int* nsm, int* cc_major, int* cc_minor) {
   if (cc_minor) cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
   return SMPK_OK;
 }
+
+namespace smpk {
+__global__ void rng_next_kernel(unsigned long long* counter, unsigned long long* snapshot) {
+  const unsigned long long v = *counter;
+  *snapshot = v;
+  *counter = v + 1ull;
+}
+}  // namespace smpk
+
+extern "C" int smpk_rng_next(uint64_t* counter, uint64_t* snapshot, void* stream) {
+  SMPK_REQUIRE(counter && snapshot, SMPK_ERR_BAD_ARG, "smpk_rng_next: null pointer");
+  smpk::rng_next_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<unsigned long long*>(counter), reinterpret_cast<unsigned long long*>(snapshot));
+  return smpk::check_launch("smpk_rng_next");
+}

@@ -400,6 +400,15 @@ __host__ __device__ __forceinline__ uint32_t dropout_threshold(float p) {
   return static_cast<uint32_t>(rintf(p * 65536.f));
 }
 
+// Philox key of one training step: the host seed plus the device-resident step word times the
+// 64-bit golden ratio (rng_step may be null: key = seed).  The step word is snapshotted per
+// top-level forward (smpk_rng_next), so CUDA-graph replays and consecutive steps draw new masks
+// while a layer's backward re-reads the value its forward used (oracle/philox.py step_key).
+__device__ __forceinline__ uint64_t philox_key(uint64_t seed, const uint64_t* rng_step) {
+  return rng_step ? seed + __ldg(reinterpret_cast<const unsigned long long*>(rng_step)) * 0x9E3779B97F4A7C15ull
+                  : seed;
+}
+
 // keep flags for 8 consecutive columns col0..col0+7 (col0 % 8 == 0) of logical row g
 __device__ __forceinline__ void dropout_keep8(uint64_t seed, uint32_t layer, uint32_t site, uint64_t g, int col0,
                                               uint32_t thresh, bool (&keep)[8]) {

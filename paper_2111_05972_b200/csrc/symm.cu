@@ -15,13 +15,35 @@
 
 namespace smpk {
 
-__device__ unsigned long long g_symm_timeout_peer = 0;  // 1 + peer index that never arrived
+// 1 + index of the peer whose signal never arrived, written by the barrier kernel into pinned,
+// device-mapped host memory right before it traps: the trap makes the failure sticky (every later
+// CUDA call on this context fails, so no stale peer data is ever consumed) and the host can still
+// read which peer was stuck without a CUDA call (smpk_symm_timeout_peer).
+static volatile unsigned long long* g_timeout_host = nullptr;
+static unsigned long long* g_timeout_dev = nullptr;
+
+static int timeout_word_init() {
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    void* h = nullptr;
+    err = cudaHostAlloc(&h, sizeof(unsigned long long), cudaHostAllocMapped | cudaHostAllocPortable);
+    if (err != cudaSuccess) return;
+    *reinterpret_cast<volatile unsigned long long*>(h) = 0;
+    void* d = nullptr;
+    err = cudaHostGetDevicePointer(&d, h, 0);
+    if (err != cudaSuccess) return;
+    g_timeout_host = reinterpret_cast<volatile unsigned long long*>(h);
+    g_timeout_dev = reinterpret_cast<unsigned long long*>(d);
+  });
+  return err == cudaSuccess ? SMPK_OK : SMPK_ERR_CUDA;
+}
 
 // local_flags[0..31]: epoch last signalled by each peer; local_flags[32]: this rank's epoch
 // counter (device-resident so graph replays advance it; every rank runs the same barrier
 // sequence, so the counters stay in lockstep).
 __global__ void symm_barrier_kernel(uint32_t* const* peer_flags, uint32_t* local_flags, int T, int rank,
-                                    unsigned long long timeout_ns) {
+                                    unsigned long long timeout_ns, unsigned long long* timeout_word) {
   const int t = threadIdx.x;
   const uint32_t epoch = *reinterpret_cast<volatile uint32_t*>(local_flags + 32) + 1;
   __syncwarp();
@@ -38,8 +60,10 @@ __global__ void symm_barrier_kernel(uint32_t* const* peer_flags, uint32_t* local
     unsigned long long now;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
     if (now - t0 > timeout_ns) {
-      atomicExch(&g_symm_timeout_peer, (unsigned long long)(t + 1));
-      break;
+      asm volatile("st.volatile.sys.global.u64 [%0], %1;" ::"l"(timeout_word), "l"((unsigned long long)(t + 1))
+                   : "memory");
+      __threadfence_system();
+      __trap();  // sticky: the step fails loudly instead of reading a stuck peer's stale region
     }
     __nanosleep(64);
   }
@@ -85,15 +109,13 @@ extern "C" int smpk_symm_barrier(void* const* peer_flags, void* local_flags, int
                                  void* stream) {
   SMPK_REQUIRE(peer_flags && local_flags && T > 0 && T <= 32 && rank >= 0 && rank < T, SMPK_ERR_BAD_ARG,
                "smpk_symm_barrier: bad arguments");
+  SMPK_REQUIRE(timeout_word_init() == SMPK_OK, SMPK_ERR_CUDA, "smpk_symm_barrier: mapped timeout word");
   symm_barrier_kernel<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<uint32_t* const*>(peer_flags), reinterpret_cast<uint32_t*>(local_flags), T, rank,
-      (unsigned long long)(timeout_s * 1e9));
+      (unsigned long long)(timeout_s * 1e9), g_timeout_dev);
   return check_launch("smpk_symm_barrier");
 }
 
-// 0 = no timeout so far; otherwise 1 + index of the peer whose signal never arrived (host sync).
-extern "C" int smpk_symm_timeout_peer(void) {
-  unsigned long long v = 0;
-  cudaMemcpyFromSymbol(&v, g_symm_timeout_peer, sizeof(v));
-  return (int)v;
-}
+// 0 = no timeout so far; otherwise 1 + index of the peer whose signal never arrived.  A plain
+// host read of mapped memory: valid after the barrier's trap has poisoned the CUDA context.
+extern "C" int smpk_symm_timeout_peer(void) { return g_timeout_host ? (int)*g_timeout_host : 0; }

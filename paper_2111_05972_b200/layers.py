@@ -51,6 +51,8 @@ class LayerMeta:
     shard_rows: bool = False  # activations row-sharded between sub-layers (AG in / RS out)
     comm: str = "peer"  # "peer": fused NVLink peer-store collectives; "nccl": torch.distributed
     push_next: bool = False  # the next sub-layer gathers this output unnormalised: push it from the epilogue
+    grad: bool = True  # grad mode was on at the sub-layer call (Function.forward always runs without it)
+    rng: object = None  # device step snapshot of this forward (ops.rng_next): Philox key = seed + step * golden
 
 
 class LinearFn(torch.autograd.Function):
@@ -103,7 +105,7 @@ def attn_core_fwd(qkv: torch.Tensor, B: int, s: int, m: LayerMeta, mask_add):
     K.gemm_raw(qkv, 0, ld, (dh, s * ld), qkv[:, hd:], 0, ld, (dh, s * ld), S, s, (s * s, hl * s * s),
                s, s, dh, nb=(hl, B))
     P, Pd = ops.softmax_fwd(S, scale=1.0 / math.sqrt(dh), mask_add=mask_add, causal=m.causal, p=m.p_attn,
-                            seed=m.seed, layer=m.layer_id, sample_offset=m.sample_offset, head_offset=m.head_offset,
+                            seed=m.seed, rng=m.rng, layer=m.layer_id, sample_offset=m.sample_offset, head_offset=m.head_offset,
                             nh_global=m.heads_global)
     del S
     ctx = torch.empty(B * s, hd, dtype=qkv.dtype, device=qkv.device)
@@ -124,7 +126,7 @@ def attn_core_bwd(dctx: torch.Tensor, qkv: torch.Tensor, P, Pd, B: int, s: int, 
     # dV = Pd^T dctx
     K.gemm_raw(Pd, 1, s, (s * s, hl * s * s), dctx, 1, hd, (dh, s * hd), dqkv[:, 2 * hd:], ld, (dh, s * ld),
                s, dh, s, nb=(hl, B))
-    dS = ops.softmax_bwd(P, dP, scale=1.0 / math.sqrt(dh), p=m.p_attn, seed=m.seed, layer=m.layer_id,
+    dS = ops.softmax_bwd(P, dP, scale=1.0 / math.sqrt(dh), p=m.p_attn, seed=m.seed, rng=m.rng, layer=m.layer_id,
                          sample_offset=m.sample_offset, head_offset=m.head_offset, nh_global=m.heads_global, out=dP)
     # dQ = dS K ; dK = dS^T Q
     K.gemm_raw(dS, 0, s, (s * s, hl * s * s), qkv[:, hd:], 1, ld, (dh, s * ld), dqkv, ld, (dh, s * ld),
@@ -167,7 +169,7 @@ def _keep_bits_async(B: int, s: int, m: LayerMeta, device):
     side = _side_stream()
     side.wait_stream(main)
     with torch.cuda.stream(side):
-        ops.attn_dropout_bits(B, m.heads_local, s, s, p=m.p_attn, seed=m.seed, layer=m.layer_id,
+        ops.attn_dropout_bits(B, m.heads_local, s, s, p=m.p_attn, seed=m.seed, rng=m.rng, layer=m.layer_id,
                               sample_offset=m.sample_offset, head_offset=m.head_offset, nh_global=m.heads_global,
                               out=bits)
     return bits, (lambda: main.wait_stream(side))
@@ -369,24 +371,32 @@ def _gather_grad(dy2, r, mean, rstd, m: LayerMeta, site: int, keep=None):
     caller has to reduce it itself."""
     R, H = dy2.shape
     has_ln = m._post_w is not None
-    kw = dict(p=m.p_hidden, seed=m.seed, layer=m.layer_id, site=site, row_offset=m.row_offset,
+    kw = dict(p=m.p_hidden, seed=m.seed, rng=m.rng, layer=m.layer_id, site=site, row_offset=m.row_offset,
               want_dr=m.post_ln, keep_in=keep)
     if _peer(m, R):
         pool = get_pool()
         T = m.tp_size
-        G = pool.scratch("grad_gather", T * R * H * 2)
+        # one gather region per site: the weight-gradient GEMMs of this sub-layer may still read it
+        # on the side stream (tp_overlap_sms) when the next sub-layer's exchange starts; peers write
+        # the same site's region again only two exchanges later, after this rank's side-stream join
+        # has been ordered before a barrier they wait on (ADVICE r01: cross-rank write-after-read)
+        G = pool.scratch(f"grad_gather{site}", T * R * H * 2)
         tbl, off = pool.peers(G, pool.me * R * H)
         nv = 3 if has_ln else 1  # [dgamma, dbeta,] dbias: this rank's partial sums over its own rows
-        pg = torch.empty(nv, H, dtype=torch.bfloat16, device=dy2.device)
+        pg = torch.empty(nv, H, dtype=torch.float32, device=dy2.device)
         dr, _, dgw, dgb, dbias = ops.ln_bwd(dy2, r, mean, rstd, m._post_w, out_peers=tbl, peer_off=off,
-                                            param_grads_out=pg, want_dbias=True, **kw)
-        # the replicated-parameter gradients ride the same barrier: push this rank's [nv, H] partial
-        # into every peer's slot, then sum the T slots in ascending rank order
-        L = pool.scratch(f"vec_grads{nv}", T * nv * H * 2)
-        ltbl, loff = pool.peers(L, pool.me * nv * H)
-        ops.bdr_ln(pg, want_r=False, out_peers=ltbl, peer_off=loff)
+                                            param_grads_out=pg, want_dbias=True, grads_f32=True, **kw)
+        # the replicated-parameter gradients ride the same barrier: copy this rank's fp32 [nv, H]
+        # partial into every peer's slot, then sum the T slots in ascending rank order in fp32 and
+        # round once (the same precision as the NCCL path's fp32 allreduce, _sync_replicated)
+        L = pool.scratch(f"vec_grads{nv}", T * nv * H * 4)
+        pool.push_copy(pg, L + pool.me * nv * H * 4)
         pool.barrier()
-        tot, _, _, _ = ops.bdr_ln(pool.view(L, (T * nv, H)), nslots=T, slot_stride=nv * H, rows=nv, cols=H)
+        slots = pool.view(L, (T, nv, H), dtype=torch.float32)
+        tot = slots[0].clone()
+        for j in range(1, T):
+            tot += slots[j]
+        tot = tot.to(torch.bfloat16)
         if has_ln:
             dgw, dgb = tot[0], tot[1]
             m._post_synced = True
@@ -441,12 +451,12 @@ class AttentionFn(torch.autograd.Function):
         kb = ops.keep_bytes(R, H, x.device) if m.p_hidden > 0 else None  # reused by the backward
         Gn, pkw = _push_target(m, R, H)
         r, y, mu2, rs2 = ops.bdr_ln(ox, bias=bo, residual=x2, gamma=post_w if m.post_ln else None,
-                                    beta=post_b if m.post_ln else None, eps=m.eps, p=m.p_hidden, seed=m.seed,
+                                    beta=post_b if m.post_ln else None, eps=m.eps, p=m.p_hidden, seed=m.seed, rng=m.rng,
                                     layer=m.layer_id, site=SITE_ATTN_OUT, row_offset=m.row_offset, rows=R, cols=H,
                                     keep_out=kb, **skw, **pkw)
         ctx.kb = kb
         _free(PR)
-        if not any(ctx.needs_input_grad):
+        if not (m.grad and any(ctx.needs_input_grad)):  # no backward will run: release the gather now
             _free(G)
             G = None
         ctx.m, ctx.shape, ctx.fused, ctx.B, ctx.G = m, (b, s, H), fused, B, G
@@ -518,12 +528,12 @@ class MlpFn(torch.autograd.Function):
         kb = ops.keep_bytes(R, H, x.device) if m.p_hidden > 0 else None  # reused by the backward
         Gn, pkw = _push_target(m, R, H)
         r, y, mu2, rs2 = ops.bdr_ln(gx, bias=b2, residual=x2, gamma=post_w if m.post_ln else None,
-                                    beta=post_b if m.post_ln else None, eps=m.eps, p=m.p_hidden, seed=m.seed,
+                                    beta=post_b if m.post_ln else None, eps=m.eps, p=m.p_hidden, seed=m.seed, rng=m.rng,
                                     layer=m.layer_id, site=SITE_MLP_OUT, row_offset=m.row_offset, rows=R, cols=H,
                                     keep_out=kb, **skw, **pkw)
         ctx.kb = kb
         _free(PR)
-        if not any(ctx.needs_input_grad):
+        if not (m.grad and any(ctx.needs_input_grad)):  # no backward will run: release the gather now
             _free(G)
             G = None
         ctx.m, ctx.shape, ctx.G = m, (b, s, H), G

@@ -58,20 +58,20 @@ class BiasDropResidualFn(torch.autograd.Function):
     """r = residual + dropout(x + bias) on the local channels (global dropout columns)."""
 
     @staticmethod
-    def forward(ctx, x, bias, residual, p, seed, layer, site, row_offset, col_offset):
-        r, _, _, _, _ = ops.bdr_ln_dist(x, bias=bias, residual=residual, p=p, seed=seed, layer=layer, site=site,
+    def forward(ctx, x, bias, residual, p, seed, layer, site, row_offset, col_offset, rng=None):
+        r, _, _, _, _ = ops.bdr_ln_dist(x, bias=bias, residual=residual, p=p, seed=seed, rng=rng, layer=layer, site=site,
                                         row_offset=row_offset, col_offset=col_offset)
-        ctx.cfg = (p, seed, layer, site, row_offset, col_offset)
+        ctx.cfg = (p, seed, layer, site, row_offset, col_offset, rng)
         ctx.has_res = residual is not None
         return r
 
     @staticmethod
     def backward(ctx, dr):
-        p, seed, layer, site, row_offset, col_offset = ctx.cfg
+        p, seed, layer, site, row_offset, col_offset, rng = ctx.cfg
         dr = dr.contiguous()
-        _, dsub, _, _, dbias = ops.ln_bwd_dist(dr, None, None, None, None, p=p, seed=seed, layer=layer, site=site,
+        _, dsub, _, _, dbias = ops.ln_bwd_dist(dr, None, None, None, None, p=p, seed=seed, rng=rng, layer=layer, site=site,
                                                row_offset=row_offset, col_offset=col_offset, want_dbias=True)
-        return dsub, dbias, (dr if ctx.has_res else None), None, None, None, None, None, None
+        return dsub, dbias, (dr if ctx.has_res else None), None, None, None, None, None, None, None
 
 
 class InputSplitLinearRS(torch.autograd.Function):
@@ -168,7 +168,7 @@ def attention(X, mod, mask_add, m: L.LayerMeta, j: int):
     ctxv = AttentionCoreFn.apply(qkv, mask_add, Bg, s, m)
     o = InputSplitLinearRS.apply(ctxv, mod.dense_weight, T)  # [M, H/T]
     r = BiasDropResidualFn.apply(o, mod.dense_bias, x2, m.p_hidden, m.seed, m.layer_id, SITE_ATTN_OUT, m.row_offset,
-                                 j * hs)
+                                 j * hs, m.rng)
     if m.post_ln:
         r = DistLayerNormFn.apply(r, mod.post_ln_weight, mod.post_ln_bias, m.eps, H)
     return r.view(Bg, s, hs)
@@ -186,7 +186,7 @@ def mlp(X, mod, m: L.LayerMeta, j: int):
     a = BiasActFn.apply(z, mod.fc1_bias, m.activation)
     g = InputSplitLinearRS.apply(a, mod.fc2_weight, T)  # [M, H/T]
     r = BiasDropResidualFn.apply(g, mod.fc2_bias, x2, m.p_hidden, m.seed, m.layer_id, SITE_MLP_OUT, m.row_offset,
-                                 j * hs)
+                                 j * hs, m.rng)
     if m.post_ln:
         r = DistLayerNormFn.apply(r, mod.post_ln_weight, mod.post_ln_bias, m.eps, H)
     return r.view(Bg, s, hs)

@@ -18,7 +18,7 @@ from . import collectives as C
 from . import layers as L
 from . import memory_mode as MM
 from .errors import NotDivisibleError, ShapeMismatchError
-from .state import STATE, next_layer_id
+from .state import STATE, begin_forward, next_layer_id
 
 DTYPE = torch.bfloat16
 
@@ -178,7 +178,7 @@ class _LayerBase(DistributedModule):
                            p_hidden=self.hidden_dropout_prob if self.training else 0.0,
                            causal=self.causal_mask_size is not None, pre_ln=self.pre_layernorm,
                            post_ln=self.post_layernorm, activation=self.activation, layer_id=self.layer_id,
-                           seed=STATE.seed + 0x9E3779B97F4A7C15 * STATE.step, head_offset=STATE.tp_rank * hl,
+                           seed=STATE.seed, rng=STATE.rng_cur, grad=torch.is_grad_enabled(), head_offset=STATE.tp_rank * hl,
                            sample_offset=sample_offset, tp_size=T, row_offset=row_offset, shard_rows=shard,
                            comm=STATE.config.get("tp_comm", "peer"))
 
@@ -334,7 +334,9 @@ def _row_ctx(B: int, s: int):
 
 
 def _entry(x, attention_mask):
-    """Module entry: in row-sharded mode only the attention mask is gathered over the TP group."""
+    """Module entry: in row-sharded mode only the attention mask is gathered over the TP group.
+    Also snapshots / advances the device dropout step word (state.begin_forward)."""
+    begin_forward()
     B, s = x.shape[0], x.shape[1]
     mask = _mask_2d(attention_mask, B, s)
     rc = _row_ctx(B, s)
@@ -478,6 +480,7 @@ class DistributedTransformerLMHead(DistributedModule):
     def forward(self, input_ids, attention_mask=None, labels=None):
         b, s = input_ids.shape
         T = STATE.tp_size
+        begin_forward()
         gathered = not (STATE.prescaled or T == 1)
         ids = C.all_gather(input_ids.contiguous(), 0) if gathered else input_ids
         mask = _mask_2d(attention_mask, b, s)

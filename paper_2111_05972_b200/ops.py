@@ -13,11 +13,20 @@ from .kernels import _check_cuda, _ptr, _stream
 SITE_ATTN_PROB, SITE_ATTN_OUT, SITE_MLP_OUT = 0, 1, 2
 
 
+def rng_next(counter: torch.Tensor) -> torch.Tensor:
+    """Snapshot the device step counter into a new 1-element tensor and increment the counter
+    (smpk_rng_next, on the current stream; CUDA-graph capturable)."""
+    _check_cuda(counter)
+    snap = torch.empty(1, dtype=torch.int64, device=counter.device)
+    _lib.call("smpk_rng_next", _ptr(counter), _ptr(snap), _stream())
+    return snap
+
+
 def _f32(t):
     return None if t is None else t
 
 
-def bdr_ln(x: torch.Tensor, *, bias=None, residual=None, gamma=None, beta=None, eps=1e-5, p=0.0, seed=0,
+def bdr_ln(x: torch.Tensor, *, bias=None, residual=None, gamma=None, beta=None, eps=1e-5, p=0.0, seed=0, rng=None,
            layer=0, site=SITE_ATTN_OUT, row_offset=0, want_r=True, want_y=True, nslots=1, slot_stride=0,
            out_peers=None, peer_off=0, rows=None, cols=None, keep_out=None, x_peers=None, x_peer_off=0):
     """r = residual + dropout(x + bias); y = LN(r). Returns (r, y, mean, rstd) (None where not computed).
@@ -37,7 +46,7 @@ def bdr_ln(x: torch.Tensor, *, bias=None, residual=None, gamma=None, beta=None, 
     npeers = 0 if out_peers is None else out_peers.numel()
     _lib.call("smpk_bdr_ln_fwd_ex", _ptr(x), int(nslots), int(slot_stride), _ptr(bias), _ptr(residual), _ptr(r),
               _ptr(gamma), _ptr(beta), _ptr(y), _ptr(mean), _ptr(rstd), _ptr(out_peers), npeers, int(peer_off), M, H,
-              float(eps), float(p), int(seed) & (2 ** 64 - 1), int(layer), int(site), int(row_offset),
+              float(eps), float(p), int(seed) & (2 ** 64 - 1), _ptr(rng), int(layer), int(site), int(row_offset),
               _ptr(keep_out if p > 0 else None), _ptr(x_peers), int(x_peer_off), _stream())
     return r, y, mean, rstd
 
@@ -58,7 +67,7 @@ def add(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     return r
 
 
-def ln_bwd(dy, r, mean, rstd, gamma, *, dres=None, p=0.0, seed=0, layer=0, site=SITE_ATTN_OUT, row_offset=0,
+def ln_bwd(dy, r, mean, rstd, gamma, *, dres=None, p=0.0, seed=0, rng=None, layer=0, site=SITE_ATTN_OUT, row_offset=0,
            want_dgamma=True, want_dbias=True, grads_f32=False, want_dr=True, nslots=1, slot_stride=0,
            out_peers=None, peer_off=0, rows=None, cols=None, keep_in=None, x_peers=None, x_peer_off=0,
            param_grads_out=None):
@@ -87,7 +96,7 @@ def ln_bwd(dy, r, mean, rstd, gamma, *, dres=None, p=0.0, seed=0, layer=0, site=
     npeers = 0 if out_peers is None else out_peers.numel()
     _lib.call("smpk_ln_bwd_ex", _ptr(dy), int(nslots), int(slot_stride), _ptr(r), _ptr(mean), _ptr(rstd),
               _ptr(gamma), _ptr(dres), _ptr(dr), _ptr(dsub), _ptr(out_peers), npeers, int(peer_off), _ptr(dgamma),
-              _ptr(dbeta), _ptr(dbias), int(grads_f32), 0, M, H, float(p), int(seed) & (2 ** 64 - 1), int(layer),
+              _ptr(dbeta), _ptr(dbias), int(grads_f32), 0, M, H, float(p), int(seed) & (2 ** 64 - 1), _ptr(rng), int(layer),
               int(site), int(row_offset), _ptr(keep_in if p > 0 else None), _ptr(x_peers), int(x_peer_off), _ptr(ws),
               int(ws_bytes), _stream(),
               launches=2 if (dgamma is not None or dbeta is not None or dbias is not None) else 1)
@@ -96,7 +105,7 @@ def ln_bwd(dy, r, mean, rstd, gamma, *, dres=None, p=0.0, seed=0, layer=0, site=
     return dr, dsub, dgamma, dbeta, dbias
 
 
-def softmax_fwd(scores: torch.Tensor, *, scale: float, mask_add=None, causal=False, p=0.0, seed=0, layer=0,
+def softmax_fwd(scores: torch.Tensor, *, scale: float, mask_add=None, causal=False, p=0.0, seed=0, rng=None, layer=0,
                 sample_offset=0, head_offset=0, nh_global=None):
     """scores [B, nh, sq, sk] -> (P, Pd) with Pd = P when p == 0."""
     _check_cuda(scores, mask_add)
@@ -106,18 +115,18 @@ def softmax_fwd(scores: torch.Tensor, *, scale: float, mask_add=None, causal=Fal
     if mask_add is not None:
         mask_add = mask_add.reshape(B, sk).to(torch.float32).contiguous()
     _lib.call("smpk_softmax_fwd", _ptr(scores), _ptr(P), _ptr(Pd), _ptr(mask_add), B, nh, sq, sk, float(scale),
-              int(bool(causal)), float(p), int(seed) & (2 ** 64 - 1), int(layer), int(sample_offset), int(head_offset),
+              int(bool(causal)), float(p), int(seed) & (2 ** 64 - 1), _ptr(rng), int(layer), int(sample_offset), int(head_offset),
               int(nh_global if nh_global is not None else nh), _stream())
     return P, (Pd if Pd is not None else P)
 
 
-def softmax_bwd(P: torch.Tensor, dPd: torch.Tensor, *, scale: float, p=0.0, seed=0, layer=0, sample_offset=0,
+def softmax_bwd(P: torch.Tensor, dPd: torch.Tensor, *, scale: float, p=0.0, seed=0, rng=None, layer=0, sample_offset=0,
                 head_offset=0, nh_global=None, out=None):
     _check_cuda(P, dPd)
     B, nh, sq, sk = P.shape
     dS = out if out is not None else torch.empty_like(P)
     _lib.call("smpk_softmax_bwd", _ptr(P), _ptr(dPd), _ptr(dS), B, nh, sq, sk, float(scale), float(p),
-              int(seed) & (2 ** 64 - 1), int(layer), int(sample_offset), int(head_offset),
+              int(seed) & (2 ** 64 - 1), _ptr(rng), int(layer), int(sample_offset), int(head_offset),
               int(nh_global if nh_global is not None else nh), _stream())
     return dS
 
@@ -134,7 +143,7 @@ def colsum(x: torch.Tensor, *, out_dtype=None) -> torch.Tensor:
     return out
 
 
-def attn_dropout_bits(B: int, nh: int, sq: int, sk: int, *, p: float, seed=0, layer=0, sample_offset=0,
+def attn_dropout_bits(B: int, nh: int, sq: int, sk: int, *, p: float, seed=0, rng=None, layer=0, sample_offset=0,
                       head_offset=0, nh_global=None, device=None, out=None) -> torch.Tensor | None:
     """Keep bits [B, nh, sq, sk/32] (uint32 words as int32) of the attention-probability dropout;
     None when p == 0.  Generated once per layer and shared by the forward and the backward."""
@@ -143,7 +152,7 @@ def attn_dropout_bits(B: int, nh: int, sq: int, sk: int, *, p: float, seed=0, la
     bits = out if out is not None else torch.empty(B, nh, sq, sk // 32, dtype=torch.int32,
                                                    device=device or torch.cuda.current_device())
     _check_cuda(bits)
-    _lib.call("smpk_attn_dropout_bits", B, nh, sq, sk, float(p), int(seed) & (2 ** 64 - 1), int(layer),
+    _lib.call("smpk_attn_dropout_bits", B, nh, sq, sk, float(p), int(seed) & (2 ** 64 - 1), _ptr(rng), int(layer),
               int(sample_offset), int(head_offset), int(nh_global if nh_global is not None else nh), _ptr(bits),
               _stream())
     return bits
@@ -189,7 +198,7 @@ def flash_attn_fwd(qkv: torch.Tensor, B: int, s: int, nh: int, dh: int, *, mask_
 # channel-sharded (memory-mode) LayerNorm and the standalone bias + activation
 # ---------------------------------------------------------------------------
 
-def bdr_ln_dist(x: torch.Tensor, *, bias=None, residual=None, gamma=None, beta=None, eps=1e-5, p=0.0, seed=0, layer=0,
+def bdr_ln_dist(x: torch.Tensor, *, bias=None, residual=None, gamma=None, beta=None, eps=1e-5, p=0.0, seed=0, rng=None, layer=0,
                 site=SITE_ATTN_OUT, row_offset=0, col_offset=0, want_r=True, row_sums=False, ext_sums=None,
                 h_total=0):
     """smpk_bdr_ln_fwd_dist on the local H/T columns.  row_sums=True also returns the partial
@@ -206,12 +215,12 @@ def bdr_ln_dist(x: torch.Tensor, *, bias=None, residual=None, gamma=None, beta=N
         rstd = torch.empty(M, dtype=torch.float32, device=dev)
     sums = torch.empty(M, 2, dtype=torch.float32, device=dev) if row_sums else None
     _lib.call("smpk_bdr_ln_fwd_dist", _ptr(x), _ptr(bias), _ptr(residual), _ptr(r), _ptr(gamma), _ptr(beta), _ptr(y),
-              _ptr(mean), _ptr(rstd), M, H, float(eps), float(p), int(seed) & (2 ** 64 - 1), int(layer), int(site),
+              _ptr(mean), _ptr(rstd), M, H, float(eps), float(p), int(seed) & (2 ** 64 - 1), _ptr(rng), int(layer), int(site),
               int(row_offset), int(col_offset), _ptr(sums), _ptr(ext_sums), int(h_total), _stream())
     return r, y, mean, rstd, sums
 
 
-def ln_bwd_dist(dy, r, mean, rstd, gamma, *, dres=None, p=0.0, seed=0, layer=0, site=SITE_ATTN_OUT, row_offset=0,
+def ln_bwd_dist(dy, r, mean, rstd, gamma, *, dres=None, p=0.0, seed=0, rng=None, layer=0, site=SITE_ATTN_OUT, row_offset=0,
                 col_offset=0, sums_only=False, ext_sums=None, h_total=0, want_dbias=False):
     """smpk_ln_bwd_dist.  sums_only=True returns the partial [M, 2] (sum g, sum g*xhat); otherwise
     (dr, dsub, dgamma, dbeta, dbias) with the row means taken from ext_sums (gamma None: no LN)."""
@@ -223,7 +232,7 @@ def ln_bwd_dist(dy, r, mean, rstd, gamma, *, dres=None, p=0.0, seed=0, layer=0, 
     if sums_only:
         sums = torch.empty(M, 2, dtype=torch.float32, device=dev)
         _lib.call("smpk_ln_bwd_dist", _ptr(dy), _ptr(r), _ptr(mean), _ptr(rstd), _ptr(gamma), None, None, None, None,
-                  None, None, 0, M, H, float(p), int(seed) & (2 ** 64 - 1), int(layer), int(site), int(row_offset),
+                  None, None, 0, M, H, float(p), int(seed) & (2 ** 64 - 1), _ptr(rng), int(layer), int(site), int(row_offset),
                   int(col_offset), _ptr(sums), None, 0, _ptr(ws), int(ws_bytes), _stream(), launches=1)
         return sums
     dr = torch.empty(M, H, dtype=torch.bfloat16, device=dev)
@@ -232,7 +241,7 @@ def ln_bwd_dist(dy, r, mean, rstd, gamma, *, dres=None, p=0.0, seed=0, layer=0, 
     dbeta = torch.empty(H, dtype=torch.bfloat16, device=dev) if gamma is not None else None
     dbias = torch.empty(H, dtype=torch.bfloat16, device=dev) if want_dbias else None
     _lib.call("smpk_ln_bwd_dist", _ptr(dy), _ptr(r), _ptr(mean), _ptr(rstd), _ptr(gamma), _ptr(dres), _ptr(dr),
-              _ptr(dsub), _ptr(dgamma), _ptr(dbeta), _ptr(dbias), 0, M, H, float(p), int(seed) & (2 ** 64 - 1),
+              _ptr(dsub), _ptr(dgamma), _ptr(dbeta), _ptr(dbias), 0, M, H, float(p), int(seed) & (2 ** 64 - 1), _ptr(rng),
               int(layer), int(site), int(row_offset), int(col_offset), None, _ptr(ext_sums), int(h_total), _ptr(ws),
               int(ws_bytes), _stream(), launches=2 if (dgamma is not None or dbias is not None) else 1)
     return dr, (dsub if dsub is not None else dr), dgamma, dbeta, dbias

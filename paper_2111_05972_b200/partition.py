@@ -9,6 +9,10 @@ without the reference on the box:
   * recursive device-set splitting and BFS tree partition (partition.py:102-178).
 tests/test_planning_golden.py checks every function bit-exactly against golden
 vectors produced by the reference itself (tests/golden/make_golden.py).
+
+PROVENANCE: vendored from the reference's mpsim planner (/root/reference/pkg/src/mpsim/partition.py, model_graph.py), restated
+rule for rule so that partition assignments stay bit-exact with the reference (the north_star keeps this code in
+Python); it is off the GPU hot path and earns no credit as newly built work.
 """
 from __future__ import annotations
 

@@ -14,6 +14,11 @@
 * ``static_schedule`` turns the scheduler decisions into per-stage op lists for a
   chain of P stages (record-and-replay "static mode"), which
   ``PipelineEngine`` executes SPMD (one process per GPU).
+
+PROVENANCE: the scheduler section (SchedulePolicy, SchedulerState, ready_backwards, next_action) and
+the routing section (D2DBuffers, route) are vendored from the reference (mpsim pipeline.py:96-165,
+comm.py:157-225) so schedule decisions and D2D routing stay bit-exact with it; they stay in Python
+per the north_star.  static_schedule, StageChannel and PipelineEngine are original.
 """
 from __future__ import annotations
 

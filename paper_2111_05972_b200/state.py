@@ -52,7 +52,9 @@ class State:
     pp_group_ranks: list = field(default_factory=lambda: [0])
     initialized: bool = False
     layer_counter: int = 0
-    step: int = 0
+    step: int = 0  # host mirror: forwards issued eagerly (graph replays advance only the device word)
+    rng_counter: object = None  # device int64 step word (one per process), advanced per top-level forward
+    rng_cur: object = None  # snapshot of the step word the current forward's dropout kernels read
 
     # -- accessors mirroring smp.tp_rank() / smp.tp_size() ...
     @property
@@ -133,6 +135,11 @@ def init(config: dict | None = None, *, backend: str | None = None) -> State:
                     setattr(st, f"{kind}_group", g)
     st.initialized = True
     st.layer_counter = 0
+    st.step = 0
+    st.rng_cur = None
+    if torch.cuda.is_available():  # created eagerly: a counter first allocated inside a CUDA-graph
+        # capture would be re-zeroed by every replay
+        st.rng_counter = torch.zeros(1, dtype=torch.int64, device=torch.device("cuda", torch.cuda.current_device()))
     return st
 
 
@@ -160,6 +167,34 @@ def get_pool():
         pool = SymmPool(cap, STATE.tp_group, ranks, ranks.index(STATE.rank))
         STATE._pool = pool
     return pool
+
+
+def begin_forward():
+    """Start of a top-level smp forward (module entry): snapshot the device step word and advance
+    it, so every training step -- eager or a CUDA-graph replay -- draws fresh dropout masks while
+    the backward re-reads the snapshot its forward used."""
+    from . import ops
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if STATE.rng_counter is None or STATE.rng_counter.device != dev:
+        if torch.cuda.is_current_stream_capturing():
+            raise RuntimeError("smp: the dropout step counter must exist before CUDA-graph capture "
+                               "(call smp.init() / run one eager step on this device first)")
+        STATE.rng_counter = torch.zeros(1, dtype=torch.int64, device=dev)
+    STATE.rng_cur = ops.rng_next(STATE.rng_counter)
+    STATE.step += 1
+    return STATE.rng_cur
+
+
+def rng_step() -> int:
+    """Current value of the device step word (synchronising read; tests / checkpoints)."""
+    return 0 if STATE.rng_counter is None else int(STATE.rng_counter.item())
+
+
+def set_rng_step(step: int) -> None:
+    """Restore the device step word (resume from a checkpoint)."""
+    if STATE.rng_counter is None:
+        STATE.rng_counter = torch.zeros(1, dtype=torch.int64, device=torch.device("cuda", torch.cuda.current_device()))
+    STATE.rng_counter.fill_(int(step))
 
 
 def next_layer_id() -> int:

@@ -15,8 +15,25 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
+from .errors import PeerTimeoutError
 
 ALIGN = 1024
+
+
+def check_peer_timeout(timeout_s: float | None = None) -> None:
+    peer = _lib.lib().smpk_symm_timeout_peer()
+    if peer:
+        after = f" after {timeout_s:g} s" if timeout_s is not None else ""
+        raise PeerTimeoutError(f"symmetric-memory barrier timed out{after} waiting for TP peer {peer - 1}")
+
+
+def synchronize() -> None:
+    """torch.cuda.synchronize() that turns a trapped peer barrier into PeerTimeoutError."""
+    try:
+        torch.cuda.synchronize()
+    except RuntimeError as e:
+        check_peer_timeout()
+        raise e
 
 
 class SymmPool:
@@ -117,6 +134,14 @@ class SymmPool:
         assert off % elem_size == 0
         return self.base_array, off // elem_size + elem_off
 
+    def push_copy(self, src: torch.Tensor, off: int) -> None:
+        """Copy the contiguous tensor src to byte offset `off` of every rank's pool (own included),
+        on the current stream (copy engine over NVLink; capturable)."""
+        st = torch.cuda.current_stream().cuda_stream
+        nbytes = src.numel() * src.element_size()
+        for j in range(self.T):
+            _lib.call("smpk_copy_async", self.bases[j] + off, src.data_ptr(), nbytes, st)
+
     def view(self, off: int, shape, dtype=torch.bfloat16) -> torch.Tensor:
         n = 1
         for s in shape:
@@ -130,9 +155,9 @@ class SymmPool:
                   float(self.timeout_s), torch.cuda.current_stream().cuda_stream)
 
     def check(self) -> None:
-        peer = _lib.lib().smpk_symm_timeout_peer()
-        if peer:
-            raise RuntimeError(f"symmetric-memory barrier timed out waiting for TP peer {peer - 1}")
+        """Raise PeerTimeoutError if a barrier of this process timed out (the barrier kernel traps,
+        so the CUDA context is poisoned; the stuck peer is read from mapped host memory)."""
+        check_peer_timeout(self.timeout_s)
 
     def close(self) -> None:
         for p in self._mapped:

@@ -34,6 +34,11 @@ CASES = [
     ("bert_dropout", 4, 64, 256, 1024, 128, 2, False, False, True, "gelu", 0.1),
     ("gpt_dropout", 8, 64, 512, 2048, 256, 2, True, True, False, "gelu_tanh", 0.1),
     ("wide_heads", 2, 128, 256, 1024, 128, 2, True, True, False, "gelu", 0.0),
+    # the benchmarked layer (BASELINE.json configs[1], bench.py): BERT-large, 16x64 heads, s=512,
+    # post-LN, GeLU(erf), dropout 0.1 with bit-exact Philox masks, padding mask on sample 0
+    ("bert_large", 16, 64, 1024, 4096, 512, 2, False, False, True, "gelu", 0.1),
+    # the GPT-3 1.3B layer shape (configs[2]): 16x128 heads, s=2048, causal, pre-LN, gelu_tanh
+    ("gpt_1p3b", 16, 128, 2048, 8192, 2048, 1, True, True, False, "gelu_tanh", 0.1),
 ]
 
 
@@ -125,3 +130,107 @@ def test_layer_deterministic(smp_single):
         outs.append((y.detach().clone(), x.grad.clone(), layer.attention.qkv_weight.grad.clone()))
     for u, v in zip(*outs):
         assert torch.equal(u, v)
+
+
+def _dropout_layer(smp):
+    layer = smp.nn.DistributedTransformerLayer(num_attention_heads=4, attention_head_size=64, hidden_size=256,
+                                               intermediate_size=1024, attention_dropout_prob=0.1,
+                                               hidden_dropout_prob=0.1, layer_id=0)
+    cfg = tp.LayerConfig(num_attention_heads=4, attention_head_size=64, hidden_size=256, intermediate_size=1024,
+                         attention_dropout_prob=0.1, hidden_dropout_prob=0.1)
+    params = {k: v.to(torch.bfloat16).double() for k, v in tp.init_layer_params(cfg, seed=1).items()}
+    layer.load_full({k: v.to(torch.bfloat16) for k, v in params.items()})
+    return layer, cfg, params
+
+
+def _oracle_y(x, params, cfg, step):
+    return tp.transformer_layer_ref(x.double(), params, cfg, None, tp.DropoutCtx(seed=7, layer=0, step=step))
+
+
+def test_dropout_masks_advance_per_step_eager(smp_single):
+    """Two consecutive training forwards draw different masks (device step word 0, then 1),
+    and each matches the oracle keyed with its own step (philox.step_key)."""
+    smp = smp_single
+    layer, cfg, params = _dropout_layer(smp)
+    g = torch.Generator().manual_seed(0)
+    x = torch.randn(2, 128, 256, generator=g).to(torch.bfloat16)
+    ys = [layer(x.cuda()).float().cpu() for _ in range(2)]
+    assert not torch.equal(ys[0], ys[1])
+    assert smp.rng_step() == 2
+    for step, y in enumerate(ys):
+        assert rel(y, _oracle_y(x, params, cfg, step)) < TOL
+    # the other step's mask is far off: the comparison is sensitive to the key
+    assert rel(ys[0], _oracle_y(x, params, cfg, 1)) > 5 * TOL
+
+
+def test_dropout_masks_advance_per_graph_replay(smp_single):
+    """A captured fwd+bwd step replayed twice draws fresh masks each replay (the step word is
+    advanced by a kernel inside the graph), and the backward uses its own forward's mask."""
+    smp = smp_single
+    layer, cfg, params = _dropout_layer(smp)
+    g = torch.Generator().manual_seed(0)
+    x = torch.randn(2, 128, 256, generator=g).to(torch.bfloat16)
+    dy = torch.randn(2, 128, 256, generator=g).to(torch.bfloat16)
+    xs = x.cuda().requires_grad_(True)
+    dys = dy.cuda()
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):  # warm-up (eager, step 0)
+        layer(xs).backward(dys)
+    torch.cuda.current_stream().wait_stream(st)
+    graph = torch.cuda.CUDAGraph()
+    xs.grad = None
+    with torch.cuda.graph(graph):
+        yg = layer(xs)
+        yg.backward(dys)
+    torch.cuda.synchronize()
+    outs = []
+    for _ in range(2):
+        step = smp.rng_step()
+        graph.replay()
+        torch.cuda.synchronize()
+        outs.append((step, yg.detach().float().cpu(), xs.grad.detach().float().cpu()))
+    assert outs[1][0] == outs[0][0] + 1
+    assert not torch.equal(outs[0][1], outs[1][1])
+    for step, y, dx in outs:
+        xr = x.double().requires_grad_(True)
+        yr = tp.transformer_layer_ref(xr, params, cfg, None, tp.DropoutCtx(seed=7, layer=0, step=step))
+        yr.backward(dy.double())
+        assert rel(y, yr.detach()) < TOL and rel(dx, xr.grad) < TOL
+
+
+def test_bert_large_24_layer_stack_vs_oracle(smp_single):
+    """The full benchmarked stack (24 BERT-large layers, dropout 0.1, b=1, s=512) against the fp64
+    oracle: output and input gradient within 3e-2 after 24 layers, plus the first
+    and last layers' QKV / FC2 weight gradients."""
+    smp = smp_single
+    L, nh, dh, H, I, s = 24, 16, 64, 1024, 4096, 512
+    cfg = tp.LayerConfig(num_attention_heads=nh, attention_head_size=dh, hidden_size=H, intermediate_size=I,
+                         attention_dropout_prob=0.1, hidden_dropout_prob=0.1)
+    params = [{k: v.to(torch.bfloat16).double() for k, v in tp.init_layer_params(cfg, seed=100 + l).items()}
+              for l in range(L)]
+    model = smp.nn.DistributedTransformer(num_layers=L, num_attention_heads=nh, attention_head_size=dh,
+                                          hidden_size=H, intermediate_size=I, attention_dropout_prob=0.1,
+                                          hidden_dropout_prob=0.1)
+    for l, layer in enumerate(model.seq_layers):
+        assert layer.layer_id == l
+        layer.load_full({k: v.to(torch.bfloat16) for k, v in params[l].items()})
+    g = torch.Generator().manual_seed(0)
+    x = torch.randn(1, s, H, generator=g).to(torch.bfloat16)
+    dy = torch.randn(1, s, H, generator=g).to(torch.bfloat16)
+    xg = x.cuda().requires_grad_(True)
+    y = model(xg)
+    y.backward(dy.cuda())
+    torch.cuda.synchronize()
+    xr = x.double().requires_grad_(True)
+    pr = [{k: v.clone().requires_grad_(True) for k, v in p.items()} for p in params]
+    yr = tp.transformer_ref(xr, pr, cfg, None, seed=7)
+    yr.backward(dy.double())
+    errs = {"y": rel(y, yr), "dx": rel(xg.grad, xr.grad)}
+    for l in (0, L - 1):
+        lay = model.seq_layers[l]
+        wq, wk, wv = pr[l]["wqkv"].grad.split(H, 0)
+        errs[f"dwqkv{l}"] = rel(lay.attention.qkv_weight.grad, torch.cat([wq, wk, wv], 0))
+        errs[f"dw2_{l}"] = rel(lay.output.fc2_weight.grad, pr[l]["w2"].grad)
+    bad = {k: v for k, v in errs.items() if not v < 3e-2}
+    assert not bad, f"{bad} (all: {errs})"

@@ -32,3 +32,23 @@ def test_mask_layout_and_rate():
     assert philox.threshold(0.1) == 6554 and philox.threshold(0.0) == 0
     # masks are a pure function of logical coordinates
     assert np.array_equal(philox.keep_mask(rows[10:20], cols, 3, 1, 42, 0.1), keep[10:20])
+
+
+def test_c_restatement_matches_numpy():
+    """oracle/philox_grid.c (built by oracle/Makefile) == the numpy restatement, bit for bit,
+    including step keys (philox.step_key) and ragged column counts."""
+    import pytest
+    if philox._clib() is None:
+        pytest.skip("oracle/libphilox_grid.so not built (make -C oracle)")
+    rows = np.array([0, 1, 7, 12345, 2 ** 31 + 5, 4096 * 24 - 1], dtype=np.int64)
+    for n_cols, seed, step, p in ((1024, 7, 0, 0.1), (13, 42, 3, 0.5), (2048, 0, 2 ** 40, 0.25)):
+        key = philox.step_key(seed, step)
+        a = philox.keep_grid(rows, n_cols, 5, 2, key, p, use_c=True)
+        b = philox.keep_grid(rows, n_cols, 5, 2, key, p, use_c=False)
+        assert np.array_equal(a, b)
+
+
+def test_step_key():
+    assert philox.step_key(7, 0) == 7
+    assert philox.step_key(7, 1) == (7 + 0x9E3779B97F4A7C15) % 2 ** 64
+    assert philox.step_key(2 ** 64 - 1, 1) == (0x9E3779B97F4A7C15 - 1)
