@@ -60,7 +60,7 @@ __global__ void symm_barrier_kernel(uint32_t* const* peer_flags, uint32_t* local
     unsigned long long now;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
     if (now - t0 > timeout_ns) {
-      asm volatile("st.volatile.sys.global.u64 [%0], %1;" ::"l"(timeout_word), "l"((unsigned long long)(t + 1))
+      asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(timeout_word), "l"((unsigned long long)(t + 1))
                    : "memory");
       __threadfence_system();
       __trap();  // sticky: the step fails loudly instead of reading a stuck peer's stale region
