@@ -125,6 +125,7 @@ def test_layer_deterministic(smp_single):
         x.grad = None
         for prm in layer.parameters():
             prm.grad = None
+        smp.set_rng_step(0)  # same training step: same dropout masks
         y = layer(x)
         y.float().square().sum().backward()
         outs.append((y.detach().clone(), x.grad.clone(), layer.attention.qkv_weight.grad.clone()))
@@ -157,10 +158,10 @@ def test_dropout_masks_advance_per_step_eager(smp_single):
     ys = [layer(x.cuda()).float().cpu() for _ in range(2)]
     assert not torch.equal(ys[0], ys[1])
     assert smp.rng_step() == 2
-    for step, y in enumerate(ys):
-        assert rel(y, _oracle_y(x, params, cfg, step)) < TOL
+    errs = [rel(y, _oracle_y(x, params, cfg, step)) for step, y in enumerate(ys)]
+    assert max(errs) < TOL, errs
     # the other step's mask is far off: the comparison is sensitive to the key
-    assert rel(ys[0], _oracle_y(x, params, cfg, 1)) > 5 * TOL
+    assert rel(ys[0], _oracle_y(x, params, cfg, 1)) > 10 * errs[0]
 
 
 def test_dropout_masks_advance_per_graph_replay(smp_single):
