@@ -41,11 +41,30 @@ CFG = dict(num_layers=24, num_attention_heads=16, attention_head_size=64, hidden
            pre_layernorm=False, post_layernorm=True)
 SEQ = 512
 BATCH_PER_GPU = 8
+# BASELINE.json configs[2] (the north_star's ">= 60% of peak" target): GPT-3 1.3B with the
+# vocab-parallel embedding, tied LM head and vocab-parallel cross-entropy; 8 sequences of 2048
+# tokens per GPU (the paper's prescaled TP=8 batch, is 8 sequences per step)
+GPT_CFG = dict(num_layers=24, num_attention_heads=16, attention_head_size=128, hidden_size=2048,
+               intermediate_size=8192, vocab_size=50257, num_positions=2048, attention_dropout_prob=0.1,
+               hidden_dropout_prob=0.1, activation="gelu_tanh", layernorm_epsilon=1e-5, causal_mask_size=2048,
+               pre_layernorm=True, post_layernorm=False)
+GPT_SEQ = 2048
+GPT_BATCH_PER_GPU = 8
 
 
 def flops_per_token_layer(H=1024, s=SEQ, causal=False):
     """fwd+bwd algorithmic FLOPs per token per layer: 72 H^2 + 12 s H (non-causal)."""
     return 72 * H * H + (6 if causal else 12) * s * H
+
+
+def flops_per_token(workload: str) -> float:
+    """fwd+bwd algorithmic FLOPs per token of the whole model: BERT-large 1.963 GFLOP
+    (24 layers); GPT-1.3B 8.469 GFLOP (24 causal layers + the tied LM head's 6 H V)."""
+    if workload == "gpt1.3b":
+        c = GPT_CFG
+        return (c["num_layers"] * flops_per_token_layer(c["hidden_size"], GPT_SEQ, causal=True)
+                + 6 * c["hidden_size"] * c["vocab_size"])
+    return flops_per_token_layer() * CFG["num_layers"]
 
 
 def gemm_traffic():
@@ -121,28 +140,52 @@ class ClockSampler:
 # CPU reference (the oracle restatement; the reference has no TP code)
 # ---------------------------------------------------------------------------
 
-def cpu_reference_sample(max_seconds=15.0, min_iters=2):
-    """One BERT-large layer fwd+bwd, 1 sequence of 512 tokens, torch fp32 on all host cores.
-    Returns (tokens/s of the 24-layer stack, threads, seconds, iterations)."""
+def cpu_reference_sample(max_seconds=15.0, min_iters=2, workload="bert-large"):
+    """The CPU oracle (oracle/tp.py, torch fp32 on all host cores) on a bounded sample: one layer
+    fwd+bwd on one sequence (BERT-large: 512 tokens; GPT-1.3B: 2048 causal tokens, plus the tied
+    LM head + CE on the same tokens), scaled to the whole model's per-token cost.
+    Returns (tokens/s of the whole model, threads, seconds, iterations)."""
     from oracle import tp
     threads = os.cpu_count() or 1
     torch.set_num_threads(threads)
-    cfg = tp.LayerConfig(num_attention_heads=16, attention_head_size=64, hidden_size=1024, intermediate_size=4096,
-                         attention_dropout_prob=0.1, hidden_dropout_prob=0.1)
+    gpt = workload == "gpt1.3b"
+    c = GPT_CFG if gpt else CFG
+    seq = GPT_SEQ if gpt else SEQ
+    cfg = tp.LayerConfig(num_attention_heads=c["num_attention_heads"], attention_head_size=c["attention_head_size"],
+                         hidden_size=c["hidden_size"], intermediate_size=c["intermediate_size"],
+                         attention_dropout_prob=0.1, hidden_dropout_prob=0.1, activation=c["activation"],
+                         causal_mask_size=seq if gpt else None, pre_layernorm=c["pre_layernorm"],
+                         post_layernorm=c["post_layernorm"])
     p = {k: v.requires_grad_(True) for k, v in tp.init_layer_params(cfg, 1, dtype=torch.float32).items()}
-    x = torch.randn(1, SEQ, 1024, requires_grad=True)
-    dy = torch.randn(1, SEQ, 1024)
+    H = c["hidden_size"]
+    x = torch.randn(1, seq, H, requires_grad=True)
+    dy = torch.randn(1, seq, H)
     dctx = tp.DropoutCtx(seed=0, layer=0, torch_rng=True)
-    tp.transformer_layer_ref(x, p, cfg, None, dctx).backward(dy)  # untimed warm-up
+    E = (torch.randn(c["vocab_size"], H) * 0.02).requires_grad_(True) if gpt else None
+    tgt = torch.randint(0, c["vocab_size"], (seq,)) if gpt else None
+
+    def one():
+        tp.transformer_layer_ref(x, p, cfg, None, dctx).backward(dy)
+
+    def head():
+        logits = x.detach().reshape(seq, H) @ E.t()
+        tp.cross_entropy_ref(logits, tgt, c["vocab_size"]).sum().backward()
+
+    one()  # untimed warm-up
     t0 = time.perf_counter()
     it = 0
     while it < min_iters or (time.perf_counter() - t0 < max_seconds and it < 50):
-        y = tp.transformer_layer_ref(x, p, cfg, None, dctx)
-        y.backward(dy)
+        one()
         it += 1
     dt = time.perf_counter() - t0
-    per_layer_tok_s = SEQ * it / dt
-    return per_layer_tok_s / CFG["num_layers"], threads, dt, it
+    sec_per_tok = dt / (seq * it) * c["num_layers"]
+    if gpt:
+        head()
+        t1 = time.perf_counter()
+        head()
+        sec_per_tok += (time.perf_counter() - t1) / seq
+        dt += time.perf_counter() - t1
+    return 1.0 / sec_per_tok, threads, dt, it
 
 
 def cpu_model():
@@ -156,22 +199,45 @@ def cpu_model():
     return "unknown"
 
 
+def _cpu_sample_text(workload, it, dt):
+    reps = f" x {it} iters ({dt:.1f} s)" if it else ""
+    if workload == "gpt1.3b":
+        return (f"1 GPT-1.3B layer fwd+bwd{reps} on 1x{GPT_SEQ} causal tokens + the tied LM head and CE on the "
+                f"same tokens, torch fp32 CPU oracle (oracle/tp.py), scaled to 24 layers + head")
+    return (f"1 BERT-large layer fwd+bwd{reps} on 1x{SEQ} tokens, torch fp32 CPU oracle (oracle/tp.py), "
+            f"scaled to the 24-layer stack")
+
+
+def _config(workload, world, args):
+    if workload == "gpt1.3b":
+        return {"workload": "gpt3-1.3b-24L-vocab-parallel-lm (BASELINE.json configs[2] shapes)",
+                "model": "GPT-3 1.3B: 24L H2048 16x128 FFN8192 causal pre-LN gelu_tanh dropout0.1, vocab-parallel "
+                         "embedding V=50257->50304 + tied LM head + vocab-parallel CE",
+                "global_batch": GPT_BATCH_PER_GPU * world, "per_gpu_batch": GPT_BATCH_PER_GPU, "seq_len": GPT_SEQ,
+                "parallelism": f"tp{world} ({args.optimize} mode, TP across DP ranks)",
+                "tp_comm": args.tp_comm, "l2": "inputs larger than L2 (logits alone 1.6 GB per step)"}
+    return {"workload": "bert-large-24L-tp-layer-stack (BASELINE.json configs[1])",
+            "model": "BERT-large DistributedTransformer 24L H1024 16x64 FFN4096 post-LN gelu dropout0.1",
+            "global_batch": BATCH_PER_GPU * world, "per_gpu_batch": BATCH_PER_GPU, "seq_len": SEQ,
+            "parallelism": f"tp{world} ({args.optimize} mode, TP across DP ranks)",
+            "tp_comm": args.tp_comm, "l2": "inputs larger than L2 (saved activations ~6 GB per step)"}
+
+
 def run_reference(args, rank):
     if rank != 0:
         return
     steps = []
     for i in range(args.warmup + args.steps):
-        v, threads, dt, it = cpu_reference_sample(max_seconds=args.ref_seconds, min_iters=1)
+        v, threads, dt, it = cpu_reference_sample(max_seconds=args.ref_seconds, min_iters=1,
+                                                  workload=args.workload)
         if i >= args.warmup:
             steps.append(v)
     value = statistics.median(steps)
-    sample = (f"1 BERT-large layer fwd+bwd on 1x{SEQ} tokens, torch fp32 CPU oracle (oracle/tp.py), "
-              f"scaled to the 24-layer stack; {cpu_model()}")
+    sample = _cpu_sample_text(args.workload, None, None) + f"; {cpu_model()}"
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-            "config": {"workload": "bert-large-24L-tp-layer-stack", "global_batch": BATCH_PER_GPU * args.gpus,
-                       "seq_len": SEQ, "parallelism": f"tp{args.gpus}"},
+            "config": _config(args.workload, args.gpus, args),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -250,15 +316,31 @@ def run_gpu(args, rank, world, local):
               "tp_overlap_sms": args.tp_overlap_sms if args.tp_overlap_sms >= 0 else (96 if world >= 4 else 0)})
     STATE_OVERLAP["sms"] = smp.state.STATE.config.get("tp_overlap_sms", 0) if world > 1 else 0
     torch.manual_seed(1000 + rank)
-    model = smp.nn.DistributedTransformer(**CFG)
+    gpt = args.workload == "gpt1.3b"
+    if gpt:
+        # token ids in, per-token CE out: the LM objective (mean over valid tokens) is backpropagated
+        model = smp.nn.DistributedTransformerLMHead(**GPT_CFG)
+        B, s, H = GPT_BATCH_PER_GPU, GPT_SEQ, GPT_CFG["hidden_size"]
+        g = torch.Generator().manual_seed(7 + rank)
+        ids_h = torch.randint(0, GPT_CFG["vocab_size"], (B, s), generator=g)
+        lab_h = torch.full_like(ids_h, -100)
+        lab_h[:, :-1] = ids_h[:, 1:]  # next-token targets of uniform-random tokens
+        x, dy = ids_h.cuda(), lab_h.cuda()
+    else:
+        model = smp.nn.DistributedTransformer(**CFG)
+        B, s, H = BATCH_PER_GPU, SEQ, CFG["hidden_size"]
+        x = torch.randn(B, s, H, device="cuda", dtype=torch.bfloat16, requires_grad=True)
+        dy = torch.randn(B, s, H, device="cuda", dtype=torch.bfloat16)
     model.train()
-    B, s, H = BATCH_PER_GPU, SEQ, CFG["hidden_size"]
-    x = torch.randn(B, s, H, device="cuda", dtype=torch.bfloat16, requires_grad=True)
-    dy = torch.randn(B, s, H, device="cuda", dtype=torch.bfloat16)
+    n_valid = B * (s - 1)
 
     def step(inp, grad):
         for prm in model.parameters():
             prm.grad = None
+        if gpt:
+            loss = model(inp, labels=grad).sum() / n_valid
+            loss.backward()
+            return loss
         y = model(inp)
         y.backward(grad)
         return y
@@ -320,11 +402,14 @@ def run_gpu(args, rank, world, local):
     value = tokens_step / (ms / 1e3)
 
     # -------- e2e through the public API: pinned host input + upstream grad in, loss out
-    xh = torch.randn(B, s, H, dtype=torch.bfloat16).pin_memory()
-    dyh = torch.randn(B, s, H, dtype=torch.bfloat16).pin_memory()
+    if gpt:  # token ids + targets in, the mean loss out
+        xh, dyh = ids_h.pin_memory(), lab_h.pin_memory()
+    else:
+        xh = torch.randn(B, s, H, dtype=torch.bfloat16).pin_memory()
+        dyh = torch.randn(B, s, H, dtype=torch.bfloat16).pin_memory()
     lossh = torch.empty(1, dtype=torch.float32).pin_memory()
-    xd = torch.empty(B, s, H, device="cuda", dtype=torch.bfloat16)
-    dyd = torch.empty_like(xd)
+    xd = torch.empty_like(x)
+    dyd = torch.empty_like(dy)
 
     def e2e_step():
         if args.graph:
@@ -336,9 +421,10 @@ def run_gpu(args, rank, world, local):
         else:
             xd.copy_(xh, non_blocking=True)
             dyd.copy_(dyh, non_blocking=True)
-            y = step(xd.detach().requires_grad_(True), dyd)
+            y = step(xd if gpt else xd.detach().requires_grad_(True), dyd)
             g = dyd
-        lossh.copy_((y.detach().float() * g.float()).sum().reshape(1), non_blocking=True)
+        out = y.detach().float().reshape(1) if gpt else (y.detach().float() * g.float()).sum().reshape(1)
+        lossh.copy_(out, non_blocking=True)
 
     e2e_step()
     torch.cuda.synchronize()
@@ -357,33 +443,40 @@ def run_gpu(args, rank, world, local):
         return
     peaks, peak_kind = load_peaks()
     peak_sus = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    peak_burst = peaks["bf16_tflops"]
+    # the roofline denominator follows the clocks the kernels actually ran at: a short bench at
+    # the maximum SM clock is compared with the BURST peak (measured at max clock); only a run whose
+    # median SM clock under load sat clearly below max uses the sustained figure
+    at_max = bool(clocks.get("sm_mhz") and clocks.get("sm_max_mhz") and clocks["sm_mhz"] >= 0.95 * clocks["sm_max_mhz"])
+    peak_roof = peak_burst if (at_max or clocks.get("sm_mhz") is None) else peak_sus
     achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
-    flops_tok = flops_per_token_layer() * CFG["num_layers"]
+    flops_tok = flops_per_token(args.workload)
     model_tflops = value / world * flops_tok / 1e12  # per GPU
     cpu = None
     if not args.skip_cpu_baseline:
-        v, threads, dt, it = cpu_reference_sample(max_seconds=args.ref_seconds)
+        v, threads, dt, it = cpu_reference_sample(max_seconds=args.ref_seconds, workload=args.workload)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"1 BERT-large layer fwd+bwd x {it} iters on 1x{SEQ} tokens ({dt:.1f} s), torch fp32 "
-                         f"CPU oracle, scaled to 24 layers; {cpu_model()}"}
+               "sample": _cpu_sample_text(args.workload, it, dt) + f"; {cpu_model()}"}
+    cfg_line = _config(args.workload, world, args)
+    cfg_line["tp_overlap_sms"] = STATE_OVERLAP.get("sms", 0)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic tokens' hidden states, random-init weights",
-        "config": {"workload": "bert-large-24L-tp-layer-stack (BASELINE.json configs[1])",
-                   "model": "BERT-large DistributedTransformer 24L H1024 16x64 FFN4096 post-LN gelu dropout0.1",
-                   "global_batch": B * world, "per_gpu_batch": B, "seq_len": s,
-                   "parallelism": f"tp{world} ({args.optimize} mode, TP across DP ranks)",
-                   "tp_comm": args.tp_comm, "tp_overlap_sms": STATE_OVERLAP.get("sms", 0),
-                   "l2": "inputs larger than L2 (saved activations ~6 GB per step)"},
+        "vs_baseline": None, "dtype": "bf16",
+        "data": ("synthetic uniform-random token ids, random-init weights" if gpt else
+                 "synthetic tokens' hidden states, random-init weights"),
+        "config": cfg_line,
         "mfu": {"model_tflops_per_gpu": model_tflops, "flops_per_token": flops_tok,
                 "frac_of_sustained": model_tflops / peak_sus, "frac_of_burst": model_tflops / peaks["bf16_tflops"],
                 "peak_kind": peak_kind},
         "roofline": {"bound": "tensor", "kernel": "smpk gemm_bf16_tcgen05 (all GEMM launches of the step)",
                      "timing": ("CUPTI kernel records of replays of the step graph" if args.graph
                                 else "CUDA events around each GEMM launch (eager)"),
-                     "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s", "frac": achieved / peak_sus,
-                     "peak_kind": f"{peak_kind} bf16_tflops_sustained (kernel timed inside a long step)",
+                     "achieved": achieved, "peak": peak_roof, "unit": "TFLOP/s", "frac": achieved / peak_roof,
+                     "peak_kind": (f"{peak_kind} bf16_tflops (burst: SM clock at max during the timed region)"
+                                   if peak_roof == peak_burst else
+                                   f"{peak_kind} bf16_tflops_sustained (SM clock below max under load)"),
+                     "frac_of_burst": achieved / peak_burst, "frac_of_sustained": achieved / peak_sus,
                      "launches_per_step": gemm_launches // args.steps,
                      "gemm_ms_per_step": gemm_ms / args.steps, "traffic": gemm_traffic(),
                      "traffic_unit": "DRAM bytes per GEMM launch (ncu, profiles/gemm_traffic.json)"},
@@ -402,6 +495,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="smpk", choices=["smpk", "reference"])
+    ap.add_argument("--workload", default="bert-large", choices=["bert-large", "gpt1.3b"],
+                    help="bert-large: BASELINE.json configs[1] (the metric's config, default); gpt1.3b: configs[2] "
+                         "shapes (the north_star's >= 60%% of peak target) with embedding + LM head + CE")
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--graph", type=int, default=1, help="capture the step in a CUDA graph (1) or run eagerly (0)")

@@ -368,6 +368,11 @@ SMPK_API int smpk_p2p_recv(void* dst, const void* local_slot, int64_t bytes, con
  * the same snapshot, so interleaved microbatches (pipeline schedules) stay consistent. */
 SMPK_API int smpk_rng_next(uint64_t* counter, uint64_t* snapshot, void* stream);
 
+/* Debug: per-CTA globaltimer records of the last fused-attention forward launched with
+ * SMPK_FA_TRACE=1 in the environment (20 u64 per CTA; see csrc/flash_attn.cu).  Diagnostics only. */
+SMPK_API int smpk_debug_fa_trace(void* host_out, int n_cta);
+SMPK_API int smpk_debug_fb_trace(void* host_out, int n_cta); /* backward: 32 u64 per CTA */
+
 #ifdef __cplusplus
 }
 #endif

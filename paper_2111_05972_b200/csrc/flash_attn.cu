@@ -41,11 +41,12 @@ struct FaFwdArgs {
   float scale_log2;          // log2(e) / sqrt(dh)
   int causal;
   float inv_keep;
+  int trace;
 };
 
-template <int DH>
+template <int DH, int NS_ = (DH == 64 ? 3 : 1)>
 struct FaFwdCfg {
-  static constexpr int NS = DH == 64 ? 2 : 1;  // K/V ring depth
+  static constexpr int NS = NS_;  // K/V ring depth
   static constexpr int Q_BYTES = FA_BQ * DH * 2;
   static constexpr int K_BYTES = FA_BK * DH * 2;
   static constexpr int V_BYTES = FA_BK * DH * 2;
@@ -59,22 +60,35 @@ struct FaFwdCfg {
   static constexpr uint32_t TMEM_COLS = 512;  // S0 [0,128) S1 [128,256) O0 [256,256+DH) O1 [256+DH, 256+2DH)
 };
 
-template <int DH>
+// debug timeline (SMPK_FA_TRACE=1): per CTA [0] start [1] Q landed (MMA warp) [2..9] group-0 S_j ready
+// [10..17] group-0 P_j stored [18] epilogue done (group 0) [19] %smid
+__device__ unsigned long long g_fa_trace[1024 * 20];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <int DH, int NS_>
 __global__ void __launch_bounds__(FA_THREADS, 1)
     flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const FaFwdArgs a) {
-  using Cfg = FaFwdCfg<DH>;
+  using Cfg = FaFwdCfg<DH, NS_>;
   constexpr int NS = Cfg::NS;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // pointer arithmetic on the __shared__ array (not an integer round trip) keeps the shared
+  // address space visible to the compiler: LDS / STS instead of generic LD / ST
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
+  static_assert(NS <= 4, "K/V ring depth");
   uint64_t* q_full = bar + 0;
   uint64_t* kv_full = bar + 1;        // [NS]
-  uint64_t* kv_empty = bar + 3;       // [NS]
-  uint64_t* s_full = bar + 5;         // [2]
-  uint64_t* p_full = bar + 7;         // [2]
-  uint64_t* o_done = bar + 9;         // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t* kv_empty = bar + 5;       // [NS]
+  uint64_t* s_full = bar + 9;         // [2]
+  uint64_t* p_full = bar + 11;        // [2]
+  uint64_t* o_done = bar + 13;        // [2]
+  uint64_t* s_read = bar + 15;        // [2] softmax group t has loaded S_t into registers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_qt = a.s / FA_BQ;
@@ -100,6 +114,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       mbar_init(&s_full[t], 1);
       mbar_init(&p_full[t], 4);  // one arrive per softmax warp
       mbar_init(&o_done[t], 1);
+      mbar_init(&s_read[t], 4);  // one arrive per softmax warp
     }
     fence_barrier_init();
   }
@@ -108,6 +123,14 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  unsigned long long* trc = (a.trace && cta_lin < 1024) ? g_fa_trace + cta_lin * 20 : nullptr;
+  if (trc && threadIdx.x == 0) {
+    trc[0] = gtime();
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    trc[19] = smid;
+  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -137,13 +160,15 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (whole warp; one elected lane issues) ----------------
+    // Event-driven: S_t(j+1) is issued as soon as softmax group t has READ S_t(j) into registers
+    // (s_read), so the next scores are computed while the group is still exponentiating; P_t(j).V_j
+    // follows p_full.  Both groups' events are polled, so neither waits behind the other's phase.
     const uint32_t idS = make_idesc_bf16(128, FA_BK, false, false);
     const uint32_t idO = make_idesc_bf16(128, DH, false, true);
     const uint32_t q_base = smem_u32(smem + Cfg::OFF_Q);
     const uint32_t p_base = smem_u32(smem + Cfg::OFF_P);
-    auto issue_s = [&](int t, int j) {  // S_t = Q_t K_j^T
+    auto issue_s = [&](int t, int j) {  // S_t = Q_t K_j^T (caller checked kv_full)
       const int st = j % NS;
-      mbar_wait(&kv_full[st], (j / NS) & 1);
       tc_fence_after();
       const uint32_t qb = q_base + t * Cfg::Q_BYTES;
       const uint32_t kbase = smem_u32(smem + Cfg::OFF_K + st * Cfg::K_BYTES);
@@ -158,9 +183,8 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       }
       __syncwarp();
     };
-    auto issue_pv = [&](int t, int j) {  // O_t += P_t V_j
+    auto issue_pv = [&](int t, int j) {  // O_t += P_t V_j (caller checked p_full)
       const int st = j % NS;
-      mbar_wait(&p_full[t], j & 1);
       tc_fence_after();
       const uint32_t pb = p_base + t * Cfg::P_BYTES;
       const uint32_t vbase = smem_u32(smem + Cfg::OFF_V + st * Cfg::V_BYTES);
@@ -177,30 +201,38 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       __syncwarp();
     };
     mbar_wait(q_full, 0);
-    if (nkt0 > 0) issue_s(0, 0);
-    if (nkt1 > 0) issue_s(1, 0);
-    for (int j = 0; j < n_iter; ++j) {
-      // S_t(j+1) overwrites S_t(j): p_full_t(j) implies the softmax group has read it
-      if constexpr (NS > 1) {
-        if (j < nkt0) {
-          issue_pv(0, j);
-          if (j + 1 < nkt0) issue_s(0, j + 1);
+    if (trc && lane == 0) trc[1] = gtime();
+    const int nkt[2] = {nkt0, nkt1};
+    int s_next[2] = {0, 0}, pv_next[2] = {0, 0};
+    int rel = 0;  // next K/V iteration whose ring stage has not been released
+    while (rel < n_iter) {
+      bool progress = false;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int ks = s_next[t];
+        // S_t(ks) may overwrite S_t(ks-1) once the group has loaded it (s_read), and needs K_ks
+        if (ks < nkt[t] && (ks == 0 || mbar_test(&s_read[t], (ks - 1) & 1)) &&
+            mbar_test(&kv_full[ks % NS], (ks / NS) & 1)) {
+          issue_s(t, ks);
+          s_next[t] = ks + 1;
+          progress = true;
         }
-        if (j < nkt1) {
-          issue_pv(1, j);
-          if (j + 1 < nkt1) issue_s(1, j + 1);
+        const int kp = pv_next[t];
+        if (kp < s_next[t] && mbar_test(&p_full[t], kp & 1)) {
+          issue_pv(t, kp);
+          pv_next[t] = kp + 1;
+          progress = true;
         }
-        if (elect_one()) umma_commit(&kv_empty[j % NS]);  // K_j / V_j consumed by every MMA above
-        __syncwarp();
-      } else {
-        // single K/V stage: both P.V products must release it before K_{j+1} can land
-        if (j < nkt0) issue_pv(0, j);
-        if (j < nkt1) issue_pv(1, j);
-        if (elect_one()) umma_commit(&kv_empty[0]);
-        __syncwarp();
-        if (j + 1 < nkt0) issue_s(0, j + 1);
-        if (j + 1 < nkt1) issue_s(1, j + 1);
       }
+      // K/V stage of iteration `rel` is free once every query tile that uses it issued its P.V
+      // (the commit tracks all MMAs issued before it, including the S that read K_rel)
+      while (rel < n_iter && (rel >= nkt0 || pv_next[0] > rel) && (rel >= nkt1 || pv_next[1] > rel)) {
+        if (elect_one()) umma_commit(&kv_empty[rel % NS]);
+        __syncwarp();
+        ++rel;
+        progress = true;
+      }
+      if (!progress) __nanosleep(20);
     }
   } else if (warp >= 4) {
     // ---------------- softmax groups (thread = query row) ----------------
@@ -215,6 +247,9 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     const float* mrow = a.mask ? a.mask + (int64_t)b * a.s : nullptr;
     const uint32_t* krow = a.keep ? a.keep + (((int64_t)b * a.nh + h) * a.s + q) * (a.s / 32) : nullptr;
     uint8_t* p_smem = smem + Cfg::OFF_P + t * Cfg::P_BYTES;
+    // m: the running max the exponents are taken against (log2 domain).  It is only moved when
+    // a row's max grows by more than 8 (P <= 2^8 stays exact enough in bf16 / fp32), so the O
+    // rescale in TMEM is rare; l is kept consistent with m.
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < nkt; ++j) {
       const int key0 = j * FA_BK;
@@ -222,52 +257,63 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       uint4 kw = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
       if (krow) kw = __ldg(reinterpret_cast<const uint4*>(krow + key0 / 32));
       mbar_wait(&s_full[t], j & 1);
+      if (trc && threadIdx.x == 128 && j < 8) trc[2 + j] = gtime();
       tc_fence_after();
       uint32_t sv[128];
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(sv + c * 32));
       tmem_ld_wait();
-      // scaled (+ masked) scores in the log2 domain
-      float x[128];
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_read[t]);  // S_t may now be overwritten by S_t(j+1)
+      // x = log2-domain logits; without a mask the scale is folded into the exponent's FFMA
+      float* x = reinterpret_cast<float*>(sv);
+      float xs = a.scale_log2;
       if (mrow) {
         const float4* mp = reinterpret_cast<const float4*>(mrow + key0);
 #pragma unroll
         for (int k4 = 0; k4 < 32; ++k4) {
           const float4 mk = __ldg(mp + k4);
-          x[4 * k4 + 0] = fmaf(__uint_as_float(sv[4 * k4 + 0]), a.scale_log2, mk.x * 1.4426950408889634f);
-          x[4 * k4 + 1] = fmaf(__uint_as_float(sv[4 * k4 + 1]), a.scale_log2, mk.y * 1.4426950408889634f);
-          x[4 * k4 + 2] = fmaf(__uint_as_float(sv[4 * k4 + 2]), a.scale_log2, mk.z * 1.4426950408889634f);
-          x[4 * k4 + 3] = fmaf(__uint_as_float(sv[4 * k4 + 3]), a.scale_log2, mk.w * 1.4426950408889634f);
+          x[4 * k4 + 0] = fmaf(x[4 * k4 + 0], a.scale_log2, mk.x * 1.4426950408889634f);
+          x[4 * k4 + 1] = fmaf(x[4 * k4 + 1], a.scale_log2, mk.y * 1.4426950408889634f);
+          x[4 * k4 + 2] = fmaf(x[4 * k4 + 2], a.scale_log2, mk.z * 1.4426950408889634f);
+          x[4 * k4 + 3] = fmaf(x[4 * k4 + 3], a.scale_log2, mk.w * 1.4426950408889634f);
         }
-      } else {
-#pragma unroll
-        for (int k = 0; k < 128; ++k) x[k] = __uint_as_float(sv[k]) * a.scale_log2;
+        xs = 1.f;
       }
       if (diag) {
 #pragma unroll
         for (int k = 0; k < 128; ++k)
           if (k > r) x[k] = -INFINITY;
       }
-      float mx = x[0];
+      float mx8[8];
 #pragma unroll
-      for (int k = 1; k < 128; ++k) mx = fmaxf(mx, x[k]);
-      const float m_new = fmaxf(m, mx);
-      const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
-      const float alpha = (m == -INFINITY) ? 0.f : ex2_approx(m - m_use);
-      // P = exp2(x - m); rowsum before dropout; dropped entries zero (1/(1-p) in the epilogue)
+      for (int i = 0; i < 8; ++i) mx8[i] = x[i];
+#pragma unroll
+      for (int k = 8; k < 128; ++k) mx8[k & 7] = fmaxf(mx8[k & 7], x[k]);
+      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * xs;
+      float alpha = 1.f;
+      if (mx > m + 8.f) {  // (also the first finite max: m = -inf)
+        alpha = (m == -INFINITY) ? 0.f : ex2_approx(m - mx);
+        m = mx;
+      }
+      const float m_use = (m == -INFINITY) ? 0.f : m;
+      const float nm = -m_use;
+      // P = exp2(x*xs - m); row sum before dropout; dropped entries zero (1/(1-p) in the epilogue)
       uint32_t pk[64];
-      float rowsum = 0.f;
+      float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       const uint32_t kws[4] = {kw.x, kw.y, kw.z, kw.w};
 #pragma unroll
       for (int k = 0; k < 128; k += 2) {
-        const float p0 = ex2_approx(x[k] - m_use);
-        const float p1 = ex2_approx(x[k + 1] - m_use);
-        rowsum += p0 + p1;
+        const float p0 = ex2_approx(fmaf(x[k], xs, nm));
+        const float p1 = ex2_approx(fmaf(x[k + 1], xs, nm));
+        rs8[(k >> 1) & 7] += p0 + p1;
         const uint32_t w = kws[k >> 5];
         pk[k >> 1] = pack_bf16x2(((w >> (k & 31)) & 1u) ? p0 : 0.f, ((w >> ((k + 1) & 31)) & 1u) ? p1 : 0.f);
       }
+      const float rowsum = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
       l = l * alpha + rowsum;
-      m = m_new;
       if (j > 0) {
         // P.V of tile j-1 must have finished: it reads the P buffer we overwrite below and
         // accumulates into the O we rescale
@@ -300,6 +346,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[t]);
+      if (trc && threadIdx.x == 128 && j < 8) trc[10 + j] = gtime();
     }
     // epilogue: O * (1/(1-p)) / l -> bf16; lse
     if (nkt > 0) {
@@ -322,7 +369,9 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           *reinterpret_cast<uint4*>(orow + c * 32 + g * 8) = u;
         }
       }
-      if (a.lse) a.lse[((int64_t)b * a.nh + h) * a.s + q] = (l > 0.f) ? m + __log2f(l) : -INFINITY;
+      // +inf marks a fully masked row (the backward then recomputes P = exp2(... - lse) = 0)
+      if (a.lse) a.lse[((int64_t)b * a.nh + h) * a.s + q] = (l > 0.f) ? m + __log2f(l) : INFINITY;
+      if (trc && threadIdx.x == 128) trc[18] = gtime();
     }
   }
   tc_fence_before();
@@ -408,16 +457,38 @@ extern "C" int smpk_flash_attn_fwd(const void* qkv, int64_t ld, int B, int nh, i
   a.scale_log2 = scale * 1.4426950408889634f;
   a.causal = causal;
   a.inv_keep = p_drop > 0.f ? 1.f / (1.f - p_drop) : 1.f;
+  static int trace_env = -1, ns_env = -1;
+  if (trace_env < 0) {
+    const char* e = getenv("SMPK_FA_TRACE");
+    trace_env = (e && e[0] == '1') ? 1 : 0;
+    const char* n = getenv("SMPK_FA_NS");
+    ns_env = n ? atoi(n) : 0;
+  }
+  a.trace = trace_env;
   dim3 grid((s / 128 + 1) / 2, nh, B);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (dh == 64) {
-    static unsigned long long once = 0;
-    smem_attr_once(flash_fwd_kernel<64>, FaFwdCfg<64>::SMEM, once);
-    flash_fwd_kernel<64><<<grid, FA_THREADS, FaFwdCfg<64>::SMEM, st>>>(tq, tk, tv, a);
+    if (ns_env == 2) {
+      static unsigned long long once = 0;
+      smem_attr_once(flash_fwd_kernel<64, 2>, FaFwdCfg<64, 2>::SMEM, once);
+      flash_fwd_kernel<64, 2><<<grid, FA_THREADS, FaFwdCfg<64, 2>::SMEM, st>>>(tq, tk, tv, a);
+    } else {
+      static unsigned long long once = 0;
+      smem_attr_once(flash_fwd_kernel<64, 3>, FaFwdCfg<64, 3>::SMEM, once);
+      flash_fwd_kernel<64, 3><<<grid, FA_THREADS, FaFwdCfg<64, 3>::SMEM, st>>>(tq, tk, tv, a);
+    }
   } else {
     static unsigned long long once = 0;
-    smem_attr_once(flash_fwd_kernel<128>, FaFwdCfg<128>::SMEM, once);
-    flash_fwd_kernel<128><<<grid, FA_THREADS, FaFwdCfg<128>::SMEM, st>>>(tq, tk, tv, a);
+    smem_attr_once(flash_fwd_kernel<128, 1>, FaFwdCfg<128, 1>::SMEM, once);
+    flash_fwd_kernel<128, 1><<<grid, FA_THREADS, FaFwdCfg<128, 1>::SMEM, st>>>(tq, tk, tv, a);
   }
   return check_launch("smpk_flash_attn_fwd");
+}
+
+// debug: copy the forward timeline records of the last traced launch (SMPK_FA_TRACE=1)
+extern "C" int smpk_debug_fa_trace(void* host_out, int n_cta) {
+  if (n_cta > 1024) n_cta = 1024;
+  cudaError_t e = cudaMemcpyFromSymbol(host_out, smpk::g_fa_trace, (size_t)n_cta * 20 * 8);
+  SMPK_REQUIRE(e == cudaSuccess, SMPK_ERR_CUDA, "smpk_debug_fa_trace: %s", cudaGetErrorString(e));
+  return SMPK_OK;
 }

@@ -26,6 +26,28 @@ int make_tma_4d(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer,
                 int nb2, int64_t s2, int box_inner, int box_outer, const char* name);
 int make_tma_4d_b32(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t ld, int box_inner,
                     int box_outer, const char* name);
+int make_tma_4d_f32sw(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t ld, int box_inner,
+                      int box_outer, const char* name);
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(0), "r"(0)
+               : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.4d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(0), "r"(0)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 constexpr int FB_THREADS = 256;
 
@@ -41,7 +63,9 @@ struct FaBwdArgs {
   bf16* dqkv;
   int64_t ld;  // of qkv / dqkv
   int64_t H;   // nh * dh
-  float* dq_part;  // [n_kt][B*s][H]
+  float* dq_part;  // [n_kt][B*s][H] (v1 kernel)
+  int trace;
+  int* dq_cnt;     // [B][nh][n_qt] contributors of each query tile's dQ so far (zeroed by the delta kernel)
 };
 
 template <int DH>
@@ -70,7 +94,9 @@ __global__ void __launch_bounds__(FB_THREADS, (DH == 64 ? 2 : 1))
                      const __grid_constant__ CUtensorMap tmBits, const FaBwdArgs a) {
   using Cfg = FaBwdCfg<DH>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // pointer arithmetic on the __shared__ array (not an integer round trip) keeps the shared
+  // address space visible to the compiler: LDS / STS instead of generic LD / ST
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
   uint64_t* kv_full = bar + 0;
   uint64_t* qdo_full = bar + 1;
@@ -380,13 +406,521 @@ __global__ void __launch_bounds__(FB_THREADS, (DH == 64 ? 2 : 1))
   }
 }
 
+// ===========================================================================
+// Pipelined backward (default).  CTA = (key tile j, head, sample), one CTA per SM, 512 threads:
+//   warp 0      TMA producer: K_j, V_j once; per query tile i a stage {Q_i, dO_i, lse_i, Delta_i,
+//               keep bits} (NQ stages: the next tile streams in while this one computes)
+//   warp 1      MMA issuer:  S(t+1) = Q K^T into the other A buffer while tile t is in its
+//               softmax passes; dV += Pd^T dO, dP = dO V^T; dK += dS^T Q, dQ = dS K (own region)
+//   warp 2      TMEM allocator (512 columns)
+//   warps 4-11  softmax backward, 8 warps: query row = TMEM lane (warp % 4), key half = warp / 4
+//   warps 12-15 dQ drain (fp32 partial per key tile, summed in key-tile order by
+//               smpk_flash_dq_reduce) overlapping the next tile, then the dK / dV epilogue
+// TMEM: A0 [0,128), A1 [128,256) (S -> dP, NA = 2 buffers at dh = 64), dV, dK, dQ.
+// ===========================================================================
+constexpr int FB2_THREADS = 512;
+
+// debug timeline (SMPK_FA_TRACE=1): per CTA 32 u64: [0] start [1] K/V landed (MMA warp), per tile t < 4:
+// [2+t] S^T ready [6+t] P stored [10+t] dP^T ready [14+t] dS stored [18+t] dQ ready [22+t] dQ drained
+// (elementwise warp 4 / drain warp 12, lane 0) [26] end [27] %smid
+__device__ unsigned long long g_fb_trace[2048 * 64];
+__device__ __forceinline__ unsigned long long gtime_b() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <int DH>
+struct FaBwd2Cfg {
+  static constexpr int NA = DH == 64 ? 2 : 1;  // S^T / dP^T TMEM buffers
+  static constexpr int NQ = DH == 64 ? 2 : 1;  // query-tile smem stages
+  static constexpr int TILE = 128 * DH * 2;
+  static constexpr int OFF_K = 0;
+  static constexpr int OFF_V = OFF_K + TILE;
+  static constexpr int OFF_PDT = OFF_V + TILE;        // Pd^T (128 x 128 bf16)
+  static constexpr int OFF_DST = OFF_PDT + 32768;     // dS^T
+  static constexpr int OFF_STAGE = OFF_DST + 32768;   // NQ x {Q, dO, lse, Delta, bits}
+  static constexpr int ST_Q = 0, ST_DO = TILE, ST_LSE = 2 * TILE, ST_DELTA = ST_LSE + 512, ST_BITS = ST_DELTA + 512;
+  static constexpr int STAGE_BYTES = ST_BITS + 2048;
+  static constexpr int OFF_KBT = OFF_STAGE + NQ * STAGE_BYTES;  // the key tile's additive mask (128 fp32)
+  static constexpr int SG = DH == 64 ? 2 : 1;                   // dQ staging boxes [128 rows x 32 fp32]
+  static constexpr int OFF_DQS = (OFF_KBT + 512 + 1023) / 1024 * 1024;
+  static constexpr int OFF_BAR = OFF_DQS + SG * 16384;
+  static constexpr int SMEM = 1024 + OFF_BAR + 256;
+  static constexpr uint32_t COL_A = 0, COL_DV = NA * 128, COL_DK = COL_DV + DH, COL_DQ = COL_DK + DH;
+  static_assert(COL_DQ + DH <= 512, "TMEM budget");
+  static_assert(SMEM <= 232448, "smem budget");
+};
+
+template <int DH>
+__global__ void __launch_bounds__(FB2_THREADS, 1)
+    flash_bwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                      const __grid_constant__ CUtensorMap tmBits, const __grid_constant__ CUtensorMap tmDQ,
+                      const FaBwdArgs a) {
+  using Cfg = FaBwd2Cfg<DH>;
+  constexpr int NA = Cfg::NA, NQ = Cfg::NQ;
+  extern __shared__ uint8_t smem_raw[];
+  // pointer arithmetic on the __shared__ array (not an integer round trip) keeps the shared
+  // address space visible to the compiler: LDS / STS instead of generic LD / ST
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* qdo_full = bar + 1;   // [NQ]
+  uint64_t* qdo_empty = bar + 3;  // [NQ]
+  uint64_t* s_full = bar + 5;     // [NA]
+  uint64_t* p_full = bar + 7;
+  uint64_t* dp_full = bar + 8;
+  uint64_t* ds_full = bar + 9;
+  uint64_t* pdt_free = bar + 10;
+  uint64_t* dst_free = bar + 11;
+  uint64_t* dq_full = bar + 12;
+  uint64_t* dq_free = bar + 13;
+  uint64_t* kv_done = bar + 14;
+  uint64_t* dqa_full = bar + 15;  // the earlier key tiles' dQ sum landed in the staging boxes
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_kt = a.s / 128;
+  const int j = (int)blockIdx.x;  // key tile
+  const int h = blockIdx.y, b = blockIdx.z;
+  // query tile processed at step t: causal i = j + t; otherwise rotated, i = (j + t) mod n_kt, so the
+  // key-tile CTAs of one (head, sample) work on different query tiles at every step and tile i's
+  // dQ contributions arrive in step order (contribution number t; see the drain warps)
+  const int nt = a.causal ? n_kt - j : n_kt;
+  auto qtile = [&](int t) { return a.causal ? j + t : (j + t) % n_kt; };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmDO);
+    if (a.dropout) tma_prefetch_desc(&tmBits);
+    mbar_init(kv_full, 1);
+    for (int u = 0; u < NQ; ++u) {
+      mbar_init(&qdo_full[u], 1);
+      mbar_init(&qdo_empty[u], 1);
+    }
+    for (int u = 0; u < NA; ++u) mbar_init(&s_full[u], 1);
+    mbar_init(p_full, 8);  // one arrive per softmax warp
+    mbar_init(dp_full, 1);
+    mbar_init(ds_full, 8);
+    mbar_init(pdt_free, 1);
+    mbar_init(dst_free, 1);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_free, 4);  // one arrive per drain warp
+    mbar_init(kv_done, 1);
+    mbar_init(dqa_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int64_t bh_row = ((int64_t)b * a.nh + h) * a.s;
+  const int cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  unsigned long long* trc = (a.trace && cta_lin < 2048) ? g_fb_trace + cta_lin * 64 : nullptr;
+  if (trc && threadIdx.x == 0) {
+    trc[0] = gtime_b();
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    trc[27] = smid;
+  }
+#define FB_TR(slot)                                      \
+  do {                                                   \
+    if (trc && lane == 0 && t < 4) trc[(slot) + t] = gtime_b(); \
+  } while (0)
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      mbar_arrive_expect_tx(kv_full, 2 * Cfg::TILE);
+#pragma unroll
+      for (int c = 0; c < DH / 64; ++c) {
+        tma_load_4d(smem + Cfg::OFF_K + c * 16384, &tmK, kv_full, c * 64, j * 128, h, b);
+        tma_load_4d(smem + Cfg::OFF_V + c * 16384, &tmV, kv_full, c * 64, j * 128, h, b);
+      }
+      for (int t = 0; t < nt; ++t) {
+        const int i = qtile(t), u = t % NQ;
+        if (t >= NQ) mbar_wait(&qdo_empty[u], ((t / NQ) - 1) & 1);
+        uint8_t* stg = smem + Cfg::OFF_STAGE + u * Cfg::STAGE_BYTES;
+        mbar_arrive_expect_tx(&qdo_full[u], 2 * Cfg::TILE + 1024 + (a.dropout ? 2048 : 0));
+        const int64_t off = bh_row + (int64_t)i * 128;
+#pragma unroll
+        for (int c = 0; c < DH / 64; ++c) {
+          tma_load_4d(stg + Cfg::ST_Q + c * 16384, &tmQ, &qdo_full[u], c * 64, i * 128, h, b);
+          tma_load_4d(stg + Cfg::ST_DO + c * 16384, &tmDO, &qdo_full[u], c * 64, i * 128, h, b);
+        }
+        bulk_load(stg + Cfg::ST_LSE, a.lse + off, 512, &qdo_full[u]);
+        bulk_load(stg + Cfg::ST_DELTA, a.delta + off, 512, &qdo_full[u]);
+        if (a.dropout) tma_load_4d(stg + Cfg::ST_BITS, &tmBits, &qdo_full[u], j * 4, (int)off, 0, 0);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (whole warp; one elected lane issues) ----------------
+    // Query rows on the TMEM lanes: S = Q K^T and dP = dO V^T (M = queries); P / dS live in smem
+    // as [query rows x keys] (K-major for dQ = dS K, and the MN-major A operand of
+    // dV += P^T dO / dK += dS^T Q, M = keys).
+    const uint32_t idQK = make_idesc_bf16(128, 128, false, false);  // S, dP
+    const uint32_t idTM = make_idesc_bf16(128, DH, true, true);     // dV, dK: A = P^T / dS^T (MN-major)
+    const uint32_t idKM = make_idesc_bf16(128, DH, false, true);    // dQ: A = dS (K-major), B = K (MN-major)
+    const uint32_t k_base = smem_u32(smem + Cfg::OFF_K), v_base = smem_u32(smem + Cfg::OFF_V);
+    const uint32_t pdt = smem_u32(smem + Cfg::OFF_PDT), dst = smem_u32(smem + Cfg::OFF_DST);
+    const uint32_t tdV = tmem + Cfg::COL_DV, tdK = tmem + Cfg::COL_DK, tdQ = tmem + Cfg::COL_DQ;
+    auto stage_base = [&](int t) { return smem_u32(smem + Cfg::OFF_STAGE + (t % NQ) * Cfg::STAGE_BYTES); };
+    auto issue_s = [&](int t) {  // S(t) = Q_t K^T -> A[t % NA]
+      mbar_wait(&qdo_full[t % NQ], (t / NQ) & 1);
+      tc_fence_after();
+      const uint32_t qb = stage_base(t) + Cfg::ST_Q;
+      if (elect_one()) {
+#pragma unroll
+        for (int c = 0; c < DH / 64; ++c)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(tmem + (t % NA) * 128, make_sw128_desc(qb + c * 16384 + k * 32, 16, 1024),
+                      make_sw128_desc(k_base + c * 16384 + k * 32, 16, 1024), idQK, (c | k) != 0);
+        umma_commit(&s_full[t % NA]);
+      }
+      __syncwarp();
+    };
+    mbar_wait(kv_full, 0);
+    if (trc && lane == 0) trc[1] = gtime_b();
+    if (nt > 0) issue_s(0);
+    for (int t = 0; t < nt; ++t) {
+      const uint32_t tA = tmem + (t % NA) * 128;
+      const uint32_t dob = stage_base(t) + Cfg::ST_DO, qb = stage_base(t) + Cfg::ST_Q;
+      // the next tile's scores while this tile is in its softmax passes (its A buffer's dP was
+      // consumed by tile t-1's dS pass, waited below in the previous iteration)
+      if (NA == 2 && t + 1 < nt) issue_s(t + 1);
+      mbar_wait(p_full, t & 1);  // Pd(t) in smem; S(t) read
+      tc_fence_after();
+      if (elect_one()) {  // dV += Pd^T dO ; dP = dO V^T -> A[t % NA]
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          umma_bf16(tdV, make_sw128_desc(pdt + k * 2048, 16384, 1024), make_sw128_desc(dob + k * 2048, 16384, 1024),
+                    idTM, (t > 0) || (k != 0));
+        umma_commit(pdt_free);
+#pragma unroll
+        for (int c = 0; c < DH / 64; ++c)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(tA, make_sw128_desc(dob + c * 16384 + k * 32, 16, 1024),
+                      make_sw128_desc(v_base + c * 16384 + k * 32, 16, 1024), idQK, (c | k) != 0);
+        umma_commit(dp_full);
+      }
+      __syncwarp();
+      mbar_wait(ds_full, t & 1);  // dS(t) in smem; dP(t) read
+      if (t > 0) mbar_wait(dq_free, (t - 1) & 1);  // dQ(t-1) drained
+      tc_fence_after();
+      if (elect_one()) {  // dK += dS^T Q ; dQ = dS K
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          umma_bf16(tdK, make_sw128_desc(dst + k * 2048, 16384, 1024), make_sw128_desc(qb + k * 2048, 16384, 1024),
+                    idTM, (t > 0) || (k != 0));
+#pragma unroll
+        for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(tdQ, make_sw128_desc(dst + kb * 16384 + k * 32, 16, 1024),
+                      make_sw128_desc(k_base + kb * 8192 + k * 2048, 16384, 1024), idKM, (kb | k) != 0);
+        umma_commit(dq_full);
+        umma_commit(dst_free);
+        umma_commit(&qdo_empty[t % NQ]);
+        if (t == nt - 1) umma_commit(kv_done);
+      }
+      __syncwarp();
+      if (NA == 1 && t + 1 < nt) issue_s(t + 1);
+    }
+  } else if (warp >= 4 && warp < 12) {
+    // ---------------- softmax backward: query row qr = TMEM lane, 64 keys per warp ----------------
+    // per-query lse / Delta are per-thread scalars and the keep bits of (query, 64 keys) are two
+    // words of the thread's own row, so the shared-memory traffic per element is the 2-byte P / dS
+    // store only (the MIO queue was the limiter with key rows on the lanes)
+    const int e = warp - 4;
+    const int lq = e & 3, qh = e >> 2;
+    const int qr = lq * 32 + lane;
+    const uint32_t t_lane = static_cast<uint32_t>(lq * 32) << 16;
+    uint8_t* pd_s = smem + Cfg::OFF_PDT + qh * 16384;  // this warp's 64-key chunk
+    uint8_t* ds_s = smem + Cfg::OFF_DST + qh * 16384;
+    float* mk_s = reinterpret_cast<float*>(smem + Cfg::OFF_KBT);  // additive mask (log2 domain) of the keys
+    const int tid = threadIdx.x - 128;  // 0..255
+    if (a.mask) {
+      if (tid < 128) mk_s[tid] = a.mask[(int64_t)b * a.s + j * 128 + tid] * 1.4426950408889634f;
+      named_barrier_sync(1, 256);
+    }
+    const float scale_log2 = a.scale_log2, inv_keep = a.inv_keep;
+    for (int t = 0; t < nt; ++t) {
+      const int i = qtile(t);
+      const bool diag = a.causal && (i == j);
+      const uint8_t* stg = smem + Cfg::OFF_STAGE + (t % NQ) * Cfg::STAGE_BYTES;
+      mbar_wait(&qdo_full[t % NQ], (t / NQ) & 1);
+      const float nls = -reinterpret_cast<const float*>(stg + Cfg::ST_LSE)[qr];  // +inf lse: masked row
+      const float dlt = reinterpret_cast<const float*>(stg + Cfg::ST_DELTA)[qr];
+      uint32_t kw0 = 0xffffffffu, kw1 = 0xffffffffu;
+      if (a.dropout) {
+        const uint2 w = *reinterpret_cast<const uint2*>(stg + Cfg::ST_BITS + qr * 16 + qh * 8);
+        kw0 = w.x;
+        kw1 = w.y;
+      }
+      mbar_wait(&s_full[t % NA], (t / NA) & 1);
+      if (e == 0) FB_TR(2);
+      tc_fence_after();
+      const uint32_t tA = tmem + (t % NA) * 128 + t_lane + qh * 64;
+      // ---- P pass: P (bf16, kept for dS) and Pd = keep ? P : 0 -> smem
+      uint32_t pp[32];
+      uint32_t sv[64];
+      tmem_ld_32x32b_x32(tA, *reinterpret_cast<uint32_t(*)[32]>(sv));
+      tmem_ld_32x32b_x32(tA + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+      tmem_ld_wait();
+      if (e == 0) FB_TR(32);
+      if (t > 0) mbar_wait(pdt_free, (t - 1) & 1);  // dV(t-1) has read Pd
+      if (e == 0) FB_TR(36);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {  // 8 keys per 16-B granule
+        float pr[8];
+        if (a.mask) {
+          const float4 m0 = *reinterpret_cast<const float4*>(mk_s + qh * 64 + c * 8);
+          const float4 m1 = *reinterpret_cast<const float4*>(mk_s + qh * 64 + c * 8 + 4);
+          const float mm[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            pr[u] = ex2_approx(fmaf(__uint_as_float(sv[c * 8 + u]), scale_log2, mm[u] + nls));
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) pr[u] = ex2_approx(fmaf(__uint_as_float(sv[c * 8 + u]), scale_log2, nls));
+        }
+        if (diag) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (qh * 64 + c * 8 + u > qr) pr[u] = 0.f;  // key after query
+        }
+        const uint32_t w = c < 4 ? kw0 : kw1;
+        const int sh = (c & 3) * 8;
+        uint32_t pd[4];
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) {
+          pp[(c * 8 + u) >> 1] = pack_bf16x2(pr[u], pr[u + 1]);
+          pd[u >> 1] = pack_bf16x2(((w >> (sh + u)) & 1u) ? pr[u] : 0.f, ((w >> (sh + u + 1)) & 1u) ? pr[u + 1] : 0.f);
+        }
+        *reinterpret_cast<uint4*>(pd_s + sw128_offset(qr, c)) = make_uint4(pd[0], pd[1], pd[2], pd[3]);
+      }
+      if (e == 0) FB_TR(40);
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      if (e == 0) FB_TR(6);
+      // ---- dS pass: dS = P * (keep ? dP/(1-p) : 0  - Delta)
+      mbar_wait(dp_full, t & 1);
+      if (e == 0) FB_TR(10);
+      tc_fence_after();
+      tmem_ld_32x32b_x32(tA, *reinterpret_cast<uint32_t(*)[32]>(sv));
+      tmem_ld_32x32b_x32(tA + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+      tmem_ld_wait();
+      if (t > 0) mbar_wait(dst_free, (t - 1) & 1);  // dK / dQ(t-1) have read dS
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint32_t w = c < 4 ? kw0 : kw1;
+        const int sh = (c & 3) * 8;
+        uint32_t dsw[4];
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) {
+          const float2 pf = unpack_bf16x2(pp[(c * 8 + u) >> 1]);
+          const float dp0 = ((w >> (sh + u)) & 1u) ? __uint_as_float(sv[c * 8 + u]) * inv_keep : 0.f;
+          const float dp1 = ((w >> (sh + u + 1)) & 1u) ? __uint_as_float(sv[c * 8 + u + 1]) * inv_keep : 0.f;
+          dsw[u >> 1] = pack_bf16x2(pf.x * (dp0 - dlt), pf.y * (dp1 - dlt));
+        }
+        *reinterpret_cast<uint4*>(ds_s + sw128_offset(qr, c)) = make_uint4(dsw[0], dsw[1], dsw[2], dsw[3]);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ds_full);
+      if (e == 0) FB_TR(14);
+    }
+    // dK (scaled; warps 4-7) and dV (1/(1-p); warps 8-11) rows of this key tile -> dqkv (bf16),
+    // written while the drain warps finish the last dQ tile
+    if (nt > 0) {
+      mbar_wait(kv_done, 0);
+      tc_fence_after();
+    }
+    {
+      const int key = j * 128 + qr;  // key row = TMEM lane of the dK / dV accumulators
+      bf16* orow = a.dqkv + ((int64_t)b * a.s + key) * a.ld + (qh ? 2 * a.H : a.H) + (int64_t)h * DH;
+      const float sc = qh ? a.inv_keep : a.scale;
+      const uint32_t col = qh ? Cfg::COL_DV : Cfg::COL_DK;
+#pragma unroll
+      for (int c = 0; c < DH / 32; ++c) {
+        uint32_t kv[32];
+        if (nt > 0) {
+          tmem_ld_32x32b_x32(tmem + col + t_lane + c * 32, kv);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) kv[q] = 0u;
+        }
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          uint4 u;
+          u.x = pack_bf16x2(__uint_as_float(kv[g * 8 + 0]) * sc, __uint_as_float(kv[g * 8 + 1]) * sc);
+          u.y = pack_bf16x2(__uint_as_float(kv[g * 8 + 2]) * sc, __uint_as_float(kv[g * 8 + 3]) * sc);
+          u.z = pack_bf16x2(__uint_as_float(kv[g * 8 + 4]) * sc, __uint_as_float(kv[g * 8 + 5]) * sc);
+          u.w = pack_bf16x2(__uint_as_float(kv[g * 8 + 6]) * sc, __uint_as_float(kv[g * 8 + 7]) * sc);
+          *reinterpret_cast<uint4*>(orow + c * 32 + g * 8) = u;
+        }
+      }
+    }
+  } else if (warp >= 12) {
+    // ---------------- dQ drain (query row = TMEM lane), then the dK / dV epilogue ----------------
+    // dQ of query tile i is the sum over key tiles j of dS_ij K_j.  The key-tile CTAs add their
+    // terms into an fp32 accumulator in ascending j order (bit-deterministic): j = 0 TMA-stores,
+    // later ones TMA reduce-add (the add happens in L2, off the SM's load/store pipe), each after
+    // the previous contributor released the tile's counter; the last contributor instead loads
+    // the sum of the others, adds its own term in registers and writes bf16 dQ into dqkv.
+    const int lq = warp & 3;
+    const int rr = lq * 32 + lane;
+    const uint32_t t_lane = static_cast<uint32_t>(lq * 32) << 16;
+    const bool issuer = (warp == 12 && lane == 0);
+    uint8_t* dqs = smem + Cfg::OFF_DQS;
+    uint32_t dqa_phase = 0;
+    int* cnt_base = a.dq_cnt + ((int64_t)b * a.nh + h) * n_kt;
+    for (int t = 0; t < nt; ++t) {
+      const int i = qtile(t);
+      // this CTA is contribution number t of query tile i's dQ (causal: key tiles i, i-1, ..., 0;
+      // otherwise j = i, i-1, ... mod n_kt): wait until t earlier contributions are complete
+      const int ncontrib = a.causal ? i + 1 : n_kt;
+      const bool firstc = (t == 0), lastc = (t == ncontrib - 1);
+      int* cnt = cnt_base + i;
+      const int row0 = b * a.s + i * 128;
+      mbar_wait(dq_full, t & 1);
+      if (warp == 12) FB_TR(18);
+      tc_fence_after();
+      bool my_turn = firstc;  // (issuer) the previous contributors are done with this tile
+#pragma unroll 1
+      for (int hf = 0; hf < DH / 64; ++hf) {
+        uint32_t o[64];
+        tmem_ld_32x32b_x32(tmem + Cfg::COL_DQ + t_lane + hf * 64, *reinterpret_cast<uint32_t(*)[32]>(o));
+        tmem_ld_32x32b_x32(tmem + Cfg::COL_DQ + t_lane + hf * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(o + 32));
+        tmem_ld_wait();
+        if (hf == DH / 64 - 1) {  // dQ(t) is in registers: the next dQ MMA may overwrite it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(dq_free);
+        }
+        float* v = reinterpret_cast<float*>(o);
+#pragma unroll
+        for (int q = 0; q < 64; ++q) v[q] = __uint_as_float(o[q]) * a.scale;
+        if (!lastc) {
+#pragma unroll
+          for (int g0 = 0; g0 < 2; g0 += Cfg::SG) {
+#pragma unroll
+            for (int gg = 0; gg < Cfg::SG; ++gg) {
+              uint8_t* box = dqs + gg * 16384 + rr * 128;
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const float* src = v + (g0 + gg) * 32 + q * 4;
+                *reinterpret_cast<float4*>(box + ((q ^ (rr & 7)) << 4)) = make_float4(src[0], src[1], src[2], src[3]);
+              }
+            }
+            fence_proxy_async_smem();
+            named_barrier_sync(3, 128);
+            if (issuer) {
+              if (!my_turn) {
+                while (ld_acquire_gpu(cnt) != t) __nanosleep(32);
+                fence_proxy_async_global();
+                my_turn = true;
+              }
+#pragma unroll
+              for (int gg = 0; gg < Cfg::SG; ++gg) {
+                const int c0 = h * DH + hf * 64 + (g0 + gg) * 32;
+                if (firstc)
+                  tma_store_2d(&tmDQ, dqs + gg * 16384, c0, row0);
+                else
+                  tma_reduce_add_2d(&tmDQ, dqs + gg * 16384, c0, row0);
+              }
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+              asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging reusable
+            }
+            named_barrier_sync(3, 128);
+          }
+        } else {
+          if (!firstc) {  // add the earlier key tiles' sum
+#pragma unroll
+            for (int g0 = 0; g0 < 2; g0 += Cfg::SG) {
+              if (issuer) {
+                if (!my_turn) {
+                  while (ld_acquire_gpu(cnt) != t) __nanosleep(32);
+                  fence_proxy_async_global();
+                  my_turn = true;
+                }
+                mbar_arrive_expect_tx(dqa_full, Cfg::SG * 16384);
+#pragma unroll
+                for (int gg = 0; gg < Cfg::SG; ++gg)
+                  tma_load_4d(dqs + gg * 16384, &tmDQ, dqa_full, h * DH + hf * 64 + (g0 + gg) * 32, row0, 0, 0);
+              }
+              mbar_wait(dqa_full, dqa_phase);
+              dqa_phase ^= 1;
+#pragma unroll
+              for (int gg = 0; gg < Cfg::SG; ++gg) {
+                const uint8_t* box = dqs + gg * 16384 + rr * 128;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                  const float4 s4 = *reinterpret_cast<const float4*>(box + ((q ^ (rr & 7)) << 4));
+                  float* dv = v + (g0 + gg) * 32 + q * 4;
+                  dv[0] = s4.x + dv[0];
+                  dv[1] = s4.y + dv[1];
+                  dv[2] = s4.z + dv[2];
+                  dv[3] = s4.w + dv[3];
+                }
+              }
+              named_barrier_sync(3, 128);  // staging read by every drain thread
+            }
+          }
+          bf16* dqrow = a.dqkv + (int64_t)(row0 + rr) * a.ld + (int64_t)h * DH + hf * 64;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            uint4 u;
+            u.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
+            u.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
+            u.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
+            u.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
+            *reinterpret_cast<uint4*>(dqrow + q * 8) = u;
+          }
+        }
+      }
+      if (issuer) {
+        if (!lastc) {  // release the tile to the next key tile: our adds are complete in L2
+          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+          fence_proxy_async_global();
+          __threadfence();
+          st_release_gpu(cnt, t + 1);
+        } else if (!firstc) {
+          *cnt = 0;  // every contributor is done: reset for the next launch / graph replay
+        }
+      }
+      if (warp == 12) FB_TR(22);
+    }
+    if (trc && threadIdx.x == 384) trc[26] = gtime_b();
+  }
+#undef FB_TR
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 // Delta[b, h, q] = sum_d dO[b*s+q, h*dh+d] * O[b*s+q, h*dh+d]
 // 8 lanes per (row, head): each lane loads 16 B of O and dO per 64 columns (coalesced 128-byte
 // segments, every load of the head issued up front), then a 3-step xor-shuffle sum.
 __global__ void __launch_bounds__(256) flash_delta_kernel(const bf16* __restrict__ o, int64_t ld_o,
                                                           const bf16* __restrict__ dout, int64_t ld_do, int B,
-                                                          int nh, int s, int dh, float* __restrict__ delta) {
+                                                          int nh, int s, int dh, float* __restrict__ delta,
+                                                          int* __restrict__ cnt, int n_cnt) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (cnt && t < n_cnt) cnt[t] = 0;  // the backward's per-query-tile dQ turn counters
   const int64_t idx = t >> 3;
   const int sub = (int)(t & 7);
   const int64_t total = (int64_t)B * s * nh;
@@ -444,9 +978,21 @@ __global__ void flash_dq_reduce_kernel(const float* __restrict__ part, int n_kt,
 
 using namespace smpk;
 
+static bool bwd_v1() {
+  static int v1 = -1;
+  if (v1 < 0) {
+    const char* e = getenv("SMPK_FA_BWD_V1");
+    v1 = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v1 == 1;
+}
+
+// default kernel: fp32 dQ accumulator [B*s, H] + Delta [B, nh, s] + turn counters [B, nh, s/128];
+// SMPK_FA_BWD_V1=1 (A/B reference): one fp32 dQ partial per key tile + Delta
 extern "C" int64_t smpk_flash_attn_bwd_workspace(int B, int nh, int s, int dh) {
   const int64_t n_kt = s / 128;
-  return n_kt * (int64_t)B * s * nh * dh * 4 + (int64_t)B * nh * s * 4;
+  const int64_t acc = (bwd_v1() ? n_kt : 1) * (int64_t)B * s * nh * dh * 4;
+  return acc + (int64_t)B * nh * s * 4 + (int64_t)B * nh * n_kt * 4;
 }
 
 extern "C" int smpk_flash_attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const void* dout,
@@ -462,16 +1008,19 @@ extern "C" int smpk_flash_attn_bwd(const void* qkv, int64_t ld, const void* out,
                "smpk_flash_attn_bwd: leading dims must be multiples of 8");
   const int64_t need = smpk_flash_attn_bwd_workspace(B, nh, s, dh);
   SMPK_REQUIRE(workspace && workspace_bytes >= need, SMPK_ERR_BAD_ARG, "smpk_flash_attn_bwd: workspace too small");
+  const bool v1 = bwd_v1();
   const int64_t H = (int64_t)nh * dh;
   const int n_kt = s / 128;
   float* dq_part = reinterpret_cast<float*>(workspace);
-  float* delta = dq_part + (int64_t)n_kt * B * s * H;
+  float* delta = dq_part + (v1 ? (int64_t)n_kt : 1) * B * s * H;
+  int* cnt = reinterpret_cast<int*>(delta + (int64_t)B * nh * s);
+  const int n_cnt = B * nh * n_kt;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   {
     const int64_t total = (int64_t)B * s * nh;
     flash_delta_kernel<<<(unsigned)((total * 8 + 255) / 256), 256, 0, st>>>(
         reinterpret_cast<const bf16*>(out), ld_out, reinterpret_cast<const bf16*>(dout), ld_dout, B, nh, s, dh,
-        delta);
+        delta, cnt, n_cnt);
     int rc = check_launch("smpk_flash_attn_bwd(delta)");
     if (rc) return rc;
   }
@@ -502,7 +1051,29 @@ extern "C" int smpk_flash_attn_bwd(const void* qkv, int64_t ld, const void* out,
   a.ld = ld;
   a.H = H;
   a.dq_part = dq_part;
+  a.dq_cnt = cnt;
+  static int trace_env = -1;
+  if (trace_env < 0) {
+    const char* e = getenv("SMPK_FA_TRACE");
+    trace_env = e ? atoi(e) : 0;
+  }
+  a.trace = trace_env;
   dim3 grid(n_kt, nh, B);
+  if (!v1) {
+    CUtensorMap tdq;
+    rc = make_tma_4d_f32sw(&tdq, dq_part, H, (int64_t)B * s, H, 32, 128, "dQ accumulator");
+    if (rc) return rc;
+    if (dh == 64) {
+      static unsigned long long once = 0;
+      smem_attr_once(flash_bwd2_kernel<64>, FaBwd2Cfg<64>::SMEM, once);
+      flash_bwd2_kernel<64><<<grid, FB2_THREADS, FaBwd2Cfg<64>::SMEM, st>>>(tq, tk, tv, tdo, tbits, tdq, a);
+    } else {
+      static unsigned long long once = 0;
+      smem_attr_once(flash_bwd2_kernel<128>, FaBwd2Cfg<128>::SMEM, once);
+      flash_bwd2_kernel<128><<<grid, FB2_THREADS, FaBwd2Cfg<128>::SMEM, st>>>(tq, tk, tv, tdo, tbits, tdq, a);
+    }
+    return check_launch("smpk_flash_attn_bwd");
+  }
   if (dh == 64) {
     static unsigned long long once = 0;
     smem_attr_once(flash_bwd_kernel<64>, FaBwdCfg<64>::SMEM, once);
@@ -518,4 +1089,11 @@ extern "C" int smpk_flash_attn_bwd(const void* qkv, int64_t ld, const void* out,
   flash_dq_reduce_kernel<<<(unsigned)((n4 + 255) / 256), 256, 0, st>>>(dq_part, n_kt, (int64_t)B * s, H, s, causal,
                                                                       reinterpret_cast<bf16*>(dqkv), ld);
   return check_launch("smpk_flash_attn_bwd(dq reduce)");
+}
+
+extern "C" int smpk_debug_fb_trace(void* host_out, int n_cta) {
+  if (n_cta > 2048) n_cta = 2048;
+  cudaError_t e = cudaMemcpyFromSymbol(host_out, smpk::g_fb_trace, (size_t)n_cta * 64 * 8);
+  SMPK_REQUIRE(e == cudaSuccess, SMPK_ERR_CUDA, "smpk_debug_fb_trace: %s", cudaGetErrorString(e));
+  return SMPK_OK;
 }

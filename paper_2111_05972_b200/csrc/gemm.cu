@@ -279,7 +279,9 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensor
   constexpr int BMT = PAIR ? 2 * BM : BM;  // tile rows
   constexpr int BNL = PAIR ? BN / 2 : BN;  // B rows staged by this CTA
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // pointer arithmetic on the __shared__ array (not an integer round trip) keeps the shared
+  // address space visible to the compiler: LDS / STS instead of generic LD / ST
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
   uint8_t* sStg = sB + STAGES * Cfg::B_BYTES;  // NUM_EPI_WARPS x STG_BYTES (1024-aligned)
@@ -677,6 +679,14 @@ static int make_tma_4d_ex(CUtensorMap* map, const void* ptr, bool f32, CUtensorM
 int make_tma_4d(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t ld, int nb1, int64_t s1,
                 int nb2, int64_t s2, int box_inner, int box_outer, const char* name) {
   return make_tma_4d_ex(map, ptr, false, CU_TENSOR_MAP_SWIZZLE_128B, inner, outer, ld, nb1, s1, nb2, s2, box_inner,
+                        box_outer, name);
+}
+
+// fp32 map with SWIZZLE_128B boxes (32 fp32 = 128 B inner): the attention backward's ordered dQ
+// accumulation (TMA store / reduce-add / load of [box_outer rows x 32 cols] boxes).
+int make_tma_4d_f32sw(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t ld, int box_inner,
+                      int box_outer, const char* name) {
+  return make_tma_4d_ex(map, ptr, true, CU_TENSOR_MAP_SWIZZLE_128B, inner, outer, ld, 1, 0, 1, 0, box_inner,
                         box_outer, name);
 }
 

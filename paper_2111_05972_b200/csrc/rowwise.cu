@@ -865,7 +865,7 @@ template <int CH>
 __global__ void __launch_bounds__(32 * (PIPE_CW + 1), 1) bdr_ln_pipe_kernel(const BdrPipeArgs a) {
   const uint64_t pkey = philox_key(a.seed, a.rng_step);
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);  // keeps LDS / STS
   const int H = a.H;
   const int nin = a.nslots + (a.residual ? 1 : 0);
   const int stage_bytes = nin * H * 2;
