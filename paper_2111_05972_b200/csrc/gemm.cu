@@ -116,7 +116,7 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 // For BIAS_ACT the bf16 pre-activation is returned packed in pre[16].
 template <int EPI, int ACT, bool F32OUT, bool BETA>
 __device__ __forceinline__ void epilogue_math32(const GemmArgs& g, bool in_rows, int row, int col0, int64_t c_off,
-                                                float (&v)[32], uint32_t (&pre)[16]) {
+                                                float (&v)[32], uint32_t (&pre)[16], const uint4* auxv = nullptr) {
   const bool full = (col0 + 32 <= g.N) && g.vec_ok;
   if (g.alpha != 1.f) {
 #pragma unroll
@@ -159,7 +159,7 @@ __device__ __forceinline__ void epilogue_math32(const GemmArgs& g, bool in_rows,
         const uint4* src = reinterpret_cast<const uint4*>(ap);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          uint4 u = src[q];
+          uint4 u = auxv ? auxv[q] : src[q];
           uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -443,16 +443,34 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensor
     int acc = 0;
     uint32_t acc_phase = 0;
     const int etid = threadIdx.x - 128;  // 0 .. 32*NUM_EPI_WARPS-1
+    constexpr bool AUXPF = (EPI == SMPK_EPI_ADD);  // DACT (16 warps, 96 registers) spilled with it: slower
     for (int u = unit0; u < g.num_units; u += ustep) {
       int tile, kb0, kb1, b1, b2, tm, tn;
       decode_unit(g, u, tile, kb0, kb1);
       decode_tile(g, tile, b1, b2, tm, tn);
-      mbar_wait(&tfull_bar[acc], acc_phase);
-      tc_fence_after();
       const int rl = quarter * 32 + lane;  // row inside this CTA's 128 rows
       const int row0 = tm * BMT + (int)rank * BM + quarter * 32;  // first row of this warp's 32
       const int row = row0 + lane;
       const int64_t c_off = (int64_t)b1 * g.c_bs1 + (int64_t)b2 * g.c_bs2;
+      // DACT / ADD: the auxiliary operand (pre-activation / residual) of the next 32-column chunk
+      // is loaded one chunk ahead -- the first one while the main loop still runs -- so its HBM
+      // latency is off the epilogue's critical path (ncu r02: 11% of the DACT stall samples)
+      uint4 auxv[4];
+      auto aux_ok = [&](int i) {
+        const int colc = tn * BN + (cgroup + NGR * i) * 32;
+        return AUXPF && active && g.splits == 1 && row < g.M && colc + 32 <= g.N && g.vec_ok;
+      };
+      auto aux_load = [&](int i) {
+        if (aux_ok(i)) {
+          const uint4* src = reinterpret_cast<const uint4*>(g.aux + c_off + (int64_t)row * g.ldaux + tn * BN +
+                                                            (cgroup + NGR * i) * 32);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) auxv[q] = __ldg(src + q);
+        }
+      };
+      if constexpr (AUXPF) aux_load(0);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
       const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16);
       if (g.splits == 1) {
 #pragma unroll 1
@@ -467,8 +485,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensor
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-              if constexpr (PAIR) mbar_arrive_cluster(&tempty_bar[acc], 0);
-              else mbar_arrive(&tempty_bar[acc]);
+              if constexpr (PAIR) mbar_arrive_cluster_relaxed(&tempty_bar[acc], 0);
+              else mbar_arrive_relaxed(&tempty_bar[acc]);
             }
           }
           if (!active) continue;
@@ -478,7 +496,16 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensor
           uint32_t pre[16];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-          epilogue_math32<EPI, ACT, F32OUT, BETA>(g, row < g.M, row, col0, c_off, v, pre);
+          if constexpr (AUXPF) {
+            uint4 cur[4];
+            const bool have = aux_ok(i);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cur[q] = auxv[q];
+            if (i + 1 < CPW) aux_load(i + 1);  // next chunk's operand in flight during this one's math
+            epilogue_math32<EPI, ACT, F32OUT, BETA>(g, row < g.M, row, col0, c_off, v, pre, have ? cur : nullptr);
+          } else {
+            epilogue_math32<EPI, ACT, F32OUT, BETA>(g, row < g.M, row, col0, c_off, v, pre);
+          }
           if (g.tma_store) {
             if (lane == 0) bulk_wait_read0();  // the previous chunk's bulk store has read the box
             __syncwarp();
@@ -496,14 +523,14 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensor
             if constexpr (!F32OUT) {
               if (g.colsum_part != nullptr && row0 < g.M && col0 + lane < g.N) {  // rows >= M hold zeros
                 // lane = column: sum the box's 32 stored rows (SWIZZLE_64B granule order)
-                float cs = 0.f;
-#pragma unroll 8
+                float cs4[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent chains (row order fixed)
+#pragma unroll
                 for (int rr = 0; rr < 32; ++rr) {
                   const bf16* e = reinterpret_cast<const bf16*>(
                       stg + rr * 64 + ((((lane >> 3) ^ ((rr >> 1) & 3))) << 4) + (lane & 7) * 2);
-                  cs += bf2f(*e);
+                  cs4[rr & 3] += bf2f(*e);
                 }
-                g.colsum_part[(int64_t)(row0 >> 5) * g.N + col0 + lane] = cs;
+                g.colsum_part[(int64_t)(row0 >> 5) * g.N + col0 + lane] = (cs4[0] + cs4[1]) + (cs4[2] + cs4[3]);
               }
             }
             if (lane == 0) {
