@@ -241,10 +241,12 @@ SMPK_API int smpk_flash_attn_fwd(const void* qkv, int64_t ld, int B, int nh, int
  * heads: word ((b*nh + h)*sq + q)*(sk/32) + k/32, bit k%32 = keep(q, k) of the Philox4x32-10
  * stream (site 0, row = ((sample_offset+b)*nh_global + head_offset+h)*sq + q, col = k) that
  * oracle/philox.py restates.  Generated once per layer and read by the forward and backward.
+ * causal != 0: words whose 128-key tile lies after the query's 128-row tile are not written
+ * (the fused kernels never read them).
  */
 SMPK_API int smpk_attn_dropout_bits(int B, int nh, int sq, int sk, float p_drop, uint64_t seed, const uint64_t* rng_step, int layer,
                                     int64_t sample_offset, int head_offset, int nh_global, uint32_t* bits,
-                                    void* stream);
+                                    int causal, void* stream);
 
 /*
  * smpk_flash_attn_bwd — backward of smpk_flash_attn_fwd: from dout (grad of out, same layout),

@@ -390,9 +390,11 @@ __global__ void __launch_bounds__(128) attn_dropout_bits_kernel(int nh, int sq, 
                                                                 uint64_t seed, const uint64_t* rng_step,
                                                                 uint32_t layer,
                                                                 int64_t sample_offset, int head_offset, int nh_global,
-                                                                uint32_t* __restrict__ bits) {
+                                                                uint32_t* __restrict__ bits, int causal) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // (q, w) of this (b, h)
   if (idx >= sq * wpr) return;
+  // causal: the kernels never read words of key tiles after the query's tile (128-key tiles)
+  if (causal && ((idx % wpr) >> 2) > (idx / wpr) >> 7) return;
   const uint64_t pkey = philox_key(seed, rng_step);
   const int bh = blockIdx.y;
   const int q = idx / wpr, w = idx - q * wpr;
@@ -416,7 +418,7 @@ using namespace smpk;
 extern "C" int smpk_attn_dropout_bits(int B, int nh, int sq, int sk, float p_drop, uint64_t seed,
                                       const uint64_t* rng_step, int layer,
                                       int64_t sample_offset, int head_offset, int nh_global, uint32_t* bits,
-                                      void* stream) {
+                                      int causal, void* stream) {
   SMPK_REQUIRE(B > 0 && nh > 0 && sq > 0 && sk > 0 && sk % 32 == 0 && bits, SMPK_ERR_BAD_ARG,
                "smpk_attn_dropout_bits: bad arguments (sk must be a multiple of 32)");
   SMPK_REQUIRE(p_drop >= 0.f && p_drop < 1.f, SMPK_ERR_BAD_ARG, "smpk_attn_dropout_bits: p in [0,1)");
@@ -424,7 +426,7 @@ extern "C" int smpk_attn_dropout_bits(int B, int nh, int sq, int sk, float p_dro
   const int wpr = sk / 32;
   dim3 grid((unsigned)((sq * wpr + 127) / 128), (unsigned)(B * nh));
   attn_dropout_bits_kernel<<<grid, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      nh, sq, wpr, dropout_threshold(p_drop), seed, rng_step, (uint32_t)layer, sample_offset, head_offset, nh_global, bits);
+      nh, sq, wpr, dropout_threshold(p_drop), seed, rng_step, (uint32_t)layer, sample_offset, head_offset, nh_global, bits, causal);
   return check_launch("smpk_attn_dropout_bits");
 }
 

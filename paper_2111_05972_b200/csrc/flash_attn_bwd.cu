@@ -482,11 +482,14 @@ __global__ void __launch_bounds__(FB2_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_kt = a.s / 128;
-  const int j = (int)blockIdx.x;  // key tile
+  const int j = a.causal ? n_kt - 1 - (int)blockIdx.x : (int)blockIdx.x;  // key tile
   const int h = blockIdx.y, b = blockIdx.z;
   // query tile processed at step t: causal i = j + t; otherwise rotated, i = (j + t) mod n_kt, so the
   // key-tile CTAs of one (head, sample) work on different query tiles at every step and tile i's
-  // dQ contributions arrive in step order (contribution number t; see the drain warps)
+  // dQ contributions arrive in step order (contribution number t; see the drain warps): the CTA
+  // of contribution t waits for key tile j+1's CTA, which did its part one step earlier.  Causal
+  // groups launch key tiles in descending order (blockIdx.x = n_kt-1-j), so that predecessor was
+  // always launched first: no wait on a not-yet-resident block.
   const int nt = a.causal ? n_kt - j : n_kt;
   auto qtile = [&](int t) { return a.causal ? j + t : (j + t) % n_kt; };
 

@@ -171,7 +171,7 @@ def _keep_bits_async(B: int, s: int, m: LayerMeta, device):
     with torch.cuda.stream(side):
         ops.attn_dropout_bits(B, m.heads_local, s, s, p=m.p_attn, seed=m.seed, rng=m.rng, layer=m.layer_id,
                               sample_offset=m.sample_offset, head_offset=m.head_offset, nh_global=m.heads_global,
-                              out=bits)
+                              out=bits, causal=m.causal and s % 128 == 0)
     return bits, (lambda: main.wait_stream(side))
 
 

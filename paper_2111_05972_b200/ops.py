@@ -144,7 +144,7 @@ def colsum(x: torch.Tensor, *, out_dtype=None) -> torch.Tensor:
 
 
 def attn_dropout_bits(B: int, nh: int, sq: int, sk: int, *, p: float, seed=0, rng=None, layer=0, sample_offset=0,
-                      head_offset=0, nh_global=None, device=None, out=None) -> torch.Tensor | None:
+                      head_offset=0, nh_global=None, device=None, out=None, causal=False) -> torch.Tensor | None:
     """Keep bits [B, nh, sq, sk/32] (uint32 words as int32) of the attention-probability dropout;
     None when p == 0.  Generated once per layer and shared by the forward and the backward."""
     if p <= 0.0:
@@ -154,7 +154,7 @@ def attn_dropout_bits(B: int, nh: int, sq: int, sk: int, *, p: float, seed=0, rn
     _check_cuda(bits)
     _lib.call("smpk_attn_dropout_bits", B, nh, sq, sk, float(p), int(seed) & (2 ** 64 - 1), _ptr(rng), int(layer),
               int(sample_offset), int(head_offset), int(nh_global if nh_global is not None else nh), _ptr(bits),
-              _stream())
+              int(bool(causal)), _stream())
     return bits
 
 

@@ -116,3 +116,18 @@ def test_dropout_bits_bit_exact(shape):
     got = ((bits[..., None] >> np.arange(32, dtype=np.uint32)) & 1).reshape(B, nh, sq, sk).astype(bool)
     ref = philox.attn_prob_mask(np.arange(B) + soff, np.arange(nh) + hoff, sq, sk, nhg, layer, seed, p)
     assert np.array_equal(got, ref)
+
+
+def test_causal_keep_bits_cover_lower_triangle():
+    """causal=True writes exactly the words the causal kernels read (key tile <= query tile) and
+    they equal the full generation's."""
+    from paper_2111_05972_b200 import ops
+    B, nh, s = 2, 3, 512
+    full = ops.attn_dropout_bits(B, nh, s, s, p=0.1, seed=5, layer=2)
+    part = torch.zeros_like(full)
+    ops.attn_dropout_bits(B, nh, s, s, p=0.1, seed=5, layer=2, out=part, causal=True)
+    q = torch.arange(s, device=full.device)[:, None] // 128
+    w = torch.arange(s // 32, device=full.device)[None, :] // 4
+    need = (w <= q).expand(B, nh, s, s // 32)
+    assert torch.equal(part[need], full[need])
+    assert int(part[~need].abs().sum()) == 0
