@@ -17,8 +17,9 @@ __version__ = "0.1.0"
 from . import nn  # noqa: E402
 from .collectives import (bwd_allreduce_for_tp, fused_allgather_for_tp, fwd_allreduce_for_tp,  # noqa: E402
                           reduce_scatter_for_tp, scatter_and_merge_for_tp)
-from .errors import (IndexOutOfRangeError, NotDivisibleError, ShapeMismatchError,  # noqa: E402
+from .errors import (IndexOutOfRangeError, NotDivisibleError, PeerTimeoutError, ShapeMismatchError,  # noqa: E402
                      TensorParallelError, TopologyError)
+from .symm import synchronize  # noqa: E402
 from .state import (STATE, dp_rank, init, pp_rank, pp_size, rank, rdp_rank, reset, rng_step, set_rng_step, size,  # noqa: E402
                     tp_rank, tp_size)
 from .topology import Topology, build_topology  # noqa: E402

@@ -30,3 +30,14 @@ def test_pipeline_stage_sendrecv_2gpu():
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     print(r.stdout[-4000:])
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+
+
+def test_peer_barrier_timeout_2gpu():
+    """A TP peer that never reaches the barrier -> PeerTimeoutError naming it."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29478", os.path.join(ROOT, "tests", "mp_timeout_check.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    print(r.stdout[-4000:])
+    assert r.returncode == 0 and "PeerTimeoutError" in r.stdout, r.stdout[-4000:] + r.stderr[-4000:]
