@@ -241,24 +241,30 @@ class StageChannel:
     ``send(t)``, the consumer ``recv(out)``, each on its current stream, in the same
     order.  Flow control and completion are stream-ordered sequence words."""
 
-    def __init__(self, src: int, dst: int, slot_bytes: int, slots: int = 4, group=None):
+    def __init__(self, src: int, dst: int, slot_bytes: int, slots: int = 4, group=None, *, connect: bool = True):
         self.src, self.dst, self.slots, self.slot_bytes = src, dst, slots, slot_bytes
         self.rank = dist.get_rank() if dist.is_initialized() else 0
         self.seq = 0
+        self.peer_base = None
         if self.rank not in (src, dst):
             raise ValueError("StageChannel must be built by its two endpoint ranks")
-        is_dst = self.rank == dst
+        self.is_dst = self.rank == dst
         # dst owns the receive ring (+ ready word); src owns only a flag block (free word)
-        self.local = _Ring(slots if is_dst else 0, slot_bytes)
-        gathered = [None] * dist.get_world_size(group)
-        dist.all_gather_object(gathered, (self.rank, self.local.handle()), group=group)
-        peer = [h for r, h in gathered if r == (src if is_dst else dst)]
-        if not peer:
-            raise RuntimeError("StageChannel: peer handle missing (both ranks must construct the channel)")
+        self.local = _Ring(slots if self.is_dst else 0, slot_bytes)
+        if connect:
+            gathered = [None] * dist.get_world_size(group)
+            dist.all_gather_object(gathered, (self.rank, self.local.handle()), group=group)
+            peer = [h for r, h in gathered if r == (src if self.is_dst else dst)]
+            if not peer:
+                raise RuntimeError("StageChannel: peer handle missing (both ranks must construct the channel)")
+            self.connect(peer[0])
+
+    def connect(self, peer_handle: bytes) -> None:
+        """Map the peer endpoint's allocation (its IPC handle, exchanged by the caller)."""
         p = C.c_void_p()
-        _lib.call("smpk_p2p_import", C.create_string_buffer(peer[0], 64), C.byref(p))
+        _lib.call("smpk_p2p_import", C.create_string_buffer(peer_handle, 64), C.byref(p))
         self.peer_base = p.value
-        self.peer_flags = self.peer_base + (0 if is_dst else slots * slot_bytes)
+        self.peer_flags = self.peer_base + (0 if self.is_dst else self.slots * self.slot_bytes)
 
     @staticmethod
     def _stream():
@@ -297,62 +303,109 @@ class StageChannel:
 # ---------------------------------------------------------------------------
 
 class PipelineEngine:
-    """Runs one training step of a P-stage chain with M microbatches (one process per stage).
+    """Runs one training step of a P-stage chain with M microbatches (one process per stage and
+    TP rank: with tensor parallelism each TP rank drives its own chain of the same tp_rank,
+    topology.py:49-50, and the stage module's TP collectives run inside the stage).
 
     stage_module: this rank's module (a callable on [mb, s, H] activations); the first
     stage receives its microbatch inputs, the last stage applies ``loss_fn``.  Activations
     go forward and gradients backward over D2D StageChannels; the per-stage op order is
-    the recorded schedule of ``next_action`` (static_schedule)."""
+    the recorded schedule of ``next_action`` (static_schedule).
+
+    Transport (PAPER.md:337-350 D2D backend): every send and receive runs on a dedicated
+    send / receive stream, ordered against the compute stream by CUDA events -- a send starts
+    as soon as its producer op finished and never blocks the next op's kernels, and the
+    receive of the NEXT op is posted before the current op runs, so its payload lands while
+    this stage computes.  Channels are built from one handle exchange over the PP group."""
 
     def __init__(self, stage_module, *, pp_rank: int, pp_size: int, ranks: list, act_shape, dtype=torch.bfloat16,
                  policy: SchedulePolicy, slots: int = 4, group=None):
-        self.mod, self.s, self.P, self.ranks = stage_module, pp_rank, pp_size, ranks
+        self.mod, self.s, self.P, self.ranks = stage_module, pp_rank, pp_size, list(ranks)
         self.shape, self.dtype, self.policy = tuple(act_shape), dtype, policy
         nbytes = int(torch.Size(act_shape).numel()) * torch.tensor([], dtype=dtype).element_size()
         self.log, ops = static_schedule(policy, pp_size)
         self.ops = ops[pp_rank]
         self.fwd_in = self.fwd_out = self.bwd_in = self.bwd_out = None
-        # build channels pairwise in a fixed global order so every rank participates consistently
-        for s in range(pp_size - 1):
-            a, b = ranks[s], ranks[s + 1]
-            if self.s in (s, s + 1):
-                pg = group if group is not None else dist.new_group([a, b])
-            else:
-                dist.new_group([a, b])
-                continue
-            fwd = StageChannel(a, b, nbytes, slots, group=pg)
-            bwd = StageChannel(b, a, nbytes, slots, group=pg)
-            if self.s == s:
-                self.fwd_out, self.bwd_in = fwd, bwd
-            else:
-                self.fwd_in, self.bwd_out = fwd, bwd
+        me = self.ranks[pp_rank]
+        chans = {}
+        if pp_rank > 0:  # from the previous stage: activations in, gradients out
+            chans["fwd_in"] = StageChannel(self.ranks[pp_rank - 1], me, nbytes, slots, connect=False)
+            chans["bwd_out"] = StageChannel(me, self.ranks[pp_rank - 1], nbytes, slots, connect=False)
+        if pp_rank + 1 < pp_size:  # to the next stage
+            chans["fwd_out"] = StageChannel(me, self.ranks[pp_rank + 1], nbytes, slots, connect=False)
+            chans["bwd_in"] = StageChannel(self.ranks[pp_rank + 1], me, nbytes, slots, connect=False)
+        mine = {k: c.local.handle() for k, c in chans.items()}
+        if group is None and dist.is_initialized() and dist.get_world_size() == pp_size:
+            group = dist.group.WORLD
+        gathered = [None] * pp_size
+        dist.all_gather_object(gathered, (pp_rank, mine), group=group)
+        peer = {r: h for r, h in gathered}
+        # the endpoint on the other side of each channel
+        pairs = {"fwd_in": (pp_rank - 1, "fwd_out"), "bwd_out": (pp_rank - 1, "bwd_in"),
+                 "fwd_out": (pp_rank + 1, "fwd_in"), "bwd_in": (pp_rank + 1, "bwd_out")}
+        for k, c in chans.items():
+            r, kk = pairs[k]
+            c.connect(peer[r][kk])
+            setattr(self, k, c)
+        # separate FIFO streams for receives and sends: a receive posted ahead (waiting for its
+        # ready word) must never hold back a send the peer is waiting for
+        self.recv_stream, self.send_stream = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def _post_recv(self, op, dev):
+        """Receive the payload of op (if it is a receiving op) on the comm stream; returns
+        (tensor, ready event) or None."""
+        mb, d = op
+        ch = self.fwd_in if d == FWD else self.bwd_in
+        if ch is None:
+            return None
+        buf = torch.empty(self.shape, dtype=self.dtype, device=dev)
+        self.recv_stream.wait_stream(torch.cuda.current_stream())  # buf allocation
+        with torch.cuda.stream(self.recv_stream):
+            ch.recv(buf)
+            ev = torch.cuda.Event()
+            ev.record()
+        buf.record_stream(self.recv_stream)
+        return buf, ev
+
+    def _send(self, ch, t):
+        ev = torch.cuda.Event()
+        ev.record()  # the producer op's kernels on the compute stream
+        self.send_stream.wait_event(ev)
+        with torch.cuda.stream(self.send_stream):
+            ch.send(t)
+        t.record_stream(self.send_stream)
 
     def step(self, inputs=None, loss_fn=None):
         """inputs: list of M microbatch tensors (stage 0); loss_fn(mb, y) -> scalar (last stage).
         Returns the list of per-microbatch losses on the last stage (None elsewhere)."""
         saved, losses = {}, {}
         dev = torch.device("cuda", torch.cuda.current_device())
-        for mb, d in self.ops:
+        main = torch.cuda.current_stream()
+        pending = self._post_recv(self.ops[0], dev) if self.ops else None
+        for i, (mb, d) in enumerate(self.ops):
+            cur, pending = pending, None
+            if i + 1 < len(self.ops):  # the next op's payload streams in while this op computes
+                pending = self._post_recv(self.ops[i + 1], dev)
+            if cur is not None:
+                main.wait_event(cur[1])
             if d == FWD:
-                if self.s == 0:
-                    x = inputs[mb]
-                else:
-                    x = self.fwd_in.recv(torch.empty(self.shape, dtype=self.dtype, device=dev)).requires_grad_(True)
+                x = inputs[mb] if self.s == 0 else cur[0].requires_grad_(True)
                 y = self.mod(x)
                 saved[mb] = (x, y)
                 if self.s == self.P - 1:
                     losses[mb] = loss_fn(mb, y)
                 else:
-                    self.fwd_out.send(y.detach())
+                    self._send(self.fwd_out, y.detach())
             else:
                 x, y = saved.pop(mb)
                 if self.s == self.P - 1:
                     losses[mb].backward()
                 else:
-                    g = self.bwd_in.recv(torch.empty(self.shape, dtype=self.dtype, device=dev))
-                    torch.autograd.backward(y, g)
+                    torch.autograd.backward(y, cur[0])
                 if self.s > 0:
-                    self.bwd_out.send(x.grad)
+                    self._send(self.bwd_out, x.grad)
+        main.wait_stream(self.send_stream)  # this step's sends are ordered before the next step's work
+        main.wait_stream(self.recv_stream)
         if self.s == self.P - 1:
             return [losses[m] for m in range(self.policy.microbatches)]
         return None

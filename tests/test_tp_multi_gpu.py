@@ -41,3 +41,14 @@ def test_peer_barrier_timeout_2gpu():
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
     print(r.stdout[-4000:])
     assert r.returncode == 0 and "PeerTimeoutError" in r.stdout, r.stdout[-4000:] + r.stderr[-4000:]
+
+
+def test_tp2_x_pp2_step_4gpu():
+    """BASELINE.json configs[0]: TP=2 x PP=2 pipelined step vs the fp64 oracle (mp_tppp_check.py)."""
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+           "--master-addr", "127.0.0.1", "--master-port", "29479", os.path.join(ROOT, "tests", "mp_tppp_check.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    print(r.stdout[-4000:])
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
