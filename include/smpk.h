@@ -370,6 +370,14 @@ SMPK_API int smpk_p2p_recv(void* dst, const void* local_slot, int64_t bytes, con
  * the same snapshot, so interleaved microbatches (pipeline schedules) stay consistent. */
 SMPK_API int smpk_rng_next(uint64_t* counter, uint64_t* snapshot, void* stream);
 
+/* smpk_adam_step — fused AdamW on one slice of fp32 master parameters (data-parallel optimizer,
+ * PAPER.md:765 "shard_optimizer_state"): g = grad * grad_scale; m = b1 m + (1-b1) g;
+ * v = b2 v + (1-b2) g^2; master -= lr * ((m / (1-b1^step)) / (sqrt(v / (1-b2^step)) + eps) + wd * master);
+ * param_bf16 = bf16(master).  n % 4 == 0, 16-B aligned fp32 buffers. */
+SMPK_API int smpk_adam_step(float* master, void* param_bf16, const float* grad, float* m, float* v, int64_t n,
+                            float lr, float beta1, float beta2, float eps, float weight_decay, int step,
+                            float grad_scale, void* stream);
+
 /* Debug: per-CTA globaltimer records of the last fused-attention forward launched with
  * SMPK_FA_TRACE=1 in the environment (20 u64 per CTA; see csrc/flash_attn.cu).  Diagnostics only. */
 SMPK_API int smpk_debug_fa_trace(void* host_out, int n_cta);

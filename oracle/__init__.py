@@ -14,6 +14,9 @@ This package restates, on the CPU, the algorithms the GPU path must reproduce:
 * ``philox_grid.c`` — C restatement of the same masks (oracle/Makefile ->
                 libphilox_grid.so), so 24-layer oracle stacks draw their masks fast;
                 tests/test_philox.py checks it against the numpy version.
+* ``tpcheck``  — the SPEC's tensor-parallel invariant suite as a CLI
+                (``python -m oracle.tpcheck``; JSON report, exit 5 on violation;
+                ``--gpu`` adds the sm_100a kernels at T = 1).
 The partition / topology / schedule rows need no restatement here: the reference
 itself is importable in this container and tests/golden/make_golden.py generates
 tests/golden/reference_golden.json from it, against which the product's vendored

@@ -739,3 +739,19 @@ def plan_replacement(spec, registry: dict, tp_marks: set) -> set:
 
     visit(spec.root_id, False, False)
     return replaced
+
+
+# ---------------------------------------------------------------------------
+# AdamW (PAPER.md:765 optimizer state sharding; csrc/runtime.cu smpk_adam_step restated)
+# ---------------------------------------------------------------------------
+
+def adamw_ref(master, param_out, grad, m, v, *, lr, betas, eps, weight_decay, step, grad_scale):
+    """In-place AdamW on fp32 torch tensors (same update order as smpk_adam_step)."""
+    b1, b2 = betas
+    g = grad.float() * grad_scale
+    m.mul_(b1).add_((1.0 - b1) * g)
+    v.mul_(b2).add_((1.0 - b2) * g * g)
+    bc1, bc2 = 1.0 - b1 ** step, 1.0 - b2 ** step
+    upd = (m / bc1) / ((v / bc2).sqrt() + eps)
+    master.sub_(lr * (upd + weight_decay * master))
+    param_out.copy_(master.to(param_out.dtype))

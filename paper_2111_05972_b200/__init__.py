@@ -26,3 +26,6 @@ from .topology import Topology, build_topology  # noqa: E402
 from .replace import (DistributedModel, plan_replacement, set_tensor_parallelism, tensor_parallelism,  # noqa: E402
                       tp_register, tp_register_with_module)
 from . import pipeline  # noqa: E402,F401
+from .checkpointing import checkpoint_grouping, set_activation_checkpointing  # noqa: E402
+from .state_dict import full_state_dict, load_local_state_dict, local_state_dict  # noqa: E402
+from .dp import DistributedAdam, GradBuckets  # noqa: E402

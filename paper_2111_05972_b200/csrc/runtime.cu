@@ -88,3 +88,62 @@ extern "C" int smpk_rng_next(uint64_t* counter, uint64_t* snapshot, void* stream
       reinterpret_cast<unsigned long long*>(counter), reinterpret_cast<unsigned long long*>(snapshot));
   return smpk::check_launch("smpk_rng_next");
 }
+
+// ---------------------------------------------------------------------------
+// Fused AdamW step on one (sharded) slice of the fp32 master parameters: reads master, grad,
+// m, v (16 B / element), writes master, m, v and the bf16 model copy (14 B / element); one pass,
+// 128-bit vector access.  Used by the data-parallel optimizer (dp.py; PAPER.md:765 optimizer
+// state sharding).  grad_scale multiplies the gradient first (1 / data-parallel degree).
+// ---------------------------------------------------------------------------
+namespace smpk {
+__global__ void __launch_bounds__(256) adam_step_kernel(float* __restrict__ master, bf16* __restrict__ param,
+                                                        const float* __restrict__ grad, float* __restrict__ m,
+                                                        float* __restrict__ v, int64_t n, float lr, float b1,
+                                                        float b2, float eps, float wd, float bc1, float bc2,
+                                                        float grad_scale) {
+  const int64_t n4 = n / 4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 p = reinterpret_cast<float4*>(master)[i];
+    const float4 g = reinterpret_cast<const float4*>(grad)[i];
+    float4 mm = reinterpret_cast<float4*>(m)[i];
+    float4 vv = reinterpret_cast<float4*>(v)[i];
+    float pv[4] = {p.x, p.y, p.z, p.w}, gv[4] = {g.x, g.y, g.z, g.w}, mv[4] = {mm.x, mm.y, mm.z, mm.w},
+          sv[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float gk = gv[k] * grad_scale;
+      mv[k] = b1 * mv[k] + (1.f - b1) * gk;
+      sv[k] = b2 * sv[k] + (1.f - b2) * gk * gk;
+      const float upd = (mv[k] / bc1) / (sqrtf(sv[k] / bc2) + eps);
+      pv[k] = pv[k] - lr * (upd + wd * pv[k]);
+    }
+    reinterpret_cast<float4*>(master)[i] = make_float4(pv[0], pv[1], pv[2], pv[3]);
+    reinterpret_cast<float4*>(m)[i] = make_float4(mv[0], mv[1], mv[2], mv[3]);
+    reinterpret_cast<float4*>(v)[i] = make_float4(sv[0], sv[1], sv[2], sv[3]);
+    uint2 o;
+    o.x = pack_bf16x2(pv[0], pv[1]);
+    o.y = pack_bf16x2(pv[2], pv[3]);
+    reinterpret_cast<uint2*>(param)[i] = o;
+  }
+}
+}  // namespace smpk
+
+extern "C" int smpk_adam_step(float* master, void* param_bf16, const float* grad, float* m, float* v, int64_t n,
+                              float lr, float beta1, float beta2, float eps, float weight_decay, int step,
+                              float grad_scale, void* stream) {
+  SMPK_REQUIRE(master && param_bf16 && grad && m && v && n >= 0 && step >= 1, SMPK_ERR_BAD_ARG,
+               "smpk_adam_step: bad arguments");
+  SMPK_REQUIRE(n % 4 == 0 && ((reinterpret_cast<uintptr_t>(master) | reinterpret_cast<uintptr_t>(grad) |
+                               reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v)) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(param_bf16) & 7) == 0,
+               SMPK_ERR_BAD_ARG, "smpk_adam_step: n must be a multiple of 4 with 16-B aligned buffers");
+  if (n == 0) return SMPK_OK;
+  const float bc1 = 1.f - powf(beta1, (float)step), bc2 = 1.f - powf(beta2, (float)step);
+  int64_t grid = (n / 4 + 255) / 256;
+  const int64_t cap = (int64_t)smpk::num_sms() * 8;
+  if (grid > cap) grid = cap;
+  smpk::adam_step_kernel<<<(unsigned)grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      master, reinterpret_cast<smpk::bf16*>(param_bf16), grad, m, v, n, lr, beta1, beta2, eps, weight_decay, bc1, bc2,
+      grad_scale);
+  return smpk::check_launch("smpk_adam_step");
+}

@@ -415,6 +415,9 @@ class DistributedTransformer(DistributedModule):
             for _ in range(num_layers)])
 
     def sublayer(self, X, mask, rc):
+        if getattr(self, "_ckpt_groups", None):  # smp.set_activation_checkpointing
+            from .checkpointing import run_stack
+            return run_stack(self, X, mask, rc)
         n = len(self.seq_layers)
         for i, layer in enumerate(self.seq_layers):
             X = layer.sublayer(X, mask, rc, push_last=i + 1 < n)

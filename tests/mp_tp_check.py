@@ -240,12 +240,43 @@ def run_modules(smp, name, *, prescaled):
     return bool(flag.item())
 
 
+def run_state_dict(smp, name, *, optimize):
+    """full_state_dict all-gathers the shards back into the reference layout (bit-exact)."""
+    T, rank = dist.get_world_size(), dist.get_rank()
+    smp.init({"tensor_parallel_degree": T, "optimize": optimize, "seed": 3, "symm_pool_bytes": 64 << 20})
+    nh, dh, I = 2 * T, 64, 512 * T
+    H = nh * dh
+    cfg = tp.LayerConfig(num_attention_heads=nh, attention_head_size=dh, hidden_size=H, intermediate_size=I,
+                         pre_layernorm=True, post_layernorm=True)
+    p = {k: v.to(torch.bfloat16) for k, v in tp.init_layer_params(cfg, seed=9).items()}
+    for k in list(p):  # non-trivial LayerNorm parameters
+        if "_ln_" in k:
+            p[k] = torch.randn(p[k].shape, generator=torch.Generator().manual_seed(len(k))).to(torch.bfloat16)
+    layer = smp.nn.DistributedTransformerLayer(num_attention_heads=nh, attention_head_size=dh, hidden_size=H,
+                                               intermediate_size=I, pre_layernorm=True, post_layernorm=True,
+                                               layer_id=0)
+    layer.load_full({k: v.cuda() for k, v in p.items()})
+    full = smp.full_state_dict(layer)
+    bad = [k for k in p if not torch.equal(full[k].cpu(), p[k])]
+    ok = not bad and set(full) == set(p)
+    sd = smp.local_state_dict(layer)
+    smp.load_local_state_dict(layer, sd)
+    flag = torch.tensor([1 if ok else 0], device="cuda")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        print(f"[{name}] T={T} {'OK' if flag.item() else 'FAIL'} mismatched={bad}", flush=True)
+    smp.reset()
+    return bool(flag.item())
+
+
 def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2111_05972_b200 as smp
     results = [
+        run_state_dict(smp, "state_dict_speed", optimize="speed"),
+        run_state_dict(smp, "state_dict_memory", optimize="memory"),
         run_modules(smp, "modules_tp_across_dp", prescaled=False),
         run_modules(smp, "modules_prescaled", prescaled=True),
         run_case(smp, "tp_across_dp_post_ln", prescaled=False, causal=False, pre=False, post=True, p=0.0),

@@ -235,3 +235,21 @@ def test_bert_large_24_layer_stack_vs_oracle(smp_single):
         errs[f"dw2_{l}"] = rel(lay.output.fc2_weight.grad, pr[l]["w2"].grad)
     bad = {k: v for k, v in errs.items() if not v < 3e-2}
     assert not bad, f"{bad} (all: {errs})"
+
+
+def test_state_dict_roundtrip_tp1(smp_single):
+    """full_state_dict returns exactly what load_full loaded (T = 1: no communication)."""
+    smp = smp_single
+    cfg = tp.LayerConfig(num_attention_heads=4, attention_head_size=64, hidden_size=256, intermediate_size=1024,
+                         pre_layernorm=True, post_layernorm=True)
+    p = {k: v.to(torch.bfloat16) for k, v in tp.init_layer_params(cfg, seed=4).items()}
+    layer = smp.nn.DistributedTransformerLayer(num_attention_heads=4, attention_head_size=64, hidden_size=256,
+                                               intermediate_size=1024, pre_layernorm=True, post_layernorm=True,
+                                               layer_id=0)
+    layer.load_full({k: v.cuda() for k, v in p.items()})
+    full = smp.full_state_dict(layer)
+    assert set(full) == set(p)
+    for k in p:
+        assert torch.equal(full[k].cpu(), p[k]), k
+    sd = smp.local_state_dict(layer)
+    smp.load_local_state_dict(layer, sd)
