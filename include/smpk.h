@@ -203,6 +203,18 @@ SMPK_API int smpk_embed_bwd(const int64_t* ids, int64_t n, const void* dy, int64
                             int64_t rows_local, int dim, void* dtable, int64_t ld_dt, int out_f32,
                             int accumulate, int64_t padding_row, void* stream);
 /*
+ * smpk_embed_bwd_sorted — the same gradient for tables much larger than the batch (NCF:
+ * 10^8 rows): stable LSD radix sort of (local row, token position), then fixed-order
+ * segmented sums with one read-modify-write per unique row; O(n log rows), no float atomics
+ * (bit-deterministic).  accumulate = 0 zeroes dtable first.  dim, ld_dy, ld_dt multiples of 8.
+ * Workspace: smpk_embed_bwd_sorted_workspace(n, rows_local, dim) bytes.
+ */
+SMPK_API int64_t smpk_embed_bwd_sorted_workspace(int64_t n, int64_t rows_local, int dim);
+SMPK_API int smpk_embed_bwd_sorted(const int64_t* ids, int64_t n, const void* dy, int64_t ld_dy,
+                                   int64_t row_offset, int64_t rows_local, int dim, void* dtable, int64_t ld_dt,
+                                   int out_f32, int accumulate, int64_t padding_row, void* workspace,
+                                   int64_t workspace_bytes, void* stream);
+/*
  * Vocab-parallel softmax cross-entropy (builder-defined).
  *   fwd_local: stats[N][4] = {m_j, S_j = sum_{real cols} exp(l - m_j), l[target] if owned, owned}
  *              for the shard covering global columns [col_offset, col_offset + v_local); columns

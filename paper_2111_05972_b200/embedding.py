@@ -61,15 +61,31 @@ def embed_lookup(ids: torch.Tensor, table: torch.Tensor, *, row_offset: int, voc
 
 
 def embed_grad(ids: torch.Tensor, dy: torch.Tensor, *, rows: int, row_offset: int, padding_idx=None,
-               out_dtype=torch.bfloat16) -> torch.Tensor:
-    _check_cuda(ids, dy)
+               out_dtype=torch.bfloat16, out=None, accumulate=False, method: str = "auto") -> torch.Tensor:
+    """Deterministic scatter-add of dy rows into the rows of a (local) table.
+
+    method "sort" (default for 8-aligned widths): radix sort by row + fixed-order segmented sums,
+    O(n log rows) -- the NCF-scale path; "scan": the owner-computes kernel that scans the token
+    list once per 8-row block, O(rows * n), summing strictly in token order (small vocabularies,
+    odd widths).  out / accumulate: add into an existing gradient buffer (fp32 or bf16)."""
+    _check_cuda(ids, dy, out)
     ids = ids.reshape(-1).to(torch.int64).contiguous()
     dy = dy.reshape(ids.numel(), -1).contiguous()
     D = dy.shape[1]
-    g = torch.empty(rows, D, dtype=out_dtype, device=dy.device)
+    g = out if out is not None else torch.empty(rows, D, dtype=out_dtype, device=dy.device)
+    f32 = int(g.dtype == torch.float32)
+    pad = int(-1 if padding_idx is None else padding_idx)
+    sortable = D % 8 == 0 and g.stride(0) % 8 == 0 and D <= 8192
+    if method == "sort" or (method == "auto" and sortable):
+        n = ids.numel()
+        ws_bytes = _lib.size("smpk_embed_bwd_sorted_workspace", n, rows, D)
+        ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=dy.device)
+        _lib.call("smpk_embed_bwd_sorted", _ptr(ids), n, _ptr(dy), dy.stride(0), int(row_offset), rows, D, _ptr(g),
+                  g.stride(0), f32, int(bool(accumulate)), pad, _ptr(ws), ws.numel(), _stream(),
+                  launches=4 + 3 * max(1, (max(rows, 1).bit_length() + 7) // 8))
+        return g
     _lib.call("smpk_embed_bwd", _ptr(ids), ids.numel(), _ptr(dy), dy.stride(0), int(row_offset), rows, D, _ptr(g),
-              g.stride(0), int(out_dtype == torch.float32), 0, int(-1 if padding_idx is None else padding_idx),
-              _stream())
+              g.stride(0), f32, int(bool(accumulate)), pad, _stream())
     return g
 
 

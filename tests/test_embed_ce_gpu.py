@@ -62,6 +62,46 @@ def test_embed_grad_deterministic(smp1, D):
     assert torch.equal(got, again)
 
 
+@pytest.mark.parametrize("case", [
+    # rows, D, n, row_offset, padding, hot-row repeats, out dtype, accumulate, method
+    (300, 64, 5000, 0, 3, 50, torch.float32, False, "scan"),
+    (300, 8, 5000, 0, 3, 3000, torch.float32, False, "sort"),      # one run spanning ~100 windows
+    (12000, 64, 70000, 5000, 5123, 9000, torch.float32, True, "sort"),  # vocab shard: ids outside skipped
+    (50304, 2048, 16384, 0, None, 700, torch.bfloat16, False, "sort"),  # GPT-1.3B tied table
+    (1 << 20, 16, 300000, 0, None, 20000, torch.float32, True, "sort"),  # 3 radix passes
+])
+def test_embed_grad_sorted_vs_oracle(smp1, case):
+    """Sort-based deterministic scatter-add (csrc/embed_sort.cu) vs an fp64 index_add: vocab-shard
+    routing (ids outside [row_offset, row_offset+rows) contribute nothing), padding row, a hot row
+    whose run crosses many segment windows, accumulate into an existing buffer, bit-identical
+    reruns."""
+    from paper_2111_05972_b200 import embedding as E
+    rows, D, n, off, pad, hot, odt, acc, method = case
+    g = torch.Generator().manual_seed(rows + D)
+    ids = torch.randint(0, rows + 2 * off if off else rows, (n,), generator=g)
+    ids[torch.randperm(n, generator=g)[:hot]] = off + 7 if rows > 7 else off
+    if pad is not None:
+        ids[::97] = pad
+    dy = torch.randn(n, D, generator=g).to(torch.bfloat16)
+    base = torch.randn(rows, D, generator=g).to(odt)
+    out = base.clone().cuda() if acc else None
+    got = E.embed_grad(ids.cuda(), dy.cuda(), rows=rows, row_offset=off, padding_idx=pad, out_dtype=odt, out=out,
+                       accumulate=acc, method=method)
+    loc = ids - off
+    keep = (loc >= 0) & (loc < rows)
+    if pad is not None:
+        keep &= ids != pad
+    ref = torch.zeros(rows, D, dtype=torch.float64).index_add_(0, loc[keep], dy[keep].double())
+    if acc:
+        ref += base.double()
+    tol = 1e-5 if odt == torch.float32 else 1e-2
+    assert rel(got, ref) < tol
+    out2 = base.clone().cuda() if acc else None
+    again = E.embed_grad(ids.cuda(), dy.cuda(), rows=rows, row_offset=off, padding_idx=pad, out_dtype=odt, out=out2,
+                         accumulate=acc, method=method)
+    assert torch.equal(got, again)
+
+
 @pytest.mark.parametrize("V,N", [(4096, 300), (50257, 256), (1000, 37)])
 def test_vocab_ce_tp1(smp1, V, N):
     from paper_2111_05972_b200.embedding import vocab_padded, vocab_parallel_cross_entropy
