@@ -30,45 +30,46 @@ __device__ __forceinline__ float warp_max_f(float v) {
 // ---------------------------------------------------------------------------
 // embedding forward
 // ---------------------------------------------------------------------------
+// thread per (token, 8-column vector): consecutive threads walk a row's 16-B vectors, then the
+// next token -- coalesced for wide rows, and every lane busy for narrow ones (NCF: 8 columns per
+// rank, one vector per token; a warp per token left 31 lanes idle)
 __global__ void __launch_bounds__(256) embed_fwd_kernel(const int64_t* __restrict__ ids, int64_t n,
                                                         const bf16* __restrict__ table, int64_t ld_table,
                                                         int64_t row_offset, int64_t rows_local, int64_t vocab,
                                                         int dim, bf16* __restrict__ out, int64_t ld_out,
                                                         const bf16* __restrict__ pos_table, int64_t ld_pos, int seq,
                                                         unsigned long long* err_pos) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool vec = (dim % 8 == 0) && (ld_table % 8 == 0) && (ld_out % 8 == 0) && (ld_pos % 8 == 0);
-  for (int64_t t = (int64_t)blockIdx.x * 8 + warp; t < n; t += (int64_t)gridDim.x * 8) {
-    const int64_t id = ids[t];
-    if (id < 0 || id >= vocab) {
-      if (lane == 0 && err_pos) atomicMin(err_pos, (unsigned long long)t);
-    }
+  const int nvec = vec ? dim / 8 : dim;  // vectors (or scalars) per row
+  const int64_t total = n * nvec;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = idx / nvec;
+    const int c = (int)(idx - t * nvec);
+    const int64_t id = __ldg(ids + t);
+    if ((id < 0 || id >= vocab) && c == 0 && err_pos) atomicMin(err_pos, (unsigned long long)t);
     const int64_t loc = id - row_offset;
     const bool own = (id >= 0 && id < vocab) && loc >= 0 && loc < rows_local;
     const bf16* src = table + (own ? loc : 0) * ld_table;
     const bf16* ps = pos_table ? pos_table + (t % seq) * ld_pos : nullptr;
     bf16* dst = out + t * ld_out;
     if (vec) {
-      for (int c = lane * 8; c < dim; c += 256) {
-        uint4 u = own ? *reinterpret_cast<const uint4*>(src + c) : make_uint4(0, 0, 0, 0);
-        if (ps) {
-          uint4 p = *reinterpret_cast<const uint4*>(ps + c);
-          uint32_t a[4] = {u.x, u.y, u.z, u.w}, b[4] = {p.x, p.y, p.z, p.w};
+      uint4 u = own ? __ldg(reinterpret_cast<const uint4*>(src) + c) : make_uint4(0, 0, 0, 0);
+      if (ps) {
+        uint4 p = __ldg(reinterpret_cast<const uint4*>(ps) + c);
+        uint32_t a[4] = {u.x, u.y, u.z, u.w}, b[4] = {p.x, p.y, p.z, p.w};
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            float2 fa = unpack_bf16x2(a[j]), fb = unpack_bf16x2(b[j]);
-            a[j] = pack_bf16x2(fa.x + fb.x, fa.y + fb.y);
-          }
-          u = make_uint4(a[0], a[1], a[2], a[3]);
+        for (int j = 0; j < 4; ++j) {
+          float2 fa = unpack_bf16x2(a[j]), fb = unpack_bf16x2(b[j]);
+          a[j] = pack_bf16x2(fa.x + fb.x, fa.y + fb.y);
         }
-        *reinterpret_cast<uint4*>(dst + c) = u;
+        u = make_uint4(a[0], a[1], a[2], a[3]);
       }
+      reinterpret_cast<uint4*>(dst)[c] = u;
     } else {
-      for (int c = lane; c < dim; c += 32) {
-        float v = own ? bf2f(src[c]) : 0.f;
-        if (ps) v += bf2f(ps[c]);
-        dst[c] = f2bf(v);
-      }
+      float v = own ? bf2f(src[c]) : 0.f;
+      if (ps) v += bf2f(ps[c]);
+      dst[c] = f2bf(v);
     }
   }
 }
@@ -310,7 +311,8 @@ extern "C" int smpk_embed_fwd(const int64_t* ids, int64_t n, const void* table, 
   SMPK_REQUIRE(ids && table && out && dim > 0 && n >= 0, SMPK_ERR_BAD_ARG, "smpk_embed_fwd: bad arguments");
   SMPK_REQUIRE(!pos_table || seq > 0, SMPK_ERR_BAD_ARG, "smpk_embed_fwd: pos_table needs seq > 0");
   if (n == 0) return SMPK_OK;
-  int64_t grid = (n + 7) / 8;
+  const int64_t work = n * (dim % 8 == 0 ? dim / 8 : dim);
+  int64_t grid = (work + 255) / 256;
   if (grid > num_sms() * 16) grid = num_sms() * 16;
   embed_fwd_kernel<<<(int)grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       ids, n, reinterpret_cast<const bf16*>(table), ld_table, row_offset, rows_local, vocab, dim,

@@ -57,30 +57,50 @@ __global__ void __launch_bounds__(RS_THREADS) radix_hist_kernel(const uint32_t* 
   counts[(int64_t)threadIdx.x * num_tiles + blockIdx.x] = hist[threadIdx.x];
 }
 
-// counts[d][tile] -> global start of (digit d, tile): digit-major, tile-ordered exclusive scan
-__global__ void __launch_bounds__(256) radix_scan_kernel(int* __restrict__ counts, int num_tiles) {
-  __shared__ int tot[256];
-  const int d = threadIdx.x;
-  int s = 0;
-  int* row = counts + (int64_t)d * num_tiles;
-  for (int t = 0; t < num_tiles; ++t) {
-    const int v = row[t];
-    row[t] = s;
-    s += v;
-  }
-  tot[d] = s;
+// counts[d][tile] -> exclusive prefix over the tiles of digit d (block d, coalesced 1024-wide chunks
+// with a carried block scan) and digit_tot[d]; radix_digit_kernel turns the totals into the digit
+// bases.  Global position of (digit d, tile t) = digit_base[d] + counts[d][t].
+constexpr int SCAN_THREADS = 1024;
+__global__ void __launch_bounds__(SCAN_THREADS) radix_scan_kernel(int* __restrict__ counts, int num_tiles,
+                                                                  int* __restrict__ digit_tot) {
+  __shared__ int part[SCAN_THREADS];
+  __shared__ int carry;
+  int* row = counts + (int64_t)blockIdx.x * num_tiles;
+  if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  if (d == 0) {
-    int acc = 0;
-    for (int k = 0; k < 256; ++k) {
-      const int v = tot[k];
-      tot[k] = acc;
-      acc += v;
+  for (int base = 0; base < num_tiles; base += SCAN_THREADS) {
+    const int t = base + threadIdx.x;
+    const int v = t < num_tiles ? row[t] : 0;
+    part[threadIdx.x] = v;
+    __syncthreads();
+    for (int off = 1; off < SCAN_THREADS; off <<= 1) {  // inclusive Hillis-Steele scan
+      const int o = threadIdx.x >= off ? part[threadIdx.x - off] : 0;
+      __syncthreads();
+      part[threadIdx.x] += o;
+      __syncthreads();
     }
+    const int c = carry;
+    if (t < num_tiles) row[t] = c + part[threadIdx.x] - v;
+    __syncthreads();
+    if (threadIdx.x == SCAN_THREADS - 1) carry = c + part[threadIdx.x];
+    __syncthreads();
   }
+  if (threadIdx.x == 0) digit_tot[blockIdx.x] = carry;
+}
+
+__global__ void __launch_bounds__(256) radix_digit_kernel(int* __restrict__ digit_tot) {
+  __shared__ int part[256];
+  const int d = threadIdx.x;
+  const int v = digit_tot[d];
+  part[d] = v;
   __syncthreads();
-  const int base = tot[d];
-  for (int t = 0; t < num_tiles; ++t) row[t] += base;
+  for (int off = 1; off < 256; off <<= 1) {
+    const int o = d >= off ? part[d - off] : 0;
+    __syncthreads();
+    part[d] += o;
+    __syncthreads();
+  }
+  digit_tot[d] = part[d] - v;  // exclusive: the digit's base
 }
 
 // Stable scatter: warp w of a tile owns the tile's elements [w*256, w*256+256) in order; each
@@ -89,6 +109,7 @@ __global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(const uint32_
                                                                    const uint32_t* __restrict__ vals_in, int64_t n,
                                                                    int shift, int num_tiles,
                                                                    const int* __restrict__ counts,
+                                                                   const int* __restrict__ digit_base,
                                                                    uint32_t* __restrict__ keys_out,
                                                                    uint32_t* __restrict__ vals_out) {
   __shared__ int wc[RS_THREADS / 32][256];
@@ -132,7 +153,7 @@ __global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(const uint32_
     const int64_t i = base + it * 32 + lane;
     if (i < n) {
       const int d = (int)((key[it] >> shift) & 255);
-      const int64_t pos = (int64_t)counts[(int64_t)d * num_tiles + blockIdx.x] + wc[warp][d] + rank[it];
+      const int64_t pos = (int64_t)digit_base[d] + counts[(int64_t)d * num_tiles + blockIdx.x] + wc[warp][d] + rank[it];
       keys_out[pos] = key[it];
       vals_out[pos] = val[it];
     }
@@ -289,9 +310,13 @@ __global__ void __launch_bounds__(256) seg_large_kernel(const SegArgs a) {
   }
 }
 
-// A run crossing windows is owned by the window where it starts (tail partial): add the head
-// partials of the following windows in order until the run ends, then one read-modify-write.
+// A run crossing windows is owned by the window where it starts (tail partial): it adds the head
+// partials of the following windows up to the one where the run ends, then does one
+// read-modify-write.  The window range is found by binary search on the sorted keys and summed in
+// parallel with a fixed shape (window lanes stride the range in order, then a fixed tree), so a
+// Zipf-hot row spanning hundreds of windows costs a few microseconds, deterministically.
 __global__ void __launch_bounds__(256) seg_fixup_kernel(const SegArgs a, int num_windows) {
+  __shared__ float red[256 * 8];
   const int64_t w = blockIdx.x;
   const int nv = *a.n_valid;
   const int W = a.window;
@@ -299,25 +324,51 @@ __global__ void __launch_bounds__(256) seg_fixup_kernel(const SegArgs a, int num
   if (w * W >= nv || last + 1 >= nv) return;
   const uint32_t key = a.keys[last];
   if (a.keys[last + 1] != key) return;  // no run leaves this window
-  // the run must start in this window (otherwise an earlier window owns it)
   const int64_t i0 = w * W;
-  bool starts_here = true;
-  if (a.keys[i0] == key && i0 > 0 && a.keys[i0 - 1] == key) starts_here = false;
-  if (!starts_here) return;
+  if (a.keys[i0] == key && i0 > 0 && a.keys[i0 - 1] == key) return;  // an earlier window owns it
+  // last index of the run: binary search in (last, nv)
+  int64_t lo = last + 1, hi = nv - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (a.keys[mid] == key) lo = mid; else hi = mid - 1;
+  }
+  const int64_t u0 = w + 1, u1 = lo / W;  // windows holding head partials of this run
+  const int64_t K = u1 - u0 + 1;
   const int dim = a.dim;
-  for (int c0 = threadIdx.x * 8; c0 < dim; c0 += blockDim.x * 8) {
-    float acc[8];
-    const float* tail = a.partial + (w * 2 + 1) * (int64_t)dim + c0;
+  const int nvec = dim / 8;
+  int wl = 1;  // window lanes: a power of two with wl * nvec <= 256
+  while (nvec < 256 && wl * 2 * nvec <= 256) wl *= 2;
+  const int c = threadIdx.x % nvec, lane = threadIdx.x / nvec;
+  for (int cv = c; cv < nvec; cv += (nvec >= 256 ? 256 : nvec)) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (lane < wl) {
+      for (int64_t k = lane; k < K; k += wl) {
+        const float* head = a.partial + ((u0 + k) * 2 + 0) * (int64_t)dim + cv * 8;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = tail[e];
-    for (int64_t u = w + 1; u < num_windows; ++u) {
-      const float* head = a.partial + (u * 2 + 0) * (int64_t)dim + c0;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] += head[e];
-      const int64_t ul = min((int64_t)nv, (u + 1) * W) - 1;
-      if (ul + 1 >= nv || a.keys[ul + 1] != key) break;  // the run ends in window u
+        for (int e = 0; e < 8; ++e) acc[e] += head[e];
+      }
     }
-    rmw_row8(a, key, c0, acc);
+    if (wl > 1) {  // fixed tree over the window lanes
+      __syncthreads();
+      if (lane < wl)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) red[(lane * nvec + c) * 8 + e] = acc[e];
+      __syncthreads();
+      for (int s = wl >> 1; s > 0; s >>= 1) {
+        if (lane < s)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) red[(lane * nvec + c) * 8 + e] += red[((lane + s) * nvec + c) * 8 + e];
+        __syncthreads();
+      }
+      if (lane != 0) continue;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = red[c * 8 + e];
+    }
+    const float* tail = a.partial + (w * 2 + 1) * (int64_t)dim + cv * 8;
+    float tot[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) tot[e] = tail[e] + acc[e];
+    rmw_row8(a, key, cv * 8, tot);
   }
 }
 
@@ -341,7 +392,7 @@ static int64_t seg_windows(int64_t n, int dim) {
 extern "C" int64_t smpk_embed_bwd_sorted_workspace(int64_t n, int64_t rows_local, int dim) {
   (void)rows_local;
   const int64_t tiles = (n + RS_TILE - 1) / RS_TILE;
-  return align256(4 * n) * 4 + align256(256 * tiles * 4) + 256 + align256(seg_windows(n, dim) * 2 * dim * 4);
+  return align256(4 * n) * 4 + align256(256 * tiles * 4) + 1024 + 256 + align256(seg_windows(n, dim) * 2 * dim * 4);
 }
 
 extern "C" int smpk_embed_bwd_sorted(const int64_t* ids, int64_t n, const void* dy, int64_t ld_dy,
@@ -371,8 +422,9 @@ extern "C" int smpk_embed_bwd_sorted(const int64_t* ids, int64_t n, const void* 
   uint32_t* v1 = reinterpret_cast<uint32_t*>(ws + 3 * kb);
   const int tiles = (int)((n + RS_TILE - 1) / RS_TILE);
   int* counts = reinterpret_cast<int*>(ws + 4 * kb);
-  int* n_valid = reinterpret_cast<int*>(ws + 4 * kb + align256(256LL * tiles * 4));
-  float* partial = reinterpret_cast<float*>(ws + 4 * kb + align256(256LL * tiles * 4) + 256);
+  int* digit_base = reinterpret_cast<int*>(ws + 4 * kb + align256(256LL * tiles * 4));
+  int* n_valid = reinterpret_cast<int*>(ws + 4 * kb + align256(256LL * tiles * 4) + 1024);
+  float* partial = reinterpret_cast<float*>(ws + 4 * kb + align256(256LL * tiles * 4) + 1024 + 256);
   cudaMemsetAsync(n_valid, 0, sizeof(int), st);
   embed_keys_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ids, n, row_offset, rows_local, padding_row, k0, v0,
                                                                   n_valid);
@@ -381,8 +433,9 @@ extern "C" int smpk_embed_bwd_sorted(const int64_t* ids, int64_t n, const void* 
   const int nbits = bits_for(rows_local);  // keys in [0, rows_local] (sentinel included)
   for (int shift = 0; shift < nbits; shift += 8) {
     radix_hist_kernel<<<tiles, RS_THREADS, 0, st>>>(k0, n, shift, tiles, counts);
-    radix_scan_kernel<<<1, 256, 0, st>>>(counts, tiles);
-    radix_scatter_kernel<<<tiles, RS_THREADS, 0, st>>>(k0, v0, n, shift, tiles, counts, k1, v1);
+    radix_scan_kernel<<<256, SCAN_THREADS, 0, st>>>(counts, tiles, digit_base);
+    radix_digit_kernel<<<1, 256, 0, st>>>(digit_base);
+    radix_scatter_kernel<<<tiles, RS_THREADS, 0, st>>>(k0, v0, n, shift, tiles, counts, digit_base, k1, v1);
     rc = check_launch("smpk_embed_bwd_sorted(radix)");
     if (rc) return rc;
     uint32_t* t = k0;

@@ -82,7 +82,7 @@ def embed_grad(ids: torch.Tensor, dy: torch.Tensor, *, rows: int, row_offset: in
         ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=dy.device)
         _lib.call("smpk_embed_bwd_sorted", _ptr(ids), n, _ptr(dy), dy.stride(0), int(row_offset), rows, D, _ptr(g),
                   g.stride(0), f32, int(bool(accumulate)), pad, _ptr(ws), ws.numel(), _stream(),
-                  launches=4 + 3 * max(1, (max(rows, 1).bit_length() + 7) // 8))
+                  launches=4 + 4 * max(1, (max(rows, 1).bit_length() + 7) // 8))
         return g
     _lib.call("smpk_embed_bwd", _ptr(ids), ids.numel(), _ptr(dy), dy.stride(0), int(row_offset), rows, D, _ptr(g),
               g.stride(0), f32, int(bool(accumulate)), pad, _stream())
