@@ -300,6 +300,36 @@ SMPK_API int smpk_flash_attn_bwd(const void* qkv, int64_t ld, const void* out, i
  *                       ever consumed); smpk_symm_timeout_peer reads the record without a CUDA
  *                       call, so the host can raise PEER_TIMEOUT naming the stuck peer
  */
+/*
+ * smpk_gemm_grouped — several independent GEMMs in one launch (currently n <= 2 are fused).
+ * Each smpk_gemm_desc carries the arguments of smpk_gemm_ex2.  Two problems are fused into one
+ * persistent CTA-pair grid when one of them is a plain bf16 GEMM (no epilogue, no column sums)
+ * and both tile as 256 x 256 unsplit pairs: the plain problem's units (the long weight-gradient
+ * tiles of a backward) run first, the other's (with its fused epilogue) fill in behind them, so
+ * neither exposes its own wave tail or epilogue.  Otherwise the problems run one after the other.
+ * Used by the transformer backward for (dW, dX) pairs that read the same upstream gradient.
+ */
+typedef struct smpk_gemm_desc {
+  const void* a;
+  int a_mn_major;
+  int64_t lda, a_bs1, a_bs2;
+  const void* b;
+  int b_mn_major;
+  int64_t ldb, b_bs1, b_bs2;
+  void* c;
+  int c_f32;
+  int64_t ldc, c_bs1, c_bs2;
+  int M, N, K, nb1, nb2;
+  float alpha, beta;
+  int epilogue, act;
+  const void* bias;
+  void* aux;
+  int64_t ldaux;
+  void* workspace;
+  int64_t workspace_bytes;
+  float* colsum_part;
+} smpk_gemm_desc;
+SMPK_API int smpk_gemm_grouped(const smpk_gemm_desc* descs, int n, void* stream);
 SMPK_API int smpk_gemm_rs(const void* a, int a_mn_major, int64_t lda, const void* b, int b_mn_major, int64_t ldb,
                           void* const* peers, int npeers, int64_t ldc, int64_t rows_per_owner,
                           int64_t peer_slot_off, int M, int N, int K, void* stream);

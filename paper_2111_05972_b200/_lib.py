@@ -51,6 +51,7 @@ SIGNATURES: dict[str, list] = {
     "smpk_act_bwd": [P, P, I, I, I, P, P],
     "smpk_copy_async": [P, P, L, P],
     "smpk_rng_next": [P, P, P],
+    "smpk_gemm_grouped": [P, I, P],
     "smpk_embed_bwd_sorted": [P, L, P, L, L, L, I, P, L, I, I, L, P, L, P],
     "smpk_adam_step": [P, P, P, P, P, L, F, F, F, F, F, I, F, P],
     "smpk_debug_fa_trace": [P, I],

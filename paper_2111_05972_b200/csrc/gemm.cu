@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 
 #include "smpk_common.cuh"
 
@@ -271,9 +272,14 @@ __device__ __forceinline__ void stage_f32_row(uint8_t* box, int r, const float (
 // of A and half (BN/2 rows) of B, the leader issues M=256 cta_group::2 MMAs that read both
 // CTAs' shared memory, and each CTA's TMEM receives the accumulator of its own 128 rows —
 // halving the per-SM operand traffic through shared memory, the limit of the 1-CTA form.
-template <int BN, int STAGES, int EPI, int ACT, bool F32OUT, bool BETA, bool PAIR>
-__device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensorMap* tmB, const EpiMaps* maps,
-                                          const GemmArgs& g) {
+template <int BN, int STAGES, int EPI, int ACT, bool F32OUT, bool BETA, bool PAIR, int NPROB = 1>
+__device__ __forceinline__ void gemm_body(const CUtensorMap* tmA_arr, const CUtensorMap* tmB_arr,
+                                          const EpiMaps* maps_arr, const GemmArgs* gs) {
+  // NPROB == 2 (grouped launch): problem 1 is a plain (EPI_NONE, bf16) GEMM whose units run first
+  // (the long weight-gradient tiles), problem 0 the one with the EPI epilogue; one persistent grid
+  // walks both unit lists, so neither problem's wave tail or epilogue is exposed on its own.
+  const int U1 = NPROB == 2 ? gs[1].num_units : 0;
+  const int total_units = gs[0].num_units + U1;
   constexpr int NUM_EPI_WARPS = epi_warps(EPI);
   using Cfg = GemmCfg<BN, STAGES, PAIR, NUM_EPI_WARPS>;
   constexpr int BMT = PAIR ? 2 * BM : BM;  // tile rows
@@ -298,8 +304,10 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensor
   const int ustep = PAIR ? (gridDim.x >> 1) : gridDim.x;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(tmA);
-    tma_prefetch_desc(tmB);
+    for (int q = 0; q < NPROB; ++q) {
+      tma_prefetch_desc(tmA_arr + q);
+      tma_prefetch_desc(tmB_arr + q);
+    }
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full_bar[i], 1);
       mbar_init(&empty_bar[i], 1);
@@ -325,7 +333,12 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensor
       // ---------------- TMA producer (both CTAs of a pair) ----------------
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = unit0; u < g.num_units; u += ustep) {
+      for (int uu = unit0; uu < total_units; uu += ustep) {
+        const int p = (NPROB == 2 && uu < U1) ? 1 : 0;
+        const int u = p ? uu : uu - U1;
+        const GemmArgs& g = gs[p];
+        const CUtensorMap* tmA = tmA_arr + p;
+        const CUtensorMap* tmB = tmB_arr + p;
         int tile, kb0, kb1, b1, b2, tm, tn;
         decode_unit(g, u, tile, kb0, kb1);
         decode_tile(g, tile, b1, b2, tm, tn);
@@ -383,16 +396,19 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensor
       // The whole warp runs the loop so the descriptor arithmetic stays warp-uniform (uniform
       // registers, no per-MMA R2UR shuffles); one elected lane issues.  Descriptors are built
       // once and advanced by constant offsets (addresses are encoded >> 4 in the low 14 bits).
-      const uint32_t idesc = make_idesc_bf16(BMT, BN, g.a_mn, g.b_mn);
-      const uint64_t a_desc0 = make_sw128_desc(smem_u32(sA), g.a_mn ? BK * 128 : 16, 1024);
-      const uint64_t b_desc0 = make_sw128_desc(smem_u32(sB), g.b_mn ? BK * 128 : 16, 1024);
-      const uint32_t a_kstep = g.a_mn ? (2048 >> 4) : (32 >> 4);
-      const uint32_t b_kstep = g.b_mn ? (2048 >> 4) : (32 >> 4);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = unit0; u < g.num_units; u += ustep) {
+      for (int uu = unit0; uu < total_units; uu += ustep) {
+        const int p = (NPROB == 2 && uu < U1) ? 1 : 0;
+        const int u = p ? uu : uu - U1;
+        const GemmArgs& g = gs[p];
+        const uint32_t idesc = make_idesc_bf16(BMT, BN, g.a_mn, g.b_mn);
+        const uint64_t a_desc0 = make_sw128_desc(smem_u32(sA), g.a_mn ? BK * 128 : 16, 1024);
+        const uint64_t b_desc0 = make_sw128_desc(smem_u32(sB), g.b_mn ? BK * 128 : 16, 1024);
+        const uint32_t a_kstep = g.a_mn ? (2048 >> 4) : (32 >> 4);
+        const uint32_t b_kstep = g.b_mn ? (2048 >> 4) : (32 >> 4);
         int tile, kb0, kb1;
         decode_unit(g, u, tile, kb0, kb1);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
@@ -443,8 +459,11 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensor
     int acc = 0;
     uint32_t acc_phase = 0;
     const int etid = threadIdx.x - 128;  // 0 .. 32*NUM_EPI_WARPS-1
-    constexpr bool AUXPF = (EPI == SMPK_EPI_ADD);  // DACT (16 warps, 96 registers) spilled with it: slower
-    for (int u = unit0; u < g.num_units; u += ustep) {
+    for (int uu = unit0; uu < total_units; uu += ustep) {
+      const int p = (NPROB == 2 && uu < U1) ? 1 : 0;
+      const int u = p ? uu : uu - U1;
+      const GemmArgs& g = gs[p];
+      const EpiMaps* maps = maps_arr + p;
       int tile, kb0, kb1, b1, b2, tm, tn;
       decode_unit(g, u, tile, kb0, kb1);
       decode_tile(g, tile, b1, b2, tm, tn);
@@ -452,172 +471,181 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA, const CUtensor
       const int row0 = tm * BMT + (int)rank * BM + quarter * 32;  // first row of this warp's 32
       const int row = row0 + lane;
       const int64_t c_off = (int64_t)b1 * g.c_bs1 + (int64_t)b2 * g.c_bs2;
-      // DACT / ADD: the auxiliary operand (pre-activation / residual) of the next 32-column chunk
-      // is loaded one chunk ahead -- the first one while the main loop still runs -- so its HBM
-      // latency is off the epilogue's critical path (ncu r02: 11% of the DACT stall samples)
-      uint4 auxv[4];
-      auto aux_ok = [&](int i) {
-        const int colc = tn * BN + (cgroup + NGR * i) * 32;
-        return AUXPF && active && g.splits == 1 && row < g.M && colc + 32 <= g.N && g.vec_ok;
-      };
-      auto aux_load = [&](int i) {
-        if (aux_ok(i)) {
-          const uint4* src = reinterpret_cast<const uint4*>(g.aux + c_off + (int64_t)row * g.ldaux + tn * BN +
-                                                            (cgroup + NGR * i) * 32);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) auxv[q] = __ldg(src + q);
-        }
-      };
-      if constexpr (AUXPF) aux_load(0);
-      mbar_wait(&tfull_bar[acc], acc_phase);
-      tc_fence_after();
-      const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16);
-      if (g.splits == 1) {
-#pragma unroll 1
-        for (int i = 0; i < CPW; ++i) {
-          const int ch = cgroup + NGR * i;
-          uint32_t r[32];
-          if (active) {
-            tmem_ld_32x32b_x32(t_row + ch * 32, r);
-            tmem_ld_wait();
+      // one tile's epilogue with epilogue kind E (problem 1 of a grouped launch: plain)
+      auto tile_epi = [&](auto epi_c) {
+        constexpr int E = decltype(epi_c)::value;
+        constexpr int EA = E == EPI ? ACT : 0;
+        constexpr bool AUXPF = (E == SMPK_EPI_ADD);  // DACT (16 warps, 96 registers) spilled with it
+        // DACT / ADD: the auxiliary operand (pre-activation / residual) of the next 32-column chunk
+        // is loaded one chunk ahead -- the first one while the main loop still runs -- so its HBM
+        // latency is off the epilogue's critical path (ncu r02: 11% of the DACT stall samples)
+        uint4 auxv[4];
+        auto aux_ok = [&](int i) {
+          const int colc = tn * BN + (cgroup + NGR * i) * 32;
+          return AUXPF && active && g.splits == 1 && row < g.M && colc + 32 <= g.N && g.vec_ok;
+        };
+        auto aux_load = [&](int i) {
+          if (aux_ok(i)) {
+            const uint4* src = reinterpret_cast<const uint4*>(g.aux + c_off + (int64_t)row * g.ldaux + tn * BN +
+                                                              (cgroup + NGR * i) * 32);
+  #pragma unroll
+            for (int q = 0; q < 4; ++q) auxv[q] = __ldg(src + q);
           }
-          if (i == CPW - 1) {  // this warp's accumulator columns are in registers: free the TMEM buffer
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-              if constexpr (PAIR) mbar_arrive_cluster_relaxed(&tempty_bar[acc], 0);
-              else mbar_arrive_relaxed(&tempty_bar[acc]);
+        };
+        if constexpr (AUXPF) aux_load(0);
+
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16);
+        if (g.splits == 1) {
+  #pragma unroll 1
+          for (int i = 0; i < CPW; ++i) {
+            const int ch = cgroup + NGR * i;
+            uint32_t r[32];
+            if (active) {
+              tmem_ld_32x32b_x32(t_row + ch * 32, r);
+              tmem_ld_wait();
             }
-          }
-          if (!active) continue;
-          const int col0 = tn * BN + ch * 32;
-          if (col0 >= g.N) continue;
-          float v[32];
-          uint32_t pre[16];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-          if constexpr (AUXPF) {
-            uint4 cur[4];
-            const bool have = aux_ok(i);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) cur[q] = auxv[q];
-            if (i + 1 < CPW) aux_load(i + 1);  // next chunk's operand in flight during this one's math
-            epilogue_math32<EPI, ACT, F32OUT, BETA>(g, row < g.M, row, col0, c_off, v, pre, have ? cur : nullptr);
-          } else {
-            epilogue_math32<EPI, ACT, F32OUT, BETA>(g, row < g.M, row, col0, c_off, v, pre);
-          }
-          if (g.tma_store) {
-            if (lane == 0) bulk_wait_read0();  // the previous chunk's bulk store has read the box
-            __syncwarp();
-            if constexpr (F32OUT) {
-              stage_f32_row(stg, lane, v);
+            if (i == CPW - 1) {  // this warp's accumulator columns are in registers: free the TMEM buffer
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) {
+                if constexpr (PAIR) mbar_arrive_cluster_relaxed(&tempty_bar[acc], 0);
+                else mbar_arrive_relaxed(&tempty_bar[acc]);
+              }
+            }
+            if (!active) continue;
+            const int col0 = tn * BN + ch * 32;
+            if (col0 >= g.N) continue;
+            float v[32];
+            uint32_t pre[16];
+  #pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+            if constexpr (AUXPF) {
+              uint4 cur[4];
+              const bool have = aux_ok(i);
+  #pragma unroll
+              for (int q = 0; q < 4; ++q) cur[q] = auxv[q];
+              if (i + 1 < CPW) aux_load(i + 1);  // next chunk's operand in flight during this one's math
+              epilogue_math32<E, EA, F32OUT, BETA>(g, row < g.M, row, col0, c_off, v, pre, have ? cur : nullptr);
             } else {
-              uint32_t w[16];
-#pragma unroll
-              for (int j = 0; j < 16; ++j) w[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
-              stage_bf16_row(stg, lane, w);
-              if constexpr (EPI == SMPK_EPI_BIAS_ACT) stage_bf16_row(stg + 2048, lane, pre);
+              epilogue_math32<E, EA, F32OUT, BETA>(g, row < g.M, row, col0, c_off, v, pre);
             }
-            fence_proxy_async_smem();
-            __syncwarp();
-            if constexpr (!F32OUT) {
-              if (g.colsum_part != nullptr && row0 < g.M && col0 + lane < g.N) {  // rows >= M hold zeros
-                // lane = column: sum the box's 32 stored rows (SWIZZLE_64B granule order)
-                float cs4[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent chains (row order fixed)
-#pragma unroll
-                for (int rr = 0; rr < 32; ++rr) {
-                  const bf16* e = reinterpret_cast<const bf16*>(
-                      stg + rr * 64 + ((((lane >> 3) ^ ((rr >> 1) & 3))) << 4) + (lane & 7) * 2);
-                  cs4[rr & 3] += bf2f(*e);
-                }
-                g.colsum_part[(int64_t)(row0 >> 5) * g.N + col0 + lane] = (cs4[0] + cs4[1]) + (cs4[2] + cs4[3]);
-              }
-            }
-            if (lane == 0) {
-              if (g.npeers) {  // reduce-scatter: rows of one CTA belong to one owner
-                const int owner = (int)(row0 / g.rows_per_owner);
-                tma_store_4d(&maps->peer[owner], stg, col0, (int)(row0 - owner * g.rows_per_owner), 0, 0);
+            if (g.tma_store) {
+              if (lane == 0) bulk_wait_read0();  // the previous chunk's bulk store has read the box
+              __syncwarp();
+              if constexpr (F32OUT) {
+                stage_f32_row(stg, lane, v);
               } else {
-                tma_store_4d(&maps->c, stg, col0, row0, b1, b2);
-                if constexpr (EPI == SMPK_EPI_BIAS_ACT) tma_store_4d(&maps->aux, stg + 2048, col0, row0, b1, b2);
+                uint32_t w[16];
+  #pragma unroll
+                for (int j = 0; j < 16; ++j) w[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
+                stage_bf16_row(stg, lane, w);
+                if constexpr (E == SMPK_EPI_BIAS_ACT) stage_bf16_row(stg + 2048, lane, pre);
               }
-              bulk_commit();
+              fence_proxy_async_smem();
+              __syncwarp();
+              if constexpr (!F32OUT) {
+                if (g.colsum_part != nullptr && row0 < g.M && col0 + lane < g.N) {  // rows >= M hold zeros
+                  // lane = column: sum the box's 32 stored rows (SWIZZLE_64B granule order)
+                  float cs4[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent chains (row order fixed)
+  #pragma unroll
+                  for (int rr = 0; rr < 32; ++rr) {
+                    const bf16* e = reinterpret_cast<const bf16*>(
+                        stg + rr * 64 + ((((lane >> 3) ^ ((rr >> 1) & 3))) << 4) + (lane & 7) * 2);
+                    cs4[rr & 3] += bf2f(*e);
+                  }
+                  g.colsum_part[(int64_t)(row0 >> 5) * g.N + col0 + lane] = (cs4[0] + cs4[1]) + (cs4[2] + cs4[3]);
+                }
+              }
+              if (lane == 0) {
+                if (g.npeers) {  // reduce-scatter: rows of one CTA belong to one owner
+                  const int owner = (int)(row0 / g.rows_per_owner);
+                  tma_store_4d(&maps->peer[owner], stg, col0, (int)(row0 - owner * g.rows_per_owner), 0, 0);
+                } else {
+                  tma_store_4d(&maps->c, stg, col0, row0, b1, b2);
+                  if constexpr (E == SMPK_EPI_BIAS_ACT) tma_store_4d(&maps->aux, stg + 2048, col0, row0, b1, b2);
+                }
+                bulk_commit();
+              }
+            } else if (row < g.M) {
+              epilogue_direct32<E, F32OUT>(g, row, col0, c_off, v, pre);
             }
-          } else if (row < g.M) {
-            epilogue_direct32<EPI, F32OUT>(g, row, col0, c_off, v, pre);
+          }
+        } else {
+          // split-K: raw fp32 partial of this CTA's 128 x BN block -> ws, column-major inside the
+          // block so that a warp's store of one accumulator column is one contiguous 128-byte line
+          constexpr int HALVES = PAIR ? 2 : 1;
+          const int split = u / g.num_tiles;
+          const int sidx = tile * HALVES + (int)rank;  // this CTA's block of the tile
+          const int64_t blk = (int64_t)BM * BN;
+          float* part = g.ws + ((int64_t)split * g.num_tiles * HALVES + sidx) * blk + rl;
+  #pragma unroll 1
+          for (int i = 0; i < CPW; ++i) {
+            const int ch = cgroup + NGR * i;
+            uint32_t r[32];
+            if (active) {
+              tmem_ld_32x32b_x32(t_row + ch * 32, r);
+              tmem_ld_wait();
+              float* d = part + (int64_t)ch * 32 * BM;
+  #pragma unroll
+              for (int j = 0; j < 32; ++j) __stcg(d + j * BM, __uint_as_float(r[j]));
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (PAIR) mbar_arrive_cluster(&tempty_bar[acc], 0);
+            else mbar_arrive(&tempty_bar[acc]);
+          }
+          // all splits of a tile are co-resident (host guarantees num_units <= grid slots): wait
+          // for every partial, then this split reduces its stripe of the block's rows in split
+          // order (deterministic) and runs the epilogue on it.
+          __threadfence();
+          named_barrier_sync(1, 32 * NUM_EPI_WARPS);
+          if (etid == 0) {
+            const int nblk = g.num_tiles * HALVES;
+            atomicAdd(g.sem + sidx, 1);
+            while (ld_acquire_gpu(g.sem + sidx) < g.splits) __nanosleep(32);
+            // last one out re-arms both counters for the next launch
+            if (atomicAdd(g.sem + nblk + sidx, 1) == g.splits - 1) {
+              g.sem[sidx] = 0;
+              g.sem[nblk + sidx] = 0;
+            }
+          }
+          named_barrier_sync(1, 32 * NUM_EPI_WARPS);
+          __threadfence();
+          const int rows_per = (BM + g.splits - 1) / g.splits;
+          const int r0 = split * rows_per;
+          const int nrows = min(rows_per, BM - r0);
+          const int ngroups = (nrows + 31) >> 5;  // 32-row groups: lane = row
+          const int64_t sstride = (int64_t)g.num_tiles * HALVES * blk;
+          const float* tbase = g.ws + (int64_t)sidx * blk;
+          const int ewarp = etid >> 5;
+          for (int item = ewarp; item < ngroups * NCH; item += NUM_EPI_WARPS) {
+            const int rg = item / NCH;
+            const int ch = item - rg * NCH;
+            const int rr = r0 + rg * 32 + lane;
+            const int grow = tm * BMT + (int)rank * BM + rr;
+            const int col0 = tn * BN + ch * 32;
+            if (rr >= r0 + nrows || grow >= g.M || col0 >= g.N) continue;
+            float v[32];
+  #pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0.f;
+            const float* src0 = tbase + (int64_t)ch * 32 * BM + rr;
+            for (int sp = 0; sp < g.splits; ++sp) {
+              const float* src = src0 + sp * sstride;
+  #pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += __ldcg(src + j * BM);
+            }
+            uint32_t pre[16];
+            epilogue_math32<E, EA, F32OUT, BETA>(g, true, grow, col0, c_off, v, pre);
+            epilogue_direct32<E, F32OUT>(g, grow, col0, c_off, v, pre);
           }
         }
-      } else {
-        // split-K: raw fp32 partial of this CTA's 128 x BN block -> ws, column-major inside the
-        // block so that a warp's store of one accumulator column is one contiguous 128-byte line
-        constexpr int HALVES = PAIR ? 2 : 1;
-        const int split = u / g.num_tiles;
-        const int sidx = tile * HALVES + (int)rank;  // this CTA's block of the tile
-        const int64_t blk = (int64_t)BM * BN;
-        float* part = g.ws + ((int64_t)split * g.num_tiles * HALVES + sidx) * blk + rl;
-#pragma unroll 1
-        for (int i = 0; i < CPW; ++i) {
-          const int ch = cgroup + NGR * i;
-          uint32_t r[32];
-          if (active) {
-            tmem_ld_32x32b_x32(t_row + ch * 32, r);
-            tmem_ld_wait();
-            float* d = part + (int64_t)ch * 32 * BM;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) __stcg(d + j * BM, __uint_as_float(r[j]));
-          }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if constexpr (PAIR) mbar_arrive_cluster(&tempty_bar[acc], 0);
-          else mbar_arrive(&tempty_bar[acc]);
-        }
-        // all splits of a tile are co-resident (host guarantees num_units <= grid slots): wait
-        // for every partial, then this split reduces its stripe of the block's rows in split
-        // order (deterministic) and runs the epilogue on it.
-        __threadfence();
-        named_barrier_sync(1, 32 * NUM_EPI_WARPS);
-        if (etid == 0) {
-          const int nblk = g.num_tiles * HALVES;
-          atomicAdd(g.sem + sidx, 1);
-          while (ld_acquire_gpu(g.sem + sidx) < g.splits) __nanosleep(32);
-          // last one out re-arms both counters for the next launch
-          if (atomicAdd(g.sem + nblk + sidx, 1) == g.splits - 1) {
-            g.sem[sidx] = 0;
-            g.sem[nblk + sidx] = 0;
-          }
-        }
-        named_barrier_sync(1, 32 * NUM_EPI_WARPS);
-        __threadfence();
-        const int rows_per = (BM + g.splits - 1) / g.splits;
-        const int r0 = split * rows_per;
-        const int nrows = min(rows_per, BM - r0);
-        const int ngroups = (nrows + 31) >> 5;  // 32-row groups: lane = row
-        const int64_t sstride = (int64_t)g.num_tiles * HALVES * blk;
-        const float* tbase = g.ws + (int64_t)sidx * blk;
-        const int ewarp = etid >> 5;
-        for (int item = ewarp; item < ngroups * NCH; item += NUM_EPI_WARPS) {
-          const int rg = item / NCH;
-          const int ch = item - rg * NCH;
-          const int rr = r0 + rg * 32 + lane;
-          const int grow = tm * BMT + (int)rank * BM + rr;
-          const int col0 = tn * BN + ch * 32;
-          if (rr >= r0 + nrows || grow >= g.M || col0 >= g.N) continue;
-          float v[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = 0.f;
-          const float* src0 = tbase + (int64_t)ch * 32 * BM + rr;
-          for (int sp = 0; sp < g.splits; ++sp) {
-            const float* src = src0 + sp * sstride;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] += __ldcg(src + j * BM);
-          }
-          uint32_t pre[16];
-          epilogue_math32<EPI, ACT, F32OUT, BETA>(g, true, grow, col0, c_off, v, pre);
-          epilogue_direct32<EPI, F32OUT>(g, grow, col0, c_off, v, pre);
-        }
-      }
+      };
+      if (NPROB == 2 && p == 1) tile_epi(std::integral_constant<int, SMPK_EPI_NONE>{});
+      else tile_epi(std::integral_constant<int, EPI>{});
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -644,14 +672,27 @@ template <int BN, int STAGES, int EPI, int ACT, bool F32OUT, bool BETA>
 __global__ void __launch_bounds__(gemm_threads(EPI), 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ EpiMaps maps, const GemmArgs g) {
-  gemm_body<BN, STAGES, EPI, ACT, F32OUT, BETA, false>(&tmA, &tmB, &maps, g);
+  gemm_body<BN, STAGES, EPI, ACT, F32OUT, BETA, false>(&tmA, &tmB, &maps, &g);
 }
 
 template <int BN, int STAGES, int EPI, int ACT, bool F32OUT, bool BETA>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm_threads(EPI), 1)
     gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                            const __grid_constant__ EpiMaps maps, const GemmArgs g) {
-  gemm_body<BN, STAGES, EPI, ACT, F32OUT, BETA, true>(&tmA, &tmB, &maps, g);
+  gemm_body<BN, STAGES, EPI, ACT, F32OUT, BETA, true>(&tmA, &tmB, &maps, &g);
+}
+
+// Grouped launch of two independent GEMMs on CTA pairs (see gemm_body NPROB == 2).
+struct GroupParams {
+  CUtensorMap ta[2], tb[2];
+  EpiMaps maps[2];
+  GemmArgs g[2];
+};
+
+template <int BN, int STAGES, int EPI, int ACT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm_threads(EPI), 1)
+    gemm_bf16_tcgen05_pair_grouped(const __grid_constant__ GroupParams P) {
+  gemm_body<BN, STAGES, EPI, ACT, false, false, true, 2>(P.ta, P.tb, P.maps, P.g);
 }
 
 // ---------------------------------------------------------------------------
@@ -895,12 +936,15 @@ extern "C" int64_t smpk_gemm_workspace(int M, int N, int K, int nb1, int nb2) {
   return splitk_ws_bytes(BN, pair, tiles, splits);
 }
 
-static int gemm_impl(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, int64_t a_bs2, const void* b,
-                     int b_mn_major, int64_t ldb, int64_t b_bs1, int64_t b_bs2, void* c, int c_f32, int64_t ldc,
-                     int64_t c_bs1, int64_t c_bs2, int M, int N, int K, int nb1, int nb2, float alpha, float beta,
-                     int epilogue, int act, const void* bias, void* aux, int64_t ldaux, void* const* peers_host,
-                     int npeers, int64_t rows_per_owner, int64_t peer_slot_off, void* workspace,
-                     int64_t workspace_bytes, float* colsum_part, void* stream) {
+// Operand / epilogue maps and kernel arguments of one GEMM (no launch).  grouped: the problem runs
+// inside a grouped CTA-pair launch, so split-K is off (the other problem fills the machine).
+static int gemm_prepare(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, int64_t a_bs2, const void* b,
+                        int b_mn_major, int64_t ldb, int64_t b_bs1, int64_t b_bs2, void* c, int c_f32, int64_t ldc,
+                        int64_t c_bs1, int64_t c_bs2, int M, int N, int K, int nb1, int nb2, float alpha, float beta,
+                        int epilogue, int act, const void* bias, void* aux, int64_t ldaux, void* const* peers_host,
+                        int npeers, int64_t rows_per_owner, int64_t peer_slot_off, void* workspace,
+                        int64_t workspace_bytes, float* colsum_part, bool grouped, CUtensorMap& ta, CUtensorMap& tb,
+                        EpiMaps& maps, GemmArgs& g, int& BN, bool& pair) {
   SMPK_REQUIRE(M > 0 && N > 0 && K > 0 && nb1 > 0 && nb2 > 0, SMPK_ERR_BAD_SHAPE,
                "smpk_gemm: bad shape M=%d N=%d K=%d nb=%dx%d", M, N, K, nb1, nb2);
   SMPK_REQUIRE(a && b && (c || npeers), SMPK_ERR_BAD_ARG, "smpk_gemm: null operand");
@@ -912,15 +956,20 @@ static int gemm_impl(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, 
   SMPK_REQUIRE(!need_aux || aux, SMPK_ERR_BAD_ARG, "smpk_gemm: epilogue %d needs aux", epilogue);
   SMPK_REQUIRE(!(need_aux && c_f32), SMPK_ERR_UNSUPPORTED, "smpk_gemm: aux epilogues need bf16 C");
 
-  int BN, tiles, num_kb, splits, kb_per;
-  bool pair;
+  int tiles, num_kb, splits, kb_per;
   plan_gemm(M, N, K, nb1, nb2, BN, pair, tiles, num_kb, splits, kb_per);
+  if (grouped && splits > 1) {  // back to the unsplit CTA-pair plan
+    BN = pick_bn(N);
+    pair = BN >= 128 && M >= 2 * BM && pair_enabled();
+    tiles = ((M + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM)) * ((N + BN - 1) / BN) * nb1 * nb2;
+    splits = 1;
+    kb_per = num_kb;
+  }
   if (npeers || splits > 1 && (workspace == nullptr || workspace_bytes < splitk_ws_bytes(BN, pair, tiles, splits))) {
     splits = 1;  // no (or too small a) workspace: single pass over K
     kb_per = num_kb;
   }
 
-  CUtensorMap ta, tb;
   // an operand with batch stride 0 is broadcast over that batch dim (one map slice, coordinate 0)
   const bool a_bc1 = nb1 > 1 && a_bs1 == 0, a_bc2 = nb2 > 1 && a_bs2 == 0;
   const bool b_bc1 = nb1 > 1 && b_bs1 == 0, b_bc2 = nb2 > 1 && b_bs2 == 0;
@@ -930,7 +979,7 @@ static int gemm_impl(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, 
                         pair ? BN / 2 : BN, "B");
   if (rc) return rc;
 
-  GemmArgs g;
+  memset(&g, 0, sizeof(g));
   g.M = M;
   g.N = N;
   g.K = K;
@@ -980,7 +1029,6 @@ static int gemm_impl(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, 
   g.vec_ok = vec ? 1 : 0;
 
   // TMA-store epilogue whenever the outputs are 16-B aligned rows (always for peer stores)
-  EpiMaps maps;
   memset(&maps, 0, sizeof(maps));
   bool tma = false;
   if (npeers) {
@@ -1001,6 +1049,25 @@ static int gemm_impl(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, 
   SMPK_REQUIRE(!colsum_part || (tma && !c_f32 && nb1 == 1 && nb2 == 1 && splits == 1), SMPK_ERR_UNSUPPORTED,
                "smpk_gemm: fused column sums need a bf16, unbatched, unsplit TMA-store output");
 
+  return SMPK_OK;
+}
+
+static int gemm_impl(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, int64_t a_bs2, const void* b,
+                     int b_mn_major, int64_t ldb, int64_t b_bs1, int64_t b_bs2, void* c, int c_f32, int64_t ldc,
+                     int64_t c_bs1, int64_t c_bs2, int M, int N, int K, int nb1, int nb2, float alpha, float beta,
+                     int epilogue, int act, const void* bias, void* aux, int64_t ldaux, void* const* peers_host,
+                     int npeers, int64_t rows_per_owner, int64_t peer_slot_off, void* workspace,
+                     int64_t workspace_bytes, float* colsum_part, void* stream) {
+  CUtensorMap ta, tb;
+  EpiMaps maps;
+  GemmArgs g;
+  int BN;
+  bool pair;
+  int rc = gemm_prepare(a, a_mn_major, lda, a_bs1, a_bs2, b, b_mn_major, ldb, b_bs1, b_bs2, c, c_f32, ldc, c_bs1,
+                        c_bs2, M, N, K, nb1, nb2, alpha, beta, epilogue, act, bias, aux, ldaux, peers_host, npeers,
+                        rows_per_owner, peer_slot_off, workspace, workspace_bytes, colsum_part, false, ta, tb, maps,
+                        g, BN, pair);
+  if (rc) return rc;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   // stage counts: stages_for() (fills the 227 KB of shared memory next to the staging boxes)
   if (BN == 64) return dispatch_epilogue<64, 0, false>(ta, tb, maps, g, st);
@@ -1008,6 +1075,97 @@ static int gemm_impl(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, 
                              : dispatch_epilogue<128, 0, false>(ta, tb, maps, g, st);
   return pair ? dispatch_epilogue<256, 0, true>(ta, tb, maps, g, st)
               : dispatch_epilogue<256, 0, false>(ta, tb, maps, g, st);
+}
+
+template <int EPI, int ACT>
+static int launch_grouped(GroupParams& P, cudaStream_t st) {
+  constexpr int BN = 256;
+  constexpr int STAGES = stages_for(BN, true, epi_warps(EPI));
+  using Cfg = GemmCfg<BN, STAGES, true, epi_warps(EPI)>;
+  static_assert(Cfg::SMEM_BYTES <= 232448, "shared memory budget");
+  auto kern = gemm_bf16_tcgen05_pair_grouped<BN, STAGES, EPI, ACT>;
+  static unsigned long long attr_set = 0;
+  cudaError_t e = smem_attr_once(kern, Cfg::SMEM_BYTES, attr_set);
+  SMPK_REQUIRE(e == cudaSuccess, SMPK_ERR_CUDA, "smpk_gemm_grouped: cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+  const int slots = gemm_sms() / 2;
+  const int units = P.g[0].num_units + P.g[1].num_units;
+  const int grid = 2 * (units < slots ? units : slots);
+  kern<<<grid, gemm_threads(EPI), Cfg::SMEM_BYTES, st>>>(P);
+  return check_launch("smpk_gemm_grouped");
+}
+
+static int desc_impl(const smpk_gemm_desc& d, void* stream) {
+  return gemm_impl(d.a, d.a_mn_major, d.lda, d.a_bs1, d.a_bs2, d.b, d.b_mn_major, d.ldb, d.b_bs1, d.b_bs2, d.c,
+                   d.c_f32, d.ldc, d.c_bs1, d.c_bs2, d.M, d.N, d.K, d.nb1, d.nb2, d.alpha, d.beta, d.epilogue, d.act,
+                   d.bias, d.aux, d.ldaux, nullptr, 0, 0, 0, d.workspace, d.workspace_bytes, d.colsum_part, stream);
+}
+
+static int desc_prepare(const smpk_gemm_desc& d, CUtensorMap& ta, CUtensorMap& tb, EpiMaps& maps, GemmArgs& g,
+                        int& BN, bool& pair) {
+  return gemm_prepare(d.a, d.a_mn_major, d.lda, d.a_bs1, d.a_bs2, d.b, d.b_mn_major, d.ldb, d.b_bs1, d.b_bs2, d.c,
+                      d.c_f32, d.ldc, d.c_bs1, d.c_bs2, d.M, d.N, d.K, d.nb1, d.nb2, d.alpha, d.beta, d.epilogue,
+                      d.act, d.bias, d.aux, d.ldaux, nullptr, 0, 0, 0, nullptr, 0, d.colsum_part, true, ta, tb, maps,
+                      g, BN, pair);
+}
+
+// SMPK_GEMM_GROUP=0 disables grouped launches (A/B: the same GEMMs launched one after the other)
+static bool group_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SMPK_GEMM_GROUP");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+extern "C" int smpk_gemm_grouped(const smpk_gemm_desc* descs, int n, void* stream) {
+  SMPK_REQUIRE(descs && n >= 1, SMPK_ERR_BAD_ARG, "smpk_gemm_grouped: no problems");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (n == 2 && group_enabled()) {
+    // the plain problem (no epilogue, no fused column sums) becomes problem 1
+    int q = -1;
+    for (int i = 1; i >= 0; --i)
+      if (descs[i].epilogue == SMPK_EPI_NONE && !descs[i].colsum_part) q = i;
+    bool ok = q >= 0;
+    GroupParams P;
+    memset(&P, 0, sizeof(P));
+    if (ok) {
+      const smpk_gemm_desc* d[2] = {&descs[1 - q], &descs[q]};
+      for (int i = 0; i < 2 && ok; ++i) {
+        int BN;
+        bool pair;
+        const bool eligible = !d[i]->c_f32 && d[i]->beta == 0.f && d[i]->alpha == 1.f && d[i]->nb1 == 1 &&
+                              d[i]->nb2 == 1;
+        ok = eligible &&
+             desc_prepare(*d[i], P.ta[i], P.tb[i], P.maps[i], P.g[i], BN, pair) == SMPK_OK && BN == 256 && pair &&
+             P.g[i].splits == 1 && P.g[i].tma_store;
+      }
+    }
+    // the plain problem's (long, weight-gradient) tiles must fill at least half the CTA pairs;
+    // a small-output wgrad (e.g. the 1024 x 1024 out-projection, 16 tiles) is faster split-K on its own
+    if (ok && 2 * P.g[1].num_units < gemm_sms() / 2) ok = false;
+    if (ok) {
+      const GemmArgs& g0 = P.g[0];
+      switch (g0.epi) {
+        case SMPK_EPI_NONE: return launch_grouped<SMPK_EPI_NONE, 0>(P, st);
+        case SMPK_EPI_ADD: return launch_grouped<SMPK_EPI_ADD, 0>(P, st);
+        case SMPK_EPI_BIAS: return launch_grouped<SMPK_EPI_BIAS, 0>(P, st);
+        case SMPK_EPI_DACT:
+          if (g0.act == SMPK_ACT_GELU_ERF) return launch_grouped<SMPK_EPI_DACT, SMPK_ACT_GELU_ERF>(P, st);
+          if (g0.act == SMPK_ACT_GELU_TANH) return launch_grouped<SMPK_EPI_DACT, SMPK_ACT_GELU_TANH>(P, st);
+          if (g0.act == SMPK_ACT_RELU) return launch_grouped<SMPK_EPI_DACT, SMPK_ACT_RELU>(P, st);
+          break;
+        default:
+          break;
+      }
+    }
+  }
+  // not groupable: the problems one after the other
+  for (int i = 0; i < n; ++i) {
+    const int rc = desc_impl(descs[i], stream);
+    if (rc) return rc;
+  }
+  return SMPK_OK;
 }
 
 extern "C" int smpk_gemm(const void* a, int a_mn_major, int64_t lda, int64_t a_bs1, int64_t a_bs2, const void* b,

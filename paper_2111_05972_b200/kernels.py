@@ -54,12 +54,80 @@ class GemmProfiler:
 
 PROFILER: GemmProfiler | None = None
 
+import ctypes as _C  # noqa: E402
+
+
+class GemmDesc(_C.Structure):
+    """ctypes mirror of smpk_gemm_desc (include/smpk.h)."""
+    _fields_ = [("a", _C.c_void_p), ("a_mn_major", _C.c_int), ("lda", _C.c_int64), ("a_bs1", _C.c_int64),
+                ("a_bs2", _C.c_int64), ("b", _C.c_void_p), ("b_mn_major", _C.c_int), ("ldb", _C.c_int64),
+                ("b_bs1", _C.c_int64), ("b_bs2", _C.c_int64), ("c", _C.c_void_p), ("c_f32", _C.c_int),
+                ("ldc", _C.c_int64), ("c_bs1", _C.c_int64), ("c_bs2", _C.c_int64), ("M", _C.c_int), ("N", _C.c_int),
+                ("K", _C.c_int), ("nb1", _C.c_int), ("nb2", _C.c_int), ("alpha", _C.c_float), ("beta", _C.c_float),
+                ("epilogue", _C.c_int), ("act", _C.c_int), ("bias", _C.c_void_p), ("aux", _C.c_void_p),
+                ("ldaux", _C.c_int64), ("workspace", _C.c_void_p), ("workspace_bytes", _C.c_int64),
+                ("colsum_part", _C.c_void_p)]
+
+
+_GROUP: list | None = None  # GEMMs collected by `grouped()` (descriptor, keep-alive tensors, flops)
+_GROUP_POST: list = []
+
+
+class grouped:
+    """Collect the GEMMs issued inside the with-block and launch them together on exit
+    (smpk_gemm_grouped: two independent products fused into one persistent CTA-pair grid).
+    Work that depends on a collected GEMM's output must be deferred with `after_group`."""
+
+    def __enter__(self):
+        global _GROUP
+        if _GROUP is not None:
+            raise RuntimeError("kernels.grouped() does not nest")
+        _GROUP = []
+        return self
+
+    def __exit__(self, *exc):
+        global _GROUP, _GROUP_POST
+        items, post = _GROUP, _GROUP_POST
+        _GROUP, _GROUP_POST = None, []
+        if exc[0] is not None or not items:
+            return False
+        prof = PROFILER
+        if prof is not None:
+            e0, e1 = prof.event(), prof.event()
+            if e0 is not None:
+                e0.record()
+        arr = (GemmDesc * len(items))(*[it[0] for it in items])
+        _lib.call("smpk_gemm_grouped", _C.cast(arr, _C.c_void_p), len(items), _stream(),
+                  launches=1 if len(items) == 2 else len(items))
+        if prof is not None:
+            if e1 is not None:
+                e1.record()
+            prof.records.append((e0, e1, sum(it[2] for it in items)))
+        for fn in post:
+            fn()
+        return False
+
+
+def after_group(fn) -> None:
+    """Run fn now, or after the enclosing grouped() launch if one is collecting."""
+    if _GROUP is None:
+        fn()
+    else:
+        _GROUP_POST.append(fn)
+
 
 def gemm_raw(a, a_mn, lda, a_bs, b, b_mn, ldb, b_bs, c, ldc, c_bs, M, N, K, nb=(1, 1),
              alpha=1.0, beta=0.0, epi=EPI_NONE, act=0, bias=None, aux=None, ldaux=0, colsum_part=None) -> None:
     """Direct binding of smpk_gemm; strides in elements, batch strides as 2-tuples.
     colsum_part: fp32 [ceil(M/32), N] receiving per-32-row column sums of the output."""
     _check_cuda(a, b, c, bias, aux)
+    if _GROUP is not None:  # collected: launched by grouped.__exit__ (no split-K inside a group)
+        d = GemmDesc(_ptr(a), int(a_mn), int(lda), int(a_bs[0]), int(a_bs[1]), _ptr(b), int(b_mn), int(ldb),
+                     int(b_bs[0]), int(b_bs[1]), _ptr(c), int(c.dtype == torch.float32), int(ldc), int(c_bs[0]),
+                     int(c_bs[1]), int(M), int(N), int(K), int(nb[0]), int(nb[1]), float(alpha), float(beta),
+                     int(epi), int(act), _ptr(bias), _ptr(aux), int(ldaux), None, 0, _ptr(colsum_part))
+        _GROUP.append((d, (a, b, c, bias, aux, colsum_part), 2.0 * M * N * K * nb[0] * nb[1]))
+        return
     prof = PROFILER
     if prof is not None:
         e0, e1 = prof.event(), prof.event()
@@ -158,7 +226,7 @@ def matmul_nn(a: torch.Tensor, b: torch.Tensor, *, out=None, epi=EPI_NONE, act="
              ldaux=(aux.stride(0) if aux is not None else 0), colsum_part=part)
     if want_colsum:
         cs = torch.empty(N, dtype=c.dtype, device=c.device)
-        _lib.call("smpk_colsum_partials", _ptr(part), part.shape[0], N, _ptr(cs), 0, _stream())
+        after_group(lambda: _lib.call("smpk_colsum_partials", _ptr(part), part.shape[0], N, _ptr(cs), 0, _stream()))
         return c, cs
     return c
 

@@ -334,32 +334,44 @@ def _gather_in(x2, m: LayerMeta, ln=None):
     return _gather_rows(h, m), mean, rstd, None
 
 
-def _rs_out(a, w, w_mn: bool, m: LayerMeta, R: int, N: int):
+def _product(a, w, w_mn: bool, out=None, extra=()):
+    """a @ w (w_mn: w given [K, N]) or a @ w^T; `extra` GEMM thunks (independent weight gradients)
+    are launched together with it in one grouped persistent grid (kernels.grouped)."""
+    if not extra:
+        return K.matmul_nn(a, w, out=out) if w_mn else K.linear(a, w, out=out)
+    with K.grouped():
+        for f in extra:
+            f()
+        y = K.matmul_nn(a, w, out=out) if w_mn else K.linear(a, w, out=out)
+    return y
+
+
+def _rs_out(a, w, w_mn: bool, m: LayerMeta, R: int, N: int, extra=()):
     """Row-parallel product combined over the group -> (x, slot kwargs, region).
 
     Peer mode, "pull" (default): every rank writes its full partial product into its own
     symmetric-pool region with a local TMA-store epilogue; after one epoch barrier the consumer
     row kernel reads its rows from all T ranks' regions over NVLink and sums them in ascending
     rank order (the slot kwargs carry the peer table and offset).  "push": the GEMM epilogue
-    stores each output box straight into the owner's slot (smpk_gemm_rs).  Otherwise NCCL."""
+    stores each output box straight into the owner's slot (smpk_gemm_rs).  Otherwise NCCL.
+    extra: independent GEMM thunks fused into the same launch (backward weight gradients)."""
     if _peer(m, R):
         pool = get_pool()
         T = m.tp_size
         if STATE.config.get("tp_rs", "pull") == "pull":
             P = pool.scratch("rs_out", T * R * N * 2)
             out = pool.view(P, (T * R, N))
-            if w_mn:
-                K.matmul_nn(a, w, out=out)
-            else:
-                K.linear(a, w, out=out)
+            _product(a, w, w_mn, out=out, extra=extra)
             pool.barrier()
             return out, dict(nslots=T, x_peers=pool.base_table, x_peer_off=P // 2 + pool.me * R * N), None
+        for f in extra:
+            f()
         P = pool.scratch("partials", T * R * N * 2)
         peers, off = pool.host_peers(P, pool.me * R * N)
         K.gemm_rs(a, w, w_mn, peers, ldc=N, rows_per_owner=R, slot_off=off)
         pool.barrier()
         return pool.view(P, (T * R, N)), dict(nslots=T, slot_stride=R * N), None
-    y = K.matmul_nn(a, w) if w_mn else K.linear(a, w)
+    y = _product(a, w, w_mn, extra=extra)
     return _combine_rows(y, m), {}, None
 
 
@@ -483,20 +495,28 @@ class AttentionFn(torch.autograd.Function):
         if dbo is None:
             dbo = ops.colsum(dof)  # over all rows of the group: complete on every rank
         ov = _overlap_sms(m) > 0 and not (m.tp_size == 1 and not m.pre_ln)
-        dwo = torch.empty_like(wo) if ov else K.matmul_tn(dof, ctxv)
-        dctx = K.matmul_nn(dof, wo)
+        dwo = torch.empty_like(wo)
+        if ov:
+            dctx = K.matmul_nn(dof, wo)
+        else:  # dWo and dctx read the same dof: one grouped launch
+            with K.grouped():
+                K.matmul_tn(dof, ctxv, out=dwo)
+                dctx = K.matmul_nn(dof, wo)
         if ctx.fused:
             dqkv = ops.flash_attn_bwd(dctx, qkv, ctxv, P, B, s, m.heads_local, m.head_dim, mask_add=mask_add,
                                       causal=m.causal, p=m.p_attn, keep_bits=Pd if m.p_attn > 0 else None)
         else:
             dqkv = attn_core_bwd(dctx, qkv, P, Pd, B, s, m)
-        dwqkv = torch.empty_like(wqkv) if ov else K.matmul_tn(dqkv, hf)
+        dwqkv = torch.empty_like(wqkv)
+        wq_thunk = (lambda: K.matmul_tn(dqkv, hf, out=dwqkv))
         dbqkv = ops.colsum(dqkv)
         if m.tp_size == 1 and not m.pre_ln:
-            dx = K.matmul_nn(dqkv, wqkv, epi=K.EPI_ADD, aux=dr)
+            with K.grouped():  # dWqkv and dx read the same dqkv
+                wq_thunk()
+                dx = K.matmul_nn(dqkv, wqkv, epi=K.EPI_ADD, aux=dr)
             dpre_w = dpre_b = None
         else:
-            dhx, skw, PR = _rs_out(dqkv, wqkv, True, m, R, H)
+            dhx, skw, PR = _rs_out(dqkv, wqkv, True, m, R, H, extra=() if ov else (wq_thunk,))
             join, rsm = (lambda: None), 0
             if ov:  # weight gradients on the side stream, next to the reduce-scatter consumer
                 join, rsm = _wgrad_async(m, [lambda: K.matmul_tn(dof, ctxv, out=dwo),
@@ -557,14 +577,22 @@ class MlpFn(torch.autograd.Function):
         if db2 is None:
             db2 = ops.colsum(dgf)
         ov = _overlap_sms(m) > 0 and not (m.tp_size == 1 and not m.pre_ln)
-        dw2 = torch.empty_like(w2) if ov else K.matmul_tn(dgf, f)
-        dz, db1 = K.matmul_nn(dgf, w2, epi=K.EPI_DACT, act=m.activation, aux=z, want_colsum=True)
-        dw1 = torch.empty_like(w1) if ov else K.matmul_tn(dz, hf)
+        dw2 = torch.empty_like(w2)
+        if ov:
+            dz, db1 = K.matmul_nn(dgf, w2, epi=K.EPI_DACT, act=m.activation, aux=z, want_colsum=True)
+        else:  # dW2 and dz read the same dgf: one grouped launch (dz's dGeLU epilogue behind dW2's tiles)
+            with K.grouped():
+                K.matmul_tn(dgf, f, out=dw2)
+                dz, db1 = K.matmul_nn(dgf, w2, epi=K.EPI_DACT, act=m.activation, aux=z, want_colsum=True)
+        dw1 = torch.empty_like(w1)
+        w1_thunk = (lambda: K.matmul_tn(dz, hf, out=dw1))
         if m.tp_size == 1 and not m.pre_ln:
-            dx = K.matmul_nn(dz, w1, epi=K.EPI_ADD, aux=dr)
+            with K.grouped():  # dW1 and dx read the same dz
+                w1_thunk()
+                dx = K.matmul_nn(dz, w1, epi=K.EPI_ADD, aux=dr)
             dpre_w = dpre_b = None
         else:
-            dhx, skw, PR = _rs_out(dz, w1, True, m, R, H)
+            dhx, skw, PR = _rs_out(dz, w1, True, m, R, H, extra=() if ov else (w1_thunk,))
             join, rsm = (lambda: None), 0
             if ov:  # weight gradients on the side stream, next to the reduce-scatter consumer
                 join, rsm = _wgrad_async(m, [lambda: K.matmul_tn(dgf, f, out=dw2),

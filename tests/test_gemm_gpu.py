@@ -125,3 +125,47 @@ def test_batched_strided(K):
                      s, s, dh, nb=(nh, B), alpha=0.125)
     ref = (q.float() @ k.float().transpose(-1, -2)) * 0.125
     assert rel(c.float(), ref) < TOL
+
+
+@pytest.mark.parametrize("epi", ["none", "add", "dact"])
+def test_grouped_pair_matches_reference(epi):
+    """smpk_gemm_grouped: a weight-gradient GEMM (plain) fused with an input-gradient GEMM (plain /
+    residual add / dGeLU + fused column sums) in one persistent grid == torch fp32 references, and
+    bit-identical run to run."""
+    from paper_2111_05972_b200 import kernels as K
+    g = torch.Generator().manual_seed(11)
+    T_, H, I = 2048, 512, 1024
+    dy = (torch.randn(T_, I, generator=g) * 0.1).bfloat16().cuda()
+    x = (torch.randn(T_, H, generator=g) * 0.1).bfloat16().cuda()
+    w = (torch.randn(I, H, generator=g) * 0.1).bfloat16().cuda()  # forward weight [out, in]
+    aux = (torch.randn(T_, H, generator=g)).bfloat16().cuda()
+
+    def run():
+        dw = torch.empty(I, H, dtype=torch.bfloat16, device="cuda")
+        with K.grouped():
+            K.matmul_tn(dy, x, out=dw)
+            if epi == "none":
+                dx = K.matmul_nn(dy, w)
+                cs = None
+            elif epi == "add":
+                dx = K.matmul_nn(dy, w, epi=K.EPI_ADD, aux=aux)
+                cs = None
+            else:
+                dx, cs = K.matmul_nn(dy, w, epi=K.EPI_DACT, act="gelu", aux=aux, want_colsum=True)
+        torch.cuda.synchronize()
+        return dw, dx, cs
+
+    dw, dx, cs = run()
+    dw_ref = dy.float().t() @ x.float()
+    dx_ref = dy.float() @ w.float()
+    if epi == "add":
+        dx_ref = dx_ref + aux.float()
+    elif epi == "dact":
+        z = aux.float()
+        dx_ref = dx_ref * (0.5 * (1 + torch.erf(z / 2 ** 0.5)) + z * torch.exp(-0.5 * z * z) / (2 * torch.pi) ** 0.5)
+    rel_ = lambda a, b: ((a.float() - b).norm() / b.norm()).item()  # noqa: E731
+    assert rel_(dw, dw_ref) < 1e-2 and rel_(dx, dx_ref) < 1e-2
+    if cs is not None:
+        assert rel_(cs, dx.float().sum(0)) < 1e-2
+    dw2, dx2, cs2 = run()
+    assert torch.equal(dw, dw2) and torch.equal(dx, dx2)
