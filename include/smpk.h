@@ -424,6 +424,7 @@ SMPK_API int smpk_adam_step(float* master, void* param_bf16, const float* grad, 
  * SMPK_FA_TRACE=1 in the environment (20 u64 per CTA; see csrc/flash_attn.cu).  Diagnostics only. */
 SMPK_API int smpk_debug_fa_trace(void* host_out, int n_cta);
 SMPK_API int smpk_debug_fb_trace(void* host_out, int n_cta); /* backward: 32 u64 per CTA */
+SMPK_API int smpk_debug_gemm_trace(void* host_out, int n_cta); /* GEMM (SMPK_GEMM_TRACE=1): 40 u64 per CTA */
 
 #ifdef __cplusplus
 }

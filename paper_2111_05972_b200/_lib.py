@@ -56,6 +56,7 @@ SIGNATURES: dict[str, list] = {
     "smpk_adam_step": [P, P, P, P, P, L, F, F, F, F, F, I, F, P],
     "smpk_debug_fa_trace": [P, I],
     "smpk_debug_fb_trace": [P, I],
+    "smpk_debug_gemm_trace": [P, I],
     "smpk_ln_bwd_ex": [P, I, L, P, P, P, P, P, P, P, P, I, L, P, P, P, I, I, I, I, F, C.c_uint64, P, I, I, L, P, P, L, P,
                        L, P],
     "smpk_symm_export": [P, P, C.POINTER(L)],

@@ -65,7 +65,17 @@ struct GemmArgs {
   // fused bias-gradient column sums (TMA-store path): colsum_part[row / 32][col] = sum of the 32
   // stored bf16 rows of each output box (ceil(M/32) partial rows, reduced afterwards in order)
   float* colsum_part;
+  unsigned long long* trace;  // debug timeline (SMPK_GEMM_TRACE=1), else null
 };
+
+// debug: per CTA 40 u64: [0] start, per unit k < 8: [1+4k] main loop start (MMA warp), [2+4k] last
+// k-block issued, [3+4k] accumulator ready (epilogue warp 4), [4+4k] epilogue done (warp 4)
+__device__ unsigned long long g_gemm_trace[2048 * 40];
+__device__ __forceinline__ unsigned long long gtime_g() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // TMA store descriptors: C, the pre-activation (BIAS_ACT) and, for the reduce-scatter
 // epilogue, one descriptor per owning rank's peer-mapped partial slot.
@@ -327,6 +337,9 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA_arr, const CUte
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  unsigned long long* trc = (gs[0].trace && blockIdx.x < 2048) ? gs[0].trace + blockIdx.x * 40 : nullptr;
+  if (trc && threadIdx.x == 0) trc[0] = gtime_g();
+  int tk = 0;  // per-CTA unit counter (trace)
 
   if (warp == 0) {
     if (lane == 0) {
@@ -412,6 +425,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA_arr, const CUte
         int tile, kb0, kb1;
         decode_unit(g, u, tile, kb0, kb1);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        if (trc && lane == 0 && tk < 8) trc[1 + 4 * tk] = gtime_g();
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -441,6 +455,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA_arr, const CUte
           else umma_commit(&tfull_bar[acc]);
         }
         __syncwarp();
+        if (trc && lane == 0 && tk < 8) trc[2 + 4 * tk] = gtime_g();
+        ++tk;
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -495,6 +511,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA_arr, const CUte
         if constexpr (AUXPF) aux_load(0);
 
         mbar_wait(&tfull_bar[acc], acc_phase);
+        if (trc && warp == 4 && lane == 0 && tk < 8) trc[3 + 4 * tk] = gtime_g();
         tc_fence_after();
         const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16);
         if (g.splits == 1) {
@@ -646,6 +663,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA_arr, const CUte
       };
       if (NPROB == 2 && p == 1) tile_epi(std::integral_constant<int, SMPK_EPI_NONE>{});
       else tile_epi(std::integral_constant<int, EPI>{});
+      if (trc && warp == 4 && lane == 0 && tk < 8) trc[4 + 4 * tk] = gtime_g();
+      ++tk;
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -1046,6 +1065,16 @@ static int gemm_prepare(const void* a, int a_mn_major, int64_t lda, int64_t a_bs
   }
   g.tma_store = tma ? 1 : 0;
   g.colsum_part = colsum_part;
+  {
+    static int tr = -1;
+    static unsigned long long* tp = nullptr;
+    if (tr < 0) {
+      const char* e = getenv("SMPK_GEMM_TRACE");
+      tr = (e && e[0] == '1') ? 1 : 0;
+      if (tr) cudaGetSymbolAddress(reinterpret_cast<void**>(&tp), g_gemm_trace);
+    }
+    g.trace = tr ? tp : nullptr;
+  }
   SMPK_REQUIRE(!colsum_part || (tma && !c_f32 && nb1 == 1 && nb2 == 1 && splits == 1), SMPK_ERR_UNSUPPORTED,
                "smpk_gemm: fused column sums need a bf16, unbatched, unsplit TMA-store output");
 
@@ -1212,4 +1241,11 @@ extern "C" int smpk_gemm_rs(const void* a, int a_mn_major, int64_t lda, const vo
   return gemm_impl(a, a_mn_major, lda, 0, 0, b, b_mn_major, ldb, 0, 0, nullptr, 0, ldc, 0, 0, M, N, K, 1, 1, 1.f,
                    0.f, SMPK_EPI_NONE, 0, nullptr, nullptr, 0, peers, npeers, rows_per_owner, peer_slot_off, nullptr,
                    0, nullptr, stream);
+}
+
+extern "C" int smpk_debug_gemm_trace(void* host_out, int n_cta) {
+  if (n_cta > 2048) n_cta = 2048;
+  cudaError_t e = cudaMemcpyFromSymbol(host_out, smpk::g_gemm_trace, (size_t)n_cta * 40 * 8);
+  SMPK_REQUIRE(e == cudaSuccess, SMPK_ERR_CUDA, "smpk_debug_gemm_trace: %s", cudaGetErrorString(e));
+  return SMPK_OK;
 }

@@ -3,18 +3,20 @@ import ctypes
 import os
 import sys
 
-os.environ["SMPK_FA_TRACE"] = "1"
+os.environ.setdefault("SMPK_FA_TRACE", "1")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 
 from paper_2111_05972_b200 import _lib, ops
 
-B, nh, s, dh = 8, 16, 512, 64
+a = sys.argv[1:]
+B, nh, s, dh = (int(v) for v in (a[:4] if a else (8, 16, 512, 64)))
+causal = bool(int(a[4])) if len(a) > 4 else False
 qkv = torch.randn(B * s, 3 * nh * dh, device="cuda").bfloat16()
 bits = ops.attn_dropout_bits(B, nh, s, s, p=0.1, seed=1)
 for _ in range(5):
-    ops.flash_attn_fwd(qkv, B, s, nh, dh, p=0.1, keep_bits=bits)
+    ops.flash_attn_fwd(qkv, B, s, nh, dh, p=0.1, keep_bits=bits, causal=causal)
 torch.cuda.synchronize()
 n = (s // 256) * nh * B
 buf = np.zeros(n * 20, dtype=np.uint64)
