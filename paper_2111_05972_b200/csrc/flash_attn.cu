@@ -44,9 +44,13 @@ struct FaFwdArgs {
   int trace;
 };
 
-template <int DH, int NS_ = (DH == 64 ? 3 : 1)>
+// K and V stream through separate rings: K_{j+1} only has to wait for both tiles' S_j, V_{j+1}
+// for both tiles' P_j.V_j -- at dh = 128 (no room for two full K/V stages next to P) K is double
+// buffered and V single buffered, so the next K load overlaps the current tile's softmax.
+template <int DH, int NS_ = (DH == 64 ? 3 : 2), int NSV_ = (DH == 64 ? 3 : 1)>
 struct FaFwdCfg {
-  static constexpr int NS = NS_;  // K/V ring depth
+  static constexpr int NS = NS_;    // K ring depth
+  static constexpr int NSV = NSV_;  // V ring depth
   static constexpr int Q_BYTES = FA_BQ * DH * 2;
   static constexpr int K_BYTES = FA_BK * DH * 2;
   static constexpr int V_BYTES = FA_BK * DH * 2;
@@ -54,7 +58,7 @@ struct FaFwdCfg {
   static constexpr int OFF_Q = 0;                          // Q0, Q1
   static constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
   static constexpr int OFF_V = OFF_K + NS * K_BYTES;
-  static constexpr int OFF_P = OFF_V + NS * V_BYTES;       // P0, P1
+  static constexpr int OFF_P = OFF_V + NSV * V_BYTES;      // P0, P1
   static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
   static constexpr int SMEM = 1024 + OFF_BAR + 256;
   static constexpr uint32_t TMEM_COLS = 512;  // S0 [0,128) S1 [128,256) O0 [256,256+DH) O1 [256+DH, 256+2DH)
@@ -69,26 +73,29 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 
-template <int DH, int NS_>
+template <int DH, int NS_, int NSV_>
 __global__ void __launch_bounds__(FA_THREADS, 1)
     flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const FaFwdArgs a) {
-  using Cfg = FaFwdCfg<DH, NS_>;
+  using Cfg = FaFwdCfg<DH, NS_, NSV_>;
+  constexpr int NSV = Cfg::NSV;
   constexpr int NS = Cfg::NS;
   extern __shared__ uint8_t smem_raw[];
   // pointer arithmetic on the __shared__ array (not an integer round trip) keeps the shared
   // address space visible to the compiler: LDS / STS instead of generic LD / ST
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
-  static_assert(NS <= 4, "K/V ring depth");
+  static_assert(NS <= 4 && NSV <= 4, "K/V ring depth");
   uint64_t* q_full = bar + 0;
-  uint64_t* kv_full = bar + 1;        // [NS]
+  uint64_t* kv_full = bar + 1;        // [NS]  K ring
   uint64_t* kv_empty = bar + 5;       // [NS]
-  uint64_t* s_full = bar + 9;         // [2]
-  uint64_t* p_full = bar + 11;        // [2]
-  uint64_t* o_done = bar + 13;        // [2]
-  uint64_t* s_read = bar + 15;        // [2] softmax group t has loaded S_t into registers
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
+  uint64_t* v_full = bar + 9;         // [NSV] V ring
+  uint64_t* v_empty = bar + 13;       // [NSV]
+  uint64_t* s_full = bar + 17;        // [2]
+  uint64_t* p_full = bar + 19;        // [2]
+  uint64_t* o_done = bar + 21;        // [2]
+  uint64_t* s_read = bar + 23;        // [2] softmax group t has loaded S_t into registers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 25);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_qt = a.s / FA_BQ;
@@ -109,6 +116,10 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     for (int i = 0; i < NS; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < NSV; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1);
@@ -134,7 +145,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer ----------------
+      // ---------------- TMA producer: Q, then the K ring ----------------
       mbar_arrive_expect_tx(q_full, nq * Cfg::Q_BYTES);
       for (int t = 0; t < nq; ++t)
 #pragma unroll
@@ -144,18 +155,25 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       for (int j = 0; j < n_iter; ++j) {
         const int st = j % NS;
         mbar_wait(&kv_empty[st], ((j / NS) & 1) ^ 1);
-        mbar_arrive_expect_tx(&kv_full[st], Cfg::K_BYTES + Cfg::V_BYTES);
+        mbar_arrive_expect_tx(&kv_full[st], Cfg::K_BYTES);
         uint8_t* k_dst = smem + Cfg::OFF_K + st * Cfg::K_BYTES;
-        uint8_t* v_dst = smem + Cfg::OFF_V + st * Cfg::V_BYTES;
 #pragma unroll
         for (int kb = 0; kb < DH / 64; ++kb)
           tma_load_4d(k_dst + kb * (FA_BK * 128), &tmK, &kv_full[st], kb * 64, j * FA_BK, h, b);
+      }
+    } else if (lane == 1) {
+      // ---------------- TMA producer: the V ring ----------------
+      for (int j = 0; j < n_iter; ++j) {
+        const int st = j % NSV;
+        mbar_wait(&v_empty[st], ((j / NSV) & 1) ^ 1);
+        mbar_arrive_expect_tx(&v_full[st], Cfg::V_BYTES);
+        uint8_t* v_dst = smem + Cfg::OFF_V + st * Cfg::V_BYTES;
         // V as the MN-major B operand of P.V: [64-key block][64-wide d chunk][64 keys x 128 B]
 #pragma unroll
         for (int kb = 0; kb < FA_BK / 64; ++kb)
 #pragma unroll
           for (int c = 0; c < DH / 64; ++c)
-            tma_load_4d(v_dst + (kb * (DH / 64) + c) * 8192, &tmV, &kv_full[st], c * 64, j * FA_BK + kb * 64, h, b);
+            tma_load_4d(v_dst + (kb * (DH / 64) + c) * 8192, &tmV, &v_full[st], c * 64, j * FA_BK + kb * 64, h, b);
       }
     }
   } else if (warp == 1) {
@@ -183,8 +201,8 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       }
       __syncwarp();
     };
-    auto issue_pv = [&](int t, int j) {  // O_t += P_t V_j (caller checked p_full)
-      const int st = j % NS;
+    auto issue_pv = [&](int t, int j) {  // O_t += P_t V_j (caller checked p_full and v_full)
+      const int st = j % NSV;
       tc_fence_after();
       const uint32_t pb = p_base + t * Cfg::P_BYTES;
       const uint32_t vbase = smem_u32(smem + Cfg::OFF_V + st * Cfg::V_BYTES);
@@ -204,8 +222,8 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     if (trc && lane == 0) trc[1] = gtime();
     const int nkt[2] = {nkt0, nkt1};
     int s_next[2] = {0, 0}, pv_next[2] = {0, 0};
-    int rel = 0;  // next K/V iteration whose ring stage has not been released
-    while (rel < n_iter) {
+    int relk = 0, relv = 0;  // next iterations whose K / V ring stage has not been released
+    while (relv < n_iter) {
       bool progress = false;
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
@@ -218,18 +236,24 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           progress = true;
         }
         const int kp = pv_next[t];
-        if (kp < s_next[t] && mbar_test(&p_full[t], kp & 1)) {
+        if (kp < s_next[t] && mbar_test(&p_full[t], kp & 1) && mbar_test(&v_full[kp % NSV], (kp / NSV) & 1)) {
           issue_pv(t, kp);
           pv_next[t] = kp + 1;
           progress = true;
         }
       }
-      // K/V stage of iteration `rel` is free once every query tile that uses it issued its P.V
-      // (the commit tracks all MMAs issued before it, including the S that read K_rel)
-      while (rel < n_iter && (rel >= nkt0 || pv_next[0] > rel) && (rel >= nkt1 || pv_next[1] > rel)) {
-        if (elect_one()) umma_commit(&kv_empty[rel % NS]);
+      // K of iteration relk is free once every query tile using it issued its S; V once P.V
+      // (a commit tracks all MMAs issued before it)
+      while (relk < n_iter && (relk >= nkt0 || s_next[0] > relk) && (relk >= nkt1 || s_next[1] > relk)) {
+        if (elect_one()) umma_commit(&kv_empty[relk % NS]);
         __syncwarp();
-        ++rel;
+        ++relk;
+        progress = true;
+      }
+      while (relv < n_iter && (relv >= nkt0 || pv_next[0] > relv) && (relv >= nkt1 || pv_next[1] > relv)) {
+        if (elect_one()) umma_commit(&v_empty[relv % NSV]);
+        __syncwarp();
+        ++relv;
         progress = true;
       }
       if (!progress) __nanosleep(20);
@@ -459,30 +483,22 @@ extern "C" int smpk_flash_attn_fwd(const void* qkv, int64_t ld, int B, int nh, i
   a.scale_log2 = scale * 1.4426950408889634f;
   a.causal = causal;
   a.inv_keep = p_drop > 0.f ? 1.f / (1.f - p_drop) : 1.f;
-  static int trace_env = -1, ns_env = -1;
+  static int trace_env = -1;
   if (trace_env < 0) {
     const char* e = getenv("SMPK_FA_TRACE");
     trace_env = (e && e[0] == '1') ? 1 : 0;
-    const char* n = getenv("SMPK_FA_NS");
-    ns_env = n ? atoi(n) : 0;
   }
   a.trace = trace_env;
   dim3 grid((s / 128 + 1) / 2, nh, B);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (dh == 64) {
-    if (ns_env == 2) {
-      static unsigned long long once = 0;
-      smem_attr_once(flash_fwd_kernel<64, 2>, FaFwdCfg<64, 2>::SMEM, once);
-      flash_fwd_kernel<64, 2><<<grid, FA_THREADS, FaFwdCfg<64, 2>::SMEM, st>>>(tq, tk, tv, a);
-    } else {
-      static unsigned long long once = 0;
-      smem_attr_once(flash_fwd_kernel<64, 3>, FaFwdCfg<64, 3>::SMEM, once);
-      flash_fwd_kernel<64, 3><<<grid, FA_THREADS, FaFwdCfg<64, 3>::SMEM, st>>>(tq, tk, tv, a);
-    }
+    static unsigned long long once = 0;
+    smem_attr_once(flash_fwd_kernel<64, 3, 3>, FaFwdCfg<64, 3, 3>::SMEM, once);
+    flash_fwd_kernel<64, 3, 3><<<grid, FA_THREADS, FaFwdCfg<64, 3, 3>::SMEM, st>>>(tq, tk, tv, a);
   } else {
     static unsigned long long once = 0;
-    smem_attr_once(flash_fwd_kernel<128, 1>, FaFwdCfg<128, 1>::SMEM, once);
-    flash_fwd_kernel<128, 1><<<grid, FA_THREADS, FaFwdCfg<128, 1>::SMEM, st>>>(tq, tk, tv, a);
+    smem_attr_once(flash_fwd_kernel<128, 2, 1>, FaFwdCfg<128, 2, 1>::SMEM, once);
+    flash_fwd_kernel<128, 2, 1><<<grid, FA_THREADS, FaFwdCfg<128, 2, 1>::SMEM, st>>>(tq, tk, tv, a);
   }
   return check_launch("smpk_flash_attn_fwd");
 }
