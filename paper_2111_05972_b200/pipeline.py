@@ -14,6 +14,11 @@
 * ``static_schedule`` turns the scheduler decisions into per-stage op lists for a
   chain of P stages (record-and-replay "static mode"), which
   ``PipelineEngine`` executes SPMD (one process per GPU).
+* ``check_decision_log`` replays ``next_action`` over a recorded decision log in the reference
+  runtime's format {t, ready_backwards, action} (pipeline.py:520-524) and raises
+  ``StaticModeViolation`` at the first decision the scheduler would not have taken;
+  ``static_schedule(..., replay=log)`` / ``PipelineEngine(..., decision_log=log)`` execute such a
+  log's action sequence verbatim (e.g. one recorded by the reference's ``run_step``).
 
 PROVENANCE: the scheduler section (SchedulePolicy, SchedulerState, ready_backwards, next_action) and
 the routing section (D2DBuffers, route) are vendored from the reference (mpsim pipeline.py:96-165,
@@ -35,6 +40,10 @@ FWD = "forward"
 BWD = "backward"
 MPI = "MPI"
 D2D = "D2D"
+
+
+class StaticModeViolation(RuntimeError):
+    """A replayed schedule diverges from what the scheduler decides (pipeline.py:44, :225-246)."""
 
 
 # ---------------------------------------------------------------------------
@@ -87,15 +96,50 @@ def next_action(policy: SchedulePolicy, state: SchedulerState):
     return None
 
 
-def static_schedule(policy: SchedulePolicy, stages: int, fwd_cost: float = 1.0, bwd_cost: float = 2.0):
+def check_decision_log(policy: SchedulePolicy, log: list) -> list:
+    """Replay next_action over a recorded decision log (entries {t, ready_backwards, action},
+    the reference runtime's format, pipeline.py:520-524).  The scheduler state before entry i
+    is rebuilt from the log itself: issued forwards = the forward actions before i, issued
+    backwards = the backward actions before i, completed forwards = ready_backwards(i) plus the
+    issued backwards (a backward is only ever issued after its forward completed).  Raises
+    StaticModeViolation at the first entry whose action differs from next_action on that state,
+    or whose ready set contradicts the issued actions.  Returns the action sequence."""
+    M = policy.microbatches
+    issued_fwd, issued_bwd, acts = 0, set(), []
+    for i, e in enumerate(log):
+        ready = [int(m) for m in e["ready_backwards"]]
+        if any(m in issued_bwd or m >= issued_fwd for m in ready) or ready != sorted(set(ready)):
+            raise StaticModeViolation(f"decision {i}: ready_backwards {ready} inconsistent with the issued actions "
+                                      f"(forwards issued {issued_fwd}, backwards issued {sorted(issued_bwd)})")
+        st = SchedulerState(M, issued_fwd, set(ready) | issued_bwd, set(issued_bwd), 0)
+        want = next_action(policy, st)
+        got = (int(e["action"][0]), str(e["action"][1]))
+        if want is None or tuple(want) != got:
+            raise StaticModeViolation(f"decision {i} at t={e.get('t')}: log has {got}, the scheduler decides {want} "
+                                      f"(ready_backwards {ready})")
+        if got[1] == FWD:
+            issued_fwd += 1
+        else:
+            issued_bwd.add(got[0])
+        acts.append(got)
+    return acts
+
+
+def static_schedule(policy: SchedulePolicy, stages: int, fwd_cost: float = 1.0, bwd_cost: float = 2.0,
+                    replay: list | None = None):
     """Record the scheduler's decisions on a P-stage chain and return per-stage op lists.
 
     Event model: a forward of microbatch m visits stages 0..P-1 (each busy fwd_cost),
     a backward visits P-1..0 (bwd_cost); stages execute their queue FIFO, one op at a
     time.  pp_rank 0 consults next_action whenever it is idle, exactly like the module
     server (pipeline.py:486-530).  Returns (decision_log, ops) with ops[stage] the ordered
-    list of (microbatch, direction) that stage executes."""
+    list of (microbatch, direction) that stage executes.
+
+    replay: a decision log (checked with check_decision_log) whose action sequence rank 0
+    issues verbatim instead of consulting next_action -- each action as soon as rank 0 is idle
+    and, for a backward, its forward has completed in the model."""
     P, M = stages, policy.microbatches
+    script = check_decision_log(policy, replay) if replay is not None else None
     st = SchedulerState(M)
     busy_until = [0.0] * P
     queues = [[] for _ in range(P)]  # (ready_time, seq, mb, dir)
@@ -105,10 +149,15 @@ def static_schedule(policy: SchedulePolicy, stages: int, fwd_cost: float = 1.0, 
     seq = 0
     t = 0.0
     done_bwd = 0
-    while done_bwd < M or (policy.forward_only and len(st.completed_fwd) < M):
+    while (done_bwd < M or (policy.forward_only and len(st.completed_fwd) < M)) and \
+            (script is None or len(log) < len(script) or events or any(queues)):
         # rank 0 consults the scheduler when idle and nothing is queued for it
         if busy_until[0] <= t and not queues[0]:
-            act = next_action(policy, st)
+            if script is None:
+                act = next_action(policy, st)
+            else:
+                nxt = script[len(log)] if len(log) < len(script) else None
+                act = nxt if nxt is not None and (nxt[1] == FWD or nxt[0] in st.completed_fwd) else None
             if act is not None:
                 log.append({"t": t, "ready_backwards": ready_backwards(st), "action": list(act)})
                 mb, d = act
@@ -148,6 +197,11 @@ def static_schedule(policy: SchedulePolicy, stages: int, fwd_cost: float = 1.0, 
             else:
                 done_bwd += 1
                 st.completed_bwd += 1
+    if script is not None and len(log) < len(script):
+        raise StaticModeViolation(f"replayed log: action {len(log)} {script[len(log)]} never became issuable")
+    if done_bwd < M and not (policy.forward_only and len(st.completed_fwd) == M):
+        raise StaticModeViolation(f"replayed log ends after {len(log)} actions with {M - done_bwd} microbatches "
+                                  "unfinished")
     return log, ops
 
 
@@ -310,7 +364,9 @@ class PipelineEngine:
     stage_module: this rank's module (a callable on [mb, s, H] activations); the first
     stage receives its microbatch inputs, the last stage applies ``loss_fn``.  Activations
     go forward and gradients backward over D2D StageChannels; the per-stage op order is
-    the recorded schedule of ``next_action`` (static_schedule).
+    the recorded schedule of ``next_action`` (static_schedule), or -- with ``decision_log`` --
+    the verbatim replay of a recorded log's actions (checked against next_action first).
+    ``self.log`` is this engine's decision log in the reference format.
 
     Transport (PAPER.md:337-350 D2D backend): every send and receive runs on a dedicated
     send / receive stream, ordered against the compute stream by CUDA events -- a send starts
@@ -319,11 +375,11 @@ class PipelineEngine:
     this stage computes.  Channels are built from one handle exchange over the PP group."""
 
     def __init__(self, stage_module, *, pp_rank: int, pp_size: int, ranks: list, act_shape, dtype=torch.bfloat16,
-                 policy: SchedulePolicy, slots: int = 4, group=None):
+                 policy: SchedulePolicy, slots: int = 4, group=None, decision_log: list | None = None):
         self.mod, self.s, self.P, self.ranks = stage_module, pp_rank, pp_size, list(ranks)
         self.shape, self.dtype, self.policy = tuple(act_shape), dtype, policy
         nbytes = int(torch.Size(act_shape).numel()) * torch.tensor([], dtype=dtype).element_size()
-        self.log, ops = static_schedule(policy, pp_size)
+        self.log, ops = static_schedule(policy, pp_size, replay=decision_log)
         self.ops = ops[pp_rank]
         self.fwd_in = self.fwd_out = self.bwd_in = self.bwd_out = None
         me = self.ranks[pp_rank]

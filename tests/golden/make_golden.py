@@ -8,7 +8,9 @@ Writes tests/golden/reference_golden.json with
   * segment_children / dhondt_allocate on random cost vectors (mpsim/partition.py);
   * partition_tree assignments + loads on random module trees (model_graph + partition);
   * next_action decision sequences on random scheduler states (mpsim/pipeline.py);
-  * route() decisions for the 32-case table (mpsim/comm.py).
+  * route() decisions for the 32-case table (mpsim/comm.py);
+  * run_step decision logs {t, ready_backwards, action} of pipelined chains (mpsim/pipeline.py:859,
+    consultation rule :486-530, log entry :520-524).
 """
 import itertools
 import json
@@ -122,10 +124,37 @@ def gen_routes():
     return out
 
 
+def gen_run_step_logs():
+    """Decision logs of the reference module-server runtime on P-stage chains of L layers
+    (uniform and random per-layer forward times), both policies, forward-only included."""
+    rng = random.Random(859)
+    out = []
+    for P, M, kind, fo, uniform in itertools.product([1, 2, 3, 4], [1, 2, 3, 4, 6, 8], ["simple", "interleaved"],
+                                                     [False, True], [True, False]):
+        L = 3 * P
+        mods = [{"id": "root", "parent": None, "param_ids": []}]
+        params = []
+        for i in range(L):
+            params.append({"id": f"p{i:02d}", "bytes": 4096})
+            mods.append({"id": f"l{i:02d}", "parent": "root", "param_ids": [f"p{i:02d}"],
+                         "fwd_time": 1.0 if uniform else round(rng.uniform(0.2, 2.0), 3),
+                         "activation_bytes": 1 << 20})
+        spec = model_graph.load_model_spec(json.dumps({"modules": mods, "params": params}))
+        tree = model_graph.build_node_tree(spec)
+        costed = model_graph.compute_costs(tree, spec, 0.0)
+        asg = partition.partition_tree(costed, P)
+        topo = topology.build_topology(P, P, 1, "cluster")
+        tr = pipeline.run_step(asg, costed, topo, comm.ClusterShape(), pipeline.SchedulePolicy(kind, M, fo))
+        out.append({"P": P, "M": M, "kind": kind, "forward_only": fo, "uniform": uniform,
+                    "decision_log": [{"t": d["t"], "ready_backwards": list(d["ready_backwards"]),
+                                      "action": list(d["action"])} for d in tr.decision_log]})
+    return out
+
+
 def main():
     rng = random.Random(20211105)
     data = {"topology": gen_topology(), "segments": gen_segments(rng), "partitions": gen_partitions(rng),
-            "scheduler": gen_scheduler(rng), "routes": gen_routes()}
+            "scheduler": gen_scheduler(rng), "routes": gen_routes(), "run_step_logs": gen_run_step_logs()}
     with open(OUT, "w") as f:
         json.dump(data, f, sort_keys=True)
     print(f"wrote {OUT}: " + ", ".join(f"{k}={len(v)}" for k, v in data.items()))

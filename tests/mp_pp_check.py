@@ -50,7 +50,16 @@ def channel_stress(rank):
     return ok
 
 
-def pp_step(smp, rank, policy_kind):
+def reference_log(kind, M, P=2):
+    """The reference run_step's decision log for a P-stage uniform chain (tests/golden)."""
+    import json
+    gold = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                                       "reference_golden.json")))["run_step_logs"]
+    return [c for c in gold if (c["P"], c["M"], c["kind"], c["forward_only"], c["uniform"]) ==
+            (P, M, kind, False, True)][0]["decision_log"]
+
+
+def pp_step(smp, rank, policy_kind, replay=False):
     from paper_2111_05972_b200.pipeline import PipelineEngine, SchedulePolicy
     smp.init({"tensor_parallel_degree": 1, "pipeline_parallel_degree": 2, "optimize": "speed", "seed": 0})
     L, nh, dh, H, I, s, mb, M = 4, 4, 64, 256, 1024, 128, 2, 4
@@ -67,8 +76,11 @@ def pp_step(smp, rank, policy_kind):
                                           pre_layernorm=True, post_layernorm=False)
     for j, lay in enumerate(stage.seq_layers):
         lay.load_full({k: v.to(torch.bfloat16) for k, v in params[2 * rank + j].items()})
+    ref_log = reference_log(policy_kind, M) if replay else None
     eng = PipelineEngine(stage, pp_rank=rank, pp_size=2, ranks=[0, 1], act_shape=(mb, s, H),
-                         policy=SchedulePolicy(policy_kind, M))
+                         policy=SchedulePolicy(policy_kind, M), decision_log=ref_log)
+    if replay:  # the engine's decisions are the reference runtime's, action for action
+        assert [tuple(e["action"]) for e in eng.log] == [tuple(e["action"]) for e in ref_log]
     inputs = [x.cuda() for x in X] if rank == 0 else None
     tg = [t.cuda() for t in Tg]
     losses = eng.step(inputs, loss_fn=lambda m, y: (y.float() * tg[m].float()).sum())
@@ -99,7 +111,7 @@ def pp_step(smp, rank, policy_kind):
             errs[f"L{l}.fc2"] = rel(merged[l][1], pr[l]["w2"].grad)
         bad = {k: v for k, v in errs.items() if not v < TOL}
         ok = not bad
-        print(f"[pp2_{policy_kind}] {'OK' if ok else 'FAIL'} schedule={[tuple(e['action']) for e in eng.log]} "
+        print(f"[pp2_{policy_kind}{'_replay_reference_log' if replay else ''}] {'OK' if ok else 'FAIL'} schedule={[tuple(e['action']) for e in eng.log]} "
               + " ".join(f"{k}={v:.2e}" for k, v in errs.items()), flush=True)
     flag = torch.tensor([1 if ok else 0], device="cuda")
     dist.broadcast(flag, 0)
@@ -119,6 +131,7 @@ def main():
     res = [bool(res_t.item())]
     res.append(pp_step(smp, rank, "simple"))
     res.append(pp_step(smp, rank, "interleaved"))
+    res.append(pp_step(smp, rank, "interleaved", replay=True))
     dist.barrier()
     dist.destroy_process_group()
     sys.exit(0 if all(res) else 1)

@@ -1,6 +1,7 @@
 """Bit-exact parity of the Python-retained planning pieces against golden vectors produced
 by the reference itself (tests/golden/make_golden.py): topology / rank groups
-(A17), partition assignment (A19), microbatch scheduler decisions (A18) and D2D routing (A16)."""
+(A17), partition assignment (A19), microbatch scheduler decisions (A18, single decisions and the
+reference runtime's whole run_step decision logs) and D2D routing (A16)."""
 import json
 import os
 
@@ -60,6 +61,49 @@ def test_scheduler_decisions_bit_exact():
         st = PL.SchedulerState(c["M"], c["issued_fwd"], set(c["completed_fwd"]), set(c["issued_bwd"]), 0)
         act = PL.next_action(pol, st)
         assert (list(act) if act else None) == c["action"]
+
+
+def test_reference_run_step_decision_logs_bit_exact():
+    """next_action replayed over the reference runtime's own decision logs (run_step on P-stage
+    chains, pipeline.py:486-530 consultation rule, :520-524 log entries): every decision the
+    reference took is the one the restated scheduler takes on the same state."""
+    n = 0
+    for c in GOLD["run_step_logs"]:
+        pol = PL.SchedulePolicy(c["kind"], c["M"], c["forward_only"])
+        acts = PL.check_decision_log(pol, c["decision_log"])
+        assert len(acts) == c["M"] * (1 if c["forward_only"] else 2)
+        n += len(acts)
+    assert n > 1000
+
+
+def test_decision_log_divergence_raises():
+    c = [c for c in GOLD["run_step_logs"] if c["M"] == 4 and c["kind"] == "interleaved" and not c["forward_only"]][0]
+    pol = PL.SchedulePolicy("interleaved", 4)
+    log = [dict(e) for e in c["decision_log"]]
+    i = next(i for i, e in enumerate(log) if e["action"][1] == "backward")
+    bad = log[:i] + [dict(log[i], action=[log[i]["action"][0] + 1, "backward"])] + log[i + 1:]
+    with pytest.raises(PL.StaticModeViolation):
+        PL.check_decision_log(pol, bad)
+    bad = [dict(log[0], ready_backwards=[0])] + log[1:]  # ready before its forward was issued
+    with pytest.raises(PL.StaticModeViolation):
+        PL.check_decision_log(pol, bad)
+    with pytest.raises(PL.StaticModeViolation):  # truncated: microbatches never finish
+        PL.static_schedule(pol, c["P"], replay=log[:-1])
+
+
+def test_static_schedule_replays_reference_log():
+    """The engine's schedule replaying a reference log issues exactly the logged actions, and every
+    stage runs each microbatch's forward before its backward, forwards in issue order."""
+    for c in GOLD["run_step_logs"]:
+        pol = PL.SchedulePolicy(c["kind"], c["M"], c["forward_only"])
+        log, ops = PL.static_schedule(pol, c["P"], replay=c["decision_log"])
+        assert [tuple(e["action"]) for e in log] == [tuple(e["action"]) for e in c["decision_log"]]
+        for st_ops in ops:
+            fw = [m for m, d in st_ops if d == PL.FWD]
+            assert fw == list(range(c["M"]))
+            for m, d in st_ops:
+                if d == PL.BWD:
+                    assert st_ops.index((m, PL.FWD)) < st_ops.index((m, PL.BWD))
 
 
 def test_route_table_bit_exact():  # SPEC AC8: 32 combinations
