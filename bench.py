@@ -312,7 +312,7 @@ def run_gpu(args, rank, world, local):
 
     torch.cuda.set_device(local)
     smp.init({"tensor_parallel_degree": world, "optimize": args.optimize, "seed": 1234, "tp_comm": args.tp_comm,
-              "tp_rs": args.tp_rs,
+              "tp_rs": args.tp_rs, "tp_exchange": args.tp_exchange,
               "tp_overlap_sms": args.tp_overlap_sms if args.tp_overlap_sms >= 0 else (96 if world >= 4 else 0)})
     STATE_OVERLAP["sms"] = smp.state.STATE.config.get("tp_overlap_sms", 0) if world > 1 else 0
     torch.manual_seed(1000 + rank)
@@ -459,6 +459,7 @@ def run_gpu(args, rank, world, local):
                "sample": _cpu_sample_text(args.workload, it, dt) + f"; {cpu_model()}"}
     cfg_line = _config(args.workload, world, args)
     cfg_line["tp_overlap_sms"] = STATE_OVERLAP.get("sms", 0)
+    cfg_line["tp_exchange"] = args.tp_exchange
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -505,6 +506,8 @@ def main():
                     help="smp optimize mode of the TP layers (PAPER.md:763); the headline is speed")
     ap.add_argument("--tp-comm", default="peer", choices=["peer", "nccl"],
                     help="TP collectives: fused NVLink peer stores (default) or NCCL calls")
+    ap.add_argument("--tp-exchange", default="barrier", choices=["chunks", "barrier"],
+                    help="peer exchanges: per-owner chunks over copy-engine mailboxes, or one barrier per exchange")
     ap.add_argument("--tp-rs", default="pull", choices=["pull", "push"],
                     help="peer reduce-scatter: consumer pulls partials over NVLink, or GEMM epilogue pushes")
     ap.add_argument("--tp-overlap-sms", type=int, default=int(os.environ.get("SMPK_TP_OVERLAP_SMS", "-1")),

@@ -376,6 +376,13 @@ SMPK_API int smpk_bias_act_fwd(const void* x, const void* bias, int M, int N, in
 SMPK_API int smpk_act_bwd(const void* dy, const void* pre, int M, int N, int act, void* dx, void* stream);
 /* smpk_copy_async — stream-ordered device-to-device copy (copy engine; dst may be peer-mapped). */
 SMPK_API int smpk_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+
+/* smpk_stream_flag — stream-ordered 32-bit flag word (cuStreamWaitValue32 / cuStreamWriteValue32,
+ * no SM): op 0 waits until *word == value, op 1 writes *word = value after the stream's prior work
+ * (fenced: a preceding copy into a peer slot is visible first).  The mailbox handshake of the
+ * chunked TP exchange (PAPER.md:281 AG/RS of TP-across-DP, split into per-owner chunks so the
+ * copy engines move chunk c while the SMs compute chunk c+1). */
+SMPK_API int smpk_stream_flag(void* word, uint32_t value, int op, void* stream);
 SMPK_API int smpk_symm_export(void* ptr, void* handle_out, int64_t* offset);
 SMPK_API int smpk_symm_barrier(void* const* peer_flags, void* local_flags, int T, int rank, double timeout_s,
                                void* stream);

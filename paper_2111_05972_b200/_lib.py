@@ -50,6 +50,7 @@ SIGNATURES: dict[str, list] = {
     "smpk_bias_act_fwd": [P, P, I, I, I, P, P, P],
     "smpk_act_bwd": [P, P, I, I, I, P, P],
     "smpk_copy_async": [P, P, L, P],
+    "smpk_stream_flag": [P, C.c_uint32, I, P],
     "smpk_rng_next": [P, P, P],
     "smpk_gemm_grouped": [P, I, P],
     "smpk_embed_bwd_sorted": [P, L, P, L, L, L, I, P, L, I, I, L, P, L, P],
@@ -116,7 +117,7 @@ def lib() -> C.CDLL:
 
 
 # kernels launched by each entry point (for bench.py's gpu_launches count)
-LAUNCHES_PER_CALL = {"smpk_copy_async": 0, "smpk_set_sm_limits": 0, "smpk_ln_bwd": 2, "smpk_ln_bwd_ex": 2, "smpk_ln_bwd_dist": 2, "smpk_colsum": 2, "smpk_flash_attn_bwd": 3}
+LAUNCHES_PER_CALL = {"smpk_copy_async": 0, "smpk_stream_flag": 0, "smpk_set_sm_limits": 0, "smpk_ln_bwd": 2, "smpk_ln_bwd_ex": 2, "smpk_ln_bwd_dist": 2, "smpk_colsum": 2, "smpk_flash_attn_bwd": 3}
 launch_count = 0
 
 

@@ -130,3 +130,18 @@ extern "C" int smpk_p2p_recv(void* dst, const void* local_slot, int64_t bytes, c
   SMPK_REQUIRE(r == CUDA_SUCCESS, SMPK_ERR_CUDA, "smpk_p2p_recv: free signal failed (%d)", (int)r);
   return SMPK_OK;
 }
+
+// Stream-ordered flag words for the chunked TP exchanges (tp_exchange="chunks", exchange.py):
+// a 32-bit word in (possibly peer-mapped) device memory is awaited / written by the stream's
+// front end (cuStreamWaitValue32 / cuStreamWriteValue32) -- no SM, capturable in CUDA graphs.
+// op 0: wait *word == value (then the caller resets it); op 1: write *word = value, fenced after
+// the stream's prior work (a copy into a peer slot is visible before its ready word).
+extern "C" int smpk_stream_flag(void* word, uint32_t value, int op, void* stream) {
+  SMPK_REQUIRE(word && (op == 0 || op == 1), SMPK_ERR_BAD_ARG, "smpk_stream_flag: bad arguments");
+  SMPK_REQUIRE(load_stream_mem_ops(), SMPK_ERR_CUDA, "smpk_stream_flag: stream memory ops unavailable");
+  CUstream st = (CUstream) reinterpret_cast<cudaStream_t>(stream);
+  CUresult r = op == 0 ? g_wait(st, (CUdeviceptr)word, value, CU_STREAM_WAIT_VALUE_EQ)
+                       : g_write(st, (CUdeviceptr)word, value, CU_STREAM_WRITE_VALUE_DEFAULT);
+  SMPK_REQUIRE(r == CUDA_SUCCESS, SMPK_ERR_CUDA, "smpk_stream_flag(op %d): driver error %d", op, (int)r);
+  return SMPK_OK;
+}

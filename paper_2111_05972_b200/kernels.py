@@ -210,17 +210,24 @@ def linear(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None, *
 
 
 def matmul_nn(a: torch.Tensor, b: torch.Tensor, *, out=None, epi=EPI_NONE, act="none", aux=None,
-              alpha=1.0, beta=0.0, want_colsum=False):
+              alpha=1.0, beta=0.0, want_colsum=False, colsum_part=None):
     """C = a @ b, a [M,K] row-major, b [K,N] row-major (B operand MN-major). dgrad: dX = dY @ W.
-    want_colsum: also return the column sums of C (bf16 [N]) fused into the epilogue."""
+    want_colsum: also return the column sums of C (bf16 [N]) fused into the epilogue.
+    colsum_part: caller-owned fp32 [colsum_rows(M), N] partials instead (reduced later by the
+    caller with colsum_reduce, e.g. over several row chunks); returns (C, None)."""
     M, K = a.shape
     K2, N = b.shape
     if K != K2:
         raise ShapeMismatchError(f"matmul_nn: inner dims {K} vs {K2}")
     c = out if out is not None else torch.empty(M, N, dtype=a.dtype, device=a.device)
-    part = None
+    part = colsum_part
+    if colsum_part is not None:
+        gemm_raw(a, 0, _rowmajor(a, "a"), (0, 0), b, 1, _rowmajor(b, "b"), (0, 0), c, _rowmajor(c, "out"), (0, 0),
+                 M, N, K, alpha=alpha, beta=beta, epi=epi, act=ACT[act], aux=aux,
+                 ldaux=(aux.stride(0) if aux is not None else 0), colsum_part=part)
+        return c, None
     if want_colsum:
-        part = torch.empty(_lib.size("smpk_gemm_colsum_rows", M), N, dtype=torch.float32, device=a.device)
+        part = torch.empty(colsum_rows(M), N, dtype=torch.float32, device=a.device)
     gemm_raw(a, 0, _rowmajor(a, "a"), (0, 0), b, 1, _rowmajor(b, "b"), (0, 0), c, _rowmajor(c, "out"), (0, 0),
              M, N, K, alpha=alpha, beta=beta, epi=epi, act=ACT[act], aux=aux,
              ldaux=(aux.stride(0) if aux is not None else 0), colsum_part=part)
@@ -229,6 +236,18 @@ def matmul_nn(a: torch.Tensor, b: torch.Tensor, *, out=None, epi=EPI_NONE, act="
         after_group(lambda: _lib.call("smpk_colsum_partials", _ptr(part), part.shape[0], N, _ptr(cs), 0, _stream()))
         return c, cs
     return c
+
+
+def colsum_rows(M: int) -> int:
+    """Rows of the fp32 column-sum partials a fused-colsum GEMM with M rows writes."""
+    return _lib.size("smpk_gemm_colsum_rows", int(M))
+
+
+def colsum_reduce(part: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+    """Fixed-order reduction of fused-colsum partials [rows, N] (fp32) into out [N]."""
+    _lib.call("smpk_colsum_partials", _ptr(part), part.shape[0], part.shape[1], _ptr(out),
+              int(out.dtype == torch.float32), _stream())
+    return out
 
 
 def matmul_tn(a: torch.Tensor, b: torch.Tensor, *, out=None, alpha=1.0, beta=0.0,

@@ -26,6 +26,7 @@ from . import collectives as C
 from . import kernels as K
 from . import ops
 from .ops import SITE_ATTN_OUT, SITE_MLP_OUT
+from .exchange import AGB, AGF, RSB, RSF, chunk_order, publish_order
 from .state import STATE, get_pool
 
 
@@ -307,6 +308,142 @@ def _push_target(m: LayerMeta, R: int, H: int):
     return G, dict(out_peers=tbl, peer_off=off)
 
 
+# tp_exchange == "chunks" (default with peer comm): the sub-layer runs as T per-owner chunks, own
+# rows first; gathers and reduce-scatters move on the copy engines through the mailboxes of
+# exchange.py while the SMs compute the next chunk.  The saved tensors are the same as the
+# barrier path's (full gathered input, qkv / ctx / lse / f / z over all T*b samples), so the
+# backward is shared.
+
+def _chunked(m: LayerMeta, R: int) -> bool:
+    return m.tp_size > 1 and _peer(m, R) and STATE.config.get("tp_exchange", "barrier") == "chunks"
+
+
+def _publish(G: int, R: int, H: int, m: LayerMeta) -> None:
+    """Send this rank's rows of gather region G (already in G[me]) to every peer's G[me]."""
+    pool = get_pool()
+    xch = pool.exchange()
+    off = G + pool.me * R * H * 2
+    src = pool.view(off, (R, H))
+    for j in publish_order(pool.me, m.tp_size):
+        xch.send(AGF, j, off, src, ack=False)
+
+
+def _chunk_gather_in(x2, m: LayerMeta, ln=None):
+    """Gather region of the sub-layer input for the chunk loop: published by the previous
+    sub-layer's consumer, or (stack entry / pre-LN) written here and published now.
+    Returns (hf [T*R, H] view, mean, rstd, region)."""
+    R, H = x2.shape
+    pool = get_pool()
+    G = _PUSHED.pop((x2.data_ptr(), x2.numel()), None) if ln is None else None
+    mean = rstd = None
+    if G is None:
+        if STATE.xch_fresh:  # step entry: every rank is done with the previous step's regions
+            pool.barrier()
+            STATE.xch_fresh = False
+        G = pool.alloc(m.tp_size * R * H * 2)
+        off = G // 2 + pool.me * R * H
+        if ln is not None:
+            _, _, mean, rstd = ops.bdr_ln(x2, gamma=ln[0], beta=ln[1], eps=m.eps, want_r=False, want_y=False,
+                                          out_peers=pool.self_table, peer_off=off)
+        else:
+            ops.bdr_ln(x2, want_r=False, out_peers=pool.self_table, peer_off=off)
+        _publish(G, R, H, m)
+    return pool.view(G, (m.tp_size * R, H)), mean, rstd, G
+
+
+def _chunk_rs_slots(m: LayerMeta, R: int, N: int):
+    """This rank's reduce-scatter slots [T, R, N] (slot j = rank j's partial of my rows)."""
+    pool = get_pool()
+    P = pool.scratch("rsf_slots", m.tp_size * R * N * 2)
+    return P, pool.view(P, (m.tp_size, R, N))
+
+
+def _chunk_partial_out(c: int, P: int, slots, R: int, N: int):
+    """Output buffer of chunk c's row-parallel product: my own slot, or a staging buffer."""
+    pool = get_pool()
+    return slots[pool.me] if c == pool.me else pool.exchange().staging("rsf", c, (R, N))
+
+
+def _chunk_partial_send(c: int, P: int, dst, R: int, N: int) -> None:
+    pool = get_pool()
+    if c != pool.me:
+        pool.exchange().send(RSF, c, P + pool.me * R * N * 2, dst, ack=True, stage_tag="rsf")
+
+
+def _chunk_consume(m: LayerMeta, R: int, H: int, P: int, consume):
+    """Await the T-1 partial slots, run consume(slot kwargs, push kwargs) (the fused sum +
+    bias + dropout + residual + LayerNorm), release the slots, publish the output rows.
+    Returns (consume's result, next gather region or None)."""
+    pool = get_pool()
+    xch = pool.exchange()
+    T = m.tp_size
+    for j in range(T):
+        if j != pool.me:
+            xch.await_(RSF, j)
+    Gn = pool.alloc(T * R * H * 2) if m.push_next else None
+    pkw = dict(out_peers=pool.self_table, peer_off=Gn // 2 + pool.me * R * H) if Gn is not None else {}
+    res = consume(dict(nslots=T, slot_stride=R * H), pkw)
+    for j in range(T):
+        if j != pool.me:
+            xch.release(RSF, j)
+    xch.join()  # this sub-layer's partial copies (done: the peers consumed theirs) and older publishes
+    if Gn is not None:
+        _publish(Gn, R, H, m)
+    return res, Gn
+
+
+def _chunk_grad_publish(dy2, r, mean, rstd, m: LayerMeta, site: int, keep=None):
+    """Backward of the sub-layer epilogue on own rows (chunked exchange): the branch gradient goes
+    into this rank's slot of the site's gather region and the fp32 [nv, H] replicated-parameter
+    gradient partials into its slot of the vector region; both are published to every peer.
+    Returns (dr, gather region, vector region, nv)."""
+    R, H = dy2.shape
+    pool = get_pool()
+    xch = pool.exchange()
+    T, me = m.tp_size, pool.me
+    has_ln = m._post_w is not None
+    nv = 3 if has_ln else 1  # [dgamma, dbeta,] dbias
+    dG = pool.scratch(f"agb{site}", T * R * H * 2)
+    V = pool.scratch(f"vecb{nv}", T * nv * H * 4)
+    pg = pool.view(V + me * nv * H * 4, (nv, H), dtype=torch.float32)
+    kw = dict(p=m.p_hidden, seed=m.seed, rng=m.rng, layer=m.layer_id, site=site, row_offset=m.row_offset,
+              want_dr=m.post_ln, keep_in=keep)
+    dr, _, _, _, _ = ops.ln_bwd(dy2, r, mean, rstd, m._post_w, out_peers=pool.self_table,
+                                peer_off=dG // 2 + me * R * H, param_grads_out=pg, want_dbias=True,
+                                grads_f32=True, **kw)
+    mine = pool.view(dG + me * R * H * 2, (R, H))
+    for j in publish_order(me, T):
+        xch.send(AGB, j, dG + me * R * H * 2, mine, ack=True, extra=((V + me * nv * H * 4, pg),))
+    return dr, dG, V, nv
+
+
+def _chunk_grad_finish(m: LayerMeta, R: int, H: int, Pb: int, bslots, dr, x2, pre_w, mu1, rs1, V: int, nv: int):
+    """Await the input-gradient partial slots, reduce them into dx (+ pre-LN backward), sum the
+    replicated-parameter gradient slots in ascending rank order (fp32, rounded once), release
+    every slot.  Returns (dx, dpre_w, dpre_b, dpost_w, dpost_b, dbias_out)."""
+    pool = get_pool()
+    xch = pool.exchange()
+    T = m.tp_size
+    for j in range(T):
+        if j != pool.me:
+            xch.await_(RSB, j)
+    dx, dpre_w, dpre_b = _input_grad(bslots[0], dict(nslots=T, slot_stride=R * H), dr, x2, pre_w, mu1, rs1, m, R, H)
+    slots = pool.view(V, (T, nv, H), dtype=torch.float32)
+    tot = slots[0].clone()
+    for j in range(1, T):
+        tot += slots[j]
+    tot = tot.to(torch.bfloat16)
+    for j in range(T):
+        if j != pool.me:
+            xch.release(RSB, j)
+            xch.release(AGB, j)
+    xch.join()
+    if nv == 3:
+        m._post_synced = True
+        return dx, dpre_w, dpre_b, tot[0], tot[1], tot[2]
+    return dx, dpre_w, dpre_b, None, None, tot[0]
+
+
 def _gather_in(x2, m: LayerMeta, ln=None):
     """Column-parallel GEMM input: [pre-LN](own rows) gathered over the group.
     Returns (hf, mean, rstd, pool region or None)."""
@@ -449,23 +586,52 @@ class AttentionFn(torch.autograd.Function):
         B = b * (m.tp_size if m.shard_rows else 1)  # T*b samples when row-sharded
         if fused:  # keep bits depend only on (seed, layer, coordinates): overlap them with the QKV GEMM
             bits, join = _keep_bits_async(B, s, m, x.device)
-        hf, mu1, rs1, G = _gather_in(x2, m, (pre_w, pre_b) if m.pre_ln else None)
-        assert hf.shape[0] == B * s
-        qkv = K.linear(hf, wqkv, bqkv)
-        if fused:
-            join()
-            ctxv, lse = ops.flash_attn_fwd(qkv, B, s, m.heads_local, m.head_dim, mask_add=mask_add, causal=m.causal,
-                                           p=m.p_attn, keep_bits=bits)
-            P, Pd = lse, bits  # the backward re-reads the same keep bits
-        else:
-            ctxv, P, Pd = attn_core_fwd(qkv, B, s, m, mask_add)
-        ox, skw, PR = _rs_out(ctxv, wo, False, m, R, H)
         kb = ops.keep_bytes(R, H, x.device) if m.p_hidden > 0 else None  # reused by the backward
-        Gn, pkw = _push_target(m, R, H)
-        r, y, mu2, rs2 = ops.bdr_ln(ox, bias=bo, residual=x2, gamma=post_w if m.post_ln else None,
-                                    beta=post_b if m.post_ln else None, eps=m.eps, p=m.p_hidden, seed=m.seed, rng=m.rng,
-                                    layer=m.layer_id, site=SITE_ATTN_OUT, row_offset=m.row_offset, rows=R, cols=H,
-                                    keep_out=kb, **skw, **pkw)
+
+        def epilogue(ox, skw, pkw):  # bias + dropout + residual [+ LayerNorm] of this rank's rows
+            return ops.bdr_ln(ox, bias=bo, residual=x2, gamma=post_w if m.post_ln else None,
+                              beta=post_b if m.post_ln else None, eps=m.eps, p=m.p_hidden, seed=m.seed, rng=m.rng,
+                              layer=m.layer_id, site=SITE_ATTN_OUT, row_offset=m.row_offset, rows=R, cols=H,
+                              keep_out=kb, **skw, **pkw)
+
+        if fused and _chunked(m, R):  # per-owner chunks, copy-engine exchanges (exchange.py)
+            hf, mu1, rs1, G = _chunk_gather_in(x2, m, (pre_w, pre_b) if m.pre_ln else None)
+            pool = get_pool()
+            qkv = torch.empty(B * s, wqkv.shape[0], dtype=x.dtype, device=x.device)
+            ctxv = torch.empty(B * s, m.heads_local * m.head_dim, dtype=x.dtype, device=x.device)
+            lse = torch.empty(B, m.heads_local, s, dtype=torch.float32, device=x.device)
+            Pr, slots = _chunk_rs_slots(m, R, H)
+            mk = mask_add.reshape(B, s) if mask_add is not None else None
+            for i, c in enumerate(chunk_order(pool.me, m.tp_size)):
+                if c != pool.me:
+                    pool.exchange().await_(AGF, c)
+                rows, smp = slice(c * R, (c + 1) * R), slice(c * b, (c + 1) * b)
+                K.linear(hf[rows], wqkv, bqkv, out=qkv[rows])
+                if i == 0:
+                    join()
+                ops.flash_attn_fwd(qkv[rows], b, s, m.heads_local, m.head_dim, mask_add=None if mk is None else mk[smp],
+                                   causal=m.causal, p=m.p_attn, keep_bits=None if bits is None else bits[smp],
+                                   out=ctxv[rows], lse_out=lse[smp])
+                dst = _chunk_partial_out(c, Pr, slots, R, H)
+                K.linear(ctxv[rows], wo, out=dst)
+                _chunk_partial_send(c, Pr, dst, R, H)
+            P, Pd = lse, bits
+            (r, y, mu2, rs2), Gn = _chunk_consume(m, R, H, Pr, lambda skw, pkw: epilogue(slots[0], skw, pkw))
+            PR = None
+        else:
+            hf, mu1, rs1, G = _gather_in(x2, m, (pre_w, pre_b) if m.pre_ln else None)
+            assert hf.shape[0] == B * s
+            qkv = K.linear(hf, wqkv, bqkv)
+            if fused:
+                join()
+                ctxv, lse = ops.flash_attn_fwd(qkv, B, s, m.heads_local, m.head_dim, mask_add=mask_add,
+                                               causal=m.causal, p=m.p_attn, keep_bits=bits)
+                P, Pd = lse, bits  # the backward re-reads the same keep bits
+            else:
+                ctxv, P, Pd = attn_core_fwd(qkv, B, s, m, mask_add)
+            ox, skw, PR = _rs_out(ctxv, wo, False, m, R, H)
+            Gn, pkw = _push_target(m, R, H)
+            r, y, mu2, rs2 = epilogue(ox, skw, pkw)
         ctx.kb = kb
         _free(PR)
         if not (m.grad and any(ctx.needs_input_grad)):  # no backward will run: release the gather now
@@ -489,6 +655,42 @@ class AttentionFn(torch.autograd.Function):
             Pd = P
         dy2 = dy.reshape(R, H).contiguous()
         m._post_w = post_w if m.post_ln else None
+        if ctx.fused and _chunked(m, R):  # per-owner chunks, copy-engine exchanges (exchange.py)
+            pool = get_pool()
+            T, me = m.tp_size, pool.me
+            dr, dG, V, nv = _chunk_grad_publish(dy2, r, mu2, rs2, m, SITE_ATTN_OUT, ctx.kb)
+            if not m.post_ln:
+                dr = dy2
+            dof = pool.view(dG, (T * R, H))
+            dctx = torch.empty_like(ctxv)
+            dqkv = torch.empty_like(qkv)
+            Pb = pool.scratch("rsb_slots", T * R * H * 2)
+            bslots = pool.view(Pb, (T, R, H))
+            for c in chunk_order(me, T):
+                if c != me:
+                    pool.exchange().await_(AGB, c)
+                rows, smp = slice(c * R, (c + 1) * R), slice(c * b, (c + 1) * b)
+                K.matmul_nn(dof[rows], wo, out=dctx[rows])
+                ops.flash_attn_bwd(dctx[rows], qkv[rows], ctxv[rows], P[smp], b, s, m.heads_local, m.head_dim,
+                                   mask_add=None if mask_add is None else mask_add.reshape(B, s)[smp],
+                                   causal=m.causal, p=m.p_attn, keep_bits=Pd[smp] if m.p_attn > 0 else None,
+                                   dqkv=dqkv[rows])
+                dst = bslots[me] if c == me else pool.exchange().staging("rsb", c, (R, H))
+                K.matmul_nn(dqkv[rows], wqkv, out=dst)
+                if c != me:
+                    pool.exchange().send(RSB, c, Pb + me * R * H * 2, dst, ack=True, stage_tag="rsb")
+            dwo, dwqkv = torch.empty_like(wo), torch.empty_like(wqkv)
+            with K.grouped():  # the weight gradients hide the last partial's copy
+                K.matmul_tn(dof, ctxv, out=dwo)
+                K.matmul_tn(dqkv, hf, out=dwqkv)
+            dbqkv = ops.colsum(dqkv)
+            dx, dpre_w, dpre_b, dpost_w, dpost_b, dbo = _chunk_grad_finish(m, R, H, Pb, bslots, dr, x2, pre_w, mu1,
+                                                                           rs1, V, nv)
+            _free(ctx.G)
+            dpost_w, dpost_b, dpre_w, dpre_b = _sync_replicated(
+                [None, None, dpre_w, dpre_b] if nv == 3 else [dpost_w, dpost_b, dpre_w, dpre_b], m,
+                keep=(dpost_w, dpost_b) if nv == 3 else None)
+            return (dx.view(b, s, H), dwqkv, dbqkv, dwo, dbo, dpre_w, dpre_b, dpost_w, dpost_b, None, None)
         dr, dof, dpost_w, dpost_b, dbo, G2 = _gather_grad(dy2, r, mu2, rs2, m, SITE_ATTN_OUT, ctx.kb)
         if not m.post_ln:
             dr = dy2
@@ -542,15 +744,38 @@ class MlpFn(torch.autograd.Function):
         b, s, H = x.shape
         R = b * s
         x2 = x.reshape(R, H)
-        hf, mu1, rs1, G = _gather_in(x2, m, (pre_w, pre_b) if m.pre_ln else None)
-        f, z = K.linear(hf, w1, b1, act=m.activation)
-        gx, skw, PR = _rs_out(f, w2, False, m, R, H)
         kb = ops.keep_bytes(R, H, x.device) if m.p_hidden > 0 else None  # reused by the backward
-        Gn, pkw = _push_target(m, R, H)
-        r, y, mu2, rs2 = ops.bdr_ln(gx, bias=b2, residual=x2, gamma=post_w if m.post_ln else None,
-                                    beta=post_b if m.post_ln else None, eps=m.eps, p=m.p_hidden, seed=m.seed, rng=m.rng,
-                                    layer=m.layer_id, site=SITE_MLP_OUT, row_offset=m.row_offset, rows=R, cols=H,
-                                    keep_out=kb, **skw, **pkw)
+
+        def epilogue(gx, skw, pkw):  # bias + dropout + residual [+ LayerNorm] of this rank's rows
+            return ops.bdr_ln(gx, bias=b2, residual=x2, gamma=post_w if m.post_ln else None,
+                              beta=post_b if m.post_ln else None, eps=m.eps, p=m.p_hidden, seed=m.seed, rng=m.rng,
+                              layer=m.layer_id, site=SITE_MLP_OUT, row_offset=m.row_offset, rows=R, cols=H,
+                              keep_out=kb, **skw, **pkw)
+
+        if _chunked(m, R):  # per-owner chunks, copy-engine exchanges (exchange.py)
+            hf, mu1, rs1, G = _chunk_gather_in(x2, m, (pre_w, pre_b) if m.pre_ln else None)
+            pool = get_pool()
+            TR = m.tp_size * R
+            f = torch.empty(TR, w1.shape[0], dtype=x.dtype, device=x.device)
+            z = torch.empty_like(f) if m.activation != "none" else None
+            Pr, slots = _chunk_rs_slots(m, R, H)
+            for c in chunk_order(pool.me, m.tp_size):
+                if c != pool.me:
+                    pool.exchange().await_(AGF, c)
+                rows = slice(c * R, (c + 1) * R)
+                K.linear(hf[rows], w1, b1, act=m.activation, out=f[rows],
+                         aux_out=None if z is None else z[rows])
+                dst = _chunk_partial_out(c, Pr, slots, R, H)
+                K.linear(f[rows], w2, out=dst)
+                _chunk_partial_send(c, Pr, dst, R, H)
+            (r, y, mu2, rs2), Gn = _chunk_consume(m, R, H, Pr, lambda skw, pkw: epilogue(slots[0], skw, pkw))
+            PR = None
+        else:
+            hf, mu1, rs1, G = _gather_in(x2, m, (pre_w, pre_b) if m.pre_ln else None)
+            f, z = K.linear(hf, w1, b1, act=m.activation)
+            gx, skw, PR = _rs_out(f, w2, False, m, R, H)
+            Gn, pkw = _push_target(m, R, H)
+            r, y, mu2, rs2 = epilogue(gx, skw, pkw)
         ctx.kb = kb
         _free(PR)
         if not (m.grad and any(ctx.needs_input_grad)):  # no backward will run: release the gather now
@@ -571,6 +796,40 @@ class MlpFn(torch.autograd.Function):
         x2, hf, mu1, rs1, f, z, r, mu2, rs2, w1, w2, pre_w, post_w = ctx.saved_tensors
         dy2 = dy.reshape(R, H).contiguous()
         m._post_w = post_w if m.post_ln else None
+        if _chunked(m, R):  # per-owner chunks, copy-engine exchanges (exchange.py)
+            pool = get_pool()
+            T, me = m.tp_size, pool.me
+            dr, dG, V, nv = _chunk_grad_publish(dy2, r, mu2, rs2, m, SITE_MLP_OUT, ctx.kb)
+            if not m.post_ln:
+                dr = dy2
+            dgf = pool.view(dG, (T * R, H))
+            dz = torch.empty_like(z)
+            cr = K.colsum_rows(R)
+            part = torch.empty(T * cr, z.shape[1], dtype=torch.float32, device=z.device)
+            Pb = pool.scratch("rsb_slots", T * R * H * 2)
+            bslots = pool.view(Pb, (T, R, H))
+            for c in chunk_order(me, T):
+                if c != me:
+                    pool.exchange().await_(AGB, c)
+                rows = slice(c * R, (c + 1) * R)
+                K.matmul_nn(dgf[rows], w2, epi=K.EPI_DACT, act=m.activation, aux=z[rows], out=dz[rows],
+                            colsum_part=part[c * cr:(c + 1) * cr])
+                dst = bslots[me] if c == me else pool.exchange().staging("rsb", c, (R, H))
+                K.matmul_nn(dz[rows], w1, out=dst)
+                if c != me:
+                    pool.exchange().send(RSB, c, Pb + me * R * H * 2, dst, ack=True, stage_tag="rsb")
+            dw1, dw2 = torch.empty_like(w1), torch.empty_like(w2)
+            with K.grouped():  # the weight gradients hide the last partial's copy
+                K.matmul_tn(dgf, f, out=dw2)
+                K.matmul_tn(dz, hf, out=dw1)
+            db1 = K.colsum_reduce(part, torch.empty(z.shape[1], dtype=z.dtype, device=z.device))
+            dx, dpre_w, dpre_b, dpost_w, dpost_b, db2 = _chunk_grad_finish(m, R, H, Pb, bslots, dr, x2, pre_w, mu1,
+                                                                           rs1, V, nv)
+            _free(ctx.G)
+            dpost_w, dpost_b, dpre_w, dpre_b = _sync_replicated(
+                [None, None, dpre_w, dpre_b] if nv == 3 else [dpost_w, dpost_b, dpre_w, dpre_b], m,
+                keep=(dpost_w, dpost_b) if nv == 3 else None)
+            return (dx.view(b, s, H), dw1, db1, dw2, db2, dpre_w, dpre_b, dpost_w, dpost_b, None)
         dr, dgf, dpost_w, dpost_b, db2, G2 = _gather_grad(dy2, r, mu2, rs2, m, SITE_MLP_OUT, ctx.kb)
         if not m.post_ln:
             dr = dy2

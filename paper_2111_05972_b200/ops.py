@@ -177,7 +177,7 @@ def flash_attn_bwd(dctx: torch.Tensor, qkv: torch.Tensor, ctx: torch.Tensor, lse
 
 
 def flash_attn_fwd(qkv: torch.Tensor, B: int, s: int, nh: int, dh: int, *, mask_add=None, causal=False, p=0.0,
-                   keep_bits=None, out=None):
+                   keep_bits=None, out=None, lse_out=None):
     """Fused attention on the packed QKV buffer [B*s, 3*nh*dh] (q | k | v blocks, heads inside each).
     Dropout (p > 0) uses keep_bits from attn_dropout_bits.
     Returns (ctx [B*s, nh*dh] bf16, lse [B, nh, s] fp32 log2-domain)."""
@@ -185,7 +185,7 @@ def flash_attn_fwd(qkv: torch.Tensor, B: int, s: int, nh: int, dh: int, *, mask_
     if p > 0 and keep_bits is None:
         raise ValueError("flash_attn_fwd: dropout needs keep bits (ops.attn_dropout_bits)")
     ctx = out if out is not None else torch.empty(B * s, nh * dh, dtype=qkv.dtype, device=qkv.device)
-    lse = torch.empty(B, nh, s, dtype=torch.float32, device=qkv.device)
+    lse = lse_out if lse_out is not None else torch.empty(B, nh, s, dtype=torch.float32, device=qkv.device)
     if mask_add is not None:
         mask_add = mask_add.reshape(B, s).to(torch.float32).contiguous()
     _lib.call("smpk_flash_attn_fwd", _ptr(qkv), qkv.stride(0), B, nh, s, dh, _ptr(ctx), ctx.stride(0), _ptr(lse),

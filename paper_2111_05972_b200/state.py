@@ -32,8 +32,9 @@ DEFAULTS = {
     "seed": 0,
     "ddp": True,
     "tp_comm": "peer",  # fused NVLink peer-memory collectives ("nccl": torch.distributed calls)
-    "tp_rs": "pull",
-    "tp_overlap_sms": 0,  # >0: backward weight-gradient GEMMs on this many SMs beside the exchange  # peer reduce-scatter: consumer pulls the partials ("push": GEMM epilogue stores)
+    "tp_rs": "pull",  # barrier exchange: the consumer pulls the partials ("push": GEMM epilogue stores)
+    "tp_exchange": "barrier",  # peer mode: "chunks" = per-owner chunks + copy-engine mailboxes (exchange.py), "barrier"
+    "tp_overlap_sms": 0,  # >0: backward weight-gradient GEMMs on this many SMs beside the exchange
     "symm_pool_bytes": 4 << 30,
 }
 
@@ -55,6 +56,7 @@ class State:
     step: int = 0  # host mirror: forwards issued eagerly (graph replays advance only the device word)
     rng_counter: object = None  # device int64 step word (one per process), advanced per top-level forward
     rng_cur: object = None  # snapshot of the step word the current forward's dropout kernels read
+    xch_fresh: bool = True  # no chunked exchange issued yet in this forward (step-entry barrier due)
 
     # -- accessors mirroring smp.tp_rank() / smp.tp_size() ...
     @property
@@ -181,6 +183,7 @@ def begin_forward():
                                "(call smp.init() / run one eager step on this device first)")
         STATE.rng_counter = torch.zeros(1, dtype=torch.int64, device=dev)
     STATE.rng_cur = ops.rng_next(STATE.rng_counter)
+    STATE.xch_fresh = True
     STATE.step += 1
     return STATE.rng_cur
 

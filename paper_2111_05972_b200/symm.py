@@ -42,22 +42,30 @@ class SymmPool:
         dev = torch.device("cuda", torch.cuda.current_device())
         self.buf = torch.empty(capacity_bytes, dtype=torch.uint8, device=dev)
         self.flags = torch.zeros(64, dtype=torch.int32, device=dev)
+        from .exchange import NWORDS
+        self.xflags = torch.zeros(NWORDS, dtype=torch.int32, device=dev)  # chunked-exchange mailbox words
+        torch.cuda.synchronize()  # zeroed before any peer can map and signal them
         self.capacity = capacity_bytes
-        mine = (self._export(self.buf), self._export(self.flags))
+        mine = (self._export(self.buf), self._export(self.flags), self._export(self.xflags))
         gathered = [None] * self.T
         dist.all_gather_object(gathered, mine, group=group)
         self._mapped = []
-        bases, flag_bases = [], []
-        for j, ((hb, ob), (hf, of)) in enumerate(gathered):
+        bases, flag_bases, xflag_bases = [], [], []
+        for j, ((hb, ob), (hf, of), (hx, ox)) in enumerate(gathered):
             if j == self.me:
                 bases.append(self.buf.data_ptr())
                 flag_bases.append(self.flags.data_ptr())
+                xflag_bases.append(self.xflags.data_ptr())
                 continue
-            pb, pf = self._import(hb), self._import(hf)
-            self._mapped += [pb, pf]
+            pb, pf, px = self._import(hb), self._import(hf), self._import(hx)
+            self._mapped += [pb, pf, px]
             bases.append(pb + ob)
             flag_bases.append(pf + of)
+            xflag_bases.append(px + ox)
         self.bases = bases
+        self.xflag_bases = xflag_bases
+        self.self_table = torch.tensor([bases[my_index]], dtype=torch.int64, device=dev)
+        self._xch = None
         self.flag_table = torch.tensor(flag_bases, dtype=torch.int64, device=dev)
         self.base_table = torch.tensor(bases, dtype=torch.int64, device=dev)
         self.base_array = (C.c_void_p * self.T)(*bases)  # host copy (TMA-store descriptors)
@@ -79,6 +87,13 @@ class SymmPool:
         p = C.c_void_p()
         _lib.call("smpk_p2p_import", C.create_string_buffer(handle, 64), C.byref(p))
         return p.value
+
+    def exchange(self):
+        """The chunked-exchange mailboxes of this group (exchange.Exchange), created on first use."""
+        if self._xch is None:
+            from .exchange import Exchange
+            self._xch = Exchange(self)
+        return self._xch
 
     # -- allocation (identical sequence on every rank) -------------------------------
     def alloc(self, nbytes: int) -> int:

@@ -34,10 +34,11 @@ def gather_cpu(t):
 
 
 def run_case(smp, name, *, prescaled, causal, pre, post, p, layers=1, act="gelu", comm="peer", optimize="speed",
-             rs="pull", overlap=0):
+             rs="pull", overlap=0, exchange="chunks"):
     T, rank = dist.get_world_size(), dist.get_rank()
     smp.init({"tensor_parallel_degree": T, "optimize": optimize, "_prescaled_batch": prescaled, "seed": 11,
-              "tp_comm": comm, "tp_rs": rs, "symm_pool_bytes": 256 << 20, "tp_overlap_sms": overlap})
+              "tp_comm": comm, "tp_rs": rs, "symm_pool_bytes": 256 << 20, "tp_overlap_sms": overlap,
+              "tp_exchange": exchange})
     nh, dh, I, s, B = 2 * T, 64, 512 * T, 128, 2
     H = nh * dh
     cfg = tp.LayerConfig(num_attention_heads=nh, attention_head_size=dh, hidden_size=H, intermediate_size=I,
@@ -286,6 +287,8 @@ def main():
         run_case(smp, "stack2_nccl_comm", prescaled=False, causal=True, pre=True, post=False, p=0.1, layers=2,
                  comm="nccl"),
         run_case(smp, "stack3_peer_post_ln", prescaled=False, causal=False, pre=False, post=True, p=0.1, layers=3),
+        run_case(smp, "stack3_peer_post_ln_barrier_exchange", prescaled=False, causal=False, pre=False, post=True,
+                 p=0.1, layers=3, exchange="barrier"),
         run_case(smp, "stack2_peer_wgrad_overlap", prescaled=False, causal=False, pre=False, post=True, p=0.1,
                  layers=2, overlap=64),
         run_case(smp, "stack2_overlap_pre_ln", prescaled=False, causal=True, pre=True, post=False, p=0.1, layers=2,
