@@ -292,11 +292,14 @@ def trace_kernels(run, path_prefix: str, rank: int, steps: int = 2) -> None:
         a[0] += 1
         a[1] += ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total
     tot = sum(v[1] for v in agg.values())
-    seq = [(ev.name, ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total)
+    seq = [(ev.name, ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total,
+            ev.time_range.start, getattr(ev, "device_resource_id", -1))
            for ev in prof.events() if ev.device_type == torch.autograd.DeviceType.CUDA]
-    with open(f"{path_prefix}_rank{rank}_seq.txt", "w") as f:  # launch order of the first step
-        for name, us in seq[:len(seq) // steps]:
-            f.write(f"{us:9.1f}  {name[:110]}\n")
+    first = seq[:len(seq) // steps]
+    t0 = min(t for _, _, t, _ in first) if first else 0
+    with open(f"{path_prefix}_rank{rank}_seq.txt", "w") as f:  # the first step: duration, start, stream
+        for name, us, t, sid in sorted(first, key=lambda e: e[2]):
+            f.write(f"{us:9.1f} {t - t0:10.1f} {sid:4d}  {name[:100]}\n")
     with open(f"{path_prefix}_rank{rank}.txt", "w") as f:
         f.write(f"# {steps} steps, total kernel time {tot / steps / 1e3:.3f} ms/step\n")
         for name, (n, us) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
@@ -506,8 +509,9 @@ def main():
                     help="smp optimize mode of the TP layers (PAPER.md:763); the headline is speed")
     ap.add_argument("--tp-comm", default="peer", choices=["peer", "nccl"],
                     help="TP collectives: fused NVLink peer stores (default) or NCCL calls")
-    ap.add_argument("--tp-exchange", default="barrier", choices=["chunks", "barrier"],
-                    help="peer exchanges: per-owner chunks over copy-engine mailboxes, or one barrier per exchange")
+    ap.add_argument("--tp-exchange", default="barrier", choices=["overlap", "chunks", "barrier"],
+                    help="peer exchanges: copy-engine mailboxes with two overlapped micro-batches, per-owner chunks "
+                         "over the mailboxes, or SM pull/push behind one barrier per exchange")
     ap.add_argument("--tp-rs", default="pull", choices=["pull", "push"],
                     help="peer reduce-scatter: consumer pulls partials over NVLink, or GEMM epilogue pushes")
     ap.add_argument("--tp-overlap-sms", type=int, default=int(os.environ.get("SMPK_TP_OVERLAP_SMS", "-1")),

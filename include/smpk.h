@@ -383,6 +383,33 @@ SMPK_API int smpk_copy_async(void* dst, const void* src, int64_t bytes, void* st
  * chunked TP exchange (PAPER.md:281 AG/RS of TP-across-DP, split into per-owner chunks so the
  * copy engines move chunk c while the SMs compute chunk c+1). */
 SMPK_API int smpk_stream_flag(void* word, uint32_t value, int op, void* stream);
+
+/* Mailbox copies of the overlapped TP exchanges (tp_exchange = "overlap" / "chunks"; PAPER.md:281
+ * AG/RS of TP across DP moved while the other micro-batch computes).  smpk_peer_put copies up to
+ * SMPK_PUT_MAX_RANGES 16-byte-aligned ranges into peer-mapped slots with ordinary vector stores
+ * (a few CTAs, SMPK_PUT_CTAS, default 32), then raises each destination group's ready word
+ * (release.sys after the group's last CTA); a group with an ack word first waits for ack == 0
+ * (the receiver released the previous round) and sets ack = 1.  counter: SMPK_PUT_MAX_GROUPS
+ * zeroed words owned by this stream.  smpk_flag_wait spins until every word == value, then
+ * re-arms it to 0 (timeout: records who[i] + 1 -- the signalling peer -- for smpk_symm_timeout_peer
+ * and traps);
+ * smpk_flag_set release-stores value into every word. */
+#define SMPK_PUT_MAX_RANGES 16
+#define SMPK_PUT_MAX_GROUPS 8
+typedef struct {
+  const void* src;
+  void* dst;
+  int64_t bytes;
+  int group;
+} smpk_put_range;
+typedef struct {
+  uint32_t* ready;
+  uint32_t* ack;
+} smpk_put_group;
+SMPK_API int smpk_peer_put(const smpk_put_range* ranges, int nr, const smpk_put_group* groups, int ng, void* counter,
+                           double timeout_s, void* stream);
+SMPK_API int smpk_flag_wait(void* const* words, const int* who, int n, uint32_t value, double timeout_s, void* stream);
+SMPK_API int smpk_flag_set(void* const* words, int n, uint32_t value, void* stream);
 SMPK_API int smpk_symm_export(void* ptr, void* handle_out, int64_t* offset);
 SMPK_API int smpk_symm_barrier(void* const* peer_flags, void* local_flags, int T, int rank, double timeout_s,
                                void* stream);

@@ -51,6 +51,9 @@ SIGNATURES: dict[str, list] = {
     "smpk_act_bwd": [P, P, I, I, I, P, P],
     "smpk_copy_async": [P, P, L, P],
     "smpk_stream_flag": [P, C.c_uint32, I, P],
+    "smpk_peer_put": [P, I, P, I, P, C.c_double, P],
+    "smpk_flag_wait": [P, P, I, C.c_uint32, C.c_double, P],
+    "smpk_flag_set": [P, I, C.c_uint32, P],
     "smpk_rng_next": [P, P, P],
     "smpk_gemm_grouped": [P, I, P],
     "smpk_embed_bwd_sorted": [P, L, P, L, L, L, I, P, L, I, I, L, P, L, P],

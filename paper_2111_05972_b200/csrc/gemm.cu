@@ -890,6 +890,16 @@ static bool pair_enabled() {
   return v == 1;
 }
 
+// SMPK_GEMM_PAIR_SPLITK=1 keeps split-K GEMMs on CTA pairs (A/B measurements)
+static bool pair_splitk() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SMPK_GEMM_PAIR_SPLITK");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 static int pick_bn(int N) { return N <= 64 ? 64 : (N <= 128 ? 128 : 256); }
 
 // Tile plan: CTA pairs (256-row tiles, cta_group::2) whenever N >= 128 and M >= 256, else
@@ -902,7 +912,7 @@ static void plan_gemm(int M, int N, int K, int nb1, int nb2, int& BN, bool& pair
   tiles = ((M + rows - 1) / rows) * ((N + BN - 1) / BN) * nb1 * nb2;
   num_kb = (K + BK - 1) / BK;
   splits = choose_splits(tiles, num_kb, BN, pair ? gemm_sms() / 2 : gemm_sms(), pair ? 2 : 1);
-  if (pair && splits > 1) {
+  if (pair && splits > 1 && !pair_splitk()) {
     // measured: split-K runs faster on single-CTA tiles (finer units, shorter fix-up)
     pair = false;
     tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * nb1 * nb2;

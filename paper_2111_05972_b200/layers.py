@@ -26,7 +26,7 @@ from . import collectives as C
 from . import kernels as K
 from . import ops
 from .ops import SITE_ATTN_OUT, SITE_MLP_OUT
-from .exchange import AGB, AGF, RSB, RSF, chunk_order, publish_order
+from .exchange import AGB, AGF, RSB, RSF, chunk_order, mbkind, publish_order
 from .state import STATE, get_pool
 
 
@@ -54,6 +54,8 @@ class LayerMeta:
     push_next: bool = False  # the next sub-layer gathers this output unnormalised: push it from the epilogue
     grad: bool = True  # grad mode was on at the sub-layer call (Function.forward always runs without it)
     rng: object = None  # device step snapshot of this forward (ops.rng_next): Philox key = seed + step * golden
+    mb: int = -1  # overlapped micro-batch (tp_exchange="overlap"): 0 / 1, -1 = the whole batch
+    mb_batch: int = 0  # with mb >= 0: this rank's full batch (samples), the micro-batch is its half mb
 
 
 class LinearFn(torch.autograd.Function):
@@ -170,9 +172,17 @@ def _keep_bits_async(B: int, s: int, m: LayerMeta, device):
     side = _side_stream()
     side.wait_stream(main)
     with torch.cuda.stream(side):
-        ops.attn_dropout_bits(B, m.heads_local, s, s, p=m.p_attn, seed=m.seed, rng=m.rng, layer=m.layer_id,
-                              sample_offset=m.sample_offset, head_offset=m.head_offset, nh_global=m.heads_global,
-                              out=bits, causal=m.causal and s % 128 == 0)
+        if m.mb < 0:
+            ops.attn_dropout_bits(B, m.heads_local, s, s, p=m.p_attn, seed=m.seed, rng=m.rng, layer=m.layer_id,
+                                  sample_offset=m.sample_offset, head_offset=m.head_offset, nh_global=m.heads_global,
+                                  out=bits, causal=m.causal and s % 128 == 0)
+        else:  # micro-batch mb: rank j's samples [mb*b, (mb+1)*b) of its mb_batch, rank-major
+            b = B // m.tp_size
+            for j in range(m.tp_size):
+                ops.attn_dropout_bits(b, m.heads_local, s, s, p=m.p_attn, seed=m.seed, rng=m.rng, layer=m.layer_id,
+                                      sample_offset=m.sample_offset + j * m.mb_batch + m.mb * b,
+                                      head_offset=m.head_offset, nh_global=m.heads_global,
+                                      out=bits[j * b:(j + 1) * b], causal=m.causal and s % 128 == 0)
     return bits, (lambda: main.wait_stream(side))
 
 
@@ -324,8 +334,7 @@ def _publish(G: int, R: int, H: int, m: LayerMeta) -> None:
     xch = pool.exchange()
     off = G + pool.me * R * H * 2
     src = pool.view(off, (R, H))
-    for j in publish_order(pool.me, m.tp_size):
-        xch.send(AGF, j, off, src, ack=False)
+    xch.put(AGF, [(j, [(off, src)]) for j in publish_order(pool.me, m.tp_size)], ack=False)
 
 
 def _chunk_gather_in(x2, m: LayerMeta, ln=None):
@@ -377,15 +386,11 @@ def _chunk_consume(m: LayerMeta, R: int, H: int, P: int, consume):
     pool = get_pool()
     xch = pool.exchange()
     T = m.tp_size
-    for j in range(T):
-        if j != pool.me:
-            xch.await_(RSF, j)
+    xch.await_all(RSF, chunk_order(pool.me, T)[1:])
     Gn = pool.alloc(T * R * H * 2) if m.push_next else None
     pkw = dict(out_peers=pool.self_table, peer_off=Gn // 2 + pool.me * R * H) if Gn is not None else {}
     res = consume(dict(nslots=T, slot_stride=R * H), pkw)
-    for j in range(T):
-        if j != pool.me:
-            xch.release(RSF, j)
+    xch.release_all([RSF], chunk_order(pool.me, T)[1:])
     xch.join()  # this sub-layer's partial copies (done: the peers consumed theirs) and older publishes
     if Gn is not None:
         _publish(Gn, R, H, m)
@@ -412,8 +417,8 @@ def _chunk_grad_publish(dy2, r, mean, rstd, m: LayerMeta, site: int, keep=None):
                                 peer_off=dG // 2 + me * R * H, param_grads_out=pg, want_dbias=True,
                                 grads_f32=True, **kw)
     mine = pool.view(dG + me * R * H * 2, (R, H))
-    for j in publish_order(me, T):
-        xch.send(AGB, j, dG + me * R * H * 2, mine, ack=True, extra=((V + me * nv * H * 4, pg),))
+    xch.put(AGB, [(j, [(dG + me * R * H * 2, mine), (V + me * nv * H * 4, pg)]) for j in publish_order(me, T)],
+            ack=True)
     return dr, dG, V, nv
 
 
@@ -424,24 +429,131 @@ def _chunk_grad_finish(m: LayerMeta, R: int, H: int, Pb: int, bslots, dr, x2, pr
     pool = get_pool()
     xch = pool.exchange()
     T = m.tp_size
-    for j in range(T):
-        if j != pool.me:
-            xch.await_(RSB, j)
+    xch.await_all(RSB, chunk_order(pool.me, T)[1:])
     dx, dpre_w, dpre_b = _input_grad(bslots[0], dict(nslots=T, slot_stride=R * H), dr, x2, pre_w, mu1, rs1, m, R, H)
     slots = pool.view(V, (T, nv, H), dtype=torch.float32)
     tot = slots[0].clone()
     for j in range(1, T):
         tot += slots[j]
     tot = tot.to(torch.bfloat16)
-    for j in range(T):
-        if j != pool.me:
-            xch.release(RSB, j)
-            xch.release(AGB, j)
+    xch.release_all([RSB, AGB], chunk_order(pool.me, T)[1:])
     xch.join()
     if nv == 3:
         m._post_synced = True
         return dx, dpre_w, dpre_b, tot[0], tot[1], tot[2]
     return dx, dpre_w, dpre_b, None, None, tot[0]
+
+
+# tp_exchange == "overlap": the same whole-sub-layer GEMMs as the barrier exchange, but every
+# transfer is a copy-engine copy through the mailboxes of exchange.py (no barrier kernel, no SM
+# spent on NVLink), and DistributedTransformer runs the batch as two micro-batches on two streams,
+# so one micro-batch's exchange overlaps the other's compute.
+
+def _overlap(m: LayerMeta, R: int) -> bool:
+    return m.tp_size > 1 and _peer(m, R) and STATE.config.get("tp_exchange", "barrier") == "overlap"
+
+
+def _ov_publish(G: int, R: int, H: int, m: LayerMeta) -> None:
+    pool = get_pool()
+    xch = pool.exchange()
+    off = G + pool.me * R * H * 2
+    src = pool.view(off, (R, H))
+    xch.put(mbkind(AGF, m.mb), [(j, [(off, src)]) for j in publish_order(pool.me, m.tp_size)], ack=False,
+            mb=m.mb)
+
+
+def _ov_gather_in(x2, m: LayerMeta, ln=None):
+    """Gather region of the sub-layer input: this rank's rows (published by the previous
+    sub-layer's consumer, or written and published here), then every peer's rows awaited."""
+    R, H = x2.shape
+    pool = get_pool()
+    xch = pool.exchange()
+    G = _PUSHED.pop((x2.data_ptr(), x2.numel()), None) if ln is None else None
+    mean = rstd = None
+    if G is None:
+        if STATE.xch_fresh:  # step entry: every rank is done with the previous step's regions
+            pool.barrier()
+            STATE.xch_fresh = False
+        G = pool.alloc(m.tp_size * R * H * 2)
+        off = G // 2 + pool.me * R * H
+        if ln is not None:
+            _, _, mean, rstd = ops.bdr_ln(x2, gamma=ln[0], beta=ln[1], eps=m.eps, want_r=False, want_y=False,
+                                          out_peers=pool.self_table, peer_off=off)
+        else:
+            ops.bdr_ln(x2, want_r=False, out_peers=pool.self_table, peer_off=off)
+        _ov_publish(G, R, H, m)
+    xch.await_all(mbkind(AGF, m.mb), chunk_order(pool.me, m.tp_size)[1:])
+    return pool.view(G, (m.tp_size * R, H)), mean, rstd, G
+
+
+def _ov_rs(a, w, w_mn: bool, m: LayerMeta, R: int, N: int, kind: int, extra=()):
+    """Row-parallel product into this micro-batch's partial region; every owner's row block
+    leaves on the copy engines for its slot on the owner, the own block stays.  Returns
+    (consumer slot kwargs: the T slots as a table of local addresses, partial view)."""
+    pool = get_pool()
+    xch = pool.exchange()
+    T, me = m.tp_size, pool.me
+    k = mbkind(kind, m.mb)
+    Pp = pool.scratch(f"ovp{k}", T * R * N * 2)
+    S = pool.scratch(f"ovs{k}", T * R * N * 2)
+    P = pool.view(Pp, (T * R, N))
+    xch.reuse(("ovp", k), [c for c in range(T) if c != me])  # last round's copies out of P have left
+    _product(a, w, w_mn, out=P, extra=extra)
+    xch.put(k, [(c, [(S + me * R * N * 2, P[c * R:(c + 1) * R])]) for c in publish_order(me, T)], ack=True,
+            stage_tag=("ovp", k), mb=m.mb)
+    xch.await_all(k, chunk_order(me, T)[1:])
+    base = pool.bases[me]
+    tbl = xch.table(("ovslots", k, R, N), [base + (Pp + me * R * N * 2 if j == me else S + j * R * N * 2)
+                                           for j in range(T)])
+    return dict(nslots=T, x_peers=tbl, x_peer_off=0), P
+
+
+def _ov_release(m: LayerMeta, *kinds) -> None:
+    pool = get_pool()
+    xch = pool.exchange()
+    xch.release_all([mbkind(kind, m.mb) for kind in kinds], chunk_order(pool.me, m.tp_size)[1:])
+    xch.join(m.mb)
+
+
+def _ov_grad_publish(dy2, r, mean, rstd, m: LayerMeta, site: int, keep=None):
+    """Backward of the sub-layer epilogue on own rows; the branch gradient and the fp32
+    replicated-parameter partials are published to every peer and the peers' awaited.
+    Returns (dr, branch gradient of all T*R rows, vector region, nv)."""
+    R, H = dy2.shape
+    pool = get_pool()
+    xch = pool.exchange()
+    T, me = m.tp_size, pool.me
+    k = mbkind(AGB, m.mb)
+    has_ln = m._post_w is not None
+    nv = 3 if has_ln else 1
+    dG = pool.scratch(f"ovg{site}_{k}", T * R * H * 2)
+    V = pool.scratch(f"ovv{nv}_{k}", T * nv * H * 4)
+    pg = pool.view(V + me * nv * H * 4, (nv, H), dtype=torch.float32)
+    kw = dict(p=m.p_hidden, seed=m.seed, rng=m.rng, layer=m.layer_id, site=site, row_offset=m.row_offset,
+              want_dr=m.post_ln, keep_in=keep)
+    dr, _, _, _, _ = ops.ln_bwd(dy2, r, mean, rstd, m._post_w, out_peers=pool.self_table,
+                                peer_off=dG // 2 + me * R * H, param_grads_out=pg, want_dbias=True,
+                                grads_f32=True, **kw)
+    mine = pool.view(dG + me * R * H * 2, (R, H))
+    xch.put(k, [(j, [(dG + me * R * H * 2, mine), (V + me * nv * H * 4, pg)]) for j in publish_order(me, T)],
+            ack=True, mb=m.mb)
+    xch.await_all(k, chunk_order(me, T)[1:])
+    return dr, pool.view(dG, (T * R, H)), V, nv
+
+
+def _ov_vec_sums(m: LayerMeta, V: int, nv: int, H: int):
+    """Replicated-parameter gradient slots summed in ascending rank order (fp32, rounded once):
+    (dpost_w, dpost_b, dbias) -- the first two None without a post-LN."""
+    pool = get_pool()
+    slots = pool.view(V, (m.tp_size, nv, H), dtype=torch.float32)
+    tot = slots[0].clone()
+    for j in range(1, m.tp_size):
+        tot += slots[j]
+    tot = tot.to(torch.bfloat16)
+    if nv == 3:
+        m._post_synced = True
+        return tot[0], tot[1], tot[2]
+    return None, None, tot[0]
 
 
 def _gather_in(x2, m: LayerMeta, ln=None):
@@ -618,6 +730,22 @@ class AttentionFn(torch.autograd.Function):
             P, Pd = lse, bits
             (r, y, mu2, rs2), Gn = _chunk_consume(m, R, H, Pr, lambda skw, pkw: epilogue(slots[0], skw, pkw))
             PR = None
+        elif fused and _overlap(m, R):  # copy-engine exchanges, overlapped micro-batches
+            hf, mu1, rs1, G = _ov_gather_in(x2, m, (pre_w, pre_b) if m.pre_ln else None)
+            qkv = K.linear(hf, wqkv, bqkv)
+            join()
+            ctxv, lse = ops.flash_attn_fwd(qkv, B, s, m.heads_local, m.head_dim, mask_add=mask_add,
+                                           causal=m.causal, p=m.p_attn, keep_bits=bits)
+            P, Pd = lse, bits
+            skw, Pv = _ov_rs(ctxv, wo, False, m, R, H, RSF)
+            pool = get_pool()
+            Gn = pool.alloc(m.tp_size * R * H * 2) if m.push_next else None
+            pkw = dict(out_peers=pool.self_table, peer_off=Gn // 2 + pool.me * R * H) if Gn is not None else {}
+            r, y, mu2, rs2 = epilogue(Pv, skw, pkw)
+            _ov_release(m, RSF)
+            if Gn is not None:
+                _ov_publish(Gn, R, H, m)
+            PR = None
         else:
             hf, mu1, rs1, G = _gather_in(x2, m, (pre_w, pre_b) if m.pre_ln else None)
             assert hf.shape[0] == B * s
@@ -655,6 +783,26 @@ class AttentionFn(torch.autograd.Function):
             Pd = P
         dy2 = dy.reshape(R, H).contiguous()
         m._post_w = post_w if m.post_ln else None
+        if ctx.fused and _overlap(m, R):  # copy-engine exchanges, overlapped micro-batches
+            dr, dof, V, nv = _ov_grad_publish(dy2, r, mu2, rs2, m, SITE_ATTN_OUT, ctx.kb)
+            if not m.post_ln:
+                dr = dy2
+            dwo, dwqkv = torch.empty_like(wo), torch.empty_like(wqkv)
+            with K.grouped():  # dWo and dctx read the same dof
+                K.matmul_tn(dof, ctxv, out=dwo)
+                dctx = K.matmul_nn(dof, wo)
+            dqkv = ops.flash_attn_bwd(dctx, qkv, ctxv, P, B, s, m.heads_local, m.head_dim, mask_add=mask_add,
+                                      causal=m.causal, p=m.p_attn, keep_bits=Pd if m.p_attn > 0 else None)
+            dbqkv = ops.colsum(dqkv)
+            skw, Pv = _ov_rs(dqkv, wqkv, True, m, R, H, RSB, extra=(lambda: K.matmul_tn(dqkv, hf, out=dwqkv),))
+            dx, dpre_w, dpre_b = _input_grad(Pv, skw, dr, x2, pre_w, mu1, rs1, m, R, H)
+            dpost_w, dpost_b, dbo = _ov_vec_sums(m, V, nv, H)
+            _ov_release(m, RSB, AGB)
+            _free(ctx.G)
+            dpost_w, dpost_b, dpre_w, dpre_b = _sync_replicated(
+                [None, None, dpre_w, dpre_b] if nv == 3 else [dpost_w, dpost_b, dpre_w, dpre_b], m,
+                keep=(dpost_w, dpost_b) if nv == 3 else None)
+            return (dx.view(b, s, H), dwqkv, dbqkv, dwo, dbo, dpre_w, dpre_b, dpost_w, dpost_b, None, None)
         if ctx.fused and _chunked(m, R):  # per-owner chunks, copy-engine exchanges (exchange.py)
             pool = get_pool()
             T, me = m.tp_size, pool.me
@@ -770,6 +918,18 @@ class MlpFn(torch.autograd.Function):
                 _chunk_partial_send(c, Pr, dst, R, H)
             (r, y, mu2, rs2), Gn = _chunk_consume(m, R, H, Pr, lambda skw, pkw: epilogue(slots[0], skw, pkw))
             PR = None
+        elif _overlap(m, R):  # copy-engine exchanges, overlapped micro-batches
+            hf, mu1, rs1, G = _ov_gather_in(x2, m, (pre_w, pre_b) if m.pre_ln else None)
+            f, z = K.linear(hf, w1, b1, act=m.activation)
+            skw, Pv = _ov_rs(f, w2, False, m, R, H, RSF)
+            pool = get_pool()
+            Gn = pool.alloc(m.tp_size * R * H * 2) if m.push_next else None
+            pkw = dict(out_peers=pool.self_table, peer_off=Gn // 2 + pool.me * R * H) if Gn is not None else {}
+            r, y, mu2, rs2 = epilogue(Pv, skw, pkw)
+            _ov_release(m, RSF)
+            if Gn is not None:
+                _ov_publish(Gn, R, H, m)
+            PR = None
         else:
             hf, mu1, rs1, G = _gather_in(x2, m, (pre_w, pre_b) if m.pre_ln else None)
             f, z = K.linear(hf, w1, b1, act=m.activation)
@@ -796,6 +956,23 @@ class MlpFn(torch.autograd.Function):
         x2, hf, mu1, rs1, f, z, r, mu2, rs2, w1, w2, pre_w, post_w = ctx.saved_tensors
         dy2 = dy.reshape(R, H).contiguous()
         m._post_w = post_w if m.post_ln else None
+        if _overlap(m, R):  # copy-engine exchanges, overlapped micro-batches
+            dr, dgf, V, nv = _ov_grad_publish(dy2, r, mu2, rs2, m, SITE_MLP_OUT, ctx.kb)
+            if not m.post_ln:
+                dr = dy2
+            dw1, dw2 = torch.empty_like(w1), torch.empty_like(w2)
+            with K.grouped():  # dW2 and dz read the same dgf
+                K.matmul_tn(dgf, f, out=dw2)
+                dz, db1 = K.matmul_nn(dgf, w2, epi=K.EPI_DACT, act=m.activation, aux=z, want_colsum=True)
+            skw, Pv = _ov_rs(dz, w1, True, m, R, H, RSB, extra=(lambda: K.matmul_tn(dz, hf, out=dw1),))
+            dx, dpre_w, dpre_b = _input_grad(Pv, skw, dr, x2, pre_w, mu1, rs1, m, R, H)
+            dpost_w, dpost_b, db2 = _ov_vec_sums(m, V, nv, H)
+            _ov_release(m, RSB, AGB)
+            _free(ctx.G)
+            dpost_w, dpost_b, dpre_w, dpre_b = _sync_replicated(
+                [None, None, dpre_w, dpre_b] if nv == 3 else [dpost_w, dpost_b, dpre_w, dpre_b], m,
+                keep=(dpost_w, dpost_b) if nv == 3 else None)
+            return (dx.view(b, s, H), dw1, db1, dw2, db2, dpre_w, dpre_b, dpost_w, dpost_b, None)
         if _chunked(m, R):  # per-owner chunks, copy-engine exchanges (exchange.py)
             pool = get_pool()
             T, me = m.tp_size, pool.me

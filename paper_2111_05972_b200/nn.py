@@ -18,7 +18,7 @@ from . import collectives as C
 from . import layers as L
 from . import memory_mode as MM
 from .errors import NotDivisibleError, ShapeMismatchError
-from .state import STATE, begin_forward, next_layer_id
+from .state import STATE, begin_forward, get_pool, next_layer_id
 
 DTYPE = torch.bfloat16
 
@@ -168,8 +168,10 @@ class _LayerBase(DistributedModule):
         return STATE.optimize == "memory" and STATE.tp_size > 1
 
     def _meta(self, rc) -> L.LayerMeta:
-        """rc = (attention sample offset, own first global token row, row-sharded?)."""
-        sample_offset, row_offset, shard = rc
+        """rc = (attention sample offset, own first global token row, row-sharded?[, micro-batch,
+        full per-rank batch]) -- the last two for the overlapped micro-batches of tp_exchange="overlap"."""
+        sample_offset, row_offset, shard = rc[:3]
+        mb, mb_batch = (rc[3], rc[4]) if len(rc) > 3 else (-1, 0)
         T = STATE.tp_size
         hl = self.num_attention_heads // T
         return L.LayerMeta(hidden=self.hidden_size, heads_local=hl, heads_global=self.num_attention_heads,
@@ -180,7 +182,7 @@ class _LayerBase(DistributedModule):
                            post_ln=self.post_layernorm, activation=self.activation, layer_id=self.layer_id,
                            seed=STATE.seed, rng=STATE.rng_cur, grad=torch.is_grad_enabled(), head_offset=STATE.tp_rank * hl,
                            sample_offset=sample_offset, tp_size=T, row_offset=row_offset, shard_rows=shard,
-                           comm=STATE.config.get("tp_comm", "peer"))
+                           comm=STATE.config.get("tp_comm", "peer"), mb=mb, mb_batch=mb_batch)
 
     def _ln_params(self, prefix):
         H = self.hidden_size // STATE.tp_size if self._memory else self.hidden_size  # memory: channel chunk
@@ -311,6 +313,16 @@ class DistributedTransformerOutputLayer(_LayerBase):
                 getattr(self, f"{where}_ln_bias").copy_(p[f"mlp_{where}_ln_b"][ln_sl])
 
 
+_MB_STREAM: dict = {}
+
+
+def _microbatch_stream() -> torch.cuda.Stream:
+    dev = torch.cuda.current_device()
+    if dev not in _MB_STREAM:
+        _MB_STREAM[dev] = torch.cuda.Stream(device=dev)
+    return _MB_STREAM[dev]
+
+
 def _memory_mode() -> bool:
     return STATE.optimize == "memory" and STATE.tp_size > 1
 
@@ -418,10 +430,50 @@ class DistributedTransformer(DistributedModule):
         if getattr(self, "_ckpt_groups", None):  # smp.set_activation_checkpointing
             from .checkpointing import run_stack
             return run_stack(self, X, mask, rc)
+        if self._split_microbatches(X, rc):
+            return self._sublayer_microbatches(X, mask, rc)
         n = len(self.seq_layers)
         for i, layer in enumerate(self.seq_layers):
             X = layer.sublayer(X, mask, rc, push_last=i + 1 < n)
         return X
+
+    def _split_microbatches(self, X, rc) -> bool:
+        """tp_exchange="overlap": row-sharded speed mode with an even per-rank batch whose halves
+        are whole 128-row GEMM tiles and fused attention."""
+        if not (rc[2] and STATE.config.get("tp_exchange", "barrier") == "overlap" and STATE.tp_size > 1
+                and STATE.config.get("tp_comm", "peer") == "peer"):
+            return False
+        B, s = X.shape[0], X.shape[1]
+        lay = self.seq_layers[0].attention
+        return B % 2 == 0 and (B // 2) * s % 128 == 0 and L.use_flash(s, lay.attention_head_size)
+
+    def _sublayer_microbatches(self, X, mask, rc):
+        """The batch as two micro-batches on two streams, layer by layer in lock step: while one
+        micro-batch's gathers and reduce-scatters move on the copy engines, the other's GEMMs and
+        attention run (PAPER.md:281 TP across DP; exchange.py mailboxes).  Dropout masks and row
+        coordinates are those of the whole batch, so the result equals the unsplit stack's."""
+        B, s = X.shape[0], X.shape[1]
+        b, T = B // 2, STATE.tp_size
+        pool = get_pool()
+        if STATE.xch_fresh:  # step entry: every rank is done with the previous step's regions
+            pool.barrier()
+            STATE.xch_fresh = False
+        main = torch.cuda.current_stream()
+        side = _microbatch_stream()
+        side.wait_stream(main)
+        xs = [X[:b], X[b:]]
+        masks = [None, None] if mask is None else \
+            [mask.reshape(T, B, s)[:, h * b:(h + 1) * b].reshape(T * b, s) for h in (0, 1)]
+        rcs = [(rc[0], rc[1] + h * b * s, True, h, B) for h in (0, 1)]
+        streams = (main, side)
+        n = len(self.seq_layers)
+        for i, layer in enumerate(self.seq_layers):
+            for h in (0, 1):
+                with torch.cuda.stream(streams[h]):
+                    xs[h] = layer.sublayer(xs[h], masks[h], rcs[h], push_last=i + 1 < n)
+        main.wait_stream(side)
+        xs[1].record_stream(main)
+        return torch.cat(xs, 0)
 
     def forward(self, hidden_states, attention_mask=None):
         return _run_standalone(self, hidden_states, attention_mask)

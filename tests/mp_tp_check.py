@@ -289,6 +289,12 @@ def main():
         run_case(smp, "stack3_peer_post_ln", prescaled=False, causal=False, pre=False, post=True, p=0.1, layers=3),
         run_case(smp, "stack3_peer_post_ln_barrier_exchange", prescaled=False, causal=False, pre=False, post=True,
                  p=0.1, layers=3, exchange="barrier"),
+        run_case(smp, "stack3_peer_post_ln_overlap_exchange", prescaled=False, causal=False, pre=False, post=True,
+                 p=0.1, layers=3, exchange="overlap"),
+        run_case(smp, "stack2_pre_ln_causal_overlap_exchange", prescaled=False, causal=True, pre=True, post=False,
+                 p=0.1, layers=2, exchange="overlap"),
+        run_case(smp, "layer_both_ln_overlap_exchange", prescaled=False, causal=False, pre=True, post=True, p=0.1,
+                 exchange="overlap"),
         run_case(smp, "stack2_peer_wgrad_overlap", prescaled=False, causal=False, pre=False, post=True, p=0.1,
                  layers=2, overlap=64),
         run_case(smp, "stack2_overlap_pre_ln", prescaled=False, causal=True, pre=True, post=False, p=0.1, layers=2,
