@@ -259,6 +259,13 @@ SMPK_API int smpk_flash_attn_fwd(const void* qkv, int64_t ld, int B, int nh, int
 SMPK_API int smpk_attn_dropout_bits(int B, int nh, int sq, int sk, float p_drop, uint64_t seed, const uint64_t* rng_step, int layer,
                                     int64_t sample_offset, int head_offset, int nh_global, uint32_t* bits,
                                     int causal, void* stream);
+/* ... with the B samples in blocks of sample_block consecutive global samples, block_stride apart
+ * (sample b -> sample_offset + (b / sample_block) * block_stride + b % sample_block): the
+ * rank-major gathered samples of one overlapped micro-batch (tp_exchange = "overlap"). */
+SMPK_API int smpk_attn_dropout_bits_blocked(int B, int nh, int sq, int sk, float p_drop, uint64_t seed,
+                                            const uint64_t* rng_step, int layer, int64_t sample_offset,
+                                            int sample_block, int64_t block_stride, int head_offset, int nh_global,
+                                            uint32_t* bits, int causal, void* stream);
 
 /*
  * smpk_flash_attn_bwd — backward of smpk_flash_attn_fwd: from dout (grad of out, same layout),

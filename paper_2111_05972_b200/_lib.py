@@ -42,6 +42,7 @@ SIGNATURES: dict[str, list] = {
     "smpk_vocab_ce_bwd": [P, L, L, I, L, L, P, L, P, P, F, P, L, P],
     "smpk_flash_attn_fwd": [P, L, I, I, I, I, P, L, P, P, F, I, F, P, P],
     "smpk_attn_dropout_bits": [I, I, I, I, F, C.c_uint64, P, I, L, I, I, P, I, P],
+    "smpk_attn_dropout_bits_blocked": [I, I, I, I, F, C.c_uint64, P, I, L, I, L, I, I, P, I, P],
     "smpk_flash_attn_bwd": [P, L, P, L, P, L, P, I, I, I, I, P, P, F, I, F, P, P, L, P],
     "smpk_gemm_rs": [P, I, L, P, I, L, P, I, L, L, L, I, I, I, P],
     "smpk_bdr_ln_fwd_ex": [P, I, L, P, P, P, P, P, P, P, P, P, I, L, I, I, F, F, C.c_uint64, P, I, I, L, P, P, L, P],

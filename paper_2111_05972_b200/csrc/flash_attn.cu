@@ -408,12 +408,15 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
 
 // Attention-probability dropout keep bits (site 0 of the Philox scheme, oracle/philox.py):
 // word ((b*nh + h)*sq + q)*(sk/32) + k/32, bit k%32 = keep(row = (gs*nh_global + gh)*sq + q,
-// col = k) with gs = sample_offset + b, gh = head_offset + h.  One thread per word
+// col = k) with gs = sample_offset + (b / sample_block) * block_stride + b % sample_block (blocks of
+// sample_block consecutive samples block_stride apart: an overlapped micro-batch's rank-major
+// gathered samples), gh = head_offset + h.  One thread per word
 // (4 Philox4x32-10 calls = 32 keys).
 __global__ void __launch_bounds__(128) attn_dropout_bits_kernel(int nh, int sq, int wpr, uint32_t thresh,
                                                                 uint64_t seed, const uint64_t* rng_step,
                                                                 uint32_t layer,
-                                                                int64_t sample_offset, int head_offset, int nh_global,
+                                                                int64_t sample_offset, int sample_block,
+                                                                int64_t block_stride, int head_offset, int nh_global,
                                                                 uint32_t* __restrict__ bits, int causal) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // (q, w) of this (b, h)
   if (idx >= sq * wpr) return;
@@ -423,7 +426,8 @@ __global__ void __launch_bounds__(128) attn_dropout_bits_kernel(int nh, int sq, 
   const int bh = blockIdx.y;
   const int q = idx / wpr, w = idx - q * wpr;
   const int h = bh % nh, b = bh / nh;
-  const uint64_t grow = (uint64_t)(((sample_offset + b) * nh_global + head_offset + h) * (int64_t)sq + q);
+  const int64_t gs = sample_offset + (int64_t)(b / sample_block) * block_stride + b % sample_block;
+  const uint64_t grow = (uint64_t)((gs * nh_global + head_offset + h) * (int64_t)sq + q);
   uint32_t word = 0;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
@@ -439,19 +443,29 @@ __global__ void __launch_bounds__(128) attn_dropout_bits_kernel(int nh, int sq, 
 
 using namespace smpk;
 
-extern "C" int smpk_attn_dropout_bits(int B, int nh, int sq, int sk, float p_drop, uint64_t seed,
-                                      const uint64_t* rng_step, int layer,
-                                      int64_t sample_offset, int head_offset, int nh_global, uint32_t* bits,
-                                      int causal, void* stream) {
+extern "C" int smpk_attn_dropout_bits_blocked(int B, int nh, int sq, int sk, float p_drop, uint64_t seed,
+                                              const uint64_t* rng_step, int layer, int64_t sample_offset,
+                                              int sample_block, int64_t block_stride, int head_offset, int nh_global,
+                                              uint32_t* bits, int causal, void* stream) {
   SMPK_REQUIRE(B > 0 && nh > 0 && sq > 0 && sk > 0 && sk % 32 == 0 && bits, SMPK_ERR_BAD_ARG,
                "smpk_attn_dropout_bits: bad arguments (sk must be a multiple of 32)");
   SMPK_REQUIRE(p_drop >= 0.f && p_drop < 1.f, SMPK_ERR_BAD_ARG, "smpk_attn_dropout_bits: p in [0,1)");
   SMPK_REQUIRE((int64_t)B * nh < 65536, SMPK_ERR_UNSUPPORTED, "smpk_attn_dropout_bits: B*nh must be < 65536");
+  SMPK_REQUIRE(sample_block > 0, SMPK_ERR_BAD_ARG, "smpk_attn_dropout_bits: sample_block must be > 0");
   const int wpr = sk / 32;
   dim3 grid((unsigned)((sq * wpr + 127) / 128), (unsigned)(B * nh));
   attn_dropout_bits_kernel<<<grid, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      nh, sq, wpr, dropout_threshold(p_drop), seed, rng_step, (uint32_t)layer, sample_offset, head_offset, nh_global, bits, causal);
+      nh, sq, wpr, dropout_threshold(p_drop), seed, rng_step, (uint32_t)layer, sample_offset, sample_block,
+      block_stride, head_offset, nh_global, bits, causal);
   return check_launch("smpk_attn_dropout_bits");
+}
+
+extern "C" int smpk_attn_dropout_bits(int B, int nh, int sq, int sk, float p_drop, uint64_t seed,
+                                      const uint64_t* rng_step, int layer,
+                                      int64_t sample_offset, int head_offset, int nh_global, uint32_t* bits,
+                                      int causal, void* stream) {
+  return smpk_attn_dropout_bits_blocked(B, nh, sq, sk, p_drop, seed, rng_step, layer, sample_offset, B > 0 ? B : 1, 0,
+                                        head_offset, nh_global, bits, causal, stream);
 }
 
 extern "C" int smpk_flash_attn_fwd(const void* qkv, int64_t ld, int B, int nh, int s, int dh, void* out,

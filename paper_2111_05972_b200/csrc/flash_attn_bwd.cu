@@ -572,7 +572,12 @@ __global__ void __launch_bounds__(FB2_THREADS, 1)
     const uint32_t pdt = smem_u32(smem + Cfg::OFF_PDT), dst = smem_u32(smem + Cfg::OFF_DST);
     const uint32_t tdV = tmem + Cfg::COL_DV, tdK = tmem + Cfg::COL_DK, tdQ = tmem + Cfg::COL_DQ;
     auto stage_base = [&](int t) { return smem_u32(smem + Cfg::OFF_STAGE + (t % NQ) * Cfg::STAGE_BYTES); };
-    auto issue_s = [&](int t) {  // S(t) = Q_t K^T -> A[t % NA]
+    // TMEM: with NA == 2 (dh 64) S(t) always lands in A0 and dP(t) in A1, so the next tile's S is
+    // computed during this tile's dS pass and the next dP during the next P pass -- neither pass
+    // waits on an MMA.  With NA == 1 (dh 128: no room for a second 128-column buffer) S and dP
+    // share A.  In both, dK(t) is issued before waiting for the previous dQ drain and the Q / dO
+    // stage is released right after it, so the next tile's loads overlap that drain.
+    auto issue_s = [&](int t) {  // S(t) = Q_t K^T -> A0
       mbar_wait(&qdo_full[t % NQ], (t / NQ) & 1);
       tc_fence_after();
       const uint32_t qb = stage_base(t) + Cfg::ST_Q;
@@ -581,46 +586,59 @@ __global__ void __launch_bounds__(FB2_THREADS, 1)
         for (int c = 0; c < DH / 64; ++c)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            umma_bf16(tmem + (t % NA) * 128, make_sw128_desc(qb + c * 16384 + k * 32, 16, 1024),
+            umma_bf16(tmem, make_sw128_desc(qb + c * 16384 + k * 32, 16, 1024),
                       make_sw128_desc(k_base + c * 16384 + k * 32, 16, 1024), idQK, (c | k) != 0);
-        umma_commit(&s_full[t % NA]);
+        umma_commit(&s_full[0]);
+      }
+      __syncwarp();
+    };
+    auto issue_dp = [&](int t) {  // dP(t) = dO_t V^T -> A[NA - 1] (stage t already waited by issue_s)
+      const uint32_t dob = stage_base(t) + Cfg::ST_DO;
+      if (elect_one()) {
+#pragma unroll
+        for (int c = 0; c < DH / 64; ++c)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(tmem + (NA - 1) * 128, make_sw128_desc(dob + c * 16384 + k * 32, 16, 1024),
+                      make_sw128_desc(v_base + c * 16384 + k * 32, 16, 1024), idQK, (c | k) != 0);
+        umma_commit(dp_full);
       }
       __syncwarp();
     };
     mbar_wait(kv_full, 0);
     if (trc && lane == 0) trc[1] = gtime_b();
-    if (nt > 0) issue_s(0);
+    if (nt > 0) {
+      issue_s(0);
+      if (NA == 2) issue_dp(0);
+    }
     for (int t = 0; t < nt; ++t) {
-      const uint32_t tA = tmem + (t % NA) * 128;
       const uint32_t dob = stage_base(t) + Cfg::ST_DO, qb = stage_base(t) + Cfg::ST_Q;
-      // the next tile's scores while this tile is in its softmax passes (its A buffer's dP was
-      // consumed by tile t-1's dS pass, waited below in the previous iteration)
-      if (NA == 2 && t + 1 < nt) issue_s(t + 1);
       mbar_wait(p_full, t & 1);  // Pd(t) in smem; S(t) read
       tc_fence_after();
-      if (elect_one()) {  // dV += Pd^T dO ; dP = dO V^T -> A[t % NA]
+      if (elect_one()) {  // dV += Pd^T dO
 #pragma unroll
         for (int k = 0; k < 8; ++k)
           umma_bf16(tdV, make_sw128_desc(pdt + k * 2048, 16384, 1024), make_sw128_desc(dob + k * 2048, 16384, 1024),
                     idTM, (t > 0) || (k != 0));
         umma_commit(pdt_free);
-#pragma unroll
-        for (int c = 0; c < DH / 64; ++c)
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_bf16(tA, make_sw128_desc(dob + c * 16384 + k * 32, 16, 1024),
-                      make_sw128_desc(v_base + c * 16384 + k * 32, 16, 1024), idQK, (c | k) != 0);
-        umma_commit(dp_full);
       }
       __syncwarp();
+      if (NA == 1) issue_dp(t);                // A is free once S(t) was read
+      else if (t + 1 < nt) issue_s(t + 1);     // A0 is free: the next scores during this dS pass
       mbar_wait(ds_full, t & 1);  // dS(t) in smem; dP(t) read
-      if (t > 0) mbar_wait(dq_free, (t - 1) & 1);  // dQ(t-1) drained
       tc_fence_after();
-      if (elect_one()) {  // dK += dS^T Q ; dQ = dS K
+      if (elect_one()) {  // dK += dS^T Q, then the Q / dO stage can be refilled
 #pragma unroll
         for (int k = 0; k < 8; ++k)
           umma_bf16(tdK, make_sw128_desc(dst + k * 2048, 16384, 1024), make_sw128_desc(qb + k * 2048, 16384, 1024),
                     idTM, (t > 0) || (k != 0));
+        umma_commit(&qdo_empty[t % NQ]);
+      }
+      __syncwarp();
+      if (NA == 2 && t + 1 < nt) issue_dp(t + 1);  // A1 is free once dP(t) was read
+      if (t > 0) mbar_wait(dq_free, (t - 1) & 1);  // dQ(t-1) drained
+      tc_fence_after();
+      if (elect_one()) {  // dQ = dS K
 #pragma unroll
         for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
@@ -629,11 +647,10 @@ __global__ void __launch_bounds__(FB2_THREADS, 1)
                       make_sw128_desc(k_base + kb * 8192 + k * 2048, 16384, 1024), idKM, (kb | k) != 0);
         umma_commit(dq_full);
         umma_commit(dst_free);
-        umma_commit(&qdo_empty[t % NQ]);
         if (t == nt - 1) umma_commit(kv_done);
       }
       __syncwarp();
-      if (NA == 1 && t + 1 < nt) issue_s(t + 1);
+      if (NA == 1 && t + 1 < nt) issue_s(t + 1);  // A is free once dP(t) was read
     }
   } else if (warp >= 4 && warp < 12) {
     // ---------------- softmax backward: query row qr = TMEM lane, 64 keys per warp ----------------
@@ -666,10 +683,11 @@ __global__ void __launch_bounds__(FB2_THREADS, 1)
         kw0 = w.x;
         kw1 = w.y;
       }
-      mbar_wait(&s_full[t % NA], (t / NA) & 1);
+      mbar_wait(&s_full[0], t & 1);
       if (e == 0) FB_TR(2);
       tc_fence_after();
-      const uint32_t tA = tmem + (t % NA) * 128 + t_lane + qh * 64;
+      const uint32_t tA = tmem + t_lane + qh * 64;               // S(t)
+      const uint32_t tP = tmem + (NA - 1) * 128 + t_lane + qh * 64;  // dP(t)
       // ---- P pass: P (bf16, kept for dS) and Pd = keep ? P : 0 -> smem
       uint32_t pp[32];
       uint32_t sv[64];
@@ -718,8 +736,8 @@ __global__ void __launch_bounds__(FB2_THREADS, 1)
       mbar_wait(dp_full, t & 1);
       if (e == 0) FB_TR(10);
       tc_fence_after();
-      tmem_ld_32x32b_x32(tA, *reinterpret_cast<uint32_t(*)[32]>(sv));
-      tmem_ld_32x32b_x32(tA + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+      tmem_ld_32x32b_x32(tP, *reinterpret_cast<uint32_t(*)[32]>(sv));
+      tmem_ld_32x32b_x32(tP + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
       tmem_ld_wait();
       if (t > 0) mbar_wait(dst_free, (t - 1) & 1);  // dK / dQ(t-1) have read dS
 #pragma unroll
@@ -814,70 +832,38 @@ __global__ void __launch_bounds__(FB2_THREADS, 1)
         float* v = reinterpret_cast<float*>(o);
 #pragma unroll
         for (int q = 0; q < 64; ++q) v[q] = __uint_as_float(o[q]) * a.scale;
+        float* grow = a.dq_part + (int64_t)(row0 + rr) * a.H + (int64_t)h * DH + hf * 64;
+        if (!my_turn) {  // every drain thread waits for the earlier contributors (issuer polls)
+          if (issuer) {
+            while (ld_acquire_gpu(cnt) != t) __nanosleep(32);
+          }
+          named_barrier_sync(3, 128);
+          __threadfence();
+          my_turn = true;
+        }
         if (!lastc) {
+          // this thread's query row straight from registers: the first contributor stores, later
+          // ones add in L2 (red.global.add.v4.f32), one contributor at a time -> a fixed order
 #pragma unroll
-          for (int g0 = 0; g0 < 2; g0 += Cfg::SG) {
-#pragma unroll
-            for (int gg = 0; gg < Cfg::SG; ++gg) {
-              uint8_t* box = dqs + gg * 16384 + rr * 128;
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                const float* src = v + (g0 + gg) * 32 + q * 4;
-                *reinterpret_cast<float4*>(box + ((q ^ (rr & 7)) << 4)) = make_float4(src[0], src[1], src[2], src[3]);
-              }
-            }
-            fence_proxy_async_smem();
-            named_barrier_sync(3, 128);
-            if (issuer) {
-              if (!my_turn) {
-                while (ld_acquire_gpu(cnt) != t) __nanosleep(32);
-                fence_proxy_async_global();
-                my_turn = true;
-              }
-#pragma unroll
-              for (int gg = 0; gg < Cfg::SG; ++gg) {
-                const int c0 = h * DH + hf * 64 + (g0 + gg) * 32;
-                if (firstc)
-                  tma_store_2d(&tmDQ, dqs + gg * 16384, c0, row0);
-                else
-                  tma_reduce_add_2d(&tmDQ, dqs + gg * 16384, c0, row0);
-              }
-              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-              asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging reusable
-            }
-            named_barrier_sync(3, 128);
+          for (int q = 0; q < 16; ++q) {
+            if (firstc)
+              asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(grow + q * 4), "f"(v[q * 4]),
+                           "f"(v[q * 4 + 1]), "f"(v[q * 4 + 2]), "f"(v[q * 4 + 3])
+                           : "memory");
+            else
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(grow + q * 4), "f"(v[q * 4]),
+                           "f"(v[q * 4 + 1]), "f"(v[q * 4 + 2]), "f"(v[q * 4 + 3])
+                           : "memory");
           }
         } else {
           if (!firstc) {  // add the earlier key tiles' sum
 #pragma unroll
-            for (int g0 = 0; g0 < 2; g0 += Cfg::SG) {
-              if (issuer) {
-                if (!my_turn) {
-                  while (ld_acquire_gpu(cnt) != t) __nanosleep(32);
-                  fence_proxy_async_global();
-                  my_turn = true;
-                }
-                mbar_arrive_expect_tx(dqa_full, Cfg::SG * 16384);
-#pragma unroll
-                for (int gg = 0; gg < Cfg::SG; ++gg)
-                  tma_load_4d(dqs + gg * 16384, &tmDQ, dqa_full, h * DH + hf * 64 + (g0 + gg) * 32, row0, 0, 0);
-              }
-              mbar_wait(dqa_full, dqa_phase);
-              dqa_phase ^= 1;
-#pragma unroll
-              for (int gg = 0; gg < Cfg::SG; ++gg) {
-                const uint8_t* box = dqs + gg * 16384 + rr * 128;
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                  const float4 s4 = *reinterpret_cast<const float4*>(box + ((q ^ (rr & 7)) << 4));
-                  float* dv = v + (g0 + gg) * 32 + q * 4;
-                  dv[0] = s4.x + dv[0];
-                  dv[1] = s4.y + dv[1];
-                  dv[2] = s4.z + dv[2];
-                  dv[3] = s4.w + dv[3];
-                }
-              }
-              named_barrier_sync(3, 128);  // staging read by every drain thread
+            for (int q = 0; q < 16; ++q) {
+              const float4 s4 = __ldcg(reinterpret_cast<const float4*>(grow + q * 4));
+              v[q * 4] = s4.x + v[q * 4];
+              v[q * 4 + 1] = s4.y + v[q * 4 + 1];
+              v[q * 4 + 2] = s4.z + v[q * 4 + 2];
+              v[q * 4 + 3] = s4.w + v[q * 4 + 3];
             }
           }
           bf16* dqrow = a.dqkv + (int64_t)(row0 + rr) * a.ld + (int64_t)h * DH + hf * 64;
@@ -892,11 +878,12 @@ __global__ void __launch_bounds__(FB2_THREADS, 1)
           }
         }
       }
+      if (!lastc) {  // every thread's adds are performed before the release
+        __threadfence();
+        named_barrier_sync(3, 128);
+      }
       if (issuer) {
         if (!lastc) {  // release the tile to the next key tile: our adds are complete in L2
-          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-          fence_proxy_async_global();
-          __threadfence();
           st_release_gpu(cnt, t + 1);
         } else if (!firstc) {
           *cnt = 0;  // every contributor is done: reset for the next launch / graph replay

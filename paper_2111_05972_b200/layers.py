@@ -178,11 +178,10 @@ def _keep_bits_async(B: int, s: int, m: LayerMeta, device):
                                   out=bits, causal=m.causal and s % 128 == 0)
         else:  # micro-batch mb: rank j's samples [mb*b, (mb+1)*b) of its mb_batch, rank-major
             b = B // m.tp_size
-            for j in range(m.tp_size):
-                ops.attn_dropout_bits(b, m.heads_local, s, s, p=m.p_attn, seed=m.seed, rng=m.rng, layer=m.layer_id,
-                                      sample_offset=m.sample_offset + j * m.mb_batch + m.mb * b,
-                                      head_offset=m.head_offset, nh_global=m.heads_global,
-                                      out=bits[j * b:(j + 1) * b], causal=m.causal and s % 128 == 0)
+            ops.attn_dropout_bits(B, m.heads_local, s, s, p=m.p_attn, seed=m.seed, rng=m.rng, layer=m.layer_id,
+                                  sample_offset=m.sample_offset + m.mb * b, sample_block=b, block_stride=m.mb_batch,
+                                  head_offset=m.head_offset, nh_global=m.heads_global, out=bits,
+                                  causal=m.causal and s % 128 == 0)
     return bits, (lambda: main.wait_stream(side))
 
 

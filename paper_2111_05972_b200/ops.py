@@ -144,17 +144,25 @@ def colsum(x: torch.Tensor, *, out_dtype=None) -> torch.Tensor:
 
 
 def attn_dropout_bits(B: int, nh: int, sq: int, sk: int, *, p: float, seed=0, rng=None, layer=0, sample_offset=0,
-                      head_offset=0, nh_global=None, device=None, out=None, causal=False) -> torch.Tensor | None:
+                      head_offset=0, nh_global=None, device=None, out=None, causal=False, sample_block=None,
+                      block_stride=0) -> torch.Tensor | None:
     """Keep bits [B, nh, sq, sk/32] (uint32 words as int32) of the attention-probability dropout;
-    None when p == 0.  Generated once per layer and shared by the forward and the backward."""
+    None when p == 0.  Generated once per layer and shared by the forward and the backward.
+    sample_block / block_stride: the B samples are blocks of sample_block consecutive global
+    samples block_stride apart (an overlapped micro-batch's gathered samples)."""
     if p <= 0.0:
         return None
     bits = out if out is not None else torch.empty(B, nh, sq, sk // 32, dtype=torch.int32,
                                                    device=device or torch.cuda.current_device())
     _check_cuda(bits)
-    _lib.call("smpk_attn_dropout_bits", B, nh, sq, sk, float(p), int(seed) & (2 ** 64 - 1), _ptr(rng), int(layer),
-              int(sample_offset), int(head_offset), int(nh_global if nh_global is not None else nh), _ptr(bits),
-              int(bool(causal)), _stream())
+    if sample_block is None:
+        _lib.call("smpk_attn_dropout_bits", B, nh, sq, sk, float(p), int(seed) & (2 ** 64 - 1), _ptr(rng),
+                  int(layer), int(sample_offset), int(head_offset), int(nh_global if nh_global is not None else nh),
+                  _ptr(bits), int(bool(causal)), _stream())
+    else:
+        _lib.call("smpk_attn_dropout_bits_blocked", B, nh, sq, sk, float(p), int(seed) & (2 ** 64 - 1), _ptr(rng),
+                  int(layer), int(sample_offset), int(sample_block), int(block_stride), int(head_offset),
+                  int(nh_global if nh_global is not None else nh), _ptr(bits), int(bool(causal)), _stream())
     return bits
 
 

@@ -131,3 +131,17 @@ def test_causal_keep_bits_cover_lower_triangle():
     need = (w <= q).expand(B, nh, s, s // 32)
     assert torch.equal(part[need], full[need])
     assert int(part[~need].abs().sum()) == 0
+
+
+def test_blocked_keep_bits_equal_whole_batch_slices():
+    """The overlapped micro-batch's bits (blocks of b samples, one per rank, stride = the rank's
+    batch) are exactly the corresponding samples of the whole gathered batch's bits."""
+    from paper_2111_05972_b200 import ops
+    T, Bfull, nh, s = 3, 4, 2, 128
+    b = Bfull // 2
+    whole = ops.attn_dropout_bits(T * Bfull, nh, s, s, p=0.1, seed=9, layer=4, sample_offset=8)
+    for mb in (0, 1):
+        got = ops.attn_dropout_bits(T * b, nh, s, s, p=0.1, seed=9, layer=4, sample_offset=8 + mb * b,
+                                    sample_block=b, block_stride=Bfull)
+        want = torch.cat([whole[j * Bfull + mb * b:j * Bfull + (mb + 1) * b] for j in range(T)], 0)
+        assert torch.equal(got, want)
