@@ -832,38 +832,70 @@ __global__ void __launch_bounds__(FB2_THREADS, 1)
         float* v = reinterpret_cast<float*>(o);
 #pragma unroll
         for (int q = 0; q < 64; ++q) v[q] = __uint_as_float(o[q]) * a.scale;
-        float* grow = a.dq_part + (int64_t)(row0 + rr) * a.H + (int64_t)h * DH + hf * 64;
-        if (!my_turn) {  // every drain thread waits for the earlier contributors (issuer polls)
-          if (issuer) {
-            while (ld_acquire_gpu(cnt) != t) __nanosleep(32);
-          }
-          named_barrier_sync(3, 128);
-          __threadfence();
-          my_turn = true;
-        }
         if (!lastc) {
-          // this thread's query row straight from registers: the first contributor stores, later
-          // ones add in L2 (red.global.add.v4.f32), one contributor at a time -> a fixed order
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            if (firstc)
-              asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(grow + q * 4), "f"(v[q * 4]),
-                           "f"(v[q * 4 + 1]), "f"(v[q * 4 + 2]), "f"(v[q * 4 + 3])
-                           : "memory");
-            else
-              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(grow + q * 4), "f"(v[q * 4]),
-                           "f"(v[q * 4 + 1]), "f"(v[q * 4 + 2]), "f"(v[q * 4 + 3])
-                           : "memory");
+          for (int g0 = 0; g0 < 2; g0 += Cfg::SG) {
+#pragma unroll
+            for (int gg = 0; gg < Cfg::SG; ++gg) {
+              uint8_t* box = dqs + gg * 16384 + rr * 128;
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const float* src = v + (g0 + gg) * 32 + q * 4;
+                *reinterpret_cast<float4*>(box + ((q ^ (rr & 7)) << 4)) = make_float4(src[0], src[1], src[2], src[3]);
+              }
+            }
+            fence_proxy_async_smem();
+            named_barrier_sync(3, 128);
+            if (issuer) {
+              if (!my_turn) {
+                while (ld_acquire_gpu(cnt) != t) __nanosleep(32);
+                fence_proxy_async_global();
+                my_turn = true;
+              }
+#pragma unroll
+              for (int gg = 0; gg < Cfg::SG; ++gg) {
+                const int c0 = h * DH + hf * 64 + (g0 + gg) * 32;
+                if (firstc)
+                  tma_store_2d(&tmDQ, dqs + gg * 16384, c0, row0);
+                else
+                  tma_reduce_add_2d(&tmDQ, dqs + gg * 16384, c0, row0);
+              }
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+              asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging reusable
+            }
+            named_barrier_sync(3, 128);
           }
         } else {
           if (!firstc) {  // add the earlier key tiles' sum
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              const float4 s4 = __ldcg(reinterpret_cast<const float4*>(grow + q * 4));
-              v[q * 4] = s4.x + v[q * 4];
-              v[q * 4 + 1] = s4.y + v[q * 4 + 1];
-              v[q * 4 + 2] = s4.z + v[q * 4 + 2];
-              v[q * 4 + 3] = s4.w + v[q * 4 + 3];
+            for (int g0 = 0; g0 < 2; g0 += Cfg::SG) {
+              if (issuer) {
+                if (!my_turn) {
+                  while (ld_acquire_gpu(cnt) != t) __nanosleep(32);
+                  fence_proxy_async_global();
+                  my_turn = true;
+                }
+                mbar_arrive_expect_tx(dqa_full, Cfg::SG * 16384);
+#pragma unroll
+                for (int gg = 0; gg < Cfg::SG; ++gg)
+                  tma_load_4d(dqs + gg * 16384, &tmDQ, dqa_full, h * DH + hf * 64 + (g0 + gg) * 32, row0, 0, 0);
+              }
+              mbar_wait(dqa_full, dqa_phase);
+              dqa_phase ^= 1;
+#pragma unroll
+              for (int gg = 0; gg < Cfg::SG; ++gg) {
+                const uint8_t* box = dqs + gg * 16384 + rr * 128;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                  const float4 s4 = *reinterpret_cast<const float4*>(box + ((q ^ (rr & 7)) << 4));
+                  float* dv = v + (g0 + gg) * 32 + q * 4;
+                  dv[0] = s4.x + dv[0];
+                  dv[1] = s4.y + dv[1];
+                  dv[2] = s4.z + dv[2];
+                  dv[3] = s4.w + dv[3];
+                }
+              }
+              named_barrier_sync(3, 128);  // staging read by every drain thread
             }
           }
           bf16* dqrow = a.dqkv + (int64_t)(row0 + rr) * a.ld + (int64_t)h * DH + hf * 64;
@@ -878,12 +910,11 @@ __global__ void __launch_bounds__(FB2_THREADS, 1)
           }
         }
       }
-      if (!lastc) {  // every thread's adds are performed before the release
-        __threadfence();
-        named_barrier_sync(3, 128);
-      }
       if (issuer) {
         if (!lastc) {  // release the tile to the next key tile: our adds are complete in L2
+          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+          fence_proxy_async_global();
+          __threadfence();
           st_release_gpu(cnt, t + 1);
         } else if (!firstc) {
           *cnt = 0;  // every contributor is done: reset for the next launch / graph replay

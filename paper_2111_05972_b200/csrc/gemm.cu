@@ -900,16 +900,6 @@ static bool pair_splitk() {
   return v == 1;
 }
 
-// SMPK_GEMM_BN128_FILL=1: under-filled pair plans use 128-wide tiles (A/B measurements)
-static bool bn128_fill() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SMPK_GEMM_BN128_FILL");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
-
 static int pick_bn(int N) { return N <= 64 ? 64 : (N <= 128 ? 128 : 256); }
 
 // Tile plan: CTA pairs (256-row tiles, cta_group::2) whenever N >= 128 and M >= 256, else
@@ -921,12 +911,6 @@ static void plan_gemm(int M, int N, int K, int nb1, int nb2, int& BN, bool& pair
   const int rows = pair ? 2 * BM : BM;
   tiles = ((M + rows - 1) / rows) * ((N + BN - 1) / BN) * nb1 * nb2;
   num_kb = (K + BK - 1) / BK;
-  if (bn128_fill() && pair && BN == 256 && tiles < gemm_sms() / 2) {
-    // too few 256-wide pair tiles to fill the SMs (long-K weight gradients at T > 1): halve the
-    // tile width before resorting to split-K
-    BN = 128;
-    tiles = ((M + rows - 1) / rows) * ((N + BN - 1) / BN) * nb1 * nb2;
-  }
   splits = choose_splits(tiles, num_kb, BN, pair ? gemm_sms() / 2 : gemm_sms(), pair ? 2 : 1);
   if (pair && splits > 1 && !pair_splitk()) {
     // measured: split-K runs faster on single-CTA tiles (finer units, shorter fix-up)
