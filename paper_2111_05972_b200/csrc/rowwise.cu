@@ -1156,6 +1156,215 @@ static int64_t ln_bwd_grid(int M, int H) {
 
 extern "C" int64_t smpk_ln_bwd_workspace(int M, int H) { return ln_bwd_grid(M, H) * 3 * (int64_t)H * 4; }
 
+
+// ===========================================================================
+// Pipelined LayerNorm / dropout backward (local rows): the fast path of smpk_ln_bwd
+// ===========================================================================
+// One persistent CTA per SM.  Warp 0 streams each row's inputs (dy, r, dres, keep bytes) into a
+// deep shared-memory ring with cp.async.bulk, so ~150-200 KB of rows are in flight per SM instead
+// of the few rows the register kernel holds; 16 consumer warps form groups of W warps (one row
+// per group at a time, the lane layout and column accumulators of ln_bwd_kernel), read their
+// row from shared memory, and the groups' column partials are summed in ascending group order
+// (deterministic) into this CTA's partial row of the workspace.
+// consumer warps: 12 (13 warps allocate registers like 16 -> 128 per thread, no spills), 8 at W = 8
+__host__ __device__ constexpr int lnb_cw(int W) { return W == 8 ? 8 : 12; }
+
+template <int W, int VPT>
+__global__ void __launch_bounds__(32 * (lnb_cw(W) + 1), 1) ln_bwd_pipe_kernel(const LnBwdArgs a, int nst, int sb) {
+  constexpr int LNB_CW = lnb_cw(W);
+  constexpr int G = LNB_CW / W;  // row groups
+  const uint64_t pkey = philox_key(a.seed, a.rng_step);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  const int H = a.H;
+  const bool has_ln = a.gamma != nullptr;
+  const int o_r = H * 2, o_dres = o_r + (has_ln ? H * 2 : 0), o_keep = o_dres + (a.dres ? H * 2 : 0);
+  const int in_bytes = o_keep + (a.keep_in ? H / 8 : 0);
+  float* red = reinterpret_cast<float*>(smem + nst * sb);  // [W][VPT*8][32] flush buffer
+  float* sm = red + W * VPT * 8 * 32;                        // [2][LNB_CW] group sums
+  bf16* gam = reinterpret_cast<bf16*>(sm + 2 * LNB_CW);     // gamma [H]
+  uint64_t* full = reinterpret_cast<uint64_t*>(gam + H);
+  uint64_t* empty = full + nst;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nst; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], W);  // every warp of the owning group releases it
+    }
+    fence_barrier_init();
+  }
+  if (has_ln)
+    for (int i = threadIdx.x * 8; i < H; i += blockDim.x * 8)
+      *reinterpret_cast<uint4*>(gam + i) = *reinterpret_cast<const uint4*>(a.gamma + i);
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int row = blockIdx.x; row < a.M; row += gridDim.x, ++it) {
+        const int st = it % nst;
+        mbar_wait(&empty[st], ((it / nst) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[st], in_bytes);
+        uint8_t* dst = smem + st * sb;
+        const int64_t ro = (int64_t)row * H;
+        bulk_load(dst, a.dy + ro, H * 2, &full[st]);
+        if (has_ln) bulk_load(dst + o_r, a.r + ro, H * 2, &full[st]);
+        if (a.dres) bulk_load(dst + o_dres, a.dres + ro, H * 2, &full[st]);
+        if (a.keep_in) bulk_load(dst + o_keep, a.keep_in + (int64_t)row * (H / 8), H / 8, &full[st]);
+      }
+    }
+    return;
+  }
+  const int c = warp - 1, grp = c / W, wi = c % W;
+  const float inv_keep = a.p > 0.f ? 1.f / (1.f - a.p) : 1.f;
+  float acc_g[VPT][8], acc_b[VPT][8], acc_d[VPT][8];
+#pragma unroll
+  for (int i = 0; i < VPT; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc_g[i][j] = acc_b[i][j] = acc_d[i][j] = 0.f;
+  int it = grp;
+  for (int row = blockIdx.x + grp * gridDim.x; row < a.M; row += G * gridDim.x, it += G) {
+    const int st = it % nst;
+    const float mu = has_ln ? a.mean[row] : 0.f, rs = has_ln ? a.rstd[row] : 0.f;
+    mbar_wait(&full[st], (it / nst) & 1);
+    const uint8_t* buf = smem + st * sb;
+    // pass 1 (LayerNorm): row sums of g = dy*gamma and g*xhat, column sums of dy*xhat and dy
+    float m1 = 0.f, m2 = 0.f;
+    if (has_ln) {
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int i = 0; i < VPT; ++i) {
+        const int col = ((i * W + wi) * 32 + lane) * 8;
+        float dy[8], xh[8], gm[8];
+        load8(reinterpret_cast<const bf16*>(buf) + col, dy);
+        load8(reinterpret_cast<const bf16*>(buf + o_r) + col, xh);
+        load8(gam + col, gm);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          xh[j] = (xh[j] - mu) * rs;
+          const float gj = dy[j] * gm[j];
+          s1 += gj;
+          s2 += gj * xh[j];
+          acc_g[i][j] += dy[j] * xh[j];
+          acc_b[i][j] += dy[j];
+        }
+      }
+      m1 = group_sum<W>(s1, sm, grp, wi) / H;
+      m2 = group_sum<W>(s2, sm + LNB_CW, grp, wi) / H;
+    }
+    // pass 2: d = rs*(g - m1 - xhat*m2) (+ dres), dropout backward, stores (inputs re-read from smem)
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int col = ((i * W + wi) * 32 + lane) * 8;
+      float d[8];
+      load8(reinterpret_cast<const bf16*>(buf) + col, d);
+      if (has_ln) {
+        float xh[8], gm[8];
+        load8(reinterpret_cast<const bf16*>(buf + o_r) + col, xh);
+        load8(gam + col, gm);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) d[j] = rs * (d[j] * gm[j] - m1 - (xh[j] - mu) * rs * m2);
+      }
+      if (a.dres) {
+        float rr[8];
+        load8(reinterpret_cast<const bf16*>(buf + o_dres) + col, rr);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) d[j] += rr[j];
+      }
+      round8(d);
+      if (a.dr_out) store8(a.dr_out + (int64_t)row * H + col, d);
+      if (a.p > 0.f) {
+        bool keep[8];
+        if (a.keep_in)
+          keep8_from_byte(buf[o_keep + col / 8], keep);
+        else
+          dropout_keep8(pkey, a.layer, a.site, (uint64_t)(a.row_offset + row), col, dropout_threshold(a.p), keep);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) d[j] = keep[j] ? d[j] * inv_keep : 0.f;
+        round8(d);
+        store8(a.dsub_out + (int64_t)row * H + col, d);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc_d[i][j] += d[j];
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+  // column partials of the CTA: groups summed in ascending order through shared memory
+  float* out = a.partials + (int64_t)blockIdx.x * 3 * H;
+  float* rbuf = red + wi * (VPT * 8 * 32);
+  auto flush = [&](const float(&acc)[VPT][8], float* o) {
+    for (int sl = 0; sl < G; ++sl) {
+      if (grp == sl) {
+#pragma unroll
+        for (int i = 0; i < VPT; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float* dd = rbuf + (i * 8 + j) * 32 + lane;
+            *dd = (sl == 0) ? acc[i][j] : *dd + acc[i][j];
+          }
+      }
+      named_bar(15, LNB_CW * 32);
+    }
+    if (grp == G - 1) {
+#pragma unroll
+      for (int i = 0; i < VPT; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[((i * W + wi) * 32 + lane) * 8 + j] = rbuf[(i * 8 + j) * 32 + lane];
+    }
+    named_bar(15, LNB_CW * 32);
+  };
+  flush(acc_g, out);
+  flush(acc_b, out + H);
+  flush(acc_d, out + 2 * H);
+}
+
+static bool lnb_pipe_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SMPK_LNB_PIPE");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// Launches the pipelined backward when the call is a plain local one; returns -1 when it does not apply.
+static int ln_bwd_pipe_try(const LnBwdArgs& a, const RowGeom& geo, cudaStream_t st, int grid_limit) {
+  if (!lnb_pipe_enabled() || a.npeers || a.dy_peers || a.nslots != 1 || a.row_sums_out || a.ext_sums ||
+      a.col_offset || geo.W < 2 || a.H != geo.W * geo.VPT * 256 || a.M < 1)
+    return -1;
+  const uintptr_t al = reinterpret_cast<uintptr_t>(a.dy) | reinterpret_cast<uintptr_t>(a.r) |
+                       reinterpret_cast<uintptr_t>(a.dres) | reinterpret_cast<uintptr_t>(a.keep_in) |
+                       reinterpret_cast<uintptr_t>(a.dr_out) | reinterpret_cast<uintptr_t>(a.dsub_out);
+  if (al % 16) return -1;
+  const int H = a.H;
+  const int in_bytes = H * 2 + (a.gamma ? H * 2 : 0) + (a.dres ? H * 2 : 0) + (a.keep_in ? H / 8 : 0);
+  const int sb = (in_bytes + 127) / 128 * 128;
+  const int CW = lnb_cw(geo.W), G = CW / geo.W;
+  const int fixed = geo.W * geo.VPT * 8 * 32 * 4 + 2 * CW * 4 + H * 2 + 128;
+  int nst = (200 * 1024 - fixed) / (sb + 16);
+  if (nst > 48) nst = 48;
+  nst = nst / G * G;  // every stage owned by exactly one row group
+  if (nst < G) return -1;
+  const int smem = nst * sb + fixed + 2 * nst * 8;
+  int grid = row_sms();
+  if (grid > grid_limit) grid = grid_limit;
+  if (grid > a.M) grid = a.M;
+  switch (geo.W * 16 + geo.VPT) {
+#define SMPK_LNB_CASE(W_, V_)                                                                    \
+  case W_ * 16 + V_: {                                                                           \
+    static unsigned long long once = 0;                                                          \
+    smem_attr_once(ln_bwd_pipe_kernel<W_, V_>, 232448, once);                                    \
+    ln_bwd_pipe_kernel<W_, V_><<<grid, 32 * (lnb_cw(W_) + 1), smem, st>>>(a, nst, sb);          \
+    return grid;                                                                                 \
+  }
+    SMPK_LNB_CASE(2, 2) SMPK_LNB_CASE(4, 2) SMPK_LNB_CASE(8, 2) SMPK_LNB_CASE(2, 1) SMPK_LNB_CASE(4, 1)
+    SMPK_LNB_CASE(8, 1)
+#undef SMPK_LNB_CASE
+    default:
+      return -1;
+  }
+}
+
 static int ln_bwd_impl(const void* dy, int nslots, int64_t slot_stride, const void* r, const float* mean,
                        const float* rstd, const void* gamma, const void* dres, void* dr_out, void* dsub_out,
                        void* const* out_peers, int npeers, int64_t peer_off, void* dgamma, void* dbeta, void* dbias,
@@ -1187,13 +1396,17 @@ static int ln_bwd_impl(const void* dy, int nslots, int64_t slot_stride, const vo
               row_sums_out, ext_sums, H_total, keep_in, reinterpret_cast<const bf16* const*>(dy_peers), dy_peer_off};
   a.rng_step = rng_step;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const int red_bytes = geo.W == 8 ? 0 : geo.W * geo.VPT * 8 * 32 * 4;
-  SMPK_DISPATCH_ROW(geo.W, geo.VPT, ln_bwd_kernel, (grid, ROW_THREADS, red_bytes, st), (a));
+  int used_grid = ln_bwd_pipe_try(a, geo, st, grid);
+  if (used_grid < 0) {
+    const int red_bytes = geo.W == 8 ? 0 : geo.W * geo.VPT * 8 * 32 * 4;
+    SMPK_DISPATCH_ROW(geo.W, geo.VPT, ln_bwd_kernel, (grid, ROW_THREADS, red_bytes, st), (a));
+    used_grid = grid;
+  }
   int rc = check_launch("smpk_ln_bwd");
   if (rc) return rc;
   if (row_sums_out || (!dgamma && !dbeta && !dbias)) return SMPK_OK;
   dim3 rg((H + 31) / 32, 3);
-  colsum_reduce_launch(rg, reinterpret_cast<float*>(workspace), grid, 3, H, dgamma, dbeta, dbias, grads_f32,
+  colsum_reduce_launch(rg, reinterpret_cast<float*>(workspace), used_grid, 3, H, dgamma, dbeta, dbias, grads_f32,
                        accumulate, st);
   return check_launch("smpk_ln_bwd(reduce)");
 }
