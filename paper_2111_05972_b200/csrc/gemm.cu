@@ -972,7 +972,7 @@ static int gemm_prepare(const void* a, int a_mn_major, int64_t lda, int64_t a_bs
                         int64_t c_bs1, int64_t c_bs2, int M, int N, int K, int nb1, int nb2, float alpha, float beta,
                         int epilogue, int act, const void* bias, void* aux, int64_t ldaux, void* const* peers_host,
                         int npeers, int64_t rows_per_owner, int64_t peer_slot_off, void* workspace,
-                        int64_t workspace_bytes, float* colsum_part, bool grouped, CUtensorMap& ta, CUtensorMap& tb,
+                        int64_t workspace_bytes, float* colsum_part, int grouped, CUtensorMap& ta, CUtensorMap& tb,
                         EpiMaps& maps, GemmArgs& g, int& BN, bool& pair) {
   SMPK_REQUIRE(M > 0 && N > 0 && K > 0 && nb1 > 0 && nb2 > 0, SMPK_ERR_BAD_SHAPE,
                "smpk_gemm: bad shape M=%d N=%d K=%d nb=%dx%d", M, N, K, nb1, nb2);
@@ -987,12 +987,22 @@ static int gemm_prepare(const void* a, int a_mn_major, int64_t lda, int64_t a_bs
 
   int tiles, num_kb, splits, kb_per;
   plan_gemm(M, N, K, nb1, nb2, BN, pair, tiles, num_kb, splits, kb_per);
-  if (grouped && splits > 1) {  // back to the unsplit CTA-pair plan
+  if (grouped && splits > 1) {  // back to the CTA-pair plan
     BN = pick_bn(N);
     pair = BN >= 128 && M >= 2 * BM && pair_enabled();
     tiles = ((M + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM)) * ((N + BN - 1) / BN) * nb1 * nb2;
     splits = 1;
     kb_per = num_kb;
+    if (grouped == 2 && pair) {
+      // the grouped launch's plain problem runs its units first: split its long K so that every
+      // unit of it still fits in the first wave of CTA pairs (the fix-up needs all splits resident)
+      int sp = (gemm_sms() / 2) / tiles;
+      while (sp > 1 && (num_kb + sp - 1) / sp < 8) --sp;
+      if (sp > 1) {
+        kb_per = (num_kb + sp - 1) / sp;
+        splits = (num_kb + kb_per - 1) / kb_per;
+      }
+    }
   }
   if (npeers || splits > 1 && (workspace == nullptr || workspace_bytes < splitk_ws_bytes(BN, pair, tiles, splits))) {
     splits = 1;  // no (or too small a) workspace: single pass over K
@@ -1139,12 +1149,14 @@ static int desc_impl(const smpk_gemm_desc& d, void* stream) {
                    d.bias, d.aux, d.ldaux, nullptr, 0, 0, 0, d.workspace, d.workspace_bytes, d.colsum_part, stream);
 }
 
+// mode 1: a grouped problem kept unsplit; mode 2: the grouped launch's plain problem, which may be
+// split over K within the first wave (its workspace comes with the descriptor)
 static int desc_prepare(const smpk_gemm_desc& d, CUtensorMap& ta, CUtensorMap& tb, EpiMaps& maps, GemmArgs& g,
-                        int& BN, bool& pair) {
+                        int& BN, bool& pair, int mode = 1) {
   return gemm_prepare(d.a, d.a_mn_major, d.lda, d.a_bs1, d.a_bs2, d.b, d.b_mn_major, d.ldb, d.b_bs1, d.b_bs2, d.c,
                       d.c_f32, d.ldc, d.c_bs1, d.c_bs2, d.M, d.N, d.K, d.nb1, d.nb2, d.alpha, d.beta, d.epilogue,
-                      d.act, d.bias, d.aux, d.ldaux, nullptr, 0, 0, 0, nullptr, 0, d.colsum_part, true, ta, tb, maps,
-                      g, BN, pair);
+                      d.act, d.bias, d.aux, d.ldaux, nullptr, 0, 0, 0, mode == 2 ? d.workspace : nullptr,
+                      mode == 2 ? d.workspace_bytes : 0, d.colsum_part, mode, ta, tb, maps, g, BN, pair);
 }
 
 // SMPK_GEMM_GROUP=0 disables grouped launches (A/B: the same GEMMs launched one after the other)
@@ -1176,13 +1188,14 @@ extern "C" int smpk_gemm_grouped(const smpk_gemm_desc* descs, int n, void* strea
         const bool eligible = !d[i]->c_f32 && d[i]->beta == 0.f && d[i]->alpha == 1.f && d[i]->nb1 == 1 &&
                               d[i]->nb2 == 1;
         ok = eligible &&
-             desc_prepare(*d[i], P.ta[i], P.tb[i], P.maps[i], P.g[i], BN, pair) == SMPK_OK && BN == 256 && pair &&
-             P.g[i].splits == 1 && P.g[i].tma_store;
+             desc_prepare(*d[i], P.ta[i], P.tb[i], P.maps[i], P.g[i], BN, pair, i == 1 ? 2 : 1) == SMPK_OK &&
+             BN == 256 && pair && (i == 1 || P.g[i].splits == 1) && P.g[i].tma_store;
       }
     }
-    // the plain problem's (long, weight-gradient) tiles must fill at least half the CTA pairs;
-    // a small-output wgrad (e.g. the 1024 x 1024 out-projection, 16 tiles) is faster split-K on its own
-    if (ok && 2 * P.g[1].num_units < gemm_sms() / 2) ok = false;
+    // the plain problem's (long, weight-gradient) units must fill at least half the CTA pairs (a
+    // small-output wgrad is split over K to get there), and all of them fit in the first wave
+    if (ok && (2 * P.g[1].num_units < gemm_sms() / 2 || (P.g[1].splits > 1 && P.g[1].num_units > gemm_sms() / 2)))
+      ok = false;
     if (ok) {
       const GemmArgs& g0 = P.g[0];
       switch (g0.epi) {

@@ -121,12 +121,16 @@ def gemm_raw(a, a_mn, lda, a_bs, b, b_mn, ldb, b_bs, c, ldc, c_bs, M, N, K, nb=(
     """Direct binding of smpk_gemm; strides in elements, batch strides as 2-tuples.
     colsum_part: fp32 [ceil(M/32), N] receiving per-32-row column sums of the output."""
     _check_cuda(a, b, c, bias, aux)
-    if _GROUP is not None:  # collected: launched by grouped.__exit__ (no split-K inside a group)
+    if _GROUP is not None:  # collected: launched by grouped.__exit__
+        # a plain problem may be split over K inside the group (its units run first): workspace
+        ws_bytes = 0 if (epi != EPI_NONE or colsum_part is not None) else \
+            _lib.size("smpk_gemm_workspace", int(M), int(N), int(K), int(nb[0]), int(nb[1]))
+        ws = torch.empty(ws_bytes // 4, dtype=torch.float32, device=c.device) if ws_bytes else None
         d = GemmDesc(_ptr(a), int(a_mn), int(lda), int(a_bs[0]), int(a_bs[1]), _ptr(b), int(b_mn), int(ldb),
                      int(b_bs[0]), int(b_bs[1]), _ptr(c), int(c.dtype == torch.float32), int(ldc), int(c_bs[0]),
                      int(c_bs[1]), int(M), int(N), int(K), int(nb[0]), int(nb[1]), float(alpha), float(beta),
-                     int(epi), int(act), _ptr(bias), _ptr(aux), int(ldaux), None, 0, _ptr(colsum_part))
-        _GROUP.append((d, (a, b, c, bias, aux, colsum_part), 2.0 * M * N * K * nb[0] * nb[1]))
+                     int(epi), int(act), _ptr(bias), _ptr(aux), int(ldaux), _ptr(ws), int(ws_bytes), _ptr(colsum_part))
+        _GROUP.append((d, (a, b, c, bias, aux, colsum_part, ws), 2.0 * M * N * K * nb[0] * nb[1]))
         return
     prof = PROFILER
     if prof is not None:
