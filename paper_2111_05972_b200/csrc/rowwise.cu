@@ -853,6 +853,7 @@ struct BdrPipeArgs {
   int64_t peer_off;
   int nst;  // ring stages
   const uint64_t* rng_step = nullptr;
+  int push_lsu = 0;  // push the output rows with vector stores instead of bulk copies (SMPK_PIPE_PUSH=lsu)
 };
 
 __device__ __forceinline__ void bulk_store_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
@@ -948,7 +949,7 @@ __global__ void __launch_bounds__(32 * (PIPE_CW + 1), 1) bdr_ln_pipe_kernel(cons
       round8(v[k]);
     }
     __syncwarp();
-    const bool push = a.npeers > 0;
+    const bool push = a.npeers > 0 && !a.push_lsu;  // bulk push from the stage
     if (!push) {
       if (lane == 0) mbar_arrive(&empty[st]);  // inputs consumed: the producer may refill
     }
@@ -994,6 +995,11 @@ __global__ void __launch_bounds__(32 * (PIPE_CW + 1), 1) bdr_ln_pipe_kernel(cons
       for (int k = 0; k < CH; ++k)
 #pragma unroll
         for (int e = 0; e < 8; ++e) o[k][e] = v[k][e];
+    }
+    if (a.npeers && a.push_lsu) {  // push with plain vector stores (LSU path, next to the TMA pulls)
+#pragma unroll
+      for (int k = 0; k < CH; ++k)
+        store8_peers(a.out_peers, a.npeers, a.peer_off + (int64_t)row * H + (k * 32 + lane) * 8, o[k]);
     }
     if (push) {
       // the stage's first slot row becomes the bf16 output row, pushed to every peer in bulk
@@ -1041,6 +1047,15 @@ static int bdr_ln_pipe_launch(const BdrPipeArgs& a, cudaStream_t st) {
 using namespace smpk;
 
 // SMPK_ROW_PIPE=0 selects the register-only row kernel (A/B measurements)
+static bool push_lsu_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SMPK_PIPE_PUSH");
+    v = (e && e[0] == 'l') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 static bool pipe_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -1095,6 +1110,7 @@ static int bdr_ln_impl(const void* x, int nslots, int64_t slot_stride, const voi
                    p_drop, seed, (uint32_t)layer, (uint32_t)site, row_offset, keep_out,
                    reinterpret_cast<bf16* const*>(out_peers), npeers, peer_off, 0};
   pa.rng_step = rng_step;
+  pa.push_lsu = push_lsu_enabled() ? 1 : 0;
     const int nin = nslots + (residual ? 1 : 0);
     const int budget = 200 * 1024 - 3 * H * 2;
     const int nst = budget / (nin * H * 2);
@@ -1168,6 +1184,12 @@ extern "C" int64_t smpk_ln_bwd_workspace(int M, int H) { return ln_bwd_grid(M, H
 // (deterministic) into this CTA's partial row of the workspace.
 // consumer warps: 12 (13 warps allocate registers like 16 -> 128 per thread, no spills), 8 at W = 8
 __host__ __device__ constexpr int lnb_cw(int W) { return W == 8 ? 8 : 12; }
+
+template <int W>
+__device__ __forceinline__ void group_bar(int grp) {
+  if constexpr (W > 1) named_bar(1 + grp, W * 32);
+  else __syncwarp();
+}
 
 template <int W, int VPT>
 __global__ void __launch_bounds__(32 * (lnb_cw(W) + 1), 1) ln_bwd_pipe_kernel(const LnBwdArgs a, int nst, int sb) {
@@ -1283,12 +1305,26 @@ __global__ void __launch_bounds__(32 * (lnb_cw(W) + 1), 1) ln_bwd_pipe_kernel(co
         round8(d);
         store8(a.dsub_out + (int64_t)row * H + col, d);
       }
+      if (a.npeers) store8(reinterpret_cast<bf16*>(const_cast<uint8_t*>(buf)) + col, d);  // dy slot := output
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc_d[i][j] += d[j];
+    }
+    if (a.npeers) {
+      // the row's output (in the stage's dy slot) goes to every peer's gather region in bulk; the
+      // stage is released only once the copies have read it
+      fence_proxy_async_smem();
+      group_bar<W>(grp);
+      if (wi == 0 && lane == 0) {
+        for (int j = 0; j < a.npeers; ++j)
+          bulk_store_s2g(a.out_peers[j] + a.peer_off + (int64_t)row * H, buf, H * 2);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
   }
+  if (a.npeers && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   // column partials of the CTA: groups summed in ascending order through shared memory
   float* out = a.partials + (int64_t)blockIdx.x * 3 * H;
   float* rbuf = red + wi * (VPT * 8 * 32);
@@ -1329,8 +1365,8 @@ static bool lnb_pipe_enabled() {
 
 // Launches the pipelined backward when the call is a plain local one; returns -1 when it does not apply.
 static int ln_bwd_pipe_try(const LnBwdArgs& a, const RowGeom& geo, cudaStream_t st, int grid_limit) {
-  if (!lnb_pipe_enabled() || a.npeers || a.dy_peers || a.nslots != 1 || a.row_sums_out || a.ext_sums ||
-      a.col_offset || geo.W < 2 || a.H != geo.W * geo.VPT * 256 || a.M < 1)
+  if (!lnb_pipe_enabled() || a.npeers > 8 || a.dy_peers || a.nslots != 1 || a.row_sums_out || a.ext_sums ||
+      a.col_offset || geo.W < 2 || a.H != geo.W * geo.VPT * 256 || a.M < 1 || (a.peer_off * 2) % 16)
     return -1;
   const uintptr_t al = reinterpret_cast<uintptr_t>(a.dy) | reinterpret_cast<uintptr_t>(a.r) |
                        reinterpret_cast<uintptr_t>(a.dres) | reinterpret_cast<uintptr_t>(a.keep_in) |
