@@ -423,6 +423,7 @@ __global__ void __launch_bounds__(128) attn_dropout_bits_kernel(int nh, int sq, 
   // causal: the kernels never read words of key tiles after the query's tile (128-key tiles)
   if (causal && ((idx % wpr) >> 2) > (idx / wpr) >> 7) return;
   const uint64_t pkey = philox_key(seed, rng_step);
+  const PhiloxRoundKeys rk = philox_round_keys(static_cast<uint32_t>(pkey), static_cast<uint32_t>(pkey >> 32));
   const int bh = blockIdx.y;
   const int q = idx / wpr, w = idx - q * wpr;
   const int h = bh % nh, b = bh / nh;
@@ -430,12 +431,7 @@ __global__ void __launch_bounds__(128) attn_dropout_bits_kernel(int nh, int sq, 
   const uint64_t grow = (uint64_t)((gs * nh_global + head_offset + h) * (int64_t)sq + q);
   uint32_t word = 0;
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    bool k8[8];
-    dropout_keep8(pkey, layer, 0u, grow, w * 32 + c * 8, thresh, k8);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) word |= (k8[e] ? 1u : 0u) << (c * 8 + e);
-  }
+  for (int c = 0; c < 4; ++c) word |= dropout_keep8_bits(rk, layer, 0u, grow, w * 32 + c * 8, thresh) << (c * 8);
   bits[(int64_t)bh * sq * wpr + idx] = word;
 }
 

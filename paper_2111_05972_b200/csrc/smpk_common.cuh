@@ -420,6 +420,35 @@ __host__ __device__ __forceinline__ u32x4 philox4x32_10(u32x4 c, uint32_t k0, ui
   return c;
 }
 
+// Round keys of one Philox key, computed once when a thread makes several calls with it.
+struct PhiloxRoundKeys {
+  uint32_t k0[10], k1[10];
+};
+__host__ __device__ __forceinline__ PhiloxRoundKeys philox_round_keys(uint32_t k0, uint32_t k1) {
+  PhiloxRoundKeys r;
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    r.k0[i] = k0 + static_cast<uint32_t>(i) * 0x9E3779B9u;
+    r.k1[i] = k1 + static_cast<uint32_t>(i) * 0xBB67AE85u;
+  }
+  return r;
+}
+__host__ __device__ __forceinline__ u32x4 philox4x32_10(u32x4 c, const PhiloxRoundKeys& rk) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    const uint64_t p0 = static_cast<uint64_t>(M0) * c.x;
+    const uint64_t p1 = static_cast<uint64_t>(M1) * c.z;
+    u32x4 n;
+    n.x = static_cast<uint32_t>(p1 >> 32) ^ c.y ^ rk.k0[i];
+    n.y = static_cast<uint32_t>(p1);
+    n.z = static_cast<uint32_t>(p0 >> 32) ^ c.w ^ rk.k1[i];
+    n.w = static_cast<uint32_t>(p0);
+    c = n;
+  }
+  return c;
+}
+
 // Dropout draws 16 bits per element: one Philox call covers 8 consecutive columns.
 //   counter = (col >> 3, row, layer, site); word = out[(col >> 1) & 3];
 //   u16 = (word >> (16 * (col & 1))) & 0xffff;  keep iff u16 >= rint(p * 65536)
@@ -434,6 +463,21 @@ __host__ __device__ __forceinline__ uint32_t dropout_threshold(float p) {
 __device__ __forceinline__ uint64_t philox_key(uint64_t seed, const uint64_t* rng_step) {
   return rng_step ? seed + __ldg(reinterpret_cast<const unsigned long long*>(rng_step)) * 0x9E3779B97F4A7C15ull
                   : seed;
+}
+
+// keep flags for 8 consecutive columns (precomputed round keys of the step key)
+__device__ __forceinline__ uint32_t dropout_keep8_bits(const PhiloxRoundKeys& rk, uint32_t layer, uint32_t site,
+                                                       uint64_t g, int col0, uint32_t thresh) {
+  u32x4 c = {static_cast<uint32_t>(col0 >> 3), static_cast<uint32_t>(g), layer, site};
+  u32x4 r = philox4x32_10(c, rk);
+  const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+  uint32_t bits = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    bits |= ((w[j] & 0xffffu) >= thresh ? 1u : 0u) << (2 * j);
+    bits |= ((w[j] >> 16) >= thresh ? 1u : 0u) << (2 * j + 1);
+  }
+  return bits;
 }
 
 // keep flags for 8 consecutive columns col0..col0+7 (col0 % 8 == 0) of logical row g
