@@ -1047,6 +1047,17 @@ static int bdr_ln_pipe_launch(const BdrPipeArgs& a, cudaStream_t st) {
 using namespace smpk;
 
 // SMPK_ROW_PIPE=0 selects the register-only row kernel (A/B measurements)
+// SMPK_ROW_PIPE_LOCAL=1 routes local-row bias/dropout/residual/LayerNorm calls through the pipelined
+// kernel too (A/B measurements)
+static bool pipe_local() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SMPK_ROW_PIPE_LOCAL");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 static bool push_lsu_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -1100,7 +1111,7 @@ static int bdr_ln_impl(const void* x, int nslots, int64_t slot_stride, const voi
   const bool al = (reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(residual) |
                    reinterpret_cast<uintptr_t>(r_out) | reinterpret_cast<uintptr_t>(y_out)) % 16 == 0 &&
                   (slot_stride * 2) % 16 == 0 && (x_peer_off * 2) % 16 == 0 && (peer_off * 2) % 16 == 0;
-  if (pipe_enabled() && (x_peers || npeers) && H % 256 == 0 && (ch == 1 || ch == 2 || ch == 4 || ch == 8) && al &&
+  if (pipe_enabled() && (x_peers || npeers || pipe_local()) && H % 256 == 0 && (ch == 1 || ch == 2 || ch == 4 || ch == 8) && al &&
       !row_sums_out &&
       !ext_sums && col_offset == 0 && nslots <= 8 && npeers <= 8) {
     BdrPipeArgs pa{reinterpret_cast<const bf16*>(x), slot_stride, reinterpret_cast<const bf16* const*>(x_peers),
