@@ -479,6 +479,7 @@ __global__ void __launch_bounds__(FB2_THREADS, 1)
   uint64_t* kv_done = bar + 14;
   uint64_t* dqa_full = bar + 15;  // the earlier key tiles' dQ sum landed in the staging boxes
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  uint64_t* dst_drained = bar + 17;  // dh 128: the dQ drain is done with the dS^T buffer it borrowed
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_kt = a.s / 128;
@@ -514,6 +515,7 @@ __global__ void __launch_bounds__(FB2_THREADS, 1)
     mbar_init(dq_free, 4);  // one arrive per drain warp
     mbar_init(kv_done, 1);
     mbar_init(dqa_full, 1);
+    mbar_init(dst_drained, 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -740,6 +742,7 @@ __global__ void __launch_bounds__(FB2_THREADS, 1)
       tmem_ld_32x32b_x32(tP + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
       tmem_ld_wait();
       if (t > 0) mbar_wait(dst_free, (t - 1) & 1);  // dK / dQ(t-1) have read dS
+      if (DH == 128 && t > 0) mbar_wait(dst_drained, (t - 1) & 1);  // the dQ(t-1) drain returned it
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const uint32_t w = c < 4 ? kw0 : kw1;
@@ -816,6 +819,7 @@ __global__ void __launch_bounds__(FB2_THREADS, 1)
       const int row0 = b * a.s + i * 128;
       mbar_wait(dq_full, t & 1);
       if (warp == 12) FB_TR(18);
+      if (DH == 128 && lastc && issuer) mbar_arrive(dst_drained);  // not borrowed: phases stay in step
       tc_fence_after();
       bool my_turn = firstc;  // (issuer) the previous contributors are done with this tile
 #pragma unroll 1
@@ -832,7 +836,45 @@ __global__ void __launch_bounds__(FB2_THREADS, 1)
         float* v = reinterpret_cast<float*>(o);
 #pragma unroll
         for (int q = 0; q < 64; ++q) v[q] = __uint_as_float(o[q]) * a.scale;
-        if (!lastc) {
+        if (DH == 128 && !lastc) {
+          // dh 128 has room for one 16 KB staging box only; the dS^T buffer (32 KB) is idle from the
+          // end of the dQ(t) MMA until the next dS pass, so chunks 1 and 2 of the four 32-column
+          // chunks are staged there -- only after this tile's turn came, so the borrow is short --
+          // and it is handed back (dst_drained) once the TMA engine has read them
+          uint8_t* dsb = smem + Cfg::OFF_DST;
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            const int cidx = hf * 2 + g;  // 32-column chunk 0..3
+            uint8_t* boxb = (cidx == 1 || cidx == 2) ? dsb + (cidx - 1) * 16384 : dqs;
+            uint8_t* box = boxb + rr * 128;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float* src = v + g * 32 + q * 4;
+              *reinterpret_cast<float4*>(box + ((q ^ (rr & 7)) << 4)) = make_float4(src[0], src[1], src[2], src[3]);
+            }
+            fence_proxy_async_smem();
+            named_barrier_sync(3, 128);
+            if (issuer) {
+              if (!my_turn) {
+                while (ld_acquire_gpu(cnt) != t) __nanosleep(32);
+                fence_proxy_async_global();
+                my_turn = true;
+              }
+              const int c0 = h * DH + cidx * 32;
+              if (firstc)
+                tma_store_2d(&tmDQ, boxb, c0, row0);
+              else
+                tma_reduce_add_2d(&tmDQ, boxb, c0, row0);
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+              if (cidx == 2) {  // chunks 0-2 read: the dS^T buffer goes back, the box is reusable
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                mbar_arrive(dst_drained);
+              }
+              if (cidx == 3) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            }
+            named_barrier_sync(3, 128);
+          }
+        } else if (!lastc) {
 #pragma unroll
           for (int g0 = 0; g0 < 2; g0 += Cfg::SG) {
 #pragma unroll
