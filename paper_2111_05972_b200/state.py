@@ -35,7 +35,7 @@ DEFAULTS = {
     "tp_rs": "pull",  # barrier exchange: the consumer pulls the partials ("push": GEMM epilogue stores)
     "tp_exchange": "barrier",  # peer mode: "chunks" = per-owner chunks + copy-engine mailboxes (exchange.py), "barrier"
     "tp_overlap_sms": 0,  # >0: backward weight-gradient GEMMs on this many SMs beside the exchange
-    "symm_pool_bytes": 4 << 30,
+    "symm_pool_bytes": 8 << 30,  # per rank; a BERT-L stack at T=8 holds ~3.4 GiB of gather regions
 }
 
 
@@ -164,7 +164,7 @@ def get_pool():
     pool = getattr(STATE, "_pool", None)
     if pool is None:
         from .symm import SymmPool
-        cap = int(STATE.config.get("symm_pool_bytes", 4 << 30))
+        cap = int(STATE.config.get("symm_pool_bytes", 8 << 30))
         ranks = STATE.tp_group_ranks
         pool = SymmPool(cap, STATE.tp_group, ranks, ranks.index(STATE.rank))
         STATE._pool = pool
