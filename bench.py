@@ -481,7 +481,7 @@ def run_gpu(args, rank, world, local):
     flops_tok = flops_per_token(args.workload)
     model_tflops = value / world * flops_tok / 1e12  # per GPU
     cpu = None
-    if not args.skip_cpu_baseline:
+    if not args.skip_cpu_baseline and world == 1:  # the CPU baseline is timed on rank 0 at N=1 only
         v, threads, dt, it = cpu_reference_sample(max_seconds=args.ref_seconds, workload=args.workload)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                "sample": _cpu_sample_text(args.workload, it, dt) + f"; {cpu_model()}"}
