@@ -184,6 +184,8 @@ def begin_forward():
         STATE.rng_counter = torch.zeros(1, dtype=torch.int64, device=dev)
     STATE.rng_cur = ops.rng_next(STATE.rng_counter)
     STATE.xch_fresh = True
+    from . import layers
+    layers._PUSHED.clear()  # push records of an aborted earlier forward can never match a new input
     STATE.step += 1
     return STATE.rng_cur
 
