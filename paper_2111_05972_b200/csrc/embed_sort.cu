@@ -38,23 +38,27 @@ __global__ void __launch_bounds__(256) embed_keys_kernel(const int64_t* __restri
     keys[t] = valid ? (uint32_t)loc : (uint32_t)rows_local;  // sentinel sorts last
     vals[t] = (uint32_t)t;
   }
-  const unsigned m = __ballot_sync(0xffffffffu, valid);
-  if ((threadIdx.x & 31) == 0 && m) atomicAdd(n_valid, __popc(m));
+  const int c = __syncthreads_count(valid);  // one atomic per block (per-warp atomics on one word serialised)
+  if (threadIdx.x == 0 && c) atomicAdd(n_valid, c);
 }
 
+// digits of BITS bits (8 or 9: the row count of the table decides how many passes the keys need;
+// 27-bit keys of a 1e8-row table take three 9-bit passes instead of four 8-bit ones)
+template <int BITS>
 __global__ void __launch_bounds__(RS_THREADS) radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t n,
                                                                 int shift, int num_tiles, int* __restrict__ counts) {
-  __shared__ int hist[256];
-  hist[threadIdx.x] = 0;
+  constexpr int BINS = 1 << BITS;
+  __shared__ int hist[BINS];
+  for (int d = threadIdx.x; d < BINS; d += RS_THREADS) hist[d] = 0;
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * RS_TILE;
 #pragma unroll
   for (int k = 0; k < RS_ITEMS; ++k) {
     const int64_t i = base + k * RS_THREADS + threadIdx.x;
-    if (i < n) atomicAdd(&hist[(keys[i] >> shift) & 255], 1);
+    if (i < n) atomicAdd(&hist[(keys[i] >> shift) & (BINS - 1)], 1);
   }
   __syncthreads();
-  counts[(int64_t)threadIdx.x * num_tiles + blockIdx.x] = hist[threadIdx.x];
+  for (int d = threadIdx.x; d < BINS; d += RS_THREADS) counts[(int64_t)d * num_tiles + blockIdx.x] = hist[d];
 }
 
 // counts[d][tile] -> exclusive prefix over the tiles of digit d (block d, coalesced 1024-wide chunks
@@ -88,13 +92,15 @@ __global__ void __launch_bounds__(SCAN_THREADS) radix_scan_kernel(int* __restric
   if (threadIdx.x == 0) digit_tot[blockIdx.x] = carry;
 }
 
-__global__ void __launch_bounds__(256) radix_digit_kernel(int* __restrict__ digit_tot) {
-  __shared__ int part[256];
+template <int BITS>
+__global__ void __launch_bounds__(1 << BITS) radix_digit_kernel(int* __restrict__ digit_tot) {
+  constexpr int BINS = 1 << BITS;
+  __shared__ int part[BINS];
   const int d = threadIdx.x;
   const int v = digit_tot[d];
   part[d] = v;
   __syncthreads();
-  for (int off = 1; off < 256; off <<= 1) {
+  for (int off = 1; off < BINS; off <<= 1) {
     const int o = d >= off ? part[d - off] : 0;
     __syncthreads();
     part[d] += o;
@@ -105,6 +111,7 @@ __global__ void __launch_bounds__(256) radix_digit_kernel(int* __restrict__ digi
 
 // Stable scatter: warp w of a tile owns the tile's elements [w*256, w*256+256) in order; each
 // iteration ranks 32 consecutive elements with __match_any_sync against per-warp digit counters.
+template <int BITS>
 __global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(const uint32_t* __restrict__ keys_in,
                                                                    const uint32_t* __restrict__ vals_in, int64_t n,
                                                                    int shift, int num_tiles,
@@ -112,9 +119,10 @@ __global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(const uint32_
                                                                    const int* __restrict__ digit_base,
                                                                    uint32_t* __restrict__ keys_out,
                                                                    uint32_t* __restrict__ vals_out) {
-  __shared__ int wc[RS_THREADS / 32][256];
+  constexpr int BINS = 1 << BITS;
+  __shared__ int wc[RS_THREADS / 32][BINS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int d = lane; d < 256; d += 32) wc[warp][d] = 0;
+  for (int d = lane; d < BINS; d += 32) wc[warp][d] = 0;
   __syncwarp();
   const int64_t base = (int64_t)blockIdx.x * RS_TILE + warp * 256;
   uint32_t key[RS_ITEMS], val[RS_ITEMS];
@@ -125,7 +133,7 @@ __global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(const uint32_
     const bool ok = i < n;
     key[it] = ok ? keys_in[i] : 0u;
     val[it] = ok ? vals_in[i] : 0u;
-    const int d = ok ? (int)((key[it] >> shift) & 255) : 256 + lane;  // out-of-range lanes match nobody
+    const int d = ok ? (int)((key[it] >> shift) & (BINS - 1)) : BINS + lane;  // out-of-range lanes match nobody
     const unsigned peers = __match_any_sync(0xffffffffu, d);
     const int before = __popc(peers & ((1u << lane) - 1));
     int cnt = 0;
@@ -137,8 +145,7 @@ __global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(const uint32_
   }
   __syncthreads();
   // exclusive prefix of the per-warp counters, per digit, in warp order
-  {
-    const int d = threadIdx.x;
+  for (int d = threadIdx.x; d < BINS; d += RS_THREADS) {
     int s = 0;
 #pragma unroll
     for (int w = 0; w < RS_THREADS / 32; ++w) {
@@ -152,7 +159,7 @@ __global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(const uint32_
   for (int it = 0; it < RS_ITEMS; ++it) {
     const int64_t i = base + it * 32 + lane;
     if (i < n) {
-      const int d = (int)((key[it] >> shift) & 255);
+      const int d = (int)((key[it] >> shift) & (BINS - 1));
       const int64_t pos = (int64_t)digit_base[d] + counts[(int64_t)d * num_tiles + blockIdx.x] + wc[warp][d] + rank[it];
       keys_out[pos] = key[it];
       vals_out[pos] = val[it];
@@ -392,7 +399,7 @@ static int64_t seg_windows(int64_t n, int dim) {
 extern "C" int64_t smpk_embed_bwd_sorted_workspace(int64_t n, int64_t rows_local, int dim) {
   (void)rows_local;
   const int64_t tiles = (n + RS_TILE - 1) / RS_TILE;
-  return align256(4 * n) * 4 + align256(256 * tiles * 4) + 1024 + 256 + align256(seg_windows(n, dim) * 2 * dim * 4);
+  return align256(4 * n) * 4 + align256(512 * tiles * 4) + 2048 + 256 + align256(seg_windows(n, dim) * 2 * dim * 4);
 }
 
 extern "C" int smpk_embed_bwd_sorted(const int64_t* ids, int64_t n, const void* dy, int64_t ld_dy,
@@ -422,20 +429,28 @@ extern "C" int smpk_embed_bwd_sorted(const int64_t* ids, int64_t n, const void* 
   uint32_t* v1 = reinterpret_cast<uint32_t*>(ws + 3 * kb);
   const int tiles = (int)((n + RS_TILE - 1) / RS_TILE);
   int* counts = reinterpret_cast<int*>(ws + 4 * kb);
-  int* digit_base = reinterpret_cast<int*>(ws + 4 * kb + align256(256LL * tiles * 4));
-  int* n_valid = reinterpret_cast<int*>(ws + 4 * kb + align256(256LL * tiles * 4) + 1024);
-  float* partial = reinterpret_cast<float*>(ws + 4 * kb + align256(256LL * tiles * 4) + 1024 + 256);
+  int* digit_base = reinterpret_cast<int*>(ws + 4 * kb + align256(512LL * tiles * 4));
+  int* n_valid = reinterpret_cast<int*>(ws + 4 * kb + align256(512LL * tiles * 4) + 2048);
+  float* partial = reinterpret_cast<float*>(ws + 4 * kb + align256(512LL * tiles * 4) + 2048 + 256);
   cudaMemsetAsync(n_valid, 0, sizeof(int), st);
   embed_keys_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ids, n, row_offset, rows_local, padding_row, k0, v0,
                                                                   n_valid);
   int rc = check_launch("smpk_embed_bwd_sorted(keys)");
   if (rc) return rc;
   const int nbits = bits_for(rows_local);  // keys in [0, rows_local] (sentinel included)
-  for (int shift = 0; shift < nbits; shift += 8) {
-    radix_hist_kernel<<<tiles, RS_THREADS, 0, st>>>(k0, n, shift, tiles, counts);
-    radix_scan_kernel<<<256, SCAN_THREADS, 0, st>>>(counts, tiles, digit_base);
-    radix_digit_kernel<<<1, 256, 0, st>>>(digit_base);
-    radix_scatter_kernel<<<tiles, RS_THREADS, 0, st>>>(k0, v0, n, shift, tiles, counts, digit_base, k1, v1);
+  const int bits = ((nbits + 7) / 8) * 9 >= nbits + 9 ? 9 : 8;  // 9-bit digits when they save a pass
+  for (int shift = 0; shift < nbits; shift += bits) {
+    if (bits == 9) {
+      radix_hist_kernel<9><<<tiles, RS_THREADS, 0, st>>>(k0, n, shift, tiles, counts);
+      radix_scan_kernel<<<512, SCAN_THREADS, 0, st>>>(counts, tiles, digit_base);
+      radix_digit_kernel<9><<<1, 512, 0, st>>>(digit_base);
+      radix_scatter_kernel<9><<<tiles, RS_THREADS, 0, st>>>(k0, v0, n, shift, tiles, counts, digit_base, k1, v1);
+    } else {
+      radix_hist_kernel<8><<<tiles, RS_THREADS, 0, st>>>(k0, n, shift, tiles, counts);
+      radix_scan_kernel<<<256, SCAN_THREADS, 0, st>>>(counts, tiles, digit_base);
+      radix_digit_kernel<8><<<1, 256, 0, st>>>(digit_base);
+      radix_scatter_kernel<8><<<tiles, RS_THREADS, 0, st>>>(k0, v0, n, shift, tiles, counts, digit_base, k1, v1);
+    }
     rc = check_launch("smpk_embed_bwd_sorted(radix)");
     if (rc) return rc;
     uint32_t* t = k0;

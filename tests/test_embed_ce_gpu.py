@@ -69,6 +69,7 @@ def test_embed_grad_deterministic(smp1, D):
     (12000, 64, 70000, 5000, 5123, 9000, torch.float32, True, "sort"),  # vocab shard: ids outside skipped
     (50304, 2048, 16384, 0, None, 700, torch.bfloat16, False, "sort"),  # GPT-1.3B tied table
     (1 << 20, 16, 300000, 0, None, 20000, torch.float32, True, "sort"),  # 3 radix passes
+    ((1 << 17) + 3, 8, 200000, 0, None, 5000, torch.float32, False, "sort"),  # 18-bit keys: two 9-bit passes
 ])
 def test_embed_grad_sorted_vs_oracle(smp1, case):
     """Sort-based deterministic scatter-add (csrc/embed_sort.cu) vs an fp64 index_add: vocab-shard
