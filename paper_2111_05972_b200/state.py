@@ -35,7 +35,8 @@ DEFAULTS = {
     "tp_rs": "pull",  # barrier exchange: the consumer pulls the partials ("push": GEMM epilogue stores)
     "tp_exchange": "barrier",  # peer mode: "chunks" = per-owner chunks + copy-engine mailboxes (exchange.py), "barrier"
     "tp_overlap_sms": 0,  # >0: backward weight-gradient GEMMs on this many SMs beside the exchange
-    "symm_pool_bytes": 8 << 30,  # per rank; a BERT-L stack at T=8 holds ~3.4 GiB of gather regions
+    "symm_pool_bytes": None,  # per rank; default min(16 GiB, 10% of HBM): the forward gather regions live
+    # until the backward (BERT-L at T=8 ~3.4 GiB, GPT-1.3B at T=4 ~12.3 GiB)
 }
 
 
@@ -164,7 +165,11 @@ def get_pool():
     pool = getattr(STATE, "_pool", None)
     if pool is None:
         from .symm import SymmPool
-        cap = int(STATE.config.get("symm_pool_bytes", 8 << 30))
+        cap = STATE.config.get("symm_pool_bytes")
+        if cap is None:
+            total = torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory
+            cap = min(16 << 30, total // 10)
+        cap = int(cap)
         ranks = STATE.tp_group_ranks
         pool = SymmPool(cap, STATE.tp_group, ranks, ranks.index(STATE.rank))
         STATE._pool = pool
