@@ -64,29 +64,46 @@ __global__ void __launch_bounds__(RS_THREADS) radix_hist_kernel(const uint32_t* 
 // counts[d][tile] -> exclusive prefix over the tiles of digit d (block d, coalesced 1024-wide chunks
 // with a carried block scan) and digit_tot[d]; radix_digit_kernel turns the totals into the digit
 // bases.  Global position of (digit d, tile t) = digit_base[d] + counts[d][t].
-constexpr int SCAN_THREADS = 1024;
+constexpr int SCAN_THREADS = 256;
 __global__ void __launch_bounds__(SCAN_THREADS) radix_scan_kernel(int* __restrict__ counts, int num_tiles,
                                                                   int* __restrict__ digit_tot) {
-  __shared__ int part[SCAN_THREADS];
-  __shared__ int carry;
+  // 1024-entry chunks: 4 consecutive tiles per thread, warp shuffle scan, 8 warp totals in smem
+  __shared__ int wsum[SCAN_THREADS / 32];
   int* row = counts + (int64_t)blockIdx.x * num_tiles;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int base = 0; base < num_tiles; base += SCAN_THREADS) {
-    const int t = base + threadIdx.x;
-    const int v = t < num_tiles ? row[t] : 0;
-    part[threadIdx.x] = v;
-    __syncthreads();
-    for (int off = 1; off < SCAN_THREADS; off <<= 1) {  // inclusive Hillis-Steele scan
-      const int o = threadIdx.x >= off ? part[threadIdx.x - off] : 0;
-      __syncthreads();
-      part[threadIdx.x] += o;
-      __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int carry = 0;
+  for (int base = 0; base < num_tiles; base += 4 * SCAN_THREADS) {
+    const int t0 = base + threadIdx.x * 4;
+    int v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = t0 + k < num_tiles ? row[t0 + k] : 0;
+    const int sum = (v[0] + v[1]) + (v[2] + v[3]);
+    int x = sum;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, off);
+      if (lane >= off) x += y;
     }
-    const int c = carry;
-    if (t < num_tiles) row[t] = c + part[threadIdx.x] - v;
+    if (lane == 31) wsum[warp] = x;
     __syncthreads();
-    if (threadIdx.x == SCAN_THREADS - 1) carry = c + part[threadIdx.x];
+    if (warp == 0) {
+      int w = lane < SCAN_THREADS / 32 ? wsum[lane] : 0;
+#pragma unroll
+      for (int off = 1; off < SCAN_THREADS / 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, w, off);
+        if (lane >= off) w += y;
+      }
+      if (lane < SCAN_THREADS / 32) wsum[lane] = w;
+    }
+    __syncthreads();
+    int e = carry + (warp > 0 ? wsum[warp - 1] : 0) + x - sum;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (t0 + k < num_tiles) {
+        row[t0 + k] = e;
+        e += v[k];
+      }
+    carry += wsum[SCAN_THREADS / 32 - 1];
     __syncthreads();
   }
   if (threadIdx.x == 0) digit_tot[blockIdx.x] = carry;
