@@ -431,10 +431,7 @@ def _chunk_grad_finish(m: LayerMeta, R: int, H: int, Pb: int, bslots, dr, x2, pr
     xch.await_all(RSB, chunk_order(pool.me, T)[1:])
     dx, dpre_w, dpre_b = _input_grad(bslots[0], dict(nslots=T, slot_stride=R * H), dr, x2, pre_w, mu1, rs1, m, R, H)
     slots = pool.view(V, (T, nv, H), dtype=torch.float32)
-    tot = slots[0].clone()
-    for j in range(1, T):
-        tot += slots[j]
-    tot = tot.to(torch.bfloat16)
+    tot = slots.sum(0).to(torch.bfloat16)  # one reduction over the T slots (rank order), one rounding
     xch.release_all([RSB, AGB], chunk_order(pool.me, T)[1:])
     xch.join()
     if nv == 3:
@@ -545,10 +542,7 @@ def _ov_vec_sums(m: LayerMeta, V: int, nv: int, H: int):
     (dpost_w, dpost_b, dbias) -- the first two None without a post-LN."""
     pool = get_pool()
     slots = pool.view(V, (m.tp_size, nv, H), dtype=torch.float32)
-    tot = slots[0].clone()
-    for j in range(1, m.tp_size):
-        tot += slots[j]
-    tot = tot.to(torch.bfloat16)
+    tot = slots.sum(0).to(torch.bfloat16)  # one reduction over the T slots (rank order), one rounding
     if nv == 3:
         m._post_synced = True
         return tot[0], tot[1], tot[2]
@@ -653,10 +647,7 @@ def _gather_grad(dy2, r, mean, rstd, m: LayerMeta, site: int, keep=None):
         pool.push_copy(pg, L + pool.me * nv * H * 4)
         pool.barrier()
         slots = pool.view(L, (T, nv, H), dtype=torch.float32)
-        tot = slots[0].clone()
-        for j in range(1, T):
-            tot += slots[j]
-        tot = tot.to(torch.bfloat16)
+        tot = slots.sum(0).to(torch.bfloat16)  # one reduction over the T slots (rank order), one rounding
         if has_ln:
             dgw, dgb = tot[0], tot[1]
             m._post_synced = True
