@@ -295,13 +295,19 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       float xs = a.scale_log2;
       if (mrow) {
         const float4* mp = reinterpret_cast<const float4*>(mrow + key0);
+        const float2 sl2 = make_float2(a.scale_log2, a.scale_log2);
+        const float2 l2e = make_float2(1.4426950408889634f, 1.4426950408889634f);
 #pragma unroll
         for (int k4 = 0; k4 < 32; ++k4) {
           const float4 mk = __ldg(mp + k4);
-          x[4 * k4 + 0] = fmaf(x[4 * k4 + 0], a.scale_log2, mk.x * 1.4426950408889634f);
-          x[4 * k4 + 1] = fmaf(x[4 * k4 + 1], a.scale_log2, mk.y * 1.4426950408889634f);
-          x[4 * k4 + 2] = fmaf(x[4 * k4 + 2], a.scale_log2, mk.z * 1.4426950408889634f);
-          x[4 * k4 + 3] = fmaf(x[4 * k4 + 3], a.scale_log2, mk.w * 1.4426950408889634f);
+          const float2 y0 = __ffma2_rn(make_float2(x[4 * k4 + 0], x[4 * k4 + 1]), sl2,
+                                       __fmul2_rn(make_float2(mk.x, mk.y), l2e));
+          const float2 y1 = __ffma2_rn(make_float2(x[4 * k4 + 2], x[4 * k4 + 3]), sl2,
+                                       __fmul2_rn(make_float2(mk.z, mk.w), l2e));
+          x[4 * k4 + 0] = y0.x;
+          x[4 * k4 + 1] = y0.y;
+          x[4 * k4 + 2] = y1.x;
+          x[4 * k4 + 3] = y1.y;
         }
         xs = 1.f;
       }
@@ -310,11 +316,13 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         for (int k = 0; k < 128; ++k)
           if (k > r) x[k] = -INFINITY;
       }
-      float mx8[8];
+      float mx8[8];  // 3-input max (FMNMX3): two keys per instruction
 #pragma unroll
       for (int i = 0; i < 8; ++i) mx8[i] = x[i];
 #pragma unroll
-      for (int k = 8; k < 128; ++k) mx8[k & 7] = fmaxf(mx8[k & 7], x[k]);
+      for (int k = 8; k < 128; k += 16)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(fmaxf(mx8[i], x[k + i]), x[k + 8 + i]);
       const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                              fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * xs;
       float alpha = 1.f;
@@ -325,18 +333,21 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       const float m_use = (m == -INFINITY) ? 0.f : m;
       const float nm = -m_use;
       // P = exp2(x*xs - m); row sum before dropout; dropped entries zero (1/(1-p) in the epilogue)
+      // paired fp32 math (FFMA2 / FADD2) and packed keep masks: the pass is issue-bound
       uint32_t pk[64];
-      float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      float2 rs2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       const uint32_t kws[4] = {kw.x, kw.y, kw.z, kw.w};
+      const float2 xs2 = make_float2(xs, xs), nm2 = make_float2(nm, nm);
+      uint32_t ksh[8];
 #pragma unroll
       for (int k = 0; k < 128; k += 2) {
-        const float p0 = ex2_approx(fmaf(x[k], xs, nm));
-        const float p1 = ex2_approx(fmaf(x[k + 1], xs, nm));
-        rs8[(k >> 1) & 7] += p0 + p1;
-        const uint32_t w = kws[k >> 5];
-        pk[k >> 1] = pack_bf16x2(((w >> (k & 31)) & 1u) ? p0 : 0.f, ((w >> ((k + 1) & 31)) & 1u) ? p1 : 0.f);
+        if ((k & 31) == 0) keep_shifts(kws[k >> 5], ksh);
+        const float2 y = __ffma2_rn(make_float2(x[k], x[k + 1]), xs2, nm2);
+        const float2 pv = make_float2(ex2_approx(y.x), ex2_approx(y.y));
+        rs2[(k >> 1) & 3] = __fadd2_rn(rs2[(k >> 1) & 3], pv);
+        pk[k >> 1] = pack_bf16x2(pv.x, pv.y) & keep_pair_mask(ksh, (k & 31) >> 3, k & 7);
       }
-      const float rowsum = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+      const float rowsum = ((rs2[0].x + rs2[0].y) + (rs2[1].x + rs2[1].y)) + ((rs2[2].x + rs2[2].y) + (rs2[3].x + rs2[3].y));
       l = l * alpha + rowsum;
       if (j > 0) {
         // P.V of tile j-1 must have finished: it reads the P buffer we overwrite below and

@@ -699,32 +699,44 @@ __global__ void __launch_bounds__(FB2_THREADS, 1)
       if (e == 0) FB_TR(32);
       if (t > 0) mbar_wait(pdt_free, (t - 1) & 1);  // dV(t-1) has read Pd
       if (e == 0) FB_TR(36);
+      // paired fp32 math (FFMA2) and packed keep masks: the pass is issue-bound
+      const float2 sc2 = make_float2(scale_log2, scale_log2), nls2 = make_float2(nls, nls);
+      uint32_t ksh[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) {  // 8 keys per 16-B granule
+        if ((c & 3) == 0) keep_shifts(c < 4 ? kw0 : kw1, ksh);
         float pr[8];
         if (a.mask) {
           const float4 m0 = *reinterpret_cast<const float4*>(mk_s + qh * 64 + c * 8);
           const float4 m1 = *reinterpret_cast<const float4*>(mk_s + qh * 64 + c * 8 + 4);
           const float mm[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
-            pr[u] = ex2_approx(fmaf(__uint_as_float(sv[c * 8 + u]), scale_log2, mm[u] + nls));
+          for (int u = 0; u < 8; u += 2) {
+            const float2 y = __ffma2_rn(make_float2(__uint_as_float(sv[c * 8 + u]), __uint_as_float(sv[c * 8 + u + 1])),
+                                        sc2, __fadd2_rn(make_float2(mm[u], mm[u + 1]), nls2));
+            pr[u] = ex2_approx(y.x);
+            pr[u + 1] = ex2_approx(y.y);
+          }
         } else {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) pr[u] = ex2_approx(fmaf(__uint_as_float(sv[c * 8 + u]), scale_log2, nls));
+          for (int u = 0; u < 8; u += 2) {
+            const float2 y = __ffma2_rn(make_float2(__uint_as_float(sv[c * 8 + u]), __uint_as_float(sv[c * 8 + u + 1])),
+                                        sc2, nls2);
+            pr[u] = ex2_approx(y.x);
+            pr[u + 1] = ex2_approx(y.y);
+          }
         }
         if (diag) {
 #pragma unroll
           for (int u = 0; u < 8; ++u)
             if (qh * 64 + c * 8 + u > qr) pr[u] = 0.f;  // key after query
         }
-        const uint32_t w = c < 4 ? kw0 : kw1;
-        const int sh = (c & 3) * 8;
         uint32_t pd[4];
 #pragma unroll
         for (int u = 0; u < 8; u += 2) {
-          pp[(c * 8 + u) >> 1] = pack_bf16x2(pr[u], pr[u + 1]);
-          pd[u >> 1] = pack_bf16x2(((w >> (sh + u)) & 1u) ? pr[u] : 0.f, ((w >> (sh + u + 1)) & 1u) ? pr[u + 1] : 0.f);
+          const uint32_t p2 = pack_bf16x2(pr[u], pr[u + 1]);
+          pp[(c * 8 + u) >> 1] = p2;
+          pd[u >> 1] = p2 & keep_pair_mask(ksh, c & 3, u);
         }
         *reinterpret_cast<uint4*>(pd_s + sw128_offset(qr, c)) = make_uint4(pd[0], pd[1], pd[2], pd[3]);
       }
@@ -743,6 +755,7 @@ __global__ void __launch_bounds__(FB2_THREADS, 1)
       tmem_ld_wait();
       if (t > 0) mbar_wait(dst_free, (t - 1) & 1);  // dK / dQ(t-1) have read dS
       if (DH == 128 && t > 0) mbar_wait(dst_drained, (t - 1) & 1);  // the dQ(t-1) drain returned it
+      const float2 ik2 = make_float2(inv_keep, inv_keep), nd2 = make_float2(-dlt, -dlt);
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const uint32_t w = c < 4 ? kw0 : kw1;
@@ -751,9 +764,12 @@ __global__ void __launch_bounds__(FB2_THREADS, 1)
 #pragma unroll
         for (int u = 0; u < 8; u += 2) {
           const float2 pf = unpack_bf16x2(pp[(c * 8 + u) >> 1]);
-          const float dp0 = ((w >> (sh + u)) & 1u) ? __uint_as_float(sv[c * 8 + u]) * inv_keep : 0.f;
-          const float dp1 = ((w >> (sh + u + 1)) & 1u) ? __uint_as_float(sv[c * 8 + u + 1]) * inv_keep : 0.f;
-          dsw[u >> 1] = pack_bf16x2(pf.x * (dp0 - dlt), pf.y * (dp1 - dlt));
+          float2 d = __ffma2_rn(make_float2(__uint_as_float(sv[c * 8 + u]), __uint_as_float(sv[c * 8 + u + 1])), ik2,
+                                nd2);  // dP/(1-p) - Delta
+          if (!((w >> (sh + u)) & 1u)) d.x = -dlt;
+          if (!((w >> (sh + u + 1)) & 1u)) d.y = -dlt;
+          const float2 r = __fmul2_rn(pf, d);
+          dsw[u >> 1] = pack_bf16x2(r.x, r.y);
         }
         *reinterpret_cast<uint4*>(ds_s + sw128_offset(qr, c)) = make_uint4(dsw[0], dsw[1], dsw[2], dsw[3]);
       }

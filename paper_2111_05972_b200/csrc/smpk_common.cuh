@@ -331,6 +331,22 @@ __device__ __forceinline__ float2 unpack_bf16x2(uint32_t u) {
   return __bfloat1622float2(v);
 }
 
+// Dropout keep bits applied to packed bf16 pairs with two instructions per pair (one PRMT, one
+// AND) instead of a bit test and a select per element.  sh[s] = w << s for s = 0..7 puts bit
+// 8k+u of w at the sign bit of byte k of sh[7-u]; PRMT's sign-replicate selectors spread that
+// bit over a 16-bit half.  keep_pair_mask(sh, k, u) (u even, k, u compile-time) is 0xffff in the
+// low half iff bit 8k+u is set and 0xffff0000 iff bit 8k+u+1 is set.
+__device__ __forceinline__ void keep_shifts(uint32_t w, uint32_t (&sh)[8]) {
+#pragma unroll
+  for (int s = 0; s < 8; ++s) sh[s] = w << s;
+}
+__device__ __forceinline__ uint32_t keep_pair_mask(const uint32_t (&sh)[8], int k, int u) {
+  const uint32_t sel = ((0xCu + k) << 12) | ((0xCu + k) << 8) | ((0x8u + k) << 4) | (0x8u + k);
+  uint32_t m;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(m) : "r"(sh[7 - u]), "r"(sh[6 - u]), "r"(sel));
+  return m;
+}
+
 // bf16 round-to-nearest-even kept in fp32, with integer ops (keeps the XU pipe free).
 __device__ __forceinline__ float round_bf16(float v) {
   uint32_t u = __float_as_uint(v);
