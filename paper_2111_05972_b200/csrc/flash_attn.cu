@@ -134,6 +134,8 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
   const int cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
   unsigned long long* trc = (a.trace && cta_lin < 1024) ? g_fa_trace + cta_lin * 20 : nullptr;
   if (trc && threadIdx.x == 0) {
@@ -515,11 +517,11 @@ extern "C" int smpk_flash_attn_fwd(const void* qkv, int64_t ld, int B, int nh, i
   if (dh == 64) {
     static unsigned long long once = 0;
     smem_attr_once(flash_fwd_kernel<64, 3, 3>, FaFwdCfg<64, 3, 3>::SMEM, once);
-    flash_fwd_kernel<64, 3, 3><<<grid, FA_THREADS, FaFwdCfg<64, 3, 3>::SMEM, st>>>(tq, tk, tv, a);
+    launch_pdl(flash_fwd_kernel<64, 3, 3>, grid, FA_THREADS, FaFwdCfg<64, 3, 3>::SMEM, st, tq, tk, tv, a);
   } else {
     static unsigned long long once = 0;
     smem_attr_once(flash_fwd_kernel<128, 2, 1>, FaFwdCfg<128, 2, 1>::SMEM, once);
-    flash_fwd_kernel<128, 2, 1><<<grid, FA_THREADS, FaFwdCfg<128, 2, 1>::SMEM, st>>>(tq, tk, tv, a);
+    launch_pdl(flash_fwd_kernel<128, 2, 1>, grid, FA_THREADS, FaFwdCfg<128, 2, 1>::SMEM, st, tq, tk, tv, a);
   }
   return check_launch("smpk_flash_attn_fwd");
 }

@@ -523,6 +523,8 @@ __global__ void __launch_bounds__(FB2_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
   const int64_t bh_row = ((int64_t)b * a.nh + h) * a.s;
   const int cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
   unsigned long long* trc = (a.trace && cta_lin < 2048) ? g_fb_trace + cta_lin * 64 : nullptr;
@@ -998,6 +1000,8 @@ __global__ void __launch_bounds__(256) flash_delta_kernel(const bf16* __restrict
                                                           const bf16* __restrict__ dout, int64_t ld_do, int B,
                                                           int nh, int s, int dh, float* __restrict__ delta,
                                                           int* __restrict__ cnt, int n_cnt) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (cnt && t < n_cnt) cnt[t] = 0;  // the backward's per-query-tile dQ turn counters
   const int64_t idx = t >> 3;
@@ -1097,9 +1101,9 @@ extern "C" int smpk_flash_attn_bwd(const void* qkv, int64_t ld, const void* out,
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   {
     const int64_t total = (int64_t)B * s * nh;
-    flash_delta_kernel<<<(unsigned)((total * 8 + 255) / 256), 256, 0, st>>>(
-        reinterpret_cast<const bf16*>(out), ld_out, reinterpret_cast<const bf16*>(dout), ld_dout, B, nh, s, dh,
-        delta, cnt, n_cnt);
+    launch_pdl(flash_delta_kernel, dim3((unsigned)((total * 8 + 255) / 256)), dim3(256), 0, st,
+               reinterpret_cast<const bf16*>(out), ld_out, reinterpret_cast<const bf16*>(dout), ld_dout, B, nh, s,
+               dh, delta, cnt, n_cnt);
     int rc = check_launch("smpk_flash_attn_bwd(delta)");
     if (rc) return rc;
   }
@@ -1145,11 +1149,11 @@ extern "C" int smpk_flash_attn_bwd(const void* qkv, int64_t ld, const void* out,
     if (dh == 64) {
       static unsigned long long once = 0;
       smem_attr_once(flash_bwd2_kernel<64>, FaBwd2Cfg<64>::SMEM, once);
-      flash_bwd2_kernel<64><<<grid, FB2_THREADS, FaBwd2Cfg<64>::SMEM, st>>>(tq, tk, tv, tdo, tbits, tdq, a);
+      launch_pdl(flash_bwd2_kernel<64>, grid, FB2_THREADS, FaBwd2Cfg<64>::SMEM, st, tq, tk, tv, tdo, tbits, tdq, a);
     } else {
       static unsigned long long once = 0;
       smem_attr_once(flash_bwd2_kernel<128>, FaBwd2Cfg<128>::SMEM, once);
-      flash_bwd2_kernel<128><<<grid, FB2_THREADS, FaBwd2Cfg<128>::SMEM, st>>>(tq, tk, tv, tdo, tbits, tdq, a);
+      launch_pdl(flash_bwd2_kernel<128>, grid, FB2_THREADS, FaBwd2Cfg<128>::SMEM, st, tq, tk, tv, tdo, tbits, tdq, a);
     }
     return check_launch("smpk_flash_attn_bwd");
   }

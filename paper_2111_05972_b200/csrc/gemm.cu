@@ -337,6 +337,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA_arr, const CUte
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
   unsigned long long* trc = (gs[0].trace && blockIdx.x < 2048) ? gs[0].trace + blockIdx.x * 40 : nullptr;
   if (trc && threadIdx.x == 0) trc[0] = gtime_g();
   int tk = 0;  // per-CTA unit counter (trace)
@@ -819,7 +821,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMa
   const int slots = PAIR ? gemm_sms() / 2 : gemm_sms();  // CTA pairs (one per TPC) or CTAs
   int grid = g.num_units < slots ? g.num_units : slots;
   if (PAIR) grid *= 2;
-  kern<<<grid, gemm_threads(EPI), Cfg::SMEM_BYTES, st>>>(ta, tb, maps, g);
+  launch_pdl(kern, grid, gemm_threads(EPI), Cfg::SMEM_BYTES, st, ta, tb, maps, g);
   return check_launch("smpk_gemm");
 }
 
@@ -1139,7 +1141,7 @@ static int launch_grouped(GroupParams& P, cudaStream_t st) {
   const int slots = gemm_sms() / 2;
   const int units = P.g[0].num_units + P.g[1].num_units;
   const int grid = 2 * (units < slots ? units : slots);
-  kern<<<grid, gemm_threads(EPI), Cfg::SMEM_BYTES, st>>>(P);
+  launch_pdl(kern, grid, gemm_threads(EPI), Cfg::SMEM_BYTES, st, P);
   return check_launch("smpk_gemm_grouped");
 }
 

@@ -227,6 +227,8 @@ __device__ __forceinline__ void store8_peers(bf16* const* peers, int npeers, int
 
 template <int W, int VPT>
 __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const uint64_t pkey = philox_key(a.seed, a.rng_step);
   __shared__ float sm[2 * 8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -436,6 +438,8 @@ __device__ __forceinline__ void flush_partial(const float (&acc)[VPT][8], float*
 
 template <int W, int VPT>
 __global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const LnBwdArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const uint64_t pkey = philox_key(a.seed, a.rng_step);
   __shared__ float sm[2 * 8];
   extern __shared__ float red[];  // [W][VPT*8][32] slot reduction buffer
@@ -578,6 +582,8 @@ __global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const LnBwdArgs a) 
 template <int NG>
 __global__ void __launch_bounds__(32 * NG) colsum_reduce_kernel(const float* partials, int P, int K, int H, void* o0,
                                                                 void* o1, void* o2, int out_f32, int accumulate) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float sm[NG][33];
   const int c = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int col = blockIdx.x * 32 + c;
@@ -613,13 +619,15 @@ __global__ void __launch_bounds__(32 * NG) colsum_reduce_kernel(const float* par
 static void colsum_reduce_launch(dim3 grid, const float* partials, int P, int K, int H, void* o0, void* o1, void* o2,
                                  int out_f32, int accumulate, cudaStream_t st) {
   if (P >= 64)
-    colsum_reduce_kernel<32><<<grid, 1024, 0, st>>>(partials, P, K, H, o0, o1, o2, out_f32, accumulate);
+    launch_pdl(colsum_reduce_kernel<32>, grid, 1024, 0, st, partials, P, K, H, o0, o1, o2, out_f32, accumulate);
   else
-    colsum_reduce_kernel<8><<<grid, 256, 0, st>>>(partials, P, K, H, o0, o1, o2, out_f32, accumulate);
+    launch_pdl(colsum_reduce_kernel<8>, grid, 256, 0, st, partials, P, K, H, o0, o1, o2, out_f32, accumulate);
 }
 
 // generic column partial sums of a [M, N] bf16 matrix: grid.x = column blocks of 256, grid.y = row chunks
 __global__ void colsum_partial_kernel(const bf16* x, int M, int N, int64_t ldx, int rows_per_chunk, float* partials) {
+  pdl_trigger();
+  pdl_wait();
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= N) return;
   const int r0 = blockIdx.y * rows_per_chunk;
@@ -778,7 +786,7 @@ __global__ void __launch_bounds__(ROW_THREADS) softmax_bwd_kernel(const SoftmaxA
 #define SMPK_UNPACK(...) __VA_ARGS__
 #define SMPK_ROW_CASE(W_, V_, KERNEL, CFG, ARGS) \
   case W_ * 16 + V_:                             \
-    KERNEL<W_, V_><<<SMPK_UNPACK CFG>>> ARGS;    \
+    launch_pdl(KERNEL<W_, V_>, SMPK_UNPACK CFG, SMPK_UNPACK ARGS); \
     break;
 #define SMPK_DISPATCH_ROW(W_, VPT_, KERNEL, CFG, ARGS)                                                  \
   switch ((W_) * 16 + (VPT_)) {                                                                       \
@@ -864,6 +872,8 @@ __device__ __forceinline__ void bulk_store_s2g(void* gdst, const void* ssrc, uin
 
 template <int CH>
 __global__ void __launch_bounds__(32 * (PIPE_CW + 1), 1) bdr_ln_pipe_kernel(const BdrPipeArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const uint64_t pkey = philox_key(a.seed, a.rng_step);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);  // keeps LDS / STS
@@ -1031,7 +1041,7 @@ static int bdr_ln_pipe_launch(const BdrPipeArgs& a, cudaStream_t st) {
   case CH_: {                                                                                            \
     static unsigned long long once = 0;                                                                  \
     smem_attr_once(bdr_ln_pipe_kernel<CH_>, 232448, once);                                               \
-    bdr_ln_pipe_kernel<CH_><<<grid, 32 * (PIPE_CW + 1), smem, st>>>(a);                                  \
+    launch_pdl(bdr_ln_pipe_kernel<CH_>, grid, 32 * (PIPE_CW + 1), smem, st, a);                           \
     break;                                                                                               \
   }
     SMPK_PIPE_CASE(1) SMPK_PIPE_CASE(2) SMPK_PIPE_CASE(4) SMPK_PIPE_CASE(8)
@@ -1204,6 +1214,8 @@ __device__ __forceinline__ void group_bar(int grp) {
 
 template <int W, int VPT>
 __global__ void __launch_bounds__(32 * (lnb_cw(W) + 1), 1) ln_bwd_pipe_kernel(const LnBwdArgs a, int nst, int sb) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int LNB_CW = lnb_cw(W);
   constexpr int G = LNB_CW / W;  // row groups
   const uint64_t pkey = philox_key(a.seed, a.rng_step);
@@ -1401,7 +1413,7 @@ static int ln_bwd_pipe_try(const LnBwdArgs& a, const RowGeom& geo, cudaStream_t 
   case W_ * 16 + V_: {                                                                           \
     static unsigned long long once = 0;                                                          \
     smem_attr_once(ln_bwd_pipe_kernel<W_, V_>, 232448, once);                                    \
-    ln_bwd_pipe_kernel<W_, V_><<<grid, 32 * (lnb_cw(W_) + 1), smem, st>>>(a, nst, sb);          \
+    launch_pdl(ln_bwd_pipe_kernel<W_, V_>, grid, 32 * (lnb_cw(W_) + 1), smem, st, a, nst, sb);   \
     return grid;                                                                                 \
   }
     SMPK_LNB_CASE(2, 2) SMPK_LNB_CASE(4, 2) SMPK_LNB_CASE(8, 2) SMPK_LNB_CASE(2, 1) SMPK_LNB_CASE(4, 1)
@@ -1580,6 +1592,8 @@ extern "C" int smpk_act_bwd(const void* dy, const void* pre, int M, int N, int a
 template <int RPC>
 __global__ void __launch_bounds__(256) colsum_partial_vec_kernel(const bf16* x, int M, int N, int64_t ldx,
                                                                  float* partials) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float sm[8][32 * 8 + 1];
   const int t = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int col0 = (blockIdx.x * 32 + t) * 8;
@@ -1646,11 +1660,11 @@ extern "C" int smpk_colsum(const void* x, int M, int N, int64_t ldx, void* out, 
   float* ws = reinterpret_cast<float*>(workspace);
   const bf16* xb = reinterpret_cast<const bf16*>(x);
   if (vec) {
-    if (rpc == 256) colsum_partial_vec_kernel<256><<<g1, 256, 0, st>>>(xb, M, N, ldx, ws);
-    else if (rpc == 128) colsum_partial_vec_kernel<128><<<g1, 256, 0, st>>>(xb, M, N, ldx, ws);
-    else colsum_partial_vec_kernel<64><<<g1, 256, 0, st>>>(xb, M, N, ldx, ws);
+    if (rpc == 256) launch_pdl(colsum_partial_vec_kernel<256>, g1, 256, 0, st, xb, M, N, ldx, ws);
+    else if (rpc == 128) launch_pdl(colsum_partial_vec_kernel<128>, g1, 256, 0, st, xb, M, N, ldx, ws);
+    else launch_pdl(colsum_partial_vec_kernel<64>, g1, 256, 0, st, xb, M, N, ldx, ws);
   } else {
-    colsum_partial_kernel<<<g1, 256, 0, st>>>(xb, M, N, ldx, 256, ws);
+    launch_pdl(colsum_partial_kernel, g1, 256, 0, st, xb, M, N, ldx, 256, ws);
   }
   int rc = check_launch("smpk_colsum");
   if (rc) return rc;

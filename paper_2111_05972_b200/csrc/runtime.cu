@@ -1,6 +1,7 @@
 // runtime.cu — error reporting, device queries and version of libsmpk.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "smpk_common.cuh"
@@ -48,6 +49,15 @@ static int capped(int lim) {
 }
 int gemm_sms() { return capped(g_sm_limit_gemm) & ~1; }
 int row_sms() { return capped(g_sm_limit_rows); }
+
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SMPK_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v != 0;
+}
 
 }  // namespace smpk
 

@@ -33,6 +33,34 @@ int check_launch(const char* what);
 int num_sms();
 int gemm_sms();  // num_sms() under smpk_set_sm_limits (even)
 int row_sms();
+bool pdl_enabled();  // SMPK_PDL=0 turns programmatic dependent launch off (A/B)
+
+// ---------------------------------------------------------------------------
+// programmatic dependent launch: a kernel launched with launch_pdl may be scheduled while the
+// previous kernel on its stream is still finishing.  Every such kernel acquires its on-chip
+// resources (barriers, TMEM), then calls pdl_trigger() (its own dependents may now be scheduled:
+// all of its CTAs are resident or done and hold what they need, so they cannot starve) and
+// pdl_wait() (returns once the previous grid completed and its writes are visible) BEFORE its
+// first global-memory access.  Both are no-ops for a kernel launched without the attribute.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 // ---------------------------------------------------------------------------
 // shared-memory / mbarrier
