@@ -337,8 +337,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA_arr, const CUte
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_trigger();
-  pdl_wait();
+  pdl_wait();  // (the dependents are triggered by the producer once its last loads are issued)
   unsigned long long* trc = (gs[0].trace && blockIdx.x < 2048) ? gs[0].trace + blockIdx.x * 40 : nullptr;
   if (trc && threadIdx.x == 0) trc[0] = gtime_g();
   int tk = 0;  // per-CTA unit counter (trace)
@@ -404,6 +403,9 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap* tmA_arr, const CUte
           }
         }
       }
+      // all operand loads of this CTA issued: what is left is its last MMAs and epilogue, the
+      // window in which the next kernel's CTAs may be scheduled (programmatic dependent launch)
+      pdl_trigger();
     }
   } else if (warp == 1) {
     if (rank == 0) {
