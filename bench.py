@@ -260,18 +260,33 @@ def max_over_ranks(v: float) -> float:
     return float(t.item())
 
 
+def exclusive_us(events) -> list:
+    """(event, exclusive device us) for CUDA kernel records: the span from max(start, end of the
+    previous kernel on the same stream) to end.  With programmatic dependent launch a kernel's
+    CTAs are scheduled (and its CUPTI record starts) while its predecessor still runs; its own
+    work begins only when the predecessor ends, so the overlap is not charged to it twice."""
+    cuda = [ev for ev in events if ev.device_type == torch.autograd.DeviceType.CUDA]
+    last_end = {}
+    out = []
+    for ev in sorted(cuda, key=lambda e: e.time_range.start):
+        sid = getattr(ev, "device_resource_id", -1)
+        t0, t1 = ev.time_range.start, ev.time_range.end
+        begin = max(t0, last_end.get(sid, t0))
+        out.append((ev, max(t1 - begin, 0.0)))
+        last_end[sid] = max(t1, last_end.get(sid, t1))
+    return out
+
+
 def kernel_ms_per_step(run, name_part: str, steps: int = 3) -> float:
-    """Device time (CUPTI kernel records) per step of the kernels whose name contains name_part."""
+    """Device time (CUPTI kernel records, exclusive per stream) per step of the kernels whose name
+    contains name_part."""
     from torch.profiler import ProfilerActivity, profile
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for _ in range(steps):
             run()
         torch.cuda.synchronize()
-    us = 0.0
-    for ev in prof.events():
-        if ev.device_type == torch.autograd.DeviceType.CUDA and name_part in ev.name:
-            us += ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total
+    us = sum(d for ev, d in exclusive_us(prof.events()) if name_part in ev.name)
     return us / steps / 1e3
 
 
@@ -285,12 +300,10 @@ def trace_kernels(run, path_prefix: str, rank: int, steps: int = 2) -> None:
             run()
         torch.cuda.synchronize()
     agg = {}
-    for ev in prof.events():
-        if ev.device_type != torch.autograd.DeviceType.CUDA:
-            continue
+    for ev, us in exclusive_us(prof.events()):  # exclusive per stream (see exclusive_us)
         a = agg.setdefault(ev.name, [0, 0.0])
         a[0] += 1
-        a[1] += ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total
+        a[1] += us
     tot = sum(v[1] for v in agg.values())
     seq = [(ev.name, ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total,
             ev.time_range.start, getattr(ev, "device_resource_id", -1))
@@ -499,7 +512,7 @@ def run_gpu(args, rank, world, local):
                 "frac_of_sustained": model_tflops / peak_sus, "frac_of_burst": model_tflops / peaks["bf16_tflops"],
                 "peak_kind": peak_kind},
         "roofline": {"bound": "tensor", "kernel": "smpk gemm_bf16_tcgen05 (all GEMM launches of the step)",
-                     "timing": ("CUPTI kernel records of replays of the step graph" if args.graph
+                     "timing": ("CUPTI kernel records (exclusive per stream) of replays of the step graph" if args.graph
                                 else "CUDA events around each GEMM launch (eager)"),
                      "achieved": achieved, "peak": peak_roof, "unit": "TFLOP/s", "frac": achieved / peak_roof,
                      "peak_kind": (f"{peak_kind} bf16_tflops (burst: SM clock at max during the timed region)"

@@ -164,3 +164,27 @@ def test_hidden_keep_bytes_roundtrip(ops):
     for u, v in zip(a, b):
         if u is not None:
             assert torch.equal(u, v)
+
+
+@pytest.mark.parametrize("H", [1024, 2048])
+def test_bdr_ln_fast_path_bits(ops, H):
+    """The local fast path (bias + residual + LayerNorm, whole 256-column chunks): keep bytes equal
+    oracle/philox.py bit for bit, r equals the fp32 emulation of (x + bias) * keep / (1 - p) +
+    residual rounded to bf16 bit for bit, and y matches the fp64 LayerNorm."""
+    M, p, seed, layer, site, row0 = 517, 0.1, 11, 2, ops.SITE_ATTN_OUT, 300
+    g = torch.Generator().manual_seed(H + 1)
+    x, res = bf(torch.randn(M, H, generator=g)), bf(torch.randn(M, H, generator=g))
+    bias, gam, bet = bf(torch.randn(H, generator=g)), bf(1 + 0.1 * torch.randn(H, generator=g)), bf(
+        torch.randn(H, generator=g))
+    kb = ops.keep_bytes(M, H, "cuda")
+    r, y, mean, rstd = ops.bdr_ln(x.cuda(), bias=bias.cuda(), residual=res.cuda(), gamma=gam.cuda(), beta=bet.cuda(),
+                                  eps=1e-5, p=p, seed=seed, layer=layer, site=site, row_offset=row0, keep_out=kb)
+    keep = philox.hidden_mask(np.arange(M) + row0, H, layer, site, seed, p).reshape(M, H)
+    bits = np.unpackbits(kb.cpu().numpy(), axis=1, bitorder="little").astype(bool)
+    assert np.array_equal(bits, keep)
+    ik = np.float32(1.0) / (np.float32(1.0) - np.float32(p))
+    v = (x.float() + bias.float()) * torch.tensor(ik)
+    v = torch.where(torch.from_numpy(keep), v, torch.zeros_like(v)) + res.float()
+    assert torch.equal(r.cpu(), v.to(torch.bfloat16))
+    ref = tp.layer_norm(r.cpu().double(), gam.double(), bet.double(), 1e-5)
+    assert rel(y, ref) < TOL
