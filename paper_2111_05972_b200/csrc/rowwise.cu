@@ -51,6 +51,31 @@ __device__ __forceinline__ float group_sum(float v, float* sm, int slot, int wi)
   }
 }
 
+// Two sums over the W warps of one row group at once (one barrier round instead of two).
+template <int W>
+__device__ __forceinline__ float2 group_sum2(float2 v, float* sm, int slot, int wi) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  if constexpr (W == 1) {
+    return v;
+  } else {
+    if ((threadIdx.x & 31) == 0) reinterpret_cast<float2*>(sm)[slot * W + wi] = v;
+    named_bar(1 + slot, W * 32);
+    float2 s = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      const float2 t = reinterpret_cast<const float2*>(sm)[slot * W + i];
+      s.x += t.x;
+      s.y += t.y;
+    }
+    named_bar(1 + slot, W * 32);
+    return s;
+  }
+}
+
 // Bulk L2 prefetch of a contiguous 16-byte-aligned span (no registers held; the row kernels use it
 // to pull the next row's inputs toward L2 while the current row computes).
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
@@ -1403,62 +1428,82 @@ __global__ void __launch_bounds__(32 * (lnb_cw(W) + 1), 1) ln_bwd_pipe_kernel(co
   }
   const int c = warp - 1, grp = c / W, wi = c % W;
   const float inv_keep = a.p > 0.f ? 1.f / (1.f - a.p) : 1.f;
-  float acc_g[VPT][8], acc_b[VPT][8], acc_d[VPT][8];
+  const float inv_h = 1.f / H;
+  // paired fp32 math (FFMA2 / FADD2 / FMUL2) on (even, odd) column pairs
+  float2 acc_g[VPT][4], acc_b[VPT][4], acc_d[VPT][4];
 #pragma unroll
   for (int i = 0; i < VPT; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc_g[i][j] = acc_b[i][j] = acc_d[i][j] = 0.f;
+    for (int j = 0; j < 4; ++j) acc_g[i][j] = acc_b[i][j] = acc_d[i][j] = make_float2(0.f, 0.f);
+  const float2 ik2 = make_float2(inv_keep, inv_keep);
   int it = grp;
   for (int row = blockIdx.x + grp * gridDim.x; row < a.M; row += G * gridDim.x, it += G) {
     const int st = it % nst;
     const float mu = has_ln ? a.mean[row] : 0.f, rs = has_ln ? a.rstd[row] : 0.f;
+    const float2 nmu2 = make_float2(-mu, -mu), rs2 = make_float2(rs, rs);
     mbar_wait(&full[st], (it / nst) & 1);
     const uint8_t* buf = smem + st * sb;
     // pass 1 (LayerNorm): row sums of g = dy*gamma and g*xhat, column sums of dy*xhat and dy
-    float m1 = 0.f, m2 = 0.f;
+    float2 nm1 = make_float2(0.f, 0.f), nm2 = make_float2(0.f, 0.f);
     if (has_ln) {
-      float s1 = 0.f, s2 = 0.f;
+      float2 s1 = make_float2(0.f, 0.f), s2 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int i = 0; i < VPT; ++i) {
         const int col = ((i * W + wi) * 32 + lane) * 8;
-        float dy[8], xh[8], gm[8];
-        load8(reinterpret_cast<const bf16*>(buf) + col, dy);
-        load8(reinterpret_cast<const bf16*>(buf + o_r) + col, xh);
-        load8(gam + col, gm);
+        const uint4 du = *reinterpret_cast<const uint4*>(buf + col * 2);
+        const uint4 ru = *reinterpret_cast<const uint4*>(buf + o_r + col * 2);
+        const uint4 gu = *reinterpret_cast<const uint4*>(gam + col);
+        const uint32_t dw[4] = {du.x, du.y, du.z, du.w}, rw[4] = {ru.x, ru.y, ru.z, ru.w},
+                       gw[4] = {gu.x, gu.y, gu.z, gu.w};
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          xh[j] = (xh[j] - mu) * rs;
-          const float gj = dy[j] * gm[j];
-          s1 += gj;
-          s2 += gj * xh[j];
-          acc_g[i][j] += dy[j] * xh[j];
-          acc_b[i][j] += dy[j];
+        for (int j = 0; j < 4; ++j) {
+          const float2 dy = unpack_bf16x2(dw[j]);
+          const float2 xh = __fmul2_rn(__fadd2_rn(unpack_bf16x2(rw[j]), nmu2), rs2);
+          const float2 gj = __fmul2_rn(dy, unpack_bf16x2(gw[j]));
+          s1 = __fadd2_rn(s1, gj);
+          s2 = __ffma2_rn(gj, xh, s2);
+          acc_g[i][j] = __ffma2_rn(dy, xh, acc_g[i][j]);
+          acc_b[i][j] = __fadd2_rn(acc_b[i][j], dy);
         }
       }
-      m1 = group_sum<W>(s1, sm, grp, wi) / H;
-      m2 = group_sum<W>(s2, sm + LNB_CW, grp, wi) / H;
+      const float2 m = group_sum2<W>(make_float2(s1.x + s1.y, s2.x + s2.y), sm, grp, wi);
+      nm1 = make_float2(-m.x * inv_h, -m.x * inv_h);
+      nm2 = make_float2(-m.y * inv_h, -m.y * inv_h);
     }
     // pass 2: d = rs*(g - m1 - xhat*m2) (+ dres), dropout backward, stores (inputs re-read from smem)
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       const int col = ((i * W + wi) * 32 + lane) * 8;
-      float d[8];
-      load8(reinterpret_cast<const bf16*>(buf) + col, d);
+      const uint4 du = *reinterpret_cast<const uint4*>(buf + col * 2);
+      const uint32_t dw[4] = {du.x, du.y, du.z, du.w};
+      float2 d[4];
       if (has_ln) {
-        float xh[8], gm[8];
-        load8(reinterpret_cast<const bf16*>(buf + o_r) + col, xh);
-        load8(gam + col, gm);
+        const uint4 ru = *reinterpret_cast<const uint4*>(buf + o_r + col * 2);
+        const uint4 gu = *reinterpret_cast<const uint4*>(gam + col);
+        const uint32_t rw[4] = {ru.x, ru.y, ru.z, ru.w}, gw[4] = {gu.x, gu.y, gu.z, gu.w};
 #pragma unroll
-        for (int j = 0; j < 8; ++j) d[j] = rs * (d[j] * gm[j] - m1 - (xh[j] - mu) * rs * m2);
+        for (int j = 0; j < 4; ++j) {
+          const float2 xh = __fmul2_rn(__fadd2_rn(unpack_bf16x2(rw[j]), nmu2), rs2);
+          const float2 u = __ffma2_rn(unpack_bf16x2(dw[j]), unpack_bf16x2(gw[j]), nm1);
+          d[j] = __fmul2_rn(__ffma2_rn(xh, nm2, u), rs2);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) d[j] = unpack_bf16x2(dw[j]);
       }
       if (a.dres) {
-        float rr[8];
-        load8(reinterpret_cast<const bf16*>(buf + o_dres) + col, rr);
+        const uint4 eu = *reinterpret_cast<const uint4*>(buf + o_dres + col * 2);
+        const uint32_t ew[4] = {eu.x, eu.y, eu.z, eu.w};
 #pragma unroll
-        for (int j = 0; j < 8; ++j) d[j] += rr[j];
+        for (int j = 0; j < 4; ++j) d[j] = __fadd2_rn(d[j], unpack_bf16x2(ew[j]));
       }
-      round8(d);
-      if (a.dr_out) store8(a.dr_out + (int64_t)row * H + col, d);
+      uint32_t pk[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        pk[j] = pack_bf16x2(d[j].x, d[j].y);  // dr in bf16
+        d[j] = unpack_bf16x2(pk[j]);
+      }
+      if (a.dr_out) *reinterpret_cast<uint4*>(a.dr_out + (int64_t)row * H + col) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
       if (a.p > 0.f) {
         bool keep[8];
         if (a.keep_in)
@@ -1466,13 +1511,19 @@ __global__ void __launch_bounds__(32 * (lnb_cw(W) + 1), 1) ln_bwd_pipe_kernel(co
         else
           dropout_keep8(pkey, a.layer, a.site, (uint64_t)(a.row_offset + row), col, dropout_threshold(a.p), keep);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) d[j] = keep[j] ? d[j] * inv_keep : 0.f;
-        round8(d);
-        store8(a.dsub_out + (int64_t)row * H + col, d);
+        for (int j = 0; j < 4; ++j) {
+          float2 t = __fmul2_rn(d[j], ik2);
+          t.x = keep[2 * j] ? t.x : 0.f;
+          t.y = keep[2 * j + 1] ? t.y : 0.f;
+          pk[j] = pack_bf16x2(t.x, t.y);  // dsub in bf16
+          d[j] = unpack_bf16x2(pk[j]);
+        }
+        *reinterpret_cast<uint4*>(a.dsub_out + (int64_t)row * H + col) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }
-      if (a.npeers) store8(reinterpret_cast<bf16*>(const_cast<uint8_t*>(buf)) + col, d);  // dy slot := output
+      if (a.npeers)  // dy slot := output
+        *reinterpret_cast<uint4*>(const_cast<uint8_t*>(buf) + col * 2) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc_d[i][j] += d[j];
+      for (int j = 0; j < 4; ++j) acc_d[i][j] = __fadd2_rn(acc_d[i][j], d[j]);
     }
     if (a.npeers) {
       // the row's output (in the stage's dy slot) goes to every peer's gather region in bulk; the
@@ -1493,7 +1544,7 @@ __global__ void __launch_bounds__(32 * (lnb_cw(W) + 1), 1) ln_bwd_pipe_kernel(co
   // column partials of the CTA: groups summed in ascending order through shared memory
   float* out = a.partials + (int64_t)blockIdx.x * 3 * H;
   float* rbuf = red + wi * (VPT * 8 * 32);
-  auto flush = [&](const float(&acc)[VPT][8], float* o) {
+  auto flush = [&](const float2(&acc)[VPT][4], float* o) {
     for (int sl = 0; sl < G; ++sl) {
       if (grp == sl) {
 #pragma unroll
@@ -1501,7 +1552,8 @@ __global__ void __launch_bounds__(32 * (lnb_cw(W) + 1), 1) ln_bwd_pipe_kernel(co
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             float* dd = rbuf + (i * 8 + j) * 32 + lane;
-            *dd = (sl == 0) ? acc[i][j] : *dd + acc[i][j];
+            const float av = (j & 1) ? acc[i][j >> 1].y : acc[i][j >> 1].x;
+            *dd = (sl == 0) ? av : *dd + av;
           }
       }
       named_bar(15, LNB_CW * 32);
