@@ -142,9 +142,9 @@ __device__ __forceinline__ void epilogue_math32(const GemmArgs& g, bool in_rows,
         uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          float2 f = unpack_bf16x2(w[j]);
-          v[q * 8 + 2 * j] += f.x;
-          v[q * 8 + 2 * j + 1] += f.y;
+          const float2 f = __fadd2_rn(make_float2(v[q * 8 + 2 * j], v[q * 8 + 2 * j + 1]), unpack_bf16x2(w[j]));
+          v[q * 8 + 2 * j] = f.x;
+          v[q * 8 + 2 * j + 1] = f.y;
         }
       }
     } else {
@@ -158,9 +158,9 @@ __device__ __forceinline__ void epilogue_math32(const GemmArgs& g, bool in_rows,
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       pre[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
-      const float2 f = unpack_bf16x2(pre[j]);
-      v[2 * j] = act_fwd(ACT, f.x);
-      v[2 * j + 1] = act_fwd(ACT, f.y);
+      const float2 f = act_fwd2(ACT, unpack_bf16x2(pre[j]));
+      v[2 * j] = f.x;
+      v[2 * j + 1] = f.y;
     }
   }
   if constexpr (EPI == SMPK_EPI_DACT || EPI == SMPK_EPI_ADD) {
@@ -174,14 +174,11 @@ __device__ __forceinline__ void epilogue_math32(const GemmArgs& g, bool in_rows,
           uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            float2 f = unpack_bf16x2(w[j]);
-            if constexpr (EPI == SMPK_EPI_DACT) {
-              v[q * 8 + 2 * j] *= act_bwd(ACT, f.x);
-              v[q * 8 + 2 * j + 1] *= act_bwd(ACT, f.y);
-            } else {
-              v[q * 8 + 2 * j] += f.x;
-              v[q * 8 + 2 * j + 1] += f.y;
-            }
+            const float2 f = unpack_bf16x2(w[j]);
+            const float2 cur = make_float2(v[q * 8 + 2 * j], v[q * 8 + 2 * j + 1]);
+            const float2 r = (EPI == SMPK_EPI_DACT) ? __fmul2_rn(cur, act_bwd2(ACT, f)) : __fadd2_rn(cur, f);
+            v[q * 8 + 2 * j] = r.x;
+            v[q * 8 + 2 * j + 1] = r.y;
           }
         }
       } else {

@@ -437,6 +437,47 @@ __device__ __forceinline__ float act_bwd(int act, float z) {  // d act / dz
   return fmaf(z * 0.3989422804014327f, e, cdf);
 }
 
+// Paired forms of normal_cdf / act_fwd / act_bwd for (even, odd) column pairs: the same operation
+// sequence per lane (bit-identical results) with the fp32 arithmetic as FFMA2 / FMUL2, so an
+// epilogue warp issues half the FMA-pipe instructions (the GEMM epilogue is issue-heavy).
+__device__ __forceinline__ float2 f2c(float c) { return make_float2(c, c); }
+__device__ __forceinline__ float2 normal_cdf2(float2 z, float2& e) {
+  const float2 den = __ffma2_rn(make_float2(fabsf(z.x), fabsf(z.y)), f2c(0.23164188f), f2c(1.f));
+  const float2 t = make_float2(rcp_approx(den.x), rcp_approx(den.y));
+  const float2 zz = __fmul2_rn(__fmul2_rn(z, f2c(-0.72134752f)), z);
+  e = make_float2(ex2_approx(zz.x), ex2_approx(zz.y));
+  float2 p = __ffma2_rn(t, f2c(0.5307027145f), f2c(-0.7265760135f));
+  p = __ffma2_rn(t, p, f2c(0.7107068705f));
+  p = __ffma2_rn(t, p, f2c(-0.142248368f));
+  p = __ffma2_rn(t, p, f2c(0.127414796f));
+  const float2 q = __fmul2_rn(__fmul2_rn(t, p), e);
+  return make_float2(z.x >= 0.f ? 1.f - q.x : q.x, z.y >= 0.f ? 1.f - q.y : q.y);
+}
+__device__ __forceinline__ float2 act_fwd2(int act, float2 z) {
+  if (act == SMPK_ACT_RELU) return make_float2(z.x > 0.f ? z.x : 0.f, z.y > 0.f ? z.y : 0.f);
+  if (act == SMPK_ACT_GELU_TANH) {
+    const float2 u = __fmul2_rn(z, __ffma2_rn(__fmul2_rn(z, z), f2c(0.0356774081f), f2c(0.7978845608f)));
+    const float2 hz = __fmul2_rn(f2c(0.5f), z);
+    return __ffma2_rn(hz, make_float2(tanh_approx(u.x), tanh_approx(u.y)), hz);
+  }
+  float2 e;
+  return __fmul2_rn(z, normal_cdf2(z, e));
+}
+__device__ __forceinline__ float2 act_bwd2(int act, float2 z) {
+  if (act == SMPK_ACT_RELU) return make_float2(z.x > 0.f ? 1.f : 0.f, z.y > 0.f ? 1.f : 0.f);
+  if (act == SMPK_ACT_GELU_TANH) {
+    const float2 z2 = __fmul2_rn(z, z);
+    const float2 u = __fmul2_rn(z, __ffma2_rn(z2, f2c(0.0356774081f), f2c(0.7978845608f)));
+    const float2 t = make_float2(tanh_approx(u.x), tanh_approx(u.y));
+    const float2 du = __ffma2_rn(z2, f2c(0.1070322243f), f2c(0.7978845608f));
+    return __ffma2_rn(__fmul2_rn(__fmul2_rn(f2c(0.5f), z), du), __ffma2_rn(make_float2(-t.x, -t.y), t, f2c(1.f)),
+                      __ffma2_rn(f2c(0.5f), t, f2c(0.5f)));
+  }
+  float2 e;
+  const float2 cdf = normal_cdf2(z, e);
+  return __ffma2_rn(__fmul2_rn(z, f2c(0.3989422804014327f)), e, cdf);
+}
+
 // ---------------------------------------------------------------------------
 // Philox4x32-10 (counter-based; reproduced bit-exactly by oracle/philox.py)
 // ---------------------------------------------------------------------------
