@@ -401,8 +401,9 @@ __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs
 
 // Local fast path of bdr_ln_fwd (one input slot, no peers, bias + residual + LayerNorm, whole
 // 256-column chunks): the flags the general kernel tests per chunk are fixed, bias / gamma / beta
-// stay in registers across rows, and the fp32 math runs as paired FFMA2 / FADD2 / FMUL2.  The
-// general kernel issued ~58 instructions per element here (ncu: issue-bound at 62 %).
+// are re-read per row from L1 (holding them in registers spilled at 3 CTAs per SM), and the fp32
+// math runs as paired FFMA2 / FADD2 / FMUL2.  The general kernel issued ~58 instructions per
+// element here (ncu: issue-bound at 62 %).
 __device__ __forceinline__ float2 bf2f(uint32_t w) { return unpack_bf16x2(w); }
 
 template <int W, int VPT>
