@@ -12,7 +12,9 @@ One JSON line on rank 0:
   value      whole-job tokens/s, inputs resident in HBM, device-timed (CUDA events, max over ranks)
   e2e        same metric through the public API with pinned-host inputs copied in and the
              loss read back every step
-  roofline   the dominant kernel (smpk tcgen05 GEMM): algorithmic FLOPs / event-timed launch time
+  roofline   the dominant kernel family (smpk tcgen05 GEMMs): algorithmic FLOPs / their device time
+             (CUPTI records of graph replays, each launch charged from max(start, end of its stream
+             predecessor) -- programmatic dependent launch starts records early)
   cpu_baseline  the CPU oracle (oracle/tp.py, torch fp32 on the host cores) on a bounded sample
 ``--impl reference`` times only the CPU reference path (the reference has no TP
 code; its algorithm is restated in oracle/).
