@@ -406,8 +406,9 @@ __global__ void __launch_bounds__(ROW_THREADS) bdr_ln_fwd_kernel(const BdrLnArgs
 // element here (ncu: issue-bound at 62 %).
 __device__ __forceinline__ float2 bf2f(uint32_t w) { return unpack_bf16x2(w); }
 
-template <int W, int VPT>
+template <int W, int VPT, bool BR, bool LN>
 __global__ void __launch_bounds__(ROW_THREADS, 3) bdr_ln_fwd_fast_kernel(const BdrLnArgs a) {
+  // BR: bias + dropout + residual (else r = x); LN: LayerNorm statistics and y (else r only)
   pdl_trigger();
   pdl_wait();
   const uint64_t pkey = philox_key(a.seed, a.rng_step);
@@ -416,7 +417,7 @@ __global__ void __launch_bounds__(ROW_THREADS, 3) bdr_ln_fwd_fast_kernel(const B
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = warp / W, wi = warp % W;
   const int rows_per_cta = (ROW_THREADS / 32) / W;
-  const bool drop = a.p > 0.f;
+  const bool drop = BR && a.p > 0.f;
   const float ik = drop ? 1.f / (1.f - a.p) : 1.f;
   const uint32_t thresh = dropout_threshold(a.p);
   const int row_step = gridDim.x * rows_per_cta;
@@ -430,7 +431,7 @@ __global__ void __launch_bounds__(ROW_THREADS, 3) bdr_ln_fwd_fast_kernel(const B
 #pragma unroll
       for (int i = 0; i < VPT; ++i) {
         px[i] = *reinterpret_cast<const uint4*>(a.x + (int64_t)row * a.H + col[i]);
-        pr[i] = *reinterpret_cast<const uint4*>(a.residual + (int64_t)row * a.H + col[i]);
+        if (BR) pr[i] = *reinterpret_cast<const uint4*>(a.residual + (int64_t)row * a.H + col[i]);
       }
     }
   };
@@ -444,6 +445,15 @@ __global__ void __launch_bounds__(ROW_THREADS, 3) bdr_ln_fwd_fast_kernel(const B
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       const uint32_t xw[4] = {px[i].x, px[i].y, px[i].z, px[i].w};
+      if (!BR) {  // r = x (already bf16)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          v[i][j] = bf2f(xw[j]);
+          s2 = __fadd2_rn(s2, v[i][j]);
+        }
+        if (valid && a.r_out) *reinterpret_cast<uint4*>(a.r_out + (int64_t)row * a.H + col[i]) = px[i];
+        continue;
+      }
       const uint32_t rw[4] = {pr[i].x, pr[i].y, pr[i].z, pr[i].w};
       const uint4 bb = *reinterpret_cast<const uint4*>(a.bias + col[i]);  // L1-resident across rows
       const uint32_t bw[4] = {bb.x, bb.y, bb.z, bb.w};
@@ -483,6 +493,7 @@ __global__ void __launch_bounds__(ROW_THREADS, 3) bdr_ln_fwd_fast_kernel(const B
       }
     }
     issue(row + row_step);  // next row's loads overlap this row's statistics and stores
+    if (!LN) continue;
     const float mu = group_sum<W>(s2.x + s2.y, sm, slot, wi) * inv_h;
     const float2 nmu = make_float2(-mu, -mu);
     float2 q2 = make_float2(0.f, 0.f);
@@ -1240,6 +1251,18 @@ static bool pipe_enabled() {
   return v == 1;
 }
 
+template <bool BR, bool LN>
+static int launch_fast(const RowGeom& geo, int grid, cudaStream_t st, const BdrLnArgs& a) {
+  switch (geo.W * 16 + geo.VPT) {
+    case 17: launch_pdl(bdr_ln_fwd_fast_kernel<1, 1, BR, LN>, grid, ROW_THREADS, 0, st, a); return 0;
+    case 18: launch_pdl(bdr_ln_fwd_fast_kernel<1, 2, BR, LN>, grid, ROW_THREADS, 0, st, a); return 0;
+    case 34: launch_pdl(bdr_ln_fwd_fast_kernel<2, 2, BR, LN>, grid, ROW_THREADS, 0, st, a); return 0;
+    case 66: launch_pdl(bdr_ln_fwd_fast_kernel<4, 2, BR, LN>, grid, ROW_THREADS, 0, st, a); return 0;
+    case 130: launch_pdl(bdr_ln_fwd_fast_kernel<8, 2, BR, LN>, grid, ROW_THREADS, 0, st, a); return 0;
+    default: return -1;
+  }
+}
+
 static int bdr_ln_impl(const void* x, int nslots, int64_t slot_stride, const void* bias, const void* residual,
                        void* r_out, const void* gamma, const void* beta, void* y_out, float* mean, float* rstd,
                        void* const* out_peers, int npeers, int64_t peer_off, int M, int H, float eps, float p_drop,
@@ -1298,20 +1321,16 @@ static int bdr_ln_impl(const void* x, int nslots, int64_t slot_stride, const voi
   }
   // 80 registers with the next-row prefetch: 3 resident CTAs per SM, one wave
   const int grid = row_grid(M, geo.W, 3);
-  if (fast_enabled() && !x_peers && nslots == 1 && npeers == 0 && !row_sums_out && !ext_sums && gamma && y_out &&
-      residual && bias && col_offset == 0 && H == geo.W * geo.VPT * 256 && !(reinterpret_cast<uintptr_t>(x) & 15)) {
-    switch (geo.W * 16 + geo.VPT) {
-      SMPK_ROW_CASE(1, 1, bdr_ln_fwd_fast_kernel, (grid, ROW_THREADS, 0, st), (a))
-      SMPK_ROW_CASE(1, 2, bdr_ln_fwd_fast_kernel, (grid, ROW_THREADS, 0, st), (a))
-      SMPK_ROW_CASE(2, 2, bdr_ln_fwd_fast_kernel, (grid, ROW_THREADS, 0, st), (a))
-      SMPK_ROW_CASE(4, 2, bdr_ln_fwd_fast_kernel, (grid, ROW_THREADS, 0, st), (a))
-      SMPK_ROW_CASE(8, 2, bdr_ln_fwd_fast_kernel, (grid, ROW_THREADS, 0, st), (a))
-      default:
-        goto general;
-    }
-    return check_launch("smpk_bdr_ln_fwd(fast)");
+  if (fast_enabled() && !x_peers && nslots == 1 && npeers == 0 && !row_sums_out && !ext_sums && col_offset == 0 &&
+      H == geo.W * geo.VPT * 256 && !(reinterpret_cast<uintptr_t>(x) & 15) && geo.VPT <= 2 &&
+      (geo.W == 1 || geo.W == 2 || geo.W == 4 || geo.W == 8)) {
+    const bool br = bias && residual, ln = gamma && y_out;
+    int rc = -1;
+    if (br && ln) rc = launch_fast<true, true>(geo, grid, st, a);
+    else if (br && !gamma && r_out) rc = launch_fast<true, false>(geo, grid, st, a);
+    else if (!bias && !residual && p_drop == 0.f && !keep_out && ln) rc = launch_fast<false, true>(geo, grid, st, a);
+    if (rc >= 0) return check_launch("smpk_bdr_ln_fwd(fast)");
   }
-general:
   SMPK_DISPATCH_ROW(geo.W, geo.VPT, bdr_ln_fwd_kernel, (grid, ROW_THREADS, 0, st), (a));
   return check_launch("smpk_bdr_ln_fwd");
 }

@@ -188,3 +188,27 @@ def test_bdr_ln_fast_path_bits(ops, H):
     assert torch.equal(r.cpu(), v.to(torch.bfloat16))
     ref = tp.layer_norm(r.cpu().double(), gam.double(), bet.double(), 1e-5)
     assert rel(y, ref) < TOL
+
+
+@pytest.mark.parametrize("H", [1024, 2048])
+def test_bdr_ln_fast_path_variants(ops, H):
+    """The pre-LN layers' two row calls on the fast path: r = residual + dropout(x + bias) without a
+    LayerNorm (keep bytes and r bit-exact), and a LayerNorm of x alone (vs the fp64 LayerNorm)."""
+    M, p, seed, layer, site, row0 = 389, 0.1, 4, 1, ops.SITE_MLP_OUT, 17
+    g = torch.Generator().manual_seed(H + 2)
+    x, res = bf(torch.randn(M, H, generator=g)), bf(torch.randn(M, H, generator=g))
+    bias, gam, bet = bf(torch.randn(H, generator=g)), bf(1 + 0.1 * torch.randn(H, generator=g)), bf(
+        torch.randn(H, generator=g))
+    kb = ops.keep_bytes(M, H, "cuda")
+    r, y, mean, rstd = ops.bdr_ln(x.cuda(), bias=bias.cuda(), residual=res.cuda(), p=p, seed=seed, layer=layer,
+                                  site=site, row_offset=row0, keep_out=kb)
+    assert y is None and mean is None
+    keep = philox.hidden_mask(np.arange(M) + row0, H, layer, site, seed, p).reshape(M, H)
+    assert np.array_equal(np.unpackbits(kb.cpu().numpy(), axis=1, bitorder="little").astype(bool), keep)
+    ik = np.float32(1.0) / (np.float32(1.0) - np.float32(p))
+    v = torch.where(torch.from_numpy(keep), (x.float() + bias.float()) * torch.tensor(ik), torch.zeros(M, H)) + res.float()
+    assert torch.equal(r.cpu(), v.to(torch.bfloat16))
+    y2, mean2, rstd2 = ops.layer_norm(x.cuda(), gam.cuda(), bet.cuda(), 1e-5)
+    ref = tp.layer_norm(x.double(), gam.double(), bet.double(), 1e-5)
+    assert rel(y2, ref) < TOL
+    assert rel(mean2, x.double().mean(1)) < 1e-5
